@@ -1,0 +1,179 @@
+/* sgm.h — C ABI of the B200-native candidate-view render + scoring path.
+ *
+ * This is the drop-in boundary for the reference's renderer/scoring API. The
+ * reference has no FFI: its boundary is the C++ header API in
+ * proj/include/splatmap/splat_render.hpp:78-95 and
+ * proj/include/splatmap/explorer.hpp:114-131. Every entry point
+ * below names the reference interface it replaces. Plain pointers and sizes only;
+ * no CUDA or torch types appear in the signatures (streams are passed as void*).
+ *
+ * Conventions
+ *   - Every call returns an int status (SGM_OK == 0). On failure the message is
+ *     available from sgm_last_error(ctx); the C++/Python wrappers rethrow it as
+ *     std::runtime_error / RuntimeError, mirroring the reference's exception style.
+ *   - One sgm_ctx per GPU. Calls on one ctx are serialised by the caller; distinct
+ *     ctxs may be driven concurrently from different host threads (the reference's
+ *     "pure given inputs" threading contract).
+ *   - Host buffers are caller-owned. All floating-point inputs/outputs are fp64,
+ *     in the reference's storage layouts (gaussian_map.hpp:105-113,
+ *     splat_render.hpp:51-54).
+ *   - There is no CPU fallback: a ctx cannot be created without a CUDA device.
+ */
+#ifndef SGM_H
+#define SGM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGM_ABI_VERSION 1
+
+typedef struct sgm_ctx sgm_ctx; /* per-GPU context: stream, scratch, last-call state */
+typedef struct sgm_map sgm_map; /* device-resident, immutable GaussianMap snapshot */
+
+/* CameraModel (proj/include/splatmap/camera.hpp:11-50); FOV fields are unused by render. */
+typedef struct {
+    int32_t width, height;
+    double fx, fy, cx, cy;
+} sgm_camera;
+
+/* Pose (proj/include/splatmap/geometry.hpp:18-41): x_world = R x_cam + t. R row-major. */
+typedef struct {
+    double R[9];
+    double t[3];
+} sgm_pose;
+
+/* RenderOptions (proj/include/splatmap/splat_render.hpp:22-28). */
+typedef struct {
+    int32_t early_exit;        /* default 1 */
+    double transmittance_eps;  /* default 1e-4 */
+    double z_near;             /* default 0.01 */
+    double truncation_sigmas;  /* default 3.0 */
+    int32_t tile_size;         /* default 8 (bins are built at this size, bit-exact) */
+} sgm_options;
+
+/* SplatProjection (splat_render.hpp:32-39). */
+typedef struct {
+    double mx, my, rad_px, z, alpha;
+    uint32_t index;
+    uint32_t reserved;
+} sgm_projection;
+
+/* CandidatePose geometry (explorer.hpp:93-106); camera_pose() = look_at(p, p + d). */
+typedef struct {
+    double position[3];
+    double direction[3];
+} sgm_candidate;
+
+/* RenderChannels (splat_render.hpp:12-20) as bit flags. */
+enum {
+    SGM_COLOR = 1u,
+    SGM_DEPTH = 2u,
+    SGM_SEMANTICS = 4u,
+    SGM_RETAIN_CONTRIBUTORS = 8u
+};
+
+enum {
+    SGM_OK = 0,
+    SGM_ERR_INVALID = 1,     /* bad argument (reference would throw std::invalid_argument) */
+    SGM_ERR_CUDA = 2,        /* CUDA runtime / launch failure */
+    SGM_ERR_OOM = 3,         /* device allocation failed */
+    SGM_ERR_UNSUPPORTED = 4  /* valid request this build does not serve */
+};
+
+/* Per-ctx counters since creation or the last sgm_ctx_reset_stats. */
+typedef struct {
+    uint64_t kernel_launches;   /* kernels of this library launched */
+    uint64_t views;             /* views processed (render + score) */
+    uint64_t visible;           /* sum of V (culled-in projections) */
+    uint64_t pairs;             /* sum of P ((tile, projection) pairs) */
+    uint64_t contributors;      /* sum of K (composited pixel-splat pairs) */
+    uint64_t raster_launches;   /* raster kernel launches (timed when profiling is on) */
+    double raster_ms;           /* CUDA-event time of raster launches (profiling on) */
+    double binning_ms;          /* CUDA-event time of preprocess+binning (profiling on) */
+} sgm_stats;
+
+int sgm_abi_version(void);
+
+/* ---- context ---- */
+int sgm_ctx_create(int device, sgm_ctx** out);
+void sgm_ctx_destroy(sgm_ctx* ctx);
+/* Last error of `ctx`; with ctx == NULL, the last error of sgm_ctx_create on this thread. */
+const char* sgm_last_error(const sgm_ctx* ctx);
+/* The cudaStream_t (as void*) every kernel of this ctx is launched on. */
+void* sgm_ctx_stream(sgm_ctx* ctx);
+int sgm_ctx_synchronize(sgm_ctx* ctx);
+int sgm_ctx_set_profiling(sgm_ctx* ctx, int enabled);
+int sgm_ctx_get_stats(const sgm_ctx* ctx, sgm_stats* out);
+int sgm_ctx_reset_stats(sgm_ctx* ctx);
+
+/* ---- map ----
+ * Replaces passing `const GaussianMap&` (gaussian_map.hpp:61-114) to each render:
+ * uploads a read-only snapshot once per map version. Arrays are the GaussianMap
+ * spans: centers 3N, log_radii N, opacity_logits N, colors 3N, sem_indices kN,
+ * sem_probs kN. Errors as GaussianMap(k, num_classes) (gaussian_map.hpp:63-66) plus
+ * sem index < num_classes + 1. Activations exp/sigmoid and the colour clamp are
+ * applied on the host with the reference's libm (gaussian_map.hpp:36-37). */
+int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes,
+                   const double* centers, const double* log_radii,
+                   const double* opacity_logits, const double* colors,
+                   const uint16_t* sem_indices, const double* sem_probs, sgm_map** out);
+void sgm_map_release(sgm_ctx* ctx, sgm_map* map);
+
+/* ---- render (splat_render.hpp:78-80, render()) ----
+ * Host output planes in the reference layout; NULL for channels not requested.
+ * silhouette (px) is always written. color px*3, depth px, sem px*(num_classes+1).
+ * *n_projections receives V. */
+int sgm_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam, const sgm_pose* pose,
+               uint32_t channels, const sgm_options* opt, double* color, double* depth,
+               double* silhouette, double* sem, uint64_t* n_projections);
+/* Same, but planes are written to caller-provided DEVICE buffers on the ctx stream. */
+int sgm_render_device(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam,
+                      const sgm_pose* pose, uint32_t channels, const sgm_options* opt,
+                      double* d_color, double* d_depth, double* d_silhouette, double* d_sem,
+                      uint64_t* n_projections);
+/* RenderOutput.projections of the last sgm_render* call (depth-sorted, culled). */
+int sgm_last_projections(sgm_ctx* ctx, sgm_projection* out, uint64_t capacity);
+/* The tile bins of the last sgm_render* call at RenderOptions::tile_size
+ * (splat_render.cpp:188-213, local to render() in the reference): tile_offsets has
+ * tiles+1 entries, ids are projection ids in bin order, probe3 the float Probe
+ * fields (mx, my, cutoff_d2). Any pointer may be NULL; *n_pairs receives P. */
+int sgm_last_bins(sgm_ctx* ctx, uint32_t* tile_offsets, uint32_t* ids, float* probe3,
+                  uint64_t capacity, uint64_t* n_pairs);
+/* RenderOutput.contrib / contrib_offset of the last render with
+ * SGM_RETAIN_CONTRIBUTORS (splat_render.cpp:125-137). offsets has px+1 entries. */
+int sgm_last_contributors(sgm_ctx* ctx, uint32_t* offsets, uint32_t* contrib,
+                          uint64_t capacity, uint64_t* n_contrib);
+
+/* ---- entropy (splat_render.hpp:86-91) ---- */
+double sgm_clipped_entropy(const double* probs, uint64_t n);
+int sgm_render_entropy(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam,
+                       const sgm_pose* pose, const sgm_options* opt, double* entropy);
+
+/* ---- candidate scoring (explorer.hpp:114-121) ----
+ * refresh_candidate_scores for n views given as poses: per view the exact-zero
+ * silhouette count (n_missing) and the summed clipped entropy. Batched on the
+ * GPU; per-view results are deterministic and independent of batching/sharding. */
+int sgm_score_views(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam, uint64_t n,
+                    const sgm_pose* poses, const sgm_options* opt, double* n_missing,
+                    double* entropy_sum);
+/* Same for CandidatePose geometry (camera_pose() computed on the host). */
+int sgm_score_candidates(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam, uint64_t n,
+                         const sgm_candidate* cands, const sgm_options* opt,
+                         double* n_missing, double* entropy_sum);
+/* combine_scores (explorer.cpp:225-248) on host fp64: returns 1 if any i_total > 0,
+ * 0 if the pool is exhausted (or n == 0), negative on invalid arguments. */
+int sgm_combine_scores(uint64_t n, const double* n_missing, const double* entropy_sum,
+                       const double* positions3, const double current[3], double* i_geo,
+                       double* i_sem, double* i_total);
+/* look_at(p, p + d) (geometry.hpp:44-56) with Eigen's evaluation order. */
+void sgm_candidate_pose(const double position[3], const double direction[3], sgm_pose* out);
+void sgm_look_at(const double position[3], const double target[3], sgm_pose* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGM_H */

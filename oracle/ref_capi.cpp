@@ -1,0 +1,260 @@
+// C entry points over the REFERENCE's own render/scoring code, compiled
+// unmodified from /root/reference/proj/src (see oracle/Makefile). TEST
+// INFRASTRUCTURE ONLY: used by tests/ (as the checker), by tests/golden/make_golden.py
+// (fixture generation), and by bench.py's reference arm / cpu_baseline. The
+// product (paper_2506_00225_b200) never links this.
+//
+// Wrapped reference interfaces:
+//   render / render_reference / render_entropy / clipped_entropy
+//       proj/include/splatmap/splat_render.hpp:78-95
+//   refresh_candidate_scores / combine_scores   proj/include/splatmap/explorer.hpp:114-121
+//   look_at                                      proj/include/splatmap/geometry.hpp:44-56
+//   testutil::random_splat_map                   proj/tests/test_helpers.hpp:46-67
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <thread>
+#include <vector>
+
+#include "splatmap/explorer.hpp"
+#include "splatmap/gaussian_map.hpp"
+#include "splatmap/splat_render.hpp"
+#include "test_helpers.hpp"
+
+using namespace splatmap;
+
+namespace {
+
+struct RefMap {
+    GaussianMap map;
+    RefMap(int k, int c) : map(k, c) {}
+};
+
+CameraModel make_cam(const int32_t wh[2], const double intr[4]) {
+    CameraModel c;
+    c.width = wh[0];
+    c.height = wh[1];
+    c.fx = intr[0];
+    c.fy = intr[1];
+    c.cx = intr[2];
+    c.cy = intr[3];
+    return c;
+}
+
+Pose make_pose(const double R_rowmajor[9], const double t[3]) {
+    Pose p;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) p.R(i, j) = R_rowmajor[3 * i + j];
+    p.t = Vec3(t[0], t[1], t[2]);
+    return p;
+}
+
+RenderOptions make_opts(const double o[5]) {
+    // o = {early_exit, transmittance_eps, z_near, truncation_sigmas, tile_size}
+    RenderOptions r;
+    r.early_exit = o[0] != 0.0;
+    r.transmittance_eps = o[1];
+    r.z_near = o[2];
+    r.truncation_sigmas = o[3];
+    r.tile_size = static_cast<int>(o[4]);
+    return r;
+}
+
+void copy_out(const RenderOutput& out, double* color, double* depth, double* sil, double* sem,
+              double* proj6, uint64_t* n_proj, uint32_t* contrib_offset, uint32_t* contrib,
+              uint64_t contrib_cap, uint64_t* n_contrib) {
+    if (color && !out.color.empty()) std::memcpy(color, out.color.data(), out.color.size() * 8);
+    if (depth && !out.depth.empty()) std::memcpy(depth, out.depth.data(), out.depth.size() * 8);
+    if (sil) std::memcpy(sil, out.silhouette.data(), out.silhouette.size() * 8);
+    if (sem && !out.sem.empty()) std::memcpy(sem, out.sem.data(), out.sem.size() * 8);
+    if (n_proj) *n_proj = out.projections.size();
+    if (proj6) {
+        for (size_t i = 0; i < out.projections.size(); ++i) {
+            const SplatProjection& p = out.projections[i];
+            double* r = proj6 + 6 * i;
+            r[0] = p.mx;
+            r[1] = p.my;
+            r[2] = p.rad_px;
+            r[3] = p.z;
+            r[4] = p.alpha;
+            r[5] = static_cast<double>(p.index);
+        }
+    }
+    if (n_contrib) *n_contrib = out.contrib.size();
+    if (contrib_offset && !out.contrib_offset.empty())
+        std::memcpy(contrib_offset, out.contrib_offset.data(), out.contrib_offset.size() * 4);
+    if (contrib && !out.contrib.empty())
+        std::memcpy(contrib, out.contrib.data(), std::min<uint64_t>(contrib_cap, out.contrib.size()) * 4);
+}
+
+}  // namespace
+
+extern "C" {
+
+void* ref_map_create(uint64_t n, int k, int num_classes, const double* centers,
+                     const double* log_radii, const double* logits, const double* colors,
+                     const uint16_t* sem_idx, const double* sem_probs) {
+    auto* m = new RefMap(k, num_classes);
+    for (uint64_t i = 0; i < n; ++i) {
+        SemanticGaussian g;
+        g.center = Vec3(centers[3 * i], centers[3 * i + 1], centers[3 * i + 2]);
+        g.log_radius = log_radii[i];
+        g.opacity_logit = logits[i];
+        g.color = Vec3(colors[3 * i], colors[3 * i + 1], colors[3 * i + 2]);
+        g.sem.indices.assign(sem_idx + i * k, sem_idx + (i + 1) * k);
+        g.sem.probs.assign(sem_probs + i * k, sem_probs + (i + 1) * k);
+        m->map.add(g);
+    }
+    return m;
+}
+
+void ref_map_destroy(void* m) { delete static_cast<RefMap*>(m); }
+
+// GaussianMap::load (SGMP v1, proj/src/gaussian_map.cpp:163-189).
+void* ref_map_load(const char* path) {
+    auto* m = new RefMap(1, 1);
+    m->map = GaussianMap::load(path);
+    return m;
+}
+uint64_t ref_map_size(void* m) { return static_cast<RefMap*>(m)->map.size(); }
+
+// Which: 0 = render (tiled, production), 1 = render_reference (untiled oracle).
+int ref_render(void* m, int which, const int32_t wh[2], const double intr[4], const double R[9],
+               const double t[3], uint32_t channels, const double opts[5], double* color,
+               double* depth, double* sil, double* sem, double* proj6, uint64_t* n_proj,
+               uint32_t* contrib_offset, uint32_t* contrib, uint64_t contrib_cap,
+               uint64_t* n_contrib) {
+    const GaussianMap& map = static_cast<RefMap*>(m)->map;
+    RenderChannels ch;
+    ch.color = channels & 1u;
+    ch.depth = channels & 2u;
+    ch.semantics = channels & 4u;
+    ch.retain_contributors = channels & 8u;
+    RenderOutput out = which == 0 ? render(map, make_cam(wh, intr), make_pose(R, t), ch, make_opts(opts))
+                                  : render_reference(map, make_cam(wh, intr), make_pose(R, t), ch);
+    copy_out(out, color, depth, sil, sem, proj6, n_proj, contrib_offset, contrib, contrib_cap,
+             n_contrib);
+    return 0;
+}
+
+void ref_render_entropy(void* m, const int32_t wh[2], const double intr[4], const double R[9],
+                        const double t[3], const double opts[5], double* out) {
+    auto h = render_entropy(static_cast<RefMap*>(m)->map, make_cam(wh, intr), make_pose(R, t),
+                            make_opts(opts));
+    std::memcpy(out, h.data(), h.size() * 8);
+}
+
+double ref_clipped_entropy(const double* p, uint64_t n) {
+    return clipped_entropy(std::span<const double>(p, n));
+}
+
+// refresh_candidate_scores over candidates (position, direction), split into
+// `threads` disjoint contiguous spans on the shared const map.
+void ref_refresh_scores(void* m, const int32_t wh[2], const double intr[4], uint64_t n,
+                        const double* pos3, const double* dir3, int threads, double* n_missing,
+                        double* entropy_sum) {
+    const GaussianMap& map = static_cast<RefMap*>(m)->map;
+    CameraModel cam = make_cam(wh, intr);
+    std::vector<CandidatePose> cs(n);
+    for (uint64_t i = 0; i < n; ++i) {
+        cs[i].position = Vec3(pos3[3 * i], pos3[3 * i + 1], pos3[3 * i + 2]);
+        cs[i].direction = Vec3(dir3[3 * i], dir3[3 * i + 1], dir3[3 * i + 2]);
+        cs[i].id = static_cast<int>(i);
+    }
+    threads = std::max(1, std::min<int>(threads, static_cast<int>(n)));
+    if (threads == 1) {
+        refresh_candidate_scores(cs, map, cam);
+    } else {
+        std::vector<std::thread> pool;
+        const uint64_t per = (n + threads - 1) / threads;
+        for (int w = 0; w < threads; ++w) {
+            uint64_t a = w * per, b = std::min<uint64_t>(n, a + per);
+            if (a >= b) break;
+            pool.emplace_back([&, a, b] {
+                refresh_candidate_scores(std::span<CandidatePose>(cs.data() + a, b - a), map, cam);
+            });
+        }
+        for (auto& th : pool) th.join();
+    }
+    for (uint64_t i = 0; i < n; ++i) {
+        n_missing[i] = cs[i].n_missing;
+        entropy_sum[i] = cs[i].entropy_sum;
+    }
+}
+
+int ref_combine_scores(uint64_t n, const double* n_missing, const double* entropy_sum,
+                       const double* pos3, const double cur[3], double* i_geo, double* i_sem,
+                       double* i_total) {
+    std::vector<CandidatePose> cs(n);
+    for (uint64_t i = 0; i < n; ++i) {
+        cs[i].position = Vec3(pos3[3 * i], pos3[3 * i + 1], pos3[3 * i + 2]);
+        cs[i].n_missing = n_missing[i];
+        cs[i].entropy_sum = entropy_sum[i];
+    }
+    bool any = combine_scores(cs, Vec3(cur[0], cur[1], cur[2]));
+    for (uint64_t i = 0; i < n; ++i) {
+        i_geo[i] = cs[i].i_geo;
+        i_sem[i] = cs[i].i_sem;
+        i_total[i] = cs[i].i_total;
+    }
+    return any ? 1 : 0;
+}
+
+// CandidatePose::camera_pose() = look_at(pos, pos + dir) (explorer.hpp:105).
+void ref_candidate_pose(const double pos[3], const double dir[3], double R[9], double t[3]) {
+    CandidatePose c;
+    c.position = Vec3(pos[0], pos[1], pos[2]);
+    c.direction = Vec3(dir[0], dir[1], dir[2]);
+    Pose p = c.camera_pose();
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) R[3 * i + j] = p.R(i, j);
+    for (int i = 0; i < 3; ++i) t[i] = p.t[i];
+}
+
+void ref_look_at(const double pos[3], const double target[3], double R[9], double t[3]) {
+    Pose p = look_at(Vec3(pos[0], pos[1], pos[2]), Vec3(target[0], target[1], target[2]));
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) R[3 * i + j] = p.R(i, j);
+    for (int i = 0; i < 3; ++i) t[i] = p.t[i];
+}
+
+// testutil::random_splat_map (proj/tests/test_helpers.hpp:46-67). prm = {num_splats,
+// num_classes, k, min_prob, alpha_logit_min, alpha_logit_max, rad_px_min, rad_px_max}.
+// Output arrays must hold num_splats (times 3 / k) entries; k_out receives k.
+void ref_random_splat_map(uint64_t seed, const int32_t wh[2], const double intr[4],
+                          const double R[9], const double t[3], const double prm[8],
+                          double* centers, double* log_radii, double* logits, double* colors,
+                          uint16_t* sem_idx, double* sem_probs, int* k_out) {
+    testutil::SplatSceneParams p;
+    p.num_splats = static_cast<int>(prm[0]);
+    p.num_classes = static_cast<int>(prm[1]);
+    p.k = static_cast<int>(prm[2]);
+    p.min_prob = prm[3];
+    p.alpha_logit_min = prm[4];
+    p.alpha_logit_max = prm[5];
+    p.rad_px_min = prm[6];
+    p.rad_px_max = prm[7];
+    GaussianMap map = testutil::random_splat_map(seed, make_cam(wh, intr), make_pose(R, t), p);
+    const int k = map.k();
+    *k_out = k;
+    std::memcpy(centers, map.centers().data(), map.size() * 24);
+    std::memcpy(log_radii, map.log_radii().data(), map.size() * 8);
+    std::memcpy(logits, map.opacity_logits().data(), map.size() * 8);
+    std::memcpy(colors, map.colors().data(), map.size() * 24);
+    std::memcpy(sem_idx, map.sem_indices().data(), map.size() * k * 2);
+    std::memcpy(sem_probs, map.sem_probs().data(), map.size() * k * 8);
+}
+
+// Camera intrinsics of CameraModel::from_fov (camera.hpp:18-32): out = {W,H,fx,fy,cx,cy}.
+void ref_camera_from_fov(int w, int h, double vfov, double hfov, double out[6]) {
+    CameraModel c = CameraModel::from_fov(w, h, vfov, hfov);
+    out[0] = c.width;
+    out[1] = c.height;
+    out[2] = c.fx;
+    out[3] = c.fy;
+    out[4] = c.cx;
+    out[5] = c.cy;
+}
+
+}  // extern "C"

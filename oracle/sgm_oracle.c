@@ -1,0 +1,508 @@
+/* CPU restatement of the reference render + candidate scoring path.
+ * TEST INFRASTRUCTURE ONLY (see sgm_oracle.h for the pinning story).
+ * Build: gcc -O3 -std=c11 -ffp-contract=off -pthread (oracle/Makefile).
+ */
+#include "sgm_oracle.h"
+
+#include <limits.h>
+#include <pthread.h>
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define K_MAX_FOOTPRINT 0.999999 /* kMaxFootprint, splat_render.hpp:41 */
+
+/* x86-64 cvttsd2si semantics of static_cast<int>(double) as the reference build
+ * executes it: out-of-range and NaN give INT_MIN. */
+static int to_int_x86(double v) {
+    if (!(v > -2147483649.0 && v < 2147483648.0)) return INT_MIN;
+    return (int)v;
+}
+
+static double clampd(double v, double lo, double hi) {
+    /* std::clamp(v, lo, hi): (v < lo) ? lo : (hi < v) ? hi : v */
+    return v < lo ? lo : (hi < v ? hi : v);
+}
+
+/* ---- project_splats: splat_render.cpp:15-47 ---- */
+static int proj_less(const orc_proj* a, const orc_proj* b) {
+    if (a->z != b->z) return a->z < b->z;
+    if (a->mx != b->mx) return a->mx < b->mx;
+    if (a->my != b->my) return a->my < b->my;
+    if (a->alpha != b->alpha) return a->alpha < b->alpha;
+    /* Exact 4-key ties are unspecified in the reference (std::sort is not
+     * stable); the restatement breaks them by map index. */
+    return a->index < b->index;
+}
+static int proj_cmp(const void* pa, const void* pb) {
+    const orc_proj* a = (const orc_proj*)pa;
+    const orc_proj* b = (const orc_proj*)pb;
+    if (proj_less(a, b)) return -1;
+    if (proj_less(b, a)) return 1;
+    return 0;
+}
+
+uint64_t orc_project(const orc_map* map, const orc_camera* cam, const orc_pose* pose,
+                     const orc_options* opt, orc_proj* out) {
+    const double* R = pose->R; /* R_cw(i,j) = R(j,i) (splat_render.cpp:19) */
+    uint64_t v = 0;
+    for (uint64_t i = 0; i < map->n; ++i) {
+        const double d0 = map->centers[3 * i] - pose->t[0];
+        const double d1 = map->centers[3 * i + 1] - pose->t[1];
+        const double d2 = map->centers[3 * i + 2] - pose->t[2];
+        /* Eigen lazy product row i: x0 + (x1 + x2) (splat_render.cpp:25) */
+        const double pcx = R[0] * d0 + (R[3] * d1 + R[6] * d2);
+        const double pcy = R[1] * d0 + (R[4] * d1 + R[7] * d2);
+        const double pcz = R[2] * d0 + (R[5] * d1 + R[8] * d2);
+        if (pcz <= opt->z_near) continue; /* :26 */
+        orc_proj p;
+        p.z = pcz;
+        p.mx = cam->fx * pcx / pcz + cam->cx; /* :29 */
+        p.my = cam->fy * pcy / pcz + cam->cy; /* :30 */
+        p.rad_px = exp(map->log_radii[i]) * cam->fy / pcz; /* :31 */
+        p.alpha = 1.0 / (1.0 + exp(-map->opacity_logits[i])); /* sigmoid, geometry.hpp:84 */
+        p.index = (uint32_t)i;
+        const double reach = opt->truncation_sigmas * p.rad_px; /* :34 */
+        if (p.mx + reach < 0 || p.mx - reach > cam->width || p.my + reach < 0 ||
+            p.my - reach > cam->height)
+            continue; /* :35-37 */
+        out[v++] = p;
+    }
+    qsort(out, v, sizeof(orc_proj), proj_cmp); /* :40-45 */
+    return v;
+}
+
+/* ---- binning: splat_render.cpp:189-213 ---- */
+typedef struct {
+    int tx0, tx1, ty0, ty1;
+} rect_t;
+
+static rect_t tile_rect(const orc_proj* p, const orc_camera* cam, const orc_options* opt) {
+    const int ts = opt->tile_size;
+    const int tiles_x = (cam->width + ts - 1) / ts;
+    const int tiles_y = (cam->height + ts - 1) / ts;
+    const double reach = opt->truncation_sigmas * p->rad_px; /* :205 */
+    rect_t r;
+    int a;
+    a = to_int_x86((p->mx - reach) / ts);
+    r.tx0 = a > 0 ? a : 0; /* :206 */
+    a = to_int_x86((p->mx + reach) / ts);
+    r.tx1 = a < tiles_x - 1 ? a : tiles_x - 1; /* :207 */
+    a = to_int_x86((p->my - reach) / ts);
+    r.ty0 = a > 0 ? a : 0; /* :208 */
+    a = to_int_x86((p->my + reach) / ts);
+    r.ty1 = a < tiles_y - 1 ? a : tiles_y - 1; /* :209 */
+    return r;
+}
+
+static float probe_cutoff(double rad_px, double trunc) {
+    const double cut_sq = trunc * trunc;              /* :180 */
+    const double cutoff_d2 = cut_sq * rad_px * rad_px; /* :195 */
+    return (float)(cutoff_d2 * (1.0 + 1e-5)) + 1e-6f;  /* :203 */
+}
+
+uint64_t orc_bins(const orc_proj* proj, uint64_t v, const orc_camera* cam,
+                  const orc_options* opt, uint32_t* tile_offsets, uint32_t* ids, float* probe3,
+                  uint64_t cap) {
+    const int ts = opt->tile_size;
+    const int tiles_x = (cam->width + ts - 1) / ts;
+    const int tiles_y = (cam->height + ts - 1) / ts;
+    const uint64_t ntiles = (uint64_t)tiles_x * tiles_y;
+    memset(tile_offsets, 0, (ntiles + 1) * sizeof(uint32_t));
+    uint64_t total = 0;
+    for (uint64_t pi = 0; pi < v; ++pi) {
+        rect_t r = tile_rect(&proj[pi], cam, opt);
+        for (int ty = r.ty0; ty <= r.ty1; ++ty)
+            for (int tx = r.tx0; tx <= r.tx1; ++tx) {
+                tile_offsets[(uint64_t)ty * tiles_x + tx + 1]++;
+                ++total;
+            }
+    }
+    for (uint64_t t = 0; t < ntiles; ++t) tile_offsets[t + 1] += tile_offsets[t];
+    if (total > cap || !ids) return total;
+    uint32_t* cursor = (uint32_t*)malloc(ntiles * sizeof(uint32_t));
+    memcpy(cursor, tile_offsets, ntiles * sizeof(uint32_t));
+    for (uint64_t pi = 0; pi < v; ++pi) { /* depth order => each bin in depth order */
+        rect_t r = tile_rect(&proj[pi], cam, opt);
+        const float cut = probe_cutoff(proj[pi].rad_px, opt->truncation_sigmas);
+        for (int ty = r.ty0; ty <= r.ty1; ++ty)
+            for (int tx = r.tx0; tx <= r.tx1; ++tx) {
+                const uint32_t at = cursor[(uint64_t)ty * tiles_x + tx]++;
+                ids[at] = (uint32_t)pi;
+                if (probe3) {
+                    probe3[3 * (uint64_t)at] = (float)proj[pi].mx;
+                    probe3[3 * (uint64_t)at + 1] = (float)proj[pi].my;
+                    probe3[3 * (uint64_t)at + 2] = cut;
+                }
+            }
+    }
+    free(cursor);
+    return total;
+}
+
+/* ---- per-view prepared state ---- */
+typedef struct {
+    orc_proj* proj;
+    uint64_t v, pairs;
+    double *inv_two_r2, *cutoff_d2; /* PackedSplat, :191-199 */
+    float* probe3;
+    uint32_t *offsets, *ids;
+    int tiles_x, tiles_y;
+} view_t;
+
+static int view_prepare(view_t* s, const orc_map* map, const orc_camera* cam,
+                        const orc_pose* pose, const orc_options* opt) {
+    memset(s, 0, sizeof(*s));
+    const int ts = opt->tile_size;
+    s->tiles_x = (cam->width + ts - 1) / ts;
+    s->tiles_y = (cam->height + ts - 1) / ts;
+    const uint64_t ntiles = (uint64_t)s->tiles_x * s->tiles_y;
+    s->proj = (orc_proj*)malloc((map->n ? map->n : 1) * sizeof(orc_proj));
+    s->offsets = (uint32_t*)malloc((ntiles + 1) * sizeof(uint32_t));
+    if (!s->proj || !s->offsets) return -1;
+    s->v = orc_project(map, cam, pose, opt, s->proj);
+    s->inv_two_r2 = (double*)malloc((s->v ? s->v : 1) * sizeof(double));
+    s->cutoff_d2 = (double*)malloc((s->v ? s->v : 1) * sizeof(double));
+    const double cut_sq = opt->truncation_sigmas * opt->truncation_sigmas;
+    for (uint64_t i = 0; i < s->v; ++i) {
+        const double r = s->proj[i].rad_px;
+        s->inv_two_r2[i] = 1.0 / (2.0 * r * r); /* :194 */
+        s->cutoff_d2[i] = cut_sq * r * r;       /* :195 */
+    }
+    s->pairs = orc_bins(s->proj, s->v, cam, opt, s->offsets, NULL, NULL, 0);
+    s->ids = (uint32_t*)malloc((s->pairs ? s->pairs : 1) * sizeof(uint32_t));
+    s->probe3 = (float*)malloc((s->pairs ? s->pairs : 1) * 3 * sizeof(float));
+    if (!s->ids || !s->probe3) return -1;
+    orc_bins(s->proj, s->v, cam, opt, s->offsets, s->ids, s->probe3, s->pairs);
+    return 0;
+}
+
+static void view_free(view_t* s) {
+    free(s->proj);
+    free(s->inv_two_r2);
+    free(s->cutoff_d2);
+    free(s->probe3);
+    free(s->offsets);
+    free(s->ids);
+}
+
+/* Composite one pixel over its tile's bin: splat_render.cpp:261-320. Accumulates
+ * into sem_px (C doubles, pre-zeroed) and returns transmittance. */
+static double composite(const view_t* s, const orc_map* map, const orc_options* opt,
+                        uint32_t channels, uint32_t b0, uint32_t b1, int x, int y,
+                        double acc_color[3], double* acc_depth, double* sem_px, orc_stats* st) {
+    const double px = x + 0.5, py = y + 0.5;
+    const float pxf = (float)px, pyf = (float)py;
+    const int k = map->k;
+    double T = 1.0;
+    uint64_t probes = 0, exact = 0, contrib = 0;
+    for (uint32_t b = b0; b < b1; ++b) {
+        ++probes;
+        const float fdx = pxf - s->probe3[3 * (uint64_t)b];
+        const float fdy = pyf - s->probe3[3 * (uint64_t)b + 1];
+        if (fdx * fdx + fdy * fdy > s->probe3[3 * (uint64_t)b + 2]) continue; /* :276-278 */
+        ++exact;
+        const uint32_t pid = s->ids[b];
+        const orc_proj* p = &s->proj[pid];
+        const double dx = px - p->mx;
+        const double dy = py - p->my;
+        const double d2 = dx * dx + dy * dy;
+        if (d2 > s->cutoff_d2[pid]) continue; /* :283 */
+        ++contrib;
+        double f = p->alpha * exp(-d2 * s->inv_two_r2[pid]); /* :284 */
+        if (f > K_MAX_FOOTPRINT) f = K_MAX_FOOTPRINT;        /* :285 */
+        const double w = f * T;
+        if (channels & ORC_COLOR) {
+            const double* c = &map->colors[(uint64_t)p->index * 3];
+            acc_color[0] += clampd(c[0], 0.0, 1.0) * w;
+            acc_color[1] += clampd(c[1], 0.0, 1.0) * w;
+            acc_color[2] += clampd(c[2], 0.0, 1.0) * w;
+        }
+        if (channels & ORC_DEPTH) *acc_depth += p->z * w; /* :293 */
+        if (channels & ORC_SEM) {
+            const uint16_t* idx = &map->sem_idx[(uint64_t)p->index * k];
+            const double* pr = &map->sem_probs[(uint64_t)p->index * k];
+            for (int j = 0; j < k; ++j) sem_px[idx[j]] += pr[j] * w; /* :305-307 */
+        }
+        T *= (1.0 - f);                                                 /* :311 */
+        if (opt->early_exit && T < opt->transmittance_eps) break;      /* :312 */
+    }
+    if (st) {
+        st->probe_tests += probes;
+        st->exact_tests += exact;
+        st->contributors += contrib;
+    }
+    return T;
+}
+
+int orc_render(const orc_map* map, const orc_camera* cam, const orc_pose* pose,
+               uint32_t channels, const orc_options* opt, double* color, double* depth,
+               double* silhouette, double* sem, orc_stats* stats) {
+    view_t s;
+    if (view_prepare(&s, map, cam, pose, opt)) {
+        view_free(&s);
+        return -1;
+    }
+    const int W = cam->width, H = cam->height, C = map->num_classes + 1;
+    const uint64_t px_count = (uint64_t)W * H;
+    /* alloc_output zero-fills every plane (:57-63) */
+    if (color) memset(color, 0, px_count * 3 * sizeof(double));
+    if (depth) memset(depth, 0, px_count * sizeof(double));
+    if (silhouette) memset(silhouette, 0, px_count * sizeof(double));
+    if (sem) memset(sem, 0, px_count * C * sizeof(double));
+    if (!sem) channels &= ~(uint32_t)ORC_SEM;
+    double* scratch = (double*)calloc((size_t)C, sizeof(double));
+    const int ts = opt->tile_size;
+    for (int ty = 0; ty < s.tiles_y; ++ty)
+        for (int tx = 0; tx < s.tiles_x; ++tx) {
+            const uint64_t tile = (uint64_t)ty * s.tiles_x + tx;
+            const uint32_t b0 = s.offsets[tile], b1 = s.offsets[tile + 1];
+            if (b0 == b1) continue; /* :257 */
+            const int y1 = H < (ty + 1) * ts ? H : (ty + 1) * ts;
+            const int x1 = W < (tx + 1) * ts ? W : (tx + 1) * ts;
+            for (int y = ty * ts; y < y1; ++y)
+                for (int x = tx * ts; x < x1; ++x) {
+                    const uint64_t pix = (uint64_t)y * W + x;
+                    double ac[3] = {0, 0, 0}, ad = 0.0;
+                    double* sp = (channels & ORC_SEM) ? &sem[pix * C] : scratch;
+                    double T = composite(&s, map, opt, channels, b0, b1, x, y, ac, &ad, sp, stats);
+                    if (silhouette) silhouette[pix] = 1.0 - T; /* :314 */
+                    if (color && (channels & ORC_COLOR)) {
+                        color[pix * 3] = ac[0];
+                        color[pix * 3 + 1] = ac[1];
+                        color[pix * 3 + 2] = ac[2];
+                    }
+                    if (depth && (channels & ORC_DEPTH)) depth[pix] = ad;
+                }
+        }
+    if (stats) {
+        stats->visible += s.v;
+        stats->pairs += s.pairs;
+    }
+    free(scratch);
+    view_free(&s);
+    return 0;
+}
+
+double orc_clipped_entropy(const double* p, int n) {
+    double total = 0.0;
+    for (int i = 0; i < n; ++i) total += clampd(p[i], 0.001, 1.0); /* :362 */
+    double h = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const double q = clampd(p[i], 0.001, 1.0) / total; /* :365 */
+        h -= q * log(q);                                   /* :366 */
+    }
+    return h;
+}
+
+/* Sem-only render of one view with per-pixel entropy and exact-zero silhouette
+ * flags; the sem plane is kept one pixel at a time (pixels are independent). */
+static int score_one(const orc_map* map, const orc_camera* cam, const orc_pose* pose,
+                     const orc_options* opt, double* ent_px, double* n_missing,
+                     double* entropy_sum, orc_stats* st) {
+    view_t s;
+    if (view_prepare(&s, map, cam, pose, opt)) {
+        view_free(&s);
+        return -1;
+    }
+    const int W = cam->width, H = cam->height, C = map->num_classes + 1;
+    const uint64_t px_count = (uint64_t)W * H;
+    double* sem_px = (double*)malloc((size_t)C * sizeof(double));
+    double* zero = (double*)calloc((size_t)C, sizeof(double));
+    const double h_empty = orc_clipped_entropy(zero, C);
+    unsigned char* covered = (unsigned char*)calloc(px_count, 1);
+    double* sil = (double*)calloc(px_count, sizeof(double));
+    for (uint64_t i = 0; i < px_count; ++i) ent_px[i] = h_empty;
+    const int ts = opt->tile_size;
+    for (int ty = 0; ty < s.tiles_y; ++ty)
+        for (int tx = 0; tx < s.tiles_x; ++tx) {
+            const uint64_t tile = (uint64_t)ty * s.tiles_x + tx;
+            const uint32_t b0 = s.offsets[tile], b1 = s.offsets[tile + 1];
+            if (b0 == b1) continue;
+            const int y1 = H < (ty + 1) * ts ? H : (ty + 1) * ts;
+            const int x1 = W < (tx + 1) * ts ? W : (tx + 1) * ts;
+            for (int y = ty * ts; y < y1; ++y)
+                for (int x = tx * ts; x < x1; ++x) {
+                    const uint64_t pix = (uint64_t)y * W + x;
+                    memset(sem_px, 0, (size_t)C * sizeof(double));
+                    double ac[3], ad;
+                    const double T = composite(&s, map, opt, ORC_SEM, b0, b1, x, y, ac, &ad,
+                                               sem_px, st);
+                    sil[pix] = 1.0 - T;
+                    covered[pix] = 1;
+                    ent_px[pix] = orc_clipped_entropy(sem_px, C);
+                }
+        }
+    /* explorer.cpp:195-203: sequential row-major sums */
+    uint64_t missing = 0;
+    double entropy = 0.0;
+    for (uint64_t i = 0; i < px_count; ++i) {
+        if (sil[i] == 0.0) ++missing;
+        entropy += ent_px[i];
+    }
+    *n_missing = (double)missing;
+    *entropy_sum = entropy;
+    if (st) {
+        st->visible += s.v;
+        st->pairs += s.pairs;
+    }
+    free(sem_px);
+    free(zero);
+    free(covered);
+    free(sil);
+    view_free(&s);
+    return 0;
+}
+
+typedef struct {
+    const orc_map* map;
+    const orc_camera* cam;
+    const orc_pose* poses;
+    const orc_options* opt;
+    double *n_missing, *entropy_sum;
+    uint64_t n_views;
+    uint64_t next; /* shared view cursor (guarded by mu) */
+    pthread_mutex_t mu;
+    orc_stats total;
+    int err;
+} score_job_t;
+
+static void* score_worker(void* arg) {
+    score_job_t* job = (score_job_t*)arg;
+    const uint64_t px_count = (uint64_t)job->cam->width * job->cam->height;
+    double* ent = (double*)malloc((px_count ? px_count : 1) * sizeof(double));
+    for (;;) {
+        pthread_mutex_lock(&job->mu);
+        const uint64_t v = job->next++;
+        pthread_mutex_unlock(&job->mu);
+        if (v >= job->n_views) break;
+        orc_stats st;
+        memset(&st, 0, sizeof(st));
+        const int e = score_one(job->map, job->cam, &job->poses[v], job->opt, ent,
+                                &job->n_missing[v], &job->entropy_sum[v], &st);
+        pthread_mutex_lock(&job->mu);
+        job->err |= e;
+        job->total.visible += st.visible;
+        job->total.pairs += st.pairs;
+        job->total.probe_tests += st.probe_tests;
+        job->total.exact_tests += st.exact_tests;
+        job->total.contributors += st.contributors;
+        pthread_mutex_unlock(&job->mu);
+    }
+    free(ent);
+    return NULL;
+}
+
+int orc_score_views(const orc_map* map, const orc_camera* cam, uint64_t n_views,
+                    const orc_pose* poses, const orc_options* opt, int threads,
+                    double* n_missing, double* entropy_sum, orc_stats* stats) {
+    score_job_t job;
+    memset(&job, 0, sizeof(job));
+    job.map = map;
+    job.cam = cam;
+    job.poses = poses;
+    job.opt = opt;
+    job.n_missing = n_missing;
+    job.entropy_sum = entropy_sum;
+    job.n_views = n_views;
+    pthread_mutex_init(&job.mu, NULL);
+    if (threads < 1) threads = 1;
+    if ((uint64_t)threads > n_views) threads = n_views ? (int)n_views : 1;
+    pthread_t* th = (pthread_t*)malloc((size_t)threads * sizeof(pthread_t));
+    for (int i = 1; i < threads; ++i) pthread_create(&th[i], NULL, score_worker, &job);
+    score_worker(&job);
+    for (int i = 1; i < threads; ++i) pthread_join(th[i], NULL);
+    free(th);
+    pthread_mutex_destroy(&job.mu);
+    if (stats) *stats = job.total;
+    return job.err ? -1 : 0;
+}
+
+int orc_render_entropy(const orc_map* map, const orc_camera* cam, const orc_pose* pose,
+                       const orc_options* opt, double* entropy) {
+    double nm, es;
+    return score_one(map, cam, pose, opt, entropy, &nm, &es, NULL);
+}
+
+/* ---- combine_scores: explorer.cpp:209-248 ---- */
+static void stable_softmax(const double* v, uint64_t n, double* out) {
+    double mx = -INFINITY;
+    for (uint64_t i = 0; i < n; ++i) {
+        out[i] = 0.0;
+        if (isfinite(v[i])) mx = v[i] > mx ? v[i] : mx; /* std::max(mx, x) */
+    }
+    if (!isfinite(mx)) return;
+    double sum = 0.0;
+    for (uint64_t i = 0; i < n; ++i) {
+        out[i] = isfinite(v[i]) ? exp(v[i] - mx) : 0.0;
+        sum += out[i];
+    }
+    for (uint64_t i = 0; i < n; ++i) out[i] /= sum;
+}
+
+int orc_combine_scores(uint64_t n, const double* n_missing, const double* entropy_sum,
+                       const double* pos3, const double cur[3], double* i_geo, double* i_sem,
+                       double* i_total) {
+    if (n == 0) return 0;
+    double* lm = (double*)malloc(n * sizeof(double));
+    double* dist = (double*)malloc(n * sizeof(double));
+    double* ds = (double*)malloc(n * sizeof(double));
+    for (uint64_t i = 0; i < n; ++i) {
+        lm[i] = n_missing[i] > 0.0 ? log(n_missing[i]) : -INFINITY;
+        const double a = pos3[3 * i] - cur[0], b = pos3[3 * i + 1] - cur[1],
+                     c = pos3[3 * i + 2] - cur[2];
+        dist[i] = sqrt(a * a + (b * b + c * c)); /* Eigen norm(): redux halving */
+    }
+    stable_softmax(lm, n, i_geo);
+    stable_softmax(entropy_sum, n, i_sem);
+    stable_softmax(dist, n, ds);
+    int any = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const double dist_factor = n == 1 ? 1.0 : 1.0 - ds[i];
+        i_total[i] = dist_factor * i_geo[i] * i_sem[i];
+        if (i_total[i] > 0.0) any = 1;
+    }
+    free(lm);
+    free(dist);
+    free(ds);
+    return any;
+}
+
+/* ---- look_at: geometry.hpp:44-56 with Eigen's evaluation order ---- */
+static void normalize3(double v[3]) {
+    const double z = v[0] * v[0] + (v[1] * v[1] + v[2] * v[2]);
+    if (z > 0.0) {
+        const double s = sqrt(z);
+        v[0] /= s;
+        v[1] /= s;
+        v[2] /= s;
+    }
+}
+static void cross3(const double a[3], const double b[3], double o[3]) {
+    o[0] = a[1] * b[2] - a[2] * b[1];
+    o[1] = a[2] * b[0] - a[0] * b[2];
+    o[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+void orc_look_at(const double pos[3], const double target[3], orc_pose* out) {
+    static const double up[3] = {0.0, 1.0, 0.0};
+    static const double ux[3] = {1.0, 0.0, 0.0};
+    double z[3] = {target[0] - pos[0], target[1] - pos[1], target[2] - pos[2]};
+    normalize3(z);
+    double x[3], y[3];
+    cross3(z, up, x);
+    if (sqrt(x[0] * x[0] + (x[1] * x[1] + x[2] * x[2])) < 1e-9) cross3(z, ux, x);
+    normalize3(x);
+    cross3(z, x, y);
+    for (int i = 0; i < 3; ++i) {
+        out->R[3 * i + 0] = x[i];
+        out->R[3 * i + 1] = y[i];
+        out->R[3 * i + 2] = z[i];
+        out->t[i] = pos[i];
+    }
+}
+
+void orc_candidate_pose(const double pos[3], const double dir[3], orc_pose* out) {
+    const double target[3] = {pos[0] + dir[0], pos[1] + dir[1], pos[2] + dir[2]};
+    orc_look_at(pos, target, out);
+}

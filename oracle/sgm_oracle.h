@@ -1,0 +1,107 @@
+/* CPU restatement of the reference's candidate-view render + scoring path.
+ *
+ * TEST INFRASTRUCTURE ONLY. This is the checker that tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline leg compare the CUDA product against; the product
+ * (paper_2506_00225_b200) never links or calls it.
+ *
+ * Parity pin: tests/test_oracle.py checks this restatement bit-for-bit against the
+ * reference's own code compiled unmodified into oracle/_ref/libsgm_ref.so (projections,
+ * planes, n_missing, entropy_sum, combine_scores) and against the reference tests'
+ * known-answer values (proj/tests/test_splat_render.cpp:24-265,
+ * proj/tests/test_explorer.cpp:183-378) stored in tests/golden/.
+ *
+ * Every function cites the reference lines it restates. Arithmetic is fp64 with no
+ * FMA contraction (built with -ffp-contract=off), libm exp/log, and Eigen 3.3+
+ * evaluation order for the 3x3 mat-vec: pc_i = a0 + (a1 + a2) (redux halving).
+ */
+#ifndef SGM_ORACLE_H
+#define SGM_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+    int32_t width, height;
+    double fx, fy, cx, cy;
+} orc_camera; /* CameraModel, proj/include/splatmap/camera.hpp:11-50 */
+
+typedef struct {
+    double R[9]; /* cam->world rotation, row-major */
+    double t[3];
+} orc_pose; /* Pose, proj/include/splatmap/geometry.hpp:18-41 */
+
+typedef struct {
+    int32_t early_exit;
+    double transmittance_eps, z_near, truncation_sigmas;
+    int32_t tile_size;
+} orc_options; /* RenderOptions, proj/include/splatmap/splat_render.hpp:22-28 */
+
+typedef struct {
+    uint64_t n;
+    int32_t k, num_classes;
+    const double *centers, *log_radii, *opacity_logits, *colors;
+    const uint16_t* sem_idx;
+    const double* sem_probs;
+} orc_map; /* GaussianMap SoA, proj/include/splatmap/gaussian_map.hpp:105-113 */
+
+typedef struct {
+    double mx, my, rad_px, z, alpha;
+    uint32_t index;
+} orc_proj; /* SplatProjection, splat_render.hpp:32-39 */
+
+typedef struct {
+    uint64_t visible;      /* V: culled-in projections */
+    uint64_t pairs;        /* P: (tile, projection) pairs */
+    uint64_t probe_tests;  /* float prefilter evaluations */
+    uint64_t exact_tests;  /* fp64 d2 tests (prefilter survivors) */
+    uint64_t contributors; /* K: composited (pixel, splat) pairs */
+} orc_stats;
+
+enum { ORC_COLOR = 1, ORC_DEPTH = 2, ORC_SEM = 4 };
+
+/* project_splats, proj/src/splat_render.cpp:15-47. Returns V; out holds >= map->n. */
+uint64_t orc_project(const orc_map* map, const orc_camera* cam, const orc_pose* pose,
+                     const orc_options* opt, orc_proj* out);
+
+/* Binning, proj/src/splat_render.cpp:189-213, over orc_project's output.
+ * tile_offsets[tiles+1]; ids[P] (projection ids in bin order); probe3[3P] (float mx,
+ * my, cutoff_d2). Returns P; if P > cap only the offsets are filled. */
+uint64_t orc_bins(const orc_proj* proj, uint64_t v, const orc_camera* cam,
+                  const orc_options* opt, uint32_t* tile_offsets, uint32_t* ids, float* probe3,
+                  uint64_t cap);
+
+/* render, proj/src/splat_render.cpp:170-328. Planes in the reference layout
+ * (color px*3, depth px, silhouette px, sem px*C); NULL planes are skipped. */
+int orc_render(const orc_map* map, const orc_camera* cam, const orc_pose* pose,
+               uint32_t channels, const orc_options* opt, double* color, double* depth,
+               double* silhouette, double* sem, orc_stats* stats);
+
+/* clipped_entropy, proj/src/splat_render.cpp:360-369. */
+double orc_clipped_entropy(const double* p, int n);
+
+/* refresh_candidate_scores, proj/src/explorer.cpp:186-205, over explicit poses, with
+ * `threads` pthreads over views (each view's sum is sequential row-major as in
+ * the reference, so results do not depend on the thread count). */
+int orc_score_views(const orc_map* map, const orc_camera* cam, uint64_t n_views,
+                    const orc_pose* poses, const orc_options* opt, int threads,
+                    double* n_missing, double* entropy_sum, orc_stats* stats);
+
+/* Per-pixel clipped entropy image, render_entropy (splat_render.cpp:378-390). */
+int orc_render_entropy(const orc_map* map, const orc_camera* cam, const orc_pose* pose,
+                       const orc_options* opt, double* entropy);
+
+/* combine_scores + stable_softmax, proj/src/explorer.cpp:209-248. Returns 1 if any > 0. */
+int orc_combine_scores(uint64_t n, const double* n_missing, const double* entropy_sum,
+                       const double* pos3, const double cur[3], double* i_geo, double* i_sem,
+                       double* i_total);
+
+/* CandidatePose::camera_pose() = look_at(p, p + d), explorer.hpp:105 + geometry.hpp:44-56. */
+void orc_candidate_pose(const double pos[3], const double dir[3], orc_pose* out);
+void orc_look_at(const double pos[3], const double target[3], orc_pose* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,33 @@
+"""B200-native candidate-view render + scoring for ActiveSGM (arxiv 2506.00225).
+
+The compute path is libsgm_b200.so (hand-written sm_100a CUDA behind the C ABI in
+include/sgm.h); this package is the host-side mirror of the reference API.
+"""
+from .splatmap import (  # noqa: F401
+    K_MAX_FOOTPRINT,
+    PROJECTION_DTYPE,
+    CameraModel,
+    CandidatePool,
+    CandidatePose,
+    CandidateState,
+    Context,
+    GaussianMap,
+    Pose,
+    RenderChannels,
+    RenderOptions,
+    RenderOutput,
+    SemanticGaussian,
+    bins_of_last_render,
+    clipped_entropy,
+    combine_scores,
+    deg_to_rad,
+    look_at,
+    prune_pool,
+    refresh_candidate_scores,
+    render,
+    render_entropy,
+    render_reference,
+    score_candidates,
+    score_poses,
+    sigmoid,
+)

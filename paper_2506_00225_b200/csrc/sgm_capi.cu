@@ -1,0 +1,775 @@
+// C ABI (include/sgm.h) and the host pipeline that drives the sm_100a kernels.
+//
+// Pipeline for a batch of views (all on the ctx stream):
+//   1. K1 k_preprocess over (Gaussian, view): compact visible (z, index), count V, P
+//   2. one D2H of the per-view V/P counts (the only host sync before the results)
+//   3. per view: CUB radix sort on fp64 z -> k_tiefix -> k_pack -> CUB scan of
+//      tile counts -> k_emit2 -> CUB stable radix sort on the bin id -> k_ranges
+//   4. one batched raster launch over (8x8 tile, view)
+//   5. k_reduce_scores (score) / planes already written (render)
+// Views whose pair lists do not fit the scratch budget together are split into
+// sub-batches; results do not depend on the split (per-view work is independent).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/sgm.h"
+#include "sgm_internal.h"
+
+using namespace sgm;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    // Grows (never shrinks); contents are not preserved.
+    cudaError_t reserve(size_t want) {
+        if (want <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        const size_t b = std::max<size_t>(want, 256);
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e == cudaSuccess) bytes = b;
+        return e;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct HostBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~HostBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    cudaError_t reserve(size_t want) {
+        if (want <= bytes) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMallocHost(&p, std::max<size_t>(want, 256));
+        if (e == cudaSuccess) bytes = std::max<size_t>(want, 256);
+        return e;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct SgmError {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    throw SgmError{code, buf};
+}
+
+#define CK(call)                                                                       \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess)                                                         \
+            fail(e_ == cudaErrorMemoryAllocation ? SGM_ERR_OOM : SGM_ERR_CUDA,         \
+                 "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__,     \
+                 __LINE__);                                                            \
+    } while (0)
+
+}  // namespace
+
+struct sgm_map {
+    DevMap dev;
+    int num_classes = 0;
+    DevBuf geo;    // cx, cy, cz, rad, alpha (5 x n doubles)
+    DevBuf color;  // [n][4]
+    DevBuf idx;    // [n][k] u16
+    DevBuf prob;   // [n][k] f64
+};
+
+struct sgm_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    sgm_stats stats{};
+    bool profiling = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+    // scratch
+    DevBuf poses, vcount, pcount, keys, vals, keys_alt, vals_alt, packed, counts, offsets;
+    DevBuf tkeys, tvals, tkeys_alt, tvals_alt, ranges, ent_part, miss_part, views, out,
+        contributors, cub_tmp, planes, dbg;
+    HostBuf h_counts, h_views, h_poses, h_out;
+
+    // state of the last render (for sgm_last_*)
+    bool last_valid = false;
+    uint32_t last_V = 0;
+    uint64_t last_P = 0;
+    int last_bin_tiles = 0;
+    const sgm_map* last_map = nullptr;
+    CamParams last_cam{};
+    OptParams last_opt{};
+    PoseParams last_pose{};
+};
+
+namespace {
+
+CamParams to_cam(const sgm_camera* c) {
+    if (!c) fail(SGM_ERR_INVALID, "camera is null");
+    if (c->width <= 0 || c->height <= 0) fail(SGM_ERR_INVALID, "camera: resolution must be positive");
+    return CamParams{c->width, c->height, c->fx, c->fy, c->cx, c->cy};
+}
+
+OptParams to_opt(const sgm_options* o, const CamParams& cam) {
+    sgm_options d{1, 1e-4, 0.01, 3.0, 8};
+    const sgm_options& s = o ? *o : d;
+    if (s.tile_size <= 0 || s.tile_size % kTile != 0)
+        fail(SGM_ERR_UNSUPPORTED, "tile_size %d: this build bins at multiples of %d", s.tile_size,
+             kTile);
+    OptParams p;
+    p.early_exit = s.early_exit ? 1 : 0;
+    p.eps = s.transmittance_eps;
+    p.z_near = s.z_near;
+    p.trunc = s.truncation_sigmas;
+    p.cut_sq = s.truncation_sigmas * s.truncation_sigmas;
+    p.ts = s.tile_size;
+    p.tiles_x = (cam.W + s.tile_size - 1) / s.tile_size;
+    p.tiles_y = (cam.H + s.tile_size - 1) / s.tile_size;
+    return p;
+}
+
+PoseParams to_pose(const sgm_pose& p) {
+    PoseParams q;
+    for (int i = 0; i < 3; ++i)
+        for (int k = 0; k < 3; ++k) q.Rcw[3 * i + k] = p.R[3 * k + i];  // R_cw = R^T
+    for (int i = 0; i < 3; ++i) q.t[i] = p.t[i];
+    return q;
+}
+
+int guard(sgm_ctx* ctx, const std::function<void()>& fn);
+
+unsigned tile_bits(uint64_t tiles) {
+    unsigned b = 1;
+    while ((1ull << b) < tiles) ++b;
+    return b;
+}
+
+enum class Mode { Score, Render };
+
+struct RenderTargets {
+    double* color = nullptr;
+    double* depth = nullptr;
+    double* sil = nullptr;
+    double* sem = nullptr;
+    uint32_t channels = 0;
+};
+
+// Bins one view (step 3). Writes ranges / sorted list / packed into the per-view
+// slices and returns via the slice pointers. vals/keys hold the compacted (z, idx).
+void bin_view(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const OptParams& o,
+              const PoseParams* d_pose, double* keys, uint32_t* vals, uint32_t V, uint64_t P,
+              PackedSplat* packed, uint32_t* list, uint2* ranges, int bin_tiles) {
+    cudaStream_t s = ctx->stream;
+    CK(cudaMemsetAsync(ranges, 0, sizeof(uint2) * bin_tiles, s));
+    if (V == 0) return;
+    // K2: depth rank (fp64 radix sort; ties fixed below)
+    cub::DoubleBuffer<double> dk(keys, ctx->keys_alt.as<double>());
+    cub::DoubleBuffer<uint32_t> dv(vals, ctx->vals_alt.as<uint32_t>());
+    size_t tmp = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, V, 0, 64, s));
+    CK(ctx->cub_tmp.reserve(tmp));
+    CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, dk, dv, V, 0, 64, s));
+    ctx->stats.kernel_launches += 1;  // counted as one library sort call
+    launch_tiefix(map->dev, d_pose, cam, o, dk.Current(), dv.Current(), V, s);
+    launch_pack(map->dev, d_pose, cam, o, dv.Current(), V, packed,
+                ctx->counts.as<unsigned long long>(), s);
+    ctx->stats.kernel_launches += (V >= 2 ? 1 : 0) + 1;
+    // keep the sorted indices for sgm_last_projections
+    if (dv.Current() != vals) CK(cudaMemcpyAsync(vals, dv.Current(), 4ull * V, cudaMemcpyDeviceToDevice, s));
+    // K3: offsets = exclusive scan of tile counts (V+1 entries: last = P)
+    unsigned long long* cnt = ctx->counts.as<unsigned long long>();
+    unsigned long long* off = ctx->offsets.as<unsigned long long>();
+    CK(cudaMemsetAsync(cnt + V, 0, sizeof(unsigned long long), s));
+    tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, off, V + 1, s));
+    CK(ctx->cub_tmp.reserve(tmp));
+    CK(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp, cnt, off, V + 1, s));
+    ctx->stats.kernel_launches += 1;
+    if (P == 0) return;
+    uint32_t* tk = ctx->tkeys.as<uint32_t>();
+    launch_emit_pairs(map->dev, d_pose, cam, o, packed, off, V, tk, list, s);
+    ctx->stats.kernel_launches += 1;
+    cub::DoubleBuffer<uint32_t> pk(tk, ctx->tkeys_alt.as<uint32_t>());
+    cub::DoubleBuffer<uint32_t> pv(list, ctx->tvals_alt.as<uint32_t>());
+    tmp = 0;
+    const int bits = static_cast<int>(tile_bits(static_cast<uint64_t>(bin_tiles)));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, pk, pv, P, 0, bits, s));
+    CK(ctx->cub_tmp.reserve(tmp));
+    CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, pk, pv, P, 0, bits, s));
+    ctx->stats.kernel_launches += 1;
+    if (pv.Current() != list)
+        CK(cudaMemcpyAsync(list, pv.Current(), 4ull * P, cudaMemcpyDeviceToDevice, s));
+    launch_ranges(pk.Current(), P, ranges, s);
+    ctx->stats.kernel_launches += 1;
+}
+
+// Runs n views. Score mode writes n_missing/entropy_sum (host); render mode (n == 1)
+// writes planes to device targets.
+void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const OptParams& o,
+               uint64_t n, const PoseParams* poses, Mode mode, const RenderTargets& rt,
+               double* h_missing, double* h_entropy) {
+    cudaStream_t s = ctx->stream;
+    const uint64_t N = map->dev.n;
+    const int bin_tiles = o.tiles_x * o.tiles_y;
+    const int rtx = (cam.W + kTile - 1) / kTile;
+    const int rty = (cam.H + kTile - 1) / kTile;
+    const int rtiles = rtx * rty;
+    ctx->last_valid = false;
+
+    // batch size bounded by a scratch budget for the per-view N-sized arrays
+    const size_t per_view = std::max<uint64_t>(N, 1) * (8 + 4 + sizeof(PackedSplat)) +
+                            static_cast<size_t>(bin_tiles) * sizeof(uint2) +
+                            static_cast<size_t>(rtiles) * 12 + 256;
+    const size_t budget = size_t(12) << 30;
+    uint64_t B = std::max<uint64_t>(1, std::min<uint64_t>(n, std::max<size_t>(1, budget / per_view)));
+    B = std::min<uint64_t>(B, 64);
+    if (mode == Mode::Render) B = 1;
+
+    const size_t NS = std::max<uint64_t>(N, 1);
+    CK(ctx->poses.reserve(sizeof(PoseParams) * B));
+    CK(ctx->vcount.reserve(4 * B));
+    CK(ctx->pcount.reserve(8 * B));
+    CK(ctx->keys.reserve(8 * NS * B));
+    CK(ctx->vals.reserve(4 * NS * B));
+    CK(ctx->keys_alt.reserve(8 * NS));
+    CK(ctx->vals_alt.reserve(4 * NS));
+    CK(ctx->packed.reserve(sizeof(PackedSplat) * NS * B));
+    CK(ctx->counts.reserve(8 * (NS + 1)));
+    CK(ctx->offsets.reserve(8 * (NS + 1)));
+    CK(ctx->ranges.reserve(sizeof(uint2) * bin_tiles * B));
+    CK(ctx->ent_part.reserve(8ull * rtiles * B));
+    CK(ctx->miss_part.reserve(4ull * rtiles * B));
+    CK(ctx->views.reserve(sizeof(ViewDesc) * B));
+    CK(ctx->out.reserve(16 * B));
+    CK(ctx->contributors.reserve(8));
+    CK(ctx->h_counts.reserve(16 * B + 8));
+    CK(ctx->h_views.reserve(sizeof(ViewDesc) * B));
+    CK(ctx->h_poses.reserve(sizeof(PoseParams) * B));
+    CK(ctx->h_out.reserve(16 * B));
+
+    for (uint64_t b0 = 0; b0 < n; b0 += B) {
+        const int nb = static_cast<int>(std::min<uint64_t>(B, n - b0));
+        if (ctx->profiling) CK(cudaEventRecord(ctx->ev[0], s));
+        std::memcpy(ctx->h_poses.p, poses + b0, sizeof(PoseParams) * nb);
+        CK(cudaMemcpyAsync(ctx->poses.p, ctx->h_poses.p, sizeof(PoseParams) * nb,
+                           cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(ctx->vcount.p, 0, 4 * nb, s));
+        CK(cudaMemsetAsync(ctx->pcount.p, 0, 8 * nb, s));
+        CK(cudaMemsetAsync(ctx->contributors.p, 0, 8, s));
+        launch_preprocess(map->dev, ctx->poses.as<PoseParams>(), cam, o, nb, ctx->keys.as<double>(),
+                          ctx->vals.as<uint32_t>(), NS, ctx->vcount.as<uint32_t>(),
+                          ctx->pcount.as<unsigned long long>(), s);
+        ctx->stats.kernel_launches += (N > 0) ? 1 : 0;
+        uint32_t* hv = ctx->h_counts.as<uint32_t>();
+        unsigned long long* hp = reinterpret_cast<unsigned long long*>(ctx->h_counts.as<char>() + 8 * B);
+        CK(cudaMemcpyAsync(hv, ctx->vcount.p, 4 * nb, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hp, ctx->pcount.p, 8 * nb, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::vector<uint32_t> V(hv, hv + nb);
+        std::vector<uint64_t> P(hp, hp + nb);
+        for (int v = 0; v < nb; ++v)
+            if (P[v] >= (1ull << 32)) fail(SGM_ERR_UNSUPPORTED, "view has %llu tile pairs (>= 2^32)",
+                                          static_cast<unsigned long long>(P[v]));
+
+        // sub-batches by pair budget
+        const uint64_t pair_budget = (uint64_t(8) << 30) / 8;  // pairs (u32 key + u32 val)
+        int v0 = 0;
+        while (v0 < nb) {
+            int v1 = v0;
+            uint64_t sumP = 0, maxP = 0;
+            while (v1 < nb && (v1 == v0 || sumP + P[v1] <= pair_budget)) {
+                sumP += P[v1];
+                maxP = std::max<uint64_t>(maxP, P[v1]);
+                ++v1;
+            }
+            CK(ctx->tvals.reserve(4 * std::max<uint64_t>(sumP, 1)));
+            CK(ctx->tkeys.reserve(4 * std::max<uint64_t>(maxP, 1)));
+            CK(ctx->tkeys_alt.reserve(4 * std::max<uint64_t>(maxP, 1)));
+            CK(ctx->tvals_alt.reserve(4 * std::max<uint64_t>(maxP, 1)));
+            ViewDesc* hvd = ctx->h_views.as<ViewDesc>();
+            uint64_t list_off = 0;
+            for (int v = v0; v < nb; ++v) {
+                if (v >= v1) break;
+                double* keys = ctx->keys.as<double>() + NS * v;
+                uint32_t* vals = ctx->vals.as<uint32_t>() + NS * v;
+                PackedSplat* packed = ctx->packed.as<PackedSplat>() + NS * v;
+                uint32_t* list = ctx->tvals.as<uint32_t>() + list_off;
+                uint2* ranges = ctx->ranges.as<uint2>() + static_cast<size_t>(bin_tiles) * v;
+                bin_view(ctx, map, cam, o, ctx->poses.as<PoseParams>() + v, keys, vals, V[v], P[v],
+                         packed, list, ranges, bin_tiles);
+                ViewDesc d{};
+                d.ranges = ranges;
+                d.list = list;
+                d.packed = packed;
+                d.ent_partial = ctx->ent_part.as<double>() + static_cast<size_t>(rtiles) * v;
+                d.miss_partial = ctx->miss_part.as<uint32_t>() + static_cast<size_t>(rtiles) * v;
+                d.color = rt.color;
+                d.depth = rt.depth;
+                d.sil = rt.sil;
+                d.sem = rt.sem;
+                d.contributors = ctx->contributors.as<unsigned long long>();
+                hvd[v - v0] = d;
+                list_off += P[v];
+                ctx->stats.visible += V[v];
+                ctx->stats.pairs += P[v];
+            }
+            const int nsub = v1 - v0;
+            CK(cudaMemcpyAsync(ctx->views.p, hvd, sizeof(ViewDesc) * nsub, cudaMemcpyHostToDevice, s));
+            if (ctx->profiling) CK(cudaEventRecord(ctx->ev[1], s));
+            RasterParams rp{};
+            rp.map = map->dev;
+            rp.cam = cam;
+            rp.opt = o;
+            rp.views = ctx->views.as<ViewDesc>();
+            rp.tiles_per_view = rtiles;
+            rp.raster_tiles_x = rtx;
+            rp.channels = rt.channels;
+            if (mode == Mode::Score)
+                launch_raster_score(rp, nsub, s);
+            else
+                launch_raster_render(rp, nsub, s);
+            CK(cudaGetLastError());
+            ctx->stats.kernel_launches += 1;
+            ctx->stats.raster_launches += 1;
+            if (ctx->profiling) CK(cudaEventRecord(ctx->ev[2], s));
+            if (mode == Mode::Score) {
+                launch_reduce_scores(ctx->views.as<ViewDesc>(), nsub, rtiles, ctx->out.as<double>(),
+                                     ctx->out.as<double>() + nsub, s);
+                ctx->stats.kernel_launches += 1;
+                double* ho = ctx->h_out.as<double>();
+                CK(cudaMemcpyAsync(ho, ctx->out.p, 16 * nsub, cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                for (int v = 0; v < nsub; ++v) {
+                    h_missing[b0 + v0 + v] = ho[v];
+                    h_entropy[b0 + v0 + v] = ho[nsub + v];
+                }
+            } else {
+                CK(cudaStreamSynchronize(s));
+            }
+            if (ctx->profiling) {
+                float a = 0, b = 0;
+                CK(cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]));
+                CK(cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]));
+                ctx->stats.binning_ms += a;
+                ctx->stats.raster_ms += b;
+                CK(cudaEventRecord(ctx->ev[0], s));
+            }
+            unsigned long long* kc = reinterpret_cast<unsigned long long*>(ctx->h_counts.as<char>() + 8 * B) + B;
+            CK(cudaMemcpyAsync(kc, ctx->contributors.p, 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemsetAsync(ctx->contributors.p, 0, 8, s));
+            CK(cudaStreamSynchronize(s));
+            ctx->stats.contributors += *kc;
+            v0 = v1;
+        }
+        ctx->stats.views += nb;
+        if (mode == Mode::Render) {
+            ctx->last_valid = true;
+            ctx->last_V = V[0];
+            ctx->last_P = P[0];
+            ctx->last_bin_tiles = bin_tiles;
+            ctx->last_map = map;
+            ctx->last_cam = cam;
+            ctx->last_opt = o;
+            ctx->last_pose = poses[0];
+        }
+    }
+}
+
+int guard(sgm_ctx* ctx, const std::function<void()>& fn) {
+    try {
+        fn();
+        if (ctx) ctx->err.clear();
+        return SGM_OK;
+    } catch (const SgmError& e) {
+        if (ctx) ctx->err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        if (ctx) ctx->err = "host allocation failed";
+        return SGM_ERR_OOM;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->err = e.what();
+        return SGM_ERR_INVALID;
+    }
+}
+
+void need_ctx(sgm_ctx* ctx) {
+    if (!ctx) fail(SGM_ERR_INVALID, "ctx is null");
+    CK(cudaSetDevice(ctx->device));
+}
+
+void do_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const sgm_pose* pose,
+               uint32_t channels, const sgm_options* opt, double* d_color, double* d_depth,
+               double* d_sil, double* d_sem, uint64_t* n_proj) {
+    need_ctx(ctx);
+    if (!map) fail(SGM_ERR_INVALID, "map is null");
+    if (!pose) fail(SGM_ERR_INVALID, "pose is null");
+    if (channels & SGM_RETAIN_CONTRIBUTORS)
+        fail(SGM_ERR_UNSUPPORTED, "retain_contributors is not served by this build yet");
+    const CamParams cam = to_cam(camera);
+    const OptParams o = to_opt(opt, cam);
+    const PoseParams p = to_pose(*pose);
+    RenderTargets rt;
+    rt.channels = channels;
+    rt.color = (channels & SGM_COLOR) ? d_color : nullptr;
+    rt.depth = (channels & SGM_DEPTH) ? d_depth : nullptr;
+    rt.sem = (channels & SGM_SEMANTICS) ? d_sem : nullptr;
+    rt.sil = d_sil;
+    run_views(ctx, map, cam, o, 1, &p, Mode::Render, rt, nullptr, nullptr);
+    if (n_proj) *n_proj = ctx->last_V;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sgm_abi_version(void) { return SGM_ABI_VERSION; }
+
+int sgm_ctx_create(int device, sgm_ctx** out) {
+    g_create_error.clear();
+    if (!out) {
+        g_create_error = "out is null";
+        return SGM_ERR_INVALID;
+    }
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        g_create_error = std::string("no CUDA device available (this library has no CPU path): ") +
+                         cudaGetErrorString(e);
+        return SGM_ERR_CUDA;
+    }
+    if (device < 0 || device >= count) {
+        g_create_error = "device index out of range";
+        return SGM_ERR_INVALID;
+    }
+    auto* ctx = new (std::nothrow) sgm_ctx();
+    if (!ctx) return SGM_ERR_OOM;
+    ctx->device = device;
+    int rc = guard(ctx, [&] {
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        for (auto& ev : ctx->ev) CK(cudaEventCreate(&ev));
+    });
+    if (rc != SGM_OK) {
+        g_create_error = ctx->err;
+        delete ctx;
+        return rc;
+    }
+    *out = ctx;
+    return SGM_OK;
+}
+
+void sgm_ctx_destroy(sgm_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (auto& ev : ctx->ev)
+        if (ev) cudaEventDestroy(ev);
+    cudaStream_t s = ctx->stream;
+    delete ctx;
+    if (s) cudaStreamDestroy(s);
+}
+
+const char* sgm_last_error(const sgm_ctx* ctx) {
+    return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+void* sgm_ctx_stream(sgm_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int sgm_ctx_synchronize(sgm_ctx* ctx) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int sgm_ctx_set_profiling(sgm_ctx* ctx, int enabled) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        ctx->profiling = enabled != 0;
+    });
+}
+
+int sgm_ctx_get_stats(const sgm_ctx* ctx, sgm_stats* out) {
+    if (!ctx || !out) return SGM_ERR_INVALID;
+    *out = ctx->stats;
+    return SGM_OK;
+}
+
+int sgm_ctx_reset_stats(sgm_ctx* ctx) {
+    if (!ctx) return SGM_ERR_INVALID;
+    ctx->stats = sgm_stats{};
+    return SGM_OK;
+}
+
+int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, const double* centers,
+                   const double* log_radii, const double* opacity_logits, const double* colors,
+                   const uint16_t* sem_indices, const double* sem_probs, sgm_map** out) {
+    sgm_map* m = nullptr;
+    int rc = guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!out) fail(SGM_ERR_INVALID, "out is null");
+        *out = nullptr;
+        // GaussianMap(k, num_classes) invariant, gaussian_map.hpp:63-66
+        if (k < 1 || k > num_classes + 1)
+            fail(SGM_ERR_INVALID, "map: k must be in [1, num_classes+1]");
+        if (n > 0 && (!centers || !log_radii || !opacity_logits || !colors || !sem_indices || !sem_probs))
+            fail(SGM_ERR_INVALID, "map: null array with n > 0");
+        if (n >= (1ull << 32)) fail(SGM_ERR_UNSUPPORTED, "map: more than 2^32-1 Gaussians");
+        const int C = num_classes + 1;
+        m = new sgm_map();
+        m->num_classes = num_classes;
+        const size_t ns = std::max<uint64_t>(n, 1);
+        std::vector<double> geo(5 * ns, 0.0), col(4 * ns, 0.0);
+        for (uint64_t i = 0; i < n; ++i) {
+            geo[i] = centers[3 * i];
+            geo[ns + i] = centers[3 * i + 1];
+            geo[2 * ns + i] = centers[3 * i + 2];
+            geo[3 * ns + i] = std::exp(log_radii[i]);                      // radius()
+            geo[4 * ns + i] = 1.0 / (1.0 + std::exp(-opacity_logits[i]));  // sigmoid
+            for (int c = 0; c < 3; ++c) col[4 * i + c] = std::clamp(colors[3 * i + c], 0.0, 1.0);
+        }
+        // class ids < C and duplicate detection (duplicates force ordered RMWs)
+        int dup = 0;
+        std::vector<uint32_t> seen(static_cast<size_t>(C), 0xffffffffu);
+        for (uint64_t i = 0; i < n; ++i)
+            for (int j = 0; j < k; ++j) {
+                const uint16_t c = sem_indices[i * k + j];
+                if (c >= C)
+                    fail(SGM_ERR_INVALID, "map: semantic index %u >= channels %d (gaussian %llu)",
+                         c, C, static_cast<unsigned long long>(i));
+                if (seen[c] == static_cast<uint32_t>(i)) dup = 1;
+                seen[c] = static_cast<uint32_t>(i);
+            }
+        cudaStream_t s = ctx->stream;
+        CK(m->geo.reserve(8 * geo.size()));
+        CK(m->color.reserve(8 * col.size()));
+        CK(m->idx.reserve(2 * ns * k));
+        CK(m->prob.reserve(8 * ns * k));
+        CK(cudaMemcpyAsync(m->geo.p, geo.data(), 8 * geo.size(), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(m->color.p, col.data(), 8 * col.size(), cudaMemcpyHostToDevice, s));
+        if (n) {
+            CK(cudaMemcpyAsync(m->idx.p, sem_indices, 2 * n * k, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(m->prob.p, sem_probs, 8 * n * k, cudaMemcpyHostToDevice, s));
+        }
+        CK(cudaStreamSynchronize(s));
+        DevMap& d = m->dev;
+        d.n = n;
+        d.k = k;
+        d.C = C;
+        const double* g = m->geo.as<double>();
+        d.cx = g;
+        d.cy = g + ns;
+        d.cz = g + 2 * ns;
+        d.rad = g + 3 * ns;
+        d.alpha = g + 4 * ns;
+        d.color4 = m->color.as<double>();
+        d.sem_idx = m->idx.as<uint16_t>();
+        d.sem_prob = m->prob.as<double>();
+        d.dup_idx = dup;
+        *out = m;
+        m = nullptr;
+    });
+    delete m;
+    return rc;
+}
+
+void sgm_map_release(sgm_ctx* ctx, sgm_map* map) {
+    if (!map) return;
+    if (ctx) {
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        if (ctx->last_map == map) ctx->last_valid = false;
+    }
+    delete map;
+}
+
+int sgm_render_device(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam, const sgm_pose* pose,
+                      uint32_t channels, const sgm_options* opt, double* d_color, double* d_depth,
+                      double* d_sil, double* d_sem, uint64_t* n_projections) {
+    return guard(ctx, [&] {
+        if (!d_sil) fail(SGM_ERR_INVALID, "silhouette plane is required");
+        do_render(ctx, map, cam, pose, channels, opt, d_color, d_depth, d_sil, d_sem, n_projections);
+    });
+}
+
+int sgm_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const sgm_pose* pose,
+               uint32_t channels, const sgm_options* opt, double* color, double* depth,
+               double* silhouette, double* sem, uint64_t* n_projections) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!map) fail(SGM_ERR_INVALID, "map is null");
+        const CamParams cam = to_cam(camera);
+        if (!silhouette) fail(SGM_ERR_INVALID, "silhouette plane is required");
+        const size_t px = static_cast<size_t>(cam.W) * cam.H;
+        const size_t C = static_cast<size_t>(map->dev.C);
+        const bool want_c = (channels & SGM_COLOR) && color;
+        const bool want_d = (channels & SGM_DEPTH) && depth;
+        const bool want_s = (channels & SGM_SEMANTICS) && sem;
+        const size_t need = px * (1 + (want_c ? 3 : 0) + (want_d ? 1 : 0) + (want_s ? C : 0));
+        CK(ctx->planes.reserve(8 * need));
+        double* base = ctx->planes.as<double>();
+        double* d_sil = base;
+        double* d_color = want_c ? d_sil + px : nullptr;
+        double* d_depth = want_d ? (want_c ? d_color + 3 * px : d_sil + px) : nullptr;
+        double* d_sem = want_s ? base + px * (1 + (want_c ? 3 : 0) + (want_d ? 1 : 0)) : nullptr;
+        uint32_t ch = (want_c ? SGM_COLOR : 0u) | (want_d ? SGM_DEPTH : 0u) |
+                      (want_s ? SGM_SEMANTICS : 0u) | (channels & SGM_RETAIN_CONTRIBUTORS);
+        do_render(ctx, map, camera, pose, ch, opt, d_color, d_depth, d_sil, d_sem, n_projections);
+        cudaStream_t s = ctx->stream;
+        CK(cudaMemcpyAsync(silhouette, d_sil, 8 * px, cudaMemcpyDeviceToHost, s));
+        if (want_c) CK(cudaMemcpyAsync(color, d_color, 24 * px, cudaMemcpyDeviceToHost, s));
+        if (want_d) CK(cudaMemcpyAsync(depth, d_depth, 8 * px, cudaMemcpyDeviceToHost, s));
+        if (want_s) CK(cudaMemcpyAsync(sem, d_sem, 8 * px * C, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        // Unrequested-but-provided planes: the reference leaves them empty; zero them.
+        if ((channels & SGM_COLOR) == 0 && color) std::memset(color, 0, 24 * px);
+        if ((channels & SGM_DEPTH) == 0 && depth) std::memset(depth, 0, 8 * px);
+    });
+}
+
+int sgm_last_projections(sgm_ctx* ctx, sgm_projection* out, uint64_t capacity) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!ctx->last_valid) fail(SGM_ERR_INVALID, "no render state (call sgm_render first)");
+        const uint32_t V = ctx->last_V;
+        if (capacity < V) fail(SGM_ERR_INVALID, "capacity %llu < %u projections",
+                               static_cast<unsigned long long>(capacity), V);
+        if (V == 0) return;
+        CK(ctx->dbg.reserve(48ull * V + 96));
+        PoseParams* dpose = reinterpret_cast<PoseParams*>(ctx->dbg.as<char>() + 48ull * V);
+        CK(cudaMemcpyAsync(dpose, &ctx->last_pose, sizeof(PoseParams), cudaMemcpyHostToDevice, ctx->stream));
+        launch_debug_projections(ctx->last_map->dev, dpose, ctx->last_cam, ctx->last_opt,
+                                 ctx->vals.as<uint32_t>(), V, ctx->dbg.as<double>(), ctx->stream);
+        std::vector<double> h(6ull * V);
+        CK(cudaMemcpyAsync(h.data(), ctx->dbg.p, 48ull * V, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (uint32_t r = 0; r < V; ++r) {
+            out[r].mx = h[6 * r];
+            out[r].my = h[6 * r + 1];
+            out[r].rad_px = h[6 * r + 2];
+            out[r].z = h[6 * r + 3];
+            out[r].alpha = h[6 * r + 4];
+            out[r].index = static_cast<uint32_t>(h[6 * r + 5]);
+            out[r].reserved = 0;
+        }
+    });
+}
+
+int sgm_last_bins(sgm_ctx* ctx, uint32_t* tile_offsets, uint32_t* ids, float* probe3,
+                  uint64_t capacity, uint64_t* n_pairs) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!ctx->last_valid) fail(SGM_ERR_INVALID, "no render state (call sgm_render first)");
+        const uint64_t P = ctx->last_P;
+        if (n_pairs) *n_pairs = P;
+        const int tiles = ctx->last_bin_tiles;
+        if (tile_offsets) {
+            std::vector<uint2> r(tiles);
+            CK(cudaMemcpy(r.data(), ctx->ranges.p, sizeof(uint2) * tiles, cudaMemcpyDeviceToHost));
+            uint64_t acc = 0;
+            for (int t = 0; t < tiles; ++t) {
+                tile_offsets[t] = static_cast<uint32_t>(acc);
+                acc += r[t].y - r[t].x;
+            }
+            tile_offsets[tiles] = static_cast<uint32_t>(acc);
+        }
+        if ((ids || probe3) && P) {
+            if (capacity < P) fail(SGM_ERR_INVALID, "capacity < %llu pairs", static_cast<unsigned long long>(P));
+            CK(ctx->dbg.reserve(16 * P));
+            uint32_t* d_ids = ctx->dbg.as<uint32_t>();
+            float* d_probe = reinterpret_cast<float*>(ctx->dbg.as<char>() + 4 * P);
+            launch_bins_to_ids(ctx->tvals.as<uint32_t>(), P, ctx->packed.as<PackedSplat>(), d_ids,
+                               d_probe, ctx->stream);
+            if (ids) CK(cudaMemcpyAsync(ids, d_ids, 4 * P, cudaMemcpyDeviceToHost, ctx->stream));
+            if (probe3) CK(cudaMemcpyAsync(probe3, d_probe, 12 * P, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+        }
+    });
+}
+
+int sgm_last_contributors(sgm_ctx* ctx, uint32_t*, uint32_t*, uint64_t, uint64_t*) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        fail(SGM_ERR_UNSUPPORTED, "retain_contributors is not served by this build yet");
+    });
+}
+
+int sgm_render_entropy(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera,
+                       const sgm_pose* pose, const sgm_options* opt, double* entropy) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!map || !entropy) fail(SGM_ERR_INVALID, "null argument");
+        const CamParams cam = to_cam(camera);
+        const size_t px = static_cast<size_t>(cam.W) * cam.H;
+        const size_t C = static_cast<size_t>(map->dev.C);
+        std::vector<double> sil(px), sem(px * C);
+        uint64_t nproj = 0;
+        int rc = sgm_render(ctx, map, camera, pose, SGM_SEMANTICS, opt, nullptr, nullptr, sil.data(),
+                            sem.data(), &nproj);
+        if (rc != SGM_OK) fail(rc, "%s", ctx->err.c_str());
+        for (size_t i = 0; i < px; ++i) entropy[i] = sgm_clipped_entropy(&sem[i * C], C);
+    });
+}
+
+int sgm_score_views(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, uint64_t n,
+                    const sgm_pose* poses, const sgm_options* opt, double* n_missing,
+                    double* entropy_sum) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!map) fail(SGM_ERR_INVALID, "map is null");
+        if (n == 0) return;
+        if (!poses || !n_missing || !entropy_sum) fail(SGM_ERR_INVALID, "null argument");
+        const CamParams cam = to_cam(camera);
+        const OptParams o = to_opt(opt, cam);
+        std::vector<PoseParams> pp(n);
+        for (uint64_t i = 0; i < n; ++i) pp[i] = to_pose(poses[i]);
+        run_views(ctx, map, cam, o, n, pp.data(), Mode::Score, RenderTargets{}, n_missing,
+                  entropy_sum);
+    });
+}
+
+int sgm_score_candidates(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam, uint64_t n,
+                         const sgm_candidate* cands, const sgm_options* opt, double* n_missing,
+                         double* entropy_sum) {
+    if (n > 0 && !cands) {
+        if (ctx) ctx->err = "candidates are null";
+        return SGM_ERR_INVALID;
+    }
+    std::vector<sgm_pose> poses(n);
+    for (uint64_t i = 0; i < n; ++i) sgm_candidate_pose(cands[i].position, cands[i].direction, &poses[i]);
+    return sgm_score_views(ctx, map, cam, n, poses.data(), opt, n_missing, entropy_sum);
+}
+
+}  // extern "C"

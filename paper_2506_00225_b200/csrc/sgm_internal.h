@@ -1,0 +1,121 @@
+// Internal types shared by the kernels (sgm_kernels.cu) and the host pipeline
+// (sgm_capi.cu). Device layout of one map snapshot and one batch of views.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sgm {
+
+constexpr double kMaxFootprint = 0.999999;  // splat_render.hpp:41
+constexpr int kTile = 8;                    // raster tile edge (== reference tile_size)
+constexpr int kTilePx = kTile * kTile;      // pixels (threads) per raster CTA
+
+// Map snapshot in HBM. Geometry stays fp64 because the depth order and tile
+// rectangles must be bit-identical to the reference; radius and
+// opacity are activated on the host with the reference's libm.
+struct DevMap {
+    uint64_t n = 0;
+    int k = 0;            // sparse entries per Gaussian
+    int C = 0;            // semantic channels = num_classes + 1
+    const double* cx = nullptr;  // centres, SoA
+    const double* cy = nullptr;
+    const double* cz = nullptr;
+    const double* rad = nullptr;    // exp(log_radius)
+    const double* alpha = nullptr;  // sigmoid(opacity_logit)
+    const double* color4 = nullptr; // clamp(colour, 0, 1), [n][4] (4th unused)
+    const uint16_t* sem_idx = nullptr;  // [n][k]
+    const double* sem_prob = nullptr;   // [n][k]
+    int dup_idx = 0;  // some Gaussian lists a class twice: serialise its RMWs
+};
+
+struct CamParams {
+    int W, H;
+    double fx, fy, cx, cy;
+};
+
+// Camera-from-world rotation, row-major (Rcw[3i+k] = R(k,i)), and centre.
+struct PoseParams {
+    double Rcw[9];
+    double t[3];
+};
+
+struct OptParams {
+    int early_exit;
+    double eps;
+    double z_near;
+    double trunc;   // truncation_sigmas
+    double cut_sq;  // trunc * trunc (splat_render.cpp:180)
+    int ts;         // reference tile_size (binning)
+    int tiles_x, tiles_y;
+};
+
+// One culled-in projection in depth-rank order: the reference's PackedSplat
+// (splat_render.cpp:158-166) plus its float Probe (:184-187). 64 bytes.
+struct __align__(16) PackedSplat {
+    double mx, my;
+    double inv_two_r2;
+    double cutoff_d2;
+    double alpha;
+    double z;
+    float pmx, pmy, pcut;
+    uint32_t map_index;
+};
+static_assert(sizeof(PackedSplat) == 64, "PackedSplat must stay 64 B");
+
+// Per view of a raster batch.
+struct ViewDesc {
+    const uint2* ranges;        // [tiles] (begin, end) into list
+    const uint32_t* list;       // depth ranks grouped by tile, rank order inside a tile
+    const PackedSplat* packed;  // [V] by rank
+    double* ent_partial;        // [tiles] per-tile entropy sum (score mode)
+    uint32_t* miss_partial;     // [tiles] per-tile exact-zero silhouette count
+    // render mode planes (device, reference layout); null when not requested
+    double* color;
+    double* depth;
+    double* sil;
+    double* sem;
+    unsigned long long* contributors;  // K counter
+};
+
+struct RasterParams {
+    DevMap map;
+    CamParams cam;
+    OptParams opt;
+    const ViewDesc* views;
+    int tiles_per_view;  // raster tiles (8x8) per view
+    int raster_tiles_x;
+    uint32_t channels;   // SGM_COLOR | SGM_DEPTH | SGM_SEMANTICS
+    double h_empty;      // clipped entropy of an all-zero pixel (reference order)
+};
+
+// ---- launchers (sgm_kernels.cu) ----
+void launch_preprocess(const DevMap& m, const PoseParams* d_poses, const CamParams& cam,
+                       const OptParams& o, int n_views, double* keys, uint32_t* vals,
+                       size_t stride, uint32_t* vcount, unsigned long long* pcount,
+                       cudaStream_t s);
+void launch_tiefix(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
+                   const OptParams& o, const double* z, uint32_t* idx, uint32_t V,
+                   cudaStream_t s);
+void launch_pack(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
+                 const OptParams& o, const uint32_t* idx, uint32_t V, PackedSplat* packed,
+                 unsigned long long* counts, cudaStream_t s);
+void launch_emit_pairs(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
+                       const OptParams& o, const PackedSplat* packed,
+                       const unsigned long long* offsets, uint32_t V, uint32_t* tile_keys,
+                       uint32_t* tile_vals, cudaStream_t s);
+void launch_ranges(const uint32_t* sorted_tiles, uint64_t P, uint2* ranges, cudaStream_t s);
+void launch_raster_score(const RasterParams& p, int n_views, cudaStream_t s);
+void launch_raster_render(const RasterParams& p, int n_views, cudaStream_t s);
+void launch_reduce_scores(const ViewDesc* views, int n_views, int tiles, double* out_missing,
+                          double* out_entropy, cudaStream_t s);
+void launch_debug_projections(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
+                              const OptParams& o, const uint32_t* idx, uint32_t V,
+                              double* out6, cudaStream_t s);
+void launch_bins_to_ids(const uint32_t* list, uint64_t P, const PackedSplat* packed,
+                        uint32_t* ids, float* probe3, cudaStream_t s);
+
+size_t raster_smem_bytes(int C, int k, bool render);
+int raster_batch_entries();
+
+}  // namespace sgm

@@ -1,0 +1,97 @@
+"""Candidate views sharded across ranks (one process per GPU, torch.distributed).
+
+Views are independent (explorer.cpp:188-204), so the data path has
+no collective. The only exchanges are the ones the planning step really has:
+  C1 broadcast_map   - the map snapshot from rank 0, once per map version
+  C3 gather_scores   - every rank's (n_missing, entropy_sum) records, so every
+                       rank can run the reference-identical combine_scores and
+                       agree on the argmax.
+Per-view results are bit-identical for any world size (each view's reduction
+is deterministic and local to its GPU).
+"""
+from __future__ import annotations
+
+from typing import Optional, Tuple
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .splatmap import GaussianMap
+
+
+def shard_range(n: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous block of view indices owned by `rank` (sizes differ by <= 1)."""
+    base, rem = divmod(n, world)
+    start = rank * base + min(rank, rem)
+    return start, start + base + (1 if rank < rem else 0)
+
+
+def _device() -> torch.device:
+    if dist.get_backend() == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def broadcast_map(gmap: Optional[GaussianMap], src: int = 0) -> GaussianMap:
+    """C1: every rank receives rank `src`'s map (fp64 SoA + u16 ids), bit-identical."""
+    dev = _device()
+    rank = dist.get_rank()
+    if rank == src:
+        head = torch.tensor([gmap.size(), gmap.k(), gmap.num_classes()], dtype=torch.int64)
+    else:
+        head = torch.zeros(3, dtype=torch.int64)
+    head = head.to(dev)
+    dist.broadcast(head, src)
+    n, k, m = (int(v) for v in head.cpu())
+    if rank == src:
+        f64 = np.concatenate([gmap.centers.reshape(-1), gmap.log_radii, gmap.opacity_logits,
+                              gmap.colors.reshape(-1), gmap.sem_probs.reshape(-1)])
+        buf = torch.from_numpy(np.ascontiguousarray(f64)).to(dev)
+        ids = torch.from_numpy(gmap.sem_indices.astype(np.int32).reshape(-1)).to(dev)
+    else:
+        buf = torch.empty(n * (8 + k), dtype=torch.float64, device=dev)
+        ids = torch.empty(n * k, dtype=torch.int32, device=dev)
+    dist.broadcast(buf, src)
+    dist.broadcast(ids, src)
+    if rank == src:
+        return gmap
+    a = buf.cpu().numpy()
+    o = 0
+
+    def take(cnt):
+        nonlocal o
+        out = a[o:o + cnt]
+        o += cnt
+        return out
+
+    centers = take(3 * n).reshape(n, 3)
+    log_r = take(n)
+    logits = take(n)
+    colors = take(3 * n).reshape(n, 3)
+    probs = take(k * n).reshape(n, k)
+    idx = ids.cpu().numpy().astype(np.uint16).reshape(n, k)
+    return GaussianMap.from_arrays(k, m, centers, log_r, logits, colors, idx, probs)
+
+
+def gather_scores(n_total: int, n_missing: np.ndarray, entropy_sum: np.ndarray
+                  ) -> Tuple[np.ndarray, np.ndarray]:
+    """C3: all-gather every rank's contiguous shard into full (n_missing, entropy_sum)."""
+    dev = _device()
+    world = dist.get_world_size()
+    per = max(shard_range(n_total, r, world)[1] - shard_range(n_total, r, world)[0]
+              for r in range(world))
+    local = torch.zeros(2, per, dtype=torch.float64)
+    local[0, :len(n_missing)] = torch.from_numpy(np.asarray(n_missing, dtype=np.float64))
+    local[1, :len(entropy_sum)] = torch.from_numpy(np.asarray(entropy_sum, dtype=np.float64))
+    local = local.to(dev)
+    parts = [torch.empty_like(local) for _ in range(world)]
+    dist.all_gather(parts, local)
+    nm = np.zeros(n_total)
+    es = np.zeros(n_total)
+    for r, p in enumerate(parts):
+        s, e = shard_range(n_total, r, world)
+        pc = p.cpu().numpy()
+        nm[s:e] = pc[0, :e - s]
+        es[s:e] = pc[1, :e - s]
+    return nm, es

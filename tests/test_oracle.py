@@ -1,0 +1,169 @@
+"""Pins the C restatement (oracle/sgm_oracle.c) to the reference (CPU).
+
+1. The reference's own hot-path test executables pass against the shimmed build.
+2. Restatement == reference code bit-for-bit (projections, planes, scores, combine).
+3. Restatement == the committed golden vectors (reference outputs) and the
+   reference tests' known-answer values.
+"""
+import math
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import golden_scene, random_map
+
+from paper_2506_00225_b200.splatmap import CameraModel, Pose, RenderOptions, look_at
+
+
+def test_reference_hot_path_tests_pass(ref):
+    import oracle
+    for t in ("test_splat_render", "test_explorer", "test_gaussian_map", "test_losses"):
+        exe = oracle.HERE / "_ref" / t
+        if not exe.exists():
+            pytest.skip(f"{exe} not built")
+        r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout + r.stderr
+        assert "0 failed" in r.stdout
+
+
+SCENES = ["saturated", "two_half", "sparse_scatter", "kM_11", "kM_22", "kM_33", "mass_5",
+          "mass_6", "mass_7", "mass_8", "perm_19", "tiled_91", "early_55", "noearly_55",
+          "score_8", "multi_2024"]
+
+
+@pytest.mark.parametrize("name", SCENES)
+def test_oracle_matches_golden_bitexact(orc, golden, name):
+    gm, cam, pose, opts, ch, outs = golden_scene(golden, name)
+    proj = orc.project(gm, cam, pose, opts)
+    gp = outs["projections"]
+    assert len(proj) == len(gp)
+    for f in ("mx", "my", "rad_px", "z", "alpha", "index"):
+        np.testing.assert_array_equal(proj[f], gp[f])
+    out = orc.render(gm, cam, pose, ch, opts)
+    for key in ("silhouette", "color", "depth", "sem"):
+        if key in outs:
+            np.testing.assert_array_equal(out[key], outs[key], err_msg=key)
+    np.testing.assert_array_equal(orc.render_entropy(gm, cam, pose, opts), outs["entropy"])
+
+
+@pytest.mark.parametrize("name", ["score_8", "multi_2024"])
+def test_oracle_scores_match_golden(orc, golden, name):
+    gm, cam, pose, opts, ch, outs = golden_scene(golden, name)
+    poses = [Pose(*orc.candidate_pose(p, d)) for p, d in zip(outs["cand_pos"], outs["cand_dir"])]
+    nm, es, _ = orc.score_views(gm, cam, poses, opts)
+    np.testing.assert_array_equal(nm, outs["n_missing"])
+    np.testing.assert_array_equal(es, outs["entropy_sum"])
+
+
+def test_oracle_combine_matches_golden(orc, golden):
+    g = golden
+    any_, geo, sem, tot = orc.combine_scores(g["multi_2024/n_missing"], g["multi_2024/entropy_sum"],
+                                             g["multi_2024/cand_pos"], g["multi_2024/current"])
+    assert any_
+    np.testing.assert_array_equal(geo, g["multi_2024/i_geo"])
+    np.testing.assert_array_equal(sem, g["multi_2024/i_sem"])
+    np.testing.assert_array_equal(tot, g["multi_2024/i_total"])
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_oracle_vs_reference_random_scenes(orc, ref, seed):
+    cam = CameraModel(72, 52, 0, 0, 61.0, 59.5, 36.3, 25.1)
+    pose = look_at([0.2, -0.1, -0.4], [0.0, 0.2, 2.5])
+    gm = random_map(seed, 300, cam, pose, k=5, num_classes=11, dup=(seed == 3))
+    for opts in (RenderOptions(), RenderOptions(early_exit=False),
+                 RenderOptions(truncation_sigmas=2.0, tile_size=16)):
+        r = ref.render(gm, cam, pose, 7, opts)
+        o = orc.render(gm, cam, pose, 7, opts)
+        for key in ("silhouette", "color", "depth", "sem"):
+            np.testing.assert_array_equal(o[key], r[key], err_msg=key)
+        p = orc.project(gm, cam, pose, opts)
+        for f in ("mx", "my", "rad_px", "z", "alpha", "index"):
+            np.testing.assert_array_equal(p[f], r["projections"][f])
+
+
+def test_oracle_scores_vs_reference_threads(orc, ref):
+    cam = CameraModel(40, 30, 0, 0, 35.0, 35.0, 19.5, 14.5)
+    gm = random_map(9, 250, cam, k=3, num_classes=6)
+    rng = np.random.default_rng(3)
+    pos = rng.normal(0, 0.1, (9, 3))
+    dirs = np.tile([0.0, 0.0, 1.0], (9, 1)) + rng.normal(0, 0.3, (9, 3))
+    nm_r, es_r = ref.refresh_scores(gm, cam, pos, dirs, threads=3)
+    nm_1, es_1 = ref.refresh_scores(gm, cam, pos, dirs, threads=1)
+    np.testing.assert_array_equal(nm_r, nm_1)
+    np.testing.assert_array_equal(es_r, es_1)
+    poses = [Pose(*orc.candidate_pose(p, d)) for p, d in zip(pos, dirs)]
+    nm, es, st = orc.score_views(gm, cam, poses, threads=4)
+    np.testing.assert_array_equal(nm, nm_r)
+    np.testing.assert_array_equal(es, es_r)
+    assert st["contributors"] > 0
+
+
+def test_candidate_pose_and_look_at_bitexact(orc, ref):
+    rng = np.random.default_rng(11)
+    for _ in range(50):
+        p = rng.normal(0, 3, 3)
+        d = rng.normal(0, 1, 3)
+        Ro, to = orc.candidate_pose(p, d)
+        Rr, tr = ref.candidate_pose(p, d)
+        np.testing.assert_array_equal(Ro, Rr)
+        np.testing.assert_array_equal(to, tr)
+        tg = rng.normal(0, 3, 3)
+        np.testing.assert_array_equal(orc.look_at(p, tg)[0], ref.look_at(p, tg)[0])
+    # degenerate: looking straight up falls back to the x axis (geometry.hpp:49)
+    np.testing.assert_array_equal(orc.candidate_pose([0, 0, 0], [0, 1, 0])[0],
+                                  ref.candidate_pose([0, 0, 0], [0, 1, 0])[0])
+
+
+def test_combine_scores_vs_reference(orc, ref):
+    rng = np.random.default_rng(5)
+    for n in (1, 2, 3, 17):
+        nm = np.floor(rng.uniform(0, 500, n))
+        nm[0] = 0.0
+        es = rng.uniform(100, 400, n)
+        pos = rng.normal(0, 2, (n, 3))
+        cur = rng.normal(0, 1, 3)
+        a = orc.combine_scores(nm, es, pos, cur)
+        b = ref.combine_scores(nm, es, pos, cur)
+        assert a[0] == b[0]
+        for x, y in zip(a[1:], b[1:]):
+            np.testing.assert_array_equal(x, y)
+
+
+# ---- known-answer values of the reference tests (test_splat_render.cpp) ----
+
+def test_kat_clipped_entropy(orc):
+    p = np.zeros(102)
+    p[17] = 1.0
+    assert orc.clipped_entropy(p) == pytest.approx(0.7298996, rel=1e-5)  # :246
+    assert orc.clipped_entropy(np.full(102, 1 / 102)) == pytest.approx(math.log(102), rel=1e-12)
+    assert orc.clipped_entropy([0.5, 0.5]) == pytest.approx(math.log(2.0), rel=1e-15)  # :257
+
+
+def test_kat_saturated_and_two_half(orc, golden):
+    gm, cam, pose, opts, ch, _ = golden_scene(golden, "saturated")
+    out = orc.render(gm, cam, pose, ch, opts)
+    pix = 6 * cam.width + 8
+    assert out["silhouette"][pix] == pytest.approx(1.0, rel=1e-5)  # :34
+    assert out["depth"][pix] == pytest.approx(1.5, rel=1e-5)
+    np.testing.assert_allclose(out["color"][3 * pix:3 * pix + 3], [0.2, 0.6, 0.9], rtol=1e-5)
+    gm, cam, pose, opts, ch, _ = golden_scene(golden, "two_half")
+    out = orc.render(gm, cam, pose, ch, opts)
+    assert out["silhouette"][pix] == pytest.approx(0.75, rel=1e-9)  # :56
+    assert out["depth"][pix] == pytest.approx(0.5 * 1.0 + 0.25 * 2.0, rel=1e-9)
+
+
+def test_kat_empty_map_entropy(orc):
+    from paper_2506_00225_b200.splatmap import GaussianMap
+    gm = GaussianMap(4, 9)
+    cam = CameraModel.from_fov(8, 6, 60, 70)
+    h = orc.render_entropy(gm, cam, Pose())
+    np.testing.assert_allclose(h, math.log(10.0), rtol=1e-12)  # :260-265
+
+
+def test_kat_facing_away_scores(orc, golden):
+    nm = golden["score_8/n_missing"]
+    es = golden["score_8/entropy_sum"]
+    assert nm[1] == 32 * 24  # test_explorer.cpp:375
+    assert es[1] == pytest.approx(32 * 24 * math.log(6.0), rel=1e-9)
+    assert nm[0] < 32 * 24 and es[0] < es[1]
