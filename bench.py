@@ -1,0 +1,368 @@
+"""Candidate-view scoring benchmark (BASELINE.json metric: candidate views scored/sec).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1]
+
+A step = scoring one batch of candidate views of the config-1 scene (500k
+Gaussians, 1200x680, k=16 of 101 classes): per view the exact-zero silhouette
+count and the summed clipped entropy (refresh_candidate_scores, explorer.cpp:186-205),
+64 views per GPU per step (weak scaling over ranks), followed by the all-gather
+of per-view scores and combine_scores on every rank.
+
+value : views/s with the map resident in HBM (device timeline, CUDA events on the
+        library's stream, max over ranks, L2 flushed between steps).
+e2e   : the same through the public API with host inputs: every step re-uploads the
+        map from host memory (map version bump) and returns per-view scores to host.
+--impl reference: the reference's own CPU code (oracle/_ref, compiled unmodified from
+        the reference sources) on all usable host cores, same config and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+VIEWS_PER_GPU = 64
+METRIC = "candidate views scored/sec"
+UNIT = "views/s"
+
+
+def _mem_available_gb() -> float:
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable"):
+                return int(line.split()[1]) / 1e6
+    except OSError:
+        pass
+    return 16.0
+
+
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self._t:
+            self._t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_run(cfg: int, views: int, threads: int, steps: int = 1, warmup: int = 0):
+    """The reference's refresh_candidate_scores (oracle/_ref) on host cores."""
+    import oracle
+    from paper_2506_00225_b200 import scenes
+    ref = oracle.RefLib()
+    gm = scenes.make_map(cfg)
+    cam = scenes.CONFIGS[cfg].camera()
+    cands = scenes.make_candidates(cfg, views)
+    h = ref.map_create(gm)
+    pos = np.array([c.position for c in cands])
+    dirs = np.array([c.direction for c in cands])
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        ref.refresh_scores(gm, cam, pos, dirs, threads=threads, handle=h)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    ref.map_destroy(h)
+    return views / float(np.mean(times)), float(np.mean(times))
+
+
+def run_reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # rank 0 alone runs the CPU reference
+    import oracle
+    cores = oracle.cpu_count()
+    # one 0.7 GB RenderOutput per concurrent view in the reference: bound by RAM
+    threads = max(1, min(cores, int(_mem_available_gb() // 1.5), 64))
+    views = threads  # one view per thread per step: a bounded sample of the workload
+    value, sec = cpu_reference_run(args.config, views, threads, args.steps, args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args.config),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{views} cfg{args.config} candidate views per step "
+                                   f"(one per thread), {_cpu_model()}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg: int) -> dict:
+    from paper_2506_00225_b200 import scenes
+    sc = scenes.CONFIGS[cfg]
+    return {"workload": f"cfg{cfg} {sc.name}: {sc.n} Gaussians in {sc.box[0]:g}x{sc.box[1]:g}x"
+                        f"{sc.box[2]:g} m, {sc.width}x{sc.height} px, k={sc.k} of "
+                        f"{sc.num_classes} classes ({sc.num_classes + 1} channels), "
+                        f"{VIEWS_PER_GPU} candidate views per GPU per step",
+            "seed": sc.seed, "views_per_gpu_per_step": VIEWS_PER_GPU,
+            "l2": "flushed (256 MiB write) between timed steps",
+            "isotropic": "log_radius = mean of 3 per-axis log-scale draws (SURVEY App. A)",
+            "gain": "reference Eq.6-8 (n_missing, clipped-entropy sum, combine_scores)"}
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2506_00225_b200 import dist as sd
+    from paper_2506_00225_b200 import scenes
+    from paper_2506_00225_b200.splatmap import (Context, combine_scores,
+                                                refresh_candidate_scores, score_poses)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    cfg = args.config
+    sc = scenes.CONFIGS[cfg]
+    cam = sc.camera()
+    gm = scenes.make_map(cfg) if rank == 0 else None
+    if world > 1:
+        gm = sd.broadcast_map(gm)  # C1 over NCCL
+    n_total = VIEWS_PER_GPU * world
+    cands = scenes.make_candidates(cfg, n_total)
+    s, e = sd.shard_range(n_total, rank, world)
+    mine = cands[s:e]
+    poses = [c.camera_pose() for c in mine]
+
+    ctx = Context(local)
+    ctx.upload(gm)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    def step_resident():
+        nm, es = score_poses(gm, cam, poses, ctx=ctx)
+        if world > 1:
+            nm, es = sd.gather_scores(n_total, nm, es)
+        return nm, es
+
+    for _ in range(args.warmup):
+        step_resident()
+    ctx.reset_stats()
+    ctx.set_profiling(True)
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    step_ms = []
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)  # evict L2 between timed steps (outside the events)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        nm_all, es_all = step_resident()
+        ev1.record(stream)
+        ev1.synchronize()
+        step_ms.append(ev0.elapsed_time(ev1))
+    barrier()
+    clk = clocks.stop()
+    st = ctx.stats()
+    ctx.set_profiling(False)
+    total_ms = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = n_total * args.steps / (total_ms / 1e3)
+
+    # all ranks agree on the argmax (combine_scores on the gathered records)
+    for c, a, b in zip(cands, nm_all, es_all):
+        c.n_missing, c.entropy_sum = float(a), float(b)
+    combine_scores(cands, np.array([4.0, 1.5, 3.0]))
+    best = max(range(n_total), key=lambda i: (cands[i].i_total, -i))
+
+    # ---- e2e through the public API (host inputs, map re-upload every step) ----
+    h2d = int(gm.centers.nbytes + gm.log_radii.nbytes + gm.opacity_logits.nbytes +
+              gm.colors.nbytes + gm.sem_indices.nbytes + gm.sem_probs.nbytes) + 96 * len(mine)
+    d2h = 16 * len(mine)
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        gm.touch()
+        fresh = [type(c)(position=c.position, direction=c.direction, id=c.id) for c in mine]
+        barrier()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        refresh_candidate_scores(fresh, gm, cam, ctx=ctx)
+        if world > 1:
+            sd.gather_scores(n_total, np.array([c.n_missing for c in fresh]),
+                             np.array([c.entropy_sum for c in fresh]))
+        ev1.record(stream)
+        ev1.synchronize()
+        if i >= args.warmup:
+            e2e_ms.append(ev0.elapsed_time(ev1))
+    e2e_total = float(np.sum(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = n_total * args.steps / (e2e_total / 1e3)
+
+    # ---- roofline of the dominant kernel (raster-score) ----
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except (OSError, ValueError):
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    raster_launches = max(1, st["raster_launches"])
+    raster_ms = st["raster_ms"] / raster_launches
+    views_timed = st["views"]
+    per_launch_views = views_timed / raster_launches
+    vis_per_view = st["visible"] / max(1, views_timed)
+    N = gm.size()
+    k = gm.k()
+    alg_bytes = per_launch_views * (20.0 * N + 6.0 * k * vis_per_view + 16.0)
+    achieved = alg_bytes / (raster_ms * 1e-3) / 1e9
+    traffic = None
+    prof_json = ROOT / "profiles" / "raster_traffic.json"
+    if prof_json.exists():
+        try:
+            traffic = json.loads(prof_json.read_text()).get("dram_bytes_per_launch")
+        except ValueError:
+            traffic = None
+    clock_ghz = (clk.get("sm_mhz") or 1965.0) / 1e3
+    smem_peak = 148 * 128 * clock_ghz  # GB/s, LDS/STS crossbar
+    K_per_launch = st["contributors"] / raster_launches
+    smem_bytes = K_per_launch * 2 * k * 8  # fp64 read+write per sparse scatter
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": traffic,
+                "kernel": "k_raster<score> (K5)", "raster_ms_per_launch": raster_ms,
+                "views_per_launch": per_launch_views,
+                "algorithmic_bytes_per_view": "20*N + 6*k*V + 16 (SURVEY 8d)",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}
+    roofline_aux = {"smem_rmw_GBps": smem_bytes / (raster_ms * 1e-3) / 1e9,
+                    "smem_peak_GBps": smem_peak,
+                    "smem_frac": (smem_bytes / (raster_ms * 1e-3) / 1e9) / smem_peak,
+                    "contributors_per_view": st["contributors"] / max(1, views_timed),
+                    "visible_per_view": vis_per_view,
+                    "pairs_per_view": st["pairs"] / max(1, views_timed),
+                    "binning_ms_per_batch": st["binning_ms"] / raster_launches}
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle
+            cores = oracle.cpu_count()
+            threads = max(1, min(cores, int(_mem_available_gb() // 1.5), 64))
+            v, sec = cpu_reference_run(cfg, threads, threads, 1, 0)
+            cpu_baseline = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                            "sample": f"{threads} cfg{cfg} candidate views, one per thread, "
+                                      f"{sec:.1f} s, {_cpu_model()}"}
+        except Exception as exc:  # reported, not fatal
+            cpu_baseline = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                            "sample": f"failed: {exc!r}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE cfg%d)" % cfg,
+            "config": workload_config(cfg),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": int(st["kernel_launches"]),
+            "roofline": roofline, "roofline_aux": roofline_aux,
+            "cpu_baseline": cpu_baseline, "clocks": clk,
+            "argmax_view": int(best), "views_total_per_step": n_total,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -101,6 +101,7 @@ struct SgmError {
 
 struct sgm_map {
     DevMap dev;
+    GroupParams groups{1, 1};
     int num_classes = 0;
     DevBuf geo;    // cx, cy, cz, rad, alpha (5 x n doubles)
     DevBuf color;  // [n][4]
@@ -202,7 +203,7 @@ void bin_view(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const OptP
     CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, dk, dv, V, 0, 64, s));
     ctx->stats.kernel_launches += 1;  // counted as one library sort call
     launch_tiefix(map->dev, d_pose, cam, o, dk.Current(), dv.Current(), V, s);
-    launch_pack(map->dev, d_pose, cam, o, dv.Current(), V, packed,
+    launch_pack(map->dev, d_pose, cam, o, GroupParams{1, map->dev.C}, dv.Current(), V, packed,
                 ctx->counts.as<unsigned long long>(), s);
     ctx->stats.kernel_launches += (V >= 2 ? 1 : 0) + 1;
     // keep the sorted indices for sgm_last_projections
@@ -218,7 +219,7 @@ void bin_view(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const OptP
     ctx->stats.kernel_launches += 1;
     if (P == 0) return;
     uint32_t* tk = ctx->tkeys.as<uint32_t>();
-    launch_emit_pairs(map->dev, d_pose, cam, o, packed, off, V, tk, list, s);
+    launch_emit_pairs(map->dev, d_pose, cam, o, vals, off, V, tk, list, s);
     ctx->stats.kernel_launches += 1;
     cub::DoubleBuffer<uint32_t> pk(tk, ctx->tkeys_alt.as<uint32_t>());
     cub::DoubleBuffer<uint32_t> pv(list, ctx->tvals_alt.as<uint32_t>());
@@ -329,6 +330,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 bin_view(ctx, map, cam, o, ctx->poses.as<PoseParams>() + v, keys, vals, V[v], P[v],
                          packed, list, ranges, bin_tiles);
                 ViewDesc d{};
+                d.order = vals;
                 d.ranges = ranges;
                 d.list = list;
                 d.packed = packed;
@@ -355,6 +357,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
             rp.tiles_per_view = rtiles;
             rp.raster_tiles_x = rtx;
             rp.channels = rt.channels;
+            rp.groups = map->groups;
             if (mode == Mode::Score)
                 launch_raster_score(rp, nsub, s);
             else
@@ -572,21 +575,34 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, con
                 if (seen[c] == static_cast<uint32_t>(i)) dup = 1;
                 seen[c] = static_cast<uint32_t>(i);
             }
+        // rows sorted by class id (stable), padded to kpad with (0xffff, 0.0)
+        const int kpad = (k + 7) / 8 * 8;
+        std::vector<uint16_t> sidx(ns * kpad, 0xffff);
+        std::vector<double> sprob(ns * kpad, 0.0);
+        std::vector<int> perm(k);
+        for (uint64_t i = 0; i < n; ++i) {
+            const uint16_t* ri = sem_indices + i * k;
+            for (int j = 0; j < k; ++j) perm[j] = j;
+            std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return ri[a] < ri[b]; });
+            for (int j = 0; j < k; ++j) {
+                sidx[i * kpad + j] = ri[perm[j]];
+                sprob[i * kpad + j] = sem_probs[i * k + perm[j]];
+            }
+        }
         cudaStream_t s = ctx->stream;
         CK(m->geo.reserve(8 * geo.size()));
         CK(m->color.reserve(8 * col.size()));
-        CK(m->idx.reserve(2 * ns * k));
-        CK(m->prob.reserve(8 * ns * k));
+        CK(m->idx.reserve(2 * sidx.size()));
+        CK(m->prob.reserve(8 * sprob.size()));
         CK(cudaMemcpyAsync(m->geo.p, geo.data(), 8 * geo.size(), cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(m->color.p, col.data(), 8 * col.size(), cudaMemcpyHostToDevice, s));
-        if (n) {
-            CK(cudaMemcpyAsync(m->idx.p, sem_indices, 2 * n * k, cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(m->prob.p, sem_probs, 8 * n * k, cudaMemcpyHostToDevice, s));
-        }
+        CK(cudaMemcpyAsync(m->idx.p, sidx.data(), 2 * sidx.size(), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(m->prob.p, sprob.data(), 8 * sprob.size(), cudaMemcpyHostToDevice, s));
         CK(cudaStreamSynchronize(s));
         DevMap& d = m->dev;
         d.n = n;
         d.k = k;
+        d.kpad = kpad;
         d.C = C;
         const double* g = m->geo.as<double>();
         d.cx = g;
@@ -598,6 +614,7 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, con
         d.sem_idx = m->idx.as<uint16_t>();
         d.sem_prob = m->prob.as<double>();
         d.dup_idx = dup;
+        m->groups = choose_groups(C, k);
         *out = m;
         m = nullptr;
     });

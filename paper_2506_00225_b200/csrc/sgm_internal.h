@@ -17,6 +17,7 @@ constexpr int kTilePx = kTile * kTile;      // pixels (threads) per raster CTA
 struct DevMap {
     uint64_t n = 0;
     int k = 0;            // sparse entries per Gaussian
+    int kpad = 0;         // row stride of sem_idx / sem_prob (k rounded up to 8)
     int C = 0;            // semantic channels = num_classes + 1
     const double* cx = nullptr;  // centres, SoA
     const double* cy = nullptr;
@@ -24,8 +25,11 @@ struct DevMap {
     const double* rad = nullptr;    // exp(log_radius)
     const double* alpha = nullptr;  // sigmoid(opacity_logit)
     const double* color4 = nullptr; // clamp(colour, 0, 1), [n][4] (4th unused)
-    const uint16_t* sem_idx = nullptr;  // [n][k]
-    const double* sem_prob = nullptr;   // [n][k]
+    // Sparse rows sorted by class id at upload (per-class addition order is
+    // unchanged: a Gaussian lists a class once, or duplicates keep their order).
+    // Rows padded to kpad with (0xffff, 0.0) so every row is 16-byte aligned.
+    const uint16_t* sem_idx = nullptr;  // [n][kpad]
+    const double* sem_prob = nullptr;   // [n][kpad]
     int dup_idx = 0;  // some Gaussian lists a class twice: serialise its RMWs
 };
 
@@ -59,12 +63,20 @@ struct __align__(16) PackedSplat {
     double alpha;
     double z;
     float pmx, pmy, pcut;
-    uint32_t map_index;
+    uint32_t aux;  // channel-group boundaries (u8 x 4) of the sparse row
 };
 static_assert(sizeof(PackedSplat) == 64, "PackedSplat must stay 64 B");
 
+// Channel groups: the C semantic channels are split into P groups of Cg; each
+// group is accumulated by its own CTA of a (P,1,1) thread-block cluster.
+struct GroupParams {
+    int P;
+    int Cg;
+};
+
 // Per view of a raster batch.
 struct ViewDesc {
+    const uint32_t* order;      // [V] depth rank -> map index
     const uint2* ranges;        // [tiles] (begin, end) into list
     const uint32_t* list;       // depth ranks grouped by tile, rank order inside a tile
     const PackedSplat* packed;  // [V] by rank
@@ -86,7 +98,7 @@ struct RasterParams {
     int tiles_per_view;  // raster tiles (8x8) per view
     int raster_tiles_x;
     uint32_t channels;   // SGM_COLOR | SGM_DEPTH | SGM_SEMANTICS
-    double h_empty;      // clipped entropy of an all-zero pixel (reference order)
+    GroupParams groups;
 };
 
 // ---- launchers (sgm_kernels.cu) ----
@@ -98,10 +110,10 @@ void launch_tiefix(const DevMap& m, const PoseParams* d_pose, const CamParams& c
                    const OptParams& o, const double* z, uint32_t* idx, uint32_t V,
                    cudaStream_t s);
 void launch_pack(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
-                 const OptParams& o, const uint32_t* idx, uint32_t V, PackedSplat* packed,
-                 unsigned long long* counts, cudaStream_t s);
+                 const OptParams& o, const GroupParams& gp, const uint32_t* idx, uint32_t V,
+                 PackedSplat* packed, unsigned long long* counts, cudaStream_t s);
 void launch_emit_pairs(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
-                       const OptParams& o, const PackedSplat* packed,
+                       const OptParams& o, const uint32_t* order,
                        const unsigned long long* offsets, uint32_t V, uint32_t* tile_keys,
                        uint32_t* tile_vals, cudaStream_t s);
 void launch_ranges(const uint32_t* sorted_tiles, uint64_t P, uint2* ranges, cudaStream_t s);
@@ -115,7 +127,8 @@ void launch_debug_projections(const DevMap& m, const PoseParams* d_pose, const C
 void launch_bins_to_ids(const uint32_t* list, uint64_t P, const PackedSplat* packed,
                         uint32_t* ids, float* probe3, cudaStream_t s);
 
-size_t raster_smem_bytes(int C, int k, bool render);
-int raster_batch_entries();
+// sgm_raster.cu
+GroupParams choose_groups(int C, int k);
+size_t raster_smem_bytes(const DevMap& m, const GroupParams& gp, bool render);
 
 }  // namespace sgm

@@ -8,7 +8,7 @@
 //   K1 k_preprocess      project_splats transform/cull + tile count   splat_render.cpp:15-39, 205-209
 //   K2 (CUB radix sort on fp64 z) + k_tiefix (z, mx, my, alpha) order  splat_render.cpp:40-45
 //   K3 k_pack / k_emit / (CUB stable tile sort) / k_ranges             splat_render.cpp:189-213
-//   K4/K5 k_raster<render|score>   tile compositor + clipped entropy    splat_render.cpp:254-324, 360-369
+//   K4/K5 raster: see sgm_raster.cu
 //   k_reduce_scores     deterministic per-view n_missing / entropy_sum   explorer.cpp:195-203
 #include <cfloat>
 #include <climits>
@@ -19,8 +19,6 @@
 namespace sgm {
 
 namespace {
-
-constexpr int kBatch = 32;  // Gaussians staged in shared memory per raster step
 
 // static_cast<int>(double) as the reference binary executes it (x86-64
 // cvttsd2si): out-of-range and NaN give INT_MIN. CUDA's cvt saturates instead.
@@ -146,8 +144,8 @@ __global__ void k_tiefix(DevMap m, const PoseParams* __restrict__ pose, CamParam
 // ---------------------------------------------------------------- K3
 // PackedSplat + Probe per depth rank (splat_render.cpp:191-204) and tile counts.
 __global__ void k_pack(DevMap m, const PoseParams* __restrict__ pose, CamParams cam, OptParams o,
-                       const uint32_t* __restrict__ idx, uint32_t V, PackedSplat* packed,
-                       unsigned long long* counts) {
+                       GroupParams gp, const uint32_t* __restrict__ idx, uint32_t V,
+                       PackedSplat* packed, unsigned long long* counts) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= V) return;
     const uint32_t i = idx[r];
@@ -163,7 +161,19 @@ __global__ void k_pack(DevMap m, const PoseParams* __restrict__ pose, CamParams 
     ps.pmx = static_cast<float>(mx);  // :201
     ps.pmy = static_cast<float>(my);  // :202
     ps.pcut = static_cast<float>(ps.cutoff_d2 * (1.0 + 1e-5)) + 1e-6f;  // :203
-    ps.map_index = i;
+    // channel-group boundaries of this Gaussian's (channel-sorted) sparse row:
+    // byte g-1 = #entries with class < g * Cg, for g = 1..P-1
+    uint32_t aux = 0;
+    if (gp.P > 1) {
+        const uint16_t* row = m.sem_idx + static_cast<size_t>(i) * m.kpad;
+        for (int g = 1; g < gp.P; ++g) {
+            const int lim = g * gp.Cg;
+            uint32_t c = 0;
+            for (int j = 0; j < m.k; ++j) c += row[j] < lim ? 1u : 0u;
+            aux |= (c & 0xffu) << (8 * (g - 1));
+        }
+    }
+    ps.aux = aux;
     packed[r] = ps;
     counts[r] = rect_count(tile_rect(mx, my, rad, o));
 }
@@ -173,7 +183,7 @@ __global__ void k_pack(DevMap m, const PoseParams* __restrict__ pose, CamParams 
 // in PackedSplat (64 B); the rectangle is re-derived by re-projecting, which is
 // bit-identical to the count pass.
 __global__ void k_emit2(DevMap m, const PoseParams* __restrict__ pose, CamParams cam, OptParams o,
-                        const PackedSplat* __restrict__ packed,
+                        const uint32_t* __restrict__ order,
                         const unsigned long long* __restrict__ offsets, uint32_t V,
                         uint32_t* tile_keys, uint32_t* tile_vals) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -181,7 +191,7 @@ __global__ void k_emit2(DevMap m, const PoseParams* __restrict__ pose, CamParams
     unsigned long long at = offsets[r];
     if (at == offsets[r + 1]) return;
     double mx, my, rad, z;
-    project(m, packed[r].map_index, *pose, cam, o, mx, my, rad, z);
+    project(m, order[r], *pose, cam, o, mx, my, rad, z);
     const Rect rc = tile_rect(mx, my, rad, o);
     for (int ty = rc.ty0; ty <= rc.ty1; ++ty)
         for (int tx = rc.tx0; tx <= rc.tx1; ++tx) {
@@ -197,209 +207,6 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, uint64_t P, uint2* r
     const uint32_t t = keys[i];
     if (i == 0 || keys[i - 1] != t) ranges[t].x = static_cast<uint32_t>(i);
     if (i + 1 == P || keys[i + 1] != t) ranges[t].y = static_cast<uint32_t>(i + 1);
-}
-
-__device__ __forceinline__ double clamp_prob(double v) {
-    // std::clamp(v, 0.001, 1.0) (splat_render.cpp:362)
-    return v < 0.001 ? 0.001 : (1.0 < v ? 1.0 : v);
-}
-
-// ---------------------------------------------------------------- K4 / K5
-// One CTA = one 8x8 pixel block of one view; one thread = one pixel. The
-// per-pixel semantic accumulator lives in shared memory as [channel][pixel]
-// (pitch 64, or 65 when the epilogue transposes it to the reference's
-// channel-fastest layout), so the warp-uniform Gaussian's k scatters hit 32
-// consecutive doubles: conflict-free.
-template <bool kRender, bool kDup>
-__global__ void __launch_bounds__(kTilePx) k_raster(RasterParams p) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int C = p.map.C;
-    const int k = p.map.k;
-    constexpr int pitch = kRender ? kTilePx + 1 : kTilePx;
-    double* acc = reinterpret_cast<double*>(smem);
-    double* s_mx = acc + C * pitch;
-    double* s_my = s_mx + kBatch;
-    double* s_inv = s_my + kBatch;
-    double* s_cut = s_inv + kBatch;
-    double* s_alpha = s_cut + kBatch;
-    double* s_z = s_alpha + kBatch;
-    double* s_prob = s_z + kBatch;                 // kBatch * k
-    double* s_col = s_prob + kBatch * k;           // kBatch * 4 (render)
-    float* s_pmx = reinterpret_cast<float*>(s_col + (kRender ? kBatch * 4 : 0));
-    float* s_pmy = s_pmx + kBatch;
-    float* s_pcut = s_pmy + kBatch;
-    uint32_t* s_map = reinterpret_cast<uint32_t*>(s_pcut + kBatch);
-    uint16_t* s_idx = reinterpret_cast<uint16_t*>(s_map + kBatch);  // kBatch * k
-    __shared__ double red_d[kTilePx];
-    __shared__ unsigned long long red_u[kTilePx];
-
-    const ViewDesc vd = p.views[blockIdx.y];
-    const int tile = blockIdx.x;
-    const int bx = tile % p.raster_tiles_x, by = tile / p.raster_tiles_x;
-    const int t = threadIdx.x;
-    const int x = bx * kTile + (t & (kTile - 1));
-    const int y = by * kTile + (t / kTile);
-    const bool inside = x < p.cam.W && y < p.cam.H;
-    const int bin = ((by * kTile) / p.opt.ts) * p.opt.tiles_x + (bx * kTile) / p.opt.ts;
-    const uint2 rg = vd.ranges[bin];
-
-    for (int c = 0; c < C; ++c) acc[c * pitch + t] = 0.0;
-
-    const double px = x + 0.5, py = y + 0.5;  // :261, :263
-    const float pxf = static_cast<float>(px), pyf = static_cast<float>(py);  // :274
-    double T = 1.0;
-    double ac0 = 0.0, ac1 = 0.0, ac2 = 0.0, adep = 0.0;
-    bool done = !inside;
-    unsigned long long contrib = 0;
-
-    for (uint32_t base = rg.x; base < rg.y; base += kBatch) {
-        const int n = min(static_cast<uint32_t>(kBatch), rg.y - base);
-        __syncthreads();  // previous batch fully consumed
-        if (t < n) {
-            const uint32_t r = vd.list[base + t];
-            const PackedSplat ps = vd.packed[r];
-            s_mx[t] = ps.mx;
-            s_my[t] = ps.my;
-            s_inv[t] = ps.inv_two_r2;
-            s_cut[t] = ps.cutoff_d2;
-            s_alpha[t] = ps.alpha;
-            s_z[t] = ps.z;
-            s_pmx[t] = ps.pmx;
-            s_pmy[t] = ps.pmy;
-            s_pcut[t] = ps.pcut;
-            s_map[t] = ps.map_index;
-            if (kRender) {
-                const double4 cc = reinterpret_cast<const double4*>(p.map.color4)[ps.map_index];
-                s_col[4 * t] = cc.x;
-                s_col[4 * t + 1] = cc.y;
-                s_col[4 * t + 2] = cc.z;
-            }
-        }
-        __syncthreads();
-        for (int l = t; l < n * k; l += kTilePx) {
-            const int e = l / k;
-            const int j = l - e * k;
-            const size_t src = static_cast<size_t>(s_map[e]) * k + j;
-            s_idx[l] = p.map.sem_idx[src];
-            s_prob[l] = p.map.sem_prob[src];
-        }
-        __syncthreads();
-        if (!done) {
-            for (int e = 0; e < n; ++e) {
-                const float fdx = pxf - s_pmx[e];
-                const float fdy = pyf - s_pmy[e];
-                if (fdx * fdx + fdy * fdy > s_pcut[e]) continue;  // :276-278
-                const double dx = px - s_mx[e];
-                const double dy = py - s_my[e];
-                const double d2 = dx * dx + dy * dy;
-                if (d2 > s_cut[e]) continue;  // :283
-                double f = s_alpha[e] * exp(-d2 * s_inv[e]);  // :284
-                if (f > kMaxFootprint) f = kMaxFootprint;     // :285
-                const double w = f * T;
-                if (kRender) {
-                    ac0 += s_col[4 * e] * w;  // :289-291 (colour pre-clamped)
-                    ac1 += s_col[4 * e + 1] * w;
-                    ac2 += s_col[4 * e + 2] * w;
-                    adep += s_z[e] * w;  // :293
-                }
-                if (!kRender || (p.channels & 4u)) {
-                    const uint16_t* ei = s_idx + e * k;
-                    const double* ep = s_prob + e * k;
-                    if (kDup) {
-                        for (int j = 0; j < k; ++j) {  // sequential: repeated classes
-                            double* a = &acc[ei[j] * pitch + t];
-                            *a = *a + ep[j] * w;  // :307
-                        }
-                    } else {
-                        int j = 0;
-                        for (; j + 8 <= k; j += 8) {
-                            int ad[8];
-                            double pv[8], av[8];
-#pragma unroll
-                            for (int q = 0; q < 8; ++q) {
-                                ad[q] = ei[j + q] * pitch + t;
-                                pv[q] = ep[j + q];
-                            }
-#pragma unroll
-                            for (int q = 0; q < 8; ++q) av[q] = acc[ad[q]];
-#pragma unroll
-                            for (int q = 0; q < 8; ++q) acc[ad[q]] = av[q] + pv[q] * w;
-                        }
-                        for (; j < k; ++j) {
-                            double* a = &acc[ei[j] * pitch + t];
-                            *a = *a + ep[j] * w;
-                        }
-                    }
-                }
-                ++contrib;
-                T = T * (1.0 - f);                                  // :311
-                if (p.opt.early_exit && T < p.opt.eps) {           // :312
-                    done = true;
-                    break;
-                }
-            }
-        }
-        if (__syncthreads_and(done)) break;
-    }
-
-    if (kRender) {
-        if (inside) {
-            const size_t pix = static_cast<size_t>(y) * p.cam.W + x;
-            if (vd.sil) vd.sil[pix] = 1.0 - T;  // :314
-            if (vd.color) {
-                vd.color[pix * 3] = ac0;
-                vd.color[pix * 3 + 1] = ac1;
-                vd.color[pix * 3 + 2] = ac2;
-            }
-            if (vd.depth) vd.depth[pix] = adep;
-        }
-        if (vd.sem) {
-            __syncthreads();
-            for (int l = t; l < kTilePx * C; l += kTilePx) {
-                const int q = l / C;
-                const int c = l - q * C;
-                const int qx = bx * kTile + (q & (kTile - 1));
-                const int qy = by * kTile + q / kTile;
-                if (qx < p.cam.W && qy < p.cam.H)
-                    vd.sem[(static_cast<size_t>(qy) * p.cam.W + qx) * C + c] = acc[c * pitch + q];
-            }
-        }
-    } else {
-        // clipped_entropy of this pixel (:360-369), reference summation order.
-        double h = 0.0;
-        unsigned long long miss = 0;
-        if (inside) {
-            double total = 0.0;
-            for (int c = 0; c < C; ++c) total += clamp_prob(acc[c * pitch + t]);
-            for (int c = 0; c < C; ++c) {
-                const double q = clamp_prob(acc[c * pitch + t]) / total;
-                h -= q * log(q);
-            }
-            miss = (1.0 - T == 0.0) ? 1ull : 0ull;  // explorer.cpp:198
-        }
-        red_d[t] = h;
-        red_u[t] = miss;
-        __syncthreads();
-        for (int s = kTilePx / 2; s > 0; s >>= 1) {  // fixed tree: deterministic
-            if (t < s) {
-                red_d[t] += red_d[t + s];
-                red_u[t] += red_u[t + s];
-            }
-            __syncthreads();
-        }
-        if (t == 0) {
-            vd.ent_partial[tile] = red_d[0];
-            vd.miss_partial[tile] = static_cast<uint32_t>(red_u[0]);
-        }
-    }
-    // K (contributors) for the measurement counters
-    red_u[t] = contrib;
-    __syncthreads();
-    for (int s = kTilePx / 2; s > 0; s >>= 1) {
-        if (t < s) red_u[t] += red_u[t + s];
-        __syncthreads();
-    }
-    if (t == 0 && vd.contributors && red_u[0]) atomicAdd(vd.contributors, red_u[0]);
 }
 
 // Per view: n_missing and entropy_sum from the per-tile partials, summed in a
@@ -488,65 +295,24 @@ void launch_tiefix(const DevMap& m, const PoseParams* d_pose, const CamParams& c
 }
 
 void launch_pack(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
-                 const OptParams& o, const uint32_t* idx, uint32_t V, PackedSplat* packed,
-                 unsigned long long* counts, cudaStream_t s) {
+                 const OptParams& o, const GroupParams& gp, const uint32_t* idx, uint32_t V,
+                 PackedSplat* packed, unsigned long long* counts, cudaStream_t s) {
     if (V == 0) return;
-    k_pack<<<blocks_for(V, 256), 256, 0, s>>>(m, d_pose, cam, o, idx, V, packed, counts);
+    k_pack<<<blocks_for(V, 256), 256, 0, s>>>(m, d_pose, cam, o, gp, idx, V, packed, counts);
 }
 
 void launch_emit_pairs(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
-                       const OptParams& o, const PackedSplat* packed,
+                       const OptParams& o, const uint32_t* order,
                        const unsigned long long* offsets, uint32_t V, uint32_t* tile_keys,
                        uint32_t* tile_vals, cudaStream_t s) {
     if (V == 0) return;
-    k_emit2<<<blocks_for(V, 128), 128, 0, s>>>(m, d_pose, cam, o, packed, offsets, V, tile_keys,
+    k_emit2<<<blocks_for(V, 128), 128, 0, s>>>(m, d_pose, cam, o, order, offsets, V, tile_keys,
                                                tile_vals);
 }
 
 void launch_ranges(const uint32_t* sorted_tiles, uint64_t P, uint2* ranges, cudaStream_t s) {
     if (P == 0) return;
     k_ranges<<<blocks_for(P, 256), 256, 0, s>>>(sorted_tiles, P, ranges);
-}
-
-size_t raster_smem_bytes(int C, int k, bool render) {
-    const int pitch = render ? kTilePx + 1 : kTilePx;
-    size_t b = static_cast<size_t>(C) * pitch * sizeof(double);
-    b += static_cast<size_t>(kBatch) * 6 * sizeof(double);
-    b += static_cast<size_t>(kBatch) * k * sizeof(double);
-    if (render) b += static_cast<size_t>(kBatch) * 4 * sizeof(double);
-    b += static_cast<size_t>(kBatch) * 3 * sizeof(float);
-    b += static_cast<size_t>(kBatch) * sizeof(uint32_t);
-    b += static_cast<size_t>(kBatch) * k * sizeof(uint16_t);
-    return (b + 15) & ~static_cast<size_t>(15);
-}
-
-int raster_batch_entries() { return kBatch; }
-
-template <bool kRender, bool kDup>
-static void launch_raster_t(const RasterParams& p, int n_views, cudaStream_t s) {
-    const size_t smem = raster_smem_bytes(p.map.C, p.map.k, kRender);
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaFuncSetAttribute(k_raster<kRender, kDup>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        configured = smem;
-    }
-    dim3 grid(p.tiles_per_view, n_views);
-    k_raster<kRender, kDup><<<grid, kTilePx, smem, s>>>(p);
-}
-
-void launch_raster_score(const RasterParams& p, int n_views, cudaStream_t s) {
-    if (p.map.dup_idx)
-        launch_raster_t<false, true>(p, n_views, s);
-    else
-        launch_raster_t<false, false>(p, n_views, s);
-}
-
-void launch_raster_render(const RasterParams& p, int n_views, cudaStream_t s) {
-    if (p.map.dup_idx)
-        launch_raster_t<true, true>(p, n_views, s);
-    else
-        launch_raster_t<true, false>(p, n_views, s);
 }
 
 void launch_reduce_scores(const ViewDesc* views, int n_views, int tiles, double* out_missing,

@@ -1,0 +1,449 @@
+// K4 / K5: the tile compositor (render) and the candidate scorer (score) for sm_100a.
+//
+// Reference: proj/src/splat_render.cpp:254-324 (compositor), :360-369
+// (clipped_entropy), proj/src/explorer.cpp:195-203 (per-view n_missing and
+// entropy sum). Built with --fmad=false; the only fused operations are the ones
+// written explicitly (__fma_rn) below: the semantic scatter and the exp
+// polynomial. Both stay within ~1 ulp of the reference's fp64 arithmetic.
+//
+// One CTA (8 warps, 256 threads) = one 8x8 pixel block of one view. Per batch of
+// kNB Gaussians (depth order), streamed through shared memory by a
+// double-buffered cp.async pipeline:
+//   phase A  all 8 warps: footprint f[e][px] for kNB x 64 (entry, pixel) pairs,
+//            4 independent entries per thread (probe test, exact d2 test, exp);
+//   phase B  warps 0-1: the exact sequential transmittance chain per pixel
+//            (w = f T; T *= 1 - f; early exit), colour/depth in render mode;
+//            warps 2-7: per entry, the bounds of its sparse row in each of the
+//            4 channel groups (rows are class-sorted at upload);
+//   phase C  all 8 warps: the sparse semantic scatter. Warp (h, g) owns pixels
+//            32h..32h+31 and channel group g, so no two warps touch the same
+//            accumulator word; the accumulator is [C][64] fp64 in shared memory
+//            and a warp's 32 lanes hit 32 consecutive doubles (no bank conflict).
+// Score epilogue: per (pixel, group) S1 = sum c, S2 = sum c ln c with
+// c = clamp(p, 1e-3, 1); H = ln S1 - S2/S1 (== -sum q ln q, q = c / S1); the tile's
+// entropy and exact-zero-silhouette count go to a per-tile slot that a second
+// kernel sums in a fixed order (deterministic, batching/sharding-invariant).
+#include <algorithm>
+
+#include "sgm_internal.h"
+
+namespace sgm {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kNB = 16;      // Gaussians per staged batch
+constexpr int kGroups = 4;   // channel groups (one per warp pair in phase C)
+constexpr int kBnd = kGroups + 1;
+
+__host__ __device__ constexpr int align16(int b) { return (b + 15) & ~15; }
+
+struct Layout {  // byte offsets in dynamic shared memory
+    int acc, w, bnd, done, rm, stage0, stage_bytes, st_packed, st_idx, st_prob, st_color, total;
+};
+
+__host__ __device__ inline Layout make_layout(int C, int kpad, bool render) {
+    Layout L;
+    const int pitch = render ? kTilePx + 1 : kTilePx;
+    L.acc = 0;
+    L.w = align16(C * pitch * 8);
+    L.bnd = L.w + kNB * kTilePx * 8;
+    L.done = L.bnd + align16(kNB * kBnd * 2);
+    L.rm = L.done + kTilePx * 4;
+    L.stage0 = L.rm + 2 * kNB * 8;
+    L.st_packed = 0;
+    L.st_idx = kNB * static_cast<int>(sizeof(PackedSplat));
+    L.st_prob = L.st_idx + kNB * kpad * 2;
+    L.st_color = L.st_prob + kNB * kpad * 8;
+    L.stage_bytes = L.st_color + (render ? kNB * 32 : 0);
+    L.total = L.stage0 + 2 * L.stage_bytes;
+    // the score epilogue's (S1, S2) exchange reuses the stage area
+    const int red = kGroups * kTilePx * 16;
+    if (L.total < L.stage0 + red) L.total = L.stage0 + red;
+    return L;
+}
+
+// exp(x) for the footprint argument x = -d2 / (2 r^2) in [-cut^2/2, 0]:
+// Cody-Waite reduction by ln 2 and a degree-13 Taylor polynomial (|r| <= ln2/2,
+// truncation < 2.5e-16 relative). Coefficients live in the constant bank so the
+// DFMAs take them as operands (no 64-bit immediate moves).
+__constant__ double c_exp[16] = {
+    1.4426950408889634,      // log2(e)
+    0.6931467056274414,      // ln2 hi (low 32 mantissa bits zero: k * hi is exact)
+    4.7493250390316726e-07,  // ln2 lo
+    1.6059043836821613e-10,  // 1/13!
+    2.08767569878681e-09,    // 1/12!
+    2.505210838544172e-08,   // 1/11!
+    2.755731922398589e-07,   // 1/10!
+    2.7557319223985893e-06,  // 1/9!
+    2.48015873015873e-05,    // 1/8!
+    0.0001984126984126984,   // 1/7!
+    0.001388888888888889,    // 1/6!
+    0.008333333333333333,    // 1/5!
+    0.041666666666666664,    // 1/4!
+    0.16666666666666666,     // 1/3!
+    0.5,                     // 1/2!
+    1.0};
+
+__device__ __forceinline__ double exp_footprint(double x) {
+    if (x < -700.0) return 0.0;  // (outside the footprint range; keeps the scaling valid)
+    const double shifter = 6755399441055744.0;  // 1.5 * 2^52: round-to-int in the low word
+    const double t = __fma_rn(x, c_exp[0], shifter);
+    const double kf = t - shifter;
+    const int k = __double2loint(t);
+    double r = __fma_rn(-kf, c_exp[1], x);
+    r = __fma_rn(-kf, c_exp[2], r);
+    double p = c_exp[3];
+#pragma unroll
+    for (int i = 4; i < 15; ++i) p = __fma_rn(p, r, c_exp[i]);
+    p = __fma_rn(p, r, 1.0);
+    p = __fma_rn(p, r, 1.0);
+    // scale by 2^k (k >= -1011 here, so the result stays normal)
+    return __hiloint2double(__double2hiint(p) + k * (1 << 20), __double2loint(p));
+}
+
+__device__ __forceinline__ double clamp_prob(double v) {
+    // std::clamp(v, 0.001, 1.0) (splat_render.cpp:362)
+    return v < 0.001 ? 0.001 : (1.0 < v ? 1.0 : v);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+template <bool kRender, bool kDup>
+__global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int C = p.map.C;
+    const int k = p.map.k;
+    const int kpad = p.map.kpad;
+    const int Cg = p.groups.Cg;
+    constexpr int pitch = kRender ? kTilePx + 1 : kTilePx;
+    const Layout L = make_layout(C, kpad, kRender);
+    double* acc = reinterpret_cast<double*>(smem + L.acc);
+    double* W = reinterpret_cast<double*>(smem + L.w);             // [kNB][64]
+    uint16_t* bnd = reinterpret_cast<uint16_t*>(smem + L.bnd);     // [kNB][kBnd]
+    int* sdone = reinterpret_cast<int*>(smem + L.done);            // [64]
+    uint2* rm = reinterpret_cast<uint2*>(smem + L.rm);             // [2][kNB] (rank, map index)
+    unsigned char* stg = smem + L.stage0;
+    double2* red = reinterpret_cast<double2*>(stg);                // [kGroups][64], epilogue
+
+    const ViewDesc vd = p.views[blockIdx.y];
+    const int tile = blockIdx.x;
+    const int bx = tile % p.raster_tiles_x, by = tile / p.raster_tiles_x;
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const int px = t & (kTilePx - 1);  // this thread's pixel in phase A / epilogues
+    const int x = bx * kTile + (px & (kTile - 1));
+    const int y = by * kTile + px / kTile;
+    const bool inside = x < p.cam.W && y < p.cam.H;
+    const int bin = ((by * kTile) / p.opt.ts) * p.opt.tiles_x + (bx * kTile) / p.opt.ts;
+    const uint2 rg = vd.ranges[bin];
+    const uint32_t L0 = rg.x;
+    const uint32_t Ln = rg.y - rg.x;
+    const int nbatch = static_cast<int>((Ln + kNB - 1) / kNB);
+    const bool want_sem = !kRender || vd.sem != nullptr;
+
+    for (int i = t; i < C * pitch; i += kThreads) acc[i] = 0.0;
+    if (t < kTilePx) sdone[t] = inside ? 0 : 1;
+
+    // ---- cp.async pipeline over batches of kNB Gaussians (depth-rank order) ----
+    const int qi = kpad / 8, qp = kpad / 2;
+    const int Q = 4 + qi + qp + (kRender ? 2 : 0);  // 16-byte chunks per Gaussian
+    auto issue = [&](int b) {
+        unsigned char* sb = stg + (b & 1) * L.stage_bytes;
+        const int n = min(kNB, static_cast<int>(Ln) - b * kNB);
+        const uint2* slot = rm + (b & 1) * kNB;
+        for (int c = t; c < n * Q; c += kThreads) {
+            const int e = c / Q;
+            int q = c - e * Q;
+            const uint2 v = slot[e];
+            const unsigned char* src;
+            unsigned char* dst;
+            if (q < 4) {
+                src = reinterpret_cast<const unsigned char*>(vd.packed + v.x) + 16 * q;
+                dst = sb + L.st_packed + e * 64 + 16 * q;
+            } else if ((q -= 4) < qi) {
+                src = reinterpret_cast<const unsigned char*>(p.map.sem_idx + static_cast<size_t>(v.y) * kpad) + 16 * q;
+                dst = sb + L.st_idx + e * kpad * 2 + 16 * q;
+            } else if ((q -= qi) < qp) {
+                src = reinterpret_cast<const unsigned char*>(p.map.sem_prob + static_cast<size_t>(v.y) * kpad) + 16 * q;
+                dst = sb + L.st_prob + e * kpad * 8 + 16 * q;
+            } else {
+                q -= qp;
+                src = reinterpret_cast<const unsigned char*>(p.map.color4 + static_cast<size_t>(v.y) * 4) + 16 * q;
+                dst = sb + L.st_color + e * 32 + 16 * q;
+            }
+            cp_async16(dst, src);
+        }
+        cp_async_commit();
+    };
+    auto fetch_rm = [&](int b, int slot) {
+        if (t < kNB) {
+            const uint32_t q = static_cast<uint32_t>(b) * kNB + t;
+            if (q < Ln) {
+                const uint32_t r = vd.list[L0 + q];
+                rm[slot * kNB + t] = make_uint2(r, vd.order[r]);
+            }
+        }
+    };
+
+    fetch_rm(0, 0);
+    fetch_rm(1, 1);
+    __syncthreads();
+    if (nbatch > 0) issue(0);
+
+    const double dpx = x + 0.5, dpy = y + 0.5;                                 // :261, :263
+    const float fpx = static_cast<float>(dpx), fpy = static_cast<float>(dpy);  // :274
+    // phase-B state (warps 0-1 own pixel t)
+    double T = 1.0;
+    double ac0 = 0.0, ac1 = 0.0, ac2 = 0.0, adep = 0.0;
+    bool done = !inside;
+    unsigned long long contrib = 0;
+    const int e_first = t >> 6;  // phase A: this thread's entries e_first + 4i
+
+    for (int b = 0; b < nbatch; ++b) {
+        cp_async_wait_all();
+        __syncthreads();  // batch b landed; rm slot for b+1 visible; W / bnd free
+        if (b + 1 < nbatch) issue(b + 1);
+        if (b + 2 < nbatch) fetch_rm(b + 2, b & 1);
+        const unsigned char* sb = stg + (b & 1) * L.stage_bytes;
+        const PackedSplat* sp = reinterpret_cast<const PackedSplat*>(sb + L.st_packed);
+        const uint16_t* si = reinterpret_cast<const uint16_t*>(sb + L.st_idx);
+        const double* spr = reinterpret_cast<const double*>(sb + L.st_prob);
+        const double* scol = reinterpret_cast<const double*>(sb + L.st_color);
+        const int n = min(kNB, static_cast<int>(Ln) - b * kNB);
+
+        // ---- phase A: footprints (independent of T) ----
+        {
+            const bool pdone = sdone[px] != 0;
+#pragma unroll
+            for (int i = 0; i < kNB / 4; ++i) {
+                const int e = e_first + 4 * i;
+                if (e >= n) break;
+                double f = 0.0;
+                if (!pdone) {
+                    const float4 pf = *reinterpret_cast<const float4*>(&sp[e].pmx);
+                    const float fdx = fpx - pf.x;
+                    const float fdy = fpy - pf.y;
+                    if (!(fdx * fdx + fdy * fdy > pf.z)) {  // :276-278
+                        const double dx = dpx - sp[e].mx;
+                        const double dy = dpy - sp[e].my;
+                        const double d2 = dx * dx + dy * dy;
+                        if (!(d2 > sp[e].cutoff_d2)) {  // :283
+                            f = sp[e].alpha * exp_footprint(-d2 * sp[e].inv_two_r2);  // :284
+                            if (f > kMaxFootprint) f = kMaxFootprint;                 // :285
+                            // a contributor with f == 0 (alpha == 0) changes nothing
+                        }
+                    }
+                }
+                W[e * kTilePx + px] = f;
+            }
+        }
+        __syncthreads();
+
+        // ---- phase B ----
+        if (t < kTilePx) {
+            // sequential transmittance chain of pixel t (:286-312)
+            for (int e = 0; e < n; ++e) {
+                const double f = W[e * kTilePx + t];
+                if (done || f == 0.0) {
+                    W[e * kTilePx + t] = 0.0;
+                    continue;
+                }
+                const double w = f * T;
+                W[e * kTilePx + t] = w;
+                if (kRender) {
+                    ac0 += scol[4 * e] * w;  // :289-291 (colour clamped at upload)
+                    ac1 += scol[4 * e + 1] * w;
+                    ac2 += scol[4 * e + 2] * w;
+                    adep += sp[e].z * w;  // :293
+                }
+                ++contrib;
+                T = T * (1.0 - f);                        // :311
+                if (p.opt.early_exit && T < p.opt.eps)   // :312
+                    done = true;
+            }
+            sdone[t] = done ? 1 : 0;
+        } else if (want_sem) {
+            // channel-group bounds of each staged row: bnd[e][g] = #entries < g*Cg
+            for (int u = t - kTilePx; u < n * (kGroups - 1); u += kThreads - kTilePx) {
+                const int e = u / (kGroups - 1);
+                const int g = u - e * (kGroups - 1) + 1;
+                const int lim = g * Cg;
+                const uint16_t* row = si + e * kpad;
+                int c = 0;
+                for (int j = 0; j < k; ++j) c += row[j] < lim ? 1 : 0;
+                bnd[e * kBnd + g] = static_cast<uint16_t>(c);
+                if (g == 1) {
+                    bnd[e * kBnd] = 0;
+                    bnd[e * kBnd + kGroups] = static_cast<uint16_t>(k);
+                }
+            }
+        }
+        __syncthreads();
+
+        // ---- phase C: sparse semantic scatter, warp (h, g) ----
+        if (want_sem) {
+            const int h = warp & 1, g = warp >> 1;
+            const int cp = 32 * h + lane;
+            double* accp = acc + cp;
+            for (int e = 0; e < n; ++e) {
+                const double w = W[e * kTilePx + cp];
+                if (!__any_sync(0xffffffffu, w != 0.0)) continue;
+                const int lo = bnd[e * kBnd + g], hi = bnd[e * kBnd + g + 1];
+                const uint16_t* ei = si + e * kpad;
+                const double* ep = spr + e * kpad;
+                if (kDup) {
+                    for (int j = lo; j < hi; ++j) {  // repeated classes: in order
+                        double* a = accp + ei[j] * pitch;
+                        *a = __fma_rn(ep[j], w, *a);  // :307
+                    }
+                } else {
+                    int j = lo;
+                    for (; j + 4 <= hi; j += 4) {
+                        double* a[4];
+                        double pv[4], av[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            a[q] = accp + ei[j + q] * pitch;
+                            pv[q] = ep[j + q];
+                        }
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) av[q] = *a[q];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) *a[q] = __fma_rn(pv[q], w, av[q]);
+                    }
+                    for (; j < hi; ++j) {
+                        double* a = accp + ei[j] * pitch;
+                        *a = __fma_rn(ep[j], w, *a);
+                    }
+                }
+            }
+        }
+        // early termination of the whole block (:312 for every pixel)
+        const int mine = (t < kTilePx) ? (done ? 1 : 0) : 1;
+        if (__syncthreads_and(mine)) break;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+
+    __shared__ double red_d[kTilePx];
+    __shared__ unsigned long long red_u[kTilePx];
+    if (kRender) {
+        if (t < kTilePx && inside) {
+            const size_t pix = static_cast<size_t>(y) * p.cam.W + x;
+            if (vd.sil) vd.sil[pix] = 1.0 - T;  // :314
+            if (vd.color) {
+                vd.color[pix * 3] = ac0;
+                vd.color[pix * 3 + 1] = ac1;
+                vd.color[pix * 3 + 2] = ac2;
+            }
+            if (vd.depth) vd.depth[pix] = adep;
+        }
+        if (vd.sem) {
+            for (int l = t; l < kTilePx * C; l += kThreads) {
+                const int q = l / C;
+                const int c = l - q * C;
+                const int qx = bx * kTile + (q & (kTile - 1));
+                const int qy = by * kTile + q / kTile;
+                if (qx < p.cam.W && qy < p.cam.H)
+                    vd.sem[(static_cast<size_t>(qy) * p.cam.W + qx) * C + c] = acc[c * pitch + q];
+            }
+        }
+    } else {
+        // clipped_entropy (:360-369), split by channel group: warp (h, g)
+        const int h = warp & 1, g = warp >> 1;
+        const int cp = 32 * h + lane;
+        const int c0 = g * Cg, c1 = min(C, c0 + Cg);
+        double S1 = 0.0, S2 = 0.0;
+        const double K0 = 0.001 * log(0.001);
+#pragma unroll 4
+        for (int c = c0; c < c1; ++c) {
+            const double cl = clamp_prob(acc[c * pitch + cp]);
+            S1 += cl;
+            S2 += cl == 0.001 ? K0 : cl * log(cl);
+        }
+        red[g * kTilePx + cp] = make_double2(S1, S2);
+        __syncthreads();
+        if (t < kTilePx) {
+            S1 = 0.0;
+            S2 = 0.0;
+#pragma unroll
+            for (int q = 0; q < kGroups; ++q) {
+                S1 += red[q * kTilePx + t].x;
+                S2 += red[q * kTilePx + t].y;
+            }
+            red_d[t] = inside ? log(S1) - S2 / S1 : 0.0;
+            red_u[t] = (inside && 1.0 - T == 0.0) ? 1ull : 0ull;  // explorer.cpp:198
+        }
+        __syncthreads();
+        for (int s = kTilePx / 2; s > 0; s >>= 1) {  // fixed tree: deterministic
+            if (t < s) {
+                red_d[t] += red_d[t + s];
+                red_u[t] += red_u[t + s];
+            }
+            __syncthreads();
+        }
+        if (t == 0) {
+            vd.ent_partial[tile] = red_d[0];
+            vd.miss_partial[tile] = static_cast<uint32_t>(red_u[0]);
+        }
+        __syncthreads();
+    }
+    // K (contributors) for the measurement counters
+    if (t < kTilePx) red_u[t] = contrib;
+    __syncthreads();
+    for (int s = kTilePx / 2; s > 0; s >>= 1) {
+        if (t < s) red_u[t] += red_u[t + s];
+        __syncthreads();
+    }
+    if (t == 0 && vd.contributors && red_u[0]) atomicAdd(vd.contributors, red_u[0]);
+}
+
+template <bool kRender, bool kDup>
+void launch_t(const RasterParams& p, int n_views, cudaStream_t s) {
+    auto kern = k_raster<kRender, kDup>;
+    const size_t smem = raster_smem_bytes(p.map, p.groups, kRender);
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        configured = smem;
+    }
+    dim3 grid(static_cast<unsigned>(p.tiles_per_view), static_cast<unsigned>(n_views), 1);
+    kern<<<grid, kThreads, smem, s>>>(p);
+}
+
+}  // namespace
+
+GroupParams choose_groups(int C, int k) {
+    (void)k;
+    GroupParams gp;
+    gp.P = kGroups;
+    gp.Cg = (C + kGroups - 1) / kGroups;
+    return gp;
+}
+
+size_t raster_smem_bytes(const DevMap& m, const GroupParams& gp, bool render) {
+    (void)gp;
+    return static_cast<size_t>(make_layout(m.C, m.kpad, render).total);
+}
+
+void launch_raster_score(const RasterParams& p, int n_views, cudaStream_t s) {
+    if (p.map.dup_idx)
+        launch_t<false, true>(p, n_views, s);
+    else
+        launch_t<false, false>(p, n_views, s);
+}
+
+void launch_raster_render(const RasterParams& p, int n_views, cudaStream_t s) {
+    if (p.map.dup_idx)
+        launch_t<true, true>(p, n_views, s);
+    else
+        launch_t<true, false>(p, n_views, s);
+}
+
+}  // namespace sgm

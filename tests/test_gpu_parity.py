@@ -257,7 +257,8 @@ def test_cfg1_full_size_properties(ctx, orc):
     np.testing.assert_allclose(es, es_o, rtol=ENT_RTOL, atol=0)
     out = sgm.render(gm, cam, poses[0], RenderChannels.scoring(), ctx=ctx)
     s = out.sem.reshape(-1, out.channels).sum(axis=1)
-    assert np.max(np.abs(s - out.silhouette)) < 1e-9
+    # probs are f32-rounded (SGMP precision), so each Gaussian's k probs sum to 1 +- ~1e-7
+    assert np.max(np.abs(s - out.silhouette)) < 1e-6
     assert out.silhouette.min() >= 0.0 and out.silhouette.max() <= 1.0
     h = np.array([sgm.clipped_entropy(out.sem[i * out.channels:(i + 1) * out.channels])
                   for i in range(0, cam.pixel_count(), 997)])
