@@ -15,12 +15,16 @@
 //            (w = f T; T *= 1 - f; early exit), colour/depth in render mode;
 //            warps 2-7: per entry, the bounds of its sparse row in each of the
 //            4 channel groups (rows are class-sorted at upload);
-//   phase C  all 8 warps: the sparse semantic scatter. Warp (h, g) owns pixels
-//            32h..32h+31 and channel group g, so no two warps touch the same
-//            accumulator word; the accumulator is [C][64] fp64 in shared memory
-//            and a warp's 32 lanes hit 32 consecutive doubles (no bank conflict).
+//   phase C  all 8 warps: the sparse semantic scatter. Warp g owns channel
+//            group g (C/8 channels) for all 64 pixels, two pixels per lane, so no
+//            two warps touch the same accumulator word. The accumulator is
+//            [C][32] double2 in shared memory (lane l holds pixels l and l+32):
+//            one LDS.128 / 2 DFMA / STS.128 per (Gaussian, class) entry covers
+//            the whole 8x8 block, and a warp's lanes hit 32 consecutive 16-byte
+//            words (no bank conflict).
 // Score epilogue: per (pixel, group) S1 = sum c, S2 = sum c ln c with
-// c = clamp(p, 1e-3, 1); H = ln S1 - S2/S1 (== -sum q ln q, q = c / S1); the tile's
+// c = clamp(p, 1e-3, 1) (a 128-entry table log, ~1 ulp); H = ln S1 - S2/S1
+// (== -sum q ln q, q = c / S1); the tile's
 // entropy and exact-zero-silhouette count go to a per-tile slot that a second
 // kernel sums in a fixed order (deterministic, batching/sharding-invariant).
 #include <algorithm>
@@ -32,8 +36,9 @@ namespace sgm {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kNB = 16;      // Gaussians per staged batch
-constexpr int kGroups = 4;   // channel groups (one per warp pair in phase C)
+constexpr int kWarps = kThreads / 32;
+constexpr int kNB = 16;            // Gaussians per staged batch
+constexpr int kGroups = kWarps;    // channel groups: one warp each in phase C
 constexpr int kBnd = kGroups + 1;
 
 __host__ __device__ constexpr int align16(int b) { return (b + 15) & ~15; }
@@ -42,11 +47,15 @@ struct Layout {  // byte offsets in dynamic shared memory
     int acc, w, bnd, done, rm, stage0, stage_bytes, st_packed, st_idx, st_prob, st_color, total;
 };
 
+// accumulator row pitch in double2 units (render: +1 so the transposed write-out
+// of the [channel][pixel] tile to the reference's [pixel][channel] layout is
+// nearly conflict-free)
+__host__ __device__ constexpr int acc_pitch(bool render) { return render ? 33 : 32; }
+
 __host__ __device__ inline Layout make_layout(int C, int kpad, bool render) {
     Layout L;
-    const int pitch = render ? kTilePx + 1 : kTilePx;
     L.acc = 0;
-    L.w = align16(C * pitch * 8);
+    L.w = align16(C * acc_pitch(render) * 16);
     L.bnd = L.w + kNB * kTilePx * 8;
     L.done = L.bnd + align16(kNB * kBnd * 2);
     L.rm = L.done + kTilePx * 4;
@@ -57,7 +66,7 @@ __host__ __device__ inline Layout make_layout(int C, int kpad, bool render) {
     L.st_color = L.st_prob + kNB * kpad * 8;
     L.stage_bytes = L.st_color + (render ? kNB * 32 : 0);
     L.total = L.stage0 + 2 * L.stage_bytes;
-    // the score epilogue's (S1, S2) exchange reuses the stage area
+    // the score epilogue's per-(group, pixel) (S1, S2) exchange reuses the stages
     const int red = kGroups * kTilePx * 16;
     if (L.total < L.stage0 + red) L.total = L.stage0 + red;
     return L;
@@ -70,7 +79,7 @@ __host__ __device__ inline Layout make_layout(int C, int kpad, bool render) {
 __constant__ double c_exp[16] = {
     1.4426950408889634,      // log2(e)
     0.6931467056274414,      // ln2 hi (low 32 mantissa bits zero: k * hi is exact)
-    4.7493250390316726e-07,  // ln2 lo
+    4.7493250390941725e-07,  // ln2 lo
     1.6059043836821613e-10,  // 1/13!
     2.08767569878681e-09,    // 1/12!
     2.505210838544172e-08,   // 1/11!
@@ -102,6 +111,32 @@ __device__ __forceinline__ double exp_footprint(double x) {
     return __hiloint2double(__double2hiint(p) + k * (1 << 20), __double2loint(p));
 }
 
+// log(x) for normal x > 0 (the epilogue's clamped probabilities, [1e-3, 1]):
+// x = m 2^e, m in [1,2); c = RN(1 / centre of m's 1/128 interval); r = m c - 1
+// (|r| <= 2^-8, exact-ish via FMA); log x = e ln2 - log c + log1p(r) with a
+// degree-7 series. ~1e-16 absolute error; ~16 instructions.
+__device__ const double2 g_logtab[128] = {
+#include "sgm_logtab.inc"
+};
+__constant__ double c_log[10] = {0.14285714285714285,  -0.16666666666666666, 0.2, -0.25,
+                                 0.3333333333333333,   -0.5,                 1.0,
+                                 0.6931467056274414,   4.7493250390941725e-07, 0.0};
+
+__device__ __forceinline__ double log_table(double x) {
+    const int hi = __double2hiint(x);
+    const int lo = __double2loint(x);
+    const double e = static_cast<double>((hi >> 20) - 1023);
+    const int i = (hi >> 13) & 0x7f;
+    const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+    const double2 tc = __ldg(&g_logtab[i]);
+    const double r = __fma_rn(m, tc.x, -1.0);
+    double q = c_log[0];
+#pragma unroll
+    for (int j = 1; j < 7; ++j) q = __fma_rn(q, r, c_log[j]);
+    const double l1p = q * r;
+    return __fma_rn(e, c_log[7], tc.y + __fma_rn(e, c_log[8], l1p));
+}
+
 __device__ __forceinline__ double clamp_prob(double v) {
     // std::clamp(v, 0.001, 1.0) (splat_render.cpp:362)
     return v < 0.001 ? 0.001 : (1.0 < v ? 1.0 : v);
@@ -114,6 +149,11 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// index of pixel q's slot in a [row][32] double2 array viewed as doubles
+__device__ __forceinline__ int pair_slot(int row, int pitch2, int q) {
+    return (row * pitch2 + (q & 31)) * 2 + (q >> 5);
+}
+
 template <bool kRender, bool kDup>
 __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -121,10 +161,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     const int k = p.map.k;
     const int kpad = p.map.kpad;
     const int Cg = p.groups.Cg;
-    constexpr int pitch = kRender ? kTilePx + 1 : kTilePx;
+    constexpr int apitch = acc_pitch(kRender);
     const Layout L = make_layout(C, kpad, kRender);
+    double2* acc2 = reinterpret_cast<double2*>(smem + L.acc);     // [C][apitch]
     double* acc = reinterpret_cast<double*>(smem + L.acc);
-    double* W = reinterpret_cast<double*>(smem + L.w);             // [kNB][64]
+    double* W = reinterpret_cast<double*>(smem + L.w);             // [kNB][32] double2
+    const double2* W2 = reinterpret_cast<const double2*>(smem + L.w);
     uint16_t* bnd = reinterpret_cast<uint16_t*>(smem + L.bnd);     // [kNB][kBnd]
     int* sdone = reinterpret_cast<int*>(smem + L.done);            // [64]
     uint2* rm = reinterpret_cast<uint2*>(smem + L.rm);             // [2][kNB] (rank, map index)
@@ -136,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     const int bx = tile % p.raster_tiles_x, by = tile / p.raster_tiles_x;
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
-    const int px = t & (kTilePx - 1);  // this thread's pixel in phase A / epilogues
+    const int px = t & (kTilePx - 1);  // this thread's pixel in phase A / B / epilogues
     const int x = bx * kTile + (px & (kTile - 1));
     const int y = by * kTile + px / kTile;
     const bool inside = x < p.cam.W && y < p.cam.H;
@@ -146,8 +188,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     const uint32_t Ln = rg.y - rg.x;
     const int nbatch = static_cast<int>((Ln + kNB - 1) / kNB);
     const bool want_sem = !kRender || vd.sem != nullptr;
+    const int g = warp;  // phase C / epilogue channel group
+    const int c0 = g * Cg, c1 = min(C, c0 + Cg);
 
-    for (int i = t; i < C * pitch; i += kThreads) acc[i] = 0.0;
+    for (int i = t; i < C * apitch; i += kThreads) acc2[i] = make_double2(0.0, 0.0);
     if (t < kTilePx) sdone[t] = inside ? 0 : 1;
 
     // ---- cp.async pipeline over batches of kNB Gaussians (depth-rank order) ----
@@ -240,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
                         }
                     }
                 }
-                W[e * kTilePx + px] = f;
+                W[pair_slot(e, 32, px)] = f;
             }
         }
         __syncthreads();
@@ -249,13 +293,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
         if (t < kTilePx) {
             // sequential transmittance chain of pixel t (:286-312)
             for (int e = 0; e < n; ++e) {
-                const double f = W[e * kTilePx + t];
+                const int s = pair_slot(e, 32, t);
+                const double f = W[s];
                 if (done || f == 0.0) {
-                    W[e * kTilePx + t] = 0.0;
+                    W[s] = 0.0;
                     continue;
                 }
                 const double w = f * T;
-                W[e * kTilePx + t] = w;
+                W[s] = w;
                 if (kRender) {
                     ac0 += scol[4 * e] * w;  // :289-291 (colour clamped at upload)
                     ac1 += scol[4 * e + 1] * w;
@@ -269,16 +314,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
             }
             sdone[t] = done ? 1 : 0;
         } else if (want_sem) {
-            // channel-group bounds of each staged row: bnd[e][g] = #entries < g*Cg
+            // channel-group bounds of each staged (class-sorted) row:
+            // bnd[e][g] = #entries with class < g * Cg
             for (int u = t - kTilePx; u < n * (kGroups - 1); u += kThreads - kTilePx) {
                 const int e = u / (kGroups - 1);
-                const int g = u - e * (kGroups - 1) + 1;
-                const int lim = g * Cg;
+                const int gg = u - e * (kGroups - 1) + 1;
+                const int lim = gg * Cg;
                 const uint16_t* row = si + e * kpad;
                 int c = 0;
                 for (int j = 0; j < k; ++j) c += row[j] < lim ? 1 : 0;
-                bnd[e * kBnd + g] = static_cast<uint16_t>(c);
-                if (g == 1) {
+                bnd[e * kBnd + gg] = static_cast<uint16_t>(c);
+                if (gg == 1) {
                     bnd[e * kBnd] = 0;
                     bnd[e * kBnd + kGroups] = static_cast<uint16_t>(k);
                 }
@@ -286,40 +332,43 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
         }
         __syncthreads();
 
-        // ---- phase C: sparse semantic scatter, warp (h, g) ----
+        // ---- phase C: sparse semantic scatter; warp g = channel group g, 64 px ----
         if (want_sem) {
-            const int h = warp & 1, g = warp >> 1;
-            const int cp = 32 * h + lane;
-            double* accp = acc + cp;
+            double2* accl = acc2 + lane;
             for (int e = 0; e < n; ++e) {
-                const double w = W[e * kTilePx + cp];
-                if (!__any_sync(0xffffffffu, w != 0.0)) continue;
+                const double2 w = W2[e * 32 + lane];
+                if (!__any_sync(0xffffffffu, (w.x != 0.0) | (w.y != 0.0))) continue;
                 const int lo = bnd[e * kBnd + g], hi = bnd[e * kBnd + g + 1];
                 const uint16_t* ei = si + e * kpad;
                 const double* ep = spr + e * kpad;
                 if (kDup) {
                     for (int j = lo; j < hi; ++j) {  // repeated classes: in order
-                        double* a = accp + ei[j] * pitch;
-                        *a = __fma_rn(ep[j], w, *a);  // :307
+                        double2* a = accl + ei[j] * apitch;
+                        double2 v = *a;
+                        v.x = __fma_rn(ep[j], w.x, v.x);  // :307
+                        v.y = __fma_rn(ep[j], w.y, v.y);
+                        *a = v;
                     }
                 } else {
                     int j = lo;
-                    for (; j + 4 <= hi; j += 4) {
-                        double* a[4];
-                        double pv[4], av[4];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            a[q] = accp + ei[j + q] * pitch;
-                            pv[q] = ep[j + q];
-                        }
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) av[q] = *a[q];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) *a[q] = __fma_rn(pv[q], w, av[q]);
+                    for (; j + 2 <= hi; j += 2) {
+                        double2* a0 = accl + ei[j] * apitch;
+                        double2* a1 = accl + ei[j + 1] * apitch;
+                        const double p0 = ep[j], p1 = ep[j + 1];
+                        double2 v0 = *a0, v1 = *a1;
+                        v0.x = __fma_rn(p0, w.x, v0.x);
+                        v0.y = __fma_rn(p0, w.y, v0.y);
+                        v1.x = __fma_rn(p1, w.x, v1.x);
+                        v1.y = __fma_rn(p1, w.y, v1.y);
+                        *a0 = v0;
+                        *a1 = v1;
                     }
-                    for (; j < hi; ++j) {
-                        double* a = accp + ei[j] * pitch;
-                        *a = __fma_rn(ep[j], w, *a);
+                    if (j < hi) {
+                        double2* a = accl + ei[j] * apitch;
+                        double2 v = *a;
+                        v.x = __fma_rn(ep[j], w.x, v.x);
+                        v.y = __fma_rn(ep[j], w.y, v.y);
+                        *a = v;
                     }
                 }
             }
@@ -351,27 +400,27 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
                 const int qx = bx * kTile + (q & (kTile - 1));
                 const int qy = by * kTile + q / kTile;
                 if (qx < p.cam.W && qy < p.cam.H)
-                    vd.sem[(static_cast<size_t>(qy) * p.cam.W + qx) * C + c] = acc[c * pitch + q];
+                    vd.sem[(static_cast<size_t>(qy) * p.cam.W + qx) * C + c] =
+                        acc[pair_slot(c, apitch, q)];
             }
         }
     } else {
-        // clipped_entropy (:360-369), split by channel group: warp (h, g)
-        const int h = warp & 1, g = warp >> 1;
-        const int cp = 32 * h + lane;
-        const int c0 = g * Cg, c1 = min(C, c0 + Cg);
-        double S1 = 0.0, S2 = 0.0;
-        const double K0 = 0.001 * log(0.001);
-#pragma unroll 4
+        // clipped_entropy (:360-369) split by channel group: warp g, pixels lane, lane+32
+        double S1x = 0.0, S2x = 0.0, S1y = 0.0, S2y = 0.0;
+#pragma unroll 2
         for (int c = c0; c < c1; ++c) {
-            const double cl = clamp_prob(acc[c * pitch + cp]);
-            S1 += cl;
-            S2 += cl == 0.001 ? K0 : cl * log(cl);
+            const double2 v = acc2[c * apitch + lane];
+            const double ax = clamp_prob(v.x), ay = clamp_prob(v.y);
+            S1x += ax;
+            S1y += ay;
+            S2x = __fma_rn(ax, log_table(ax), S2x);
+            S2y = __fma_rn(ay, log_table(ay), S2y);
         }
-        red[g * kTilePx + cp] = make_double2(S1, S2);
+        red[g * kTilePx + lane] = make_double2(S1x, S2x);
+        red[g * kTilePx + lane + 32] = make_double2(S1y, S2y);
         __syncthreads();
         if (t < kTilePx) {
-            S1 = 0.0;
-            S2 = 0.0;
+            double S1 = 0.0, S2 = 0.0;
 #pragma unroll
             for (int q = 0; q < kGroups; ++q) {
                 S1 += red[q * kTilePx + t].x;
