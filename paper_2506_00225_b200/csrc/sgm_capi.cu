@@ -3,8 +3,8 @@
 // Pipeline for a batch of views (all on the ctx stream):
 //   1. K1 k_preprocess over (Gaussian, view): compact visible (z, index), count V, P
 //   2. one D2H of the per-view V/P counts (the only host sync before the results)
-//   3. per view: CUB radix sort on fp64 z -> k_tiefix -> k_pack -> CUB scan of
-//      tile counts -> k_emit2 -> CUB stable radix sort on the bin id -> k_ranges
+//   3. per view: CUB radix sort on fp32(z) -> k_tiefix -> k_pack -> CUB scan of
+//      tile counts -> k_emit_lb -> CUB stable radix sort on the bin id -> k_ranges
 //   4. one batched raster launch over (8x8 tile, view)
 //   5. k_reduce_scores (score) / planes already written (render)
 // Views whose pair lists do not fit the scratch budget together are split into
@@ -19,6 +19,7 @@
 #include <functional>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/sgm.h"
@@ -116,12 +117,17 @@ struct sgm_ctx {
     sgm_stats stats{};
     bool profiling = false;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t bin_stream = nullptr;  // binning of the next sub-batch overlaps the raster
+    cudaEvent_t ev_ready = nullptr;
+    cudaEvent_t ev_binned[2] = {nullptr, nullptr};
+    cudaEvent_t ev_r[16] = {};  // raster start/stop pairs of one group (profiling)
 
     // scratch
-    DevBuf poses, vcount, pcount, keys, vals, keys_alt, vals_alt, packed, counts, offsets;
+    DevBuf poses, vcount, pcount, keys, vals, keys_alt, vals_alt, packed, counts, offsets, rects;
     DevBuf tkeys, tvals, tkeys_alt, tvals_alt, ranges, ent_part, miss_part, views, out,
         contributors, cub_tmp, planes, dbg;
-    HostBuf h_counts, h_views, h_poses, h_out;
+    HostBuf h_counts, h_views, h_poses, h_out, h_stage;
+    DevBuf upload_tmp;
 
     // state of the last render (for sgm_last_*)
     bool last_valid = false;
@@ -188,23 +194,23 @@ struct RenderTargets {
 
 // Bins one view (step 3). Writes ranges / sorted list / packed into the per-view
 // slices and returns via the slice pointers. vals/keys hold the compacted (z, idx).
-void bin_view(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const OptParams& o,
-              const PoseParams* d_pose, double* keys, uint32_t* vals, uint32_t V, uint64_t P,
-              PackedSplat* packed, uint32_t* list, uint2* ranges, int bin_tiles) {
-    cudaStream_t s = ctx->stream;
+void bin_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const CamParams& cam,
+              const OptParams& o, const PoseParams* d_pose, uint32_t* keys, uint32_t* vals,
+              uint32_t V, uint64_t P, PackedSplat* packed, uint32_t* list, uint2* ranges,
+              int bin_tiles) {
     CK(cudaMemsetAsync(ranges, 0, sizeof(uint2) * bin_tiles, s));
     if (V == 0) return;
-    // K2: depth rank (fp64 radix sort; ties fixed below)
-    cub::DoubleBuffer<double> dk(keys, ctx->keys_alt.as<double>());
+    // K2: depth rank (radix sort on the monotone fp32 key; runs fixed below)
+    cub::DoubleBuffer<uint32_t> dk(keys, ctx->keys_alt.as<uint32_t>());
     cub::DoubleBuffer<uint32_t> dv(vals, ctx->vals_alt.as<uint32_t>());
     size_t tmp = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, V, 0, 64, s));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, V, 0, 32, s));
     CK(ctx->cub_tmp.reserve(tmp));
-    CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, dk, dv, V, 0, 64, s));
+    CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, dk, dv, V, 0, 32, s));
     ctx->stats.kernel_launches += 1;  // counted as one library sort call
     launch_tiefix(map->dev, d_pose, cam, o, dk.Current(), dv.Current(), V, s);
     launch_pack(map->dev, d_pose, cam, o, GroupParams{1, map->dev.C}, dv.Current(), V, packed,
-                ctx->counts.as<unsigned long long>(), s);
+                ctx->counts.as<unsigned long long>(), ctx->rects.as<int4>(), s);
     ctx->stats.kernel_launches += (V >= 2 ? 1 : 0) + 1;
     // keep the sorted indices for sgm_last_projections
     if (dv.Current() != vals) CK(cudaMemcpyAsync(vals, dv.Current(), 4ull * V, cudaMemcpyDeviceToDevice, s));
@@ -219,7 +225,7 @@ void bin_view(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const OptP
     ctx->stats.kernel_launches += 1;
     if (P == 0) return;
     uint32_t* tk = ctx->tkeys.as<uint32_t>();
-    launch_emit_pairs(map->dev, d_pose, cam, o, vals, off, V, tk, list, s);
+    launch_emit_pairs(off, ctx->rects.as<int4>(), V, P, o, tk, list, s);
     ctx->stats.kernel_launches += 1;
     cub::DoubleBuffer<uint32_t> pk(tk, ctx->tkeys_alt.as<uint32_t>());
     cub::DoubleBuffer<uint32_t> pv(list, ctx->tvals_alt.as<uint32_t>());
@@ -236,11 +242,13 @@ void bin_view(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const OptP
 }
 
 // Runs n views. Score mode writes n_missing/entropy_sum (host); render mode (n == 1)
-// writes planes to device targets.
+// writes planes to device targets. Binning of sub-batch i+1 (on ctx->bin_stream)
+// overlaps the raster of sub-batch i (on ctx->stream).
 void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const OptParams& o,
                uint64_t n, const PoseParams* poses, Mode mode, const RenderTargets& rt,
                double* h_missing, double* h_entropy) {
     cudaStream_t s = ctx->stream;
+    cudaStream_t sb = ctx->bin_stream;
     const uint64_t N = map->dev.n;
     const int bin_tiles = o.tiles_x * o.tiles_y;
     const int rtx = (cam.W + kTile - 1) / kTile;
@@ -249,7 +257,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
     ctx->last_valid = false;
 
     // batch size bounded by a scratch budget for the per-view N-sized arrays
-    const size_t per_view = std::max<uint64_t>(N, 1) * (8 + 4 + sizeof(PackedSplat)) +
+    const size_t per_view = std::max<uint64_t>(N, 1) * (4 + 4 + sizeof(PackedSplat)) +
                             static_cast<size_t>(bin_tiles) * sizeof(uint2) +
                             static_cast<size_t>(rtiles) * 12 + 256;
     const size_t budget = size_t(12) << 30;
@@ -261,9 +269,10 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
     CK(ctx->poses.reserve(sizeof(PoseParams) * B));
     CK(ctx->vcount.reserve(4 * B));
     CK(ctx->pcount.reserve(8 * B));
-    CK(ctx->keys.reserve(8 * NS * B));
+    CK(ctx->keys.reserve(4 * NS * B));
     CK(ctx->vals.reserve(4 * NS * B));
-    CK(ctx->keys_alt.reserve(8 * NS));
+    CK(ctx->keys_alt.reserve(4 * NS));
+    CK(ctx->rects.reserve(sizeof(int4) * NS));
     CK(ctx->vals_alt.reserve(4 * NS));
     CK(ctx->packed.reserve(sizeof(PackedSplat) * NS * B));
     CK(ctx->counts.reserve(8 * (NS + 1)));
@@ -279,6 +288,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
     CK(ctx->h_poses.reserve(sizeof(PoseParams) * B));
     CK(ctx->h_out.reserve(16 * B));
 
+    const int kSub = 8;  // views per raster launch (binning of the next 8 overlaps)
     for (uint64_t b0 = 0; b0 < n; b0 += B) {
         const int nb = static_cast<int>(std::min<uint64_t>(B, n - b0));
         if (ctx->profiling) CK(cudaEventRecord(ctx->ev[0], s));
@@ -288,7 +298,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
         CK(cudaMemsetAsync(ctx->vcount.p, 0, 4 * nb, s));
         CK(cudaMemsetAsync(ctx->pcount.p, 0, 8 * nb, s));
         CK(cudaMemsetAsync(ctx->contributors.p, 0, 8, s));
-        launch_preprocess(map->dev, ctx->poses.as<PoseParams>(), cam, o, nb, ctx->keys.as<double>(),
+        launch_preprocess(map->dev, ctx->poses.as<PoseParams>(), cam, o, nb, ctx->keys.as<uint32_t>(),
                           ctx->vals.as<uint32_t>(), NS, ctx->vcount.as<uint32_t>(),
                           ctx->pcount.as<unsigned long long>(), s);
         ctx->stats.kernel_launches += (N > 0) ? 1 : 0;
@@ -303,8 +313,8 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
             if (P[v] >= (1ull << 32)) fail(SGM_ERR_UNSUPPORTED, "view has %llu tile pairs (>= 2^32)",
                                           static_cast<unsigned long long>(P[v]));
 
-        // sub-batches by pair budget
-        const uint64_t pair_budget = (uint64_t(8) << 30) / 8;  // pairs (u32 key + u32 val)
+        // groups of views whose pair lists fit the budget together
+        const uint64_t pair_budget = (uint64_t(8) << 30) / 4;  // u32 list entries
         int v0 = 0;
         while (v0 < nb) {
             int v1 = v0;
@@ -318,22 +328,15 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
             CK(ctx->tkeys.reserve(4 * std::max<uint64_t>(maxP, 1)));
             CK(ctx->tkeys_alt.reserve(4 * std::max<uint64_t>(maxP, 1)));
             CK(ctx->tvals_alt.reserve(4 * std::max<uint64_t>(maxP, 1)));
+            // descriptors for the whole group (list offsets known from the counts)
             ViewDesc* hvd = ctx->h_views.as<ViewDesc>();
             uint64_t list_off = 0;
-            for (int v = v0; v < nb; ++v) {
-                if (v >= v1) break;
-                double* keys = ctx->keys.as<double>() + NS * v;
-                uint32_t* vals = ctx->vals.as<uint32_t>() + NS * v;
-                PackedSplat* packed = ctx->packed.as<PackedSplat>() + NS * v;
-                uint32_t* list = ctx->tvals.as<uint32_t>() + list_off;
-                uint2* ranges = ctx->ranges.as<uint2>() + static_cast<size_t>(bin_tiles) * v;
-                bin_view(ctx, map, cam, o, ctx->poses.as<PoseParams>() + v, keys, vals, V[v], P[v],
-                         packed, list, ranges, bin_tiles);
+            for (int v = v0; v < v1; ++v) {
                 ViewDesc d{};
-                d.order = vals;
-                d.ranges = ranges;
-                d.list = list;
-                d.packed = packed;
+                d.order = ctx->vals.as<uint32_t>() + NS * v;
+                d.ranges = ctx->ranges.as<uint2>() + static_cast<size_t>(bin_tiles) * v;
+                d.list = ctx->tvals.as<uint32_t>() + list_off;
+                d.packed = ctx->packed.as<PackedSplat>() + NS * v;
                 d.ent_partial = ctx->ent_part.as<double>() + static_cast<size_t>(rtiles) * v;
                 d.miss_partial = ctx->miss_part.as<uint32_t>() + static_cast<size_t>(rtiles) * v;
                 d.color = rt.color;
@@ -346,54 +349,81 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 ctx->stats.visible += V[v];
                 ctx->stats.pairs += P[v];
             }
-            const int nsub = v1 - v0;
-            CK(cudaMemcpyAsync(ctx->views.p, hvd, sizeof(ViewDesc) * nsub, cudaMemcpyHostToDevice, s));
-            if (ctx->profiling) CK(cudaEventRecord(ctx->ev[1], s));
+            const int ngroup = v1 - v0;
+            CK(cudaMemcpyAsync(ctx->views.p, hvd, sizeof(ViewDesc) * ngroup, cudaMemcpyHostToDevice, s));
+            // the binning stream starts after everything already queued on s
+            CK(cudaEventRecord(ctx->ev_ready, s));
+            CK(cudaStreamWaitEvent(sb, ctx->ev_ready, 0));
             RasterParams rp{};
             rp.map = map->dev;
             rp.cam = cam;
             rp.opt = o;
-            rp.views = ctx->views.as<ViewDesc>();
             rp.tiles_per_view = rtiles;
             rp.raster_tiles_x = rtx;
             rp.channels = rt.channels;
             rp.groups = map->groups;
-            if (mode == Mode::Score)
-                launch_raster_score(rp, nsub, s);
-            else
-                launch_raster_render(rp, nsub, s);
-            CK(cudaGetLastError());
-            ctx->stats.kernel_launches += 1;
-            ctx->stats.raster_launches += 1;
-            if (ctx->profiling) CK(cudaEventRecord(ctx->ev[2], s));
+            for (int s0 = v0; s0 < v1; s0 += kSub) {
+                const int s1 = std::min(v1, s0 + kSub);
+                for (int v = s0; v < s1; ++v) {
+                    const ViewDesc& d = hvd[v - v0];
+                    bin_view(ctx, sb, map, cam, o, ctx->poses.as<PoseParams>() + v,
+                             ctx->keys.as<uint32_t>() + NS * v, const_cast<uint32_t*>(d.order), V[v],
+                             P[v], const_cast<PackedSplat*>(d.packed), const_cast<uint32_t*>(d.list),
+                             const_cast<uint2*>(d.ranges), bin_tiles);
+                }
+                const int slot = (s0 / kSub) & 1;
+                CK(cudaEventRecord(ctx->ev_binned[slot], sb));
+                CK(cudaStreamWaitEvent(s, ctx->ev_binned[slot], 0));
+                rp.views = ctx->views.as<ViewDesc>() + (s0 - v0);
+                const int pr = ((s0 - v0) / kSub) % 8;  // profiling event pair
+                if (ctx->profiling) CK(cudaEventRecord(ctx->ev_r[2 * pr], s));
+                if (mode == Mode::Score)
+                    launch_raster_score(rp, s1 - s0, s);
+                else
+                    launch_raster_render(rp, s1 - s0, s);
+                CK(cudaGetLastError());
+                if (ctx->profiling) CK(cudaEventRecord(ctx->ev_r[2 * pr + 1], s));
+                ctx->stats.kernel_launches += 1;
+                ctx->stats.raster_launches += 1;
+            }
             if (mode == Mode::Score) {
-                launch_reduce_scores(ctx->views.as<ViewDesc>(), nsub, rtiles, ctx->out.as<double>(),
-                                     ctx->out.as<double>() + nsub, s);
+                launch_reduce_scores(ctx->views.as<ViewDesc>(), ngroup, rtiles, ctx->out.as<double>(),
+                                     ctx->out.as<double>() + ngroup, s);
                 ctx->stats.kernel_launches += 1;
                 double* ho = ctx->h_out.as<double>();
-                CK(cudaMemcpyAsync(ho, ctx->out.p, 16 * nsub, cudaMemcpyDeviceToHost, s));
+                CK(cudaMemcpyAsync(ho, ctx->out.p, 16 * ngroup, cudaMemcpyDeviceToHost, s));
+                unsigned long long* kc = hp + B;
+                CK(cudaMemcpyAsync(kc, ctx->contributors.p, 8, cudaMemcpyDeviceToHost, s));
+                CK(cudaMemsetAsync(ctx->contributors.p, 0, 8, s));
                 CK(cudaStreamSynchronize(s));
-                for (int v = 0; v < nsub; ++v) {
+                for (int v = 0; v < ngroup; ++v) {
                     h_missing[b0 + v0 + v] = ho[v];
-                    h_entropy[b0 + v0 + v] = ho[nsub + v];
+                    h_entropy[b0 + v0 + v] = ho[ngroup + v];
                 }
+                ctx->stats.contributors += *kc;
             } else {
+                unsigned long long* kc = hp + B;
+                CK(cudaMemcpyAsync(kc, ctx->contributors.p, 8, cudaMemcpyDeviceToHost, s));
+                CK(cudaMemsetAsync(ctx->contributors.p, 0, 8, s));
                 CK(cudaStreamSynchronize(s));
+                ctx->stats.contributors += *kc;
             }
             if (ctx->profiling) {
-                float a = 0, b = 0;
-                CK(cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]));
-                CK(cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]));
-                ctx->stats.binning_ms += a;
-                ctx->stats.raster_ms += b;
-                CK(cudaEventRecord(ctx->ev[0], s));
+                const int nsub = std::min(8, (ngroup + kSub - 1) / kSub);
+                for (int q = 0; q < nsub; ++q) {
+                    float ms = 0;
+                    CK(cudaEventElapsedTime(&ms, ctx->ev_r[2 * q], ctx->ev_r[2 * q + 1]));
+                    ctx->stats.raster_ms += ms;
+                }
             }
-            unsigned long long* kc = reinterpret_cast<unsigned long long*>(ctx->h_counts.as<char>() + 8 * B) + B;
-            CK(cudaMemcpyAsync(kc, ctx->contributors.p, 8, cudaMemcpyDeviceToHost, s));
-            CK(cudaMemsetAsync(ctx->contributors.p, 0, 8, s));
-            CK(cudaStreamSynchronize(s));
-            ctx->stats.contributors += *kc;
             v0 = v1;
+        }
+        if (ctx->profiling) {
+            CK(cudaEventRecord(ctx->ev[3], s));
+            CK(cudaEventSynchronize(ctx->ev[3]));
+            float total = 0;
+            CK(cudaEventElapsedTime(&total, ctx->ev[0], ctx->ev[3]));
+            ctx->stats.binning_ms += total;  // whole-batch span; raster share in raster_ms
         }
         ctx->stats.views += nb;
         if (mode == Mode::Render) {
@@ -482,7 +512,15 @@ int sgm_ctx_create(int device, sgm_ctx** out) {
     int rc = guard(ctx, [&] {
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        int prio_low = 0, prio_high = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high));
+        // binning kernels are small and latency-bound: give them priority so the
+        // block scheduler slots them in as raster CTAs of the previous sub-batch retire
+        CK(cudaStreamCreateWithPriority(&ctx->bin_stream, cudaStreamNonBlocking, prio_high));
         for (auto& ev : ctx->ev) CK(cudaEventCreate(&ev));
+        CK(cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming));
+        for (auto& ev : ctx->ev_binned) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        for (auto& ev : ctx->ev_r) CK(cudaEventCreate(&ev));
     });
     if (rc != SGM_OK) {
         g_create_error = ctx->err;
@@ -497,11 +535,18 @@ void sgm_ctx_destroy(sgm_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->bin_stream) cudaStreamSynchronize(ctx->bin_stream);
     for (auto& ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
-    cudaStream_t s = ctx->stream;
+    if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
+    for (auto& ev : ctx->ev_binned)
+        if (ev) cudaEventDestroy(ev);
+    for (auto& ev : ctx->ev_r)
+        if (ev) cudaEventDestroy(ev);
+    cudaStream_t s = ctx->stream, s2 = ctx->bin_stream;
     delete ctx;
     if (s) cudaStreamDestroy(s);
+    if (s2) cudaStreamDestroy(s2);
 }
 
 const char* sgm_last_error(const sgm_ctx* ctx) {
@@ -551,53 +596,76 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, con
             fail(SGM_ERR_INVALID, "map: null array with n > 0");
         if (n >= (1ull << 32)) fail(SGM_ERR_UNSUPPORTED, "map: more than 2^32-1 Gaussians");
         const int C = num_classes + 1;
+        const int kpad = (k + 7) / 8 * 8;
         m = new sgm_map();
         m->num_classes = num_classes;
         const size_t ns = std::max<uint64_t>(n, 1);
-        std::vector<double> geo(5 * ns, 0.0), col(4 * ns, 0.0);
-        for (uint64_t i = 0; i < n; ++i) {
-            geo[i] = centers[3 * i];
-            geo[ns + i] = centers[3 * i + 1];
-            geo[2 * ns + i] = centers[3 * i + 2];
-            geo[3 * ns + i] = std::exp(log_radii[i]);                      // radius()
-            geo[4 * ns + i] = 1.0 / (1.0 + std::exp(-opacity_logits[i]));  // sigmoid
-            for (int c = 0; c < 3; ++c) col[4 * i + c] = std::clamp(colors[3 * i + c], 0.0, 1.0);
-        }
-        // class ids < C and duplicate detection (duplicates force ordered RMWs)
-        int dup = 0;
-        std::vector<uint32_t> seen(static_cast<size_t>(C), 0xffffffffu);
-        for (uint64_t i = 0; i < n; ++i)
-            for (int j = 0; j < k; ++j) {
-                const uint16_t c = sem_indices[i * k + j];
-                if (c >= C)
-                    fail(SGM_ERR_INVALID, "map: semantic index %u >= channels %d (gaussian %llu)",
-                         c, C, static_cast<unsigned long long>(i));
-                if (seen[c] == static_cast<uint32_t>(i)) dup = 1;
-                seen[c] = static_cast<uint32_t>(i);
+        // pinned staging: geo SoA (5 ns), colour (4 ns), raw rows (k ns u16 + k ns f64)
+        const size_t geo_b = 8 * 5 * ns, col_b = 8 * 4 * ns, idx_b = 2 * static_cast<size_t>(k) * ns,
+                     prob_b = 8 * static_cast<size_t>(k) * ns;
+        CK(ctx->h_stage.reserve(geo_b + col_b + prob_b + idx_b + 64));
+        char* hs = ctx->h_stage.as<char>();
+        double* geo = reinterpret_cast<double*>(hs);
+        double* col = reinterpret_cast<double*>(hs + geo_b);
+        double* rprob = reinterpret_cast<double*>(hs + geo_b + col_b);
+        uint16_t* ridx = reinterpret_cast<uint16_t*>(hs + geo_b + col_b + prob_b);
+        // host side (reference libm, gaussian_map.hpp:36-37), split over threads
+        const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        const unsigned nth = n > 65536 ? hw : 1;
+        std::vector<int> bad(nth, -1), dup(nth, 0);
+        auto work = [&](unsigned w) {
+            const uint64_t a = n * w / nth, b = n * (w + 1) / nth;
+            std::vector<uint32_t> seen(static_cast<size_t>(C), 0xffffffffu);
+            for (uint64_t i = a; i < b; ++i) {
+                geo[i] = centers[3 * i];
+                geo[ns + i] = centers[3 * i + 1];
+                geo[2 * ns + i] = centers[3 * i + 2];
+                geo[3 * ns + i] = std::exp(log_radii[i]);                      // radius()
+                geo[4 * ns + i] = 1.0 / (1.0 + std::exp(-opacity_logits[i]));  // sigmoid
+                for (int c = 0; c < 3; ++c) col[4 * i + c] = std::clamp(colors[3 * i + c], 0.0, 1.0);
+                col[4 * i + 3] = 0.0;
+                for (int j = 0; j < k; ++j) {
+                    const uint16_t c = sem_indices[i * k + j];
+                    if (c >= C) {
+                        if (bad[w] < 0) bad[w] = static_cast<int>(i % 0x7fffffff);
+                        continue;
+                    }
+                    if (seen[c] == static_cast<uint32_t>(i)) dup[w] = 1;
+                    seen[c] = static_cast<uint32_t>(i);
+                }
             }
-        // rows sorted by class id (stable), padded to kpad with (0xffff, 0.0)
-        const int kpad = (k + 7) / 8 * 8;
-        std::vector<uint16_t> sidx(ns * kpad, 0xffff);
-        std::vector<double> sprob(ns * kpad, 0.0);
-        std::vector<int> perm(k);
-        for (uint64_t i = 0; i < n; ++i) {
-            const uint16_t* ri = sem_indices + i * k;
-            for (int j = 0; j < k; ++j) perm[j] = j;
-            std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return ri[a] < ri[b]; });
-            for (int j = 0; j < k; ++j) {
-                sidx[i * kpad + j] = ri[perm[j]];
-                sprob[i * kpad + j] = sem_probs[i * k + perm[j]];
-            }
+            std::memcpy(ridx + a * k, sem_indices + a * k, 2 * (b - a) * k);
+            std::memcpy(rprob + a * k, sem_probs + a * k, 8 * (b - a) * k);
+        };
+        if (nth == 1) {
+            work(0);
+        } else {
+            std::vector<std::thread> pool;
+            for (unsigned w = 0; w < nth; ++w) pool.emplace_back(work, w);
+            for (auto& th : pool) th.join();
         }
+        for (unsigned w = 0; w < nth; ++w)
+            if (bad[w] >= 0)
+                fail(SGM_ERR_INVALID, "map: semantic index >= channels %d (near gaussian %d)", C, bad[w]);
+        int has_dup = 0;
+        for (unsigned w = 0; w < nth; ++w) has_dup |= dup[w];
         cudaStream_t s = ctx->stream;
-        CK(m->geo.reserve(8 * geo.size()));
-        CK(m->color.reserve(8 * col.size()));
-        CK(m->idx.reserve(2 * sidx.size()));
-        CK(m->prob.reserve(8 * sprob.size()));
-        CK(cudaMemcpyAsync(m->geo.p, geo.data(), 8 * geo.size(), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(m->color.p, col.data(), 8 * col.size(), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(m->idx.p, sidx.data(), 2 * sidx.size(), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(m->prob.p, sprob.data(), 8 * sprob.size(), cudaMemcpyHostToDevice, s));
+        CK(m->geo.reserve(geo_b));
+        CK(m->color.reserve(col_b));
+        CK(m->idx.reserve(2 * ns * kpad));
+        CK(m->prob.reserve(8 * ns * kpad));
+        CK(ctx->upload_tmp.reserve(idx_b + prob_b + 64));
+        char* draw = ctx->upload_tmp.as<char>();
+        CK(cudaMemcpyAsync(m->geo.p, geo, geo_b, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(m->color.p, col, col_b, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(draw, rprob, prob_b, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(draw + prob_b, ridx, idx_b, cudaMemcpyHostToDevice, s));
+        // rows sorted by class id (stable) and padded to kpad, on the GPU
+        launch_sort_rows(reinterpret_cast<const uint16_t*>(draw + prob_b),
+                         reinterpret_cast<const double*>(draw), n, k, kpad, m->idx.as<uint16_t>(),
+                         m->prob.as<double>(), s);
+        ctx->stats.kernel_launches += n ? 1 : 0;
+        CK(cudaGetLastError());
         CK(cudaStreamSynchronize(s));
         DevMap& d = m->dev;
         d.n = n;
@@ -613,7 +681,7 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, con
         d.color4 = m->color.as<double>();
         d.sem_idx = m->idx.as<uint16_t>();
         d.sem_prob = m->prob.as<double>();
-        d.dup_idx = dup;
+        d.dup_idx = has_dup;
         m->groups = choose_groups(C, k);
         *out = m;
         m = nullptr;

@@ -103,18 +103,17 @@ struct RasterParams {
 
 // ---- launchers (sgm_kernels.cu) ----
 void launch_preprocess(const DevMap& m, const PoseParams* d_poses, const CamParams& cam,
-                       const OptParams& o, int n_views, double* keys, uint32_t* vals,
+                       const OptParams& o, int n_views, uint32_t* keys, uint32_t* vals,
                        size_t stride, uint32_t* vcount, unsigned long long* pcount,
                        cudaStream_t s);
 void launch_tiefix(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
-                   const OptParams& o, const double* z, uint32_t* idx, uint32_t V,
+                   const OptParams& o, const uint32_t* key, uint32_t* idx, uint32_t V,
                    cudaStream_t s);
 void launch_pack(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
                  const OptParams& o, const GroupParams& gp, const uint32_t* idx, uint32_t V,
-                 PackedSplat* packed, unsigned long long* counts, cudaStream_t s);
-void launch_emit_pairs(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
-                       const OptParams& o, const uint32_t* order,
-                       const unsigned long long* offsets, uint32_t V, uint32_t* tile_keys,
+                 PackedSplat* packed, unsigned long long* counts, int4* rects, cudaStream_t s);
+void launch_emit_pairs(const unsigned long long* offsets, const int4* rects, uint32_t V,
+                       unsigned long long P, const OptParams& o, uint32_t* tile_keys,
                        uint32_t* tile_vals, cudaStream_t s);
 void launch_ranges(const uint32_t* sorted_tiles, uint64_t P, uint2* ranges, cudaStream_t s);
 void launch_raster_score(const RasterParams& p, int n_views, cudaStream_t s);
@@ -126,6 +125,9 @@ void launch_debug_projections(const DevMap& m, const PoseParams* d_pose, const C
                               double* out6, cudaStream_t s);
 void launch_bins_to_ids(const uint32_t* list, uint64_t P, const PackedSplat* packed,
                         uint32_t* ids, float* probe3, cudaStream_t s);
+
+void launch_sort_rows(const uint16_t* idx, const double* prob, uint64_t n, int k, int kpad,
+                      uint16_t* out_idx, double* out_prob, cudaStream_t s);
 
 // sgm_raster.cu
 GroupParams choose_groups(int C, int k);

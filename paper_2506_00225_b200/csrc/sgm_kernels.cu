@@ -6,8 +6,10 @@
 // (which has no FMA: proj/CMakeLists.txt:3,8-10, default -march=x86-64).
 //
 //   K1 k_preprocess      project_splats transform/cull + tile count   splat_render.cpp:15-39, 205-209
-//   K2 (CUB radix sort on fp64 z) + k_tiefix (z, mx, my, alpha) order  splat_render.cpp:40-45
-//   K3 k_pack / k_emit / (CUB stable tile sort) / k_ranges             splat_render.cpp:189-213
+//   K2 CUB radix sort on the fp32-rounded depth (monotone) + k_tiefix: runs of
+//      equal fp32 keys re-sorted by the full fp64 (z, mx, my, alpha) key  splat_render.cpp:40-45
+//   K3 k_pack / k_emit_lb (load-balanced over pairs) / CUB stable tile sort / k_ranges
+//                                                                       splat_render.cpp:189-213
 //   K4/K5 raster: see sgm_raster.cu
 //   k_reduce_scores     deterministic per-view n_missing / entropy_sum   explorer.cpp:195-203
 #include <cfloat>
@@ -72,8 +74,14 @@ __device__ __forceinline__ unsigned long long rect_count(const Rect& r) {
 // ---------------------------------------------------------------- K1
 // grid (ceil(N/256), views). Compacts visible Gaussians per view (order is
 // arbitrary; the full-key sort below canonicalises it) and counts pairs.
+// Order-preserving map of a float to uint32 (negative values reversed).
+__device__ __forceinline__ uint32_t sortable(float f) {
+    const uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
 __global__ void __launch_bounds__(256) k_preprocess(DevMap m, const PoseParams* __restrict__ poses,
-                                                    CamParams cam, OptParams o, double* keys,
+                                                    CamParams cam, OptParams o, uint32_t* keys,
                                                     uint32_t* vals, size_t stride,
                                                     uint32_t* vcount,
                                                     unsigned long long* pcount) {
@@ -94,7 +102,7 @@ __global__ void __launch_bounds__(256) k_preprocess(DevMap m, const PoseParams* 
     }
     if (vis) {
         const uint32_t pos = base + __popc(mask & ((1u << lane) - 1u));
-        keys[v * stride + pos] = z;
+        keys[v * stride + pos] = sortable(static_cast<float>(z));  // monotone in z
         vals[v * stride + pos] = static_cast<uint32_t>(i);
     }
 #pragma unroll
@@ -103,41 +111,86 @@ __global__ void __launch_bounds__(256) k_preprocess(DevMap m, const PoseParams* 
 }
 
 // ---------------------------------------------------------------- K2 tie fix-up
-// After the radix sort on z, runs of equal z are re-ordered by (mx, my, alpha)
-// and finally map index (splat_render.cpp:40-45; index breaks exact 4-key ties,
-// which std::sort leaves unspecified).
-__device__ __forceinline__ bool proj_less(double amx, double amy, double aal, uint32_t ai,
-                                          double bmx, double bmy, double bal, uint32_t bi) {
-    if (amx != bmx) return amx < bmx;
-    if (amy != bmy) return amy < bmy;
-    if (aal != bal) return aal < bal;
-    return ai < bi;
+// The radix sort orders by fp32(z), which is monotone in z, so the exact order
+// (z, mx, my, alpha) of splat_render.cpp:40-45 only has to be restored inside
+// runs of equal fp32 keys (map index breaks exact 4-key ties, which std::sort
+// leaves unspecified). One thread per run: insertion sort for short runs,
+// heapsort for long ones (degenerate maps, e.g. a fronto-parallel plane).
+struct FullKey {
+    double z, mx, my, al;
+    uint32_t i;
+};
+
+__device__ __forceinline__ FullKey full_key(const DevMap& m, uint32_t i, const PoseParams& P,
+                                            const CamParams& cam, const OptParams& o) {
+    FullKey k;
+    double rad;
+    project(m, i, P, cam, o, k.mx, k.my, rad, k.z);
+    k.al = m.alpha[i];
+    k.i = i;
+    return k;
+}
+
+__device__ __forceinline__ bool key_less(const FullKey& a, const FullKey& b) {
+    if (a.z != b.z) return a.z < b.z;
+    if (a.mx != b.mx) return a.mx < b.mx;
+    if (a.my != b.my) return a.my < b.my;
+    if (a.al != b.al) return a.al < b.al;
+    return a.i < b.i;
 }
 
 __global__ void k_tiefix(DevMap m, const PoseParams* __restrict__ pose, CamParams cam, OptParams o,
-                         const double* __restrict__ z, uint32_t* idx, uint32_t V) {
+                         const uint32_t* __restrict__ key, uint32_t* idx, uint32_t V) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r + 1 >= V) return;
-    if (!(z[r] == z[r + 1])) return;
-    if (r > 0 && z[r - 1] == z[r]) return;  // not the head of the run
+    if (key[r] != key[r + 1]) return;
+    if (r > 0 && key[r - 1] == key[r]) return;  // not the head of the run
     uint32_t e = r + 1;
-    while (e < V && z[e] == z[r]) ++e;
-    // insertion sort idx[r, e) (runs are a handful of entries)
-    for (uint32_t a = r + 1; a < e; ++a) {
-        const uint32_t ia = idx[a];
-        double amx, amy, arad, az;
-        project(m, ia, *pose, cam, o, amx, amy, arad, az);
-        const double aal = m.alpha[ia];
-        uint32_t b = a;
-        while (b > r) {
-            const uint32_t ib = idx[b - 1];
-            double bmx, bmy, brad, bz;
-            project(m, ib, *pose, cam, o, bmx, bmy, brad, bz);
-            if (!proj_less(amx, amy, aal, ia, bmx, bmy, m.alpha[ib], ib)) break;
-            idx[b] = ib;
-            --b;
+    while (e < V && key[e] == key[r]) ++e;
+    const PoseParams P = *pose;
+    const uint32_t n = e - r;
+    uint32_t* a = idx + r;
+    if (n <= 32) {
+        for (uint32_t q = 1; q < n; ++q) {
+            const uint32_t iq = a[q];
+            const FullKey kq = full_key(m, iq, P, cam, o);
+            uint32_t b = q;
+            while (b > 0) {
+                const FullKey kb = full_key(m, a[b - 1], P, cam, o);
+                if (!key_less(kq, kb)) break;
+                a[b] = a[b - 1];
+                --b;
+            }
+            a[b] = iq;
         }
-        idx[b] = ia;
+        return;
+    }
+    // heapsort (max-heap) on a[0, n)
+    auto sift = [&](uint32_t root, uint32_t end) {
+        while (true) {
+            uint32_t child = 2 * root + 1;
+            if (child >= end) break;
+            FullKey kc = full_key(m, a[child], P, cam, o);
+            if (child + 1 < end) {
+                const FullKey k2 = full_key(m, a[child + 1], P, cam, o);
+                if (key_less(kc, k2)) {
+                    ++child;
+                    kc = k2;
+                }
+            }
+            if (!key_less(full_key(m, a[root], P, cam, o), kc)) break;
+            const uint32_t tmp = a[root];
+            a[root] = a[child];
+            a[child] = tmp;
+            root = child;
+        }
+    };
+    for (uint32_t s0 = n / 2; s0-- > 0;) sift(s0, n);
+    for (uint32_t end = n - 1; end > 0; --end) {
+        const uint32_t tmp = a[0];
+        a[0] = a[end];
+        a[end] = tmp;
+        sift(0, end);
     }
 }
 
@@ -145,7 +198,7 @@ __global__ void k_tiefix(DevMap m, const PoseParams* __restrict__ pose, CamParam
 // PackedSplat + Probe per depth rank (splat_render.cpp:191-204) and tile counts.
 __global__ void k_pack(DevMap m, const PoseParams* __restrict__ pose, CamParams cam, OptParams o,
                        GroupParams gp, const uint32_t* __restrict__ idx, uint32_t V,
-                       PackedSplat* packed, unsigned long long* counts) {
+                       PackedSplat* packed, unsigned long long* counts, int4* rects) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= V) return;
     const uint32_t i = idx[r];
@@ -175,30 +228,48 @@ __global__ void k_pack(DevMap m, const PoseParams* __restrict__ pose, CamParams 
     }
     ps.aux = aux;
     packed[r] = ps;
-    counts[r] = rect_count(tile_rect(mx, my, rad, o));
+    const Rect rc = tile_rect(mx, my, rad, o);
+    counts[r] = rect_count(rc);
+    rects[r] = make_int4(rc.tx0, rc.ty0, rc.tx1 - rc.tx0 + 1, rc.ty1 - rc.ty0 + 1);
 }
 
 // Emits (bin, rank) pairs in rank order at the scanned offsets; a stable sort on
 // the bin key then yields every bin in depth order (:210-212). rad_px is not kept
 // in PackedSplat (64 B); the rectangle is re-derived by re-projecting, which is
 // bit-identical to the count pass.
-__global__ void k_emit2(DevMap m, const PoseParams* __restrict__ pose, CamParams cam, OptParams o,
-                        const uint32_t* __restrict__ order,
-                        const unsigned long long* __restrict__ offsets, uint32_t V,
-                        uint32_t* tile_keys, uint32_t* tile_vals) {
-    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= V) return;
-    unsigned long long at = offsets[r];
-    if (at == offsets[r + 1]) return;
-    double mx, my, rad, z;
-    project(m, order[r], *pose, cam, o, mx, my, rad, z);
-    const Rect rc = tile_rect(mx, my, rad, o);
-    for (int ty = rc.ty0; ty <= rc.ty1; ++ty)
-        for (int tx = rc.tx0; tx <= rc.tx1; ++tx) {
-            tile_keys[at] = static_cast<uint32_t>(ty * o.tiles_x + tx);
-            tile_vals[at] = r;
-            ++at;
+// Load-balanced: each thread emits kPerThread consecutive pairs. The first
+// pair's rank comes from a binary search over the scanned counts; then the
+// thread walks forward (pairs of one rank are contiguous).
+constexpr int kPerThread = 8;
+__global__ void k_emit_lb(const unsigned long long* __restrict__ offsets, const int4* __restrict__ rects,
+                          uint32_t V, unsigned long long P, int tiles_x, uint32_t* tile_keys,
+                          uint32_t* tile_vals) {
+    const unsigned long long i0 =
+        (static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x) * kPerThread;
+    if (i0 >= P) return;
+    // largest r with offsets[r] <= i0
+    uint32_t lo = 0, hi = V;  // offsets[V] == P > i0
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) / 2;
+        if (offsets[mid] <= i0) lo = mid; else hi = mid;
+    }
+    uint32_t r = lo;
+    unsigned long long beg = offsets[r], end = offsets[r + 1];
+    int4 rc = rects[r];
+    const unsigned long long i1 = min(P, i0 + kPerThread);
+    for (unsigned long long i = i0; i < i1; ++i) {
+        while (i >= end) {
+            ++r;
+            beg = end;
+            end = offsets[r + 1];
+            rc = rects[r];
         }
+        const uint32_t j = static_cast<uint32_t>(i - beg);
+        const uint32_t dy = j / static_cast<uint32_t>(rc.z);
+        const uint32_t dx = j - dy * static_cast<uint32_t>(rc.z);
+        tile_keys[i] = static_cast<uint32_t>((rc.y + static_cast<int>(dy)) * tiles_x + rc.x + static_cast<int>(dx));
+        tile_vals[i] = r;
+    }
 }
 
 __global__ void k_ranges(const uint32_t* __restrict__ keys, uint64_t P, uint2* ranges) {
@@ -271,6 +342,33 @@ __global__ void k_bins_to_ids(const uint32_t* __restrict__ list, uint64_t P,
     }
 }
 
+// Class-sorts each Gaussian's sparse row (stable insertion sort: a Gaussian
+// listing a class twice keeps their order) and pads it to kpad with
+// (0xffff, 0.0). Per-class addition order in the compositor is unchanged.
+__global__ void k_sort_rows(const uint16_t* __restrict__ idx, const double* __restrict__ prob,
+                            uint64_t n, int k, int kpad, uint16_t* out_idx, double* out_prob) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint16_t* oi = out_idx + i * kpad;
+    double* op = out_prob + i * kpad;
+    for (int j = 0; j < k; ++j) {
+        const uint16_t c = idx[i * k + j];
+        const double pv = prob[i * k + j];
+        int q = j;
+        while (q > 0 && oi[q - 1] > c) {
+            oi[q] = oi[q - 1];
+            op[q] = op[q - 1];
+            --q;
+        }
+        oi[q] = c;
+        op[q] = pv;
+    }
+    for (int j = k; j < kpad; ++j) {
+        oi[j] = 0xffff;
+        op[j] = 0.0;
+    }
+}
+
 inline unsigned blocks_for(uint64_t n, unsigned threads) {
     return static_cast<unsigned>((n + threads - 1) / threads);
 }
@@ -279,7 +377,7 @@ inline unsigned blocks_for(uint64_t n, unsigned threads) {
 
 // ---------------------------------------------------------------- launchers
 void launch_preprocess(const DevMap& m, const PoseParams* d_poses, const CamParams& cam,
-                       const OptParams& o, int n_views, double* keys, uint32_t* vals,
+                       const OptParams& o, int n_views, uint32_t* keys, uint32_t* vals,
                        size_t stride, uint32_t* vcount, unsigned long long* pcount,
                        cudaStream_t s) {
     if (m.n == 0 || n_views == 0) return;
@@ -288,26 +386,26 @@ void launch_preprocess(const DevMap& m, const PoseParams* d_poses, const CamPara
 }
 
 void launch_tiefix(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
-                   const OptParams& o, const double* z, uint32_t* idx, uint32_t V,
+                   const OptParams& o, const uint32_t* key, uint32_t* idx, uint32_t V,
                    cudaStream_t s) {
     if (V < 2) return;
-    k_tiefix<<<blocks_for(V, 256), 256, 0, s>>>(m, d_pose, cam, o, z, idx, V);
+    k_tiefix<<<blocks_for(V, 256), 256, 0, s>>>(m, d_pose, cam, o, key, idx, V);
 }
 
 void launch_pack(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
                  const OptParams& o, const GroupParams& gp, const uint32_t* idx, uint32_t V,
-                 PackedSplat* packed, unsigned long long* counts, cudaStream_t s) {
+                 PackedSplat* packed, unsigned long long* counts, int4* rects, cudaStream_t s) {
     if (V == 0) return;
-    k_pack<<<blocks_for(V, 256), 256, 0, s>>>(m, d_pose, cam, o, gp, idx, V, packed, counts);
+    k_pack<<<blocks_for(V, 256), 256, 0, s>>>(m, d_pose, cam, o, gp, idx, V, packed, counts, rects);
 }
 
-void launch_emit_pairs(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
-                       const OptParams& o, const uint32_t* order,
-                       const unsigned long long* offsets, uint32_t V, uint32_t* tile_keys,
+void launch_emit_pairs(const unsigned long long* offsets, const int4* rects, uint32_t V,
+                       unsigned long long P, const OptParams& o, uint32_t* tile_keys,
                        uint32_t* tile_vals, cudaStream_t s) {
-    if (V == 0) return;
-    k_emit2<<<blocks_for(V, 128), 128, 0, s>>>(m, d_pose, cam, o, order, offsets, V, tile_keys,
-                                               tile_vals);
+    if (V == 0 || P == 0) return;
+    const unsigned long long threads = (P + kPerThread - 1) / kPerThread;
+    k_emit_lb<<<blocks_for(threads, 256), 256, 0, s>>>(offsets, rects, V, P, o.tiles_x, tile_keys,
+                                                       tile_vals);
 }
 
 void launch_ranges(const uint32_t* sorted_tiles, uint64_t P, uint2* ranges, cudaStream_t s) {
@@ -326,6 +424,12 @@ void launch_debug_projections(const DevMap& m, const PoseParams* d_pose, const C
                               double* out6, cudaStream_t s) {
     if (V == 0) return;
     k_debug_projections<<<blocks_for(V, 256), 256, 0, s>>>(m, d_pose, cam, o, idx, V, out6);
+}
+
+void launch_sort_rows(const uint16_t* idx, const double* prob, uint64_t n, int k, int kpad,
+                      uint16_t* out_idx, double* out_prob, cudaStream_t s) {
+    if (n == 0) return;
+    k_sort_rows<<<blocks_for(n, 256), 256, 0, s>>>(idx, prob, n, k, kpad, out_idx, out_prob);
 }
 
 void launch_bins_to_ids(const uint32_t* list, uint64_t P, const PackedSplat* packed,

@@ -263,3 +263,25 @@ def test_cfg1_full_size_properties(ctx, orc):
     h = np.array([sgm.clipped_entropy(out.sem[i * out.channels:(i + 1) * out.channels])
                   for i in range(0, cam.pixel_count(), 997)])
     assert np.all(h > 0) and np.all(h <= math.log(out.channels) + 1e-12)
+
+
+def test_fronto_parallel_plane_long_depth_run(ctx, orc):
+    """300 Gaussians at one exact depth: a single run of equal depth keys far longer
+    than the insertion-sort limit (heapsort path of k_tiefix)."""
+    cam = CameraModel(64, 48, 0, 0, 50.0, 50.0, 32.0, 24.0)
+    rng = np.random.default_rng(12)
+    n = 300
+    centers = np.stack([rng.uniform(-0.6, 0.6, n), rng.uniform(-0.45, 0.45, n), np.full(n, 1.25)],
+                       axis=1)
+    centers[::7, :2] = centers[1::7, :2][: len(centers[::7])]  # some exact (z, mx, my) ties too
+    gm = sgm.GaussianMap.from_arrays(3, 6, centers, np.full(n, -3.0), rng.normal(0, 1, n),
+                                     rng.uniform(0, 1, (n, 3)),
+                                     np.stack([rng.choice(7, 3, replace=False) for _ in range(n)]),
+                                     rng.dirichlet(np.ones(3), n))
+    out = sgm.render(gm, cam, Pose(), ctx=ctx)
+    assert_projections(out, orc.project(gm, cam, Pose()))
+    assert_planes(out, orc.render(gm, cam, Pose(), 7))
+    nm, es = sgm.score_poses(gm, cam, [Pose()], ctx=ctx)
+    nm_o, es_o, _ = orc.score_views(gm, cam, [Pose()])
+    assert nm[0] == nm_o[0]
+    np.testing.assert_allclose(es, es_o, rtol=ENT_RTOL)
