@@ -326,10 +326,19 @@ class RefLib:
                "sem": np.zeros(px * C_) if channels & 4 else None}
         proj = np.zeros((max(n, 1), 6))
         nproj = C.c_uint64()
+        ncon = C.c_uint64()
+        off = np.zeros(px + 1, dtype=np.uint32) if channels & 8 else None
+        cap = px * max(n, 1) if channels & 8 else 0
+        con = np.zeros(max(cap, 1), dtype=np.uint32) if channels & 8 else None
         self.lib.ref_render(h, which, wh.ctypes.data_as(_pi32), _dp(intr), _dp(R), _dp(t),
                             channels, _dp(o), _dp(out["color"]), _dp(out["depth"]),
                             _dp(out["silhouette"]), _dp(out["sem"]), _dp(proj), C.byref(nproj),
-                            None, None, 0, None)
+                            None if off is None else off.ctypes.data_as(_pu32),
+                            None if con is None else con.ctypes.data_as(_pu32), cap,
+                            C.byref(ncon))
+        if channels & 8:
+            out["contrib_offset"] = off
+            out["contrib"] = con[:ncon.value].copy()
         p6 = proj[:nproj.value]
         arr = np.zeros(nproj.value, dtype=PROJ_DTYPE)
         for i, f in enumerate(["mx", "my", "rad_px", "z", "alpha"]):

@@ -125,7 +125,10 @@ struct sgm_ctx {
     // scratch
     DevBuf poses, vcount, pcount, keys, vals, keys_alt, vals_alt, packed, counts, offsets, rects;
     DevBuf tkeys, tvals, tkeys_alt, tvals_alt, ranges, ent_part, miss_part, views, out,
-        contributors, cub_tmp, planes, dbg;
+        contributors, cub_tmp, planes, dbg, ccount, coffset, contrib;
+    uint64_t last_ncontrib = 0;
+    bool last_has_contrib = false;
+    int last_px = 0;
     HostBuf h_counts, h_views, h_poses, h_out, h_stage;
     DevBuf upload_tmp;
 
@@ -190,6 +193,9 @@ struct RenderTargets {
     double* sil = nullptr;
     double* sem = nullptr;
     uint32_t channels = 0;
+    uint32_t* contrib = nullptr;            // retain_contributors
+    uint32_t* contrib_count = nullptr;      // pass 1
+    const unsigned long long* contrib_offset = nullptr;  // pass 2
 };
 
 // Bins one view (step 3). Writes ranges / sorted list / packed into the per-view
@@ -344,6 +350,9 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 d.sil = rt.sil;
                 d.sem = rt.sem;
                 d.contributors = ctx->contributors.as<unsigned long long>();
+                d.contrib = rt.contrib;
+                d.contrib_count = rt.contrib_count;
+                d.contrib_offset = rt.contrib_offset;
                 hvd[v - v0] = d;
                 list_off += P[v];
                 ctx->stats.visible += V[v];
@@ -467,8 +476,6 @@ void do_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const
     need_ctx(ctx);
     if (!map) fail(SGM_ERR_INVALID, "map is null");
     if (!pose) fail(SGM_ERR_INVALID, "pose is null");
-    if (channels & SGM_RETAIN_CONTRIBUTORS)
-        fail(SGM_ERR_UNSUPPORTED, "retain_contributors is not served by this build yet");
     const CamParams cam = to_cam(camera);
     const OptParams o = to_opt(opt, cam);
     const PoseParams p = to_pose(*pose);
@@ -478,7 +485,41 @@ void do_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const
     rt.depth = (channels & SGM_DEPTH) ? d_depth : nullptr;
     rt.sem = (channels & SGM_SEMANTICS) ? d_sem : nullptr;
     rt.sil = d_sil;
-    run_views(ctx, map, cam, o, 1, &p, Mode::Render, rt, nullptr, nullptr);
+    ctx->last_has_contrib = false;
+    if (channels & SGM_RETAIN_CONTRIBUTORS) {
+        // pass 1: per-pixel contributor counts (splat_render.cpp:215-216, 310)
+        const size_t px = static_cast<size_t>(cam.W) * cam.H;
+        CK(ctx->ccount.reserve(4 * (px + 1)));
+        CK(ctx->coffset.reserve(8 * (px + 1)));
+        CK(ctx->contrib.reserve(4));
+        CK(cudaMemsetAsync(ctx->ccount.p, 0, 4 * (px + 1), ctx->stream));
+        rt.contrib = ctx->contrib.as<uint32_t>();
+        rt.contrib_count = ctx->ccount.as<uint32_t>();
+        run_views(ctx, map, cam, o, 1, &p, Mode::Render, rt, nullptr, nullptr);
+        // offsets = exclusive scan (flatten_contributors, :125-137)
+        size_t tmp = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ctx->ccount.as<uint32_t>(),
+                                         ctx->coffset.as<unsigned long long>(), px + 1, ctx->stream));
+        CK(ctx->cub_tmp.reserve(tmp));
+        CK(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp, ctx->ccount.as<uint32_t>(),
+                                         ctx->coffset.as<unsigned long long>(), px + 1, ctx->stream));
+        ctx->stats.kernel_launches += 1;
+        unsigned long long total = 0;
+        CK(cudaMemcpyAsync(&total, ctx->coffset.as<unsigned long long>() + px, 8,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (total >= (1ull << 32)) fail(SGM_ERR_UNSUPPORTED, "more than 2^32 contributors");
+        CK(ctx->contrib.reserve(4 * std::max<unsigned long long>(total, 1)));
+        // pass 2: write the depth-ordered contributor ranks
+        rt.contrib = ctx->contrib.as<uint32_t>();
+        rt.contrib_offset = ctx->coffset.as<unsigned long long>();
+        run_views(ctx, map, cam, o, 1, &p, Mode::Render, rt, nullptr, nullptr);
+        ctx->last_ncontrib = total;
+        ctx->last_has_contrib = true;
+        ctx->last_px = static_cast<int>(px);
+    } else {
+        run_views(ctx, map, cam, o, 1, &p, Mode::Render, rt, nullptr, nullptr);
+    }
     if (n_proj) *n_proj = ctx->last_V;
 }
 
@@ -804,10 +845,28 @@ int sgm_last_bins(sgm_ctx* ctx, uint32_t* tile_offsets, uint32_t* ids, float* pr
     });
 }
 
-int sgm_last_contributors(sgm_ctx* ctx, uint32_t*, uint32_t*, uint64_t, uint64_t*) {
+int sgm_last_contributors(sgm_ctx* ctx, uint32_t* offsets, uint32_t* contrib, uint64_t capacity,
+                          uint64_t* n_contrib) {
     return guard(ctx, [&] {
         need_ctx(ctx);
-        fail(SGM_ERR_UNSUPPORTED, "retain_contributors is not served by this build yet");
+        if (!ctx->last_valid || !ctx->last_has_contrib)
+            fail(SGM_ERR_INVALID, "no retained contributors (render with SGM_RETAIN_CONTRIBUTORS)");
+        const uint64_t total = ctx->last_ncontrib;
+        if (n_contrib) *n_contrib = total;
+        const size_t px = static_cast<size_t>(ctx->last_px);
+        if (offsets) {
+            std::vector<unsigned long long> off(px + 1);
+            CK(cudaMemcpyAsync(off.data(), ctx->coffset.p, 8 * (px + 1), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            for (size_t i = 0; i <= px; ++i) offsets[i] = static_cast<uint32_t>(off[i]);
+        }
+        if (contrib && total) {
+            if (capacity < total) fail(SGM_ERR_INVALID, "capacity < %llu contributors",
+                                       static_cast<unsigned long long>(total));
+            CK(cudaMemcpyAsync(contrib, ctx->contrib.p, 4 * total, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+        }
     });
 }
 

@@ -63,7 +63,7 @@ struct __align__(16) PackedSplat {
     double alpha;
     double z;
     float pmx, pmy, pcut;
-    uint32_t aux;  // channel-group boundaries (u8 x 4) of the sparse row
+    uint32_t aux;  // depth rank (projection id) of this record
 };
 static_assert(sizeof(PackedSplat) == 64, "PackedSplat must stay 64 B");
 
@@ -88,6 +88,11 @@ struct ViewDesc {
     double* sil;
     double* sem;
     unsigned long long* contributors;  // K counter
+    // retain_contributors (render mode): pass 1 counts per pixel into contrib_count
+    // (contrib_offset == null); pass 2 writes depth ranks at contrib_offset[pixel]
+    uint32_t* contrib;
+    uint32_t* contrib_count;
+    const unsigned long long* contrib_offset;
 };
 
 struct RasterParams {

@@ -199,6 +199,7 @@ __global__ void k_tiefix(DevMap m, const PoseParams* __restrict__ pose, CamParam
 __global__ void k_pack(DevMap m, const PoseParams* __restrict__ pose, CamParams cam, OptParams o,
                        GroupParams gp, const uint32_t* __restrict__ idx, uint32_t V,
                        PackedSplat* packed, unsigned long long* counts, int4* rects) {
+    (void)gp;
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= V) return;
     const uint32_t i = idx[r];
@@ -214,18 +215,7 @@ __global__ void k_pack(DevMap m, const PoseParams* __restrict__ pose, CamParams 
     ps.pmx = static_cast<float>(mx);  // :201
     ps.pmy = static_cast<float>(my);  // :202
     ps.pcut = static_cast<float>(ps.cutoff_d2 * (1.0 + 1e-5)) + 1e-6f;  // :203
-    // channel-group boundaries of this Gaussian's (channel-sorted) sparse row:
-    // byte g-1 = #entries with class < g * Cg, for g = 1..P-1
-    uint32_t aux = 0;
-    if (gp.P > 1) {
-        const uint16_t* row = m.sem_idx + static_cast<size_t>(i) * m.kpad;
-        for (int g = 1; g < gp.P; ++g) {
-            const int lim = g * gp.Cg;
-            uint32_t c = 0;
-            for (int j = 0; j < m.k; ++j) c += row[j] < lim ? 1u : 0u;
-            aux |= (c & 0xffu) << (8 * (g - 1));
-        }
-    }
+    const uint32_t aux = r;  // depth rank (contributor id)
     ps.aux = aux;
     packed[r] = ps;
     const Rect rc = tile_rect(mx, my, rad, o);

@@ -247,6 +247,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     double ac0 = 0.0, ac1 = 0.0, ac2 = 0.0, adep = 0.0;
     bool done = !inside;
     unsigned long long contrib = 0;
+    uint32_t ncontrib_px = 0;  // retain_contributors: this pixel's list length so far
+    const size_t pix_t = inside ? static_cast<size_t>(y) * p.cam.W + x : 0;
     const int e_first = t >> 6;  // phase A: this thread's entries e_first + 4i
 
     for (int b = 0; b < nbatch; ++b) {
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
             for (int i = 0; i < kNB / 4; ++i) {
                 const int e = e_first + 4 * i;
                 if (e >= n) break;
-                double f = 0.0;
+                double f = -1.0;  // not a contributor
                 if (!pdone) {
                     const float4 pf = *reinterpret_cast<const float4*>(&sp[e].pmx);
                     const float fdx = fpx - pf.x;
@@ -280,7 +282,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
                         if (!(d2 > sp[e].cutoff_d2)) {  // :283
                             f = sp[e].alpha * exp_footprint(-d2 * sp[e].inv_two_r2);  // :284
                             if (f > kMaxFootprint) f = kMaxFootprint;                 // :285
-                            // a contributor with f == 0 (alpha == 0) changes nothing
                         }
                     }
                 }
@@ -295,12 +296,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
             for (int e = 0; e < n; ++e) {
                 const int s = pair_slot(e, 32, t);
                 const double f = W[s];
-                if (done || f == 0.0) {
+                if (done || f < 0.0) {
                     W[s] = 0.0;
                     continue;
                 }
                 const double w = f * T;
                 W[s] = w;
+                if (kRender && vd.contrib) {  // retain_contributors (:310): depth ranks in order
+                    if (vd.contrib_offset)
+                        vd.contrib[vd.contrib_offset[pix_t] + ncontrib_px] = sp[e].aux;
+                    ++ncontrib_px;
+                }
                 if (kRender) {
                     ac0 += scol[4 * e] * w;  // :289-291 (colour clamped at upload)
                     ac1 += scol[4 * e + 1] * w;
@@ -392,6 +398,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
                 vd.color[pix * 3 + 2] = ac2;
             }
             if (vd.depth) vd.depth[pix] = adep;
+            if (vd.contrib && !vd.contrib_offset) vd.contrib_count[pix] = ncontrib_px;
         }
         if (vd.sem) {
             for (int l = t; l < kTilePx * C; l += kThreads) {

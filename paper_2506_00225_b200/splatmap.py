@@ -513,6 +513,15 @@ def render(gmap: GaussianMap, camera: CameraModel, pose: Pose,
         c.check(N.lib.sgm_last_projections(
             c.handle, proj.ctypes.data_as(C.POINTER(N.sgm_projection)), nproj.value))
     out.projections = proj
+    if ch.retain_contributors:  # RenderOutput.contrib / contrib_offset (:125-137)
+        ncon = C.c_uint64()
+        c.check(N.lib.sgm_last_contributors(c.handle, None, None, 0, C.byref(ncon)))
+        out.contrib_offset = np.zeros(px + 1, dtype=np.uint32)
+        con = np.zeros(max(ncon.value, 1), dtype=np.uint32)
+        c.check(N.lib.sgm_last_contributors(
+            c.handle, out.contrib_offset.ctypes.data_as(C.POINTER(C.c_uint32)),
+            con.ctypes.data_as(C.POINTER(C.c_uint32)), ncon.value, C.byref(ncon)))
+        out.contrib = con[:ncon.value]
     return out
 
 

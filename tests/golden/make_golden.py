@@ -60,7 +60,7 @@ def main() -> None:
     store = {}
     scenes = []
 
-    def add_scene(name, gmap, cam, pose, opts: RenderOptions, channels=7):
+    def add_scene(name, gmap, cam, pose, opts: RenderOptions, channels=15):
         out = ref.render(gmap, cam, pose, channels=channels, opt=opts)
         pre = f"{name}/"
         store[pre + "centers"] = gmap.centers
@@ -76,8 +76,8 @@ def main() -> None:
         store[pre + "opts"] = np.array([1.0 if opts.early_exit else 0.0, opts.transmittance_eps,
                                         opts.z_near, opts.truncation_sigmas, opts.tile_size])
         store[pre + "channels"] = np.array([channels])
-        for key in ("silhouette", "color", "depth", "sem"):
-            if out[key] is not None:
+        for key in ("silhouette", "color", "depth", "sem", "contrib", "contrib_offset"):
+            if out.get(key) is not None:
                 store[pre + key] = out[key]
         store[pre + "projections"] = out["projections"]
         store[pre + "entropy"] = ref.render_entropy(gmap, cam, pose, opts)

@@ -71,6 +71,29 @@ def test_render_matches_reference_golden(ctx, orc, golden, name):
     np.testing.assert_allclose(h, outs["entropy"], rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("name", ["kM_11", "tiled_91", "early_55", "noearly_55", "perm_19",
+                                  "score_8", "saturated"])
+def test_retained_contributors_match_reference(ctx, golden, name):
+    """RenderOutput.contrib / contrib_offset (splat_render.cpp:215-216, 310, 125-137)."""
+    gm, cam, pose, opts, _, outs = golden_scene(golden, name)
+    out = sgm.render(gm, cam, pose, RenderChannels.all(True), opts, ctx=ctx)
+    np.testing.assert_array_equal(out.contrib_offset, outs["contrib_offset"])
+    np.testing.assert_array_equal(out.contrib, outs["contrib"])
+    assert_planes(out, outs)
+
+
+def test_retained_contributors_random_vs_reference(ctx, ref):
+    cam = CameraModel(77, 53, 0, 0, 61.0, 59.5, 38.3, 26.1)
+    pose = look_at([0.2, -0.1, -0.4], [0.0, 0.2, 2.5])
+    gm = random_map(21, 500, cam, pose, k=4, num_classes=9)
+    gm.opacity_logits[::17] = -1e4  # alpha == 0 contributors stay in the lists
+    for opts in (RenderOptions(), RenderOptions(early_exit=False)):
+        out = sgm.render(gm, cam, pose, RenderChannels.all(True), opts, ctx=ctx)
+        r = ref.render(gm, cam, pose, 15, opts)
+        np.testing.assert_array_equal(out.contrib_offset, r["contrib_offset"])
+        np.testing.assert_array_equal(out.contrib, r["contrib"])
+
+
 def test_reference_kats_on_gpu(ctx, golden):
     gm, cam, pose, opts, _, _ = golden_scene(golden, "saturated")
     out = sgm.render(gm, cam, pose, ctx=ctx)
