@@ -164,6 +164,20 @@ int sgm_score_views(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam, uin
 int sgm_score_candidates(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam, uint64_t n,
                          const sgm_candidate* cands, const sgm_options* opt,
                          double* n_missing, double* entropy_sum);
+/* ---- Fisher-information gain (extension; no reference counterpart) ----
+ * Diagonal Fisher information of the rendered colour and depth with respect to each
+ * Gaussian's theta = (mu_x, mu_y, mu_z, log_radius, opacity_logit, c_r, c_g, c_b): the
+ * per-pixel Jacobian of the analytic chain in proj/src/losses.cpp:242-335, chained to world
+ * space per pixel and squared, summed over pixels and the R, G, B, depth channels.
+ * sgm_fisher_prior: H_prior = sum over the n past poses (kept with the map); optional host
+ * copy H_out [N][8]. sgm_score_views_fisher: per view n_missing, entropy_sum and the
+ * FisherRF-style gain  sum_{i,theta} H_view / (H_prior + lambda)  (deterministic). */
+int sgm_fisher_prior(sgm_ctx* ctx, sgm_map* map, const sgm_camera* cam, uint64_t n,
+                     const sgm_pose* poses, const sgm_options* opt, double lambda, double* H_out);
+int sgm_score_views_fisher(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam, uint64_t n,
+                           const sgm_pose* poses, const sgm_options* opt, double* n_missing,
+                           double* entropy_sum, double* fisher_gain);
+
 /* combine_scores (explorer.cpp:225-248) on host fp64: returns 1 if any i_total > 0,
  * 0 if the pool is exhausted (or n == 0), negative on invalid arguments. */
 int sgm_combine_scores(uint64_t n, const double* n_missing, const double* entropy_sum,

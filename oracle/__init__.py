@@ -161,6 +161,33 @@ class Oracle:
         L.orc_candidate_pose.argtypes = [_pd, _pd, C.POINTER(orc_pose)]
         L.orc_look_at.restype = None
         L.orc_look_at.argtypes = [_pd, _pd, C.POINTER(orc_pose)]
+        L.orc_fisher_accumulate.restype = C.c_int
+        L.orc_fisher_accumulate.argtypes = [C.POINTER(orc_map), C.POINTER(orc_camera), C.c_uint64,
+                                            C.POINTER(orc_pose), C.POINTER(orc_options), _pd]
+        L.orc_fisher_gain.restype = C.c_int
+        L.orc_fisher_gain.argtypes = [C.POINTER(orc_map), C.POINTER(orc_camera), C.c_uint64,
+                                      C.POINTER(orc_pose), C.POINTER(orc_options), _pd,
+                                      C.c_double, _pd]
+
+    def fisher_accumulate(self, m, cam, poses, opt=None) -> np.ndarray:
+        """Fisher diagonal summed over `poses`: (N, 8) = (mu xyz, log_r, logit, rgb)."""
+        ma = _MapArrays(m)
+        H = np.zeros((max(ma.n, 1), 8))
+        arr = (orc_pose * max(len(poses), 1))(*[_pose(p) for p in poses])
+        cm, cc, co = ma.c(), _cam(cam), _opts(opt)
+        assert self.lib.orc_fisher_accumulate(C.byref(cm), C.byref(cc), len(poses), arr,
+                                              C.byref(co), _dp(H)) == 0
+        return H[:ma.n]
+
+    def fisher_gain(self, m, cam, poses, H_prior, lam, opt=None) -> np.ndarray:
+        ma = _MapArrays(m)
+        Hp = np.ascontiguousarray(H_prior, dtype=np.float64)
+        g = np.zeros(len(poses))
+        arr = (orc_pose * max(len(poses), 1))(*[_pose(p) for p in poses])
+        cm, cc, co = ma.c(), _cam(cam), _opts(opt)
+        assert self.lib.orc_fisher_gain(C.byref(cm), C.byref(cc), len(poses), arr, C.byref(co),
+                                        _dp(Hp), float(lam), _dp(g)) == 0
+        return g
 
     def project(self, m, cam, pose, opt=None) -> np.ndarray:
         ma = _MapArrays(m)

@@ -506,3 +506,153 @@ void orc_candidate_pose(const double pos[3], const double dir[3], orc_pose* out)
     const double target[3] = {pos[0] + dir[0], pos[1] + dir[1], pos[2] + dir[2]};
     orc_look_at(pos, target, out);
 }
+
+/* ---- Fisher-information extension ---- */
+
+/* J^2 contributions of every contributor of one pixel, in depth order. `sink(i, th, v)`
+ * receives v = sum over the 4 channels of (dR_ch/dtheta_i)^2 for theta = th. */
+typedef void (*fisher_sink)(void* ctx, uint32_t map_index, int theta, double v);
+
+static void fisher_pixel(const view_t* s, const orc_map* map, const orc_camera* cam,
+                         const orc_pose* pose, const orc_options* opt, uint32_t b0, uint32_t b1,
+                         int x, int y, fisher_sink sink, void* sctx, uint32_t* ids, double* fs,
+                         double* ts, unsigned char* clamped) {
+    const double px = x + 0.5, py = y + 0.5;
+    const float pxf = (float)px, pyf = (float)py;
+    /* forward: the contributor sequence exactly as composite() (splat_render.cpp:275-313) */
+    uint32_t n = 0;
+    double T = 1.0, Rc[4] = {0, 0, 0, 0};
+    for (uint32_t b = b0; b < b1; ++b) {
+        const float fdx = pxf - s->probe3[3 * (uint64_t)b];
+        const float fdy = pyf - s->probe3[3 * (uint64_t)b + 1];
+        if (fdx * fdx + fdy * fdy > s->probe3[3 * (uint64_t)b + 2]) continue;
+        const uint32_t pid = s->ids[b];
+        const orc_proj* p = &s->proj[pid];
+        const double dx = px - p->mx, dy = py - p->my;
+        const double d2 = dx * dx + dy * dy;
+        if (d2 > s->cutoff_d2[pid]) continue;
+        double f = p->alpha * exp(-d2 * s->inv_two_r2[pid]);
+        clamped[n] = f > K_MAX_FOOTPRINT;
+        if (f > K_MAX_FOOTPRINT) f = K_MAX_FOOTPRINT;
+        const double w = f * T;
+        const double* c = &map->colors[(uint64_t)p->index * 3];
+        for (int ch = 0; ch < 3; ++ch) Rc[ch] += clampd(c[ch], 0.0, 1.0) * w;
+        Rc[3] += p->z * w;
+        ids[n] = pid;
+        fs[n] = f;
+        ts[n] = T;
+        ++n;
+        T *= (1.0 - f);
+        if (opt->early_exit && T < opt->transmittance_eps) break;
+    }
+    /* per contributor: dR/df with S = R - P (inclusive prefix), losses.cpp:285-288 */
+    double P[4] = {0, 0, 0, 0};
+    const double* R = pose->R;
+    for (uint32_t j = 0; j < n; ++j) {
+        const orc_proj* p = &s->proj[ids[j]];
+        const double f = fs[j], Tj = ts[j], w = f * Tj;
+        const double* craw = &map->colors[(uint64_t)p->index * 3];
+        double v[4];
+        for (int ch = 0; ch < 3; ++ch) v[ch] = clampd(craw[ch], 0.0, 1.0);
+        v[3] = p->z;
+        double Jsq[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const double dx = px - p->mx, dy = py - p->my;
+        const double r = p->rad_px, r2 = r * r;
+        for (int ch = 0; ch < 4; ++ch) {
+            P[ch] += v[ch] * w;
+            const double S = Rc[ch] - P[ch];
+            const double dRdf = v[ch] * Tj - S / (1.0 - f);
+            double g_a = 0, g_mx = 0, g_my = 0, g_r = 0;
+            if (!clamped[j] && r > 0.0) { /* losses.cpp:297-304 */
+                g_a = dRdf * f / p->alpha;
+                g_mx = dRdf * f * dx / r2;
+                g_my = dRdf * f * dy / r2;
+                g_r = dRdf * f * (dx * dx + dy * dy) / (r2 * r);
+            }
+            const double g_z = ch == 3 ? w : 0.0; /* depth channel: dD/dz = w */
+            /* projection -> world, losses.cpp:323-334 */
+            const double dX = g_mx * cam->fx / p->z;
+            const double dY = g_my * cam->fy / p->z;
+            const double dZ = g_z - g_mx * (p->mx - cam->cx) / p->z - g_my * (p->my - cam->cy) / p->z -
+                              g_r * r / p->z;
+            for (int a = 0; a < 3; ++a) {
+                const double dw = R[3 * a] * dX + R[3 * a + 1] * dY + R[3 * a + 2] * dZ;
+                Jsq[a] += dw * dw;
+            }
+            const double jl = g_r * r; /* d/d log_r = g_r * rad_px, :333 */
+            const double jo = g_a * p->alpha * (1.0 - p->alpha); /* :334 */
+            Jsq[3] += jl * jl;
+            Jsq[4] += jo * jo;
+            if (ch < 3 && craw[ch] > 0.0 && craw[ch] < 1.0) Jsq[5 + ch] += w * w; /* :291-294 */
+        }
+        for (int th = 0; th < 8; ++th) sink(sctx, p->index, th, Jsq[th]);
+    }
+}
+
+typedef struct {
+    double* H;
+} acc_ctx_t;
+static void sink_acc(void* ctx, uint32_t i, int th, double v) {
+    ((acc_ctx_t*)ctx)->H[8 * (uint64_t)i + th] += v;
+}
+
+typedef struct {
+    const double* Hp;
+    double lambda;
+    double sum;
+} gain_ctx_t;
+static void sink_gain(void* ctx, uint32_t i, int th, double v) {
+    gain_ctx_t* g = (gain_ctx_t*)ctx;
+    g->sum += v / (g->Hp[8 * (uint64_t)i + th] + g->lambda);
+}
+
+static int fisher_view(const orc_map* map, const orc_camera* cam, const orc_pose* pose,
+                       const orc_options* opt, fisher_sink sink, void* sctx) {
+    view_t s;
+    if (view_prepare(&s, map, cam, pose, opt)) {
+        view_free(&s);
+        return -1;
+    }
+    const uint64_t cap = s.v + 1;
+    uint32_t* ids = (uint32_t*)malloc(cap * sizeof(uint32_t));
+    double* fs = (double*)malloc(cap * sizeof(double));
+    double* ts = (double*)malloc(cap * sizeof(double));
+    unsigned char* cl = (unsigned char*)malloc(cap);
+    const int ts_ = opt->tile_size, W = cam->width, H = cam->height;
+    for (int ty = 0; ty < s.tiles_y; ++ty)
+        for (int tx = 0; tx < s.tiles_x; ++tx) {
+            const uint64_t tile = (uint64_t)ty * s.tiles_x + tx;
+            const uint32_t b0 = s.offsets[tile], b1 = s.offsets[tile + 1];
+            if (b0 == b1) continue;
+            const int y1 = H < (ty + 1) * ts_ ? H : (ty + 1) * ts_;
+            const int x1 = W < (tx + 1) * ts_ ? W : (tx + 1) * ts_;
+            for (int y = ty * ts_; y < y1; ++y)
+                for (int x = tx * ts_; x < x1; ++x)
+                    fisher_pixel(&s, map, cam, pose, opt, b0, b1, x, y, sink, sctx, ids, fs, ts, cl);
+        }
+    free(ids);
+    free(fs);
+    free(ts);
+    free(cl);
+    view_free(&s);
+    return 0;
+}
+
+int orc_fisher_accumulate(const orc_map* map, const orc_camera* cam, uint64_t n_views,
+                          const orc_pose* poses, const orc_options* opt, double* H) {
+    acc_ctx_t a = {H};
+    for (uint64_t v = 0; v < n_views; ++v)
+        if (fisher_view(map, cam, &poses[v], opt, sink_acc, &a)) return -1;
+    return 0;
+}
+
+int orc_fisher_gain(const orc_map* map, const orc_camera* cam, uint64_t n_views,
+                    const orc_pose* poses, const orc_options* opt, const double* H_prior,
+                    double lambda, double* gain) {
+    for (uint64_t v = 0; v < n_views; ++v) {
+        gain_ctx_t g = {H_prior, lambda, 0.0};
+        if (fisher_view(map, cam, &poses[v], opt, sink_gain, &g)) return -1;
+        gain[v] = g.sum;
+    }
+    return 0;
+}

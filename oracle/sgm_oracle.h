@@ -97,6 +97,20 @@ int orc_combine_scores(uint64_t n, const double* n_missing, const double* entrop
                        const double* pos3, const double cur[3], double* i_geo, double* i_sem,
                        double* i_total);
 
+/* Fisher-information extension (no reference counterpart). Parameters per
+ * Gaussian, theta = (mu_x, mu_y, mu_z, log_radius, opacity_logit, c_r, c_g, c_b). Rendered
+ * channels ch = (R, G, B, depth). The per-pixel Jacobian dR_ch/dtheta restates the analytic
+ * chain of proj/src/losses.cpp:242-335 with unit seeds per channel (suffix sums formed as
+ * S_j = R - P_j from the inclusive prefix P_j), chained to world space per pixel BEFORE squaring:
+ *   H[8 i + theta] += sum_px sum_ch (dR_ch(px) / dtheta_i)^2
+ * orc_fisher_accumulate adds the diagonal of all n poses into H (8 N doubles).
+ * orc_fisher_gain returns per view  sum_{px,i,theta} J^2 / (H_prior[8 i + theta] + lambda). */
+int orc_fisher_accumulate(const orc_map* map, const orc_camera* cam, uint64_t n_views,
+                          const orc_pose* poses, const orc_options* opt, double* H);
+int orc_fisher_gain(const orc_map* map, const orc_camera* cam, uint64_t n_views,
+                    const orc_pose* poses, const orc_options* opt, const double* H_prior,
+                    double lambda, double* gain);
+
 /* CandidatePose::camera_pose() = look_at(p, p + d), explorer.hpp:105 + geometry.hpp:44-56. */
 void orc_candidate_pose(const double pos[3], const double dir[3], orc_pose* out);
 void orc_look_at(const double pos[3], const double target[3], orc_pose* out);

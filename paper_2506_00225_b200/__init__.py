@@ -21,6 +21,7 @@ from .splatmap import (  # noqa: F401
     clipped_entropy,
     combine_scores,
     deg_to_rad,
+    fisher_prior,
     look_at,
     prune_pool,
     refresh_candidate_scores,
@@ -29,5 +30,6 @@ from .splatmap import (  # noqa: F401
     render_reference,
     score_candidates,
     score_poses,
+    score_poses_fisher,
     sigmoid,
 )

@@ -104,6 +104,8 @@ struct sgm_map {
     DevMap dev;
     GroupParams groups{1, 1};
     int num_classes = 0;
+    DevBuf fisher_H, fisher_invp;  // Fisher prior (sgm_fisher_prior)
+    bool has_prior = false;
     DevBuf geo;    // cx, cy, cz, rad, alpha (5 x n doubles)
     DevBuf color;  // [n][4]
     DevBuf idx;    // [n][k] u16
@@ -125,7 +127,7 @@ struct sgm_ctx {
     // scratch
     DevBuf poses, vcount, pcount, keys, vals, keys_alt, vals_alt, packed, counts, offsets, rects;
     DevBuf tkeys, tvals, tkeys_alt, tvals_alt, ranges, ent_part, miss_part, views, out,
-        contributors, cub_tmp, planes, dbg, ccount, coffset, contrib;
+        contributors, cub_tmp, planes, dbg, ccount, coffset, contrib, fis_part;
     uint64_t last_ncontrib = 0;
     bool last_has_contrib = false;
     int last_px = 0;
@@ -186,6 +188,7 @@ unsigned tile_bits(uint64_t tiles) {
 }
 
 enum class Mode { Score, Render };
+enum class Fisher { None, Prior, Gain };
 
 struct RenderTargets {
     double* color = nullptr;
@@ -252,7 +255,8 @@ void bin_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const CamParams&
 // overlaps the raster of sub-batch i (on ctx->stream).
 void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const OptParams& o,
                uint64_t n, const PoseParams* poses, Mode mode, const RenderTargets& rt,
-               double* h_missing, double* h_entropy) {
+               double* h_missing, double* h_entropy, Fisher fk = Fisher::None,
+               double* h_fisher = nullptr, double* d_H = nullptr) {
     cudaStream_t s = ctx->stream;
     cudaStream_t sb = ctx->bin_stream;
     const uint64_t N = map->dev.n;
@@ -287,12 +291,13 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
     CK(ctx->ent_part.reserve(8ull * rtiles * B));
     CK(ctx->miss_part.reserve(4ull * rtiles * B));
     CK(ctx->views.reserve(sizeof(ViewDesc) * B));
-    CK(ctx->out.reserve(16 * B));
+    CK(ctx->out.reserve(24 * B));
+    if (fk == Fisher::Gain) CK(ctx->fis_part.reserve(8ull * rtiles * B));
     CK(ctx->contributors.reserve(8));
     CK(ctx->h_counts.reserve(16 * B + 8));
     CK(ctx->h_views.reserve(sizeof(ViewDesc) * B));
     CK(ctx->h_poses.reserve(sizeof(PoseParams) * B));
-    CK(ctx->h_out.reserve(16 * B));
+    CK(ctx->h_out.reserve(24 * B));
 
     const int kSub = 8;  // views per raster launch (binning of the next 8 overlaps)
     for (uint64_t b0 = 0; b0 < n; b0 += B) {
@@ -340,6 +345,9 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
             for (int v = v0; v < v1; ++v) {
                 ViewDesc d{};
                 d.order = ctx->vals.as<uint32_t>() + NS * v;
+                d.pose = ctx->poses.as<PoseParams>() + v;
+                d.fis_partial = fk == Fisher::Gain ? ctx->fis_part.as<double>() + static_cast<size_t>(rtiles) * v
+                                                   : nullptr;
                 d.ranges = ctx->ranges.as<uint2>() + static_cast<size_t>(bin_tiles) * v;
                 d.list = ctx->tvals.as<uint32_t>() + list_off;
                 d.packed = ctx->packed.as<PackedSplat>() + NS * v;
@@ -386,21 +394,33 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 rp.views = ctx->views.as<ViewDesc>() + (s0 - v0);
                 const int pr = ((s0 - v0) / kSub) % 8;  // profiling event pair
                 if (ctx->profiling) CK(cudaEventRecord(ctx->ev_r[2 * pr], s));
-                if (mode == Mode::Score)
-                    launch_raster_score(rp, s1 - s0, s);
-                else
-                    launch_raster_render(rp, s1 - s0, s);
+                FisherParams fp{};
+                fp.H = d_H;
+                fp.invp = map->fisher_invp.as<double>();
+                if (fk == Fisher::Prior) {
+                    launch_fisher_prior(rp, fp, s1 - s0, s);
+                } else {
+                    if (mode == Mode::Score)
+                        launch_raster_score(rp, s1 - s0, s);
+                    else
+                        launch_raster_render(rp, s1 - s0, s);
+                    if (fk == Fisher::Gain) {
+                        launch_fisher_gain(rp, fp, s1 - s0, s);
+                        ctx->stats.kernel_launches += 1;
+                    }
+                }
                 CK(cudaGetLastError());
                 if (ctx->profiling) CK(cudaEventRecord(ctx->ev_r[2 * pr + 1], s));
                 ctx->stats.kernel_launches += 1;
                 ctx->stats.raster_launches += 1;
             }
-            if (mode == Mode::Score) {
+            if (mode == Mode::Score && fk != Fisher::Prior) {
+                double* dfis = fk == Fisher::Gain ? ctx->out.as<double>() + 2 * ngroup : nullptr;
                 launch_reduce_scores(ctx->views.as<ViewDesc>(), ngroup, rtiles, ctx->out.as<double>(),
-                                     ctx->out.as<double>() + ngroup, s);
+                                     ctx->out.as<double>() + ngroup, dfis, s);
                 ctx->stats.kernel_launches += 1;
                 double* ho = ctx->h_out.as<double>();
-                CK(cudaMemcpyAsync(ho, ctx->out.p, 16 * ngroup, cudaMemcpyDeviceToHost, s));
+                CK(cudaMemcpyAsync(ho, ctx->out.p, 24 * ngroup, cudaMemcpyDeviceToHost, s));
                 unsigned long long* kc = hp + B;
                 CK(cudaMemcpyAsync(kc, ctx->contributors.p, 8, cudaMemcpyDeviceToHost, s));
                 CK(cudaMemsetAsync(ctx->contributors.p, 0, 8, s));
@@ -408,6 +428,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 for (int v = 0; v < ngroup; ++v) {
                     h_missing[b0 + v0 + v] = ho[v];
                     h_entropy[b0 + v0 + v] = ho[ngroup + v];
+                    if (h_fisher) h_fisher[b0 + v0 + v] = ho[2 * ngroup + v];
                 }
                 ctx->stats.contributors += *kc;
             } else {
@@ -901,6 +922,51 @@ int sgm_score_views(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, 
         for (uint64_t i = 0; i < n; ++i) pp[i] = to_pose(poses[i]);
         run_views(ctx, map, cam, o, n, pp.data(), Mode::Score, RenderTargets{}, n_missing,
                   entropy_sum);
+    });
+}
+
+int sgm_fisher_prior(sgm_ctx* ctx, sgm_map* map, const sgm_camera* camera, uint64_t n,
+                     const sgm_pose* poses, const sgm_options* opt, double lambda, double* H_out) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!map) fail(SGM_ERR_INVALID, "map is null");
+        if (n > 0 && !poses) fail(SGM_ERR_INVALID, "poses are null");
+        if (!(lambda > 0.0)) fail(SGM_ERR_INVALID, "lambda must be > 0");
+        const CamParams cam = to_cam(camera);
+        const OptParams o = to_opt(opt, cam);
+        const size_t nh = 8 * std::max<uint64_t>(map->dev.n, 1);
+        CK(map->fisher_H.reserve(8 * nh));
+        CK(map->fisher_invp.reserve(8 * nh));
+        CK(cudaMemsetAsync(map->fisher_H.p, 0, 8 * nh, ctx->stream));
+        std::vector<PoseParams> pp(n);
+        for (uint64_t i = 0; i < n; ++i) pp[i] = to_pose(poses[i]);
+        if (n) run_views(ctx, map, cam, o, n, pp.data(), Mode::Score, RenderTargets{}, nullptr, nullptr,
+                         Fisher::Prior, nullptr, map->fisher_H.as<double>());
+        launch_fisher_invp(map->fisher_H.as<double>(), lambda, 8 * map->dev.n, map->fisher_invp.as<double>(),
+                           ctx->stream);
+        ctx->stats.kernel_launches += 1;
+        if (H_out && map->dev.n)
+            CK(cudaMemcpyAsync(H_out, map->fisher_H.p, 64 * map->dev.n, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        map->has_prior = true;
+    });
+}
+
+int sgm_score_views_fisher(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, uint64_t n,
+                           const sgm_pose* poses, const sgm_options* opt, double* n_missing,
+                           double* entropy_sum, double* fisher_gain) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!map) fail(SGM_ERR_INVALID, "map is null");
+        if (!map->has_prior) fail(SGM_ERR_INVALID, "no Fisher prior (call sgm_fisher_prior first)");
+        if (n == 0) return;
+        if (!poses || !n_missing || !entropy_sum || !fisher_gain) fail(SGM_ERR_INVALID, "null argument");
+        const CamParams cam = to_cam(camera);
+        const OptParams o = to_opt(opt, cam);
+        std::vector<PoseParams> pp(n);
+        for (uint64_t i = 0; i < n; ++i) pp[i] = to_pose(poses[i]);
+        run_views(ctx, map, cam, o, n, pp.data(), Mode::Score, RenderTargets{}, n_missing, entropy_sum,
+                  Fisher::Gain, fisher_gain, nullptr);
     });
 }
 

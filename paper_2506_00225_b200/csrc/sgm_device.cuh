@@ -1,0 +1,88 @@
+// Device helpers shared by the raster (sgm_raster.cu) and Fisher (sgm_fisher.cu) kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sgm {
+namespace {
+
+// exp(x) for the footprint argument x = -d2 / (2 r^2) in [-cut^2/2, 0]:
+// Cody-Waite reduction by ln 2 and a degree-13 Taylor polynomial (|r| <= ln2/2,
+// truncation < 2.5e-16 relative). Coefficients live in the constant bank so the
+// DFMAs take them as operands (no 64-bit immediate moves).
+static __constant__ double c_exp[16] = {
+    1.4426950408889634,      // log2(e)
+    0.6931467056274414,      // ln2 hi (low 32 mantissa bits zero: k * hi is exact)
+    4.7493250390941725e-07,  // ln2 lo
+    1.6059043836821613e-10,  // 1/13!
+    2.08767569878681e-09,    // 1/12!
+    2.505210838544172e-08,   // 1/11!
+    2.755731922398589e-07,   // 1/10!
+    2.7557319223985893e-06,  // 1/9!
+    2.48015873015873e-05,    // 1/8!
+    0.0001984126984126984,   // 1/7!
+    0.001388888888888889,    // 1/6!
+    0.008333333333333333,    // 1/5!
+    0.041666666666666664,    // 1/4!
+    0.16666666666666666,     // 1/3!
+    0.5,                     // 1/2!
+    1.0};
+
+__device__ __forceinline__ double exp_footprint(double x) {
+    if (x < -700.0) return 0.0;  // (outside the footprint range; keeps the scaling valid)
+    const double shifter = 6755399441055744.0;  // 1.5 * 2^52: round-to-int in the low word
+    const double t = __fma_rn(x, c_exp[0], shifter);
+    const double kf = t - shifter;
+    const int k = __double2loint(t);
+    double r = __fma_rn(-kf, c_exp[1], x);
+    r = __fma_rn(-kf, c_exp[2], r);
+    double p = c_exp[3];
+#pragma unroll
+    for (int i = 4; i < 15; ++i) p = __fma_rn(p, r, c_exp[i]);
+    p = __fma_rn(p, r, 1.0);
+    p = __fma_rn(p, r, 1.0);
+    // scale by 2^k (k >= -1011 here, so the result stays normal)
+    return __hiloint2double(__double2hiint(p) + k * (1 << 20), __double2loint(p));
+}
+
+// log(x) for normal x > 0 (the epilogue's clamped probabilities, [1e-3, 1]):
+// x = m 2^e, m in [1,2); c = RN(1 / centre of m's 1/128 interval); r = m c - 1
+// (|r| <= 2^-8, exact-ish via FMA); log x = e ln2 - log c + log1p(r) with a
+// degree-7 series. ~1e-16 absolute error; ~16 instructions.
+static __device__ const double2 g_logtab[128] = {
+#include "sgm_logtab.inc"
+};
+static __constant__ double c_log[10] = {0.14285714285714285,  -0.16666666666666666, 0.2, -0.25,
+                                 0.3333333333333333,   -0.5,                 1.0,
+                                 0.6931467056274414,   4.7493250390941725e-07, 0.0};
+
+__device__ __forceinline__ double log_table(double x) {
+    const int hi = __double2hiint(x);
+    const int lo = __double2loint(x);
+    const double e = static_cast<double>((hi >> 20) - 1023);
+    const int i = (hi >> 13) & 0x7f;
+    const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+    const double2 tc = __ldg(&g_logtab[i]);
+    const double r = __fma_rn(m, tc.x, -1.0);
+    double q = c_log[0];
+#pragma unroll
+    for (int j = 1; j < 7; ++j) q = __fma_rn(q, r, c_log[j]);
+    const double l1p = q * r;
+    return __fma_rn(e, c_log[7], tc.y + __fma_rn(e, c_log[8], l1p));
+}
+
+__device__ __forceinline__ double clamp_prob(double v) {
+    // std::clamp(v, 0.001, 1.0) (splat_render.cpp:362)
+    return v < 0.001 ? 0.001 : (1.0 < v ? 1.0 : v);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+}  // namespace
+}  // namespace sgm

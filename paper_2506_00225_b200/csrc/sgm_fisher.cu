@@ -1,0 +1,319 @@
+// K6 / K7: diagonal Fisher information of the rendered colour and depth with respect to
+// the Gaussian parameters, accumulated through the blend (new feature, no
+// reference counterpart; parity pinned by finite differences of the oracle renderer).
+//
+// Parameters per Gaussian: theta = (mu_x, mu_y, mu_z, log_radius, opacity_logit, c_r, c_g,
+// c_b); channels: R, G, B, depth. The per-pixel Jacobian is the analytic chain of
+// proj/src/losses.cpp:242-335 with a unit seed per channel, chained to world space per
+// pixel before squaring:  H[i][theta] += sum_px sum_ch (dR_ch(px)/dtheta_i)^2.
+//
+// One CTA (8 warps) = one 8x8 block of one view; two passes over the block's depth-ordered
+// list (same cp.async staging as the raster):
+//   pass 0  phase A footprints, phase B transmittance chain -> rendered R_ch per pixel
+//   pass 1  phase A again; phase B: dR_ch/df_j = v_ch T_j - S_ch / (1 - f_j) with the suffix
+//           S = R - P_j (P_j the inclusive prefix, so no reverse sweep is needed); phase C
+//           (all 8 warps, 4 (Gaussian, pixel) pairs per thread): the 8 squared Jacobians,
+//           warp-reduced over pixels, then
+//             prior mode: one fp64 RED per (Gaussian, parameter, tile) into H
+//             gain mode : sum_theta H_tile[theta] / (H_prior[theta] + lambda) folded into a
+//                         per-tile partial in fixed order (deterministic per-view gain).
+#include "sgm_device.cuh"
+#include "sgm_internal.h"
+
+namespace sgm {
+
+namespace {
+
+constexpr int kFThreads = 256;
+constexpr int kFNB = 16;
+
+struct FLayout {
+    int f, dr, w, red, gacc, emap, rm, done, stage0, stage_bytes, st_color, total;
+};
+
+__host__ __device__ inline FLayout fisher_layout() {
+    FLayout L;
+    L.f = 0;                                  // [kFNB][64] footprint code
+    L.dr = L.f + kFNB * kTilePx * 8;          // [4][kFNB][64] dR/df
+    L.w = L.dr + 4 * kFNB * kTilePx * 8;      // [kFNB][64] w
+    L.red = L.w + kFNB * kTilePx * 8;         // [kFNB][2][8] per-half J^2 sums
+    L.gacc = L.red + kFNB * 2 * 8 * 8;        // [kFNB][8] gain terms
+    L.emap = L.gacc + kFNB * 8 * 8;           // [2][kFNB] map index
+    L.rm = L.emap + 2 * kFNB * 4;             // [2][kFNB] (rank, map index)
+    L.done = L.rm + 2 * kFNB * 8;             // [64]
+    L.stage0 = L.done + kTilePx * 4;
+    L.st_color = kFNB * static_cast<int>(sizeof(PackedSplat));
+    L.stage_bytes = L.st_color + kFNB * 32;
+    L.total = L.stage0 + 2 * L.stage_bytes;
+    return L;
+}
+
+// footprint codes in the f array
+constexpr double kNotContrib = -1.0;
+constexpr double kClamped = -2.0;
+
+template <bool kGain>
+__global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherParams fp) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const FLayout L = fisher_layout();
+    double* F = reinterpret_cast<double*>(smem + L.f);
+    double* DR = reinterpret_cast<double*>(smem + L.dr);
+    double* Wv = reinterpret_cast<double*>(smem + L.w);
+    double* red = reinterpret_cast<double*>(smem + L.red);
+    double* gacc = reinterpret_cast<double*>(smem + L.gacc);
+    uint32_t* emap = reinterpret_cast<uint32_t*>(smem + L.emap);
+    uint2* rm = reinterpret_cast<uint2*>(smem + L.rm);
+    int* sdone = reinterpret_cast<int*>(smem + L.done);
+    unsigned char* stg = smem + L.stage0;
+
+    const ViewDesc vd = p.views[blockIdx.y];
+    const int tile = blockIdx.x;
+    const int bx = tile % p.raster_tiles_x, by = tile / p.raster_tiles_x;
+    const int t = threadIdx.x;
+    const int lane = t & 31;
+    const int px = t & (kTilePx - 1);
+    const int x = bx * kTile + (px & (kTile - 1));
+    const int y = by * kTile + px / kTile;
+    const bool inside = x < p.cam.W && y < p.cam.H;
+    const int bin = ((by * kTile) / p.opt.ts) * p.opt.tiles_x + (bx * kTile) / p.opt.ts;
+    const uint2 rg = vd.ranges[bin];
+    const uint32_t L0 = rg.x;
+    const uint32_t Ln = rg.y - rg.x;
+    const int nbatch = static_cast<int>((Ln + kFNB - 1) / kFNB);
+    const double dpx = x + 0.5, dpy = y + 0.5;
+    const float fpx = static_cast<float>(dpx), fpy = static_cast<float>(dpy);
+    const int e_first = t >> 6;
+
+    constexpr int Q = 4 + 2;  // 16-byte chunks per Gaussian: PackedSplat + colour
+    auto issue = [&](int b) {
+        unsigned char* sb = stg + (b & 1) * L.stage_bytes;
+        const int n = min(kFNB, static_cast<int>(Ln) - b * kFNB);
+        const uint2* slot = rm + (b & 1) * kFNB;
+        for (int c = t; c < n * Q; c += kFThreads) {
+            const int e = c / Q;
+            const int q = c - e * Q;
+            const uint2 v = slot[e];
+            const unsigned char* src;
+            unsigned char* dst;
+            if (q < 4) {
+                src = reinterpret_cast<const unsigned char*>(vd.packed + v.x) + 16 * q;
+                dst = sb + e * 64 + 16 * q;
+                if (q == 0) emap[(b & 1) * kFNB + e] = v.y;
+            } else {
+                src = reinterpret_cast<const unsigned char*>(p.map.color4 + static_cast<size_t>(v.y) * 4) + 16 * (q - 4);
+                dst = sb + L.st_color + e * 32 + 16 * (q - 4);
+            }
+            const unsigned sdst = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst), "l"(src) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    auto fetch_rm = [&](int b, int slot) {
+        if (t < kFNB) {
+            const uint32_t q = static_cast<uint32_t>(b) * kFNB + t;
+            if (q < Ln) {
+                const uint32_t r = vd.list[L0 + q];
+                rm[slot * kFNB + t] = make_uint2(r, vd.order[r]);
+            }
+        }
+    };
+
+    double Rc[4] = {0.0, 0.0, 0.0, 0.0};  // pass 0 result (threads t < 64)
+    double gsum = 0.0;                     // gain of this tile (thread 0, fixed order)
+
+    for (int pass = 0; pass < 2; ++pass) {
+        double T = 1.0;
+        double Pc[4] = {0.0, 0.0, 0.0, 0.0};
+        bool done = !inside;
+        if (t < kTilePx) sdone[t] = inside ? 0 : 1;
+        __syncthreads();
+        fetch_rm(0, 0);
+        fetch_rm(1, 1);
+        __syncthreads();
+        if (nbatch > 0) issue(0);
+        for (int b = 0; b < nbatch; ++b) {
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
+            __syncthreads();
+            if (b + 1 < nbatch) issue(b + 1);
+            if (b + 2 < nbatch) fetch_rm(b + 2, b & 1);
+            const unsigned char* sb = stg + (b & 1) * L.stage_bytes;
+            const PackedSplat* sp = reinterpret_cast<const PackedSplat*>(sb);
+            const double* scol = reinterpret_cast<const double*>(sb + L.st_color);
+            const uint32_t* em = emap + (b & 1) * kFNB;
+            const int n = min(kFNB, static_cast<int>(Ln) - b * kFNB);
+
+            // phase A: raw footprints (splat_render.cpp:276-285), clamp recorded
+            {
+                const bool pdone = sdone[px] != 0;
+#pragma unroll
+                for (int i = 0; i < kFNB / 4; ++i) {
+                    const int e = e_first + 4 * i;
+                    if (e >= n) break;
+                    double f = kNotContrib;
+                    if (!pdone) {
+                        const float4 pf = *reinterpret_cast<const float4*>(&sp[e].pmx);
+                        const float fdx = fpx - pf.x;
+                        const float fdy = fpy - pf.y;
+                        if (!(fdx * fdx + fdy * fdy > pf.z)) {
+                            const double dx = dpx - sp[e].mx;
+                            const double dy = dpy - sp[e].my;
+                            const double d2 = dx * dx + dy * dy;
+                            if (!(d2 > sp[e].cutoff_d2)) {
+                                f = sp[e].alpha * exp_footprint(-d2 * sp[e].inv_two_r2);
+                                if (f > kMaxFootprint) f = kClamped;
+                            }
+                        }
+                    }
+                    F[e * kTilePx + px] = f;
+                }
+            }
+            __syncthreads();
+
+            // phase B: transmittance chain of pixel t
+            if (t < kTilePx) {
+                for (int e = 0; e < n; ++e) {
+                    const int s = e * kTilePx + t;
+                    const double code = F[s];
+                    if (done || code == kNotContrib) {
+                        F[s] = kNotContrib;
+                        continue;
+                    }
+                    const double f = code == kClamped ? kMaxFootprint : code;
+                    const double w = f * T;
+                    const double v[4] = {scol[4 * e], scol[4 * e + 1], scol[4 * e + 2], sp[e].z};
+                    if (pass == 0) {
+#pragma unroll
+                        for (int ch = 0; ch < 4; ++ch) Rc[ch] += v[ch] * w;
+                    } else {
+                        // dR/df_j = v T_j - S / (1 - f_j), S = R - P_j  (losses.cpp:285-288)
+#pragma unroll
+                        for (int ch = 0; ch < 4; ++ch) {
+                            Pc[ch] += v[ch] * w;
+                            DR[(ch * kFNB + e) * kTilePx + t] = v[ch] * T - (Rc[ch] - Pc[ch]) / (1.0 - f);
+                        }
+                        Wv[s] = w;
+                    }
+                    T = T * (1.0 - f);
+                    if (p.opt.early_exit && T < p.opt.eps) done = true;
+                }
+                sdone[t] = done ? 1 : 0;
+            }
+            __syncthreads();
+
+            // phase C (pass 1): squared Jacobians, reduced over the block's pixels
+            if (pass == 1) {
+                const PoseParams& P = *vd.pose;
+#pragma unroll 1
+                for (int i = 0; i < kFNB / 4; ++i) {
+                    const int e = e_first + 4 * i;
+                    if (e >= n) break;  // warp-uniform (e depends on the warp only)
+                    double J[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                    const int s = e * kTilePx + px;
+                    const double code = F[s];
+                    if (code != kNotContrib) {
+                        const bool clamped = code == kClamped;
+                        const double f = clamped ? kMaxFootprint : code;
+                        const double w = Wv[s];
+                        const PackedSplat& g = sp[e];
+                        const double r2 = 0.5 / g.inv_two_r2;
+                        const double r = sqrt(r2);
+                        const double dx = dpx - g.mx, dy = dpy - g.my;
+                        const double d2 = dx * dx + dy * dy;
+                        const double iz = 1.0 / g.z;
+                        const bool chain = !clamped && g.alpha > 0.0;  // losses.cpp:297
+#pragma unroll
+                        for (int ch = 0; ch < 4; ++ch) {
+                            const double dRdf = DR[(ch * kFNB + e) * kTilePx + px];
+                            double g_a = 0, g_mx = 0, g_my = 0, g_r = 0;
+                            if (chain) {
+                                const double q = dRdf * f;
+                                g_a = q / g.alpha;
+                                g_mx = q * dx / r2;
+                                g_my = q * dy / r2;
+                                g_r = q * d2 / (r2 * r);
+                            }
+                            const double g_z = ch == 3 ? w : 0.0;
+                            const double dX = g_mx * p.cam.fx * iz;
+                            const double dY = g_my * p.cam.fy * iz;
+                            const double dZ = g_z - g_mx * (g.mx - p.cam.cx) * iz -
+                                              g_my * (g.my - p.cam.cy) * iz - g_r * r * iz;
+#pragma unroll
+                            for (int a = 0; a < 3; ++a) {  // d_world = R d_cam, R = Rcw^T
+                                const double dw = P.Rcw[a] * dX + P.Rcw[3 + a] * dY + P.Rcw[6 + a] * dZ;
+                                J[a] += dw * dw;
+                            }
+                            const double jl = g_r * r;
+                            const double jo = g_a * g.alpha * (1.0 - g.alpha);
+                            J[3] += jl * jl;
+                            J[4] += jo * jo;
+                            if (ch < 3) {
+                                const double c = scol[4 * e + ch];
+                                if (c > 0.0 && c < 1.0) J[5 + ch] += w * w;  // losses.cpp:291-294
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        double v = J[q];
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+                        if (lane == 0) red[(e * 2 + (px >> 5)) * 8 + q] = v;
+                    }
+                }
+                __syncthreads();
+                if (t < n * 8) {
+                    const int e = t >> 3, q = t & 7;
+                    const double sum = red[(e * 2) * 8 + q] + red[(e * 2 + 1) * 8 + q];
+                    const size_t slot = static_cast<size_t>(em[e]) * 8 + q;
+                    if (kGain)
+                        gacc[t] = sum * fp.invp[slot];
+                    else if (sum != 0.0)
+                        atomicAdd(&fp.H[slot], sum);
+                }
+                __syncthreads();
+                if (kGain && t == 0)
+                    for (int u = 0; u < n * 8; ++u) gsum += gacc[u];
+            }
+            const int mine = (t < kTilePx) ? (done ? 1 : 0) : 1;
+            if (__syncthreads_and(mine)) break;
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();
+    }
+    if (kGain && t == 0) vd.fis_partial[tile] = gsum;
+}
+
+template <bool kGain>
+void launch_fisher_t(const RasterParams& p, const FisherParams& fp, int n_views, cudaStream_t s) {
+    auto kern = k_fisher<kGain>;
+    const size_t smem = static_cast<size_t>(fisher_layout().total);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        configured = true;
+    }
+    dim3 grid(static_cast<unsigned>(p.tiles_per_view), static_cast<unsigned>(n_views), 1);
+    kern<<<grid, kFThreads, smem, s>>>(p, fp);
+}
+
+__global__ void k_fisher_invp(const double* __restrict__ H, double lambda, size_t n, double* invp) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) invp[i] = 1.0 / (H[i] + lambda);
+}
+
+}  // namespace
+
+void launch_fisher_prior(const RasterParams& p, const FisherParams& fp, int n_views, cudaStream_t s) {
+    launch_fisher_t<false>(p, fp, n_views, s);
+}
+
+void launch_fisher_gain(const RasterParams& p, const FisherParams& fp, int n_views, cudaStream_t s) {
+    launch_fisher_t<true>(p, fp, n_views, s);
+}
+
+void launch_fisher_invp(const double* H, double lambda, size_t n, double* invp, cudaStream_t s) {
+    if (n == 0) return;
+    k_fisher_invp<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(H, lambda, n, invp);
+}
+
+}  // namespace sgm

@@ -74,9 +74,17 @@ struct GroupParams {
     int Cg;
 };
 
+// Fisher extension (sgm_fisher.cu)
+struct FisherParams {
+    double* H;           // [N][8] prior accumulation (prior mode)
+    const double* invp;  // [N][8] 1 / (H_prior + lambda) (gain mode)
+};
+
 // Per view of a raster batch.
 struct ViewDesc {
     const uint32_t* order;      // [V] depth rank -> map index
+    const PoseParams* pose;     // device pose of this view
+    double* fis_partial;        // [tiles] per-tile Fisher gain (gain mode)
     const uint2* ranges;        // [tiles] (begin, end) into list
     const uint32_t* list;       // depth ranks grouped by tile, rank order inside a tile
     const PackedSplat* packed;  // [V] by rank
@@ -124,7 +132,10 @@ void launch_ranges(const uint32_t* sorted_tiles, uint64_t P, uint2* ranges, cuda
 void launch_raster_score(const RasterParams& p, int n_views, cudaStream_t s);
 void launch_raster_render(const RasterParams& p, int n_views, cudaStream_t s);
 void launch_reduce_scores(const ViewDesc* views, int n_views, int tiles, double* out_missing,
-                          double* out_entropy, cudaStream_t s);
+                          double* out_entropy, double* out_fisher, cudaStream_t s);
+void launch_fisher_prior(const RasterParams& p, const FisherParams& fp, int n_views, cudaStream_t s);
+void launch_fisher_gain(const RasterParams& p, const FisherParams& fp, int n_views, cudaStream_t s);
+void launch_fisher_invp(const double* H, double lambda, size_t n, double* invp, cudaStream_t s);
 void launch_debug_projections(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
                               const OptParams& o, const uint32_t* idx, uint32_t V,
                               double* out6, cudaStream_t s);

@@ -273,31 +273,37 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, uint64_t P, uint2* r
 // Per view: n_missing and entropy_sum from the per-tile partials, summed in a
 // fixed order that depends only on the tile count (sharding-invariant).
 __global__ void __launch_bounds__(256) k_reduce_scores(const ViewDesc* __restrict__ views, int tiles,
-                                                       double* out_missing, double* out_entropy) {
+                                                       double* out_missing, double* out_entropy,
+                                                       double* out_fisher) {
     __shared__ double sd[256];
+    __shared__ double sf[256];
     __shared__ unsigned long long su[256];
     const ViewDesc vd = views[blockIdx.x];
     const int t = threadIdx.x;
     const int per = (tiles + 255) / 256;
-    double h = 0.0;
+    double h = 0.0, fi = 0.0;
     unsigned long long m = 0;
     for (int i = t * per; i < min(tiles, (t + 1) * per); ++i) {
         h += vd.ent_partial[i];
         m += vd.miss_partial[i];
+        if (out_fisher) fi += vd.fis_partial[i];
     }
     sd[t] = h;
     su[t] = m;
+    sf[t] = fi;
     __syncthreads();
     for (int s = 128; s > 0; s >>= 1) {
         if (t < s) {
             sd[t] += sd[t + s];
             su[t] += su[t + s];
+            sf[t] += sf[t + s];
         }
         __syncthreads();
     }
     if (t == 0) {
         out_missing[blockIdx.x] = static_cast<double>(su[0]);
         out_entropy[blockIdx.x] = sd[0];
+        if (out_fisher) out_fisher[blockIdx.x] = sf[0];
     }
 }
 
@@ -404,9 +410,9 @@ void launch_ranges(const uint32_t* sorted_tiles, uint64_t P, uint2* ranges, cuda
 }
 
 void launch_reduce_scores(const ViewDesc* views, int n_views, int tiles, double* out_missing,
-                          double* out_entropy, cudaStream_t s) {
+                          double* out_entropy, double* out_fisher, cudaStream_t s) {
     if (n_views == 0) return;
-    k_reduce_scores<<<n_views, 256, 0, s>>>(views, tiles, out_missing, out_entropy);
+    k_reduce_scores<<<n_views, 256, 0, s>>>(views, tiles, out_missing, out_entropy, out_fisher);
 }
 
 void launch_debug_projections(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,

@@ -623,6 +623,43 @@ def score_poses(gmap: GaussianMap, camera: CameraModel, poses: Sequence[Pose],
     return nm, es
 
 
+def fisher_prior(gmap: GaussianMap, camera: CameraModel, poses: Sequence[Pose],
+                 lam: float = 1.0, options: Optional[RenderOptions] = None,
+                 ctx: Optional[Context] = None) -> np.ndarray:
+    """Fisher-information prior (extension): the diagonal Fisher information of
+    the rendered colour and depth w.r.t. each Gaussian's (mu xyz, log_radius, opacity_logit,
+    rgb), summed over `poses` (e.g. past keyframes). Kept with the map's device snapshot for
+    score_poses_fisher; returns H as an (N, 8) array."""
+    c = _ctx(ctx)
+    handle = c.upload(gmap)
+    n = len(poses)
+    H = np.zeros((max(gmap.size(), 1), 8))
+    arr = (N.sgm_pose * max(n, 1))(*[p._c() for p in poses])
+    opt = (options if options is not None else RenderOptions())._c()
+    cam_c = camera._c()
+    c.check(N.lib.sgm_fisher_prior(c.handle, handle, C.byref(cam_c), n, arr, C.byref(opt),
+                                   float(lam), N.dptr(H)))
+    return H[:gmap.size()]
+
+
+def score_poses_fisher(gmap: GaussianMap, camera: CameraModel, poses: Sequence[Pose],
+                       options: Optional[RenderOptions] = None, ctx: Optional[Context] = None):
+    """Per view (n_missing, entropy_sum, fisher_gain) with the FisherRF-style gain
+    sum_{i,theta} H_view / (H_prior + lambda) against the map's fisher_prior."""
+    c = _ctx(ctx)
+    handle = c.upload(gmap)
+    n = len(poses)
+    nm, es, fg = np.zeros(n), np.zeros(n), np.zeros(n)
+    if n == 0:
+        return nm, es, fg
+    arr = (N.sgm_pose * n)(*[p._c() for p in poses])
+    opt = (options if options is not None else RenderOptions())._c()
+    cam_c = camera._c()
+    c.check(N.lib.sgm_score_views_fisher(c.handle, handle, C.byref(cam_c), n, arr, C.byref(opt),
+                                         N.dptr(nm), N.dptr(es), N.dptr(fg)))
+    return nm, es, fg
+
+
 def refresh_candidate_scores(candidates: List[CandidatePose], gmap: GaussianMap,
                              scoring_camera: CameraModel, ctx: Optional[Context] = None) -> None:
     """explorer.cpp:186-205: caches n_missing and entropy_sum on every Active

@@ -1,0 +1,62 @@
+"""Fisher-information gain on the GPU (sgm_fisher_prior / sgm_score_views_fisher) vs the
+FD-pinned CPU oracle (tests/test_fisher_oracle.py). The prior uses fp64 atomics, so it is
+compared with a tolerance; the per-view gain is deterministic."""
+import numpy as np
+import pytest
+
+from conftest import random_map
+
+import paper_2506_00225_b200 as sgm
+from paper_2506_00225_b200 import scenes
+from paper_2506_00225_b200.splatmap import CameraModel, RenderOptions, look_at
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return sgm.Context(0)
+
+
+@pytest.mark.parametrize("opts", [RenderOptions(), RenderOptions(early_exit=False, truncation_sigmas=12.0)],
+                         ids=["default", "fd-options"])
+def test_fisher_prior_and_gain_vs_oracle(ctx, orc, opts):
+    cam = CameraModel(45, 37, 0, 0, 40.0, 41.0, 22.3, 18.1)
+    pose = look_at([0.1, -0.05, -0.4], [0.0, 0.1, 2.5])
+    gm = random_map(3, 250, cam, pose, k=3, num_classes=7)
+    gm.colors[::5] = np.clip(gm.colors[::5], 0.0, 1.0)
+    gm.opacity_logits[::11] = 12.0  # some clamped footprints (alpha ~ 1)
+    prior_poses = [look_at([0.05 * i, 0.02 * i, -0.4], [0.0, 0.1, 2.5]) for i in range(4)]
+    H = sgm.fisher_prior(gm, cam, prior_poses, lam=0.5, options=opts, ctx=ctx)
+    H_o = orc.fisher_accumulate(gm, cam, prior_poses, opts)
+    np.testing.assert_allclose(H, H_o, rtol=1e-9, atol=1e-12 * H_o.max())
+    cands = [look_at([0.1 * i - 0.2, 0.0, -0.4], [0.0, 0.1, 2.5]) for i in range(6)]
+    nm, es, g = sgm.score_poses_fisher(gm, cam, cands, opts, ctx=ctx)
+    nm2, es2 = sgm.score_poses(gm, cam, cands, opts, ctx=ctx)
+    np.testing.assert_array_equal(nm, nm2)
+    np.testing.assert_array_equal(es, es2)
+    g_o = orc.fisher_gain(gm, cam, cands, H_o, 0.5, opts)
+    np.testing.assert_allclose(g, g_o, rtol=1e-9)
+    # deterministic: the gain does not depend on batching
+    _, _, g1 = sgm.score_poses_fisher(gm, cam, cands[:1], opts, ctx=ctx)
+    assert g1[0] == g[0]
+
+
+def test_fisher_requires_prior_and_positive_lambda(ctx):
+    cam = CameraModel(16, 12, 0, 0, 14.0, 14.0, 8.0, 6.0)
+    gm = random_map(1, 20, cam, k=2, num_classes=3)
+    with pytest.raises(RuntimeError, match="prior"):
+        sgm.score_poses_fisher(gm, cam, [sgm.Pose()], ctx=ctx)
+    with pytest.raises(RuntimeError, match="lambda"):
+        sgm.fisher_prior(gm, cam, [sgm.Pose()], lam=0.0, ctx=ctx)
+
+
+def test_fisher_cfg0_scene_vs_oracle(ctx, orc):
+    gm = scenes.make_map(0, n=3000)
+    cam = scenes.CONFIGS[0].camera()
+    poses = scenes.render_poses(0, 8)
+    H = sgm.fisher_prior(gm, cam, poses[:4], lam=1.0, ctx=ctx)
+    H_o = orc.fisher_accumulate(gm, cam, poses[:4])
+    np.testing.assert_allclose(H, H_o, rtol=1e-9, atol=1e-12 * H_o.max())
+    _, _, g = sgm.score_poses_fisher(gm, cam, poses[4:], ctx=ctx)
+    np.testing.assert_allclose(g, orc.fisher_gain(gm, cam, poses[4:], H_o, 1.0), rtol=1e-9)
