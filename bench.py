@@ -263,6 +263,40 @@ def main() -> None:
     combine_scores(cands, np.array([4.0, 1.5, 3.0]))
     best = max(range(n_total), key=lambda i: (cands[i].i_total, -i))
 
+    # ---- cfg1 with the Fisher-information gain: prior from 32 past poses,
+    #      then the same candidates scored with n_missing + entropy + Fisher gain ----
+    fisher = None
+    try:
+        from paper_2506_00225_b200.splatmap import fisher_prior, score_poses_fisher
+        prior_poses = [c.camera_pose() for c in scenes.make_candidates(cfg, 32, stream=2)]
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        fisher_prior(gm, cam, prior_poses, lam=1.0, ctx=ctx)
+        ev1.record(stream)
+        ev1.synchronize()
+        prior_ms = ev0.elapsed_time(ev1)
+        for _ in range(max(1, args.warmup)):
+            score_poses_fisher(gm, cam, poses, ctx=ctx)
+        f_ms = []
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            _, _, gains = score_poses_fisher(gm, cam, poses, ctx=ctx)
+            ev1.record(stream)
+            ev1.synchronize()
+            f_ms.append(ev0.elapsed_time(ev1))
+        fisher = {"views_per_s": len(poses) * args.steps / (float(np.sum(f_ms)) / 1e3),
+                  "ms_per_step": float(np.mean(f_ms)), "prior_poses": len(prior_poses),
+                  "prior_ms": prior_ms, "lambda": 1.0,
+                  "gain": "sum_{i,theta} H_view / (H_prior + lambda), theta = mu xyz, log_r, "
+                          "logit, rgb; channels R,G,B,depth"}
+    except Exception as exc:  # reported, not fatal
+        fisher = {"error": repr(exc)}
+
     # ---- e2e through the public API (host inputs, map re-upload every step) ----
     h2d = int(gm.centers.nbytes + gm.log_radii.nbytes + gm.opacity_logits.nbytes +
               gm.colors.nbytes + gm.sem_indices.nbytes + gm.sem_probs.nbytes) + 96 * len(mine)
@@ -329,7 +363,7 @@ def main() -> None:
                     "contributors_per_view": st["contributors"] / max(1, views_timed),
                     "visible_per_view": vis_per_view,
                     "pairs_per_view": st["pairs"] / max(1, views_timed),
-                    "binning_ms_per_batch": st["binning_ms"] / raster_launches}
+                    "batch_span_ms_per_raster_launch": st["binning_ms"] / raster_launches}
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -358,6 +392,7 @@ def main() -> None:
             "roofline": roofline, "roofline_aux": roofline_aux,
             "cpu_baseline": cpu_baseline, "clocks": clk,
             "argmax_view": int(best), "views_total_per_step": n_total,
+            "with_fisher_gain": fisher,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

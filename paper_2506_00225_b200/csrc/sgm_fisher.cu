@@ -28,7 +28,7 @@ constexpr int kFThreads = 256;
 constexpr int kFNB = 16;
 
 struct FLayout {
-    int f, dr, w, red, gacc, emap, rm, done, stage0, stage_bytes, st_color, total;
+    int f, dr, w, red, gacc, emap, rm, done, pose, stage0, stage_bytes, st_color, total;
 };
 
 __host__ __device__ inline FLayout fisher_layout() {
@@ -41,7 +41,8 @@ __host__ __device__ inline FLayout fisher_layout() {
     L.emap = L.gacc + kFNB * 8 * 8;           // [2][kFNB] map index
     L.rm = L.emap + 2 * kFNB * 4;             // [2][kFNB] (rank, map index)
     L.done = L.rm + 2 * kFNB * 8;             // [64]
-    L.stage0 = L.done + kTilePx * 4;
+    L.pose = L.done + kTilePx * 4;            // Rcw (9 doubles) + pad
+    L.stage0 = L.pose + 16 * 8;
     L.st_color = kFNB * static_cast<int>(sizeof(PackedSplat));
     L.stage_bytes = L.st_color + kFNB * 32;
     L.total = L.stage0 + 2 * L.stage_bytes;
@@ -53,7 +54,7 @@ constexpr double kNotContrib = -1.0;
 constexpr double kClamped = -2.0;
 
 template <bool kGain>
-__global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherParams fp) {
+__global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherParams fp) {
     extern __shared__ __align__(16) unsigned char smem[];
     const FLayout L = fisher_layout();
     double* F = reinterpret_cast<double*>(smem + L.f);
@@ -64,6 +65,7 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
     uint32_t* emap = reinterpret_cast<uint32_t*>(smem + L.emap);
     uint2* rm = reinterpret_cast<uint2*>(smem + L.rm);
     int* sdone = reinterpret_cast<int*>(smem + L.done);
+    double* sR = reinterpret_cast<double*>(smem + L.pose);  // camera-from-world rotation
     unsigned char* stg = smem + L.stage0;
 
     const ViewDesc vd = p.views[blockIdx.y];
@@ -118,6 +120,7 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
         }
     };
 
+    if (t < 9) sR[t] = vd.pose->Rcw[t];
     double Rc[4] = {0.0, 0.0, 0.0, 0.0};  // pass 0 result (threads t < 64)
     double gsum = 0.0;                     // gain of this tile (thread 0, fixed order)
 
@@ -186,10 +189,11 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
                         for (int ch = 0; ch < 4; ++ch) Rc[ch] += v[ch] * w;
                     } else {
                         // dR/df_j = v T_j - S / (1 - f_j), S = R - P_j  (losses.cpp:285-288)
+                        const double i1f = 1.0 / (1.0 - f);
 #pragma unroll
                         for (int ch = 0; ch < 4; ++ch) {
                             Pc[ch] += v[ch] * w;
-                            DR[(ch * kFNB + e) * kTilePx + t] = v[ch] * T - (Rc[ch] - Pc[ch]) / (1.0 - f);
+                            DR[(ch * kFNB + e) * kTilePx + t] = v[ch] * T - (Rc[ch] - Pc[ch]) * i1f;
                         }
                         Wv[s] = w;
                     }
@@ -202,7 +206,6 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
 
             // phase C (pass 1): squared Jacobians, reduced over the block's pixels
             if (pass == 1) {
-                const PoseParams& P = *vd.pose;
 #pragma unroll 1
                 for (int i = 0; i < kFNB / 4; ++i) {
                     const int e = e_first + 4 * i;
@@ -215,35 +218,38 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
                         const double f = clamped ? kMaxFootprint : code;
                         const double w = Wv[s];
                         const PackedSplat& g = sp[e];
-                        const double r2 = 0.5 / g.inv_two_r2;
-                        const double r = sqrt(r2);
+                        // d f / d(param), hoisted out of the channel loop (losses.cpp:297-304)
+                        const double inv_r2 = 2.0 * g.inv_two_r2;
+                        const double r = sqrt(0.5 / g.inv_two_r2);
                         const double dx = dpx - g.mx, dy = dpy - g.my;
                         const double d2 = dx * dx + dy * dy;
                         const double iz = 1.0 / g.z;
                         const bool chain = !clamped && g.alpha > 0.0;  // losses.cpp:297
-#pragma unroll
+                        const double fa = chain ? f / g.alpha : 0.0;
+                        const double fmx = chain ? f * dx * inv_r2 : 0.0;
+                        const double fmy = chain ? f * dy * inv_r2 : 0.0;
+                        const double fr = chain ? f * d2 * inv_r2 / r : 0.0;
+                        const double oa = g.alpha * (1.0 - g.alpha);
+                        // projection -> camera Jacobian rows (losses.cpp:323-326)
+                        const double kx = p.cam.fx * iz, ky = p.cam.fy * iz;
+                        const double zx = (g.mx - p.cam.cx) * iz, zy = (g.my - p.cam.cy) * iz;
+                        const double zr = r * iz;
+#pragma unroll 1
                         for (int ch = 0; ch < 4; ++ch) {
                             const double dRdf = DR[(ch * kFNB + e) * kTilePx + px];
-                            double g_a = 0, g_mx = 0, g_my = 0, g_r = 0;
-                            if (chain) {
-                                const double q = dRdf * f;
-                                g_a = q / g.alpha;
-                                g_mx = q * dx / r2;
-                                g_my = q * dy / r2;
-                                g_r = q * d2 / (r2 * r);
-                            }
+                            const double g_a = dRdf * fa, g_mx = dRdf * fmx, g_my = dRdf * fmy,
+                                         g_r = dRdf * fr;
                             const double g_z = ch == 3 ? w : 0.0;
-                            const double dX = g_mx * p.cam.fx * iz;
-                            const double dY = g_my * p.cam.fy * iz;
-                            const double dZ = g_z - g_mx * (g.mx - p.cam.cx) * iz -
-                                              g_my * (g.my - p.cam.cy) * iz - g_r * r * iz;
+                            const double dX = g_mx * kx;
+                            const double dY = g_my * ky;
+                            const double dZ = g_z - g_mx * zx - g_my * zy - g_r * zr;
 #pragma unroll
                             for (int a = 0; a < 3; ++a) {  // d_world = R d_cam, R = Rcw^T
-                                const double dw = P.Rcw[a] * dX + P.Rcw[3 + a] * dY + P.Rcw[6 + a] * dZ;
+                                const double dw = sR[a] * dX + sR[3 + a] * dY + sR[6 + a] * dZ;
                                 J[a] += dw * dw;
                             }
                             const double jl = g_r * r;
-                            const double jo = g_a * g.alpha * (1.0 - g.alpha);
+                            const double jo = g_a * oa;
                             J[3] += jl * jl;
                             J[4] += jo * jo;
                             if (ch < 3) {
@@ -271,8 +277,14 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
                         atomicAdd(&fp.H[slot], sum);
                 }
                 __syncthreads();
+                if (kGain && t < 8) {  // fixed-order two-level sum: deterministic
+                    double part = 0.0;
+                    for (int u = t; u < n * 8; u += 8) part += gacc[u];
+                    red[t] = part;
+                }
+                __syncthreads();
                 if (kGain && t == 0)
-                    for (int u = 0; u < n * 8; ++u) gsum += gacc[u];
+                    for (int u = 0; u < 8; ++u) gsum += red[u];
             }
             const int mine = (t < kTilePx) ? (done ? 1 : 0) : 1;
             if (__syncthreads_and(mine)) break;
