@@ -213,50 +213,55 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
                     double J[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                     const int s = e * kTilePx + px;
                     const double code = F[s];
-                    if (code != kNotContrib) {
+                    const bool contrib = code != kNotContrib;
+                    if (contrib) {
                         const bool clamped = code == kClamped;
                         const double f = clamped ? kMaxFootprint : code;
                         const double w = Wv[s];
                         const PackedSplat& g = sp[e];
-                        // d f / d(param), hoisted out of the channel loop (losses.cpp:297-304)
+                        // d f / d(param) (losses.cpp:297-304); zero when clamped or alpha == 0
+                        const bool chain = !clamped && g.alpha > 0.0;
                         const double inv_r2 = 2.0 * g.inv_two_r2;
                         const double r = sqrt(0.5 / g.inv_two_r2);
                         const double dx = dpx - g.mx, dy = dpy - g.my;
                         const double d2 = dx * dx + dy * dy;
                         const double iz = 1.0 / g.z;
-                        const bool chain = !clamped && g.alpha > 0.0;  // losses.cpp:297
                         const double fa = chain ? f / g.alpha : 0.0;
                         const double fmx = chain ? f * dx * inv_r2 : 0.0;
                         const double fmy = chain ? f * dy * inv_r2 : 0.0;
                         const double fr = chain ? f * d2 * inv_r2 / r : 0.0;
-                        const double oa = g.alpha * (1.0 - g.alpha);
-                        // projection -> camera Jacobian rows (losses.cpp:323-326)
-                        const double kx = p.cam.fx * iz, ky = p.cam.fy * iz;
-                        const double zx = (g.mx - p.cam.cx) * iz, zy = (g.my - p.cam.cy) * iz;
-                        const double zr = r * iz;
-#pragma unroll 1
-                        for (int ch = 0; ch < 4; ++ch) {
-                            const double dRdf = DR[(ch * kFNB + e) * kTilePx + px];
-                            const double g_a = dRdf * fa, g_mx = dRdf * fmx, g_my = dRdf * fmy,
-                                         g_r = dRdf * fr;
-                            const double g_z = ch == 3 ? w : 0.0;
-                            const double dX = g_mx * kx;
-                            const double dY = g_my * ky;
-                            const double dZ = g_z - g_mx * zx - g_my * zy - g_r * zr;
+                        // d_cam(ch) = dR_ch/df * u + [ch == depth] * w * e_z with
+                        // u = (fmx fx/z, fmy fy/z, -(fmx (mx-cx) + fmy (my-cy) + fr r) / z)
+                        // (losses.cpp:323-326), so with v = R u (world, R = Rcw^T):
+                        //   sum_ch J_a^2 = S_rgb v_a^2 + (dR_D/df v_a + w R_{a,z})^2
+                        const double ux = fmx * p.cam.fx * iz;
+                        const double uy = fmy * p.cam.fy * iz;
+                        const double uz = -(fmx * (g.mx - p.cam.cx) + fmy * (g.my - p.cam.cy) + fr * r) * iz;
+                        const double d0 = DR[(0 * kFNB + e) * kTilePx + px];
+                        const double d1 = DR[(1 * kFNB + e) * kTilePx + px];
+                        const double d2c = DR[(2 * kFNB + e) * kTilePx + px];
+                        const double dD = DR[(3 * kFNB + e) * kTilePx + px];
+                        const double Srgb = d0 * d0 + d1 * d1 + d2c * d2c;
+                        const double Sall = Srgb + dD * dD;
 #pragma unroll
-                            for (int a = 0; a < 3; ++a) {  // d_world = R d_cam, R = Rcw^T
-                                const double dw = sR[a] * dX + sR[3 + a] * dY + sR[6 + a] * dZ;
-                                J[a] += dw * dw;
-                            }
-                            const double jl = g_r * r;
-                            const double jo = g_a * oa;
-                            J[3] += jl * jl;
-                            J[4] += jo * jo;
-                            if (ch < 3) {
-                                const double c = scol[4 * e + ch];
-                                if (c > 0.0 && c < 1.0) J[5 + ch] += w * w;  // losses.cpp:291-294
-                            }
+                        for (int a = 0; a < 3; ++a) {
+                            const double va = sR[a] * ux + sR[3 + a] * uy + sR[6 + a] * uz;
+                            const double dep = dD * va + w * sR[6 + a];
+                            J[a] = Srgb * va * va + dep * dep;
                         }
+                        const double jl = fr * r;                       // d/d log_r (:333)
+                        const double jo = fa * g.alpha * (1.0 - g.alpha);  // d/d logit (:334)
+                        J[3] = Sall * jl * jl;
+                        J[4] = Sall * jo * jo;
+#pragma unroll
+                        for (int ch = 0; ch < 3; ++ch) {
+                            const double c = scol[4 * e + ch];
+                            if (c > 0.0 && c < 1.0) J[5 + ch] = w * w;  // losses.cpp:291-294
+                        }
+                    }
+                    if (!__any_sync(0xffffffffu, contrib)) {
+                        if (lane < 8) red[(e * 2 + (px >> 5)) * 8 + lane] = 0.0;
+                        continue;
                     }
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
