@@ -34,6 +34,23 @@ thread_local std::string g_create_error;
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+        o.p = nullptr;
+        o.bytes = 0;
+    }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            if (p) cudaFree(p);
+            p = o.p;
+            bytes = o.bytes;
+            o.p = nullptr;
+            o.bytes = 0;
+        }
+        return *this;
+    }
     ~DevBuf() {
         if (p) cudaFree(p);
     }
@@ -133,6 +150,25 @@ struct sgm_ctx {
     int last_px = 0;
     HostBuf h_counts, h_views, h_poses, h_out, h_stage;
     DevBuf upload_tmp;
+    // device buffers of released maps, reused by the next upload (a map version bump
+    // otherwise pays cudaFree + cudaMalloc of ~0.2 KB per Gaussian)
+    std::vector<DevBuf> pool;
+
+    void take(DevBuf& dst, size_t want) {
+        if (dst.bytes >= want) return;
+        size_t best = pool.size();
+        for (size_t i = 0; i < pool.size(); ++i)
+            if (pool[i].bytes >= want && (best == pool.size() || pool[i].bytes < pool[best].bytes))
+                best = i;
+        if (best == pool.size()) return;
+        dst = std::move(pool[best]);
+        pool.erase(pool.begin() + static_cast<long>(best));
+    }
+    void give(DevBuf&& b) {
+        if (!b.p) return;
+        pool.push_back(std::move(b));
+        while (pool.size() > 16) pool.erase(pool.begin());  // bounded: oldest first
+    }
 
     // state of the last render (for sgm_last_*)
     bool last_valid = false;
@@ -712,6 +748,10 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, con
         int has_dup = 0;
         for (unsigned w = 0; w < nth; ++w) has_dup |= dup[w];
         cudaStream_t s = ctx->stream;
+        ctx->take(m->geo, geo_b);
+        ctx->take(m->color, col_b);
+        ctx->take(m->idx, 2 * ns * kpad);
+        ctx->take(m->prob, 8 * ns * kpad);
         CK(m->geo.reserve(geo_b));
         CK(m->color.reserve(col_b));
         CK(m->idx.reserve(2 * ns * kpad));
@@ -757,7 +797,12 @@ void sgm_map_release(sgm_ctx* ctx, sgm_map* map) {
     if (ctx) {
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
+        cudaStreamSynchronize(ctx->bin_stream);
         if (ctx->last_map == map) ctx->last_valid = false;
+        ctx->give(std::move(map->geo));
+        ctx->give(std::move(map->color));
+        ctx->give(std::move(map->idx));
+        ctx->give(std::move(map->prob));
     }
     delete map;
 }
