@@ -142,7 +142,8 @@ struct sgm_ctx {
     cudaEvent_t ev_r[16] = {};  // raster start/stop pairs of one group (profiling)
 
     // scratch
-    DevBuf poses, vcount, pcount, keys, vals, keys_alt, vals_alt, packed, counts, offsets, rects;
+    DevBuf poses, vcount, pcount, keys, vals, keys_alt, vals_alt, packed, counts, offsets, rects,
+        bounds;
     DevBuf tkeys, tvals, tkeys_alt, tvals_alt, ranges, ent_part, miss_part, views, out,
         contributors, cub_tmp, planes, dbg, ccount, coffset, contrib, fis_part;
     uint64_t last_ncontrib = 0;
@@ -241,8 +242,8 @@ struct RenderTargets {
 // slices and returns via the slice pointers. vals/keys hold the compacted (z, idx).
 void bin_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const CamParams& cam,
               const OptParams& o, const PoseParams* d_pose, uint32_t* keys, uint32_t* vals,
-              uint32_t V, uint64_t P, PackedSplat* packed, uint32_t* list, uint2* ranges,
-              int bin_tiles) {
+              uint32_t V, uint64_t P, PackedSplat* packed, uint4* bounds, uint32_t* list,
+              uint2* ranges, int bin_tiles) {
     CK(cudaMemsetAsync(ranges, 0, sizeof(uint2) * bin_tiles, s));
     if (V == 0) return;
     // K2: depth rank (radix sort on the monotone fp32 key; runs fixed below)
@@ -254,8 +255,8 @@ void bin_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const CamParams&
     CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, dk, dv, V, 0, 32, s));
     ctx->stats.kernel_launches += 1;  // counted as one library sort call
     launch_tiefix(map->dev, d_pose, cam, o, dk.Current(), dv.Current(), V, s);
-    launch_pack(map->dev, d_pose, cam, o, GroupParams{1, map->dev.C}, dv.Current(), V, packed,
-                ctx->counts.as<unsigned long long>(), ctx->rects.as<int4>(), s);
+    launch_pack(map->dev, d_pose, cam, o, map->groups, dv.Current(), V, packed,
+                ctx->counts.as<unsigned long long>(), ctx->rects.as<int4>(), bounds, s);
     ctx->stats.kernel_launches += (V >= 2 ? 1 : 0) + 1;
     // keep the sorted indices for sgm_last_projections
     if (dv.Current() != vals) CK(cudaMemcpyAsync(vals, dv.Current(), 4ull * V, cudaMemcpyDeviceToDevice, s));
@@ -303,7 +304,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
     ctx->last_valid = false;
 
     // batch size bounded by a scratch budget for the per-view N-sized arrays
-    const size_t per_view = std::max<uint64_t>(N, 1) * (4 + 4 + sizeof(PackedSplat)) +
+    const size_t per_view = std::max<uint64_t>(N, 1) * (4 + 4 + sizeof(PackedSplat) + 16) +
                             static_cast<size_t>(bin_tiles) * sizeof(uint2) +
                             static_cast<size_t>(rtiles) * 12 + 256;
     const size_t budget = size_t(12) << 30;
@@ -321,6 +322,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
     CK(ctx->rects.reserve(sizeof(int4) * NS));
     CK(ctx->vals_alt.reserve(4 * NS));
     CK(ctx->packed.reserve(sizeof(PackedSplat) * NS * B));
+    CK(ctx->bounds.reserve(sizeof(uint4) * NS * B));
     CK(ctx->counts.reserve(8 * (NS + 1)));
     CK(ctx->offsets.reserve(8 * (NS + 1)));
     CK(ctx->ranges.reserve(sizeof(uint2) * bin_tiles * B));
@@ -387,6 +389,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 d.ranges = ctx->ranges.as<uint2>() + static_cast<size_t>(bin_tiles) * v;
                 d.list = ctx->tvals.as<uint32_t>() + list_off;
                 d.packed = ctx->packed.as<PackedSplat>() + NS * v;
+                d.bounds = ctx->bounds.as<uint4>() + NS * v;
                 d.ent_partial = ctx->ent_part.as<double>() + static_cast<size_t>(rtiles) * v;
                 d.miss_partial = ctx->miss_part.as<uint32_t>() + static_cast<size_t>(rtiles) * v;
                 d.color = rt.color;
@@ -421,8 +424,8 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                     const ViewDesc& d = hvd[v - v0];
                     bin_view(ctx, sb, map, cam, o, ctx->poses.as<PoseParams>() + v,
                              ctx->keys.as<uint32_t>() + NS * v, const_cast<uint32_t*>(d.order), V[v],
-                             P[v], const_cast<PackedSplat*>(d.packed), const_cast<uint32_t*>(d.list),
-                             const_cast<uint2*>(d.ranges), bin_tiles);
+                             P[v], const_cast<PackedSplat*>(d.packed), const_cast<uint4*>(d.bounds),
+                             const_cast<uint32_t*>(d.list), const_cast<uint2*>(d.ranges), bin_tiles);
                 }
                 const int slot = (s0 / kSub) & 1;
                 CK(cudaEventRecord(ctx->ev_binned[slot], sb));

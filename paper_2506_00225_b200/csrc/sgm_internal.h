@@ -88,6 +88,7 @@ struct ViewDesc {
     const uint2* ranges;        // [tiles] (begin, end) into list
     const uint32_t* list;       // depth ranks grouped by tile, rank order inside a tile
     const PackedSplat* packed;  // [V] by rank
+    const uint4* bounds;        // [V] by rank: raster channel-group bounds (8 x u16)
     double* ent_partial;        // [tiles] per-tile entropy sum (score mode)
     uint32_t* miss_partial;     // [tiles] per-tile exact-zero silhouette count
     // render mode planes (device, reference layout); null when not requested
@@ -124,7 +125,8 @@ void launch_tiefix(const DevMap& m, const PoseParams* d_pose, const CamParams& c
                    cudaStream_t s);
 void launch_pack(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
                  const OptParams& o, const GroupParams& gp, const uint32_t* idx, uint32_t V,
-                 PackedSplat* packed, unsigned long long* counts, int4* rects, cudaStream_t s);
+                 PackedSplat* packed, unsigned long long* counts, int4* rects, uint4* bounds,
+                 cudaStream_t s);
 void launch_emit_pairs(const unsigned long long* offsets, const int4* rects, uint32_t V,
                        unsigned long long P, const OptParams& o, uint32_t* tile_keys,
                        uint32_t* tile_vals, cudaStream_t s);

@@ -198,8 +198,8 @@ __global__ void k_tiefix(DevMap m, const PoseParams* __restrict__ pose, CamParam
 // PackedSplat + Probe per depth rank (splat_render.cpp:191-204) and tile counts.
 __global__ void k_pack(DevMap m, const PoseParams* __restrict__ pose, CamParams cam, OptParams o,
                        GroupParams gp, const uint32_t* __restrict__ idx, uint32_t V,
-                       PackedSplat* packed, unsigned long long* counts, int4* rects) {
-    (void)gp;
+                       PackedSplat* packed, unsigned long long* counts, int4* rects,
+                       uint4* bounds) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= V) return;
     const uint32_t i = idx[r];
@@ -221,6 +221,21 @@ __global__ void k_pack(DevMap m, const PoseParams* __restrict__ pose, CamParams 
     const Rect rc = tile_rect(mx, my, rad, o);
     counts[r] = rect_count(rc);
     rects[r] = make_int4(rc.tx0, rc.ty0, rc.tx1 - rc.tx0 + 1, rc.ty1 - rc.ty0 + 1);
+    if (bounds) {
+        // raster channel groups of the class-sorted row: b[g] = #entries with class <
+        // (g + 1) * Cg for g = 0..6, b[7] = k (u16 each)
+        const uint16_t* row = m.sem_idx + static_cast<size_t>(i) * m.kpad;
+        uint32_t b[8];
+        int j = 0;
+        for (int g = 0; g < 7; ++g) {
+            const int lim = (g + 1) * gp.Cg;
+            while (j < m.k && row[j] < lim) ++j;
+            b[g] = static_cast<uint32_t>(j);
+        }
+        b[7] = static_cast<uint32_t>(m.k);
+        bounds[r] = make_uint4(b[0] | (b[1] << 16), b[2] | (b[3] << 16), b[4] | (b[5] << 16),
+                               b[6] | (b[7] << 16));
+    }
 }
 
 // Emits (bin, rank) pairs in rank order at the scanned offsets; a stable sort on
@@ -390,9 +405,11 @@ void launch_tiefix(const DevMap& m, const PoseParams* d_pose, const CamParams& c
 
 void launch_pack(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
                  const OptParams& o, const GroupParams& gp, const uint32_t* idx, uint32_t V,
-                 PackedSplat* packed, unsigned long long* counts, int4* rects, cudaStream_t s) {
+                 PackedSplat* packed, unsigned long long* counts, int4* rects, uint4* bounds,
+                 cudaStream_t s) {
     if (V == 0) return;
-    k_pack<<<blocks_for(V, 256), 256, 0, s>>>(m, d_pose, cam, o, gp, idx, V, packed, counts, rects);
+    k_pack<<<blocks_for(V, 256), 256, 0, s>>>(m, d_pose, cam, o, gp, idx, V, packed, counts, rects,
+                                              bounds);
 }
 
 void launch_emit_pairs(const unsigned long long* offsets, const int4* rects, uint32_t V,

@@ -45,7 +45,8 @@ constexpr int kBnd = kGroups + 1;
 __host__ __device__ constexpr int align16(int b) { return (b + 15) & ~15; }
 
 struct Layout {  // byte offsets in dynamic shared memory
-    int acc, w, bnd, done, rm, stage0, stage_bytes, st_packed, st_idx, st_prob, st_color, total;
+    int acc, w, segp, tpx, done, rm, stage0, stage_bytes, st_packed, st_bnd, st_idx, st_prob,
+        st_color, total;
 };
 
 // accumulator row pitch in double2 units (render: +1 so the transposed write-out
@@ -57,12 +58,14 @@ __host__ __device__ inline Layout make_layout(int C, int kpad, bool render) {
     Layout L;
     L.acc = 0;
     L.w = align16(C * acc_pitch(render) * 16);
-    L.bnd = L.w + kNB * kTilePx * 8;
-    L.done = L.bnd + align16(kNB * kBnd * 2);
+    L.segp = L.w + kNB * kTilePx * 8;          // [4][64] segment products (score phase B)
+    L.tpx = L.segp + 4 * kTilePx * 8;          // [64] pixel transmittance
+    L.done = L.tpx + kTilePx * 8;
     L.rm = L.done + kTilePx * 4;
     L.stage0 = L.rm + 2 * kNB * 8;
     L.st_packed = 0;
-    L.st_idx = kNB * static_cast<int>(sizeof(PackedSplat));
+    L.st_bnd = kNB * static_cast<int>(sizeof(PackedSplat));      // [kNB] uint4 group bounds
+    L.st_idx = L.st_bnd + kNB * 16;
     L.st_prob = L.st_idx + kNB * kpad * 2;
     L.st_color = L.st_prob + kNB * kpad * 8;
     L.stage_bytes = L.st_color + (render ? kNB * 32 : 0);
@@ -91,7 +94,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     double* acc = reinterpret_cast<double*>(smem + L.acc);
     double* W = reinterpret_cast<double*>(smem + L.w);             // [kNB][32] double2
     const double2* W2 = reinterpret_cast<const double2*>(smem + L.w);
-    uint16_t* bnd = reinterpret_cast<uint16_t*>(smem + L.bnd);     // [kNB][kBnd]
+    double* segp = reinterpret_cast<double*>(smem + L.segp);       // [4][64]
+    double* sT = reinterpret_cast<double*>(smem + L.tpx);          // [64]
     int* sdone = reinterpret_cast<int*>(smem + L.done);            // [64]
     uint2* rm = reinterpret_cast<uint2*>(smem + L.rm);             // [2][kNB] (rank, map index)
     unsigned char* stg = smem + L.stage0;
@@ -116,11 +120,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     const int c0 = g * Cg, c1 = min(C, c0 + Cg);
 
     for (int i = t; i < C * apitch; i += kThreads) acc2[i] = make_double2(0.0, 0.0);
-    if (t < kTilePx) sdone[t] = inside ? 0 : 1;
+    if (t < kTilePx) {
+        sdone[t] = inside ? 0 : 1;
+        sT[t] = 1.0;
+    }
 
     // ---- cp.async pipeline over batches of kNB Gaussians (depth-rank order) ----
     const int qi = kpad / 8, qp = kpad / 2;
-    const int Q = 4 + qi + qp + (kRender ? 2 : 0);  // 16-byte chunks per Gaussian
+    const int Q = 5 + qi + qp + (kRender ? 2 : 0);  // 16-byte chunks per Gaussian
     auto issue = [&](int b) {
         unsigned char* sb = stg + (b & 1) * L.stage_bytes;
         const int n = min(kNB, static_cast<int>(Ln) - b * kNB);
@@ -134,7 +141,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
             if (q < 4) {
                 src = reinterpret_cast<const unsigned char*>(vd.packed + v.x) + 16 * q;
                 dst = sb + L.st_packed + e * 64 + 16 * q;
-            } else if ((q -= 4) < qi) {
+            } else if (q == 4) {
+                src = reinterpret_cast<const unsigned char*>(vd.bounds + v.x);
+                dst = sb + L.st_bnd + e * 16;
+            } else if ((q -= 5) < qi) {
                 src = reinterpret_cast<const unsigned char*>(p.map.sem_idx + static_cast<size_t>(v.y) * kpad) + 16 * q;
                 dst = sb + L.st_idx + e * kpad * 2 + 16 * q;
             } else if ((q -= qi) < qp) {
@@ -182,6 +192,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
         if (b + 2 < nbatch) fetch_rm(b + 2, b & 1);
         const unsigned char* sb = stg + (b & 1) * L.stage_bytes;
         const PackedSplat* sp = reinterpret_cast<const PackedSplat*>(sb + L.st_packed);
+        const uint16_t* sbnd = reinterpret_cast<const uint16_t*>(sb + L.st_bnd);  // [kNB][8]
         const uint16_t* si = reinterpret_cast<const uint16_t*>(sb + L.st_idx);
         const double* spr = reinterpret_cast<const double*>(sb + L.st_prob);
         const double* scol = reinterpret_cast<const double*>(sb + L.st_color);
@@ -214,50 +225,73 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
         }
         __syncthreads();
 
-        // ---- phase B ----
-        if (t < kTilePx) {
-            // sequential transmittance chain of pixel t (:286-312)
-            for (int e = 0; e < n; ++e) {
-                const int s = pair_slot(e, 32, t);
-                const double f = W[s];
-                if (done || f < 0.0) {
-                    W[s] = 0.0;
-                    continue;
-                }
-                const double w = f * T;
-                W[s] = w;
-                if (kRender && vd.contrib) {  // retain_contributors (:310): depth ranks in order
-                    if (vd.contrib_offset)
-                        vd.contrib[vd.contrib_offset[pix_t] + ncontrib_px] = sp[e].aux;
-                    ++ncontrib_px;
-                }
-                if (kRender) {
+        // ---- phase B: transmittance chain (:286-312) ----
+        if (kRender) {
+            // render: sequential per pixel (warps 0-1): colour/depth and the ordered
+            // contributor lists of retain_contributors
+            if (t < kTilePx) {
+                for (int e = 0; e < n; ++e) {
+                    const int s = pair_slot(e, 32, t);
+                    const double f = W[s];
+                    if (done || f < 0.0) {
+                        W[s] = 0.0;
+                        continue;
+                    }
+                    const double w = f * T;
+                    W[s] = w;
+                    if (vd.contrib) {  // retain_contributors (:310): depth ranks in order
+                        if (vd.contrib_offset)
+                            vd.contrib[vd.contrib_offset[pix_t] + ncontrib_px] = sp[e].aux;
+                        ++ncontrib_px;
+                    }
                     ac0 += scol[4 * e] * w;  // :289-291 (colour clamped at upload)
                     ac1 += scol[4 * e + 1] * w;
                     ac2 += scol[4 * e + 2] * w;
                     adep += sp[e].z * w;  // :293
+                    ++contrib;
+                    T = T * (1.0 - f);                        // :311
+                    if (p.opt.early_exit && T < p.opt.eps)   // :312
+                        done = true;
                 }
-                ++contrib;
-                T = T * (1.0 - f);                        // :311
-                if (p.opt.early_exit && T < p.opt.eps)   // :312
-                    done = true;
+                sdone[t] = done ? 1 : 0;
             }
-            sdone[t] = done ? 1 : 0;
-        } else if (want_sem) {
-            // channel-group bounds of each staged (class-sorted) row:
-            // bnd[e][g] = #entries with class < g * Cg
-            for (int u = t - kTilePx; u < n * (kGroups - 1); u += kThreads - kTilePx) {
-                const int e = u / (kGroups - 1);
-                const int gg = u - e * (kGroups - 1) + 1;
-                const int lim = gg * Cg;
-                const uint16_t* row = si + e * kpad;
-                int c = 0;
-                for (int j = 0; j < k; ++j) c += row[j] < lim ? 1 : 0;
-                bnd[e * kBnd + gg] = static_cast<uint16_t>(c);
-                if (gg == 1) {
-                    bnd[e * kBnd] = 0;
-                    bnd[e * kBnd + kGroups] = static_cast<uint16_t>(k);
+        } else {
+            // score: all 8 warps, 4 threads per pixel, 4 entries each. A segment starts at
+            // T_pixel * prod(earlier segments' (1 - f)) (fixed association); since T only
+            // decreases, a segment starting below eps lies after the early exit (:312).
+            const int part = t >> 6;
+            const int eb = 4 * part, ee = min(n, eb + 4);
+            const bool pdone = sdone[px] != 0;
+            double prod = 1.0;
+            if (!pdone)
+                for (int e = eb; e < ee; ++e) {
+                    const double f = W[pair_slot(e, 32, px)];
+                    if (f >= 0.0) prod = prod * (1.0 - f);
                 }
+            segp[part * kTilePx + px] = prod;
+            __syncthreads();
+            double Ts = sT[px];
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+                if (q < part) Ts = Ts * segp[q * kTilePx + px];
+            bool exited = pdone || (p.opt.early_exit && Ts < p.opt.eps);
+            double Tc = Ts;
+            for (int e = eb; e < ee; ++e) {
+                const int s = pair_slot(e, 32, px);
+                const double f = W[s];
+                if (exited || f < 0.0) {
+                    W[s] = 0.0;
+                    continue;
+                }
+                W[s] = f * Tc;
+                ++contrib;
+                Tc = Tc * (1.0 - f);
+                if (p.opt.early_exit && Tc < p.opt.eps) exited = true;
+            }
+            __syncthreads();  // all segments read sT / segp
+            if (part == 3) {
+                sT[px] = Tc;  // product over the batch (only its == 1 / < eps matter later)
+                sdone[px] = (pdone || (p.opt.early_exit && Tc < p.opt.eps)) ? 1 : 0;
             }
         }
         __syncthreads();
@@ -268,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
             for (int e = 0; e < n; ++e) {
                 const double2 w = W2[e * 32 + lane];
                 if (!__any_sync(0xffffffffu, (w.x != 0.0) | (w.y != 0.0))) continue;
-                const int lo = bnd[e * kBnd + g], hi = bnd[e * kBnd + g + 1];
+                const int lo = g == 0 ? 0 : sbnd[e * 8 + g - 1], hi = sbnd[e * 8 + g];
                 const uint16_t* ei = si + e * kpad;
                 const double* ep = spr + e * kpad;
                 if (kDup) {
@@ -304,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
             }
         }
         // early termination of the whole block (:312 for every pixel)
-        const int mine = (t < kTilePx) ? (done ? 1 : 0) : 1;
+        const int mine = kRender ? ((t < kTilePx) ? (done ? 1 : 0) : 1) : sdone[px];
         if (__syncthreads_and(mine)) break;
     }
     cp_async_wait_all();
@@ -358,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
                 S2 += red[q * kTilePx + t].y;
             }
             red_d[t] = inside ? log(S1) - S2 / S1 : 0.0;
-            red_u[t] = (inside && 1.0 - T == 0.0) ? 1ull : 0ull;  // explorer.cpp:198
+            red_u[t] = (inside && 1.0 - sT[t] == 0.0) ? 1ull : 0ull;  // explorer.cpp:198
         }
         __syncthreads();
         for (int s = kTilePx / 2; s > 0; s >>= 1) {  // fixed tree: deterministic
@@ -375,7 +409,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
         __syncthreads();
     }
     // K (contributors) for the measurement counters
-    if (t < kTilePx) red_u[t] = contrib;
+    if (kRender) {
+        if (t < kTilePx) red_u[t] = contrib;
+    } else {
+        for (int q = 0; q < 4; ++q) {  // fold the 4 segment threads of each pixel, in order
+            if ((t >> 6) == q) red_u[px] = (q == 0 ? 0ull : red_u[px]) + contrib;
+            __syncthreads();
+        }
+    }
     __syncthreads();
     for (int s = kTilePx / 2; s > 0; s >>= 1) {
         if (t < s) red_u[t] += red_u[t + s];
