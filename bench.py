@@ -159,6 +159,66 @@ def run_reference_arm(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def measure_render(ctx, stream, flush, args) -> dict:
+    """Full render (colour + depth + silhouette + 102-channel semantics, reference layout,
+    fp64) of one frame: device-resident planes and through the host API (D2H included),
+    for cfg0 (340x600, the paper's resolution) and cfg1 (680x1200); the reference's own
+    render() on one host core for cfg0 beside it (the paper publishes 3.1 ms/frame at
+    340x600x102 on an RTX A6000)."""
+    import torch
+    from paper_2506_00225_b200 import scenes
+    from paper_2506_00225_b200.splatmap import RenderChannels, render, render_device
+    out = {}
+    for cfg in (0, 1):
+        gm = scenes.make_map(cfg)
+        cam = scenes.CONFIGS[cfg].camera()
+        pose = scenes.render_poses(cfg, 1)[0]
+        px = cam.pixel_count()
+        C = gm.channels()
+        planes = torch.empty(px * (5 + C), dtype=torch.float64, device="cuda")
+        base = planes.data_ptr()
+        ptrs = dict(sil_ptr=base, color_ptr=base + 8 * px, depth_ptr=base + 32 * px,
+                    sem_ptr=base + 40 * px)
+        ch = RenderChannels.all()
+        for _ in range(3):
+            render_device(gm, cam, pose, ch, ctx=ctx, **ptrs)
+        ms = []
+        for _ in range(max(3, args.steps)):
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            render_device(gm, cam, pose, ch, ctx=ctx, **ptrs)
+            e1.record(stream)
+            e1.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        render(gm, cam, pose, ch, ctx=ctx)
+        t0 = time.perf_counter()
+        reps = 2
+        for _ in range(reps):
+            render(gm, cam, pose, ch, ctx=ctx)
+        host_ms = (time.perf_counter() - t0) * 1e3 / reps
+        entry = {"device_ms": float(np.median(ms)), "e2e_host_ms": host_ms,
+                 "planes_bytes": int(8 * px * (5 + C)),
+                 "resolution": f"{cam.width}x{cam.height}x{C}"}
+        if cfg == 0:
+            try:
+                import oracle
+                ref = oracle.RefLib()
+                h = ref.map_create(gm)
+                ref.render(gm, cam, pose, 7, handle=h, n_map=gm.size())
+                t0 = time.perf_counter()
+                ref.render(gm, cam, pose, 7, handle=h, n_map=gm.size())
+                entry["reference_cpu_1core_ms"] = (time.perf_counter() - t0) * 1e3
+                ref.map_destroy(h)
+            except Exception as exc:
+                entry["reference_cpu_1core_ms"] = repr(exc)
+        out[f"cfg{cfg}"] = entry
+        del planes
+    return out
+
+
 def workload_config(cfg: int) -> dict:
     from paper_2506_00225_b200 import scenes
     sc = scenes.CONFIGS[cfg]
@@ -180,6 +240,8 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="use the torch.distributed path (NCCL broadcast / all-gather) even at N=1")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
@@ -194,17 +256,18 @@ def main() -> None:
                                                 refresh_candidate_scores, score_poses)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    dist_on = world > 1 or args.force_dist
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if dist_on:
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     cfg = args.config
     sc = scenes.CONFIGS[cfg]
     cam = sc.camera()
     gm = scenes.make_map(cfg) if rank == 0 else None
-    if world > 1:
+    if dist_on:
         gm = sd.broadcast_map(gm)  # C1 over NCCL
     n_total = VIEWS_PER_GPU * world
     cands = scenes.make_candidates(cfg, n_total)
@@ -218,13 +281,13 @@ def main() -> None:
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def barrier():
-        if world > 1:
+        if dist_on:
             tdist.barrier()
         torch.cuda.synchronize()
 
     def step_resident():
         nm, es = score_poses(gm, cam, poses, ctx=ctx)
-        if world > 1:
+        if dist_on:
             nm, es = sd.gather_scores(n_total, nm, es)
         return nm, es
 
@@ -251,7 +314,7 @@ def main() -> None:
     st = ctx.stats()
     ctx.set_profiling(False)
     total_ms = float(np.sum(step_ms))
-    if world > 1:
+    if dist_on:
         t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         total_ms = float(t.item())
@@ -297,6 +360,14 @@ def main() -> None:
     except Exception as exc:  # reported, not fatal
         fisher = {"error": repr(exc)}
 
+    # ---- secondary metric: semantic render ms/frame (device-resident and e2e) ----
+    render_info = None
+    if rank == 0:
+        try:
+            render_info = measure_render(ctx, stream, flush, args)
+        except Exception as exc:  # reported, not fatal
+            render_info = {"error": repr(exc)}
+
     # ---- e2e through the public API (host inputs, map re-upload every step) ----
     h2d = int(gm.centers.nbytes + gm.log_radii.nbytes + gm.opacity_logits.nbytes +
               gm.colors.nbytes + gm.sem_indices.nbytes + gm.sem_probs.nbytes) + 96 * len(mine)
@@ -310,7 +381,7 @@ def main() -> None:
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         refresh_candidate_scores(fresh, gm, cam, ctx=ctx)
-        if world > 1:
+        if dist_on:
             sd.gather_scores(n_total, np.array([c.n_missing for c in fresh]),
                              np.array([c.entropy_sum for c in fresh]))
         ev1.record(stream)
@@ -318,7 +389,7 @@ def main() -> None:
         if i >= args.warmup:
             e2e_ms.append(ev0.elapsed_time(ev1))
     e2e_total = float(np.sum(e2e_ms))
-    if world > 1:
+    if dist_on:
         t = torch.tensor([e2e_total], dtype=torch.float64, device="cuda")
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         e2e_total = float(t.item())
@@ -393,9 +464,10 @@ def main() -> None:
             "cpu_baseline": cpu_baseline, "clocks": clk,
             "argmax_view": int(best), "views_total_per_step": n_total,
             "with_fisher_gain": fisher,
+            "render_ms_per_frame": render_info,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         tdist.destroy_process_group()
 
 

@@ -525,6 +525,24 @@ def render(gmap: GaussianMap, camera: CameraModel, pose: Pose,
     return out
 
 
+def render_device(gmap: GaussianMap, camera: CameraModel, pose: Pose, channels: RenderChannels,
+                  options: Optional[RenderOptions] = None, ctx: Optional[Context] = None, *,
+                  color_ptr: int = 0, depth_ptr: int = 0, sil_ptr: int = 0,
+                  sem_ptr: int = 0) -> int:
+    """render() into caller-owned DEVICE planes (reference layout, fp64), on the ctx stream
+    (sgm_render_device). Returns the number of projections."""
+    c = _ctx(ctx)
+    handle = c.upload(gmap)
+    nproj = C.c_uint64()
+    opt = (options if options is not None else RenderOptions())._c()
+    cam_c, pose_c = camera._c(), pose._c()
+    c.check(N.lib.sgm_render_device(c.handle, handle, C.byref(cam_c), C.byref(pose_c),
+                                    channels.flags(), C.byref(opt), color_ptr or None,
+                                    depth_ptr or None, sil_ptr or None, sem_ptr or None,
+                                    C.byref(nproj)))
+    return nproj.value
+
+
 def bins_of_last_render(tiles: int, ctx: Optional[Context] = None):
     """The tile bins the last render() on `ctx` built at RenderOptions::tile_size
     (bit-exactness hook; splat_render.cpp:188-213 keeps them local):
