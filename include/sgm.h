@@ -178,6 +178,21 @@ int sgm_score_views_fisher(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* c
                            const sgm_pose* poses, const sgm_options* opt, double* n_missing,
                            double* entropy_sum, double* fisher_gain);
 
+/* ---- mapping step: losses + analytic backward ----
+ * Renders the map at `pose` (render(..., RenderChannels::all(true)), splat_render.cpp:170),
+ * then mapping_loss + semantic_loss (losses.cpp:40-160) against the frame planes (rgb px*3,
+ * depth px, sem px*(num_classes+1), float, Frame layout, frame.hpp:12-65) and backward
+ * (losses.cpp:162-362). weights = {lambda_hd, lambda_cos, mask_k, use_hd, use_cos, use_kl,
+ * kl_clip_norm} (LossWeights, losses.hpp:9-17); report = {photometric, depth, semantic,
+ * photometric_px, depth_px, semantic_px, uncovered_px} (LossReport). Gradient arrays are the
+ * ParamGradients spans (center 3N, log_radius N, opacity_logit N, color 3N, sem kN) and may
+ * be NULL. A non-finite gradient fails like the reference's throw. */
+int sgm_backward(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam, const sgm_pose* pose,
+                 const sgm_options* opt, const float* rgb, const float* depth, const float* sem,
+                 const double weights[7], int include_mapping, int include_semantic,
+                 double report[7], double* g_center, double* g_log_radius,
+                 double* g_opacity_logit, double* g_color, double* g_sem);
+
 /* combine_scores (explorer.cpp:225-248) on host fp64: returns 1 if any i_total > 0,
  * 0 if the pool is exhausted (or n == 0), negative on invalid arguments. */
 int sgm_combine_scores(uint64_t n, const double* n_missing, const double* entropy_sum,

@@ -309,6 +309,40 @@ class RefLib:
         L.ref_random_splat_map.argtypes = [C.c_uint64, _pi32, _pd, _pd, _pd, _pd, _pd, _pd, _pd,
                                            _pd, _pu16, _pd, _pi32]
         L.ref_camera_from_fov.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, _pd]
+        L.ref_backward.restype = C.c_int
+        L.ref_backward.argtypes = [C.c_void_p, _pi32, _pd, _pd, _pd, _pd, C.c_int, _pf, _pf, _pf,
+                                   _pd, C.c_int, C.c_int, _pd, _pd, _pd, _pd, _pd, _pd,
+                                   C.c_char_p, C.c_int]
+
+    def backward(self, m, cam, frame, weights, include_mapping=True, include_semantic=True,
+                 opt=None):
+        """The reference's render(all(true)) + mapping_loss + semantic_loss + backward."""
+        h = self.map_create(m)
+        wh, intr = self._cam(cam)
+        R, t = self._pose(frame.pose)
+        o = self._opts(opt)
+        n, k = m.size(), m.k()
+        wv = np.array([weights.lambda_hd, weights.lambda_cos, float(weights.mask_k),
+                       float(weights.use_hd), float(weights.use_cos), float(weights.use_kl),
+                       weights.kl_clip_norm])
+        rep = np.zeros(7)
+        out = {"center": np.zeros(3 * n), "log_radius": np.zeros(n),
+               "opacity_logit": np.zeros(n), "color": np.zeros(3 * n), "sem": np.zeros(k * n)}
+        err = C.create_string_buffer(512)
+        pf = C.POINTER(C.c_float)
+        rgb = np.ascontiguousarray(frame.rgb, dtype=np.float32)
+        dep = np.ascontiguousarray(frame.depth, dtype=np.float32)
+        sem = np.ascontiguousarray(frame.sem, dtype=np.float32)
+        rc = self.lib.ref_backward(h, wh.ctypes.data_as(_pi32), _dp(intr), _dp(R), _dp(t), _dp(o),
+                                   frame.num_classes, rgb.ctypes.data_as(pf), dep.ctypes.data_as(pf),
+                                   sem.ctypes.data_as(pf), _dp(wv), int(include_mapping),
+                                   int(include_semantic), _dp(rep), _dp(out["center"]),
+                                   _dp(out["log_radius"]), _dp(out["opacity_logit"]),
+                                   _dp(out["color"]), _dp(out["sem"]), err, 512)
+        self.map_destroy(h)
+        if rc != 0:
+            raise RuntimeError(err.value.decode())
+        return rep, out
 
     # --- maps
     def map_create(self, m):

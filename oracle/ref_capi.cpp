@@ -258,3 +258,67 @@ void ref_camera_from_fov(int w, int h, double vfov, double hfov, double out[6]) 
 }
 
 }  // extern "C"
+
+// ---- losses + backward (proj/src/losses.cpp) over the reference's own render ----
+#include "splatmap/losses.hpp"
+
+extern "C" {
+
+// weights = {lambda_hd, lambda_cos, mask_k, use_hd, use_cos, use_kl, kl_clip_norm};
+// report  = {photometric, depth, semantic, photometric_px, depth_px, semantic_px, uncovered_px}
+// grads: center 3N, log_radius N, opacity_logit N, color 3N, sem kN. Returns 0, or 1 when the
+// reference throws (message copied to err).
+int ref_backward(void* m, const int32_t wh[2], const double intr[4], const double R[9],
+                 const double t[3], const double opts[5], int num_classes, const float* rgb,
+                 const float* depth, const float* sem, const double weights[7],
+                 int include_mapping, int include_semantic, double* report, double* g_center,
+                 double* g_logr, double* g_logit, double* g_color, double* g_sem, char* err,
+                 int err_cap) {
+    const GaussianMap& map = static_cast<RefMap*>(m)->map;
+    CameraModel cam = make_cam(wh, intr);
+    Frame fr;
+    fr.width = cam.width;
+    fr.height = cam.height;
+    fr.num_classes = num_classes;
+    fr.pose = make_pose(R, t);
+    fr.allocate();
+    const size_t px = static_cast<size_t>(cam.width) * cam.height;
+    std::memcpy(fr.rgb.data(), rgb, px * 3 * 4);
+    std::memcpy(fr.depth.data(), depth, px * 4);
+    std::memcpy(fr.sem.data(), sem, px * fr.channels() * 4);
+    LossWeights w;
+    w.lambda_hd = weights[0];
+    w.lambda_cos = weights[1];
+    w.mask_k = static_cast<int>(weights[2]);
+    w.use_hd = weights[3] != 0.0;
+    w.use_cos = weights[4] != 0.0;
+    w.use_kl = weights[5] != 0.0;
+    w.kl_clip_norm = weights[6];
+    try {
+        RenderOutput out = render(map, cam, fr.pose, RenderChannels::all(true), make_opts(opts));
+        LossReport a = mapping_loss(out, fr);
+        LossReport b = semantic_loss(out, fr, w);
+        report[0] = a.photometric;
+        report[1] = a.depth;
+        report[2] = b.semantic;
+        report[3] = static_cast<double>(a.photometric_px);
+        report[4] = static_cast<double>(a.depth_px);
+        report[5] = static_cast<double>(b.semantic_px);
+        report[6] = static_cast<double>(b.uncovered_px);
+        ParamGradients g = backward(out, fr, map, w, include_mapping != 0, include_semantic != 0);
+        std::memcpy(g_center, g.center.data(), g.center.size() * 8);
+        std::memcpy(g_logr, g.log_radius.data(), g.log_radius.size() * 8);
+        std::memcpy(g_logit, g.opacity_logit.data(), g.opacity_logit.size() * 8);
+        std::memcpy(g_color, g.color.data(), g.color.size() * 8);
+        std::memcpy(g_sem, g.sem.data(), g.sem.size() * 8);
+    } catch (const std::exception& e) {
+        if (err && err_cap > 0) {
+            std::strncpy(err, e.what(), err_cap - 1);
+            err[err_cap - 1] = 0;
+        }
+        return 1;
+    }
+    return 0;
+}
+
+}  // extern "C"

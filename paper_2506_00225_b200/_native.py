@@ -104,6 +104,9 @@ SIGNATURES = {
     "sgm_score_views_fisher": (C.c_int, [_vp, _vp, C.POINTER(sgm_camera), C.c_uint64,
                                          C.POINTER(sgm_pose), C.POINTER(sgm_options), _pd, _pd,
                                          _pd]),
+    "sgm_backward": (C.c_int, [_vp, _vp, C.POINTER(sgm_camera), C.POINTER(sgm_pose),
+                               C.POINTER(sgm_options), _pf, _pf, _pf, _pd, C.c_int, C.c_int, _pd,
+                               _pd, _pd, _pd, _pd, _pd]),
     "sgm_combine_scores": (C.c_int, [C.c_uint64, _pd, _pd, _pd, _pd, _pd, _pd, _pd]),
     "sgm_candidate_pose": (None, [_pd, _pd, C.POINTER(sgm_pose)]),
     "sgm_look_at": (None, [_pd, _pd, C.POINTER(sgm_pose)]),

@@ -125,8 +125,9 @@ struct sgm_map {
     bool has_prior = false;
     DevBuf geo;    // cx, cy, cz, rad, alpha (5 x n doubles)
     DevBuf color;  // [n][4]
-    DevBuf idx;    // [n][k] u16
-    DevBuf prob;   // [n][k] f64
+    DevBuf idx;    // [n][kpad] u16 (class-sorted)
+    DevBuf prob;   // [n][kpad] f64
+    DevBuf perm;   // [n][kpad] u16 original entry index
 };
 
 struct sgm_ctx {
@@ -145,7 +146,8 @@ struct sgm_ctx {
     DevBuf poses, vcount, pcount, keys, vals, keys_alt, vals_alt, packed, counts, offsets, rects,
         bounds;
     DevBuf tkeys, tvals, tkeys_alt, tvals_alt, ranges, ent_part, miss_part, views, out,
-        contributors, cub_tmp, planes, dbg, ccount, coffset, contrib, fis_part;
+        contributors, cub_tmp, planes, dbg, ccount, coffset, contrib, fis_part, bw_frame,
+        bw_flags, bw_part, bw_grad;
     uint64_t last_ncontrib = 0;
     bool last_has_contrib = false;
     int last_px = 0;
@@ -755,10 +757,12 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, con
         ctx->take(m->color, col_b);
         ctx->take(m->idx, 2 * ns * kpad);
         ctx->take(m->prob, 8 * ns * kpad);
+        ctx->take(m->perm, 2 * ns * kpad);
         CK(m->geo.reserve(geo_b));
         CK(m->color.reserve(col_b));
         CK(m->idx.reserve(2 * ns * kpad));
         CK(m->prob.reserve(8 * ns * kpad));
+        CK(m->perm.reserve(2 * ns * kpad));
         CK(ctx->upload_tmp.reserve(idx_b + prob_b + 64));
         char* draw = ctx->upload_tmp.as<char>();
         CK(cudaMemcpyAsync(m->geo.p, geo, geo_b, cudaMemcpyHostToDevice, s));
@@ -768,7 +772,7 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, con
         // rows sorted by class id (stable) and padded to kpad, on the GPU
         launch_sort_rows(reinterpret_cast<const uint16_t*>(draw + prob_b),
                          reinterpret_cast<const double*>(draw), n, k, kpad, m->idx.as<uint16_t>(),
-                         m->prob.as<double>(), s);
+                         m->prob.as<double>(), m->perm.as<uint16_t>(), s);
         ctx->stats.kernel_launches += n ? 1 : 0;
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(s));
@@ -786,6 +790,7 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, con
         d.color4 = m->color.as<double>();
         d.sem_idx = m->idx.as<uint16_t>();
         d.sem_prob = m->prob.as<double>();
+        d.sem_perm = m->perm.as<uint16_t>();
         d.dup_idx = has_dup;
         m->groups = choose_groups(C, k);
         *out = m;
@@ -806,6 +811,7 @@ void sgm_map_release(sgm_ctx* ctx, sgm_map* map) {
         ctx->give(std::move(map->color));
         ctx->give(std::move(map->idx));
         ctx->give(std::move(map->prob));
+        ctx->give(std::move(map->perm));
     }
     delete map;
 }
@@ -1015,6 +1021,141 @@ int sgm_score_views_fisher(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* c
         for (uint64_t i = 0; i < n; ++i) pp[i] = to_pose(poses[i]);
         run_views(ctx, map, cam, o, n, pp.data(), Mode::Score, RenderTargets{}, n_missing, entropy_sum,
                   Fisher::Gain, fisher_gain, nullptr);
+    });
+}
+
+int sgm_backward(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const sgm_pose* pose,
+                 const sgm_options* opt, const float* rgb, const float* depth, const float* sem,
+                 const double weights[7], int include_mapping, int include_semantic,
+                 double report[7], double* g_center, double* g_log_radius,
+                 double* g_opacity_logit, double* g_color, double* g_sem) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!map || !pose || !rgb || !depth || !sem || !weights || !report)
+            fail(SGM_ERR_INVALID, "null argument");
+        const CamParams cam = to_cam(camera);
+        const OptParams o = to_opt(opt, cam);
+        const PoseParams p = to_pose(*pose);
+        cudaStream_t s = ctx->stream;
+        const size_t px = static_cast<size_t>(cam.W) * cam.H;
+        const int C = map->dev.C, k = map->dev.k;
+        const uint64_t N = map->dev.n;
+        const size_t NS = std::max<uint64_t>(N, 1);
+        // device planes: rendered (sil, color, depth, sem) + frame (rgb, depth, sem)
+        const size_t rend_b = 8 * px * (5 + C), frame_b = 4 * px * (4 + C);
+        CK(ctx->planes.reserve(rend_b));
+        CK(ctx->bw_frame.reserve(frame_b + 16));
+        CK(ctx->ccount.reserve(4 * (px + 1)));
+        CK(ctx->contrib.reserve(4));
+        CK(ctx->bw_flags.reserve(px + 16));
+        const size_t nlb = backward_loss_blocks(cam.W, cam.H);
+        CK(ctx->bw_part.reserve(64 * nlb + 64 + 64));
+        CK(ctx->bw_grad.reserve(8 * (NS * (8 + k) + 5 * NS) + 64));
+        double* d_sil = ctx->planes.as<double>();
+        double* d_color = d_sil + px;
+        double* d_depth = d_color + 3 * px;
+        double* d_sem = d_depth + px;
+        float* f_rgb = ctx->bw_frame.as<float>();
+        float* f_depth = f_rgb + 3 * px;
+        float* f_sem = f_depth + px;
+        CK(cudaMemcpyAsync(f_rgb, rgb, 12 * px, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(f_depth, depth, 4 * px, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(f_sem, sem, 4 * px * C, cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(ctx->ccount.p, 0, 4 * (px + 1), s));
+        // 1. forward render + contributor counts (the reference's render(..., all(true)))
+        RenderTargets rt;
+        rt.channels = SGM_COLOR | SGM_DEPTH | SGM_SEMANTICS;
+        rt.color = d_color;
+        rt.depth = d_depth;
+        rt.sil = d_sil;
+        rt.sem = d_sem;
+        rt.contrib = ctx->contrib.as<uint32_t>();
+        rt.contrib_count = ctx->ccount.as<uint32_t>();
+        run_views(ctx, map, cam, o, 1, &p, Mode::Render, rt, nullptr, nullptr);
+        const uint32_t V = ctx->last_V;
+        // 2. loss masks, reports and mask counts
+        double* g = ctx->bw_grad.as<double>();
+        BackwardParams b{};
+        b.W = cam.W;
+        b.H = cam.H;
+        b.C = C;
+        b.color = d_color;
+        b.depth = d_depth;
+        b.sil = d_sil;
+        b.sem = d_sem;
+        b.ccount = ctx->ccount.as<uint32_t>();
+        b.rgb = f_rgb;
+        b.fdepth = f_depth;
+        b.fsem = f_sem;
+        b.flags = ctx->bw_flags.as<uint8_t>();
+        b.tau = std::log(weights[2]);
+        b.lambda_hd = weights[0];
+        b.lambda_cos = weights[1];
+        b.use_hd = weights[3] != 0.0;
+        b.use_cos = weights[4] != 0.0;
+        b.use_kl = weights[5] != 0.0;
+        b.include_mapping = include_mapping != 0;
+        b.include_semantic = include_semantic != 0;
+        double* totals = ctx->bw_part.as<double>() + 8 * nlb;
+        b.totals = totals;
+        b.gcenter = g;
+        b.glogr = g + 3 * NS;
+        b.glogit = g + 4 * NS;
+        b.gcolor = g + 5 * NS;
+        b.gsem = g + 8 * NS;
+        b.gproj = g + (8 + k) * NS;
+        b.sem_perm = map->dev.sem_perm;
+        CK(cudaMemsetAsync(g, 0, 8 * (NS * (8 + k) + 5 * NS), s));
+        launch_loss_pixels(b, ctx->bw_part.as<double>(), totals, s);
+        // 3. backward over the block lists of the render above (same binning)
+        RasterParams rp{};
+        rp.map = map->dev;
+        rp.cam = cam;
+        rp.opt = o;
+        rp.views = ctx->views.as<ViewDesc>();
+        rp.tiles_per_view = ((cam.W + kTile - 1) / kTile) * ((cam.H + kTile - 1) / kTile);
+        rp.raster_tiles_x = (cam.W + kTile - 1) / kTile;
+        rp.channels = rt.channels;
+        rp.groups = map->groups;
+        launch_backward(rp, b, s);
+        // 4. projection -> world, KL clipping, finiteness
+        launch_chain(map->dev, ctx->poses.as<PoseParams>(), cam, o, ctx->vals.as<uint32_t>(), V,
+                     b.gproj, b, s);
+        if (b.use_kl && b.include_semantic && weights[6] > 0.0)
+            launch_kl_clip(b.gsem, N, k, weights[6], s);
+        unsigned long long* bad = reinterpret_cast<unsigned long long*>(totals + 8);
+        CK(cudaMemsetAsync(bad, 0xff, 5 * 8, s));
+        const double* arrs[5] = {b.gcenter, b.glogr, b.glogit, b.gcolor, b.gsem};
+        const uint64_t lens[5] = {3 * N, N, N, 3 * N, static_cast<uint64_t>(k) * N};
+        for (int a = 0; a < 5; ++a) launch_finite(arrs[a], lens[a], bad + a, s);
+        ctx->stats.kernel_launches += 4 + 5;
+        CK(cudaGetLastError());
+        double h_tot[8];
+        unsigned long long h_bad[5];
+        CK(cudaMemcpyAsync(h_tot, totals, 64, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(h_bad, bad, 40, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        static const char* names[5] = {"center", "log_radius", "opacity_logit", "color", "sem"};
+        static const uint64_t stride[5] = {3, 1, 1, 3, 0};
+        for (int a = 0; a < 5; ++a)
+            if (h_bad[a] != ~0ull)  // losses.cpp:349-360
+                fail(SGM_ERR_INVALID, "backward: non-finite gradient for gaussian %llu parameter %s",
+                     static_cast<unsigned long long>(h_bad[a] / (a == 4 ? k : stride[a])), names[a]);
+        report[0] = h_tot[3] > 0 ? h_tot[0] / h_tot[3] : 0.0;  // photometric (:57)
+        report[1] = h_tot[4] > 0 ? h_tot[1] / h_tot[4] : 0.0;  // depth (:58)
+        report[2] = h_tot[5] > 0 ? h_tot[2] / h_tot[5] : 0.0;  // semantic (:158)
+        report[3] = h_tot[3];
+        report[4] = h_tot[4];
+        report[5] = h_tot[5];
+        report[6] = h_tot[6];
+        if (N) {
+            if (g_center) CK(cudaMemcpyAsync(g_center, b.gcenter, 24 * N, cudaMemcpyDeviceToHost, s));
+            if (g_log_radius) CK(cudaMemcpyAsync(g_log_radius, b.glogr, 8 * N, cudaMemcpyDeviceToHost, s));
+            if (g_opacity_logit) CK(cudaMemcpyAsync(g_opacity_logit, b.glogit, 8 * N, cudaMemcpyDeviceToHost, s));
+            if (g_color) CK(cudaMemcpyAsync(g_color, b.gcolor, 24 * N, cudaMemcpyDeviceToHost, s));
+            if (g_sem) CK(cudaMemcpyAsync(g_sem, b.gsem, 8 * N * k, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
     });
 }
 

@@ -30,6 +30,7 @@ struct DevMap {
     // Rows padded to kpad with (0xffff, 0.0) so every row is 16-byte aligned.
     const uint16_t* sem_idx = nullptr;  // [n][kpad]
     const double* sem_prob = nullptr;   // [n][kpad]
+    const uint16_t* sem_perm = nullptr; // [n][kpad] original entry index of each sorted slot
     int dup_idx = 0;  // some Gaussian lists a class twice: serialise its RMWs
 };
 
@@ -78,6 +79,32 @@ struct GroupParams {
 struct FisherParams {
     double* H;           // [N][8] prior accumulation (prior mode)
     const double* invp;  // [N][8] 1 / (H_prior + lambda) (gain mode)
+};
+
+// Backward pass (sgm_backward.cu): mapping / semantic losses and their gradients.
+struct BackwardParams {
+    int W, H, C;
+    const double* color;     // rendered planes (device, reference layout)
+    const double* depth;
+    const double* sil;
+    const double* sem;
+    const uint32_t* ccount;  // contributors per pixel
+    const float* rgb;        // frame planes (device): px*3, px, px*C
+    const float* fdepth;
+    const float* fsem;
+    uint8_t* flags;          // per pixel: bit0 photometric mask, bit1 semantic mask
+    double tau;              // ln(mask_k)
+    double lambda_hd, lambda_cos;
+    int use_hd, use_cos, use_kl;
+    int include_mapping, include_semantic;
+    const double* totals;    // device [8] (k_loss_pixels)
+    double* gproj;           // [V][5] projection-space (alpha, mx, my, rad, z)
+    double* gcenter;         // [N][3]
+    double* glogr;           // [N]
+    double* glogit;          // [N]
+    double* gcolor;          // [N][3]
+    double* gsem;            // [N][k] (original entry order)
+    const uint16_t* sem_perm;
 };
 
 // Per view of a raster batch.
@@ -145,7 +172,16 @@ void launch_bins_to_ids(const uint32_t* list, uint64_t P, const PackedSplat* pac
                         uint32_t* ids, float* probe3, cudaStream_t s);
 
 void launch_sort_rows(const uint16_t* idx, const double* prob, uint64_t n, int k, int kpad,
-                      uint16_t* out_idx, double* out_prob, cudaStream_t s);
+                      uint16_t* out_idx, double* out_prob, uint16_t* out_perm, cudaStream_t s);
+// sgm_backward.cu
+size_t backward_loss_blocks(int W, int H);
+void launch_loss_pixels(const BackwardParams& b, double* part, double* totals, cudaStream_t s);
+void launch_backward(const RasterParams& p, const BackwardParams& b, cudaStream_t s);
+void launch_chain(const DevMap& m, const PoseParams* d_pose, const CamParams& cam, const OptParams& o,
+                  const uint32_t* order, uint32_t V, const double* gproj, const BackwardParams& b,
+                  cudaStream_t s);
+void launch_kl_clip(double* gsem, uint64_t n, int k, double clip, cudaStream_t s);
+void launch_finite(const double* v, uint64_t len, unsigned long long* bad, cudaStream_t s);
 
 // sgm_raster.cu
 GroupParams choose_groups(int C, int k);

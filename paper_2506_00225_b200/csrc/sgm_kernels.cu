@@ -357,11 +357,13 @@ __global__ void k_bins_to_ids(const uint32_t* __restrict__ list, uint64_t P,
 // listing a class twice keeps their order) and pads it to kpad with
 // (0xffff, 0.0). Per-class addition order in the compositor is unchanged.
 __global__ void k_sort_rows(const uint16_t* __restrict__ idx, const double* __restrict__ prob,
-                            uint64_t n, int k, int kpad, uint16_t* out_idx, double* out_prob) {
+                            uint64_t n, int k, int kpad, uint16_t* out_idx, double* out_prob,
+                            uint16_t* out_perm) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     uint16_t* oi = out_idx + i * kpad;
     double* op = out_prob + i * kpad;
+    uint16_t* om = out_perm + i * kpad;
     for (int j = 0; j < k; ++j) {
         const uint16_t c = idx[i * k + j];
         const double pv = prob[i * k + j];
@@ -369,14 +371,17 @@ __global__ void k_sort_rows(const uint16_t* __restrict__ idx, const double* __re
         while (q > 0 && oi[q - 1] > c) {
             oi[q] = oi[q - 1];
             op[q] = op[q - 1];
+            om[q] = om[q - 1];
             --q;
         }
         oi[q] = c;
         op[q] = pv;
+        om[q] = static_cast<uint16_t>(j);
     }
     for (int j = k; j < kpad; ++j) {
         oi[j] = 0xffff;
         op[j] = 0.0;
+        om[j] = 0;
     }
 }
 
@@ -440,9 +445,10 @@ void launch_debug_projections(const DevMap& m, const PoseParams* d_pose, const C
 }
 
 void launch_sort_rows(const uint16_t* idx, const double* prob, uint64_t n, int k, int kpad,
-                      uint16_t* out_idx, double* out_prob, cudaStream_t s) {
+                      uint16_t* out_idx, double* out_prob, uint16_t* out_perm, cudaStream_t s) {
     if (n == 0) return;
-    k_sort_rows<<<blocks_for(n, 256), 256, 0, s>>>(idx, prob, n, k, kpad, out_idx, out_prob);
+    k_sort_rows<<<blocks_for(n, 256), 256, 0, s>>>(idx, prob, n, k, kpad, out_idx, out_prob,
+                                                   out_perm);
 }
 
 void launch_bins_to_ids(const uint32_t* list, uint64_t P, const PackedSplat* packed,

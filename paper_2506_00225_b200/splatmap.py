@@ -641,6 +641,100 @@ def score_poses(gmap: GaussianMap, camera: CameraModel, poses: Sequence[Pose],
     return nm, es
 
 
+# --------------------------------------------------------------------------- mapping step
+
+@dataclass
+class Frame:
+    """Posed RGB-D-semantic observation (frame.hpp:12-65): rgb (H*W*3), depth (H*W, 0 =
+    invalid), sem (H*W*(num_classes+1)), all float32."""
+
+    width: int
+    height: int
+    num_classes: int
+    pose: Pose
+    rgb: np.ndarray
+    depth: np.ndarray
+    sem: np.ndarray
+
+    def channels(self) -> int:
+        return self.num_classes + 1
+
+
+@dataclass
+class LossWeights:
+    """losses.hpp:9-17."""
+
+    lambda_hd: float = 0.8
+    lambda_cos: float = 0.2
+    mask_k: int = 16
+    use_hd: bool = True
+    use_cos: bool = True
+    use_kl: bool = False
+    kl_clip_norm: float = 1.0
+
+
+@dataclass
+class LossReport:
+    """losses.hpp:19-31."""
+
+    photometric: float = 0.0
+    depth: float = 0.0
+    semantic: float = 0.0
+    photometric_px: int = 0
+    depth_px: int = 0
+    semantic_px: int = 0
+    uncovered_px: int = 0
+
+    def mapping_total(self) -> float:
+        return self.depth + 0.5 * self.photometric
+
+    def total(self) -> float:
+        return self.mapping_total() + self.semantic
+
+
+@dataclass
+class ParamGradients:
+    """losses.hpp:47-63 (arrays parallel to GaussianMap storage)."""
+
+    center: np.ndarray
+    log_radius: np.ndarray
+    opacity_logit: np.ndarray
+    color: np.ndarray
+    sem: np.ndarray
+
+
+def backward(gmap: GaussianMap, camera: CameraModel, frame: Frame,
+             weights: Optional[LossWeights] = None, include_mapping: bool = True,
+             include_semantic: bool = True, options: Optional[RenderOptions] = None,
+             ctx: Optional[Context] = None):
+    """One mapping step on the GPU: render(map, camera, frame.pose, all(true)), mapping_loss +
+    semantic_loss, and the analytic backward (losses.cpp:40-362). Returns (LossReport,
+    ParamGradients); raises like the reference on a non-finite gradient."""
+    w = weights if weights is not None else LossWeights()
+    c = _ctx(ctx)
+    handle = c.upload(gmap)
+    n, k = gmap.size(), gmap.k()
+    wv = np.array([w.lambda_hd, w.lambda_cos, float(w.mask_k), float(w.use_hd),
+                   float(w.use_cos), float(w.use_kl), w.kl_clip_norm])
+    rep = np.zeros(7)
+    g = ParamGradients(np.zeros(3 * n), np.zeros(n), np.zeros(n), np.zeros(3 * n), np.zeros(k * n))
+    rgb = np.ascontiguousarray(frame.rgb, dtype=np.float32)
+    dep = np.ascontiguousarray(frame.depth, dtype=np.float32)
+    sem = np.ascontiguousarray(frame.sem, dtype=np.float32)
+    pf = C.POINTER(C.c_float)
+    opt = (options if options is not None else RenderOptions())._c()
+    cam_c, pose_c = camera._c(), frame.pose._c()
+    c.check(N.lib.sgm_backward(c.handle, handle, C.byref(cam_c), C.byref(pose_c), C.byref(opt),
+                               rgb.ctypes.data_as(pf), dep.ctypes.data_as(pf),
+                               sem.ctypes.data_as(pf), N.dptr(wv), int(include_mapping),
+                               int(include_semantic), N.dptr(rep), N.dptr(g.center),
+                               N.dptr(g.log_radius), N.dptr(g.opacity_logit), N.dptr(g.color),
+                               N.dptr(g.sem)))
+    report = LossReport(float(rep[0]), float(rep[1]), float(rep[2]), int(rep[3]), int(rep[4]),
+                        int(rep[5]), int(rep[6]))
+    return report, g
+
+
 def fisher_prior(gmap: GaussianMap, camera: CameraModel, poses: Sequence[Pose],
                  lam: float = 1.0, options: Optional[RenderOptions] = None,
                  ctx: Optional[Context] = None) -> np.ndarray:
