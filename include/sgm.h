@@ -202,6 +202,59 @@ int sgm_combine_scores(uint64_t n, const double* n_missing, const double* entrop
 void sgm_candidate_pose(const double position[3], const double direction[3], sgm_pose* out);
 void sgm_look_at(const double position[3], const double target[3], sgm_pose* out);
 
+/* ---- exploration map + candidate sampling ----
+ * Replaces splatmap::ExplorationMap (explorer.hpp:11-83, explorer.cpp:11-139) with a
+ * device-resident u8 grid (0 unknown, 1 free, 2 occupied; linear id (iz*dy + iy)*dx + ix)
+ * and a device changelog. Results are bit-identical to the reference: the same voxel
+ * states, counts and changelog order. */
+typedef struct sgm_emap sgm_emap;
+
+/* Aabb (geometry.hpp:58-67). */
+typedef struct {
+    double min[3];
+    double max[3];
+} sgm_aabb;
+
+/* ExplorationMap(bounds, voxel_size) (explorer.cpp:11-20): origin = bounds.min,
+ * dims = max(ceil(extent / voxel), 1). voxel_size <= 0 -> SGM_ERR_INVALID. */
+int sgm_emap_create(sgm_ctx* ctx, const sgm_aabb* bounds, double voxel_size, sgm_emap** out);
+void sgm_emap_destroy(sgm_ctx* ctx, sgm_emap* emap);
+/* origin(), voxel_size(), dims(), free_count(), occupied_count(), changelog_size(). Any
+ * output may be NULL. */
+int sgm_emap_info(sgm_ctx* ctx, const sgm_emap* emap, double origin[3], double* voxel_size,
+                  int32_t dims[3], uint64_t* free_count, uint64_t* occupied_count,
+                  uint64_t* changelog_size);
+/* integrate_frame (explorer.cpp:53-110): the Amanatides-Woo walk of every stride-th depth
+ * pixel. depth is the Frame depth plane (cam->width * cam->height floats, 0 = invalid),
+ * host memory for sgm_emap_integrate and device memory for the _device variant.
+ * *newly_freed receives the number of voxels this frame appended to the changelog. */
+int sgm_emap_integrate(sgm_ctx* ctx, sgm_emap* emap, const sgm_camera* cam,
+                       const sgm_pose* pose, const float* depth, int32_t stride,
+                       uint64_t* newly_freed);
+int sgm_emap_integrate_device(sgm_ctx* ctx, sgm_emap* emap, const sgm_camera* cam,
+                              const sgm_pose* pose, const float* d_depth, int32_t stride,
+                              uint64_t* newly_freed);
+/* take_changelog (explorer.cpp:112-116): copies min(size, capacity) ids to out, sets *n to
+ * the size and clears the changelog. capacity < size -> SGM_ERR_INVALID, nothing cleared. */
+int sgm_emap_take_changelog(sgm_ctx* ctx, sgm_emap* emap, int32_t* out, uint64_t capacity,
+                            uint64_t* n);
+/* reseed_changelog_with_free (explorer.cpp:118-122). */
+int sgm_emap_reseed_changelog_with_free(sgm_ctx* ctx, sgm_emap* emap);
+/* seed_free_region / seed_occupied_region (explorer.cpp:124-132). */
+int sgm_emap_seed_region(sgm_ctx* ctx, sgm_emap* emap, const sgm_aabb* box, int occupied);
+/* grid() (explorer.hpp:42): copies voxel_count bytes of state to host `out`. */
+int sgm_emap_grid(sgm_ctx* ctx, const sgm_emap* emap, uint8_t* out, uint64_t capacity);
+/* sample_candidates (explorer.cpp:157-184): consumes the changelog and writes one
+ * (position, direction) per free, freshly logged lattice point x fibonacci direction, in
+ * the reference's order. heights: n_heights values; v1 > 0 lattice spacing; v2 >= 1
+ * directions (max elevation 45 deg). capacity too small -> SGM_ERR_INVALID with *n_out =
+ * the count needed and the changelog left untouched. */
+int sgm_sample_candidates(sgm_ctx* ctx, sgm_emap* emap, double v1, int32_t v2,
+                          const double* heights, int32_t n_heights, sgm_candidate* out,
+                          uint64_t capacity, uint64_t* n_out);
+/* fibonacci_directions (explorer.cpp:142-155), host fp64: count x 3 doubles. */
+void sgm_fibonacci_directions(int32_t count, double max_elevation_deg, double* out3);
+
 #ifdef __cplusplus
 }
 #endif

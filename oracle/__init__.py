@@ -83,6 +83,12 @@ class orc_stats(C.Structure):
                 ("exact_tests", C.c_uint64), ("contributors", C.c_uint64)]
 
 
+class orc_emap(C.Structure):
+    _fields_ = [("origin", C.c_double * 3), ("voxel", C.c_double), ("dims", C.c_int32 * 3),
+                ("nvox", C.c_uint64), ("grid", C.POINTER(C.c_uint8)), ("log", C.POINTER(C.c_int32)),
+                ("log_n", C.c_uint64), ("free_count", C.c_uint64), ("occupied_count", C.c_uint64)]
+
+
 PROJ_DTYPE = np.dtype([("mx", "<f8"), ("my", "<f8"), ("rad_px", "<f8"), ("z", "<f8"),
                        ("alpha", "<f8"), ("index", "<u4"), ("pad", "<u4")])
 
@@ -168,6 +174,27 @@ class Oracle:
         L.orc_fisher_gain.argtypes = [C.POINTER(orc_map), C.POINTER(orc_camera), C.c_uint64,
                                       C.POINTER(orc_pose), C.POINTER(orc_options), _pd,
                                       C.c_double, _pd]
+        L.orc_emap_init.restype = C.c_int
+        L.orc_emap_init.argtypes = [C.POINTER(orc_emap), _pd, _pd, C.c_double]
+        L.orc_emap_free.argtypes = [C.POINTER(orc_emap)]
+        L.orc_emap_integrate.restype = C.c_uint64
+        L.orc_emap_integrate.argtypes = [C.POINTER(orc_emap), C.POINTER(orc_camera),
+                                         C.POINTER(orc_pose), _pf, C.c_int]
+        L.orc_emap_seed.argtypes = [C.POINTER(orc_emap), _pd, _pd, C.c_int]
+        L.orc_emap_reseed.argtypes = [C.POINTER(orc_emap)]
+        L.orc_fibonacci_directions.argtypes = [C.c_int, C.c_double, _pd]
+        L.orc_sample_candidates.restype = C.c_uint64
+        L.orc_sample_candidates.argtypes = [C.POINTER(orc_emap), C.c_double, C.c_int, _pd, C.c_int,
+                                            _pd, C.c_uint64]
+
+    def emap(self, bmin, bmax, voxel) -> "OracleEmap":
+        return OracleEmap(self, bmin, bmax, voxel)
+
+    def fibonacci_directions(self, count, max_elev=45.0) -> np.ndarray:
+        out = np.zeros((max(count, 0), 3))
+        if count > 0:
+            self.lib.orc_fibonacci_directions(count, max_elev, _dp(out))
+        return out
 
     def fisher_accumulate(self, m, cam, poses, opt=None) -> np.ndarray:
         """Fisher diagonal summed over `poses`: (N, 8) = (mu xyz, log_r, logit, rgb)."""
@@ -280,6 +307,127 @@ class Oracle:
         return np.array(out.R[:]).reshape(3, 3), np.array(out.t[:])
 
 
+def _v3(v):
+    return np.ascontiguousarray(np.asarray(v, dtype=np.float64).reshape(3))
+
+
+def _depth(depth):
+    return np.ascontiguousarray(depth, dtype=np.float32).reshape(-1)
+
+
+class OracleEmap:
+    """ExplorationMap restated in C (orc_emap_*). Same interface as RefEmap."""
+
+    def __init__(self, orc, bmin, bmax, voxel):
+        self.o = orc
+        self.e = orc_emap()
+        if orc.lib.orc_emap_init(C.byref(self.e), _dp(_v3(bmin)), _dp(_v3(bmax)), float(voxel)):
+            raise ValueError("emap: voxel size must be > 0")
+
+    def __del__(self):
+        if getattr(self, "e", None) is not None:
+            self.o.lib.orc_emap_free(C.byref(self.e))
+
+    def integrate(self, cam, pose, depth, stride=2) -> int:
+        c, p, d = _cam(cam), _pose(pose), _depth(depth)
+        return int(self.o.lib.orc_emap_integrate(C.byref(self.e), C.byref(c), C.byref(p),
+                                                   d.ctypes.data_as(_pf), int(stride)))
+
+    def grid(self) -> np.ndarray:
+        return np.ctypeslib.as_array(self.e.grid, shape=(self.e.nvox,)).copy()
+
+    def info(self) -> dict:
+        return {"free": int(self.e.free_count), "occupied": int(self.e.occupied_count),
+                "changelog": int(self.e.log_n), "dims": tuple(self.e.dims),
+                "origin": tuple(self.e.origin), "voxels": int(self.e.nvox)}
+
+    def take_changelog(self) -> np.ndarray:
+        n = int(self.e.log_n)
+        out = (np.ctypeslib.as_array(self.e.log, shape=(n,)).copy() if n
+               else np.zeros(0, np.int32))
+        self.e.log_n = 0
+        return out
+
+    def reseed(self) -> None:
+        self.o.lib.orc_emap_reseed(C.byref(self.e))
+
+    def seed(self, bmin, bmax, occupied=False) -> None:
+        self.o.lib.orc_emap_seed(C.byref(self.e), _dp(_v3(bmin)), _dp(_v3(bmax)), int(occupied))
+
+    def sample_candidates(self, v1, v2, heights):
+        h = np.ascontiguousarray(heights, dtype=np.float64)
+        e2 = orc_emap.from_buffer_copy(self.e)  # count first, without consuming
+        n = int(self.o.lib.orc_sample_candidates(C.byref(e2), float(v1), int(v2), _dp(h), len(h),
+                                                  None, 0))
+        out = np.zeros((max(n, 1), 6))
+        self.o.lib.orc_sample_candidates(C.byref(self.e), float(v1), int(v2), _dp(h), len(h),
+                                         _dp(out), n)
+        return out[:n, :3].copy(), out[:n, 3:].copy()
+
+
+class RefEmap:
+    """The reference's own ExplorationMap (explorer.cpp:11-184) via ref_emap_*."""
+
+    def __init__(self, ref, bmin, bmax, voxel):
+        self.r = ref
+        self.voxel = float(voxel)
+        self.h = ref.lib.ref_emap_create(_dp(_v3(bmin)), _dp(_v3(bmax)), float(voxel))
+        if not self.h:
+            raise ValueError("emap: voxel size must be > 0")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.r.lib.ref_emap_destroy(self.h)
+            self.h = None
+
+    def integrate(self, cam, pose, depth, stride=2) -> int:
+        wh, intr = RefLib._cam(cam)
+        R, t = RefLib._pose(pose)
+        d = _depth(depth)
+        return int(self.r.lib.ref_emap_integrate(self.h, wh.ctypes.data_as(_pi32), _dp(intr),
+                                                 _dp(R), _dp(t), d.ctypes.data_as(_pf),
+                                                 int(stride)))
+
+    def info(self) -> dict:
+        info = np.zeros(4, np.uint64)
+        dims = np.zeros(3, np.int32)
+        origin = np.zeros(3)
+        self.r.lib.ref_emap_info(self.h, info.ctypes.data_as(_pu64), dims.ctypes.data_as(_pi32),
+                                 _dp(origin))
+        return {"free": int(info[0]), "occupied": int(info[1]), "changelog": int(info[2]),
+                "dims": tuple(int(v) for v in dims), "origin": tuple(float(v) for v in origin),
+                "voxels": int(info[3])}
+
+    def grid(self) -> np.ndarray:
+        out = np.zeros(self.info()["voxels"], np.uint8)
+        self.r.lib.ref_emap_grid(self.h, out.ctypes.data_as(C.POINTER(C.c_uint8)))
+        return out
+
+    def take_changelog(self) -> np.ndarray:
+        out = np.zeros(max(self.info()["changelog"], 1), np.int32)
+        n = int(self.r.lib.ref_emap_take_changelog(self.h, out.ctypes.data_as(_pi32)))
+        return out[:n].copy()
+
+    def reseed(self) -> None:
+        self.r.lib.ref_emap_reseed(self.h)
+
+    def seed(self, bmin, bmax, occupied=False) -> None:
+        self.r.lib.ref_emap_seed(self.h, _dp(_v3(bmin)), _dp(_v3(bmax)), int(occupied))
+
+    def sample_candidates(self, v1, v2, heights):
+        h = np.ascontiguousarray(heights, dtype=np.float64)
+        # upper bound: every lattice point free and fresh
+        info = self.info()
+        nx = int(info["dims"][0] * self.voxel / v1) + 2
+        nz = int(info["dims"][2] * self.voxel / v1) + 2
+        cap = max(1, len(h) * nx * nz * int(v2))
+        out = np.zeros((cap, 6))
+        n = int(self.r.lib.ref_sample_candidates(self.h, float(v1), int(v2), _dp(h), len(h),
+                                                 _dp(out), cap))
+        assert n <= cap
+        return out[:n, :3].copy(), out[:n, 3:].copy()
+
+
 class RefLib:
     """The reference's own code (oracle/_ref/libsgm_ref.so)."""
 
@@ -309,10 +457,51 @@ class RefLib:
         L.ref_random_splat_map.argtypes = [C.c_uint64, _pi32, _pd, _pd, _pd, _pd, _pd, _pd, _pd,
                                            _pd, _pu16, _pd, _pi32]
         L.ref_camera_from_fov.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, _pd]
+        L.ref_emap_create.restype = C.c_void_p
+        L.ref_emap_create.argtypes = [_pd, _pd, C.c_double]
+        L.ref_emap_destroy.argtypes = [C.c_void_p]
+        L.ref_emap_info.argtypes = [C.c_void_p, _pu64, _pi32, _pd]
+        L.ref_emap_integrate.restype = C.c_uint64
+        L.ref_emap_integrate.argtypes = [C.c_void_p, _pi32, _pd, _pd, _pd, _pf, C.c_int]
+        L.ref_emap_grid.argtypes = [C.c_void_p, C.POINTER(C.c_uint8)]
+        L.ref_emap_take_changelog.restype = C.c_uint64
+        L.ref_emap_take_changelog.argtypes = [C.c_void_p, _pi32]
+        L.ref_emap_reseed.argtypes = [C.c_void_p]
+        L.ref_emap_seed.argtypes = [C.c_void_p, _pd, _pd, C.c_int]
+        L.ref_sample_candidates.restype = C.c_uint64
+        L.ref_sample_candidates.argtypes = [C.c_void_p, C.c_double, C.c_int, _pd, C.c_int, _pd,
+                                            C.c_uint64]
+        L.ref_fibonacci_directions.argtypes = [C.c_int, C.c_double, _pd]
+        L.ref_raycast_depth.restype = C.c_int
+        L.ref_raycast_depth.argtypes = [_pd, _pd, C.c_int, _pd, C.c_int, _pd, _pi32, _pd, _pd,
+                                        _pd, _pf]
         L.ref_backward.restype = C.c_int
         L.ref_backward.argtypes = [C.c_void_p, _pi32, _pd, _pd, _pd, _pd, C.c_int, _pf, _pf, _pf,
                                    _pd, C.c_int, C.c_int, _pd, _pd, _pd, _pd, _pd, _pd,
                                    C.c_char_p, C.c_int]
+
+    def emap(self, bmin, bmax, voxel) -> RefEmap:
+        return RefEmap(self, bmin, bmax, voxel)
+
+    def fibonacci_directions(self, count, max_elev=45.0) -> np.ndarray:
+        out = np.zeros((max(count, 0), 3))
+        if count > 0:
+            self.lib.ref_fibonacci_directions(count, max_elev, _dp(out))
+        return out
+
+    def raycast_depth(self, bmin, bmax, cam, pose, boxes=(), spheres=()) -> np.ndarray:
+        """Depth plane of raycast_frame (scene_sim.hpp:31) for a room with boxes / spheres."""
+        b = np.ascontiguousarray(np.asarray(boxes, dtype=np.float64).reshape(-1, 6))
+        sp = np.ascontiguousarray(np.asarray(spheres, dtype=np.float64).reshape(-1, 4))
+        wh, intr = self._cam(cam)
+        R, t = self._pose(pose)
+        out = np.zeros(cam.width * cam.height, np.float32)
+        rc = self.lib.ref_raycast_depth(_dp(_v3(bmin)), _dp(_v3(bmax)), len(b), _dp(b), len(sp),
+                                        _dp(sp), wh.ctypes.data_as(_pi32), _dp(intr), _dp(R),
+                                        _dp(t), out.ctypes.data_as(_pf))
+        if rc:
+            raise ValueError("raycast_depth: invalid scene")
+        return out
 
     def backward(self, m, cam, frame, weights, include_mapping=True, include_semantic=True,
                  opt=None):

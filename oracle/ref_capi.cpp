@@ -322,3 +322,127 @@ int ref_backward(void* m, const int32_t wh[2], const double intr[4], const doubl
 }
 
 }  // extern "C"
+
+// ---- ExplorationMap + candidate sampling (proj/src/explorer.cpp:11-184) and the
+// reference simulator's depth raycast (proj/src/scene_sim.cpp) for test frames ----
+#include "splatmap/scene.hpp"
+#include "splatmap/scene_sim.hpp"
+
+extern "C" {
+
+void* ref_emap_create(const double bmin[3], const double bmax[3], double voxel) {
+    try {
+        Aabb b;
+        b.min = Vec3(bmin[0], bmin[1], bmin[2]);
+        b.max = Vec3(bmax[0], bmax[1], bmax[2]);
+        return new ExplorationMap(b, voxel);
+    } catch (...) {
+        return nullptr;
+    }
+}
+
+void ref_emap_destroy(void* h) { delete static_cast<ExplorationMap*>(h); }
+
+// info = {free_count, occupied_count, changelog_size, voxel_count}; dims[3]; origin[3]
+void ref_emap_info(void* h, uint64_t info[4], int32_t dims[3], double origin[3]) {
+    auto* e = static_cast<ExplorationMap*>(h);
+    info[0] = e->free_count();
+    info[1] = e->occupied_count();
+    info[2] = e->changelog_size();
+    info[3] = e->voxel_count();
+    for (int a = 0; a < 3; ++a) {
+        dims[a] = e->dims()[a];
+        origin[a] = e->origin()[a];
+    }
+}
+
+uint64_t ref_emap_integrate(void* h, const int32_t wh[2], const double intr[4], const double R[9],
+                            const double t[3], const float* depth, int stride) {
+    Frame f;
+    f.width = wh[0];
+    f.height = wh[1];
+    f.pose = make_pose(R, t);
+    f.depth.assign(depth, depth + static_cast<size_t>(wh[0]) * wh[1]);
+    return static_cast<ExplorationMap*>(h)->integrate_frame(f, make_cam(wh, intr), stride);
+}
+
+void ref_emap_grid(void* h, uint8_t* out) {
+    auto g = static_cast<ExplorationMap*>(h)->grid();
+    for (size_t i = 0; i < g.size(); ++i) out[i] = static_cast<uint8_t>(g[i]);
+}
+
+uint64_t ref_emap_take_changelog(void* h, int32_t* out) {
+    std::vector<int> log = static_cast<ExplorationMap*>(h)->take_changelog();
+    std::memcpy(out, log.data(), log.size() * 4);
+    return log.size();
+}
+
+void ref_emap_reseed(void* h) { static_cast<ExplorationMap*>(h)->reseed_changelog_with_free(); }
+
+void ref_emap_seed(void* h, const double bmin[3], const double bmax[3], int occupied) {
+    Aabb b;
+    b.min = Vec3(bmin[0], bmin[1], bmin[2]);
+    b.max = Vec3(bmax[0], bmax[1], bmax[2]);
+    auto* e = static_cast<ExplorationMap*>(h);
+    if (occupied) e->seed_occupied_region(b);
+    else e->seed_free_region(b);
+}
+
+// sample_candidates: out6 = {position, direction} per candidate (capacity entries).
+uint64_t ref_sample_candidates(void* h, double v1, int v2, const double* heights, int nh,
+                               double* out6, uint64_t capacity) {
+    SamplingSchedule s;
+    s.v1 = v1;
+    s.v2 = v2;
+    s.heights.assign(heights, heights + nh);
+    auto c = sample_candidates(*static_cast<ExplorationMap*>(h), s);
+    for (size_t i = 0; i < c.size() && i < capacity; ++i)
+        for (int a = 0; a < 3; ++a) {
+            out6[6 * i + a] = c[i].position[a];
+            out6[6 * i + 3 + a] = c[i].direction[a];
+        }
+    return c.size();
+}
+
+void ref_fibonacci_directions(int count, double max_elev, double* out3) {
+    auto d = fibonacci_directions(count, max_elev);
+    for (size_t i = 0; i < d.size(); ++i)
+        for (int a = 0; a < 3; ++a) out3[3 * i + a] = d[i][a];
+}
+
+// raycast_frame depth of a room (bounds) with axis-aligned boxes (min, max) and spheres
+// (centre, radius): the reference simulator's own depth (scene_sim.hpp:31).
+int ref_raycast_depth(const double bmin[3], const double bmax[3], int n_boxes, const double* boxes6,
+                      int n_spheres, const double* spheres4, const int32_t wh[2],
+                      const double intr[4], const double R[9], const double t[3], float* depth) {
+    try {
+        SceneSpec s;
+        s.bounds.min = Vec3(bmin[0], bmin[1], bmin[2]);
+        s.bounds.max = Vec3(bmax[0], bmax[1], bmax[2]);
+        s.num_classes = 6;
+        for (int i = 0; i < n_boxes; ++i) {
+            ScenePrimitive p;
+            p.kind = ScenePrimitive::Kind::Box;
+            p.box_min = Vec3(boxes6[6 * i], boxes6[6 * i + 1], boxes6[6 * i + 2]);
+            p.box_max = Vec3(boxes6[6 * i + 3], boxes6[6 * i + 4], boxes6[6 * i + 5]);
+            p.class_id = 3;
+            s.primitives.push_back(p);
+        }
+        for (int i = 0; i < n_spheres; ++i) {
+            ScenePrimitive p;
+            p.kind = ScenePrimitive::Kind::Sphere;
+            p.center = Vec3(spheres4[4 * i], spheres4[4 * i + 1], spheres4[4 * i + 2]);
+            p.radius = spheres4[4 * i + 3];
+            p.class_id = 4;
+            s.primitives.push_back(p);
+        }
+        s.validate();
+        Frame f = raycast_frame(s, make_cam(wh, intr), make_pose(R, t));
+        std::memcpy(depth, f.depth.data(), f.depth.size() * 4);
+        return 0;
+    } catch (...) {
+        return 1;
+    }
+}
+
+}  // extern "C"

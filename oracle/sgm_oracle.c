@@ -656,3 +656,193 @@ int orc_fisher_gain(const orc_map* map, const orc_camera* cam, uint64_t n_views,
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------ ExplorationMap */
+
+enum { ORC_UNKNOWN = 0, ORC_FREE = 1, ORC_OCCUPIED = 2 };
+#define ORC_PI 3.14159265358979323846 /* glibc M_PI */
+
+int orc_emap_init(orc_emap* e, const double bmin[3], const double bmax[3], double voxel) {
+    memset(e, 0, sizeof(*e));
+    if (voxel <= 0) return -1; /* explorer.cpp:13 */
+    e->voxel = voxel;
+    e->nvox = 1;
+    for (int a = 0; a < 3; ++a) {
+        e->origin[a] = bmin[a];
+        int d = to_int_x86(ceil((bmax[a] - bmin[a]) / voxel)); /* :14-17 */
+        e->dims[a] = d < 1 ? 1 : d;                             /* :18 cwiseMax */
+        e->nvox *= (uint64_t)e->dims[a];
+    }
+    e->grid = (uint8_t*)calloc(e->nvox, 1);
+    e->log = (int32_t*)malloc(e->nvox * sizeof(int32_t));
+    if (!e->grid || !e->log) {
+        orc_emap_free(e);
+        return -1;
+    }
+    return 0;
+}
+
+void orc_emap_free(orc_emap* e) {
+    free(e->grid);
+    free(e->log);
+    e->grid = NULL;
+    e->log = NULL;
+}
+
+static int emap_in_grid(const orc_emap* e, int ix, int iy, int iz) { /* explorer.hpp:28-30 */
+    return ix >= 0 && iy >= 0 && iz >= 0 && ix < e->dims[0] && iy < e->dims[1] && iz < e->dims[2];
+}
+
+static int emap_linear(const orc_emap* e, int ix, int iy, int iz) { /* explorer.hpp:25-27 */
+    return (iz * e->dims[1] + iy) * e->dims[0] + ix;
+}
+
+static int emap_voxel_at(const orc_emap* e, const double p[3]) { /* explorer.cpp:22-29 */
+    int ix = to_int_x86(floor((p[0] - e->origin[0]) / e->voxel));
+    int iy = to_int_x86(floor((p[1] - e->origin[1]) / e->voxel));
+    int iz = to_int_x86(floor((p[2] - e->origin[2]) / e->voxel));
+    if (!emap_in_grid(e, ix, iy, iz)) return -1;
+    return emap_linear(e, ix, iy, iz);
+}
+
+static void emap_mark_free(orc_emap* e, int id) { /* explorer.cpp:38-43 */
+    if (e->grid[id] != ORC_UNKNOWN) return;
+    e->grid[id] = ORC_FREE;
+    ++e->free_count;
+    e->log[e->log_n++] = id;
+}
+
+static void emap_mark_occupied(orc_emap* e, int id) { /* explorer.cpp:45-51 */
+    if (e->grid[id] == ORC_OCCUPIED) return;
+    if (e->grid[id] == ORC_FREE) --e->free_count;
+    e->grid[id] = ORC_OCCUPIED;
+    ++e->occupied_count;
+}
+
+uint64_t orc_emap_integrate(orc_emap* e, const orc_camera* cam, const orc_pose* pose,
+                            const float* depth, int stride) {
+    const uint64_t before = e->log_n;
+    for (int y = 0; y < cam->height; y += stride) {
+        for (int x = 0; x < cam->width; x += stride) {
+            float d = depth[(size_t)y * cam->width + x];
+            if (d <= 0) continue; /* :58 */
+            const double dd = (double)d;
+            /* end = R * (pixel_ray(x, y) * d) + t   camera.hpp:45-47, geometry.hpp:22 */
+            const double c[3] = {(x + 0.5 - cam->cx) / cam->fx * dd, (y + 0.5 - cam->cy) / cam->fy * dd,
+                                 1.0 * dd};
+            double start[3], end[3], dir[3];
+            int idx[3], step[3];
+            double t_max[3], t_delta[3];
+            for (int i = 0; i < 3; ++i) {
+                start[i] = pose->t[i];
+                end[i] = (pose->R[3 * i] * c[0] + (pose->R[3 * i + 1] * c[1] + pose->R[3 * i + 2] * c[2])) +
+                         pose->t[i];
+            }
+            for (int a = 0; a < 3; ++a) idx[a] = to_int_x86(floor((start[a] - e->origin[a]) / e->voxel));
+            for (int a = 0; a < 3; ++a) dir[a] = end[a] - start[a];
+            const double len = sqrt(dir[0] * dir[0] + (dir[1] * dir[1] + dir[2] * dir[2]));
+            if (len < 1e-12) continue; /* :68 */
+            for (int a = 0; a < 3; ++a) dir[a] = dir[a] / len;
+            const double q[3] = {end[0] - dir[0] * 1e-6, end[1] - dir[1] * 1e-6, end[2] - dir[2] * 1e-6};
+            const int hit = emap_voxel_at(e, q); /* :72 */
+            for (int a = 0; a < 3; ++a) { /* :77-89 */
+                if (fabs(dir[a]) < 1e-12) {
+                    step[a] = 0;
+                    t_max[a] = 1e300;
+                    t_delta[a] = 1e300;
+                } else {
+                    step[a] = dir[a] > 0 ? 1 : -1;
+                    double boundary = e->origin[a] + (idx[a] + (dir[a] > 0 ? 1.0 : 0.0)) * e->voxel;
+                    t_max[a] = (boundary - start[a]) / dir[a];
+                    t_delta[a] = e->voxel / fabs(dir[a]);
+                }
+            }
+            double t = 0.0;
+            int guard = e->dims[0] + e->dims[1] + e->dims[2] + 4;
+            while (guard-- > 0 && t <= len) { /* :93-104 */
+                if (!emap_in_grid(e, idx[0], idx[1], idx[2])) break;
+                int id = emap_linear(e, idx[0], idx[1], idx[2]);
+                if (id == hit) break;
+                emap_mark_free(e, id);
+                int axis = 0;
+                if (t_max[1] < t_max[axis]) axis = 1;
+                if (t_max[2] < t_max[axis]) axis = 2;
+                t = t_max[axis];
+                t_max[axis] += t_delta[axis];
+                idx[axis] += step[axis];
+            }
+            if (hit >= 0) emap_mark_occupied(e, hit); /* :105 */
+        }
+    }
+    return e->log_n - before;
+}
+
+void orc_emap_seed(orc_emap* e, const double bmin[3], const double bmax[3], int occupied) {
+    for (uint64_t i = 0; i < e->nvox; ++i) { /* explorer.cpp:124-132 */
+        const int id = (int)i;
+        const int ix = id % e->dims[0], iy = (id / e->dims[0]) % e->dims[1],
+                  iz = id / (e->dims[0] * e->dims[1]); /* voxel_center, :31-36 */
+        const double p[3] = {e->origin[0] + e->voxel * (ix + 0.5), e->origin[1] + e->voxel * (iy + 0.5),
+                             e->origin[2] + e->voxel * (iz + 0.5)};
+        int in = 1;
+        for (int a = 0; a < 3; ++a) in = in && p[a] >= bmin[a] && p[a] <= bmax[a];
+        if (!in) continue;
+        if (occupied) emap_mark_occupied(e, id);
+        else emap_mark_free(e, id);
+    }
+}
+
+void orc_emap_reseed(orc_emap* e) { /* explorer.cpp:118-122 */
+    e->log_n = 0;
+    for (uint64_t i = 0; i < e->nvox; ++i)
+        if (e->grid[i] == ORC_FREE) e->log[e->log_n++] = (int32_t)i;
+}
+
+void orc_fibonacci_directions(int count, double max_elev_deg, double* out3) {
+    const double golden_angle = ORC_PI * (3.0 - sqrt(5.0));
+    const double s_max = sin(max_elev_deg * ORC_PI / 180.0); /* deg_to_rad, geometry.hpp:86 */
+    for (int j = 0; j < count; ++j) {
+        double s = count == 1 ? 0.0 : s_max * (1.0 - (2.0 * j + 1.0) / count);
+        double r = sqrt(fmax(0.0, 1.0 - s * s));
+        double az = golden_angle * j;
+        out3[3 * j + 0] = r * cos(az);
+        out3[3 * j + 1] = s;
+        out3[3 * j + 2] = r * sin(az);
+    }
+}
+
+uint64_t orc_sample_candidates(orc_emap* e, double v1, int v2, const double* heights, int nh,
+                               double* out6, uint64_t capacity) {
+    const uint64_t n_fresh = e->log_n; /* take_changelog (:159) */
+    e->log_n = 0;
+    if (n_fresh == 0) return 0;
+    uint8_t* fresh = (uint8_t*)calloc(e->nvox, 1);
+    double* dirs = (double*)malloc(sizeof(double) * 3 * (size_t)(v2 > 0 ? v2 : 1));
+    if (!fresh || !dirs) {
+        free(fresh);
+        free(dirs);
+        return 0;
+    }
+    for (uint64_t i = 0; i < n_fresh; ++i) fresh[e->log[i]] = 1;
+    orc_fibonacci_directions(v2, 45.0, dirs);
+    double top[3];
+    for (int a = 0; a < 3; ++a) top[a] = e->origin[a] + (double)e->dims[a] * e->voxel;
+    uint64_t n = 0;
+    for (int hi = 0; hi < nh; ++hi)
+        for (double x = e->origin[0]; x <= top[0] + 1e-9; x += v1)
+            for (double z = e->origin[2]; z <= top[2] + 1e-9; z += v1) {
+                const double p[3] = {x, heights[hi], z};
+                int id = emap_voxel_at(e, p);
+                if (id < 0 || e->grid[id] != ORC_FREE || !fresh[id]) continue;
+                for (int d = 0; d < v2; ++d, ++n) {
+                    if (n >= capacity) continue;
+                    for (int a = 0; a < 3; ++a) {
+                        out6[6 * n + a] = p[a];
+                        out6[6 * n + 3 + a] = dirs[3 * d + a];
+                    }
+                }
+            }
+    free(fresh);
+    free(dirs);
+    return n;
+}

@@ -112,6 +112,34 @@ int orc_fisher_gain(const orc_map* map, const orc_camera* cam, uint64_t n_views,
                     double lambda, double* gain);
 
 /* CandidatePose::camera_pose() = look_at(p, p + d), explorer.hpp:105 + geometry.hpp:44-56. */
+/* ExplorationMap, proj/include/splatmap/explorer.hpp:11-83 (grid states 0/1/2, changelog). */
+typedef struct {
+    double origin[3];
+    double voxel;
+    int32_t dims[3];
+    uint64_t nvox;
+    uint8_t* grid;
+    int32_t* log;
+    uint64_t log_n, free_count, occupied_count;
+} orc_emap;
+
+/* ExplorationMap ctor (explorer.cpp:11-20); returns 0, or -1 for voxel <= 0 / no memory. */
+int orc_emap_init(orc_emap* e, const double bmin[3], const double bmax[3], double voxel);
+void orc_emap_free(orc_emap* e);
+/* integrate_frame (explorer.cpp:53-110), sequential; returns the newly logged count. */
+uint64_t orc_emap_integrate(orc_emap* e, const orc_camera* cam, const orc_pose* pose,
+                            const float* depth, int stride);
+/* seed_free_region / seed_occupied_region (explorer.cpp:124-132). */
+void orc_emap_seed(orc_emap* e, const double bmin[3], const double bmax[3], int occupied);
+/* reseed_changelog_with_free (explorer.cpp:118-122). */
+void orc_emap_reseed(orc_emap* e);
+/* fibonacci_directions (explorer.cpp:142-155). */
+void orc_fibonacci_directions(int count, double max_elev_deg, double* out3);
+/* sample_candidates (explorer.cpp:157-184): consumes the changelog; writes up to capacity
+ * (position, direction) 6-tuples and returns the total count. */
+uint64_t orc_sample_candidates(orc_emap* e, double v1, int v2, const double* heights, int nh,
+                               double* out6, uint64_t capacity);
+
 void orc_candidate_pose(const double pos[3], const double dir[3], orc_pose* out);
 void orc_look_at(const double pos[3], const double target[3], orc_pose* out);
 

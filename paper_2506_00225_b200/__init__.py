@@ -38,3 +38,11 @@ from .splatmap import (  # noqa: F401
     score_poses_fisher,
     sigmoid,
 )
+from .explore import (  # noqa: F401,E402
+    Aabb,
+    ExplorationMap,
+    SamplingSchedule,
+    VoxelState,
+    fibonacci_directions,
+    sample_candidates,
+)

@@ -55,6 +55,10 @@ class sgm_candidate(C.Structure):
     _fields_ = [("position", C.c_double * 3), ("direction", C.c_double * 3)]
 
 
+class sgm_aabb(C.Structure):
+    _fields_ = [("min", C.c_double * 3), ("max", C.c_double * 3)]
+
+
 class sgm_stats(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("views", C.c_uint64),
                 ("visible", C.c_uint64), ("pairs", C.c_uint64),
@@ -70,7 +74,24 @@ _pu64 = C.POINTER(C.c_uint64)
 _pf = C.POINTER(C.c_float)
 
 # Every symbol include/sgm.h declares, with its ctypes signature.
+_pi32 = C.POINTER(C.c_int32)
+_pu8 = C.POINTER(C.c_uint8)
+
 SIGNATURES = {
+    "sgm_emap_create": (C.c_int, [_vp, C.POINTER(sgm_aabb), C.c_double, C.POINTER(_vp)]),
+    "sgm_emap_destroy": (None, [_vp, _vp]),
+    "sgm_emap_info": (C.c_int, [_vp, _vp, _pd, _pd, _pi32, _pu64, _pu64, _pu64]),
+    "sgm_emap_integrate": (C.c_int, [_vp, _vp, C.POINTER(sgm_camera), C.POINTER(sgm_pose), _pf,
+                                     C.c_int32, _pu64]),
+    "sgm_emap_integrate_device": (C.c_int, [_vp, _vp, C.POINTER(sgm_camera),
+                                            C.POINTER(sgm_pose), _vp, C.c_int32, _pu64]),
+    "sgm_emap_take_changelog": (C.c_int, [_vp, _vp, _pi32, C.c_uint64, _pu64]),
+    "sgm_emap_reseed_changelog_with_free": (C.c_int, [_vp, _vp]),
+    "sgm_emap_seed_region": (C.c_int, [_vp, _vp, C.POINTER(sgm_aabb), C.c_int]),
+    "sgm_emap_grid": (C.c_int, [_vp, _vp, _pu8, C.c_uint64]),
+    "sgm_sample_candidates": (C.c_int, [_vp, _vp, C.c_double, C.c_int32, _pd, C.c_int32,
+                                        C.POINTER(sgm_candidate), C.c_uint64, _pu64]),
+    "sgm_fibonacci_directions": (None, [C.c_int32, C.c_double, _pd]),
     "sgm_abi_version": (C.c_int, []),
     "sgm_ctx_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
     "sgm_ctx_destroy": (None, [_vp]),

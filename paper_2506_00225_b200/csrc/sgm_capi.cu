@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <new>
 #include <string>
 #include <thread>
@@ -583,6 +584,67 @@ void do_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const
         run_views(ctx, map, cam, o, 1, &p, Mode::Render, rt, nullptr, nullptr);
     }
     if (n_proj) *n_proj = ctx->last_V;
+}
+
+}  // namespace
+
+struct sgm_emap {
+    EmapParams p{};
+    DevBuf grid, first_free, first_hit, log, keys, keys_alt, ids, ids_alt, fresh, counters, depth,
+        lattice, ok, sort_tmp;
+    HostBuf h_counters;
+    uint64_t log_n = 0, free_count = 0, occupied_count = 0;
+};
+
+namespace {
+
+// Sorts the n emitted (key, id) pairs by key and appends the ids to the changelog.
+void emap_append_sorted(sgm_ctx* ctx, sgm_emap* em, uint64_t n) {
+    if (n == 0) return;
+    cudaStream_t s = ctx->stream;
+    cub::DoubleBuffer<unsigned long long> dk(em->keys.as<unsigned long long>(),
+                                             em->keys_alt.as<unsigned long long>());
+    cub::DoubleBuffer<int32_t> dv(em->ids.as<int32_t>(), em->ids_alt.as<int32_t>());
+    size_t tmp = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, static_cast<int>(n), 0, 64, s));
+    CK(em->sort_tmp.reserve(tmp));
+    CK(cub::DeviceRadixSort::SortPairs(em->sort_tmp.p, tmp, dk, dv, static_cast<int>(n), 0, 64, s));
+    ctx->stats.kernel_launches += 1;
+    CK(cudaMemcpyAsync(em->log.as<int32_t>() + em->log_n, dv.Current(), 4 * n,
+                       cudaMemcpyDeviceToDevice, s));
+    em->log_n += n;
+}
+
+// Pass 2 + counts + changelog append; returns the number of newly logged voxels.
+uint64_t emap_resolve(sgm_ctx* ctx, sgm_emap* em) {
+    cudaStream_t s = ctx->stream;
+    auto* cnt = em->counters.as<unsigned long long>();
+    CK(cudaMemsetAsync(cnt, 0, 3 * sizeof(unsigned long long), s));
+    launch_emap_resolve(em->p, em->grid.as<uint8_t>(), em->first_free.as<unsigned long long>(),
+                        em->first_hit.as<uint32_t>(), em->keys.as<unsigned long long>(),
+                        em->ids.as<int32_t>(), cnt, s);
+    ctx->stats.kernel_launches += 1;
+    auto* h = em->h_counters.as<unsigned long long>();
+    CK(cudaMemcpyAsync(h, cnt, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    em->free_count = h[1];
+    em->occupied_count = h[2];
+    const uint64_t n = h[0];
+    emap_append_sorted(ctx, em, n);
+    CK(cudaStreamSynchronize(s));
+    return n;
+}
+
+uint64_t emap_integrate(sgm_ctx* ctx, sgm_emap* em, const CamParams& cam, const sgm_pose& pose,
+                        const float* d_depth, int stride) {
+    WorldPose P;
+    for (int i = 0; i < 9; ++i) P.R[i] = pose.R[i];
+    for (int i = 0; i < 3; ++i) P.t[i] = pose.t[i];
+    launch_emap_rays(em->p, cam, P, d_depth, stride, em->grid.as<uint8_t>(),
+                     em->first_free.as<unsigned long long>(), em->first_hit.as<uint32_t>(),
+                     ctx->stream);
+    ctx->stats.kernel_launches += 1;
+    return emap_resolve(ctx, em);
 }
 
 }  // namespace
@@ -1169,6 +1231,218 @@ int sgm_score_candidates(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam
     std::vector<sgm_pose> poses(n);
     for (uint64_t i = 0; i < n; ++i) sgm_candidate_pose(cands[i].position, cands[i].direction, &poses[i]);
     return sgm_score_views(ctx, map, cam, n, poses.data(), opt, n_missing, entropy_sum);
+}
+
+
+// ---------------------------------------------------------------- exploration map (f1)
+
+int sgm_emap_create(sgm_ctx* ctx, const sgm_aabb* bounds, double voxel_size, sgm_emap** out) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!out || !bounds) fail(SGM_ERR_INVALID, "emap: null argument");
+        *out = nullptr;
+        if (voxel_size <= 0) fail(SGM_ERR_INVALID, "emap: voxel size must be > 0");  // explorer.cpp:13
+        auto em = std::make_unique<sgm_emap>();
+        uint64_t nvox = 1;
+        for (int a = 0; a < 3; ++a) {
+            em->p.origin[a] = bounds->min[a];
+            const double e = bounds->max[a] - bounds->min[a];  // Aabb::extent
+            em->p.dims[a] = std::max(static_cast<int>(std::ceil(e / voxel_size)), 1);  // :14-18
+            nvox *= static_cast<uint64_t>(em->p.dims[a]);
+        }
+        if (nvox >= (1ull << 31)) fail(SGM_ERR_UNSUPPORTED, "emap: more than 2^31-1 voxels");
+        em->p.voxel = voxel_size;
+        em->p.nvox = nvox;
+        cudaStream_t s = ctx->stream;
+        CK(em->grid.reserve(nvox));
+        CK(em->first_free.reserve(8 * nvox));
+        CK(em->first_hit.reserve(4 * nvox));
+        CK(em->log.reserve(4 * nvox));
+        CK(em->keys.reserve(8 * nvox));
+        CK(em->keys_alt.reserve(8 * nvox));
+        CK(em->ids.reserve(4 * nvox));
+        CK(em->ids_alt.reserve(4 * nvox));
+        CK(em->fresh.reserve(nvox));
+        CK(em->counters.reserve(3 * sizeof(unsigned long long)));
+        CK(em->h_counters.reserve(3 * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(em->grid.p, 0, nvox, s));  // VoxelState::Unknown
+        CK(cudaMemsetAsync(em->first_free.p, 0xff, 8 * nvox, s));
+        CK(cudaMemsetAsync(em->first_hit.p, 0xff, 4 * nvox, s));
+        CK(cudaMemsetAsync(em->fresh.p, 0, nvox, s));
+        CK(cudaStreamSynchronize(s));
+        *out = em.release();
+    });
+}
+
+void sgm_emap_destroy(sgm_ctx* ctx, sgm_emap* emap) {
+    if (!emap) return;
+    if (ctx) {
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+    }
+    delete emap;
+}
+
+int sgm_emap_info(sgm_ctx* ctx, const sgm_emap* em, double origin[3], double* voxel_size,
+                  int32_t dims[3], uint64_t* free_count, uint64_t* occupied_count,
+                  uint64_t* changelog_size) {
+    return guard(ctx, [&] {
+        if (!em) fail(SGM_ERR_INVALID, "emap is null");
+        for (int a = 0; a < 3; ++a) {
+            if (origin) origin[a] = em->p.origin[a];
+            if (dims) dims[a] = em->p.dims[a];
+        }
+        if (voxel_size) *voxel_size = em->p.voxel;
+        if (free_count) *free_count = em->free_count;
+        if (occupied_count) *occupied_count = em->occupied_count;
+        if (changelog_size) *changelog_size = em->log_n;
+    });
+}
+
+int sgm_emap_integrate_device(sgm_ctx* ctx, sgm_emap* em, const sgm_camera* camera,
+                              const sgm_pose* pose, const float* d_depth, int32_t stride,
+                              uint64_t* newly_freed) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!em || !pose) fail(SGM_ERR_INVALID, "emap: null argument");
+        const CamParams cam = to_cam(camera);
+        if (stride < 1) fail(SGM_ERR_INVALID, "emap: stride must be >= 1");
+        if (!d_depth) fail(SGM_ERR_INVALID, "emap: depth is null");
+        const uint64_t n = emap_integrate(ctx, em, cam, *pose, d_depth, stride);
+        if (newly_freed) *newly_freed = n;
+    });
+}
+
+int sgm_emap_integrate(sgm_ctx* ctx, sgm_emap* em, const sgm_camera* camera, const sgm_pose* pose,
+                       const float* depth, int32_t stride, uint64_t* newly_freed) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!em || !pose) fail(SGM_ERR_INVALID, "emap: null argument");
+        const CamParams cam = to_cam(camera);
+        if (stride < 1) fail(SGM_ERR_INVALID, "emap: stride must be >= 1");
+        if (!depth) fail(SGM_ERR_INVALID, "emap: depth is null");
+        const size_t bytes = 4ull * cam.W * cam.H;
+        CK(em->depth.reserve(bytes));
+        CK(cudaMemcpyAsync(em->depth.p, depth, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        const uint64_t n = emap_integrate(ctx, em, cam, *pose, em->depth.as<float>(), stride);
+        if (newly_freed) *newly_freed = n;
+    });
+}
+
+int sgm_emap_take_changelog(sgm_ctx* ctx, sgm_emap* em, int32_t* out, uint64_t capacity,
+                            uint64_t* n) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!em) fail(SGM_ERR_INVALID, "emap is null");
+        if (n) *n = em->log_n;
+        if (em->log_n == 0) return;
+        if (!out || capacity < em->log_n)
+            fail(SGM_ERR_INVALID, "take_changelog: capacity %llu < %llu",
+                 static_cast<unsigned long long>(capacity), static_cast<unsigned long long>(em->log_n));
+        CK(cudaMemcpyAsync(out, em->log.p, 4 * em->log_n, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        em->log_n = 0;
+    });
+}
+
+int sgm_emap_reseed_changelog_with_free(sgm_ctx* ctx, sgm_emap* em) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!em) fail(SGM_ERR_INVALID, "emap is null");
+        cudaStream_t s = ctx->stream;
+        auto* cnt = em->counters.as<unsigned long long>();
+        CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
+        launch_emap_free_ids(em->p, em->grid.as<uint8_t>(), em->keys.as<unsigned long long>(),
+                             em->ids.as<int32_t>(), cnt, s);
+        ctx->stats.kernel_launches += 1;
+        auto* h = em->h_counters.as<unsigned long long>();
+        CK(cudaMemcpyAsync(h, cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        em->log_n = 0;  // explorer.cpp:119
+        emap_append_sorted(ctx, em, h[0]);
+    });
+}
+
+int sgm_emap_seed_region(sgm_ctx* ctx, sgm_emap* em, const sgm_aabb* box, int occupied) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!em || !box) fail(SGM_ERR_INVALID, "emap: null argument");
+        launch_emap_seed(em->p, *box, occupied ? 1 : 0, em->grid.as<uint8_t>(),
+                         em->first_free.as<unsigned long long>(), em->first_hit.as<uint32_t>(),
+                         ctx->stream);
+        ctx->stats.kernel_launches += 1;
+        emap_resolve(ctx, em);
+    });
+}
+
+int sgm_emap_grid(sgm_ctx* ctx, const sgm_emap* em, uint8_t* out, uint64_t capacity) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!em || !out) fail(SGM_ERR_INVALID, "emap: null argument");
+        if (capacity < em->p.nvox) fail(SGM_ERR_INVALID, "emap_grid: capacity < voxel count");
+        CK(cudaMemcpyAsync(out, em->grid.p, em->p.nvox, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int sgm_sample_candidates(sgm_ctx* ctx, sgm_emap* em, double v1, int32_t v2, const double* heights,
+                          int32_t n_heights, sgm_candidate* out, uint64_t capacity,
+                          uint64_t* n_out) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!em) fail(SGM_ERR_INVALID, "emap is null");
+        if (!(v1 > 0)) fail(SGM_ERR_INVALID, "sample_candidates: v1 must be > 0");
+        if (v2 < 0 || n_heights < 0 || (n_heights > 0 && !heights))
+            fail(SGM_ERR_INVALID, "sample_candidates: bad schedule");
+        if (n_out) *n_out = 0;
+        if (em->log_n == 0) return;  // fresh_set empty (explorer.cpp:161)
+        // lattice positions in the reference's loop order (:163-172)
+        double top[3];
+        for (int a = 0; a < 3; ++a) top[a] = em->p.origin[a] + static_cast<double>(em->p.dims[a]) * em->p.voxel;
+        std::vector<double> pos;
+        for (int hi = 0; hi < n_heights; ++hi)
+            for (double x = em->p.origin[0]; x <= top[0] + 1e-9; x += v1)
+                for (double z = em->p.origin[2]; z <= top[2] + 1e-9; z += v1) {
+                    pos.push_back(x);
+                    pos.push_back(heights[hi]);
+                    pos.push_back(z);
+                }
+        const int np = static_cast<int>(pos.size() / 3);
+        std::vector<uint8_t> ok(static_cast<size_t>(np));
+        cudaStream_t s = ctx->stream;
+        if (np > 0) {
+            CK(em->lattice.reserve(8 * pos.size()));
+            CK(em->ok.reserve(static_cast<size_t>(np)));
+            CK(cudaMemcpyAsync(em->lattice.p, pos.data(), 8 * pos.size(), cudaMemcpyHostToDevice, s));
+            launch_emap_mark(em->log.as<int32_t>(), em->log_n, em->fresh.as<uint8_t>(), 1, s);
+            launch_emap_lattice(em->p, em->lattice.as<double>(), np, em->grid.as<uint8_t>(),
+                                em->fresh.as<uint8_t>(), em->ok.as<uint8_t>(), s);
+            launch_emap_mark(em->log.as<int32_t>(), em->log_n, em->fresh.as<uint8_t>(), 0, s);
+            ctx->stats.kernel_launches += 3;
+            CK(cudaMemcpyAsync(ok.data(), em->ok.p, static_cast<size_t>(np), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
+        uint64_t hits = 0;
+        for (uint8_t f : ok) hits += f;
+        const uint64_t need = hits * static_cast<uint64_t>(v2);
+        if (n_out) *n_out = need;
+        if (need > 0 && (!out || capacity < need))
+            fail(SGM_ERR_INVALID, "sample_candidates: capacity %llu < %llu",
+                 static_cast<unsigned long long>(capacity), static_cast<unsigned long long>(need));
+        std::vector<double> dirs(3 * static_cast<size_t>(v2));
+        sgm_fibonacci_directions(v2, 45.0, dirs.data());
+        uint64_t w = 0;
+        for (int j = 0; j < np; ++j) {
+            if (!ok[static_cast<size_t>(j)]) continue;
+            for (int d = 0; d < v2; ++d, ++w) {
+                for (int a = 0; a < 3; ++a) {
+                    out[w].position[a] = pos[3 * static_cast<size_t>(j) + a];
+                    out[w].direction[a] = dirs[3 * static_cast<size_t>(d) + a];
+                }
+            }
+        }
+        em->log_n = 0;  // the changelog is consumed (:159)
+    });
 }
 
 }  // extern "C"

@@ -3,6 +3,7 @@
 // These are O(#views) fp64 scalar code; they are restated here (not linked from
 // the reference) with the reference's exact evaluation order so results are
 // bit-identical. Built with -ffp-contract=off.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <limits>
@@ -118,6 +119,21 @@ void sgm_candidate_pose(const double position[3], const double direction[3], sgm
     const double target[3] = {position[0] + direction[0], position[1] + direction[1],
                               position[2] + direction[2]};
     sgm_look_at(position, target, out);
+}
+
+// fibonacci_directions, proj/src/explorer.cpp:142-155 (libm sin/cos/sqrt, as the reference).
+void sgm_fibonacci_directions(int32_t count, double max_elevation_deg, double* out3) {
+    if (count <= 0 || !out3) return;
+    const double golden_angle = M_PI * (3.0 - std::sqrt(5.0));
+    const double s_max = std::sin(max_elevation_deg * M_PI / 180.0);  // deg_to_rad, geometry.hpp:86
+    for (int j = 0; j < count; ++j) {
+        const double s = count == 1 ? 0.0 : s_max * (1.0 - (2.0 * j + 1.0) / count);
+        const double r = std::sqrt(std::max(0.0, 1.0 - s * s));
+        const double az = golden_angle * j;
+        out3[3 * j + 0] = r * std::cos(az);
+        out3[3 * j + 1] = s;
+        out3[3 * j + 2] = r * std::sin(az);
+    }
 }
 
 }  // extern "C"

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/sgm.h"
+
 namespace sgm {
 
 constexpr double kMaxFootprint = 0.999999;  // splat_render.hpp:41
@@ -182,6 +184,33 @@ void launch_chain(const DevMap& m, const PoseParams* d_pose, const CamParams& ca
                   cudaStream_t s);
 void launch_kl_clip(double* gsem, uint64_t n, int k, double clip, cudaStream_t s);
 void launch_finite(const double* v, uint64_t len, unsigned long long* bad, cudaStream_t s);
+
+// sgm_emap.cu (exploration map, explorer.cpp:11-184)
+struct EmapParams {
+    double origin[3];
+    double voxel;
+    int dims[3];
+    uint64_t nvox;
+};
+// Camera-to-world pose as the reference stores it (R row-major, t).
+struct WorldPose {
+    double R[9];
+    double t[3];
+};
+void launch_emap_rays(const EmapParams& e, const CamParams& cam, const WorldPose& P,
+                      const float* depth, int stride, const uint8_t* grid,
+                      unsigned long long* first_free, uint32_t* first_hit, cudaStream_t s);
+void launch_emap_seed(const EmapParams& e, const sgm_aabb& box, int occupied, const uint8_t* grid,
+                      unsigned long long* first_free, uint32_t* first_hit, cudaStream_t s);
+void launch_emap_resolve(const EmapParams& e, uint8_t* grid, unsigned long long* first_free,
+                         uint32_t* first_hit, unsigned long long* log_keys, int32_t* log_ids,
+                         unsigned long long* counters, cudaStream_t s);
+void launch_emap_lattice(const EmapParams& e, const double* pos, int n, const uint8_t* grid,
+                         const uint8_t* fresh, uint8_t* ok, cudaStream_t s);
+void launch_emap_mark(const int32_t* ids, uint64_t n, uint8_t* flags, uint8_t value,
+                      cudaStream_t s);
+void launch_emap_free_ids(const EmapParams& e, const uint8_t* grid, unsigned long long* log_keys,
+                          int32_t* log_ids, unsigned long long* counter, cudaStream_t s);
 
 // sgm_raster.cu
 GroupParams choose_groups(int C, int k);
