@@ -193,6 +193,59 @@ int sgm_backward(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam, const 
                  double report[7], double* g_center, double* g_log_radius,
                  double* g_opacity_logit, double* g_color, double* g_sem);
 
+/* ---- on-device map optimisation: optimize_map (mapper.cpp:241-283) ----
+ * A frame uploaded once (Frame, frame.hpp:12-65: rgb px*3, depth px, sem px*(C) floats, with
+ * its pose) and a trainer holding the map parameters plus the Adam moments in HBM. */
+typedef struct sgm_frame sgm_frame;
+typedef struct sgm_trainer sgm_trainer;
+
+/* AdamParams, optimizer.hpp:8-21. */
+typedef struct {
+    double lr_center, lr_radius, lr_opacity, lr_color, lr_sem;
+    double beta1, beta2, eps, eps_sem;
+} sgm_adam_params;
+
+/* The MapperConfig fields optimize_map reads (mapper.hpp:18-33). */
+typedef struct {
+    int32_t prune_every;
+    double prune_opacity;
+    double divergence_factor;
+    int32_t divergence_window;
+} sgm_optimize_config;
+
+int sgm_frame_upload(sgm_ctx* ctx, int32_t width, int32_t height, int32_t num_classes,
+                     const sgm_pose* pose, const float* rgb, const float* depth, const float* sem,
+                     sgm_frame** out);
+void sgm_frame_release(sgm_ctx* ctx, sgm_frame* frame);
+
+/* GaussianMap spans as in sgm_map_upload, plus the AdamState (mapper.hpp / optimizer.hpp:24-60):
+ * adam_mv = {m, v} each laid out center 3N | log_radius N | opacity_logit N | color 3N |
+ * sem kN (2 * (8 + k) * N doubles; NULL = zero moments) and its step count. */
+int sgm_trainer_create(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes,
+                       const double* centers, const double* log_radii, const double* opacity_logits,
+                       const double* colors, const uint16_t* sem_indices, const double* sem_probs,
+                       const double* adam_mv, int64_t step_count, sgm_trainer** out);
+void sgm_trainer_destroy(sgm_ctx* ctx, sgm_trainer* tr);
+int sgm_trainer_size(sgm_ctx* ctx, const sgm_trainer* tr, uint64_t* n, int64_t* step_count);
+/* Copies the current parameters (and, if adam_mv != NULL, the moments) back to the host. */
+int sgm_trainer_download(sgm_ctx* ctx, const sgm_trainer* tr, double* centers, double* log_radii,
+                         double* opacity_logits, double* colors, uint16_t* sem_indices,
+                         double* sem_probs, double* adam_mv);
+/* The creation-time row of each current Gaussian (prune_by_opacity's `kept`, composed over
+ * every prune since sgm_trainer_create): n uint32. */
+int sgm_trainer_rows(sgm_ctx* ctx, const sgm_trainer* tr, uint32_t* rows);
+/* optimize_map: `iters` round-robin iterations over `frames` of render(all(true)) ->
+ * mapping_loss + semantic_loss -> backward -> Adam step, with opacity pruning on the
+ * prune_every cadence and the reference's divergence check. history receives one LossReport
+ * (7 doubles, as sgm_backward) per completed iteration; *n_done their count. Errors as the
+ * reference: no frames / iters < 1 -> SGM_ERR_INVALID; divergence or a non-finite gradient ->
+ * SGM_ERR_INVALID with the iterations done so far in history. */
+int sgm_optimize_map(sgm_ctx* ctx, sgm_trainer* tr, const sgm_camera* cam, uint64_t n_frames,
+                     sgm_frame* const* frames, const sgm_options* opt,
+                     const sgm_adam_params* adam, const double weights[7],
+                     const sgm_optimize_config* cfg, int32_t iters, double* history,
+                     int32_t* n_done);
+
 /* combine_scores (explorer.cpp:225-248) on host fp64: returns 1 if any i_total > 0,
  * 0 if the pool is exhausted (or n == 0), negative on invalid arguments. */
 int sgm_combine_scores(uint64_t n, const double* n_missing, const double* entropy_sum,

@@ -475,6 +475,10 @@ class RefLib:
         L.ref_raycast_depth.restype = C.c_int
         L.ref_raycast_depth.argtypes = [_pd, _pd, C.c_int, _pd, C.c_int, _pd, _pi32, _pd, _pd,
                                         _pd, _pf]
+        L.ref_optimize_map.restype = C.c_int64
+        L.ref_optimize_map.argtypes = [C.c_uint64, C.c_int, C.c_int, _pd, _pd, _pd, _pd, _pu16,
+                                       _pd, _pi32, _pd, C.c_int, _pd, _pf, _pd, _pd, _pd, C.c_int,
+                                       _pd, _pi32, C.c_char_p, C.c_int]
         L.ref_backward.restype = C.c_int
         L.ref_backward.argtypes = [C.c_void_p, _pi32, _pd, _pd, _pd, _pd, C.c_int, _pf, _pf, _pf,
                                    _pd, C.c_int, C.c_int, _pd, _pd, _pd, _pd, _pd, _pd,
@@ -502,6 +506,49 @@ class RefLib:
         if rc:
             raise ValueError("raycast_depth: invalid scene")
         return out
+
+    def optimize_map(self, m, frames, cam, cfg, iters):
+        """The reference's optimize_map (mapper.cpp:241-283) from a zero AdamState.
+        Returns (history (n_done, 7), arrays dict of the final map, error or None)."""
+        n, k = m.size(), m.k()
+        arr = {"centers": np.ascontiguousarray(m.centers, dtype=np.float64).reshape(-1).copy(),
+               "log_radii": np.ascontiguousarray(m.log_radii, dtype=np.float64).copy(),
+               "opacity_logits": np.ascontiguousarray(m.opacity_logits, dtype=np.float64).copy(),
+               "colors": np.ascontiguousarray(m.colors, dtype=np.float64).reshape(-1).copy(),
+               "sem_indices": np.ascontiguousarray(m.sem_indices, dtype=np.uint16).reshape(-1).copy(),
+               "sem_probs": np.ascontiguousarray(m.sem_probs, dtype=np.float64).reshape(-1).copy()}
+        wh, intr = self._cam(cam)
+        poses = np.concatenate([np.concatenate([np.asarray(f.pose.R, np.float64).reshape(9),
+                                                np.asarray(f.pose.t, np.float64)]) for f in frames])
+        planes = np.concatenate([np.concatenate([np.asarray(f.rgb, np.float32).reshape(-1),
+                                                 np.asarray(f.depth, np.float32).reshape(-1),
+                                                 np.asarray(f.sem, np.float32).reshape(-1)])
+                                 for f in frames]).astype(np.float32)
+        a = cfg.adam
+        adam = np.array([a.lr_center, a.lr_radius, a.lr_opacity, a.lr_color, a.lr_sem, a.beta1,
+                         a.beta2, a.eps, a.eps_sem])
+        c = np.array([float(cfg.prune_every), cfg.prune_opacity, cfg.divergence_factor,
+                      float(cfg.divergence_window)])
+        w = cfg.weights
+        wv = np.array([w.lambda_hd, w.lambda_cos, float(w.mask_k), float(w.use_hd),
+                       float(w.use_cos), float(w.use_kl), w.kl_clip_norm])
+        hist = np.zeros((max(iters, 1), 7))
+        nh = C.c_int(0)
+        err = C.create_string_buffer(512)
+        pf = C.POINTER(C.c_float)
+        m_final = self.lib.ref_optimize_map(
+            n, k, m.num_classes(), _dp(arr["centers"]), _dp(arr["log_radii"]),
+            _dp(arr["opacity_logits"]), _dp(arr["colors"]), arr["sem_indices"].ctypes.data_as(_pu16),
+            _dp(arr["sem_probs"]), wh.ctypes.data_as(_pi32), _dp(intr), len(frames), _dp(poses),
+            planes.ctypes.data_as(pf), _dp(adam), _dp(c), _dp(wv), int(iters), _dp(hist),
+            C.byref(nh), err, 512)
+        if m_final < 0:
+            return hist[:0], None, err.value.decode()
+        mf = int(m_final)
+        out = {"centers": arr["centers"][:3 * mf], "log_radii": arr["log_radii"][:mf],
+               "opacity_logits": arr["opacity_logits"][:mf], "colors": arr["colors"][:3 * mf],
+               "sem_indices": arr["sem_indices"][:k * mf], "sem_probs": arr["sem_probs"][:k * mf]}
+        return hist[: nh.value], out, None
 
     def backward(self, m, cam, frame, weights, include_mapping=True, include_semantic=True,
                  opt=None):

@@ -446,3 +446,103 @@ int ref_raycast_depth(const double bmin[3], const double bmax[3], int n_boxes, c
 }
 
 }  // extern "C"
+
+// ---- optimize_map (proj/src/mapper.cpp:241-283) on the reference's own code ----
+#include "splatmap/mapper.hpp"
+
+extern "C" {
+
+// frames: n_frames poses (R row-major 9 + t 3 = 12 doubles each) and planes (rgb px*3,
+// depth px, sem px*(num_classes+1) floats each, concatenated per frame).
+// adam = {lr_center, lr_radius, lr_opacity, lr_color, lr_sem, beta1, beta2, eps, eps_sem};
+// cfg = {prune_every, prune_opacity, divergence_factor, divergence_window};
+// weights as ref_backward. The map arrays are updated in place (sized for the input n);
+// returns the final size, or -1 on a throw (message in err), and fills history (iters x 7).
+int64_t ref_optimize_map(uint64_t n, int k, int num_classes, double* centers, double* log_radii,
+                         double* logits, double* colors, uint16_t* sem_idx, double* sem_probs,
+                         const int32_t wh[2], const double intr[4], int n_frames,
+                         const double* poses12, const float* planes, const double adam[9],
+                         const double cfg[4], const double weights[7], int iters, double* history,
+                         int* n_history, char* err, int err_cap) {
+    try {
+        GaussianMap map(k, num_classes);
+        for (uint64_t i = 0; i < n; ++i) {
+            SemanticGaussian g;
+            g.center = Vec3(centers[3 * i], centers[3 * i + 1], centers[3 * i + 2]);
+            g.log_radius = log_radii[i];
+            g.opacity_logit = logits[i];
+            g.color = Vec3(colors[3 * i], colors[3 * i + 1], colors[3 * i + 2]);
+            g.sem.indices.assign(sem_idx + i * k, sem_idx + (i + 1) * k);
+            g.sem.probs.assign(sem_probs + i * k, sem_probs + (i + 1) * k);
+            map.add(g);
+        }
+        CameraModel cam = make_cam(wh, intr);
+        const size_t px = static_cast<size_t>(wh[0]) * wh[1];
+        const size_t C = static_cast<size_t>(num_classes) + 1;
+        std::vector<Frame> fr(static_cast<size_t>(n_frames));
+        std::vector<const Frame*> fp;
+        for (int f = 0; f < n_frames; ++f) {
+            Frame& F = fr[f];
+            F.width = wh[0];
+            F.height = wh[1];
+            F.num_classes = num_classes;
+            F.pose = make_pose(poses12 + 12 * f, poses12 + 12 * f + 9);
+            const float* base = planes + static_cast<size_t>(f) * px * (4 + C);
+            F.rgb.assign(base, base + 3 * px);
+            F.depth.assign(base + 3 * px, base + 4 * px);
+            F.sem.assign(base + 4 * px, base + 4 * px + C * px);
+            fp.push_back(&F);
+        }
+        MapperConfig mc;
+        mc.adam.lr_center = adam[0];
+        mc.adam.lr_radius = adam[1];
+        mc.adam.lr_opacity = adam[2];
+        mc.adam.lr_color = adam[3];
+        mc.adam.lr_sem = adam[4];
+        mc.adam.beta1 = adam[5];
+        mc.adam.beta2 = adam[6];
+        mc.adam.eps = adam[7];
+        mc.adam.eps_sem = adam[8];
+        mc.prune_every = static_cast<int>(cfg[0]);
+        mc.prune_opacity = cfg[1];
+        mc.divergence_factor = cfg[2];
+        mc.divergence_window = static_cast<int>(cfg[3]);
+        mc.weights.lambda_hd = weights[0];
+        mc.weights.lambda_cos = weights[1];
+        mc.weights.mask_k = static_cast<int>(weights[2]);
+        mc.weights.use_hd = weights[3] != 0.0;
+        mc.weights.use_cos = weights[4] != 0.0;
+        mc.weights.use_kl = weights[5] != 0.0;
+        mc.weights.kl_clip_norm = weights[6];
+        AdamState st;
+        auto hist = optimize_map(map, st, fp, cam, mc, iters);
+        *n_history = static_cast<int>(hist.size());
+        for (size_t i = 0; i < hist.size(); ++i) {
+            const LossReport& r = hist[i];
+            double* h = history + 7 * i;
+            h[0] = r.photometric;
+            h[1] = r.depth;
+            h[2] = r.semantic;
+            h[3] = static_cast<double>(r.photometric_px);
+            h[4] = static_cast<double>(r.depth_px);
+            h[5] = static_cast<double>(r.semantic_px);
+            h[6] = static_cast<double>(r.uncovered_px);
+        }
+        const size_t m = map.size();
+        std::memcpy(centers, map.centers().data(), m * 24);
+        std::memcpy(log_radii, map.log_radii().data(), m * 8);
+        std::memcpy(logits, map.opacity_logits().data(), m * 8);
+        std::memcpy(colors, map.colors().data(), m * 24);
+        std::memcpy(sem_idx, map.sem_indices().data(), m * k * 2);
+        std::memcpy(sem_probs, map.sem_probs().data(), m * k * 8);
+        return static_cast<int64_t>(m);
+    } catch (const std::exception& e) {
+        if (err && err_cap > 0) {
+            std::strncpy(err, e.what(), static_cast<size_t>(err_cap) - 1);
+            err[err_cap - 1] = 0;
+        }
+        return -1;
+    }
+}
+
+}  // extern "C"

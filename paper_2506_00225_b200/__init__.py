@@ -46,3 +46,11 @@ from .explore import (  # noqa: F401,E402
     fibonacci_directions,
     sample_candidates,
 )
+from .mapper import (  # noqa: F401,E402
+    AdamParams,
+    AdamState,
+    DeviceFrame,
+    MapperConfig,
+    MapTrainer,
+    optimize_map,
+)

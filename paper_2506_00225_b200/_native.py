@@ -59,6 +59,16 @@ class sgm_aabb(C.Structure):
     _fields_ = [("min", C.c_double * 3), ("max", C.c_double * 3)]
 
 
+class sgm_adam_params(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("lr_center", "lr_radius", "lr_opacity", "lr_color",
+                                          "lr_sem", "beta1", "beta2", "eps", "eps_sem")]
+
+
+class sgm_optimize_config(C.Structure):
+    _fields_ = [("prune_every", C.c_int32), ("prune_opacity", C.c_double),
+                ("divergence_factor", C.c_double), ("divergence_window", C.c_int32)]
+
+
 class sgm_stats(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("views", C.c_uint64),
                 ("visible", C.c_uint64), ("pairs", C.c_uint64),
@@ -78,6 +88,19 @@ _pi32 = C.POINTER(C.c_int32)
 _pu8 = C.POINTER(C.c_uint8)
 
 SIGNATURES = {
+    "sgm_frame_upload": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.POINTER(sgm_pose),
+                                   _pf, _pf, _pf, C.POINTER(_vp)]),
+    "sgm_frame_release": (None, [_vp, _vp]),
+    "sgm_trainer_create": (C.c_int, [_vp, C.c_uint64, C.c_int32, C.c_int32, _pd, _pd, _pd, _pd,
+                                     _pu16, _pd, _pd, C.c_int64, C.POINTER(_vp)]),
+    "sgm_trainer_destroy": (None, [_vp, _vp]),
+    "sgm_trainer_size": (C.c_int, [_vp, _vp, _pu64, C.POINTER(C.c_int64)]),
+    "sgm_trainer_rows": (C.c_int, [_vp, _vp, _pu32]),
+    "sgm_trainer_download": (C.c_int, [_vp, _vp, _pd, _pd, _pd, _pd, _pu16, _pd, _pd]),
+    "sgm_optimize_map": (C.c_int, [_vp, _vp, C.POINTER(sgm_camera), C.c_uint64, C.POINTER(_vp),
+                                   C.POINTER(sgm_options), C.POINTER(sgm_adam_params), _pd,
+                                   C.POINTER(sgm_optimize_config), C.c_int32, _pd,
+                                   C.POINTER(C.c_int32)]),
     "sgm_emap_create": (C.c_int, [_vp, C.POINTER(sgm_aabb), C.c_double, C.POINTER(_vp)]),
     "sgm_emap_destroy": (None, [_vp, _vp]),
     "sgm_emap_info": (C.c_int, [_vp, _vp, _pd, _pd, _pi32, _pu64, _pu64, _pu64]),

@@ -588,6 +588,236 @@ void do_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const
 
 }  // namespace
 
+namespace {
+
+// The mapping step on device-resident frame planes: render(all(true)) with contributor
+// counts, mapping_loss + semantic_loss, backward, projection->world chain, KL clip and the
+// finiteness check (losses.cpp:40-362). Gradients stay in ctx->bw_grad:
+//   center 3NS | log_radius NS | opacity_logit NS | color 3NS | sem k*NS | proj 5NS
+// (NS = max(N, 1)); report = LossReport fields. Throws like the reference on a non-finite
+// gradient.
+void backward_core(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const OptParams& o,
+                   const PoseParams& p, const float* f_rgb, const float* f_depth,
+                   const float* f_sem, const double weights[7], int include_mapping,
+                   int include_semantic, double report[7]) {
+    cudaStream_t s = ctx->stream;
+    const size_t px = static_cast<size_t>(cam.W) * cam.H;
+    const int C = map->dev.C, k = map->dev.k;
+    const uint64_t N = map->dev.n;
+    const size_t NS = std::max<uint64_t>(N, 1);
+    // device planes: rendered (sil, color, depth, sem) + frame (rgb, depth, sem)
+    const size_t rend_b = 8 * px * (5 + C);
+    CK(ctx->planes.reserve(rend_b));
+    CK(ctx->ccount.reserve(4 * (px + 1)));
+    CK(ctx->contrib.reserve(4));
+    CK(ctx->bw_flags.reserve(px + 16));
+    const size_t nlb = backward_loss_blocks(cam.W, cam.H);
+    CK(ctx->bw_part.reserve(64 * nlb + 64 + 64));
+    CK(ctx->bw_grad.reserve(8 * (NS * (8 + k) + 5 * NS) + 64));
+    double* d_sil = ctx->planes.as<double>();
+    double* d_color = d_sil + px;
+    double* d_depth = d_color + 3 * px;
+    double* d_sem = d_depth + px;
+    CK(cudaMemsetAsync(ctx->ccount.p, 0, 4 * (px + 1), s));
+    // 1. forward render + contributor counts (the reference's render(..., all(true)))
+    RenderTargets rt;
+    rt.channels = SGM_COLOR | SGM_DEPTH | SGM_SEMANTICS;
+    rt.color = d_color;
+    rt.depth = d_depth;
+    rt.sil = d_sil;
+    rt.sem = d_sem;
+    rt.contrib = ctx->contrib.as<uint32_t>();
+    rt.contrib_count = ctx->ccount.as<uint32_t>();
+    run_views(ctx, map, cam, o, 1, &p, Mode::Render, rt, nullptr, nullptr);
+    const uint32_t V = ctx->last_V;
+    // 2. loss masks, reports and mask counts
+    double* g = ctx->bw_grad.as<double>();
+    BackwardParams b{};
+    b.W = cam.W;
+    b.H = cam.H;
+    b.C = C;
+    b.color = d_color;
+    b.depth = d_depth;
+    b.sil = d_sil;
+    b.sem = d_sem;
+    b.ccount = ctx->ccount.as<uint32_t>();
+    b.rgb = f_rgb;
+    b.fdepth = f_depth;
+    b.fsem = f_sem;
+    b.flags = ctx->bw_flags.as<uint8_t>();
+    b.tau = std::log(weights[2]);
+    b.lambda_hd = weights[0];
+    b.lambda_cos = weights[1];
+    b.use_hd = weights[3] != 0.0;
+    b.use_cos = weights[4] != 0.0;
+    b.use_kl = weights[5] != 0.0;
+    b.include_mapping = include_mapping != 0;
+    b.include_semantic = include_semantic != 0;
+    double* totals = ctx->bw_part.as<double>() + 8 * nlb;
+    b.totals = totals;
+    b.gcenter = g;
+    b.glogr = g + 3 * NS;
+    b.glogit = g + 4 * NS;
+    b.gcolor = g + 5 * NS;
+    b.gsem = g + 8 * NS;
+    b.gproj = g + (8 + k) * NS;
+    b.sem_perm = map->dev.sem_perm;
+    CK(cudaMemsetAsync(g, 0, 8 * (NS * (8 + k) + 5 * NS), s));
+    launch_loss_pixels(b, ctx->bw_part.as<double>(), totals, s);
+    // 3. backward over the block lists of the render above (same binning)
+    RasterParams rp{};
+    rp.map = map->dev;
+    rp.cam = cam;
+    rp.opt = o;
+    rp.views = ctx->views.as<ViewDesc>();
+    rp.tiles_per_view = ((cam.W + kTile - 1) / kTile) * ((cam.H + kTile - 1) / kTile);
+    rp.raster_tiles_x = (cam.W + kTile - 1) / kTile;
+    rp.channels = rt.channels;
+    rp.groups = map->groups;
+    launch_backward(rp, b, s);
+    // 4. projection -> world, KL clipping, finiteness
+    launch_chain(map->dev, ctx->poses.as<PoseParams>(), cam, o, ctx->vals.as<uint32_t>(), V,
+                 b.gproj, b, s);
+    if (b.use_kl && b.include_semantic && weights[6] > 0.0)
+        launch_kl_clip(b.gsem, N, k, weights[6], s);
+    unsigned long long* bad = reinterpret_cast<unsigned long long*>(totals + 8);
+    CK(cudaMemsetAsync(bad, 0xff, 5 * 8, s));
+    const double* arrs[5] = {b.gcenter, b.glogr, b.glogit, b.gcolor, b.gsem};
+    const uint64_t lens[5] = {3 * N, N, N, 3 * N, static_cast<uint64_t>(k) * N};
+    for (int a = 0; a < 5; ++a) launch_finite(arrs[a], lens[a], bad + a, s);
+    ctx->stats.kernel_launches += 4 + 5;
+    CK(cudaGetLastError());
+    double h_tot[8];
+    unsigned long long h_bad[5];
+    CK(cudaMemcpyAsync(h_tot, totals, 64, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_bad, bad, 40, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    static const char* names[5] = {"center", "log_radius", "opacity_logit", "color", "sem"};
+    static const uint64_t stride[5] = {3, 1, 1, 3, 0};
+    for (int a = 0; a < 5; ++a)
+        if (h_bad[a] != ~0ull)  // losses.cpp:349-360
+            fail(SGM_ERR_INVALID, "backward: non-finite gradient for gaussian %llu parameter %s",
+                 static_cast<unsigned long long>(h_bad[a] / (a == 4 ? k : stride[a])), names[a]);
+    report[0] = h_tot[3] > 0 ? h_tot[0] / h_tot[3] : 0.0;  // photometric (:57)
+    report[1] = h_tot[4] > 0 ? h_tot[1] / h_tot[4] : 0.0;  // depth (:58)
+    report[2] = h_tot[5] > 0 ? h_tot[2] / h_tot[5] : 0.0;  // semantic (:158)
+    report[3] = h_tot[3];
+    report[4] = h_tot[4];
+    report[5] = h_tot[5];
+    report[6] = h_tot[6];
+}
+
+}  // namespace
+
+struct sgm_frame {
+    int W = 0, H = 0, C = 0;
+    PoseParams pose{};
+    DevBuf planes;  // rgb px*3 | depth px | sem px*C (floats)
+};
+
+struct sgm_trainer {
+    sgm_map map;       // render snapshot, re-derived after every step
+    DevBuf P, M, V;    // parameters and Adam moments (backward_core gradient layout, NS = n)
+    DevBuf sidx;       // sem_indices kN (reference order)
+    DevBuf rows;       // creation-time row of each current Gaussian (u32)
+    DevBuf keep, kept, sel_count, sel_tmp;
+    uint64_t n = 0;
+    int k = 0, num_classes = 0, dup = 0;
+    int64_t t = 0;     // AdamState::step_count
+};
+
+namespace {
+
+// (Re)allocates the render snapshot for the current n: class-sorted rows + permutation
+// from the master indices, then the activations (k_derive).
+void trainer_rebuild(sgm_ctx* ctx, sgm_trainer* tr) {
+    cudaStream_t s = ctx->stream;
+    const uint64_t n = tr->n;
+    const int k = tr->k, C = tr->num_classes + 1, kpad = (k + 7) / 8 * 8;
+    const size_t ns = std::max<uint64_t>(n, 1);
+    sgm_map& m = tr->map;
+    CK(m.geo.reserve(8 * 5 * ns));
+    CK(m.color.reserve(8 * 4 * ns));
+    CK(m.idx.reserve(2 * ns * kpad));
+    CK(m.prob.reserve(8 * ns * kpad));
+    CK(m.perm.reserve(2 * ns * kpad));
+    const double* P = tr->P.as<double>();
+    launch_sort_rows(tr->sidx.as<uint16_t>(), P + 8 * n, n, k, kpad, m.idx.as<uint16_t>(),
+                     m.prob.as<double>(), m.perm.as<uint16_t>(), s);
+    launch_derive(P, n, k, kpad, m.perm.as<uint16_t>(), m.geo.as<double>(), m.color.as<double>(),
+                  m.prob.as<double>(), s);
+    ctx->stats.kernel_launches += n ? 2 : 0;
+    m.num_classes = tr->num_classes;
+    DevMap& d = m.dev;
+    d.n = n;
+    d.k = k;
+    d.kpad = kpad;
+    d.C = C;
+    const double* g = m.geo.as<double>();
+    d.cx = g;
+    d.cy = g + ns;
+    d.cz = g + 2 * ns;
+    d.rad = g + 3 * ns;
+    d.alpha = g + 4 * ns;
+    d.color4 = m.color.as<double>();
+    d.sem_idx = m.idx.as<uint16_t>();
+    d.sem_prob = m.prob.as<double>();
+    d.sem_perm = m.perm.as<uint16_t>();
+    d.dup_idx = tr->dup;
+    m.groups = choose_groups(C, k);
+    if (ctx->last_map == &m) ctx->last_valid = false;
+}
+
+// GaussianMap::prune_by_opacity + AdamState::compact (gaussian_map.cpp:97-124, mapper.cpp:53-69).
+void trainer_prune(sgm_ctx* ctx, sgm_trainer* tr, double thr) {
+    cudaStream_t s = ctx->stream;
+    const uint64_t n = tr->n;
+    if (n == 0) return;
+    const int k = tr->k;
+    CK(tr->keep.reserve(n));
+    CK(tr->kept.reserve(4 * n));
+    CK(tr->sel_count.reserve(8));
+    launch_keep_flags(tr->P.as<double>() + 4 * n, n, thr, tr->keep.as<uint8_t>(), s);
+    size_t tmp = 0;
+    cub::CountingInputIterator<uint32_t> ids(0);
+    CK(cub::DeviceSelect::Flagged(nullptr, tmp, ids, tr->keep.as<uint8_t>(), tr->kept.as<uint32_t>(),
+                                  tr->sel_count.as<uint32_t>(), static_cast<int>(n), s));
+    CK(tr->sel_tmp.reserve(tmp));
+    CK(cub::DeviceSelect::Flagged(tr->sel_tmp.p, tmp, ids, tr->keep.as<uint8_t>(), tr->kept.as<uint32_t>(),
+                                  tr->sel_count.as<uint32_t>(), static_cast<int>(n), s));
+    ctx->stats.kernel_launches += 2;
+    uint32_t m = 0;
+    CK(cudaMemcpyAsync(&m, tr->sel_count.p, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (m == n) return;
+    const size_t per = 8 + static_cast<size_t>(k);
+    const size_t ms = std::max<uint64_t>(m, 1);
+    const uint32_t* kept = tr->kept.as<uint32_t>();
+    // segments of the shared layout: (offset in units of n, stride)
+    const int seg_off[5] = {0, 3, 4, 5, 8};
+    const int seg_w[5] = {3, 1, 1, 3, k};
+    for (DevBuf* buf : {&tr->P, &tr->M, &tr->V}) {
+        DevBuf next;
+        CK(next.reserve(8 * per * ms));
+        for (int g = 0; g < 5; ++g)
+            launch_gather_f64(buf->as<double>() + seg_off[g] * n, next.as<double>() + seg_off[g] * m, kept,
+                              m, seg_w[g], s);
+        *buf = std::move(next);
+    }
+    DevBuf nidx, nrows;
+    CK(nidx.reserve(2 * k * ms));
+    CK(nrows.reserve(4 * ms));
+    launch_gather_u16(tr->sidx.as<uint16_t>(), nidx.as<uint16_t>(), kept, m, k, s);
+    launch_gather_u16(tr->rows.as<uint16_t>(), nrows.as<uint16_t>(), kept, m, 2, s);  // u32 as 2 x u16
+    tr->sidx = std::move(nidx);
+    tr->rows = std::move(nrows);
+    ctx->stats.kernel_launches += 16;
+    tr->n = m;
+    trainer_rebuild(ctx, tr);
+}
+
+}  // namespace
+
 struct sgm_emap {
     EmapParams p{};
     DevBuf grid, first_free, first_hit, log, keys, keys_alt, ids, ids_alt, fresh, counters, depth,
@@ -1103,119 +1333,22 @@ int sgm_backward(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, con
         const int C = map->dev.C, k = map->dev.k;
         const uint64_t N = map->dev.n;
         const size_t NS = std::max<uint64_t>(N, 1);
-        // device planes: rendered (sil, color, depth, sem) + frame (rgb, depth, sem)
-        const size_t rend_b = 8 * px * (5 + C), frame_b = 4 * px * (4 + C);
-        CK(ctx->planes.reserve(rend_b));
-        CK(ctx->bw_frame.reserve(frame_b + 16));
-        CK(ctx->ccount.reserve(4 * (px + 1)));
-        CK(ctx->contrib.reserve(4));
-        CK(ctx->bw_flags.reserve(px + 16));
-        const size_t nlb = backward_loss_blocks(cam.W, cam.H);
-        CK(ctx->bw_part.reserve(64 * nlb + 64 + 64));
-        CK(ctx->bw_grad.reserve(8 * (NS * (8 + k) + 5 * NS) + 64));
-        double* d_sil = ctx->planes.as<double>();
-        double* d_color = d_sil + px;
-        double* d_depth = d_color + 3 * px;
-        double* d_sem = d_depth + px;
+        CK(ctx->bw_frame.reserve(4 * px * (4 + C) + 16));
         float* f_rgb = ctx->bw_frame.as<float>();
         float* f_depth = f_rgb + 3 * px;
         float* f_sem = f_depth + px;
         CK(cudaMemcpyAsync(f_rgb, rgb, 12 * px, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(f_depth, depth, 4 * px, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(f_sem, sem, 4 * px * C, cudaMemcpyHostToDevice, s));
-        CK(cudaMemsetAsync(ctx->ccount.p, 0, 4 * (px + 1), s));
-        // 1. forward render + contributor counts (the reference's render(..., all(true)))
-        RenderTargets rt;
-        rt.channels = SGM_COLOR | SGM_DEPTH | SGM_SEMANTICS;
-        rt.color = d_color;
-        rt.depth = d_depth;
-        rt.sil = d_sil;
-        rt.sem = d_sem;
-        rt.contrib = ctx->contrib.as<uint32_t>();
-        rt.contrib_count = ctx->ccount.as<uint32_t>();
-        run_views(ctx, map, cam, o, 1, &p, Mode::Render, rt, nullptr, nullptr);
-        const uint32_t V = ctx->last_V;
-        // 2. loss masks, reports and mask counts
-        double* g = ctx->bw_grad.as<double>();
-        BackwardParams b{};
-        b.W = cam.W;
-        b.H = cam.H;
-        b.C = C;
-        b.color = d_color;
-        b.depth = d_depth;
-        b.sil = d_sil;
-        b.sem = d_sem;
-        b.ccount = ctx->ccount.as<uint32_t>();
-        b.rgb = f_rgb;
-        b.fdepth = f_depth;
-        b.fsem = f_sem;
-        b.flags = ctx->bw_flags.as<uint8_t>();
-        b.tau = std::log(weights[2]);
-        b.lambda_hd = weights[0];
-        b.lambda_cos = weights[1];
-        b.use_hd = weights[3] != 0.0;
-        b.use_cos = weights[4] != 0.0;
-        b.use_kl = weights[5] != 0.0;
-        b.include_mapping = include_mapping != 0;
-        b.include_semantic = include_semantic != 0;
-        double* totals = ctx->bw_part.as<double>() + 8 * nlb;
-        b.totals = totals;
-        b.gcenter = g;
-        b.glogr = g + 3 * NS;
-        b.glogit = g + 4 * NS;
-        b.gcolor = g + 5 * NS;
-        b.gsem = g + 8 * NS;
-        b.gproj = g + (8 + k) * NS;
-        b.sem_perm = map->dev.sem_perm;
-        CK(cudaMemsetAsync(g, 0, 8 * (NS * (8 + k) + 5 * NS), s));
-        launch_loss_pixels(b, ctx->bw_part.as<double>(), totals, s);
-        // 3. backward over the block lists of the render above (same binning)
-        RasterParams rp{};
-        rp.map = map->dev;
-        rp.cam = cam;
-        rp.opt = o;
-        rp.views = ctx->views.as<ViewDesc>();
-        rp.tiles_per_view = ((cam.W + kTile - 1) / kTile) * ((cam.H + kTile - 1) / kTile);
-        rp.raster_tiles_x = (cam.W + kTile - 1) / kTile;
-        rp.channels = rt.channels;
-        rp.groups = map->groups;
-        launch_backward(rp, b, s);
-        // 4. projection -> world, KL clipping, finiteness
-        launch_chain(map->dev, ctx->poses.as<PoseParams>(), cam, o, ctx->vals.as<uint32_t>(), V,
-                     b.gproj, b, s);
-        if (b.use_kl && b.include_semantic && weights[6] > 0.0)
-            launch_kl_clip(b.gsem, N, k, weights[6], s);
-        unsigned long long* bad = reinterpret_cast<unsigned long long*>(totals + 8);
-        CK(cudaMemsetAsync(bad, 0xff, 5 * 8, s));
-        const double* arrs[5] = {b.gcenter, b.glogr, b.glogit, b.gcolor, b.gsem};
-        const uint64_t lens[5] = {3 * N, N, N, 3 * N, static_cast<uint64_t>(k) * N};
-        for (int a = 0; a < 5; ++a) launch_finite(arrs[a], lens[a], bad + a, s);
-        ctx->stats.kernel_launches += 4 + 5;
-        CK(cudaGetLastError());
-        double h_tot[8];
-        unsigned long long h_bad[5];
-        CK(cudaMemcpyAsync(h_tot, totals, 64, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(h_bad, bad, 40, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        static const char* names[5] = {"center", "log_radius", "opacity_logit", "color", "sem"};
-        static const uint64_t stride[5] = {3, 1, 1, 3, 0};
-        for (int a = 0; a < 5; ++a)
-            if (h_bad[a] != ~0ull)  // losses.cpp:349-360
-                fail(SGM_ERR_INVALID, "backward: non-finite gradient for gaussian %llu parameter %s",
-                     static_cast<unsigned long long>(h_bad[a] / (a == 4 ? k : stride[a])), names[a]);
-        report[0] = h_tot[3] > 0 ? h_tot[0] / h_tot[3] : 0.0;  // photometric (:57)
-        report[1] = h_tot[4] > 0 ? h_tot[1] / h_tot[4] : 0.0;  // depth (:58)
-        report[2] = h_tot[5] > 0 ? h_tot[2] / h_tot[5] : 0.0;  // semantic (:158)
-        report[3] = h_tot[3];
-        report[4] = h_tot[4];
-        report[5] = h_tot[5];
-        report[6] = h_tot[6];
+        backward_core(ctx, map, cam, o, p, f_rgb, f_depth, f_sem, weights, include_mapping,
+                      include_semantic, report);
+        const double* g = ctx->bw_grad.as<double>();
         if (N) {
-            if (g_center) CK(cudaMemcpyAsync(g_center, b.gcenter, 24 * N, cudaMemcpyDeviceToHost, s));
-            if (g_log_radius) CK(cudaMemcpyAsync(g_log_radius, b.glogr, 8 * N, cudaMemcpyDeviceToHost, s));
-            if (g_opacity_logit) CK(cudaMemcpyAsync(g_opacity_logit, b.glogit, 8 * N, cudaMemcpyDeviceToHost, s));
-            if (g_color) CK(cudaMemcpyAsync(g_color, b.gcolor, 24 * N, cudaMemcpyDeviceToHost, s));
-            if (g_sem) CK(cudaMemcpyAsync(g_sem, b.gsem, 8 * N * k, cudaMemcpyDeviceToHost, s));
+            if (g_center) CK(cudaMemcpyAsync(g_center, g, 24 * N, cudaMemcpyDeviceToHost, s));
+            if (g_log_radius) CK(cudaMemcpyAsync(g_log_radius, g + 3 * NS, 8 * N, cudaMemcpyDeviceToHost, s));
+            if (g_opacity_logit) CK(cudaMemcpyAsync(g_opacity_logit, g + 4 * NS, 8 * N, cudaMemcpyDeviceToHost, s));
+            if (g_color) CK(cudaMemcpyAsync(g_color, g + 5 * NS, 24 * N, cudaMemcpyDeviceToHost, s));
+            if (g_sem) CK(cudaMemcpyAsync(g_sem, g + 8 * NS, 8 * N * k, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
         }
     });
@@ -1442,6 +1575,223 @@ int sgm_sample_candidates(sgm_ctx* ctx, sgm_emap* em, double v1, int32_t v2, con
             }
         }
         em->log_n = 0;  // the changelog is consumed (:159)
+    });
+}
+
+
+// ---------------------------------------------------------------- on-device optimize_map (f2)
+
+int sgm_frame_upload(sgm_ctx* ctx, int32_t width, int32_t height, int32_t num_classes,
+                     const sgm_pose* pose, const float* rgb, const float* depth, const float* sem,
+                     sgm_frame** out) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!out || !pose || !rgb || !depth || !sem) fail(SGM_ERR_INVALID, "frame: null argument");
+        *out = nullptr;
+        if (width <= 0 || height <= 0 || num_classes < 0) fail(SGM_ERR_INVALID, "frame: bad size");
+        auto f = std::make_unique<sgm_frame>();
+        f->W = width;
+        f->H = height;
+        f->C = num_classes + 1;
+        f->pose = to_pose(*pose);
+        const size_t px = static_cast<size_t>(width) * height;
+        CK(f->planes.reserve(4 * px * (4 + f->C)));
+        float* d = f->planes.as<float>();
+        CK(cudaMemcpyAsync(d, rgb, 12 * px, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(d + 3 * px, depth, 4 * px, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(d + 4 * px, sem, 4 * px * f->C, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        *out = f.release();
+    });
+}
+
+void sgm_frame_release(sgm_ctx* ctx, sgm_frame* frame) {
+    if (!frame) return;
+    if (ctx) {
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+    }
+    delete frame;
+}
+
+int sgm_trainer_create(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes,
+                       const double* centers, const double* log_radii, const double* opacity_logits,
+                       const double* colors, const uint16_t* sem_indices, const double* sem_probs,
+                       const double* adam_mv, int64_t step_count, sgm_trainer** out) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!out) fail(SGM_ERR_INVALID, "out is null");
+        *out = nullptr;
+        if (k < 1 || k > num_classes + 1) fail(SGM_ERR_INVALID, "map: k must be in [1, num_classes+1]");
+        if (n > 0 && (!centers || !log_radii || !opacity_logits || !colors || !sem_indices || !sem_probs))
+            fail(SGM_ERR_INVALID, "map: null array with n > 0");
+        if (n >= (1ull << 31)) fail(SGM_ERR_UNSUPPORTED, "trainer: more than 2^31-1 Gaussians");
+        if (step_count < 0) fail(SGM_ERR_INVALID, "trainer: negative step count");
+        const int C = num_classes + 1;
+        int dup = 0;
+        std::vector<uint32_t> seen(static_cast<size_t>(C), 0xffffffffu);
+        for (uint64_t i = 0; i < n; ++i)
+            for (int j = 0; j < k; ++j) {
+                const uint16_t c = sem_indices[i * k + j];
+                if (c >= C) fail(SGM_ERR_INVALID, "map: semantic index >= channels %d", C);
+                if (seen[c] == static_cast<uint32_t>(i)) dup = 1;
+                seen[c] = static_cast<uint32_t>(i);
+            }
+        auto tr = std::make_unique<sgm_trainer>();
+        tr->n = n;
+        tr->k = k;
+        tr->num_classes = num_classes;
+        tr->t = step_count;
+        tr->dup = dup;
+        const size_t per = 8 + static_cast<size_t>(k);
+        const size_t ns = std::max<uint64_t>(n, 1);
+        cudaStream_t s = ctx->stream;
+        CK(tr->P.reserve(8 * per * ns));
+        CK(tr->M.reserve(8 * per * ns));
+        CK(tr->V.reserve(8 * per * ns));
+        CK(tr->sidx.reserve(2 * k * ns));
+        CK(tr->rows.reserve(4 * ns));
+        {
+            std::vector<uint32_t> iota(n);
+            for (uint64_t i = 0; i < n; ++i) iota[i] = static_cast<uint32_t>(i);
+            if (n) CK(cudaMemcpyAsync(tr->rows.p, iota.data(), 4 * n, cudaMemcpyHostToDevice, s));
+            CK(cudaStreamSynchronize(s));
+        }
+        double* P = tr->P.as<double>();
+        if (n) {
+            CK(cudaMemcpyAsync(P, centers, 24 * n, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(P + 3 * n, log_radii, 8 * n, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(P + 4 * n, opacity_logits, 8 * n, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(P + 5 * n, colors, 24 * n, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(P + 8 * n, sem_probs, 8 * k * n, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(tr->sidx.p, sem_indices, 2 * k * n, cudaMemcpyHostToDevice, s));
+            if (adam_mv) {
+                CK(cudaMemcpyAsync(tr->M.p, adam_mv, 8 * per * n, cudaMemcpyHostToDevice, s));
+                CK(cudaMemcpyAsync(tr->V.p, adam_mv + per * n, 8 * per * n, cudaMemcpyHostToDevice, s));
+            } else {
+                CK(cudaMemsetAsync(tr->M.p, 0, 8 * per * n, s));
+                CK(cudaMemsetAsync(tr->V.p, 0, 8 * per * n, s));
+            }
+        }
+        trainer_rebuild(ctx, tr.get());
+        CK(cudaStreamSynchronize(s));
+        *out = tr.release();
+    });
+}
+
+void sgm_trainer_destroy(sgm_ctx* ctx, sgm_trainer* tr) {
+    if (!tr) return;
+    if (ctx) {
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        if (ctx->last_map == &tr->map) ctx->last_valid = false;
+    }
+    delete tr;
+}
+
+int sgm_trainer_size(sgm_ctx* ctx, const sgm_trainer* tr, uint64_t* n, int64_t* step_count) {
+    return guard(ctx, [&] {
+        if (!tr) fail(SGM_ERR_INVALID, "trainer is null");
+        if (n) *n = tr->n;
+        if (step_count) *step_count = tr->t;
+    });
+}
+
+int sgm_trainer_rows(sgm_ctx* ctx, const sgm_trainer* tr, uint32_t* rows) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!tr || (!rows && tr->n)) fail(SGM_ERR_INVALID, "null argument");
+        if (tr->n == 0) return;
+        CK(cudaMemcpyAsync(rows, tr->rows.p, 4 * tr->n, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int sgm_trainer_download(sgm_ctx* ctx, const sgm_trainer* tr, double* centers, double* log_radii,
+                         double* opacity_logits, double* colors, uint16_t* sem_indices,
+                         double* sem_probs, double* adam_mv) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!tr) fail(SGM_ERR_INVALID, "trainer is null");
+        const uint64_t n = tr->n;
+        if (n == 0) return;
+        const int k = tr->k;
+        const size_t per = 8 + static_cast<size_t>(k);
+        cudaStream_t s = ctx->stream;
+        const double* P = tr->P.as<double>();
+        if (centers) CK(cudaMemcpyAsync(centers, P, 24 * n, cudaMemcpyDeviceToHost, s));
+        if (log_radii) CK(cudaMemcpyAsync(log_radii, P + 3 * n, 8 * n, cudaMemcpyDeviceToHost, s));
+        if (opacity_logits) CK(cudaMemcpyAsync(opacity_logits, P + 4 * n, 8 * n, cudaMemcpyDeviceToHost, s));
+        if (colors) CK(cudaMemcpyAsync(colors, P + 5 * n, 24 * n, cudaMemcpyDeviceToHost, s));
+        if (sem_probs) CK(cudaMemcpyAsync(sem_probs, P + 8 * n, 8 * k * n, cudaMemcpyDeviceToHost, s));
+        if (sem_indices) CK(cudaMemcpyAsync(sem_indices, tr->sidx.p, 2 * k * n, cudaMemcpyDeviceToHost, s));
+        if (adam_mv) {
+            CK(cudaMemcpyAsync(adam_mv, tr->M.p, 8 * per * n, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(adam_mv + per * n, tr->V.p, 8 * per * n, cudaMemcpyDeviceToHost, s));
+        }
+        CK(cudaStreamSynchronize(s));
+    });
+}
+
+int sgm_optimize_map(sgm_ctx* ctx, sgm_trainer* tr, const sgm_camera* camera, uint64_t n_frames,
+                     sgm_frame* const* frames, const sgm_options* opt,
+                     const sgm_adam_params* adam, const double weights[7],
+                     const sgm_optimize_config* cfg, int32_t iters, double* history,
+                     int32_t* n_done) {
+    if (n_done) *n_done = 0;
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!tr || !adam || !weights || !cfg) fail(SGM_ERR_INVALID, "optimize_map: null argument");
+        if (n_frames == 0 || !frames) fail(SGM_ERR_INVALID, "optimize_map: no frames");  // mapper.cpp:244
+        if (iters < 1) fail(SGM_ERR_INVALID, "optimize_map: iters must be >= 1");       // :245
+        const CamParams cam = to_cam(camera);
+        const OptParams o = to_opt(opt, cam);
+        for (uint64_t f = 0; f < n_frames; ++f) {
+            if (!frames[f]) fail(SGM_ERR_INVALID, "optimize_map: null frame");
+            if (frames[f]->W != cam.W || frames[f]->H != cam.H || frames[f]->C != tr->num_classes + 1)
+                fail(SGM_ERR_INVALID, "optimize_map: frame %llu does not match the camera / classes",
+                     static_cast<unsigned long long>(f));
+        }
+        const AdamHyper h{adam->lr_center, adam->lr_radius, adam->lr_opacity, adam->lr_color,
+                          adam->lr_sem,    adam->beta1,     adam->beta2,      adam->eps,
+                          adam->eps_sem};
+        cudaStream_t s = ctx->stream;
+        double initial_total = -1.0;
+        int diverged_streak = 0;
+        for (int it = 0; it < iters; ++it) {
+            const sgm_frame* kf = frames[static_cast<uint64_t>(it) % n_frames];
+            if (tr->n == 0) break;  // :253
+            const size_t px = static_cast<size_t>(cam.W) * cam.H;
+            const float* fp = kf->planes.as<float>();
+            double rep[7];
+            backward_core(ctx, &tr->map, cam, o, kf->pose, fp, fp + 3 * px, fp + 4 * px, weights, 1, 1,
+                          rep);
+            // adam.step (mapper.cpp:10-51)
+            ++tr->t;
+            const double bc1 = 1.0 - std::pow(h.beta1, static_cast<double>(tr->t));
+            const double bc2 = 1.0 - std::pow(h.beta2, static_cast<double>(tr->t));
+            launch_adam(tr->P.as<double>(), ctx->bw_grad.as<double>(), tr->M.as<double>(),
+                        tr->V.as<double>(), tr->n, tr->k, h, bc1, bc2, s);
+            launch_derive(tr->P.as<double>(), tr->n, tr->k, tr->map.dev.kpad, tr->map.dev.sem_perm,
+                          tr->map.geo.as<double>(), tr->map.color.as<double>(), tr->map.prob.as<double>(), s);
+            ctx->stats.kernel_launches += 3;
+            CK(cudaGetLastError());
+            if (ctx->last_map == &tr->map) ctx->last_valid = false;
+            const double total = (rep[1] + 0.5 * rep[0]) + rep[2];  // LossReport::total (losses.hpp:29-30)
+            if (history) std::memcpy(history + 7 * static_cast<size_t>(it), rep, sizeof(rep));
+            if (initial_total < 0) initial_total = total;
+            if (initial_total > 0 && total > cfg->divergence_factor * initial_total) {
+                if (++diverged_streak >= cfg->divergence_window)
+                    fail(SGM_ERR_INVALID,
+                         "optimize_map: diverged (loss %f vs initial %f for %d iterations)", total,
+                         initial_total, diverged_streak);
+            } else {
+                diverged_streak = 0;
+            }
+            if (cfg->prune_every > 0 && tr->t % cfg->prune_every == 0) trainer_prune(ctx, tr, cfg->prune_opacity);
+            if (n_done) *n_done = it + 1;
+        }
+        CK(cudaStreamSynchronize(s));
     });
 }
 

@@ -212,6 +212,20 @@ void launch_emap_mark(const int32_t* ids, uint64_t n, uint8_t* flags, uint8_t va
 void launch_emap_free_ids(const EmapParams& e, const uint8_t* grid, unsigned long long* log_keys,
                           int32_t* log_ids, unsigned long long* counter, cudaStream_t s);
 
+// sgm_optim.cu (AdamState::step, prune, snapshot re-derivation)
+struct AdamHyper {
+    double lr_center, lr_radius, lr_opacity, lr_color, lr_sem, beta1, beta2, eps, eps_sem;
+};
+void launch_adam(double* P, const double* G, double* M, double* V, uint64_t n, int k,
+                 const AdamHyper& h, double bc1, double bc2, cudaStream_t s);
+void launch_derive(const double* P, uint64_t n, int k, int kpad, const uint16_t* perm, double* geo,
+                   double* color4, double* sprob, cudaStream_t s);
+void launch_keep_flags(const double* logit, uint64_t n, double thr, uint8_t* keep, cudaStream_t s);
+void launch_gather_f64(const double* src, double* dst, const uint32_t* kept, uint64_t m, int stride,
+                       cudaStream_t s);
+void launch_gather_u16(const uint16_t* src, uint16_t* dst, const uint32_t* kept, uint64_t m,
+                       int stride, cudaStream_t s);
+
 // sgm_raster.cu
 GroupParams choose_groups(int C, int k);
 size_t raster_smem_bytes(const DevMap& m, const GroupParams& gp, bool render);
