@@ -219,6 +219,47 @@ def measure_render(ctx, stream, flush, args) -> dict:
     return out
 
 
+def measure_mapping(ctx, args) -> dict:
+    """The mapping caller of render: optimize_map iterations (render all(true) ->
+    losses -> backward -> Adam) on the cfg1 map against two resident synthetic keyframes,
+    timed with CUDA events on the library stream; the reference's own optimize_map on one
+    host core beside it (one iteration)."""
+    import torch
+    from paper_2506_00225_b200 import scenes
+    from paper_2506_00225_b200.mapper import DeviceFrame, MapperConfig, MapTrainer
+    cfg = 1
+    gm = scenes.make_map(cfg)
+    cam = scenes.CONFIGS[cfg].camera()
+    poses = scenes.render_poses(cfg, 2)
+    frames = [scenes.make_frame(cfg, p, seed=i) for i, p in enumerate(poses)]
+    dev = [DeviceFrame(f, ctx=ctx) for f in frames]
+    mc = MapperConfig(prune_every=0)
+    tr = MapTrainer(gm, ctx=ctx)
+    tr.optimize(dev, cam, mc, 2)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    iters = 60  # MapperConfig::iters_per_step (mapper.hpp:23)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    hist = tr.optimize(dev, cam, mc, iters)
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    out = {"ms_per_iter": ms / iters, "iters": iters, "frames": 2,
+           "workload": "cfg1 map (500k Gaussians), 1200x680x102 keyframes, render all(true) + "
+                       "mapping_loss + semantic_loss + backward + Adam per iteration",
+           "loss_first_last": [hist[0].total(), hist[-1].total()]}
+    try:
+        import oracle
+        ref = oracle.RefLib()
+        t0 = time.perf_counter()
+        ref.optimize_map(gm, frames, cam, mc, 1)
+        out["reference_cpu_1core_ms_per_iter"] = (time.perf_counter() - t0) * 1e3
+    except Exception as exc:
+        out["reference_cpu_1core_ms_per_iter"] = repr(exc)
+    return out
+
+
 def workload_config(cfg: int) -> dict:
     from paper_2506_00225_b200 import scenes
     sc = scenes.CONFIGS[cfg]
@@ -362,11 +403,16 @@ def main() -> None:
 
     # ---- secondary metric: semantic render ms/frame (device-resident and e2e) ----
     render_info = None
+    mapping_info = None
     if rank == 0:
         try:
             render_info = measure_render(ctx, stream, flush, args)
         except Exception as exc:  # reported, not fatal
             render_info = {"error": repr(exc)}
+        try:
+            mapping_info = measure_mapping(ctx, args)
+        except Exception as exc:  # reported, not fatal
+            mapping_info = {"error": repr(exc)}
 
     # ---- e2e through the public API (host inputs, map re-upload every step) ----
     h2d = int(gm.centers.nbytes + gm.log_radii.nbytes + gm.opacity_logits.nbytes +
@@ -465,6 +511,7 @@ def main() -> None:
             "argmax_view": int(best), "views_total_per_step": n_total,
             "with_fisher_gain": fisher,
             "render_ms_per_frame": render_info,
+            "mapping_optimize": mapping_info,
         }
         print(json.dumps(line), flush=True)
     if dist_on:

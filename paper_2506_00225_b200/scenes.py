@@ -171,3 +171,24 @@ def render_poses(cfg: int, count: int | None = None):
                                             math.sin(2 * math.pi * i / count)]), c)
                 for i in range(count)]
     return [cd.camera_pose() for cd in make_candidates(cfg, count)]
+
+
+def make_frame(cfg: int, pose, seed: int = 0, invalid: float = 0.1):
+    """Synthetic posed RGB-D-semantic observation at the config's camera (Frame,
+    frame.hpp:12-65): rgb in [0.1, 0.9], depth in [0.5, 3] m with `invalid` zeros, and a
+    low-entropy semantic simplex (0.7 on one channel) per pixel. Seeded, float32."""
+    from .splatmap import Frame
+    c = CONFIGS[cfg]
+    cam = c.camera()
+    rng = np.random.default_rng(10_000 + 100 * cfg + seed)
+    px = cam.width * cam.height
+    C = c.num_classes + 1
+    rgb = (0.1 + 0.8 * rng.uniform(0, 1, (px, 3))).astype(np.float32)
+    depth = np.where(rng.uniform(0, 1, px) < invalid, 0.0,
+                     0.5 + 2.5 * rng.uniform(0, 1, px)).astype(np.float32)
+    p = 0.05 + rng.uniform(0, 1, (px, C))
+    p /= p.sum(axis=1, keepdims=True)
+    sem = 0.3 * p
+    sem[np.arange(px), rng.integers(0, C, px)] += 0.7
+    return Frame(cam.width, cam.height, c.num_classes, pose, rgb.reshape(-1), depth,
+                 sem.astype(np.float32).reshape(-1))

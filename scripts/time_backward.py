@@ -21,7 +21,11 @@ def main():
     ap.add_argument("--config", type=int, default=0)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--no-ref", action="store_true")
+    ap.add_argument("--optimize", type=int, default=0,
+                    help="time N optimize_map iterations on 2 resident frames instead")
     a = ap.parse_args()
+    if a.optimize:
+        return time_optimize(a)
     gm = scenes.make_map(a.config)
     cam = scenes.CONFIGS[a.config].camera()
     pose = scenes.render_poses(a.config, 1)[0]
@@ -50,6 +54,36 @@ def main():
         print(f"  {name}: max|diff|/max|ref| = {err:.3e}")
         assert err < 1e-9, name
     print("PARITY OK")
+
+
+def time_optimize(a):
+    import torch
+    from paper_2506_00225_b200.mapper import DeviceFrame, MapperConfig, MapTrainer
+    gm = scenes.make_map(a.config)
+    cam = scenes.CONFIGS[a.config].camera()
+    poses = scenes.render_poses(a.config, 2)
+    frames = [random_frame(11 + i, cam, p, gm.num_classes()) for i, p in enumerate(poses)]
+    ctx = sgm.Context(0)
+    dev = [DeviceFrame(f, ctx=ctx) for f in frames]
+    cfg = MapperConfig(prune_every=0)
+    tr = MapTrainer(gm, ctx=ctx)
+    tr.optimize(dev, cam, cfg, 2)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    hist = tr.optimize(dev, cam, cfg, a.optimize)
+    dt = time.perf_counter() - t0
+    print(f"cfg{a.config} gpu optimize_map: {a.optimize} iters in {dt * 1e3:.1f} ms = "
+          f"{dt * 1e3 / a.optimize:.2f} ms/iter; loss {hist[0].total():.5f} -> {hist[-1].total():.5f}",
+          flush=True)
+    if a.no_ref:
+        return
+    from oracle import RefLib
+    ref = RefLib()
+    t0 = time.perf_counter()
+    hr, _, err = ref.optimize_map(gm, frames, cam, cfg, 2)
+    dt = time.perf_counter() - t0
+    print(f"cfg{a.config} reference optimize_map (1 core): 2 iters in {dt * 1e3:.0f} ms = "
+          f"{dt * 1e3 / 2:.0f} ms/iter")
 
 
 if __name__ == "__main__":
