@@ -18,7 +18,7 @@
 //   phase C  all 8 warps: the sparse semantic scatter. Warp g owns channel
 //            group g (C/8 channels) for all 64 pixels, two pixels per lane, so no
 //            two warps touch the same accumulator word. The accumulator is
-//            [C][32] double2 in shared memory (lane l holds pixels l and l+32):
+//            [C][32] double2 in shared memory (lane l holds pixels 2l, 2l+1):
 //            one LDS.128 / 2 DFMA / STS.128 per (Gaussian, class) entry covers
 //            the whole 8x8 block, and a warp's lanes hit 32 consecutive 16-byte
 //            words (no bank conflict).
@@ -40,7 +40,6 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kNB = 16;            // Gaussians per staged batch
 constexpr int kGroups = kWarps;    // channel groups: one warp each in phase C
-constexpr int kBnd = kGroups + 1;
 
 __host__ __device__ constexpr int align16(int b) { return (b + 15) & ~15; }
 
@@ -76,16 +75,18 @@ __host__ __device__ inline Layout make_layout(int C, int kpad, bool render) {
     return L;
 }
 
-// index of pixel q's slot in a [row][32] double2 array viewed as doubles
+// index of pixel q's slot in a [row][pitch2] double2 array viewed as doubles: lane l
+// holds the horizontally adjacent pixels 2l, 2l+1, so quarter-warp j (lanes 8j..8j+7)
+// covers tile rows 2j, 2j+1 and its shared-memory wavefront is skipped when none of
+// those 16 pixels receives weight from an entry
 __device__ __forceinline__ int pair_slot(int row, int pitch2, int q) {
-    return (row * pitch2 + (q & 31)) * 2 + (q >> 5);
+    return row * pitch2 * 2 + q;
 }
 
 template <bool kRender, bool kDup>
 __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int C = p.map.C;
-    const int k = p.map.k;
     const int kpad = p.map.kpad;
     const int Cg = p.groups.Cg;
     constexpr int apitch = acc_pitch(kRender);
@@ -301,10 +302,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
             double2* accl = acc2 + lane;
             for (int e = 0; e < n; ++e) {
                 const double2 w = W2[e * 32 + lane];
-                if (!__any_sync(0xffffffffu, (w.x != 0.0) | (w.y != 0.0))) continue;
+                const bool nz = (w.x != 0.0) | (w.y != 0.0);
+                if (!__any_sync(0xffffffffu, nz)) continue;
                 const int lo = g == 0 ? 0 : sbnd[e * 8 + g - 1], hi = sbnd[e * 8 + g];
                 const uint16_t* ei = si + e * kpad;
                 const double* ep = spr + e * kpad;
+                if (!nz) continue;  // lanes without weight issue no shared-memory traffic
                 if (kDup) {
                     for (int j = lo; j < hi; ++j) {  // repeated classes: in order
                         double2* a = accl + ei[j] * apitch;
@@ -370,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
             }
         }
     } else {
-        // clipped_entropy (:360-369) split by channel group: warp g, pixels lane, lane+32
+        // clipped_entropy (:360-369) split by channel group: warp g, pixels 2 lane, 2 lane + 1
         double S1x = 0.0, S2x = 0.0, S1y = 0.0, S2y = 0.0;
 #pragma unroll 2
         for (int c = c0; c < c1; ++c) {
@@ -381,8 +384,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
             S2x = __fma_rn(ax, log_table(ax), S2x);
             S2y = __fma_rn(ay, log_table(ay), S2y);
         }
-        red[g * kTilePx + lane] = make_double2(S1x, S2x);
-        red[g * kTilePx + lane + 32] = make_double2(S1y, S2y);
+        red[g * kTilePx + 2 * lane] = make_double2(S1x, S2x);
+        red[g * kTilePx + 2 * lane + 1] = make_double2(S1y, S2y);
         __syncthreads();
         if (t < kTilePx) {
             double S1 = 0.0, S2 = 0.0;

@@ -13,9 +13,9 @@ for ln in dis.splitlines():
     if m:
         cur_fn = m.group(1)
         continue
-    m = re.search(r'//## File ".*?", line (\d+)', ln)
+    m = re.search(r'//## File "(.*?)", line (\d+)', ln)
     if m:
-        cur_line = int(m.group(1))
+        cur_line = (m.group(1).rsplit("/", 1)[-1], int(m.group(2)))
         continue
     m = re.match(r"\s+/\*([0-9a-f]{4,})\*/", ln)
     if m and cur_fn and fsub in cur_fn:
@@ -27,10 +27,10 @@ data = [(int(r[0], 16), int(r[ie] or 0), int(r[samp] or 0)) for r in rows[2:] if
 base = min(a for a, _, _ in data)
 ci, cs = Counter(), Counter()
 for a, n, s in data:
-    l = lines.get(a - base, -1)
+    l = lines.get(a - base, ("?", -1))
     ci[l] += n
     cs[l] += s
 ti, ts = sum(ci.values()), sum(cs.values())
 print(f"total instructions {ti:.3e}  stall samples {ts}")
 for l, n in sorted(ci.items(), key=lambda kv: -kv[1])[:top]:
-    print(f"line {l:5d}  {100*n/ti:6.2f}% inst  {100*cs[l]/ts:6.2f}% stall")
+    print(f"{l[0]:>18s}:{l[1]:<5d} {100*n/ti:6.2f}% inst  {100*cs[l]/ts:6.2f}% stall")
