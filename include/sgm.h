@@ -246,6 +246,26 @@ int sgm_optimize_map(sgm_ctx* ctx, sgm_trainer* tr, const sgm_camera* cam, uint6
                      const sgm_optimize_config* cfg, int32_t iters, double* history,
                      int32_t* n_done);
 
+/* ---- evaluation on device render planes ----
+ * semantic_metrics (evaluator.cpp:93-238) + photometric_metrics (:274-297) over views
+ * added one at a time: each sgm_eval_add_view renders `map` at the frame's pose
+ * (RenderChannels::all()) into HBM and consumes the planes there; only the C x C confusion
+ * counts and a few sums per view leave the device. */
+typedef struct sgm_evaluator sgm_evaluator;
+
+int sgm_eval_create(sgm_ctx* ctx, int32_t num_classes, sgm_evaluator** out);
+void sgm_eval_destroy(sgm_ctx* ctx, sgm_evaluator* ev);
+/* Frame size must match cam and channels num_classes + 1 ("resolution mismatch"). */
+int sgm_eval_add_view(sgm_ctx* ctx, sgm_evaluator* ev, const sgm_map* map, const sgm_camera* cam,
+                      const sgm_options* opt, const sgm_frame* frame);
+/* MetricReport (evaluator.hpp:20-42). summary = {miou_pct, top1_pct, top3_pct, map_pct,
+ * f1_pct, psnr_db, depth_l1_cm}; per_view_miou / per_view_psnr: one per added view;
+ * per_class: rows {class_id, iou_pct, ap_pct, f1_pct, gt_pixels} sorted by class_id
+ * (at most num_classes rows), *n_per_class their count. No views -> SGM_ERR_INVALID
+ * ("view count mismatch"). Any output may be NULL. */
+int sgm_eval_report(sgm_ctx* ctx, sgm_evaluator* ev, double summary[7], double* per_view_miou,
+                    double* per_view_psnr, double* per_class, uint64_t* n_per_class);
+
 /* combine_scores (explorer.cpp:225-248) on host fp64: returns 1 if any i_total > 0,
  * 0 if the pool is exhausted (or n == 0), negative on invalid arguments. */
 int sgm_combine_scores(uint64_t n, const double* n_missing, const double* entropy_sum,

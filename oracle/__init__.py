@@ -307,6 +307,17 @@ class Oracle:
         return np.array(out.R[:]).reshape(3, 3), np.array(out.t[:])
 
 
+def _frames_blob(frames):
+    """(poses (n*12 f64: R row-major, t), planes (per frame rgb | depth | sem, f32))."""
+    poses = np.concatenate([np.concatenate([np.asarray(f.pose.R, np.float64).reshape(9),
+                                            np.asarray(f.pose.t, np.float64)]) for f in frames])
+    planes = np.concatenate([np.concatenate([np.asarray(f.rgb, np.float32).reshape(-1),
+                                             np.asarray(f.depth, np.float32).reshape(-1),
+                                             np.asarray(f.sem, np.float32).reshape(-1)])
+                             for f in frames]).astype(np.float32)
+    return np.ascontiguousarray(poses), np.ascontiguousarray(planes)
+
+
 def _v3(v):
     return np.ascontiguousarray(np.asarray(v, dtype=np.float64).reshape(3))
 
@@ -479,6 +490,9 @@ class RefLib:
         L.ref_optimize_map.argtypes = [C.c_uint64, C.c_int, C.c_int, _pd, _pd, _pd, _pd, _pu16,
                                        _pd, _pi32, _pd, C.c_int, _pd, _pf, _pd, _pd, _pd, C.c_int,
                                        _pd, _pi32, C.c_char_p, C.c_int]
+        L.ref_eval.restype = C.c_int
+        L.ref_eval.argtypes = [C.c_void_p, _pi32, _pd, C.c_int, C.c_int, _pd, _pf, _pd, _pd, _pd,
+                               _pd, _pu64, C.c_char_p, C.c_int]
         L.ref_backward.restype = C.c_int
         L.ref_backward.argtypes = [C.c_void_p, _pi32, _pd, _pd, _pd, _pd, C.c_int, _pf, _pf, _pf,
                                    _pd, C.c_int, C.c_int, _pd, _pd, _pd, _pd, _pd, _pd,
@@ -507,6 +521,27 @@ class RefLib:
             raise ValueError("raycast_depth: invalid scene")
         return out
 
+    def evaluate(self, m, cam, frames):
+        """The reference's semantic_metrics + photometric_metrics over its own render of `m`
+        at each frame's pose. Returns (summary[7], per_view_miou, per_view_psnr,
+        per_class (rows of 5))."""
+        h = self.map_create(m)
+        wh, intr = self._cam(cam)
+        poses, planes = _frames_blob(frames)
+        nf = len(frames)
+        summary = np.zeros(7)
+        pvm, pvp = np.zeros(max(nf, 1)), np.zeros(max(nf, 1))
+        pc = np.zeros((max(m.num_classes(), 1), 5))
+        npc = C.c_uint64(0)
+        err = C.create_string_buffer(512)
+        rc = self.lib.ref_eval(h, wh.ctypes.data_as(_pi32), _dp(intr), m.num_classes(), nf,
+                               _dp(poses), planes.ctypes.data_as(_pf), _dp(summary), _dp(pvm),
+                               _dp(pvp), _dp(pc), C.byref(npc), err, 512)
+        self.map_destroy(h)
+        if rc:
+            raise ValueError(err.value.decode())
+        return summary, pvm[:nf], pvp[:nf], pc[: npc.value]
+
     def optimize_map(self, m, frames, cam, cfg, iters):
         """The reference's optimize_map (mapper.cpp:241-283) from a zero AdamState.
         Returns (history (n_done, 7), arrays dict of the final map, error or None)."""
@@ -518,12 +553,7 @@ class RefLib:
                "sem_indices": np.ascontiguousarray(m.sem_indices, dtype=np.uint16).reshape(-1).copy(),
                "sem_probs": np.ascontiguousarray(m.sem_probs, dtype=np.float64).reshape(-1).copy()}
         wh, intr = self._cam(cam)
-        poses = np.concatenate([np.concatenate([np.asarray(f.pose.R, np.float64).reshape(9),
-                                                np.asarray(f.pose.t, np.float64)]) for f in frames])
-        planes = np.concatenate([np.concatenate([np.asarray(f.rgb, np.float32).reshape(-1),
-                                                 np.asarray(f.depth, np.float32).reshape(-1),
-                                                 np.asarray(f.sem, np.float32).reshape(-1)])
-                                 for f in frames]).astype(np.float32)
+        poses, planes = _frames_blob(frames)
         a = cfg.adam
         adam = np.array([a.lr_center, a.lr_radius, a.lr_opacity, a.lr_color, a.lr_sem, a.beta1,
                          a.beta2, a.eps, a.eps_sem])

@@ -546,3 +546,67 @@ int64_t ref_optimize_map(uint64_t n, int k, int num_classes, double* centers, do
 }
 
 }  // extern "C"
+
+// ---- semantic_metrics + photometric_metrics (proj/src/evaluator.cpp:93-297) over the
+// reference's own render(map, camera, pose, RenderChannels::all()) of each frame ----
+#include "splatmap/evaluator.hpp"
+
+extern "C" {
+
+// frames as ref_optimize_map (poses12, planes). summary = {miou, top1, top3, map, f1, psnr,
+// depth_l1}; per_class rows {class_id, iou, ap, f1, gt_pixels} (capacity num_classes).
+int ref_eval(void* m, const int32_t wh[2], const double intr[4], int num_classes, int n_frames,
+             const double* poses12, const float* planes, double summary[7], double* per_view_miou,
+             double* per_view_psnr, double* per_class, uint64_t* n_per_class, char* err,
+             int err_cap) {
+    try {
+        const GaussianMap& map = static_cast<RefMap*>(m)->map;
+        CameraModel cam = make_cam(wh, intr);
+        const size_t px = static_cast<size_t>(wh[0]) * wh[1];
+        const size_t C = static_cast<size_t>(num_classes) + 1;
+        std::vector<Frame> fr(static_cast<size_t>(n_frames));
+        std::vector<RenderOutput> rs;
+        for (int f = 0; f < n_frames; ++f) {
+            Frame& F = fr[f];
+            F.width = wh[0];
+            F.height = wh[1];
+            F.num_classes = num_classes;
+            F.pose = make_pose(poses12 + 12 * f, poses12 + 12 * f + 9);
+            const float* base = planes + static_cast<size_t>(f) * px * (4 + C);
+            F.rgb.assign(base, base + 3 * px);
+            F.depth.assign(base + 3 * px, base + 4 * px);
+            F.sem.assign(base + 4 * px, base + 4 * px + C * px);
+            rs.push_back(render(map, cam, F.pose, RenderChannels::all()));
+        }
+        MetricReport sem = semantic_metrics(rs, fr);
+        MetricReport pho = photometric_metrics(rs, fr);
+        summary[0] = sem.miou_pct;
+        summary[1] = sem.top1_pct;
+        summary[2] = sem.top3_pct;
+        summary[3] = sem.map_pct;
+        summary[4] = sem.f1_pct;
+        summary[5] = pho.psnr_db;
+        summary[6] = pho.depth_l1_cm;
+        for (size_t i = 0; i < sem.per_view_miou.size(); ++i) per_view_miou[i] = sem.per_view_miou[i];
+        for (size_t i = 0; i < pho.per_view_psnr.size(); ++i) per_view_psnr[i] = pho.per_view_psnr[i];
+        *n_per_class = sem.per_class.size();
+        for (size_t i = 0; i < sem.per_class.size(); ++i) {
+            const PerClassMetric& pc = sem.per_class[i];
+            double* r = per_class + 5 * i;
+            r[0] = pc.class_id;
+            r[1] = pc.iou_pct;
+            r[2] = pc.ap_pct;
+            r[3] = pc.f1_pct;
+            r[4] = static_cast<double>(pc.gt_pixels);
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        if (err && err_cap > 0) {
+            std::strncpy(err, e.what(), static_cast<size_t>(err_cap) - 1);
+            err[err_cap - 1] = 0;
+        }
+        return 1;
+    }
+}
+
+}  // extern "C"

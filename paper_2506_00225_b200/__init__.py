@@ -54,3 +54,11 @@ from .mapper import (  # noqa: F401,E402
     MapTrainer,
     optimize_map,
 )
+from .evaluate import (  # noqa: F401,E402
+    Evaluator,
+    MetricReport,
+    PerClassMetric,
+    evaluate,
+    photometric_metrics,
+    semantic_metrics,
+)

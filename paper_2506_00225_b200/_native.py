@@ -88,6 +88,11 @@ _pi32 = C.POINTER(C.c_int32)
 _pu8 = C.POINTER(C.c_uint8)
 
 SIGNATURES = {
+    "sgm_eval_create": (C.c_int, [_vp, C.c_int32, C.POINTER(_vp)]),
+    "sgm_eval_destroy": (None, [_vp, _vp]),
+    "sgm_eval_add_view": (C.c_int, [_vp, _vp, _vp, C.POINTER(sgm_camera), C.POINTER(sgm_options),
+                                    _vp]),
+    "sgm_eval_report": (C.c_int, [_vp, _vp, _pd, _pd, _pd, _pd, _pu64]),
     "sgm_frame_upload": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.POINTER(sgm_pose),
                                    _pf, _pf, _pf, C.POINTER(_vp)]),
     "sgm_frame_release": (None, [_vp, _vp]),

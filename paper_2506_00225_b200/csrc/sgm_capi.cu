@@ -818,6 +818,165 @@ void trainer_prune(sgm_ctx* ctx, sgm_trainer* tr, double thr) {
 
 }  // namespace
 
+struct sgm_evaluator {
+    int num_classes = 0, C = 0;
+    struct View {
+        std::vector<unsigned long long> confusion;  // [C][C]
+        unsigned long long top1 = 0, top3 = 0, total = 0;
+        double mse_sum = 0, dep_sum = 0, dep_cnt = 0;
+        int px = 0;
+        uint32_t T = 0;      // valid (known-label) pixels
+        DevBuf scores;       // [M][T] float
+        DevBuf labels;       // [T] u16
+    };
+    std::vector<View> views;
+    DevBuf conf, counters, valid, label_px, idx, sel_count, sel_tmp, photo_part, photo_out;
+};
+
+namespace {
+
+void eval_add_view(sgm_ctx* ctx, sgm_evaluator* ev, const sgm_map* map, const CamParams& cam,
+                   const OptParams& o, const sgm_frame* fr) {
+    cudaStream_t s = ctx->stream;
+    const int C = ev->C;
+    const size_t px = static_cast<size_t>(cam.W) * cam.H;
+    if (px >= (1ull << 31)) fail(SGM_ERR_UNSUPPORTED, "evaluator: more than 2^31-1 pixels");
+    // render(map, camera, pose, RenderChannels::all()) into HBM
+    CK(ctx->planes.reserve(8 * px * (5 + C)));
+    double* d_sil = ctx->planes.as<double>();
+    double* d_color = d_sil + px;
+    double* d_depth = d_color + 3 * px;
+    double* d_sem = d_depth + px;
+    RenderTargets rt;
+    rt.channels = SGM_COLOR | SGM_DEPTH | SGM_SEMANTICS;
+    rt.color = d_color;
+    rt.depth = d_depth;
+    rt.sil = d_sil;
+    rt.sem = d_sem;
+    run_views(ctx, map, cam, o, 1, &fr->pose, Mode::Render, rt, nullptr, nullptr);
+    const float* f_rgb = fr->planes.as<float>();
+    const float* f_depth = f_rgb + 3 * px;
+    const float* f_sem = f_depth + px;
+    CK(ev->conf.reserve(8ull * C * C));
+    CK(ev->counters.reserve(64));
+    CK(ev->valid.reserve(px));
+    CK(ev->label_px.reserve(2 * px));
+    CK(ev->idx.reserve(4 * px));
+    CK(ev->sel_count.reserve(8));
+    const int nb = eval_photo_blocks(static_cast<int>(px));
+    CK(ev->photo_part.reserve(24ull * nb + 24));
+    CK(ev->photo_out.reserve(24));
+    auto* conf = ev->conf.as<unsigned long long>();
+    auto* cnt = ev->counters.as<unsigned long long>();
+    CK(cudaMemsetAsync(conf, 0, 8ull * C * C, s));
+    CK(cudaMemsetAsync(cnt, 0, 24, s));
+    launch_eval_pixels(d_sem, f_sem, static_cast<int>(px), C, conf, cnt, ev->valid.as<uint8_t>(),
+                       ev->label_px.as<uint16_t>(), s);
+    size_t tmp = 0;
+    cub::CountingInputIterator<uint32_t> ids(0);
+    CK(cub::DeviceSelect::Flagged(nullptr, tmp, ids, ev->valid.as<uint8_t>(), ev->idx.as<uint32_t>(),
+                                  ev->sel_count.as<uint32_t>(), static_cast<int>(px), s));
+    CK(ev->sel_tmp.reserve(tmp));
+    CK(cub::DeviceSelect::Flagged(ev->sel_tmp.p, tmp, ids, ev->valid.as<uint8_t>(), ev->idx.as<uint32_t>(),
+                                  ev->sel_count.as<uint32_t>(), static_cast<int>(px), s));
+    launch_eval_photo(d_color, d_depth, f_rgb, f_depth, static_cast<int>(px), ev->photo_part.as<double>(),
+                      ev->photo_out.as<double>(), s);
+    ctx->stats.kernel_launches += 5;
+    sgm_evaluator::View v;
+    v.px = static_cast<int>(px);
+    v.confusion.resize(static_cast<size_t>(C) * C);
+    unsigned long long hc[3];
+    double hp[3];
+    CK(cudaMemcpyAsync(v.confusion.data(), conf, 8ull * C * C, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hc, cnt, 24, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hp, ev->photo_out.p, 24, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&v.T, ev->sel_count.p, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    v.top1 = hc[0];
+    v.top3 = hc[1];
+    v.total = hc[2];
+    v.mse_sum = hp[0];
+    v.dep_sum = hp[1];
+    v.dep_cnt = hp[2];
+    const int M = C - 1;
+    CK(v.scores.reserve(4ull * std::max<uint32_t>(v.T, 1) * std::max(M, 1)));
+    CK(v.labels.reserve(2ull * std::max<uint32_t>(v.T, 1)));
+    launch_eval_scores(d_sem, d_sil, ev->idx.as<uint32_t>(), ev->label_px.as<uint16_t>(), v.T, C,
+                       v.scores.as<float>(), v.labels.as<uint16_t>(), s);
+    ctx->stats.kernel_launches += 1;
+    CK(cudaStreamSynchronize(s));
+    ev->views.push_back(std::move(v));
+}
+
+// AP per class (evaluator.cpp:151-188) over all views' valid pixels, in (view, pixel) order.
+// Returns -1 for classes without positives.
+std::vector<double> eval_ap(sgm_ctx* ctx, sgm_evaluator* ev, const std::vector<uint64_t>& positives) {
+    cudaStream_t s = ctx->stream;
+    const int M = ev->C - 1;
+    uint64_t T = 0;
+    for (auto& v : ev->views) T += v.T;
+    std::vector<double> ap(static_cast<size_t>(std::max(M, 0)), -1.0);
+    if (T == 0 || M <= 0) return ap;
+    if (T >= (1ull << 31)) fail(SGM_ERR_UNSUPPORTED, "evaluator: more than 2^31-1 labelled pixels");
+    DevBuf sc, lab, keys, keys_alt, pos, pos_alt, tp, terms, sum, tmpb;
+    CK(sc.reserve(4 * T));
+    CK(lab.reserve(2 * T));
+    CK(keys.reserve(4 * T));
+    CK(keys_alt.reserve(4 * T));
+    CK(pos.reserve(4 * T));
+    CK(pos_alt.reserve(4 * T));
+    CK(tp.reserve(4 * T));
+    CK(terms.reserve(8 * T));
+    CK(sum.reserve(8 * static_cast<size_t>(M)));
+    uint64_t off = 0;
+    for (auto& v : ev->views) {
+        if (v.T) CK(cudaMemcpyAsync(lab.as<uint16_t>() + off, v.labels.p, 2ull * v.T, cudaMemcpyDeviceToDevice, s));
+        off += v.T;
+    }
+    const int n = static_cast<int>(T);
+    size_t need = 0, t1 = 0, t2 = 0, t3 = 0;
+    {
+        cub::DoubleBuffer<uint32_t> dk(keys.as<uint32_t>(), keys_alt.as<uint32_t>());
+        cub::DoubleBuffer<uint32_t> dv(pos.as<uint32_t>(), pos_alt.as<uint32_t>());
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, t1, dk, dv, n, 0, 32, s));
+        CK(cub::DeviceScan::InclusiveSum(nullptr, t2, pos.as<uint32_t>(), tp.as<uint32_t>(), n, s));
+        CK(cub::DeviceReduce::Sum(nullptr, t3, terms.as<double>(), sum.as<double>(), n, s));
+        need = std::max(t1, std::max(t2, t3));
+    }
+    CK(tmpb.reserve(need));
+    for (int c = 0; c < M; ++c) {
+        if (positives[static_cast<size_t>(c)] == 0) continue;  // :166
+        off = 0;
+        for (auto& v : ev->views) {
+            if (v.T)
+                CK(cudaMemcpyAsync(sc.as<float>() + off, v.scores.as<float>() + static_cast<size_t>(c) * v.T,
+                                   4ull * v.T, cudaMemcpyDeviceToDevice, s));
+            off += v.T;
+        }
+        launch_eval_keys(sc.as<float>(), lab.as<uint16_t>(), static_cast<uint32_t>(T), c, keys.as<uint32_t>(),
+                         pos.as<uint32_t>(), s);
+        cub::DoubleBuffer<uint32_t> dk(keys.as<uint32_t>(), keys_alt.as<uint32_t>());
+        cub::DoubleBuffer<uint32_t> dv(pos.as<uint32_t>(), pos_alt.as<uint32_t>());
+        size_t t = need;
+        CK(cub::DeviceRadixSort::SortPairs(tmpb.p, t, dk, dv, n, 0, 32, s));  // stable
+        t = need;
+        CK(cub::DeviceScan::InclusiveSum(tmpb.p, t, dv.Current(), tp.as<uint32_t>(), n, s));
+        launch_eval_ap_terms(dv.Current(), tp.as<uint32_t>(), static_cast<uint32_t>(T),
+                             static_cast<double>(positives[static_cast<size_t>(c)]), terms.as<double>(), s);
+        t = need;
+        CK(cub::DeviceReduce::Sum(tmpb.p, t, terms.as<double>(), sum.as<double>() + c, n, s));
+        ctx->stats.kernel_launches += 5;
+    }
+    std::vector<double> h(static_cast<size_t>(M));
+    CK(cudaMemcpyAsync(h.data(), sum.p, 8ull * M, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int c = 0; c < M; ++c)
+        if (positives[static_cast<size_t>(c)]) ap[static_cast<size_t>(c)] = h[static_cast<size_t>(c)];
+    return ap;
+}
+
+}  // namespace
+
 struct sgm_emap {
     EmapParams p{};
     DevBuf grid, first_free, first_hit, log, keys, keys_alt, ids, ids_alt, fresh, counters, depth,
@@ -1792,6 +1951,181 @@ int sgm_optimize_map(sgm_ctx* ctx, sgm_trainer* tr, const sgm_camera* camera, ui
             if (n_done) *n_done = it + 1;
         }
         CK(cudaStreamSynchronize(s));
+    });
+}
+
+
+// ---------------------------------------------------------------- evaluation (f3)
+
+int sgm_eval_create(sgm_ctx* ctx, int32_t num_classes, sgm_evaluator** out) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!out) fail(SGM_ERR_INVALID, "out is null");
+        *out = nullptr;
+        if (num_classes < 0 || num_classes > 65534) fail(SGM_ERR_INVALID, "evaluator: bad class count");
+        auto ev = std::make_unique<sgm_evaluator>();
+        ev->num_classes = num_classes;
+        ev->C = num_classes + 1;
+        *out = ev.release();
+    });
+}
+
+void sgm_eval_destroy(sgm_ctx* ctx, sgm_evaluator* ev) {
+    if (!ev) return;
+    if (ctx) {
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+    }
+    delete ev;
+}
+
+int sgm_eval_add_view(sgm_ctx* ctx, sgm_evaluator* ev, const sgm_map* map, const sgm_camera* camera,
+                      const sgm_options* opt, const sgm_frame* frame) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!ev || !map || !frame) fail(SGM_ERR_INVALID, "evaluator: null argument");
+        const CamParams cam = to_cam(camera);
+        const OptParams o = to_opt(opt, cam);
+        if (frame->W != cam.W || frame->H != cam.H || frame->C != ev->C || map->dev.C != ev->C)
+            fail(SGM_ERR_INVALID, "semantic_metrics: resolution mismatch");  // evaluator.cpp:107-108
+        eval_add_view(ctx, ev, map, cam, o, frame);
+    });
+}
+
+int sgm_eval_report(sgm_ctx* ctx, sgm_evaluator* ev, double summary[7], double* per_view_miou,
+                    double* per_view_psnr, double* per_class, uint64_t* n_per_class) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!ev) fail(SGM_ERR_INVALID, "evaluator is null");
+        if (ev->views.empty()) fail(SGM_ERR_INVALID, "semantic_metrics: view count mismatch");  // :95-96
+        const int C = ev->C, M = C - 1;
+        const size_t CC = static_cast<size_t>(C) * C;
+        std::vector<unsigned long long> pooled(CC, 0);
+        unsigned long long top1 = 0, top3 = 0, total = 0;
+        std::vector<double> view_miou;
+        for (const auto& v : ev->views) {  // :100-148
+            top1 += v.top1;
+            top3 += v.top3;
+            total += v.total;
+            for (size_t i = 0; i < CC; ++i) pooled[i] += v.confusion[i];
+            double iou_sum = 0;
+            int iou_classes = 0;
+            for (int c = 0; c < C; ++c) {
+                int64_t rowsum = 0;
+                for (int m = 0; m < C; ++m) rowsum += static_cast<int64_t>(v.confusion[static_cast<size_t>(c) * C + m]);
+                if (rowsum == 0) continue;  // !present[c]
+                const int64_t tp = static_cast<int64_t>(v.confusion[static_cast<size_t>(c) * C + c]);
+                int64_t fn = 0, fp = 0;
+                for (int m = 0; m < C; ++m)
+                    if (m != c) {
+                        fn += static_cast<int64_t>(v.confusion[static_cast<size_t>(c) * C + m]);
+                        fp += static_cast<int64_t>(v.confusion[static_cast<size_t>(m) * C + c]);
+                    }
+                const int64_t uni = tp + fn + fp;
+                if (uni > 0) {
+                    iou_sum += static_cast<double>(tp) / uni;
+                    ++iou_classes;
+                }
+            }
+            view_miou.push_back(iou_classes ? 100.0 * iou_sum / iou_classes : 0.0);
+        }
+        double miou = 0.0;  // std::accumulate in order, then / size
+        for (double x : view_miou) miou += x;
+        miou /= static_cast<double>(view_miou.size());
+        const double top1_pct = total ? 100.0 * top1 / total : 0.0;
+        const double top3_pct = total ? 100.0 * top3 / total : 0.0;
+        // AP (:151-196): positives of class c = its ground-truth pixel count
+        std::vector<uint64_t> positives(static_cast<size_t>(std::max(M, 0)), 0);
+        for (int c = 0; c < M; ++c)
+            for (int m = 0; m < C; ++m) positives[static_cast<size_t>(c)] += pooled[static_cast<size_t>(c) * C + m];
+        const std::vector<double> ap = eval_ap(ctx, ev, positives);
+        struct PC {
+            int id;
+            double iou = 0, ap = 0, f1 = 0;
+            uint64_t gt = 0;
+        };
+        std::vector<PC> pcs;
+        double ap_sum = 0;
+        int ap_classes = 0;
+        for (int c = 0; c < M; ++c) {
+            if (ap[static_cast<size_t>(c)] < 0) continue;
+            ap_sum += ap[static_cast<size_t>(c)];
+            ++ap_classes;
+            PC pc;
+            pc.id = c;
+            pc.ap = 100.0 * ap[static_cast<size_t>(c)];
+            pc.gt = positives[static_cast<size_t>(c)];
+            pcs.push_back(pc);
+        }
+        const double map_pct = ap_classes ? 100.0 * ap_sum / ap_classes : 0.0;
+        double f1_sum = 0;  // macro F1 (:199-232)
+        int f1_classes = 0;
+        for (int c = 0; c < M; ++c) {
+            const int64_t tp = static_cast<int64_t>(pooled[static_cast<size_t>(c) * C + c]);
+            int64_t fn = 0, fp = 0;
+            for (int m = 0; m < C; ++m)
+                if (m != c) {
+                    fn += static_cast<int64_t>(pooled[static_cast<size_t>(c) * C + m]);
+                    fp += static_cast<int64_t>(pooled[static_cast<size_t>(m) * C + c]);
+                }
+            if (tp + fn + fp == 0) continue;
+            const double f1 = tp > 0 ? 2.0 * tp / (2.0 * tp + fp + fn) : 0.0;
+            f1_sum += f1;
+            ++f1_classes;
+            const double iou = tp + fn + fp > 0 ? static_cast<double>(tp) / (tp + fn + fp) : 0.0;
+            bool found = false;
+            for (auto& pc : pcs)
+                if (pc.id == c) {
+                    pc.f1 = 100.0 * f1;
+                    pc.iou = 100.0 * iou;
+                    found = true;
+                }
+            if (!found) {
+                PC pc;
+                pc.id = c;
+                pc.f1 = 100.0 * f1;
+                pc.iou = 100.0 * iou;
+                pcs.push_back(pc);
+            }
+        }
+        const double f1_pct = f1_classes ? 100.0 * f1_sum / f1_classes : 0.0;
+        std::sort(pcs.begin(), pcs.end(), [](const PC& a, const PC& b) { return a.id < b.id; });
+        // photometric (:274-297)
+        std::vector<double> psnr;
+        double dep_sum = 0, dep_cnt = 0;
+        for (const auto& v : ev->views) {
+            double mse = v.mse_sum / static_cast<double>(3ull * v.px);  // mapper.cpp:97-107
+            psnr.push_back(mse <= 0.0 ? 100.0 : std::min(100.0, 10.0 * std::log10(1.0 / mse)));
+            dep_sum += v.dep_sum;
+            dep_cnt += v.dep_cnt;
+        }
+        double psnr_db = 0.0;
+        for (double x : psnr) psnr_db += x;
+        psnr_db /= static_cast<double>(psnr.size());
+        const double depth_l1 = dep_cnt > 0 ? 100.0 * dep_sum / dep_cnt : 0.0;
+        if (summary) {
+            summary[0] = miou;
+            summary[1] = top1_pct;
+            summary[2] = top3_pct;
+            summary[3] = map_pct;
+            summary[4] = f1_pct;
+            summary[5] = psnr_db;
+            summary[6] = depth_l1;
+        }
+        for (size_t i = 0; i < ev->views.size(); ++i) {
+            if (per_view_miou) per_view_miou[i] = view_miou[i];
+            if (per_view_psnr) per_view_psnr[i] = psnr[i];
+        }
+        if (per_class)
+            for (size_t i = 0; i < pcs.size(); ++i) {
+                double* r = per_class + 5 * i;
+                r[0] = pcs[i].id;
+                r[1] = pcs[i].iou;
+                r[2] = pcs[i].ap;
+                r[3] = pcs[i].f1;
+                r[4] = static_cast<double>(pcs[i].gt);
+            }
+        if (n_per_class) *n_per_class = pcs.size();
     });
 }
 

@@ -226,6 +226,21 @@ void launch_gather_f64(const double* src, double* dst, const uint32_t* kept, uin
 void launch_gather_u16(const uint16_t* src, uint16_t* dst, const uint32_t* kept, uint64_t m,
                        int stride, cudaStream_t s);
 
+// sgm_eval.cu (semantic_metrics / photometric_metrics on device planes)
+void launch_eval_pixels(const double* sem, const float* fsem, int px, int C,
+                        unsigned long long* confusion, unsigned long long* counters, uint8_t* valid,
+                        uint16_t* label, cudaStream_t s);
+void launch_eval_scores(const double* sem, const double* sil, const uint32_t* idx,
+                        const uint16_t* label, uint32_t T, int C, float* scores, uint16_t* lab_out,
+                        cudaStream_t s);
+int eval_photo_blocks(int px);
+void launch_eval_photo(const double* color, const double* depth, const float* rgb,
+                       const float* gdepth, int px, double* part, double* out, cudaStream_t s);
+void launch_eval_keys(const float* scores, const uint16_t* label, uint32_t T, int c, uint32_t* keys,
+                      uint32_t* pos, cudaStream_t s);
+void launch_eval_ap_terms(const uint32_t* pos, const uint32_t* tp, uint32_t T, double P,
+                          double* terms, cudaStream_t s);
+
 // sgm_raster.cu
 GroupParams choose_groups(int C, int k);
 size_t raster_smem_bytes(const DevMap& m, const GroupParams& gp, bool render);

@@ -18,7 +18,8 @@ from paper_2506_00225_b200.splatmap import CameraModel, Pose, RenderOptions, loo
 
 def test_reference_hot_path_tests_pass(ref):
     import oracle
-    for t in ("test_splat_render", "test_explorer", "test_gaussian_map", "test_losses"):
+    for t in ("test_splat_render", "test_explorer", "test_gaussian_map", "test_losses",
+              "test_evaluator"):
         exe = oracle.HERE / "_ref" / t
         if not exe.exists():
             pytest.skip(f"{exe} not built")
