@@ -319,7 +319,6 @@ __global__ void __launch_bounds__(kBThreads, 2) k_backward(RasterParams p, Backw
         const PackedSplat* sp = reinterpret_cast<const PackedSplat*>(sb);
         const double* scol = reinterpret_cast<const double*>(sb + L.st_color);
         const uint16_t* si = reinterpret_cast<const uint16_t*>(sb + L.st_idx);
-        const double* spr = reinterpret_cast<const double*>(sb + L.st_prob);
         const uint32_t* em = emap + (bb & 1) * kBNB;
         const int n = min(kBNB, static_cast<int>(Ln) - bb * kBNB);
 
@@ -445,7 +444,6 @@ __global__ void __launch_bounds__(kBThreads, 2) k_backward(RasterParams p, Backw
                     const uint16_t orig = b.sem_perm[static_cast<size_t>(m) * kpad + j];
                     atomicAdd(&b.gsem[static_cast<size_t>(m) * k + orig], sum);
                 }
-                (void)spr;
             }
         }
         const int mine = (t < kTilePx) ? (done ? 1 : 0) : 1;

@@ -10,6 +10,7 @@
 // Views whose pair lists do not fit the scratch budget together are split into
 // sub-batches; results do not depend on the split (per-view work is independent).
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 #include <cmath>
@@ -779,7 +780,7 @@ void trainer_prune(sgm_ctx* ctx, sgm_trainer* tr, double thr) {
     CK(tr->sel_count.reserve(8));
     launch_keep_flags(tr->P.as<double>() + 4 * n, n, thr, tr->keep.as<uint8_t>(), s);
     size_t tmp = 0;
-    cub::CountingInputIterator<uint32_t> ids(0);
+    thrust::counting_iterator<uint32_t> ids(0);
     CK(cub::DeviceSelect::Flagged(nullptr, tmp, ids, tr->keep.as<uint8_t>(), tr->kept.as<uint32_t>(),
                                   tr->sel_count.as<uint32_t>(), static_cast<int>(n), s));
     CK(tr->sel_tmp.reserve(tmp));
@@ -825,12 +826,12 @@ struct sgm_evaluator {
         unsigned long long top1 = 0, top3 = 0, total = 0;
         double mse_sum = 0, dep_sum = 0, dep_cnt = 0;
         int px = 0;
-        uint32_t T = 0;      // valid (known-label) pixels
+        uint32_t T = 0;      // pixels (unknown-labelled ones carry label 0xffff)
         DevBuf scores;       // [M][T] float
         DevBuf labels;       // [T] u16
     };
     std::vector<View> views;
-    DevBuf conf, counters, valid, label_px, idx, sel_count, sel_tmp, photo_part, photo_out;
+    DevBuf conf, counters, photo_part, photo_out;
 };
 
 namespace {
@@ -859,10 +860,6 @@ void eval_add_view(sgm_ctx* ctx, sgm_evaluator* ev, const sgm_map* map, const Ca
     const float* f_sem = f_depth + px;
     CK(ev->conf.reserve(8ull * C * C));
     CK(ev->counters.reserve(64));
-    CK(ev->valid.reserve(px));
-    CK(ev->label_px.reserve(2 * px));
-    CK(ev->idx.reserve(4 * px));
-    CK(ev->sel_count.reserve(8));
     const int nb = eval_photo_blocks(static_cast<int>(px));
     CK(ev->photo_part.reserve(24ull * nb + 24));
     CK(ev->photo_out.reserve(24));
@@ -870,27 +867,23 @@ void eval_add_view(sgm_ctx* ctx, sgm_evaluator* ev, const sgm_map* map, const Ca
     auto* cnt = ev->counters.as<unsigned long long>();
     CK(cudaMemsetAsync(conf, 0, 8ull * C * C, s));
     CK(cudaMemsetAsync(cnt, 0, 24, s));
-    launch_eval_pixels(d_sem, f_sem, static_cast<int>(px), C, conf, cnt, ev->valid.as<uint8_t>(),
-                       ev->label_px.as<uint16_t>(), s);
-    size_t tmp = 0;
-    cub::CountingInputIterator<uint32_t> ids(0);
-    CK(cub::DeviceSelect::Flagged(nullptr, tmp, ids, ev->valid.as<uint8_t>(), ev->idx.as<uint32_t>(),
-                                  ev->sel_count.as<uint32_t>(), static_cast<int>(px), s));
-    CK(ev->sel_tmp.reserve(tmp));
-    CK(cub::DeviceSelect::Flagged(ev->sel_tmp.p, tmp, ids, ev->valid.as<uint8_t>(), ev->idx.as<uint32_t>(),
-                                  ev->sel_count.as<uint32_t>(), static_cast<int>(px), s));
-    launch_eval_photo(d_color, d_depth, f_rgb, f_depth, static_cast<int>(px), ev->photo_part.as<double>(),
-                      ev->photo_out.as<double>(), s);
-    ctx->stats.kernel_launches += 5;
     sgm_evaluator::View v;
     v.px = static_cast<int>(px);
+    v.T = static_cast<uint32_t>(px);
+    const int M = C - 1;
+    CK(v.scores.reserve(4ull * px * std::max(M, 1)));
+    CK(v.labels.reserve(2ull * px));
+    launch_eval_view(d_sem, d_sil, f_sem, static_cast<int>(px), C, conf, cnt, v.labels.as<uint16_t>(),
+                     v.scores.as<float>(), s);
+    launch_eval_photo(d_color, d_depth, f_rgb, f_depth, static_cast<int>(px), ev->photo_part.as<double>(),
+                      ev->photo_out.as<double>(), s);
+    ctx->stats.kernel_launches += 3;
     v.confusion.resize(static_cast<size_t>(C) * C);
     unsigned long long hc[3];
     double hp[3];
     CK(cudaMemcpyAsync(v.confusion.data(), conf, 8ull * C * C, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hc, cnt, 24, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hp, ev->photo_out.p, 24, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&v.T, ev->sel_count.p, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     v.top1 = hc[0];
     v.top3 = hc[1];
@@ -898,17 +891,11 @@ void eval_add_view(sgm_ctx* ctx, sgm_evaluator* ev, const sgm_map* map, const Ca
     v.mse_sum = hp[0];
     v.dep_sum = hp[1];
     v.dep_cnt = hp[2];
-    const int M = C - 1;
-    CK(v.scores.reserve(4ull * std::max<uint32_t>(v.T, 1) * std::max(M, 1)));
-    CK(v.labels.reserve(2ull * std::max<uint32_t>(v.T, 1)));
-    launch_eval_scores(d_sem, d_sil, ev->idx.as<uint32_t>(), ev->label_px.as<uint16_t>(), v.T, C,
-                       v.scores.as<float>(), v.labels.as<uint16_t>(), s);
-    ctx->stats.kernel_launches += 1;
-    CK(cudaStreamSynchronize(s));
     ev->views.push_back(std::move(v));
 }
 
-// AP per class (evaluator.cpp:151-188) over all views' valid pixels, in (view, pixel) order.
+// AP per class (evaluator.cpp:151-188) over all views' pixels in (view, pixel) order; the
+// unknown-labelled ones sort after every valid score and are never positive.
 // Returns -1 for classes without positives.
 std::vector<double> eval_ap(sgm_ctx* ctx, sgm_evaluator* ev, const std::vector<uint64_t>& positives) {
     cudaStream_t s = ctx->stream;
@@ -917,7 +904,7 @@ std::vector<double> eval_ap(sgm_ctx* ctx, sgm_evaluator* ev, const std::vector<u
     for (auto& v : ev->views) T += v.T;
     std::vector<double> ap(static_cast<size_t>(std::max(M, 0)), -1.0);
     if (T == 0 || M <= 0) return ap;
-    if (T >= (1ull << 31)) fail(SGM_ERR_UNSUPPORTED, "evaluator: more than 2^31-1 labelled pixels");
+    if (T >= (1ull << 31)) fail(SGM_ERR_UNSUPPORTED, "evaluator: more than 2^31-1 pixels in total");
     DevBuf sc, lab, keys, keys_alt, pos, pos_alt, tp, terms, sum, tmpb;
     CK(sc.reserve(4 * T));
     CK(lab.reserve(2 * T));

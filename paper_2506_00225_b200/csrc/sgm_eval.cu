@@ -2,16 +2,18 @@
 // semantic_metrics (proj/src/evaluator.cpp:93-238) and photometric_metrics (:274-297)
 // without copying the px*(5+C) fp64 planes of each view to the host.
 //
-// Per view (k_eval_pixels, one thread per pixel):
+// Per view (k_eval_view, 32-pixel tiles staged in shared memory with coalesced loads):
 //   gt label = Frame::label_at (first max over the float simplex, frame.hpp:41-47);
 //   pixels labelled "unknown" are skipped (:111); pred = argmax_channel (first max);
 //   top-1 / top-3 (strictly-higher count with index tie-break, :120-123) counters and the
-//   C x C confusion matrix (a shared-memory histogram flushed with 64-bit atomics).
-// The valid pixels are compacted in pixel order; k_eval_scores writes the per-class AP
-// score float(q[c] / s) (0 when s <= 1e-9, :163-164) for every valid pixel, class-major.
+//   C x C confusion matrix (warp-aggregated 64-bit atomics); the per-class AP score
+//   float(q[c] / s) (0 when s <= 1e-9, :163-164) of every pixel, class-major, written as
+//   32 consecutive floats per class row.
 // At report time each class is stable-radix-sorted by descending score (ties keep the
-// (view, pixel) order of the reference's std::stable_sort, :168-169) and AP is the
-// sum over positives of (recall - prev_recall) * precision (:170-180).
+// (view, pixel) order of the reference's std::stable_sort, :168-169). Unknown-labelled
+// pixels get the largest key, so they sort after every valid score and leave the ranks of
+// the valid ones as in the reference's compacted list; AP is the sum over positives of
+// (recall - prev_recall) * precision (:170-180).
 // k_eval_photo: per-pixel squared colour error and valid-depth |error|, reduced in a
 // fixed order (deterministic).
 #include "sgm_internal.h"
@@ -21,71 +23,74 @@ namespace sgm {
 namespace {
 
 constexpr int kEvalThreads = 256;
+constexpr int kTileP = 32;  // pixels per k_eval_view block
 
-__global__ void __launch_bounds__(kEvalThreads) k_eval_pixels(
-    const double* __restrict__ sem, const float* __restrict__ fsem, int px, int C,
-    unsigned long long* __restrict__ confusion, unsigned long long* __restrict__ counters,
-    uint8_t* __restrict__ valid, uint16_t* __restrict__ label, int use_smem) {
-    extern __shared__ unsigned int hist[];  // [C][C], or none: global atomics (large C)
-    const bool local = use_smem != 0;
-    if (local)
-        for (int i = threadIdx.x; i < C * C; i += blockDim.x) hist[i] = 0;
+__global__ void __launch_bounds__(kEvalThreads) k_eval_view(
+    const double* __restrict__ sem, const double* __restrict__ sil, const float* __restrict__ fsem,
+    int px, int C, unsigned long long* __restrict__ confusion,
+    unsigned long long* __restrict__ counters, uint16_t* __restrict__ label,
+    float* __restrict__ scores) {
+    extern __shared__ __align__(16) unsigned char esm[];
+    double* q_s = reinterpret_cast<double*>(esm);            // [32][C]
+    float* f_s = reinterpret_cast<float*>(q_s + kTileP * C);  // [32][C]
+    __shared__ double s_sil[kTileP];
+    const int base = blockIdx.x * kTileP;
+    const int np = min(kTileP, px - base);
+    const size_t off = static_cast<size_t>(base) * C;
+    for (int i = threadIdx.x; i < np * C; i += blockDim.x) {
+        q_s[i] = sem[off + i];
+        f_s[i] = fsem[off + i];
+    }
+    if (threadIdx.x < np) s_sil[threadIdx.x] = sil[base + threadIdx.x];
     __syncthreads();
-    unsigned top1 = 0, top3 = 0, total = 0;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < px) {
-        const float* f = fsem + static_cast<size_t>(i) * C;
-        int gt = 0;
-        for (int m = 1; m < C; ++m)
-            if (f[m] > f[gt]) gt = m;
-        const bool ok = gt != C - 1;  // unknown_class() == num_classes
-        valid[i] = ok;
-        label[i] = static_cast<uint16_t>(gt);
+    if (threadIdx.x < 32) {
+        const int p = threadIdx.x;
+        bool ok = false;
+        int gt = 0, pred = 0, higher = 0;
+        if (p < np) {
+            const float* f = f_s + p * C;
+            for (int m = 1; m < C; ++m)  // Frame::label_at (frame.hpp:41-47)
+                if (f[m] > f[gt]) gt = m;
+            ok = gt != C - 1;  // unknown_class()
+            if (ok) {
+                const double* q = q_s + p * C;
+                for (int m = 1; m < C; ++m)  // argmax_channel (evaluator.cpp:18-23)
+                    if (q[m] > q[pred]) pred = m;
+                const double qg = q[gt];
+                for (int m = 0; m < C; ++m)  // :120-123
+                    if (q[m] > qg || (q[m] == qg && m < gt)) ++higher;
+            }
+            label[base + p] = ok ? static_cast<uint16_t>(gt) : static_cast<uint16_t>(0xffff);
+        }
+        // confusion: warp-aggregated over equal (gt, pred) cells
+        const unsigned act = __ballot_sync(0xffffffffu, ok);
         if (ok) {
-            const double* q = sem + static_cast<size_t>(i) * C;
-            int pred = 0;
-            for (int m = 1; m < C; ++m)
-                if (q[m] > q[pred]) pred = m;
-            if (local) atomicAdd(&hist[gt * C + pred], 1u);
-            else atomicAdd(&confusion[gt * C + pred], 1ull);
-            ++total;
-            top1 += pred == gt;
-            const double qg = q[gt];
-            int higher = 0;
-            for (int m = 0; m < C; ++m)
-                if (q[m] > qg || (q[m] == qg && m < gt)) ++higher;
-            top3 += higher < 3;
+            const int cell = gt * C + pred;
+            const unsigned same = __match_any_sync(act, cell);
+            if (p == __ffs(same) - 1)
+                atomicAdd(&confusion[cell], static_cast<unsigned long long>(__popc(same)));
+        }
+        unsigned top1 = ok && pred == gt, top3 = ok && higher < 3, tot = ok;
+        for (int o = 16; o; o >>= 1) {
+            top1 += __shfl_xor_sync(0xffffffffu, top1, o);
+            top3 += __shfl_xor_sync(0xffffffffu, top3, o);
+            tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        }
+        if (p == 0 && tot) {
+            atomicAdd(&counters[0], static_cast<unsigned long long>(top1));
+            atomicAdd(&counters[1], static_cast<unsigned long long>(top3));
+            atomicAdd(&counters[2], static_cast<unsigned long long>(tot));
         }
     }
-    for (int o = 16; o; o >>= 1) {
-        top1 += __shfl_xor_sync(0xffffffffu, top1, o);
-        top3 += __shfl_xor_sync(0xffffffffu, top3, o);
-        total += __shfl_xor_sync(0xffffffffu, total, o);
+    // AP scores float(q[c] / s) (0 when s <= 1e-9), evaluator.cpp:163-164
+    const int p = threadIdx.x & 31;
+    if (p < np) {
+        const double sv = s_sil[p];
+        const double* q = q_s + p * C;
+        for (int c = threadIdx.x >> 5; c < C - 1; c += kEvalThreads / 32)
+            scores[static_cast<size_t>(c) * px + base + p] =
+                sv > 1e-9 ? static_cast<float>(q[c] / sv) : 0.0f;
     }
-    if ((threadIdx.x & 31) == 0 && total) {
-        atomicAdd(&counters[0], static_cast<unsigned long long>(top1));
-        atomicAdd(&counters[1], static_cast<unsigned long long>(top3));
-        atomicAdd(&counters[2], static_cast<unsigned long long>(total));
-    }
-    __syncthreads();
-    if (local)
-        for (int j = threadIdx.x; j < C * C; j += blockDim.x)
-            if (hist[j]) atomicAdd(&confusion[j], static_cast<unsigned long long>(hist[j]));
-}
-
-// scores[c * T + j] for the view's valid pixels j (pixel index idx[j]); M = C - 1 classes
-__global__ void k_eval_scores(const double* __restrict__ sem, const double* __restrict__ sil,
-                              const uint32_t* __restrict__ idx, const uint16_t* __restrict__ label,
-                              uint32_t T, int C, float* __restrict__ scores,
-                              uint16_t* __restrict__ lab_out) {
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= T) return;
-    const uint32_t i = idx[j];
-    lab_out[j] = label[i];
-    const double s = sil[i];
-    const double* q = sem + static_cast<size_t>(i) * C;
-    for (int c = 0; c < C - 1; ++c)
-        scores[static_cast<size_t>(c) * T + j] = s > 1e-9 ? static_cast<float>(q[c] / s) : 0.0f;
 }
 
 // Per-block partial sums of (sum (colour - rgb)^2, sum |depth - gt| over gt > 0, count).
@@ -139,7 +144,7 @@ __global__ void k_eval_photo_sum(const double* __restrict__ part, int nb, double
     out[2] = c;
 }
 
-// Descending-order radix key of a non-negative float score (ties keep input order).
+// Descending-order radix key of a non-negative float score; unknown pixels last.
 __global__ void k_eval_keys(const float* __restrict__ s, const uint16_t* __restrict__ label,
                             uint32_t T, int c, uint32_t* __restrict__ keys,
                             uint32_t* __restrict__ pos) {
@@ -147,7 +152,7 @@ __global__ void k_eval_keys(const float* __restrict__ s, const uint16_t* __restr
     if (j >= T) return;
     uint32_t u = __float_as_uint(s[j]);
     u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);  // ascending-sortable
-    keys[j] = ~u;                                      // descending
+    keys[j] = label[j] == 0xffff ? 0xffffffffu : ~u;  // descending
     pos[j] = label[j] == c;
 }
 
@@ -170,29 +175,21 @@ inline unsigned nb(uint64_t n, unsigned t) { return static_cast<unsigned>((n + t
 
 }  // namespace
 
-size_t eval_pixels_smem(int C) { return 4ull * C * C; }
+size_t eval_view_smem(int C) { return static_cast<size_t>(kTileP) * C * 12; }
 
-void launch_eval_pixels(const double* sem, const float* fsem, int px, int C,
-                        unsigned long long* confusion, unsigned long long* counters, uint8_t* valid,
-                        uint16_t* label, cudaStream_t s) {
-    size_t smem = eval_pixels_smem(C);
-    const int use_smem = smem <= 200 * 1024 ? 1 : 0;
-    if (!use_smem) smem = 0;
+void launch_eval_view(const double* sem, const double* sil, const float* fsem, int px, int C,
+                      unsigned long long* confusion, unsigned long long* counters, uint16_t* label,
+                      float* scores, cudaStream_t s) {
+    const size_t smem = eval_view_smem(C);
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(k_eval_pixels, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_eval_view, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
         configured = smem;
     }
     if (px > 0)
-        k_eval_pixels<<<nb(px, kEvalThreads), kEvalThreads, smem, s>>>(
-            sem, fsem, px, C, confusion, counters, valid, label, use_smem);
-}
-
-void launch_eval_scores(const double* sem, const double* sil, const uint32_t* idx,
-                        const uint16_t* label, uint32_t T, int C, float* scores, uint16_t* lab_out,
-                        cudaStream_t s) {
-    if (T > 0) k_eval_scores<<<nb(T, 256), 256, 0, s>>>(sem, sil, idx, label, T, C, scores, lab_out);
+        k_eval_view<<<nb(px, kTileP), kEvalThreads, smem, s>>>(sem, sil, fsem, px, C, confusion,
+                                                               counters, label, scores);
 }
 
 int eval_photo_blocks(int px) { return static_cast<int>(nb(px, kEvalThreads)); }

@@ -227,12 +227,9 @@ void launch_gather_u16(const uint16_t* src, uint16_t* dst, const uint32_t* kept,
                        int stride, cudaStream_t s);
 
 // sgm_eval.cu (semantic_metrics / photometric_metrics on device planes)
-void launch_eval_pixels(const double* sem, const float* fsem, int px, int C,
-                        unsigned long long* confusion, unsigned long long* counters, uint8_t* valid,
-                        uint16_t* label, cudaStream_t s);
-void launch_eval_scores(const double* sem, const double* sil, const uint32_t* idx,
-                        const uint16_t* label, uint32_t T, int C, float* scores, uint16_t* lab_out,
-                        cudaStream_t s);
+void launch_eval_view(const double* sem, const double* sil, const float* fsem, int px, int C,
+                      unsigned long long* confusion, unsigned long long* counters, uint16_t* label,
+                      float* scores, cudaStream_t s);
 int eval_photo_blocks(int px);
 void launch_eval_photo(const double* color, const double* depth, const float* rgb,
                        const float* gdepth, int px, double* part, double* out, cudaStream_t s);
