@@ -273,6 +273,39 @@ def workload_config(cfg: int) -> dict:
             "gain": "reference Eq.6-8 (n_missing, clipped-entropy sum, combine_scores)"}
 
 
+def measure_aniso(ctx, stream, flush, args, cfg, cam, poses) -> dict:
+    """The same candidate views scored with anisotropic EWA footprints (no
+    reference counterpart): the config's drawn per-axis log-scales and quaternions."""
+    import torch
+
+    from paper_2506_00225_b200 import scenes
+    from paper_2506_00225_b200.splatmap import score_poses
+
+    gma = scenes.make_map(cfg, aniso=True)
+    for _ in range(max(1, args.warmup)):
+        score_poses(gma, cam, poses, ctx=ctx)
+    ctx.reset_stats()
+    ms = []
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        score_poses(gma, cam, poses, ctx=ctx)
+        ev1.record(stream)
+        ev1.synchronize()
+        ms.append(ev0.elapsed_time(ev1))
+    st = ctx.stats()
+    views = max(1, st["views"])
+    return {"views_per_s": len(poses) * args.steps / (float(np.sum(ms)) / 1e3),
+            "ms_per_step": float(np.mean(ms)),
+            "visible_per_view": st["visible"] / views, "pairs_per_view": st["pairs"] / views,
+            "contributors_per_view": st["contributors"] / views,
+            "footprint": "EWA: Sigma2D = J R_cw Sigma R_cw^T J^T, alpha exp(-q/2), q <= trunc^2; "
+                         "Sigma from the config's per-axis log-scales and quaternions"}
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -404,7 +437,12 @@ def main() -> None:
     # ---- secondary metric: semantic render ms/frame (device-resident and e2e) ----
     render_info = None
     mapping_info = None
+    aniso_info = None
     if rank == 0:
+        try:
+            aniso_info = measure_aniso(ctx, stream, flush, args, cfg, cam, poses)
+        except Exception as exc:  # reported, not fatal
+            aniso_info = {"error": repr(exc)}
         try:
             render_info = measure_render(ctx, stream, flush, args)
         except Exception as exc:  # reported, not fatal
@@ -512,6 +550,7 @@ def main() -> None:
             "with_fisher_gain": fisher,
             "render_ms_per_frame": render_info,
             "mapping_optimize": mapping_info,
+            "anisotropic_ewa": aniso_info,
         }
         print(json.dumps(line), flush=True)
     if dist_on:

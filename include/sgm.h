@@ -123,6 +123,19 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes,
                    const uint16_t* sem_indices, const double* sem_probs, sgm_map** out);
 void sgm_map_release(sgm_ctx* ctx, sgm_map* map);
 
+/* ---- anisotropic splat mode (NO reference counterpart, parity unpinned) ----
+ * Switches an uploaded map to per-Gaussian anisotropic footprints: log_scales 3N (per-axis
+ * log sigma), quats 4N ((w, x, y, z), normalised here). World covariance
+ * Sigma = R(q) diag(exp(ls))^2 R(q)^T; projection by EWA, Sigma2D = J R_cw Sigma R_cw^T J^T
+ * (J: pinhole Jacobian at the camera-space centre, its direction clamped to 1.3x the
+ * half field of view as in 3D Gaussian splatting); footprint alpha exp(-q / 2) with
+ * q = d^T Sigma2D^-1 d, cut at q > truncation_sigmas^2; tiles from the truncated
+ * axis-aligned extent. log_radii are then unused. Both NULL restores the isotropic
+ * (reference) footprint. render / score / render_entropy / eval accept such maps;
+ * the Fisher and backward entry points return SGM_ERR_UNSUPPORTED for them. */
+int sgm_map_set_anisotropic(sgm_ctx* ctx, sgm_map* map, const double* log_scales,
+                            const double* quats);
+
 /* ---- render (splat_render.hpp:78-80, render()) ----
  * Host output planes in the reference layout; NULL for channels not requested.
  * silhouette (px) is always written. color px*3, depth px, sem px*(num_classes+1).

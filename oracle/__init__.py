@@ -70,12 +70,15 @@ class orc_options(C.Structure):
 class orc_map(C.Structure):
     _fields_ = [("n", C.c_uint64), ("k", C.c_int32), ("num_classes", C.c_int32),
                 ("centers", _pd), ("log_radii", _pd), ("opacity_logits", _pd),
-                ("colors", _pd), ("sem_idx", _pu16), ("sem_probs", _pd)]
+                ("colors", _pd), ("sem_idx", _pu16), ("sem_probs", _pd),
+                ("log_scales", _pd), ("quats", _pd)]
 
 
 class orc_proj(C.Structure):
     _fields_ = [("mx", C.c_double), ("my", C.c_double), ("rad_px", C.c_double),
-                ("z", C.c_double), ("alpha", C.c_double), ("index", C.c_uint32)]
+                ("z", C.c_double), ("alpha", C.c_double), ("index", C.c_uint32),
+                ("rx", C.c_double), ("ry", C.c_double), ("qa", C.c_double), ("qb", C.c_double),
+                ("qc", C.c_double)]
 
 
 class orc_stats(C.Structure):
@@ -90,7 +93,8 @@ class orc_emap(C.Structure):
 
 
 PROJ_DTYPE = np.dtype([("mx", "<f8"), ("my", "<f8"), ("rad_px", "<f8"), ("z", "<f8"),
-                       ("alpha", "<f8"), ("index", "<u4"), ("pad", "<u4")])
+                       ("alpha", "<f8"), ("index", "<u4"), ("pad", "<u4"), ("rx", "<f8"),
+                       ("ry", "<f8"), ("qa", "<f8"), ("qb", "<f8"), ("qc", "<f8")])
 
 
 def _cam(cam) -> orc_camera:
@@ -128,11 +132,15 @@ class _MapArrays:
         self.colors = np.ascontiguousarray(m.colors, dtype=np.float64)
         self.idx = np.ascontiguousarray(m.sem_indices, dtype=np.uint16)
         self.probs = np.ascontiguousarray(m.sem_probs, dtype=np.float64)
+        # anisotropic mode: optional per-axis log-scales and quaternions
+        ls, qs = getattr(m, "log_scales", None), getattr(m, "quats", None)
+        self.log_scales = None if ls is None else np.ascontiguousarray(ls, dtype=np.float64)
+        self.quats = None if qs is None else np.ascontiguousarray(qs, dtype=np.float64)
 
     def c(self) -> orc_map:
         return orc_map(self.n, self.k, self.num_classes, _dp(self.centers), _dp(self.log_radii),
                        _dp(self.logits), _dp(self.colors), self.idx.ctypes.data_as(_pu16),
-                       _dp(self.probs))
+                       _dp(self.probs), _dp(self.log_scales), _dp(self.quats))
 
 
 class Oracle:

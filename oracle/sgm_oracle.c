@@ -42,9 +42,79 @@ static int proj_cmp(const void* pa, const void* pb) {
     return 0;
 }
 
+/* ---- anisotropic mode (f4, no reference): covariance and EWA projection ----
+ * Every expression is evaluated left to right with one rounding per operation
+ * (-ffp-contract=off); the CUDA product uses the same order, so projections and bins
+ * are bit-identical between the two. */
+void orc_cov3(const double ls[3], const double q4[4], double S[6]) {
+    const double nrm = sqrt(((q4[0] * q4[0] + q4[1] * q4[1]) + q4[2] * q4[2]) + q4[3] * q4[3]);
+    const double w = q4[0] / nrm, x = q4[1] / nrm, y = q4[2] / nrm, z = q4[3] / nrm;
+    double R[9];
+    R[0] = 1.0 - 2.0 * (y * y + z * z);
+    R[1] = 2.0 * (x * y - w * z);
+    R[2] = 2.0 * (x * z + w * y);
+    R[3] = 2.0 * (x * y + w * z);
+    R[4] = 1.0 - 2.0 * (x * x + z * z);
+    R[5] = 2.0 * (y * z - w * x);
+    R[6] = 2.0 * (x * z - w * y);
+    R[7] = 2.0 * (y * z + w * x);
+    R[8] = 1.0 - 2.0 * (x * x + y * y);
+    const double s0 = exp(ls[0]), s1 = exp(ls[1]), s2 = exp(ls[2]);
+    const double v0 = s0 * s0, v1 = s1 * s1, v2 = s2 * s2;
+    static const int I[6] = {0, 0, 0, 1, 1, 2}, J[6] = {0, 1, 2, 1, 2, 2};
+    for (int e = 0; e < 6; ++e) {
+        const double* a = R + 3 * I[e];
+        const double* b = R + 3 * J[e];
+        S[e] = ((a[0] * b[0]) * v0 + (a[1] * b[1]) * v1) + (a[2] * b[2]) * v2;
+    }
+}
+
+/* Sigma2D and the cull of one anisotropic Gaussian at camera-space (pcx, pcy, pcz). */
+static int ewa_project(const double S[6], const double* R, const orc_camera* cam,
+                       const orc_options* opt, double pcx, double pcy, double pcz, orc_proj* p) {
+    /* the Jacobian is taken at the view direction clamped to 1.3x the half field of view
+     * (as 3D Gaussian splatting does): the linearisation is meaningless for centres far
+     * outside the frustum, where the unclamped -f x / z^2 term explodes near z_near */
+    const double limx = 1.3 * ((0.5 * cam->width) / cam->fx);
+    const double limy = 1.3 * ((0.5 * cam->height) / cam->fy);
+    const double txz = clampd(pcx / pcz, -limx, limx), tyz = clampd(pcy / pcz, -limy, limy);
+    const double tx = txz * pcz, ty = tyz * pcz;
+    const double zz = pcz * pcz;
+    const double j00 = cam->fx / pcz, j02 = -(cam->fx * tx) / zz;
+    const double j11 = cam->fy / pcz, j12 = -(cam->fy * ty) / zz;
+    /* M = J R_cw; R_cw(i, k) = R[3 k + i] */
+    const double a0 = j00 * R[0] + j02 * R[2], a1 = j00 * R[3] + j02 * R[5],
+                 a2 = j00 * R[6] + j02 * R[8];
+    const double b0 = j11 * R[1] + j12 * R[2], b1 = j11 * R[4] + j12 * R[5],
+                 b2 = j11 * R[7] + j12 * R[8];
+    const double ta0 = (S[0] * a0 + S[1] * a1) + S[2] * a2;
+    const double ta1 = (S[1] * a0 + S[3] * a1) + S[4] * a2;
+    const double ta2 = (S[2] * a0 + S[4] * a1) + S[5] * a2;
+    const double tb0 = (S[0] * b0 + S[1] * b1) + S[2] * b2;
+    const double tb1 = (S[1] * b0 + S[3] * b1) + S[4] * b2;
+    const double tb2 = (S[2] * b0 + S[4] * b1) + S[5] * b2;
+    const double va = (a0 * ta0 + a1 * ta1) + a2 * ta2;
+    const double vb = (b0 * ta0 + b1 * ta1) + b2 * ta2;
+    const double vc = (b0 * tb0 + b1 * tb1) + b2 * tb2;
+    const double det = va * vc - vb * vb;
+    if (!(det > 0.0)) return 0;
+    p->rx = opt->truncation_sigmas * sqrt(va);
+    p->ry = opt->truncation_sigmas * sqrt(vc);
+    if (p->mx + p->rx < 0 || p->mx - p->rx > cam->width || p->my + p->ry < 0 ||
+        p->my - p->ry > cam->height)
+        return 0;
+    p->qa = vc / det;
+    p->qb = -vb / det;
+    p->qc = va / det;
+    const double hm = 0.5 * (va + vc), hd = 0.5 * (va - vc);
+    p->rad_px = sqrt(hm + sqrt(hd * hd + vb * vb));
+    return 1;
+}
+
 uint64_t orc_project(const orc_map* map, const orc_camera* cam, const orc_pose* pose,
                      const orc_options* opt, orc_proj* out) {
     const double* R = pose->R; /* R_cw(i,j) = R(j,i) (splat_render.cpp:19) */
+    const int aniso = map->log_scales && map->quats;
     uint64_t v = 0;
     for (uint64_t i = 0; i < map->n; ++i) {
         const double d0 = map->centers[3 * i] - pose->t[0];
@@ -56,13 +126,22 @@ uint64_t orc_project(const orc_map* map, const orc_camera* cam, const orc_pose* 
         const double pcz = R[2] * d0 + (R[5] * d1 + R[8] * d2);
         if (pcz <= opt->z_near) continue; /* :26 */
         orc_proj p;
+        memset(&p, 0, sizeof(p));
         p.z = pcz;
         p.mx = cam->fx * pcx / pcz + cam->cx; /* :29 */
         p.my = cam->fy * pcy / pcz + cam->cy; /* :30 */
-        p.rad_px = exp(map->log_radii[i]) * cam->fy / pcz; /* :31 */
         p.alpha = 1.0 / (1.0 + exp(-map->opacity_logits[i])); /* sigmoid, geometry.hpp:84 */
         p.index = (uint32_t)i;
+        if (aniso) {
+            double S[6];
+            orc_cov3(&map->log_scales[3 * i], &map->quats[4 * i], S);
+            if (!ewa_project(S, R, cam, opt, pcx, pcy, pcz, &p)) continue;
+            out[v++] = p;
+            continue;
+        }
+        p.rad_px = exp(map->log_radii[i]) * cam->fy / pcz; /* :31 */
         const double reach = opt->truncation_sigmas * p.rad_px; /* :34 */
+        p.rx = p.ry = reach;
         if (p.mx + reach < 0 || p.mx - reach > cam->width || p.my + reach < 0 ||
             p.my - reach > cam->height)
             continue; /* :35-37 */
@@ -81,16 +160,16 @@ static rect_t tile_rect(const orc_proj* p, const orc_camera* cam, const orc_opti
     const int ts = opt->tile_size;
     const int tiles_x = (cam->width + ts - 1) / ts;
     const int tiles_y = (cam->height + ts - 1) / ts;
-    const double reach = opt->truncation_sigmas * p->rad_px; /* :205 */
+    /* reach = truncation_sigmas * rad_px (:205); per axis in the anisotropic mode */
     rect_t r;
     int a;
-    a = to_int_x86((p->mx - reach) / ts);
+    a = to_int_x86((p->mx - p->rx) / ts);
     r.tx0 = a > 0 ? a : 0; /* :206 */
-    a = to_int_x86((p->mx + reach) / ts);
+    a = to_int_x86((p->mx + p->rx) / ts);
     r.tx1 = a < tiles_x - 1 ? a : tiles_x - 1; /* :207 */
-    a = to_int_x86((p->my - reach) / ts);
+    a = to_int_x86((p->my - p->ry) / ts);
     r.ty0 = a > 0 ? a : 0; /* :208 */
-    a = to_int_x86((p->my + reach) / ts);
+    a = to_int_x86((p->my + p->ry) / ts);
     r.ty1 = a < tiles_y - 1 ? a : tiles_y - 1; /* :209 */
     return r;
 }
@@ -124,7 +203,10 @@ uint64_t orc_bins(const orc_proj* proj, uint64_t v, const orc_camera* cam,
     memcpy(cursor, tile_offsets, ntiles * sizeof(uint32_t));
     for (uint64_t pi = 0; pi < v; ++pi) { /* depth order => each bin in depth order */
         rect_t r = tile_rect(&proj[pi], cam, opt);
-        const float cut = probe_cutoff(proj[pi].rad_px, opt->truncation_sigmas);
+        /* anisotropic entries (qa > 0) carry the Mahalanobis cut trunc^2 instead */
+        const float cut = proj[pi].qa > 0.0
+                              ? (float)(opt->truncation_sigmas * opt->truncation_sigmas)
+                              : probe_cutoff(proj[pi].rad_px, opt->truncation_sigmas);
         for (int ty = r.ty0; ty <= r.ty1; ++ty)
             for (int tx = r.tx0; tx <= r.tx1; ++tx) {
                 const uint32_t at = cursor[(uint64_t)ty * tiles_x + tx]++;
@@ -194,10 +276,40 @@ static double composite(const view_t* s, const orc_map* map, const orc_options* 
     const double px = x + 0.5, py = y + 0.5;
     const float pxf = (float)px, pyf = (float)py;
     const int k = map->k;
+    const int aniso = map->log_scales && map->quats;
+    const double cut_sq = opt->truncation_sigmas * opt->truncation_sigmas;
     double T = 1.0;
     uint64_t probes = 0, exact = 0, contrib = 0;
     for (uint32_t b = b0; b < b1; ++b) {
         ++probes;
+        if (aniso) { /* f4: no float probe; exact Mahalanobis test */
+            ++exact;
+            const uint32_t pid = s->ids[b];
+            const orc_proj* p = &s->proj[pid];
+            const double dx = px - p->mx;
+            const double dy = py - p->my;
+            const double q = (p->qa * (dx * dx) + (2.0 * p->qb) * (dx * dy)) + p->qc * (dy * dy);
+            if (q > cut_sq) continue;
+            ++contrib;
+            double f = p->alpha * exp(-0.5 * q);
+            if (f > K_MAX_FOOTPRINT) f = K_MAX_FOOTPRINT;
+            const double w = f * T;
+            if (channels & ORC_COLOR) {
+                const double* c = &map->colors[(uint64_t)p->index * 3];
+                acc_color[0] += clampd(c[0], 0.0, 1.0) * w;
+                acc_color[1] += clampd(c[1], 0.0, 1.0) * w;
+                acc_color[2] += clampd(c[2], 0.0, 1.0) * w;
+            }
+            if (channels & ORC_DEPTH) *acc_depth += p->z * w;
+            if (channels & ORC_SEM) {
+                const uint16_t* idx = &map->sem_idx[(uint64_t)p->index * k];
+                const double* pr = &map->sem_probs[(uint64_t)p->index * k];
+                for (int j = 0; j < k; ++j) sem_px[idx[j]] += pr[j] * w;
+            }
+            T *= (1.0 - f);
+            if (opt->early_exit && T < opt->transmittance_eps) break;
+            continue;
+        }
         const float fdx = pxf - s->probe3[3 * (uint64_t)b];
         const float fdy = pyf - s->probe3[3 * (uint64_t)b + 1];
         if (fdx * fdx + fdy * fdy > s->probe3[3 * (uint64_t)b + 2]) continue; /* :276-278 */
@@ -640,6 +752,7 @@ static int fisher_view(const orc_map* map, const orc_camera* cam, const orc_pose
 
 int orc_fisher_accumulate(const orc_map* map, const orc_camera* cam, uint64_t n_views,
                           const orc_pose* poses, const orc_options* opt, double* H) {
+    if (map->log_scales && map->quats) return -1; /* isotropic chain only */
     acc_ctx_t a = {H};
     for (uint64_t v = 0; v < n_views; ++v)
         if (fisher_view(map, cam, &poses[v], opt, sink_acc, &a)) return -1;
@@ -649,6 +762,7 @@ int orc_fisher_accumulate(const orc_map* map, const orc_camera* cam, uint64_t n_
 int orc_fisher_gain(const orc_map* map, const orc_camera* cam, uint64_t n_views,
                     const orc_pose* poses, const orc_options* opt, const double* H_prior,
                     double lambda, double* gain) {
+    if (map->log_scales && map->quats) return -1; /* isotropic chain only */
     for (uint64_t v = 0; v < n_views; ++v) {
         gain_ctx_t g = {H_prior, lambda, 0.0};
         if (fisher_view(map, cam, &poses[v], opt, sink_gain, &g)) return -1;

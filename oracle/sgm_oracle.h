@@ -44,12 +44,19 @@ typedef struct {
     const double *centers, *log_radii, *opacity_logits, *colors;
     const uint16_t* sem_idx;
     const double* sem_probs;
+    /* Anisotropic splat mode (NO reference counterpart, parity unpinned):
+     * when both are non-NULL, log_scales (3N, per-axis log sigma) and quats (4N, (w, x, y, z),
+     * normalised here) replace log_radii. See orc_cov3 / orc_project below. */
+    const double *log_scales, *quats;
 } orc_map; /* GaussianMap SoA, proj/include/splatmap/gaussian_map.hpp:105-113 */
 
 typedef struct {
     double mx, my, rad_px, z, alpha;
     uint32_t index;
-} orc_proj; /* SplatProjection, splat_render.hpp:32-39 */
+    /* binning reach (x, y) in pixels and, anisotropic mode only, the conic (inverse 2D
+     * covariance) qa, qb, qc. Isotropic: rx = ry = truncation_sigmas * rad_px (:205). */
+    double rx, ry, qa, qb, qc;
+} orc_proj; /* SplatProjection, splat_render.hpp:32-39 (+ mode fields) */
 
 typedef struct {
     uint64_t visible;      /* V: culled-in projections */
@@ -61,7 +68,17 @@ typedef struct {
 
 enum { ORC_COLOR = 1, ORC_DEPTH = 2, ORC_SEM = 4 };
 
-/* project_splats, proj/src/splat_render.cpp:15-47. Returns V; out holds >= map->n. */
+/* World covariance of one anisotropic Gaussian, Sigma = R(q) diag(exp(2 ls)) R(q)^T, as
+ * (xx, xy, xz, yy, yz, zz); evaluation order as documented in sgm_oracle.c. */
+void orc_cov3(const double log_scale[3], const double quat[4], double out6[6]);
+
+/* project_splats, proj/src/splat_render.cpp:15-47. Returns V; out holds >= map->n.
+ * Anisotropic mode (EWA, Zwicker et al. 2001 as used by 3D Gaussian splatting):
+ * Sigma2D = J R_cw Sigma R_cw^T J^T with J the pinhole Jacobian at the camera-space
+ * centre, its direction x/z, y/z clamped to 1.3 (W/2)/fx, 1.3 (H/2)/fy; culled when det(Sigma2D) <= 0 or the truncated axis-aligned extent
+ * (trunc sqrt(Sigma2D_xx), trunc sqrt(Sigma2D_yy)) misses the image (:34-37 analogue);
+ * rad_px = sqrt(largest eigenvalue) (informational). The footprint is
+ * alpha exp(-q / 2), q = d^T Sigma2D^-1 d, cut at q > trunc^2 (the isotropic d2 > 9 r^2). */
 uint64_t orc_project(const orc_map* map, const orc_camera* cam, const orc_pose* pose,
                      const orc_options* opt, orc_proj* out);
 

@@ -132,6 +132,7 @@ SIGNATURES = {
     "sgm_map_upload": (C.c_int, [_vp, C.c_uint64, C.c_int32, C.c_int32, _pd, _pd, _pd, _pd,
                                  _pu16, _pd, C.POINTER(_vp)]),
     "sgm_map_release": (None, [_vp, _vp]),
+    "sgm_map_set_anisotropic": (C.c_int, [_vp, _vp, _pd, _pd]),
     "sgm_render": (C.c_int, [_vp, _vp, C.POINTER(sgm_camera), C.POINTER(sgm_pose), C.c_uint32,
                              C.POINTER(sgm_options), _pd, _pd, _pd, _pd, _pu64]),
     "sgm_render_device": (C.c_int, [_vp, _vp, C.POINTER(sgm_camera), C.POINTER(sgm_pose),

@@ -130,6 +130,7 @@ struct sgm_map {
     DevBuf idx;    // [n][kpad] u16 (class-sorted)
     DevBuf prob;   // [n][kpad] f64
     DevBuf perm;   // [n][kpad] u16 original entry index
+    DevBuf cov;    // anisotropic mode: [6][n] world covariance (sgm_map_set_anisotropic)
 };
 
 struct sgm_ctx {
@@ -1250,8 +1251,70 @@ void sgm_map_release(sgm_ctx* ctx, sgm_map* map) {
         ctx->give(std::move(map->idx));
         ctx->give(std::move(map->prob));
         ctx->give(std::move(map->perm));
+        ctx->give(std::move(map->cov));
     }
     delete map;
+}
+
+int sgm_map_set_anisotropic(sgm_ctx* ctx, sgm_map* map, const double* log_scales,
+                            const double* quats) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!map) fail(SGM_ERR_INVALID, "map is null");
+        CK(cudaStreamSynchronize(ctx->stream));
+        CK(cudaStreamSynchronize(ctx->bin_stream));
+        if (ctx->last_map == map) ctx->last_valid = false;
+        DevMap& d = map->dev;
+        if (!log_scales && !quats) {  // back to the isotropic (reference) footprint
+            d.aniso = 0;
+            d.cov = nullptr;
+            return;
+        }
+        const uint64_t n = d.n;
+        if (n > 0 && (!log_scales || !quats)) fail(SGM_ERR_INVALID, "anisotropic: null array with n > 0");
+        const size_t ns = std::max<uint64_t>(n, 1);
+        CK(ctx->h_stage.reserve(8 * 6 * ns));
+        double* cov = ctx->h_stage.as<double>();
+        std::vector<int> bad(1, -1);
+        // Sigma = R(q) diag(exp(ls))^2 R(q)^T, left-to-right evaluation with one rounding
+        // per operation (-ffp-contract=off); oracle/sgm_oracle.c orc_cov3 states the same
+        // order, so both sides project identical covariances.
+        for (uint64_t i = 0; i < n; ++i) {
+            const double* q4 = quats + 4 * i;
+            const double nrm = std::sqrt(((q4[0] * q4[0] + q4[1] * q4[1]) + q4[2] * q4[2]) + q4[3] * q4[3]);
+            if (!(nrm > 0.0) || !std::isfinite(nrm)) {
+                bad[0] = static_cast<int>(i % 0x7fffffff);
+                break;
+            }
+            const double w = q4[0] / nrm, x = q4[1] / nrm, y = q4[2] / nrm, z = q4[3] / nrm;
+            double R[9];
+            R[0] = 1.0 - 2.0 * (y * y + z * z);
+            R[1] = 2.0 * (x * y - w * z);
+            R[2] = 2.0 * (x * z + w * y);
+            R[3] = 2.0 * (x * y + w * z);
+            R[4] = 1.0 - 2.0 * (x * x + z * z);
+            R[5] = 2.0 * (y * z - w * x);
+            R[6] = 2.0 * (x * z - w * y);
+            R[7] = 2.0 * (y * z + w * x);
+            R[8] = 1.0 - 2.0 * (x * x + y * y);
+            const double s0 = std::exp(log_scales[3 * i]), s1 = std::exp(log_scales[3 * i + 1]),
+                         s2 = std::exp(log_scales[3 * i + 2]);
+            const double v0 = s0 * s0, v1 = s1 * s1, v2 = s2 * s2;
+            static const int I[6] = {0, 0, 0, 1, 1, 2}, J[6] = {0, 1, 2, 1, 2, 2};
+            for (int e = 0; e < 6; ++e) {
+                const double* a = R + 3 * I[e];
+                const double* b = R + 3 * J[e];
+                cov[e * n + i] = ((a[0] * b[0]) * v0 + (a[1] * b[1]) * v1) + (a[2] * b[2]) * v2;
+            }
+        }
+        if (bad[0] >= 0) fail(SGM_ERR_INVALID, "anisotropic: zero or non-finite quaternion (gaussian %d)", bad[0]);
+        ctx->take(map->cov, 8 * 6 * ns);
+        CK(map->cov.reserve(8 * 6 * ns));
+        CK(cudaMemcpyAsync(map->cov.p, cov, 8 * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        d.cov = map->cov.as<double>();
+        d.aniso = 1;
+    });
 }
 
 int sgm_render_device(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam, const sgm_pose* pose,
@@ -1349,8 +1412,9 @@ int sgm_last_bins(sgm_ctx* ctx, uint32_t* tile_offsets, uint32_t* ids, float* pr
             CK(ctx->dbg.reserve(16 * P));
             uint32_t* d_ids = ctx->dbg.as<uint32_t>();
             float* d_probe = reinterpret_cast<float*>(ctx->dbg.as<char>() + 4 * P);
-            launch_bins_to_ids(ctx->tvals.as<uint32_t>(), P, ctx->packed.as<PackedSplat>(), d_ids,
-                               d_probe, ctx->stream);
+            launch_bins_to_ids(ctx->tvals.as<uint32_t>(), P, ctx->packed.as<PackedSplat>(),
+                               ctx->last_map->dev.aniso, ctx->last_opt.cut_sq, d_ids, d_probe,
+                               ctx->stream);
             if (ids) CK(cudaMemcpyAsync(ids, d_ids, 4 * P, cudaMemcpyDeviceToHost, ctx->stream));
             if (probe3) CK(cudaMemcpyAsync(probe3, d_probe, 12 * P, cudaMemcpyDeviceToHost, ctx->stream));
             CK(cudaStreamSynchronize(ctx->stream));
@@ -1422,6 +1486,8 @@ int sgm_fisher_prior(sgm_ctx* ctx, sgm_map* map, const sgm_camera* camera, uint6
     return guard(ctx, [&] {
         need_ctx(ctx);
         if (!map) fail(SGM_ERR_INVALID, "map is null");
+        if (map->dev.aniso)
+            fail(SGM_ERR_UNSUPPORTED, "the Fisher / backward chain is isotropic only (anisotropic map)");
         if (n > 0 && !poses) fail(SGM_ERR_INVALID, "poses are null");
         if (!(lambda > 0.0)) fail(SGM_ERR_INVALID, "lambda must be > 0");
         const CamParams cam = to_cam(camera);
@@ -1450,6 +1516,8 @@ int sgm_score_views_fisher(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* c
     return guard(ctx, [&] {
         need_ctx(ctx);
         if (!map) fail(SGM_ERR_INVALID, "map is null");
+        if (map->dev.aniso)
+            fail(SGM_ERR_UNSUPPORTED, "the Fisher / backward chain is isotropic only (anisotropic map)");
         if (!map->has_prior) fail(SGM_ERR_INVALID, "no Fisher prior (call sgm_fisher_prior first)");
         if (n == 0) return;
         if (!poses || !n_missing || !entropy_sum || !fisher_gain) fail(SGM_ERR_INVALID, "null argument");
@@ -1471,6 +1539,8 @@ int sgm_backward(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, con
         need_ctx(ctx);
         if (!map || !pose || !rgb || !depth || !sem || !weights || !report)
             fail(SGM_ERR_INVALID, "null argument");
+        if (map->dev.aniso)
+            fail(SGM_ERR_UNSUPPORTED, "the Fisher / backward chain is isotropic only (anisotropic map)");
         const CamParams cam = to_cam(camera);
         const OptParams o = to_opt(opt, cam);
         const PoseParams p = to_pose(*pose);

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
 #include "../../include/sgm.h"
@@ -34,6 +35,10 @@ struct DevMap {
     const double* sem_prob = nullptr;   // [n][kpad]
     const uint16_t* sem_perm = nullptr; // [n][kpad] original entry index of each sorted slot
     int dup_idx = 0;  // some Gaussian lists a class twice: serialise its RMWs
+    // Anisotropic splat mode (no reference counterpart): the world
+    // covariance replaces rad; projections use the EWA footprint (sgm_kernels.cu).
+    int aniso = 0;
+    const double* cov = nullptr;  // [6][n] SoA: xx, xy, xz, yy, yz, zz
 };
 
 struct CamParams {
@@ -69,6 +74,24 @@ struct __align__(16) PackedSplat {
     uint32_t aux;  // depth rank (projection id) of this record
 };
 static_assert(sizeof(PackedSplat) == 64, "PackedSplat must stay 64 B");
+
+// The same record in the anisotropic mode: the conic (inverse 2D covariance) takes
+// the slots of inv_two_r2, cutoff_d2 and the float probe (the cut is the constant
+// Mahalanobis trunc^2); alpha, z and aux keep their offsets.
+struct __align__(16) PackedSplatA {
+    double mx, my;
+    double qa, qb;
+    double alpha;
+    double z;
+    double qc;
+    uint32_t pad;
+    uint32_t aux;
+};
+static_assert(sizeof(PackedSplatA) == 64, "PackedSplatA must stay 64 B");
+static_assert(offsetof(PackedSplatA, alpha) == offsetof(PackedSplat, alpha) &&
+                  offsetof(PackedSplatA, z) == offsetof(PackedSplat, z) &&
+                  offsetof(PackedSplatA, aux) == offsetof(PackedSplat, aux),
+              "PackedSplatA must share alpha / z / aux with PackedSplat");
 
 // Channel groups: the C semantic channels are split into P groups of Cg; each
 // group is accumulated by its own CTA of a (P,1,1) thread-block cluster.
@@ -170,8 +193,8 @@ void launch_fisher_invp(const double* H, double lambda, size_t n, double* invp, 
 void launch_debug_projections(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
                               const OptParams& o, const uint32_t* idx, uint32_t V,
                               double* out6, cudaStream_t s);
-void launch_bins_to_ids(const uint32_t* list, uint64_t P, const PackedSplat* packed,
-                        uint32_t* ids, float* probe3, cudaStream_t s);
+void launch_bins_to_ids(const uint32_t* list, uint64_t P, const PackedSplat* packed, int aniso,
+                        double cut_sq, uint32_t* ids, float* probe3, cudaStream_t s);
 
 void launch_sort_rows(const uint16_t* idx, const double* prob, uint64_t n, int k, int kpad,
                       uint16_t* out_idx, double* out_prob, uint16_t* out_perm, cudaStream_t s);

@@ -28,10 +28,63 @@ __device__ __forceinline__ int to_int_x86(double v) {
     return (v > -2147483649.0 && v < 2147483648.0) ? static_cast<int>(v) : INT_MIN;
 }
 
+// Projection of one Gaussian: centre, depth, the binning reach per axis and, in
+// the anisotropic mode, the conic.
+struct Proj {
+    double mx, my, z, rad;  // rad: rad_px (isotropic) / sqrt(largest eigenvalue) (anisotropic)
+    double rx, ry;          // truncated reach along x / y (isotropic: trunc * rad_px, :34, :205)
+    double qa, qb, qc;      // anisotropic only: inverse 2D covariance
+};
+
+// EWA projection (no reference): Sigma2D = J R_cw Sigma R_cw^T J^T with J
+// the pinhole Jacobian at pc. Same operation order as oracle/sgm_oracle.c ewa_project
+// (no contraction), so projections and bins are bit-identical to the oracle.
+__device__ __forceinline__ bool ewa(const DevMap& m, uint64_t i, const PoseParams& P,
+                                    const CamParams& cam, const OptParams& o, double pcx,
+                                    double pcy, double pcz, Proj& q) {
+    // Jacobian at the view direction clamped to 1.3x the half field of view (as 3D
+    // Gaussian splatting does), so off-frustum centres near z_near stay bounded
+    const double limx = 1.3 * ((0.5 * cam.W) / cam.fx);
+    const double limy = 1.3 * ((0.5 * cam.H) / cam.fy);
+    const double rxz = pcx / pcz, ryz = pcy / pcz;
+    const double txz = rxz < -limx ? -limx : (limx < rxz ? limx : rxz);  // std::clamp order
+    const double tyz = ryz < -limy ? -limy : (limy < ryz ? limy : ryz);
+    const double tx = txz * pcz, ty = tyz * pcz;
+    const double zz = pcz * pcz;
+    const double j00 = cam.fx / pcz, j02 = -(cam.fx * tx) / zz;
+    const double j11 = cam.fy / pcz, j12 = -(cam.fy * ty) / zz;
+    const double* R = P.Rcw;  // row-major R_cw
+    const double a0 = j00 * R[0] + j02 * R[6], a1 = j00 * R[1] + j02 * R[7], a2 = j00 * R[2] + j02 * R[8];
+    const double b0 = j11 * R[3] + j12 * R[6], b1 = j11 * R[4] + j12 * R[7], b2 = j11 * R[5] + j12 * R[8];
+    const uint64_t n = m.n;
+    const double sxx = m.cov[i], sxy = m.cov[n + i], sxz = m.cov[2 * n + i];
+    const double syy = m.cov[3 * n + i], syz = m.cov[4 * n + i], szz = m.cov[5 * n + i];
+    const double ta0 = (sxx * a0 + sxy * a1) + sxz * a2;
+    const double ta1 = (sxy * a0 + syy * a1) + syz * a2;
+    const double ta2 = (sxz * a0 + syz * a1) + szz * a2;
+    const double tb0 = (sxx * b0 + sxy * b1) + sxz * b2;
+    const double tb1 = (sxy * b0 + syy * b1) + syz * b2;
+    const double tb2 = (sxz * b0 + syz * b1) + szz * b2;
+    const double va = (a0 * ta0 + a1 * ta1) + a2 * ta2;
+    const double vb = (b0 * ta0 + b1 * ta1) + b2 * ta2;
+    const double vc = (b0 * tb0 + b1 * tb1) + b2 * tb2;
+    const double det = va * vc - vb * vb;
+    if (!(det > 0.0)) return false;
+    q.rx = o.trunc * sqrt(va);
+    q.ry = o.trunc * sqrt(vc);
+    if (q.mx + q.rx < 0 || q.mx - q.rx > cam.W || q.my + q.ry < 0 || q.my - q.ry > cam.H)
+        return false;
+    q.qa = vc / det;
+    q.qb = -vb / det;
+    q.qc = va / det;
+    const double hm = 0.5 * (va + vc), hd = 0.5 * (va - vc);
+    q.rad = sqrt(hm + sqrt(hd * hd + vb * vb));
+    return true;
+}
+
 // project_splats for one Gaussian (splat_render.cpp:24-37). Returns visibility.
 __device__ __forceinline__ bool project(const DevMap& m, uint64_t i, const PoseParams& P,
-                                        const CamParams& cam, const OptParams& o, double& mx,
-                                        double& my, double& rad_px, double& z) {
+                                        const CamParams& cam, const OptParams& o, Proj& q) {
     const double d0 = m.cx[i] - P.t[0];
     const double d1 = m.cy[i] - P.t[1];
     const double d2 = m.cz[i] - P.t[2];
@@ -40,12 +93,14 @@ __device__ __forceinline__ bool project(const DevMap& m, uint64_t i, const PoseP
     if (pcz <= o.z_near) return false;  // :26
     const double pcx = P.Rcw[0] * d0 + (P.Rcw[1] * d1 + P.Rcw[2] * d2);
     const double pcy = P.Rcw[3] * d0 + (P.Rcw[4] * d1 + P.Rcw[5] * d2);
-    z = pcz;
-    mx = cam.fx * pcx / pcz + cam.cx;       // :29
-    my = cam.fy * pcy / pcz + cam.cy;       // :30
-    rad_px = m.rad[i] * cam.fy / pcz;       // :31 (exp done on host)
-    const double reach = o.trunc * rad_px;  // :34
-    if (mx + reach < 0 || mx - reach > cam.W || my + reach < 0 || my - reach > cam.H)
+    q.z = pcz;
+    q.mx = cam.fx * pcx / pcz + cam.cx;  // :29
+    q.my = cam.fy * pcy / pcz + cam.cy;  // :30
+    if (m.aniso) return ewa(m, i, P, cam, o, pcx, pcy, pcz, q);
+    q.rad = m.rad[i] * cam.fy / pcz;     // :31 (exp done on host)
+    const double reach = o.trunc * q.rad;  // :34
+    q.rx = q.ry = reach;
+    if (q.mx + reach < 0 || q.mx - reach > cam.W || q.my + reach < 0 || q.my - reach > cam.H)
         return false;  // :35-37
     return true;
 }
@@ -54,14 +109,13 @@ struct Rect {
     int tx0, tx1, ty0, ty1;
 };
 
-__device__ __forceinline__ Rect tile_rect(double mx, double my, double rad_px,
-                                          const OptParams& o) {
-    const double reach = o.trunc * rad_px;  // :205
+__device__ __forceinline__ Rect tile_rect(const Proj& q, const OptParams& o) {
+    // reach = trunc * rad_px (:205), per axis in the anisotropic mode
     Rect r;
-    r.tx0 = max(0, to_int_x86((mx - reach) / o.ts));               // :206
-    r.tx1 = min(o.tiles_x - 1, to_int_x86((mx + reach) / o.ts));   // :207
-    r.ty0 = max(0, to_int_x86((my - reach) / o.ts));               // :208
-    r.ty1 = min(o.tiles_y - 1, to_int_x86((my + reach) / o.ts));   // :209
+    r.tx0 = max(0, to_int_x86((q.mx - q.rx) / o.ts));               // :206
+    r.tx1 = min(o.tiles_x - 1, to_int_x86((q.mx + q.rx) / o.ts));   // :207
+    r.ty0 = max(0, to_int_x86((q.my - q.ry) / o.ts));               // :208
+    r.ty1 = min(o.tiles_y - 1, to_int_x86((q.my + q.ry) / o.ts));   // :209
     return r;
 }
 
@@ -88,9 +142,9 @@ __global__ void __launch_bounds__(256) k_preprocess(DevMap m, const PoseParams* 
     const int v = blockIdx.y;
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const PoseParams& P = poses[v];
-    double mx = 0, my = 0, rad = 0, z = 0;
-    const bool vis = i < m.n && project(m, i, P, cam, o, mx, my, rad, z);
-    unsigned long long cnt = vis ? rect_count(tile_rect(mx, my, rad, o)) : 0ull;
+    Proj q;
+    const bool vis = i < m.n && project(m, i, P, cam, o, q);
+    unsigned long long cnt = vis ? rect_count(tile_rect(q, o)) : 0ull;
 
     const unsigned mask = __ballot_sync(0xffffffffu, vis);
     const int lane = threadIdx.x & 31;
@@ -102,7 +156,7 @@ __global__ void __launch_bounds__(256) k_preprocess(DevMap m, const PoseParams* 
     }
     if (vis) {
         const uint32_t pos = base + __popc(mask & ((1u << lane) - 1u));
-        keys[v * stride + pos] = sortable(static_cast<float>(z));  // monotone in z
+        keys[v * stride + pos] = sortable(static_cast<float>(q.z));  // monotone in z
         vals[v * stride + pos] = static_cast<uint32_t>(i);
     }
 #pragma unroll
@@ -124,8 +178,11 @@ struct FullKey {
 __device__ __forceinline__ FullKey full_key(const DevMap& m, uint32_t i, const PoseParams& P,
                                             const CamParams& cam, const OptParams& o) {
     FullKey k;
-    double rad;
-    project(m, i, P, cam, o, k.mx, k.my, rad, k.z);
+    Proj q;
+    project(m, i, P, cam, o, q);
+    k.mx = q.mx;
+    k.my = q.my;
+    k.z = q.z;
     k.al = m.alpha[i];
     k.i = i;
     return k;
@@ -203,22 +260,37 @@ __global__ void k_pack(DevMap m, const PoseParams* __restrict__ pose, CamParams 
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= V) return;
     const uint32_t i = idx[r];
-    double mx, my, rad, z;
-    project(m, i, *pose, cam, o, mx, my, rad, z);
-    PackedSplat ps;
-    ps.mx = mx;
-    ps.my = my;
-    ps.inv_two_r2 = 1.0 / (2.0 * rad * rad);  // :194
-    ps.cutoff_d2 = o.cut_sq * rad * rad;      // :195
-    ps.alpha = m.alpha[i];
-    ps.z = z;
-    ps.pmx = static_cast<float>(mx);  // :201
-    ps.pmy = static_cast<float>(my);  // :202
-    ps.pcut = static_cast<float>(ps.cutoff_d2 * (1.0 + 1e-5)) + 1e-6f;  // :203
+    Proj q;
+    project(m, i, *pose, cam, o, q);
     const uint32_t aux = r;  // depth rank (contributor id)
-    ps.aux = aux;
-    packed[r] = ps;
-    const Rect rc = tile_rect(mx, my, rad, o);
+    if (m.aniso) {
+        PackedSplatA pa;
+        pa.mx = q.mx;
+        pa.my = q.my;
+        pa.qa = q.qa;
+        pa.qb = q.qb;
+        pa.alpha = m.alpha[i];
+        pa.z = q.z;
+        pa.qc = q.qc;
+        pa.pad = 0;
+        pa.aux = aux;
+        reinterpret_cast<PackedSplatA*>(packed)[r] = pa;
+    } else {
+        const double rad = q.rad;
+        PackedSplat ps;
+        ps.mx = q.mx;
+        ps.my = q.my;
+        ps.inv_two_r2 = 1.0 / (2.0 * rad * rad);  // :194
+        ps.cutoff_d2 = o.cut_sq * rad * rad;      // :195
+        ps.alpha = m.alpha[i];
+        ps.z = q.z;
+        ps.pmx = static_cast<float>(q.mx);  // :201
+        ps.pmy = static_cast<float>(q.my);  // :202
+        ps.pcut = static_cast<float>(ps.cutoff_d2 * (1.0 + 1e-5)) + 1e-6f;  // :203
+        ps.aux = aux;
+        packed[r] = ps;
+    }
+    const Rect rc = tile_rect(q, o);
     counts[r] = rect_count(rc);
     rects[r] = make_int4(rc.tx0, rc.ty0, rc.tx1 - rc.tx0 + 1, rc.ty1 - rc.ty0 + 1);
     if (bounds) {
@@ -328,24 +400,29 @@ __global__ void k_debug_projections(DevMap m, const PoseParams* __restrict__ pos
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= V) return;
     const uint32_t i = idx[r];
-    double mx, my, rad, z;
-    project(m, i, *pose, cam, o, mx, my, rad, z);
-    out6[6 * r] = mx;
-    out6[6 * r + 1] = my;
-    out6[6 * r + 2] = rad;
-    out6[6 * r + 3] = z;
+    Proj q;
+    project(m, i, *pose, cam, o, q);
+    out6[6 * r] = q.mx;
+    out6[6 * r + 1] = q.my;
+    out6[6 * r + 2] = q.rad;
+    out6[6 * r + 3] = q.z;
     out6[6 * r + 4] = m.alpha[i];
     out6[6 * r + 5] = static_cast<double>(i);
 }
 
 __global__ void k_bins_to_ids(const uint32_t* __restrict__ list, uint64_t P,
-                              const PackedSplat* __restrict__ packed, uint32_t* ids,
-                              float* probe3) {
+                              const PackedSplat* __restrict__ packed, int aniso, float cut,
+                              uint32_t* ids, float* probe3) {
     const uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (b >= P) return;
     const uint32_t r = list[b];
     if (ids) ids[b] = r;
-    if (probe3) {
+    if (probe3 && aniso) {  // anisotropic: centre and the Mahalanobis cut
+        const PackedSplat ps = packed[r];
+        probe3[3 * b] = static_cast<float>(ps.mx);
+        probe3[3 * b + 1] = static_cast<float>(ps.my);
+        probe3[3 * b + 2] = cut;
+    } else if (probe3) {
         const PackedSplat ps = packed[r];
         probe3[3 * b] = ps.pmx;
         probe3[3 * b + 1] = ps.pmy;
@@ -451,10 +528,11 @@ void launch_sort_rows(const uint16_t* idx, const double* prob, uint64_t n, int k
                                                    out_perm);
 }
 
-void launch_bins_to_ids(const uint32_t* list, uint64_t P, const PackedSplat* packed,
-                        uint32_t* ids, float* probe3, cudaStream_t s) {
+void launch_bins_to_ids(const uint32_t* list, uint64_t P, const PackedSplat* packed, int aniso,
+                        double cut_sq, uint32_t* ids, float* probe3, cudaStream_t s) {
     if (P == 0) return;
-    k_bins_to_ids<<<blocks_for(P, 256), 256, 0, s>>>(list, P, packed, ids, probe3);
+    k_bins_to_ids<<<blocks_for(P, 256), 256, 0, s>>>(list, P, packed, aniso,
+                                                     static_cast<float>(cut_sq), ids, probe3);
 }
 
 }  // namespace sgm

@@ -83,7 +83,7 @@ __device__ __forceinline__ int pair_slot(int row, int pitch2, int q) {
     return row * pitch2 * 2 + q;
 }
 
-template <bool kRender, bool kDup>
+template <bool kRender, bool kDup, bool kAniso>
 __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int C = p.map.C;
@@ -207,7 +207,18 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
                 const int e = e_first + 4 * i;
                 if (e >= n) break;
                 double f = -1.0;  // not a contributor
-                if (!pdone) {
+                if (kAniso && !pdone) {
+                    // f4 (no reference): f = alpha exp(-q / 2), q = d^T Sigma2D^-1 d, cut at
+                    // q > trunc^2 -- the order of oracle/sgm_oracle.c composite()
+                    const PackedSplatA& a = reinterpret_cast<const PackedSplatA&>(sp[e]);
+                    const double dx = dpx - a.mx;
+                    const double dy = dpy - a.my;
+                    const double q = (a.qa * (dx * dx) + (2.0 * a.qb) * (dx * dy)) + a.qc * (dy * dy);
+                    if (!(q > p.opt.cut_sq)) {
+                        f = a.alpha * exp_footprint(-0.5 * q);
+                        if (f > kMaxFootprint) f = kMaxFootprint;
+                    }
+                } else if (!pdone) {
                     const float4 pf = *reinterpret_cast<const float4*>(&sp[e].pmx);
                     const float fdx = fpx - pf.x;
                     const float fdy = fpy - pf.y;
@@ -428,9 +439,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     if (t == 0 && vd.contributors && red_u[0]) atomicAdd(vd.contributors, red_u[0]);
 }
 
-template <bool kRender, bool kDup>
+template <bool kRender, bool kDup, bool kAniso>
 void launch_t(const RasterParams& p, int n_views, cudaStream_t s) {
-    auto kern = k_raster<kRender, kDup>;
+    auto kern = k_raster<kRender, kDup, kAniso>;
     const size_t smem = raster_smem_bytes(p.map, p.groups, kRender);
     static size_t configured = 0;
     if (smem > configured) {
@@ -456,18 +467,26 @@ size_t raster_smem_bytes(const DevMap& m, const GroupParams& gp, bool render) {
     return static_cast<size_t>(make_layout(m.C, m.kpad, render).total);
 }
 
+template <bool kRender>
+void launch_mode(const RasterParams& p, int n_views, cudaStream_t s) {
+    if (p.map.aniso) {
+        if (p.map.dup_idx)
+            launch_t<kRender, true, true>(p, n_views, s);
+        else
+            launch_t<kRender, false, true>(p, n_views, s);
+    } else if (p.map.dup_idx) {
+        launch_t<kRender, true, false>(p, n_views, s);
+    } else {
+        launch_t<kRender, false, false>(p, n_views, s);
+    }
+}
+
 void launch_raster_score(const RasterParams& p, int n_views, cudaStream_t s) {
-    if (p.map.dup_idx)
-        launch_t<false, true>(p, n_views, s);
-    else
-        launch_t<false, false>(p, n_views, s);
+    launch_mode<false>(p, n_views, s);
 }
 
 void launch_raster_render(const RasterParams& p, int n_views, cudaStream_t s) {
-    if (p.map.dup_idx)
-        launch_t<true, true>(p, n_views, s);
-    else
-        launch_t<true, false>(p, n_views, s);
+    launch_mode<true>(p, n_views, s);
 }
 
 }  // namespace sgm

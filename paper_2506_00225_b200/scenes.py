@@ -72,8 +72,11 @@ def _f32(a: np.ndarray) -> np.ndarray:
     return np.asarray(a, dtype=np.float32).astype(np.float64)
 
 
-def make_map(cfg: int, n: int | None = None) -> GaussianMap:
-    """The config's Gaussian cloud (optionally its first-n-Gaussians prefix stream)."""
+def make_map(cfg: int, n: int | None = None, aniso: bool = False) -> GaussianMap:
+    """The config's Gaussian cloud (optionally its first-n-Gaussians prefix stream).
+
+    aniso=True also attaches the drawn per-axis log-scales and quaternions (fp32-rounded),
+    switching the map to the anisotropic EWA footprint."""
     sc = CONFIGS[cfg]
     n = sc.n if n is None else n
     rng = np.random.Generator(np.random.PCG64(sc.seed))
@@ -102,6 +105,8 @@ def make_map(cfg: int, n: int | None = None) -> GaussianMap:
     gm = GaussianMap.from_arrays(k, m, _f32(centers), _f32(log_scales.mean(axis=1)), _f32(logits),
                                  _f32(colors), idx, _f32(probs))
     gm.quaternions = quat.astype(np.float32)  # unused by the isotropic path
+    if aniso:
+        gm.set_anisotropic(_f32(log_scales), _f32(quat))
     return gm
 
 

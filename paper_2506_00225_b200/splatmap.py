@@ -205,11 +205,17 @@ class GaussianMap:
         self.sem_indices = np.zeros((0, self._k), dtype=np.uint16)
         self.sem_probs = np.zeros((0, self._k))
         self.source_frames = np.zeros(0, dtype=np.uint32)
+        # Anisotropic splat mode (no reference counterpart): optional
+        # per-axis log-scales (N x 3) and rotation quaternions (w, x, y, z) (N x 4).
+        # When both are set, render / score use EWA footprints instead of log_radii.
+        self.log_scales: Optional[np.ndarray] = None
+        self.quats: Optional[np.ndarray] = None
         self._version = 0
 
     @classmethod
     def from_arrays(cls, k, num_classes, centers, log_radii, opacity_logits, colors,
-                    sem_indices, sem_probs, source_frames=None) -> "GaussianMap":
+                    sem_indices, sem_probs, source_frames=None, log_scales=None,
+                    quats=None) -> "GaussianMap":
         m = cls(k, num_classes)
         n = len(log_radii)
         m.centers = np.ascontiguousarray(np.asarray(centers, dtype=np.float64).reshape(n, 3))
@@ -220,7 +226,23 @@ class GaussianMap:
         m.sem_probs = np.ascontiguousarray(np.asarray(sem_probs, dtype=np.float64).reshape(n, k))
         m.source_frames = (np.zeros(n, dtype=np.uint32) if source_frames is None
                            else np.ascontiguousarray(source_frames, dtype=np.uint32))
+        if log_scales is not None or quats is not None:
+            m.set_anisotropic(log_scales, quats)
         return m
+
+    def set_anisotropic(self, log_scales, quats) -> None:
+        """Per-Gaussian anisotropic footprints (f4 extension); (None, None) reverts to the
+        reference's isotropic log_radius footprint."""
+        if log_scales is None and quats is None:
+            self.log_scales = self.quats = None
+        else:
+            n = self.size()
+            self.log_scales = np.ascontiguousarray(np.asarray(log_scales, dtype=np.float64).reshape(n, 3))
+            self.quats = np.ascontiguousarray(np.asarray(quats, dtype=np.float64).reshape(n, 4))
+        self.touch()
+
+    def anisotropic(self) -> bool:
+        return self.log_scales is not None and self.quats is not None
 
     def k(self) -> int:
         return self._k
@@ -251,6 +273,9 @@ class GaussianMap:
         self.sem_indices = np.vstack([self.sem_indices,
                                       np.asarray(g.sem_indices, dtype=np.uint16)[None]])
         self.sem_probs = np.vstack([self.sem_probs, np.asarray(g.sem_probs, dtype=np.float64)[None]])
+        if self.anisotropic():  # a plain SemanticGaussian joins as a sphere of its radius
+            self.log_scales = np.vstack([self.log_scales, np.full((1, 3), float(g.log_radius))])
+            self.quats = np.vstack([self.quats, np.array([[1.0, 0.0, 0.0, 0.0]])])
         self.source_frames = np.append(self.source_frames, np.uint32(g.source_frame))
         self.touch()
 
@@ -474,6 +499,14 @@ class Context:
             self.handle, n, gmap.k(), gmap.num_classes(), N.dptr(arrs[0]), N.dptr(arrs[1]),
             N.dptr(arrs[2]), N.dptr(arrs[3]), idx.ctypes.data_as(C.POINTER(C.c_uint16)),
             N.dptr(probs), C.byref(h)))
+        if gmap.anisotropic():
+            ls = np.ascontiguousarray(gmap.log_scales, dtype=np.float64)
+            qs = np.ascontiguousarray(gmap.quats, dtype=np.float64)
+            try:
+                self.check(N.lib.sgm_map_set_anisotropic(self.handle, h, N.dptr(ls), N.dptr(qs)))
+            except Exception:
+                N.lib.sgm_map_release(self.handle, h)
+                raise
         return h
 
     def release(self, handle) -> None:
