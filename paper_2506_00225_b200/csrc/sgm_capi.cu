@@ -1,10 +1,12 @@
 // C ABI (include/sgm.h) and the host pipeline that drives the sm_100a kernels.
 //
 // Pipeline for a batch of views (all on the ctx stream):
-//   1. K1 k_preprocess over (Gaussian, view): compact visible (z, index), count V, P
-//   2. one D2H of the per-view V/P counts (the only host sync before the results)
-//   3. per view: CUB radix sort on fp32(z) -> k_tiefix -> k_pack -> CUB scan of
-//      tile counts -> k_emit_lb -> CUB stable radix sort on the bin id -> k_ranges
+//   1. K1 k_preprocess over (Gaussian, view): compact visible (z, index), count V, P and
+//      the row pairs R (tile rows spanned)
+//   2. one D2H of the per-view V/P/R counts (the only host sync before the results)
+//   3. per view (binning stream): CUB radix sort on fp32(z) -> k_tiefix -> k_pack ->
+//      k_bin_hist + k_bin_scan (tile ranges) -> k_emit_rows + CUB stable row sort ->
+//      k_row_segs / k_seg_pass x2 / k_seg_scan (ordered scatter into the tile lists)
 //   4. one batched raster launch over (8x8 tile, view)
 //   5. k_reduce_scores (score) / planes already written (render)
 // Views whose pair lists do not fit the scratch budget together are split into
@@ -147,7 +149,7 @@ struct sgm_ctx {
 
     // scratch
     DevBuf poses, vcount, pcount, keys, vals, keys_alt, vals_alt, packed, counts, offsets, rects,
-        bounds;
+        bounds, bdiff, rranges, rvals, segs, segcnt;
     DevBuf tkeys, tvals, tkeys_alt, tvals_alt, ranges, ent_part, miss_part, views, out,
         contributors, cub_tmp, planes, dbg, ccount, coffset, contrib, fis_part, bw_frame,
         bw_flags, bw_part, bw_grad;
@@ -247,7 +249,7 @@ struct RenderTargets {
 // slices and returns via the slice pointers. vals/keys hold the compacted (z, idx).
 void bin_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const CamParams& cam,
               const OptParams& o, const PoseParams* d_pose, uint32_t* keys, uint32_t* vals,
-              uint32_t V, uint64_t P, PackedSplat* packed, uint4* bounds, uint32_t* list,
+              uint32_t V, uint64_t P, uint64_t R, PackedSplat* packed, uint4* bounds, uint32_t* list,
               uint2* ranges, int bin_tiles) {
     CK(cudaMemsetAsync(ranges, 0, sizeof(uint2) * bin_tiles, s));
     if (V == 0) return;
@@ -265,31 +267,43 @@ void bin_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const CamParams&
     ctx->stats.kernel_launches += (V >= 2 ? 1 : 0) + 1;
     // keep the sorted indices for sgm_last_projections
     if (dv.Current() != vals) CK(cudaMemcpyAsync(vals, dv.Current(), 4ull * V, cudaMemcpyDeviceToDevice, s));
-    // K3: offsets = exclusive scan of tile counts (V+1 entries: last = P)
-    unsigned long long* cnt = ctx->counts.as<unsigned long long>();
-    unsigned long long* off = ctx->offsets.as<unsigned long long>();
-    CK(cudaMemsetAsync(cnt + V, 0, sizeof(unsigned long long), s));
-    tmp = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, off, V + 1, s));
-    CK(ctx->cub_tmp.reserve(tmp));
-    CK(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp, cnt, off, V + 1, s));
-    ctx->stats.kernel_launches += 1;
     if (P == 0) return;
-    uint32_t* tk = ctx->tkeys.as<uint32_t>();
-    launch_emit_pairs(off, ctx->rects.as<int4>(), V, P, o, tk, list, s);
-    ctx->stats.kernel_launches += 1;
-    cub::DoubleBuffer<uint32_t> pk(tk, ctx->tkeys_alt.as<uint32_t>());
-    cub::DoubleBuffer<uint32_t> pv(list, ctx->tvals_alt.as<uint32_t>());
-    tmp = 0;
-    const int bits = static_cast<int>(tile_bits(static_cast<uint64_t>(bin_tiles)));
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, pk, pv, P, 0, bits, s));
-    CK(ctx->cub_tmp.reserve(tmp));
-    CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, pk, pv, P, 0, bits, s));
-    ctx->stats.kernel_launches += 1;
-    if (pv.Current() != list)
-        CK(cudaMemcpyAsync(list, pv.Current(), 4ull * P, cudaMemcpyDeviceToDevice, s));
-    launch_ranges(pk.Current(), P, ranges, s);
-    ctx->stats.kernel_launches += 1;
+    // K3 (row-bucketed, no sort of the P pairs): tile ranges from the rectangles' 2D
+    // difference array; each tile row's ranks in rank order (R = sum of rows spanned pairs,
+    // stably sorted by row); then one CTA per tile row scatters its ranks into the tile lists
+    // in rank order (sgm_kernels.cu)
+    const int X = o.tiles_x + 1, Y = o.tiles_y + 1;
+    int* diff = ctx->bdiff.as<int>();
+    CK(cudaMemsetAsync(diff, 0, sizeof(int) * X * Y, s));
+    unsigned long long* rows = ctx->counts.as<unsigned long long>();
+    unsigned long long* roff = ctx->offsets.as<unsigned long long>();
+    launch_bin_hist(ctx->rects.as<int4>(), V, o.tiles_x, diff, rows, s);
+    launch_bin_scan(diff, o.tiles_x, o.tiles_y, ranges, s);
+    CK(cudaMemsetAsync(rows + V, 0, sizeof(unsigned long long), s));
+    size_t tmp2 = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, rows, roff, V + 1, s));
+    CK(ctx->cub_tmp.reserve(tmp2));
+    CK(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp2, rows, roff, V + 1, s));
+    uint32_t* rk = ctx->tkeys.as<uint32_t>();
+    unsigned long long* rv = ctx->rvals.as<unsigned long long>();
+    launch_emit_rows(roff, ctx->rects.as<int4>(), V, R, rk, rv, s);
+    cub::DoubleBuffer<uint32_t> qk(rk, ctx->tkeys_alt.as<uint32_t>());
+    cub::DoubleBuffer<unsigned long long> qv(rv, ctx->tvals_alt.as<unsigned long long>());
+    tmp2 = 0;
+    const int rbits = static_cast<int>(tile_bits(static_cast<uint64_t>(o.tiles_y)));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, qk, qv, R, 0, rbits, s));
+    CK(ctx->cub_tmp.reserve(tmp2));
+    CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp2, qk, qv, R, 0, rbits, s));
+    uint2* rranges = ctx->rranges.as<uint2>();
+    CK(cudaMemsetAsync(rranges, 0, sizeof(uint2) * o.tiles_y, s));
+    launch_ranges(qk.Current(), R, rranges, s);
+    const uint64_t G = row_scatter_segments(R, o.tiles_y);
+    CK(ctx->segs.reserve(sizeof(uint4) * G + 16));
+    CK(ctx->segcnt.reserve(sizeof(uint32_t) * G * o.tiles_x));
+    launch_row_scatter(qv.Current(), rranges, ranges, o.tiles_x, o.tiles_y, R,
+                       ctx->segs.as<uint4>(), reinterpret_cast<uint32_t*>(ctx->segs.as<char>() + sizeof(uint4) * G),
+                       ctx->segcnt.as<uint32_t>(), list, s);
+    ctx->stats.kernel_launches += 7;
 }
 
 // Runs n views. Score mode writes n_missing/entropy_sum (host); render mode (n == 1)
@@ -320,7 +334,9 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
     const size_t NS = std::max<uint64_t>(N, 1);
     CK(ctx->poses.reserve(sizeof(PoseParams) * B));
     CK(ctx->vcount.reserve(4 * B));
-    CK(ctx->pcount.reserve(8 * B));
+    CK(ctx->pcount.reserve(16 * B));  // pairs P | row pairs R per view
+    CK(ctx->bdiff.reserve(sizeof(int) * (o.tiles_x + 1) * (o.tiles_y + 1)));
+    CK(ctx->rranges.reserve(sizeof(uint2) * o.tiles_y));
     CK(ctx->keys.reserve(4 * NS * B));
     CK(ctx->vals.reserve(4 * NS * B));
     CK(ctx->keys_alt.reserve(4 * NS));
@@ -337,7 +353,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
     CK(ctx->out.reserve(24 * B));
     if (fk == Fisher::Gain) CK(ctx->fis_part.reserve(8ull * rtiles * B));
     CK(ctx->contributors.reserve(8));
-    CK(ctx->h_counts.reserve(16 * B + 8));
+    CK(ctx->h_counts.reserve(32 * B + 16));  // V (u32) | P | R | contributors
     CK(ctx->h_views.reserve(sizeof(ViewDesc) * B));
     CK(ctx->h_poses.reserve(sizeof(PoseParams) * B));
     CK(ctx->h_out.reserve(24 * B));
@@ -350,19 +366,21 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
         CK(cudaMemcpyAsync(ctx->poses.p, ctx->h_poses.p, sizeof(PoseParams) * nb,
                            cudaMemcpyHostToDevice, s));
         CK(cudaMemsetAsync(ctx->vcount.p, 0, 4 * nb, s));
-        CK(cudaMemsetAsync(ctx->pcount.p, 0, 8 * nb, s));
+        CK(cudaMemsetAsync(ctx->pcount.p, 0, 16 * nb, s));
         CK(cudaMemsetAsync(ctx->contributors.p, 0, 8, s));
         launch_preprocess(map->dev, ctx->poses.as<PoseParams>(), cam, o, nb, ctx->keys.as<uint32_t>(),
                           ctx->vals.as<uint32_t>(), NS, ctx->vcount.as<uint32_t>(),
-                          ctx->pcount.as<unsigned long long>(), s);
+                          ctx->pcount.as<unsigned long long>(),
+                          ctx->pcount.as<unsigned long long>() + nb, s);
         ctx->stats.kernel_launches += (N > 0) ? 1 : 0;
         uint32_t* hv = ctx->h_counts.as<uint32_t>();
         unsigned long long* hp = reinterpret_cast<unsigned long long*>(ctx->h_counts.as<char>() + 8 * B);
         CK(cudaMemcpyAsync(hv, ctx->vcount.p, 4 * nb, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(hp, ctx->pcount.p, 8 * nb, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hp, ctx->pcount.p, 16 * nb, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         std::vector<uint32_t> V(hv, hv + nb);
         std::vector<uint64_t> P(hp, hp + nb);
+        std::vector<uint64_t> R(hp + nb, hp + 2 * nb);  // (row, rank) pairs of the binning
         for (int v = 0; v < nb; ++v)
             if (P[v] >= (1ull << 32)) fail(SGM_ERR_UNSUPPORTED, "view has %llu tile pairs (>= 2^32)",
                                           static_cast<unsigned long long>(P[v]));
@@ -378,10 +396,13 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 maxP = std::max<uint64_t>(maxP, P[v1]);
                 ++v1;
             }
+            uint64_t maxR = 1;
+            for (int v = v0; v < v1; ++v) maxR = std::max<uint64_t>(maxR, R[v]);
             CK(ctx->tvals.reserve(4 * std::max<uint64_t>(sumP, 1)));
-            CK(ctx->tkeys.reserve(4 * std::max<uint64_t>(maxP, 1)));
-            CK(ctx->tkeys_alt.reserve(4 * std::max<uint64_t>(maxP, 1)));
-            CK(ctx->tvals_alt.reserve(4 * std::max<uint64_t>(maxP, 1)));
+            CK(ctx->tkeys.reserve(4 * maxR));
+            CK(ctx->tkeys_alt.reserve(4 * maxR));
+            CK(ctx->tvals_alt.reserve(8 * maxR));
+            CK(ctx->rvals.reserve(8 * maxR));
             // descriptors for the whole group (list offsets known from the counts)
             ViewDesc* hvd = ctx->h_views.as<ViewDesc>();
             uint64_t list_off = 0;
@@ -429,7 +450,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                     const ViewDesc& d = hvd[v - v0];
                     bin_view(ctx, sb, map, cam, o, ctx->poses.as<PoseParams>() + v,
                              ctx->keys.as<uint32_t>() + NS * v, const_cast<uint32_t*>(d.order), V[v],
-                             P[v], const_cast<PackedSplat*>(d.packed), const_cast<uint4*>(d.bounds),
+                             P[v], R[v], const_cast<PackedSplat*>(d.packed), const_cast<uint4*>(d.bounds),
                              const_cast<uint32_t*>(d.list), const_cast<uint2*>(d.ranges), bin_tiles);
                 }
                 const int slot = (s0 / kSub) & 1;
@@ -465,7 +486,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 ctx->stats.kernel_launches += 1;
                 double* ho = ctx->h_out.as<double>();
                 CK(cudaMemcpyAsync(ho, ctx->out.p, 24 * ngroup, cudaMemcpyDeviceToHost, s));
-                unsigned long long* kc = hp + B;
+                unsigned long long* kc = hp + 2 * B;
                 CK(cudaMemcpyAsync(kc, ctx->contributors.p, 8, cudaMemcpyDeviceToHost, s));
                 CK(cudaMemsetAsync(ctx->contributors.p, 0, 8, s));
                 CK(cudaStreamSynchronize(s));
@@ -476,7 +497,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 }
                 ctx->stats.contributors += *kc;
             } else {
-                unsigned long long* kc = hp + B;
+                unsigned long long* kc = hp + 2 * B;
                 CK(cudaMemcpyAsync(kc, ctx->contributors.p, 8, cudaMemcpyDeviceToHost, s));
                 CK(cudaMemsetAsync(ctx->contributors.p, 0, 8, s));
                 CK(cudaStreamSynchronize(s));

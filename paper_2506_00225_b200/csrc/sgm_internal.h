@@ -171,7 +171,7 @@ struct RasterParams {
 void launch_preprocess(const DevMap& m, const PoseParams* d_poses, const CamParams& cam,
                        const OptParams& o, int n_views, uint32_t* keys, uint32_t* vals,
                        size_t stride, uint32_t* vcount, unsigned long long* pcount,
-                       cudaStream_t s);
+                       unsigned long long* rcount, cudaStream_t s);
 void launch_tiefix(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
                    const OptParams& o, const uint32_t* key, uint32_t* idx, uint32_t V,
                    cudaStream_t s);
@@ -179,10 +179,19 @@ void launch_pack(const DevMap& m, const PoseParams* d_pose, const CamParams& cam
                  const OptParams& o, const GroupParams& gp, const uint32_t* idx, uint32_t V,
                  PackedSplat* packed, unsigned long long* counts, int4* rects, uint4* bounds,
                  cudaStream_t s);
-void launch_emit_pairs(const unsigned long long* offsets, const int4* rects, uint32_t V,
-                       unsigned long long P, const OptParams& o, uint32_t* tile_keys,
-                       uint32_t* tile_vals, cudaStream_t s);
 void launch_ranges(const uint32_t* sorted_tiles, uint64_t P, uint2* ranges, cudaStream_t s);
+// row-bucketed binning (sgm_kernels.cu): tile ranges from a 2D difference array, each
+// row's ranks in rank order, then a per-row ordered scatter into the tile lists
+void launch_bin_hist(const int4* rects, uint32_t V, int tiles_x, int* diff,
+                     unsigned long long* rows, cudaStream_t s);
+void launch_bin_scan(int* diff, int tiles_x, int tiles_y, uint2* ranges, cudaStream_t s);
+void launch_emit_rows(const unsigned long long* offsets, const int4* rects, uint32_t V,
+                      unsigned long long R, uint32_t* row_keys, unsigned long long* row_vals,
+                      cudaStream_t s);
+void launch_row_scatter(const unsigned long long* row_list, const uint2* row_ranges,
+                        const uint2* tile_ranges, int tiles_x, int tiles_y, uint64_t R, uint4* segs,
+                        uint32_t* nseg, uint32_t* cnt, uint32_t* list, cudaStream_t s);
+uint64_t row_scatter_segments(uint64_t R, int tiles_y);  // upper bound on segments
 void launch_raster_score(const RasterParams& p, int n_views, cudaStream_t s);
 void launch_raster_render(const RasterParams& p, int n_views, cudaStream_t s);
 void launch_reduce_scores(const ViewDesc* views, int n_views, int tiles, double* out_missing,

@@ -8,10 +8,13 @@
 //   K1 k_preprocess      project_splats transform/cull + tile count   splat_render.cpp:15-39, 205-209
 //   K2 CUB radix sort on the fp32-rounded depth (monotone) + k_tiefix: runs of
 //      equal fp32 keys re-sorted by the full fp64 (z, mx, my, alpha) key  splat_render.cpp:40-45
-//   K3 k_pack / k_emit_lb (load-balanced over pairs) / CUB stable tile sort / k_ranges
-//                                                                       splat_render.cpp:189-213
+//   K3 k_pack, then row-bucketed binning without sorting the (tile, rank) pairs:
+//      k_bin_hist + k_bin_scan (tile ranges from a 2D difference array), k_emit_rows + CUB
+//      stable row sort (each tile row's ranks in rank order), k_row_segs / k_seg_pass /
+//      k_seg_scan (ordered, coalesced scatter into the tile lists)   splat_render.cpp:189-213
 //   K4/K5 raster: see sgm_raster.cu
 //   k_reduce_scores     deterministic per-view n_missing / entropy_sum   explorer.cpp:195-203
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 #include <cstdio>
@@ -138,13 +141,16 @@ __global__ void __launch_bounds__(256) k_preprocess(DevMap m, const PoseParams* 
                                                     CamParams cam, OptParams o, uint32_t* keys,
                                                     uint32_t* vals, size_t stride,
                                                     uint32_t* vcount,
-                                                    unsigned long long* pcount) {
+                                                    unsigned long long* pcount,
+                                                    unsigned long long* rcount) {
     const int v = blockIdx.y;
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const PoseParams& P = poses[v];
     Proj q;
     const bool vis = i < m.n && project(m, i, P, cam, o, q);
-    unsigned long long cnt = vis ? rect_count(tile_rect(q, o)) : 0ull;
+    const Rect rc0 = vis ? tile_rect(q, o) : Rect{0, -1, 0, -1};
+    unsigned long long cnt = vis ? rect_count(rc0) : 0ull;
+    unsigned long long rows = cnt ? static_cast<unsigned long long>(rc0.ty1 - rc0.ty0 + 1) : 0ull;
 
     const unsigned mask = __ballot_sync(0xffffffffu, vis);
     const int lane = threadIdx.x & 31;
@@ -160,8 +166,14 @@ __global__ void __launch_bounds__(256) k_preprocess(DevMap m, const PoseParams* 
         vals[v * stride + pos] = static_cast<uint32_t>(i);
     }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, off);
-    if (lane == 0 && cnt) atomicAdd(&pcount[v], cnt);
+    for (int off = 16; off > 0; off >>= 1) {
+        cnt += __shfl_down_sync(0xffffffffu, cnt, off);
+        rows += __shfl_down_sync(0xffffffffu, rows, off);
+    }
+    if (lane == 0 && cnt) {
+        atomicAdd(&pcount[v], cnt);
+        atomicAdd(&rcount[v], rows);
+    }
 }
 
 // ---------------------------------------------------------------- K2 tie fix-up
@@ -310,22 +322,21 @@ __global__ void k_pack(DevMap m, const PoseParams* __restrict__ pose, CamParams 
     }
 }
 
-// Emits (bin, rank) pairs in rank order at the scanned offsets; a stable sort on
-// the bin key then yields every bin in depth order (:210-212). rad_px is not kept
-// in PackedSplat (64 B); the rectangle is re-derived by re-projecting, which is
-// bit-identical to the count pass.
-// Load-balanced: each thread emits kPerThread consecutive pairs. The first
-// pair's rank comes from a binary search over the scanned counts; then the
-// thread walks forward (pairs of one rank are contiguous).
+// Emits (tile row, rank | column range) pairs in rank order at the scanned per-rank row
+// counts: one per tile row a rectangle spans; a stable sort on the row key then yields
+// every row's ranks in rank order (the input of the per-row scatter below).
+// Load-balanced: each thread emits kPerThread consecutive pairs. The first pair's rank
+// comes from a binary search over the scanned counts; then the thread walks forward
+// (pairs of one rank are contiguous).
 constexpr int kPerThread = 8;
-__global__ void k_emit_lb(const unsigned long long* __restrict__ offsets, const int4* __restrict__ rects,
-                          uint32_t V, unsigned long long P, int tiles_x, uint32_t* tile_keys,
-                          uint32_t* tile_vals) {
+__global__ void k_emit_rows(const unsigned long long* __restrict__ offsets, const int4* __restrict__ rects,
+                            uint32_t V, unsigned long long R, uint32_t* row_keys,
+                            unsigned long long* row_vals) {
     const unsigned long long i0 =
         (static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x) * kPerThread;
-    if (i0 >= P) return;
+    if (i0 >= R) return;
     // largest r with offsets[r] <= i0
-    uint32_t lo = 0, hi = V;  // offsets[V] == P > i0
+    uint32_t lo = 0, hi = V;  // offsets[V] == R > i0
     while (hi - lo > 1) {
         const uint32_t mid = (lo + hi) / 2;
         if (offsets[mid] <= i0) lo = mid; else hi = mid;
@@ -333,7 +344,7 @@ __global__ void k_emit_lb(const unsigned long long* __restrict__ offsets, const 
     uint32_t r = lo;
     unsigned long long beg = offsets[r], end = offsets[r + 1];
     int4 rc = rects[r];
-    const unsigned long long i1 = min(P, i0 + kPerThread);
+    const unsigned long long i1 = min(R, i0 + kPerThread);
     for (unsigned long long i = i0; i < i1; ++i) {
         while (i >= end) {
             ++r;
@@ -342,10 +353,183 @@ __global__ void k_emit_lb(const unsigned long long* __restrict__ offsets, const 
             rc = rects[r];
         }
         const uint32_t j = static_cast<uint32_t>(i - beg);
-        const uint32_t dy = j / static_cast<uint32_t>(rc.z);
-        const uint32_t dx = j - dy * static_cast<uint32_t>(rc.z);
-        tile_keys[i] = static_cast<uint32_t>((rc.y + static_cast<int>(dy)) * tiles_x + rc.x + static_cast<int>(dx));
-        tile_vals[i] = r;
+        row_keys[i] = static_cast<uint32_t>(rc.y) + j;
+        row_vals[i] = (static_cast<unsigned long long>(r) << 32) |
+                      (static_cast<unsigned long long>(rc.x) << 16) |
+                      static_cast<unsigned long long>(rc.x + rc.z - 1);
+    }
+}
+
+// ---------------------------------------------------------------- row-bucketed binning
+// The bins of :210-212 are, per tile, the ranks whose rectangle covers the tile, in rank
+// order. Built without sorting the (tile, rank) pairs:
+//   k_bin_hist   per rank: 2D difference-array corners of its rectangle (tile counts) and
+//                its row count (number of tile rows spanned);
+//   k_bin_scan   one CTA: 2D prefix of the difference array -> per-tile counts -> exclusive
+//                scan in bin order -> ranges[bin] = (begin, end);
+//   rows         (row, rank) pairs emitted in rank order and stably sorted by row (small:
+//                one pair per spanned row, not per tile) -> each row's ranks in rank order;
+//   k_row_scatter one CTA per tile row: chunks of 32 consecutive ranks; warp w owns the
+//                columns tx = w mod 8, and for each column a ballot over the chunk gives every
+//                covering rank its slot (cursor + popc of the lanes before it), so each tile's
+//                list is written in rank order with coalesced stores.
+__global__ void k_bin_hist(const int4* __restrict__ rects, uint32_t V, int tiles_x,
+                           int* __restrict__ diff, unsigned long long* __restrict__ rows) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= V) return;
+    const int4 rc = rects[r];
+    const bool any = rc.z > 0 && rc.w > 0;
+    rows[r] = any ? static_cast<unsigned long long>(rc.w) : 0ull;
+    if (!any) return;
+    const int X = tiles_x + 1;
+    const int x0 = rc.x, x1 = rc.x + rc.z, y0 = rc.y, y1 = rc.y + rc.w;  // half-open
+    atomicAdd(&diff[y0 * X + x0], 1);
+    atomicAdd(&diff[y0 * X + x1], -1);
+    atomicAdd(&diff[y1 * X + x0], -1);
+    atomicAdd(&diff[y1 * X + x1], 1);
+}
+
+constexpr int kScanThreads = 1024;
+__global__ void __launch_bounds__(kScanThreads) k_bin_scan(int* __restrict__ diff, int tiles_x,
+                                                           int tiles_y, uint2* __restrict__ ranges) {
+    const int X = tiles_x + 1;
+    const int t = threadIdx.x;
+    // prefix along x, then along y: diff[y][x] becomes the tile count
+    for (int y = t; y < tiles_y; y += kScanThreads) {
+        int acc = 0;
+        for (int x = 0; x < tiles_x; ++x) {
+            acc += diff[y * X + x];
+            diff[y * X + x] = acc;
+        }
+    }
+    __syncthreads();
+    for (int x = t; x < tiles_x; x += kScanThreads) {
+        int acc = 0;
+        for (int y = 0; y < tiles_y; ++y) {
+            acc += diff[y * X + x];
+            diff[y * X + x] = acc;
+        }
+    }
+    __syncthreads();
+    // exclusive scan over bins (row-major), each thread a contiguous segment
+    __shared__ uint32_t part[kScanThreads];
+    const int T = tiles_x * tiles_y;
+    const int per = (T + kScanThreads - 1) / kScanThreads;
+    const int b0 = min(T, t * per), b1 = min(T, b0 + per);
+    uint32_t sum = 0;
+    for (int b = b0; b < b1; ++b) sum += static_cast<uint32_t>(diff[(b / tiles_x) * X + b % tiles_x]);
+    part[t] = sum;
+    __syncthreads();
+    for (int off = 1; off < kScanThreads; off <<= 1) {  // Hillis-Steele inclusive scan
+        const uint32_t v = t >= off ? part[t - off] : 0u;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    uint32_t run = part[t] - sum;
+    for (int b = b0; b < b1; ++b) {
+        const uint32_t c = static_cast<uint32_t>(diff[(b / tiles_x) * X + b % tiles_x]);
+        ranges[b] = make_uint2(run, run + c);
+        run += c;
+    }
+}
+
+// Each tile row's list (ranks in rank order) is cut into segments of kSeg entries; a
+// segment x 32-column block is one warp's work unit. Lanes hold 32 consecutive entries of
+// a chunk; for every column of the block a ballot over the chunk marks the covering
+// entries, which take consecutive slots of that column's list (coalesced stores). The
+// column cursors live in the registers of the lanes (lane l <-> column cb + l).
+//   pass 0 counts per (segment, column), k_seg_scan turns them into per-segment bases,
+//   pass 1 writes. Segments of a row are independent, so dense rows spread over the GPU.
+constexpr int kSeg = 1024;
+
+__global__ void __launch_bounds__(1024) k_row_segs(const uint2* __restrict__ row_ranges, int tiles_y,
+                                                   uint4* __restrict__ segs, uint32_t* __restrict__ nseg_out) {
+    // segment g = (row, begin, end, -): each row's list cut into kSeg pieces, rows in order.
+    // Thread t owns a contiguous block of rows; a block scan places its segments.
+    __shared__ uint32_t part[1024];
+    const int t = threadIdx.x;
+    const int per = (tiles_y + 1023) / 1024;
+    const int y0 = min(tiles_y, t * per), y1 = min(tiles_y, y0 + per);
+    uint32_t mine = 0;
+    for (int y = y0; y < y1; ++y) {
+        const uint2 rr = row_ranges[y];
+        mine += (rr.y - rr.x + kSeg - 1) / kSeg;
+    }
+    part[t] = mine;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+        const uint32_t v = t >= off ? part[t - off] : 0u;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    uint32_t g = part[t] - mine;
+    for (int y = y0; y < y1; ++y) {
+        const uint2 rr = row_ranges[y];
+        for (uint32_t b = rr.x; b < rr.y; b += kSeg) segs[g++] = make_uint4(y, b, min(rr.y, b + kSeg), 0u);
+    }
+    if (t == 1023) *nseg_out = part[1023];
+}
+
+template <bool kWrite>
+__global__ void __launch_bounds__(256) k_seg_pass(const unsigned long long* __restrict__ row_list,
+                                                  const uint4* __restrict__ segs,
+                                                  const uint32_t* __restrict__ nseg, int tiles_x,
+                                                  uint32_t* __restrict__ cnt, uint32_t* __restrict__ list) {
+    const uint32_t g = blockIdx.x;
+    if (g >= *nseg) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cb = (blockIdx.y * (blockDim.x >> 5) + warp) * 32;
+    if (cb >= tiles_x) return;
+    const uint4 sg = segs[g];
+    const int col = cb + lane;
+    const bool has = col < tiles_x;
+    const int last = min(tiles_x, cb + 32) - 1;
+    uint32_t cur = (kWrite && has) ? cnt[static_cast<size_t>(g) * tiles_x + col] : 0u;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint32_t base = sg.y; base < sg.z; base += 32) {
+        const bool valid = base + lane < sg.z;
+        const unsigned long long e = valid ? row_list[base + lane] : 0ull;
+        const int x0 = valid ? static_cast<int>((e >> 16) & 0xffffu) : INT_MAX;
+        const int x1 = valid ? static_cast<int>(e & 0xffffu) : INT_MIN;
+        const int lo = max(cb, __reduce_min_sync(0xffffffffu, x0));
+        const int hi = min(last, __reduce_max_sync(0xffffffffu, x1));
+        for (int c = lo; c <= hi; ++c) {
+            const bool cov = x0 <= c && c <= x1;
+            const uint32_t bal = __ballot_sync(0xffffffffu, cov);
+            const int owner = c - cb;
+            if (kWrite) {
+                const uint32_t at = __shfl_sync(0xffffffffu, cur, owner);
+                if (cov) list[at + __popc(bal & lt)] = static_cast<uint32_t>(e >> 32);
+            }
+            if (lane == owner) cur += __popc(bal);
+        }
+    }
+    if (!kWrite && has) cnt[static_cast<size_t>(g) * tiles_x + col] = cur;
+}
+
+// per (row, column): exclusive scan of the segment counts over the row's segments, offset by
+// the tile's list start
+__global__ void k_seg_scan(const uint4* __restrict__ segs, const uint32_t* __restrict__ nseg,
+                           const uint2* __restrict__ tile_ranges, int tiles_x, int tiles_y,
+                           uint32_t* __restrict__ cnt) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= tiles_x * tiles_y) return;
+    const int y = i / tiles_x, x = i - y * tiles_x;
+    const uint32_t G = *nseg;
+    // the row's segments are contiguous; find the first by binary search on segs[].x
+    uint32_t lo = 0, hi = G;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) / 2;
+        if (static_cast<int>(segs[mid].x) < y) lo = mid + 1; else hi = mid;
+    }
+    uint32_t run = tile_ranges[i].x;
+    for (uint32_t g = lo; g < G && static_cast<int>(segs[g].x) == y; ++g) {
+        const size_t k = static_cast<size_t>(g) * tiles_x + x;
+        const uint32_t c = cnt[k];
+        cnt[k] = run;
+        run += c;
     }
 }
 
@@ -472,10 +656,11 @@ inline unsigned blocks_for(uint64_t n, unsigned threads) {
 void launch_preprocess(const DevMap& m, const PoseParams* d_poses, const CamParams& cam,
                        const OptParams& o, int n_views, uint32_t* keys, uint32_t* vals,
                        size_t stride, uint32_t* vcount, unsigned long long* pcount,
-                       cudaStream_t s) {
+                       unsigned long long* rcount, cudaStream_t s) {
     if (m.n == 0 || n_views == 0) return;
     dim3 grid(blocks_for(m.n, 256), n_views);
-    k_preprocess<<<grid, 256, 0, s>>>(m, d_poses, cam, o, keys, vals, stride, vcount, pcount);
+    k_preprocess<<<grid, 256, 0, s>>>(m, d_poses, cam, o, keys, vals, stride, vcount, pcount,
+                                      rcount);
 }
 
 void launch_tiefix(const DevMap& m, const PoseParams* d_pose, const CamParams& cam,
@@ -494,13 +679,41 @@ void launch_pack(const DevMap& m, const PoseParams* d_pose, const CamParams& cam
                                               bounds);
 }
 
-void launch_emit_pairs(const unsigned long long* offsets, const int4* rects, uint32_t V,
-                       unsigned long long P, const OptParams& o, uint32_t* tile_keys,
-                       uint32_t* tile_vals, cudaStream_t s) {
-    if (V == 0 || P == 0) return;
-    const unsigned long long threads = (P + kPerThread - 1) / kPerThread;
-    k_emit_lb<<<blocks_for(threads, 256), 256, 0, s>>>(offsets, rects, V, P, o.tiles_x, tile_keys,
-                                                       tile_vals);
+void launch_emit_rows(const unsigned long long* offsets, const int4* rects, uint32_t V,
+                      unsigned long long R, uint32_t* row_keys, unsigned long long* row_vals,
+                      cudaStream_t s) {
+    if (V == 0 || R == 0) return;
+    const unsigned long long threads = (R + kPerThread - 1) / kPerThread;
+    k_emit_rows<<<blocks_for(threads, 256), 256, 0, s>>>(offsets, rects, V, R, row_keys, row_vals);
+}
+
+void launch_bin_hist(const int4* rects, uint32_t V, int tiles_x, int* diff,
+                     unsigned long long* rows, cudaStream_t s) {
+    if (V == 0) return;
+    k_bin_hist<<<blocks_for(V, 256), 256, 0, s>>>(rects, V, tiles_x, diff, rows);
+}
+
+void launch_bin_scan(int* diff, int tiles_x, int tiles_y, uint2* ranges, cudaStream_t s) {
+    k_bin_scan<<<1, kScanThreads, 0, s>>>(diff, tiles_x, tiles_y, ranges);
+}
+
+void launch_row_scatter(const unsigned long long* row_list, const uint2* row_ranges,
+                        const uint2* tile_ranges, int tiles_x, int tiles_y, uint64_t R, uint4* segs,
+                        uint32_t* nseg, uint32_t* cnt, uint32_t* list, cudaStream_t s) {
+    if (R == 0) return;
+    const uint64_t gmax = R / kSeg + static_cast<uint64_t>(tiles_y) + 1;
+    k_row_segs<<<1, 1024, 0, s>>>(row_ranges, tiles_y, segs, nseg);
+    const int blocks = (tiles_x + 31) / 32;  // 32-column blocks, one warp each
+    const int warps = std::min(8, blocks);
+    const dim3 grid(static_cast<unsigned>(gmax), static_cast<unsigned>((blocks + warps - 1) / warps));
+    k_seg_pass<false><<<grid, 32 * warps, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list);
+    k_seg_scan<<<blocks_for(static_cast<uint64_t>(tiles_x) * tiles_y, 256), 256, 0, s>>>(
+        segs, nseg, tile_ranges, tiles_x, tiles_y, cnt);
+    k_seg_pass<true><<<grid, 32 * warps, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list);
+}
+
+uint64_t row_scatter_segments(uint64_t R, int tiles_y) {
+    return R / kSeg + static_cast<uint64_t>(tiles_y) + 1;
 }
 
 void launch_ranges(const uint32_t* sorted_tiles, uint64_t P, uint2* ranges, cudaStream_t s) {

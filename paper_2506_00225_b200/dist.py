@@ -38,19 +38,23 @@ def broadcast_map(gmap: Optional[GaussianMap], src: int = 0) -> GaussianMap:
     dev = _device()
     rank = dist.get_rank()
     if rank == src:
-        head = torch.tensor([gmap.size(), gmap.k(), gmap.num_classes()], dtype=torch.int64)
+        head = torch.tensor([gmap.size(), gmap.k(), gmap.num_classes(),
+                             1 if gmap.anisotropic() else 0], dtype=torch.int64)
     else:
-        head = torch.zeros(3, dtype=torch.int64)
+        head = torch.zeros(4, dtype=torch.int64)
     head = head.to(dev)
     dist.broadcast(head, src)
-    n, k, m = (int(v) for v in head.cpu())
+    n, k, m, aniso = (int(v) for v in head.cpu())
+    extra = 7 * n if aniso else 0  # f4: per-axis log-scales (3N) and quaternions (4N)
     if rank == src:
-        f64 = np.concatenate([gmap.centers.reshape(-1), gmap.log_radii, gmap.opacity_logits,
-                              gmap.colors.reshape(-1), gmap.sem_probs.reshape(-1)])
-        buf = torch.from_numpy(np.ascontiguousarray(f64)).to(dev)
+        parts = [gmap.centers.reshape(-1), gmap.log_radii, gmap.opacity_logits,
+                 gmap.colors.reshape(-1), gmap.sem_probs.reshape(-1)]
+        if aniso:
+            parts += [gmap.log_scales.reshape(-1), gmap.quats.reshape(-1)]
+        buf = torch.from_numpy(np.ascontiguousarray(np.concatenate(parts))).to(dev)
         ids = torch.from_numpy(gmap.sem_indices.astype(np.int32).reshape(-1)).to(dev)
     else:
-        buf = torch.empty(n * (8 + k), dtype=torch.float64, device=dev)
+        buf = torch.empty(n * (8 + k) + extra, dtype=torch.float64, device=dev)
         ids = torch.empty(n * k, dtype=torch.int32, device=dev)
     dist.broadcast(buf, src)
     dist.broadcast(ids, src)
@@ -71,7 +75,10 @@ def broadcast_map(gmap: Optional[GaussianMap], src: int = 0) -> GaussianMap:
     colors = take(3 * n).reshape(n, 3)
     probs = take(k * n).reshape(n, k)
     idx = ids.cpu().numpy().astype(np.uint16).reshape(n, k)
-    return GaussianMap.from_arrays(k, m, centers, log_r, logits, colors, idx, probs)
+    ls = take(3 * n).reshape(n, 3) if aniso else None
+    qs = take(4 * n).reshape(n, 4) if aniso else None
+    return GaussianMap.from_arrays(k, m, centers, log_r, logits, colors, idx, probs,
+                                   log_scales=ls, quats=qs)
 
 
 def gather_scores(n_total: int, n_missing: np.ndarray, entropy_sum: np.ndarray

@@ -30,7 +30,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, aniso=False):
     import sys
     from pathlib import Path
     sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -42,7 +42,7 @@ def _worker(rank, world, port, out):
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    gm = scenes.make_map(0, n=600) if rank == 0 else None
+    gm = scenes.make_map(0, n=600, aniso=aniso) if rank == 0 else None
     gm = sd.broadcast_map(gm)
     cam = CameraModel(48, 30, 0, 0, 30.0, 30.0, 24.0, 15.0)
     cands = scenes.make_candidates(0, 7)
@@ -52,19 +52,22 @@ def _worker(rank, world, port, out):
     nm_all, es_all = sd.gather_scores(len(cands), nm, es)
     _, _, _, tot = orc.combine_scores(nm_all, es_all, [c.position for c in cands], [2.0, 1.5, 2.0])
     out[rank] = (gm.centers.tobytes(), gm.sem_indices.tobytes(), nm_all.tobytes(),
-                 es_all.tobytes(), int(np.argmax(tot)))
+                 es_all.tobytes(), int(np.argmax(tot)),
+                 None if gm.log_scales is None else (gm.log_scales.tobytes() + gm.quats.tobytes()))
     dist.destroy_process_group()
 
 
-def test_two_rank_gloo_broadcast_shard_gather(orc):
+@pytest.mark.parametrize("aniso", [False, True])
+def test_two_rank_gloo_broadcast_shard_gather(orc, aniso):
     from paper_2506_00225_b200 import scenes
     from paper_2506_00225_b200.splatmap import CameraModel
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), out, aniso), nprocs=2, join=True)
     a, b = out[0], out[1]
     assert a == b  # identical map, identical gathered scores, identical argmax on every rank
-    gm = scenes.make_map(0, n=600)
+    gm = scenes.make_map(0, n=600, aniso=aniso)
+    assert (a[5] is not None) == aniso
     assert a[0] == gm.centers.tobytes()
     cam = CameraModel(48, 30, 0, 0, 30.0, 30.0, 24.0, 15.0)
     cands = scenes.make_candidates(0, 7)

@@ -308,3 +308,46 @@ def test_fronto_parallel_plane_long_depth_run(ctx, orc):
     nm_o, es_o, _ = orc.score_views(gm, cam, [Pose()])
     assert nm[0] == nm_o[0]
     np.testing.assert_allclose(es, es_o, rtol=ENT_RTOL)
+
+
+def test_cfg3_full_size_vs_oracle(ctx, orc):
+    """Config 3 at full size (2M Gaussians, k=8 of 42 channels, 1920x1080): two candidate
+    views against the oracle, plus the batched == one-by-one property."""
+    gm = scenes.make_map(3)
+    cam = scenes.CONFIGS[3].camera()
+    poses = [c.camera_pose() for c in scenes.make_candidates(3, 2)]
+    nm, es = sgm.score_poses(gm, cam, poses, ctx=ctx)
+    nm_o, es_o, _ = orc.score_views(gm, cam, poses, threads=2)
+    np.testing.assert_array_equal(nm, nm_o)
+    np.testing.assert_allclose(es, es_o, rtol=ENT_RTOL, atol=0)
+    a, b = sgm.score_poses(gm, cam, [poses[1]], ctx=ctx)
+    assert a[0] == nm[1] and b[0] == es[1]
+
+
+def test_cfg4_dense_overlap_vs_oracle(ctx, orc):
+    """Config 4's dense-overlap shape (1 m^3 cube, log-scales N(-2.5, 0.3), opacity
+    sigmoid(N(1, 1)), k=32): long per-tile lists and early-exit divergence. A 60k-Gaussian
+    prefix keeps the oracle's bins in memory; a render checks the planes too."""
+    gm = scenes.make_map(4, n=60_000)
+    cam = scenes.CONFIGS[4].camera()
+    poses = [c.camera_pose() for c in scenes.make_candidates(4, 2)]
+    nm, es = sgm.score_poses(gm, cam, poses, ctx=ctx)
+    nm_o, es_o, st = orc.score_views(gm, cam, poses, threads=2)
+    assert st["pairs"] > 50 * cam.pixel_count() // 64  # > 50 splats per tile on average
+    np.testing.assert_array_equal(nm, nm_o)
+    np.testing.assert_allclose(es, es_o, rtol=ENT_RTOL, atol=0)
+    out = sgm.render(gm, cam, poses[0], RenderChannels.all(), ctx=ctx)
+    assert_planes(out, orc.render(gm, cam, poses[0], 7))
+
+
+def test_wide_image_bins_exact(ctx, orc):
+    """More than 256 bin columns (the row scatter's column blocks span two CTA groups) and
+    more than one 1024-entry segment per tile row: bins bit-exact, planes vs the oracle."""
+    cam = CameraModel(2200, 48, 0, 0, 400.0, 400.0, 1100.0, 24.0)
+    pose = Pose()
+    gm = random_map(41, 5000, cam, pose, k=3, num_classes=5, rad_px=(0.5, 30.0), spread=1.0)
+    opts = RenderOptions()
+    out = sgm.render(gm, cam, pose, RenderChannels.all(), opts, ctx=ctx)
+    assert_projections(out, orc.project(gm, cam, pose, opts))
+    assert_bins(ctx, orc, gm, cam, pose, opts, out)
+    assert_planes(out, orc.render(gm, cam, pose, 7, opts))
