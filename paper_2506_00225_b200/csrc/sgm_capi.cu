@@ -64,7 +64,8 @@ struct DevBuf {
         if (p) cudaFree(p);
         p = nullptr;
         bytes = 0;
-        const size_t b = std::max<size_t>(want, 256);
+        // 1/8 headroom: per-view sizes vary, so exact-size growth would reallocate often
+        const size_t b = std::max<size_t>(want + want / 8, 256);
         cudaError_t e = cudaMalloc(&p, b);
         if (e == cudaSuccess) bytes = b;
         return e;
@@ -297,9 +298,7 @@ void bin_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const CamParams&
     uint2* rranges = ctx->rranges.as<uint2>();
     CK(cudaMemsetAsync(rranges, 0, sizeof(uint2) * o.tiles_y, s));
     launch_ranges(qk.Current(), R, rranges, s);
-    const uint64_t G = row_scatter_segments(R, o.tiles_y);
-    CK(ctx->segs.reserve(sizeof(uint4) * G + 16));
-    CK(ctx->segcnt.reserve(sizeof(uint32_t) * G * o.tiles_x));
+    const uint64_t G = row_scatter_segments(R, o.tiles_y);  // buffers sized per group (run_views)
     launch_row_scatter(qv.Current(), rranges, ranges, o.tiles_x, o.tiles_y, R,
                        ctx->segs.as<uint4>(), reinterpret_cast<uint32_t*>(ctx->segs.as<char>() + sizeof(uint4) * G),
                        ctx->segcnt.as<uint32_t>(), list, s);
@@ -403,6 +402,11 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
             CK(ctx->tkeys_alt.reserve(4 * maxR));
             CK(ctx->tvals_alt.reserve(8 * maxR));
             CK(ctx->rvals.reserve(8 * maxR));
+            // row-scatter segments of the largest view (reserved here, not between the
+            // views' binning launches: a reallocation would synchronise the device)
+            const uint64_t maxG = row_scatter_segments(maxR, o.tiles_y);
+            CK(ctx->segs.reserve(sizeof(uint4) * maxG + 16));
+            CK(ctx->segcnt.reserve(sizeof(uint32_t) * maxG * o.tiles_x));
             // descriptors for the whole group (list offsets known from the counts)
             ViewDesc* hvd = ctx->h_views.as<ViewDesc>();
             uint64_t list_off = 0;

@@ -509,6 +509,41 @@ __global__ void __launch_bounds__(256) k_seg_pass(const unsigned long long* __re
     if (!kWrite && has) cnt[static_cast<size_t>(g) * tiles_x + col] = cur;
 }
 
+// Pass 0 without ballots: a segment's per-column counts from a shared-memory difference
+// array (+1 at x0, -1 at x1 + 1 per entry), prefix-summed over the columns.
+__global__ void __launch_bounds__(256) k_seg_count(const unsigned long long* __restrict__ row_list,
+                                                   const uint4* __restrict__ segs,
+                                                   const uint32_t* __restrict__ nseg, int tiles_x,
+                                                   uint32_t* __restrict__ cnt) {
+    extern __shared__ int sdiff[];  // [tiles_x + 1]
+    const uint32_t g = blockIdx.x;
+    if (g >= *nseg) return;
+    const uint4 sg = segs[g];
+    for (int c = threadIdx.x; c <= tiles_x; c += blockDim.x) sdiff[c] = 0;
+    __syncthreads();
+    for (uint32_t i = sg.y + threadIdx.x; i < sg.z; i += blockDim.x) {
+        const unsigned long long e = row_list[i];
+        atomicAdd(&sdiff[(e >> 16) & 0xffffu], 1);
+        atomicAdd(&sdiff[(e & 0xffffu) + 1], -1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // one warp: running prefix over the columns, 32 at a time
+        int carry = 0;
+        for (int c0 = 0; c0 < tiles_x; c0 += 32) {
+            const int c = c0 + threadIdx.x;
+            int v = c < tiles_x ? sdiff[c] : 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, v, off);
+                if (static_cast<int>(threadIdx.x) >= off) v += u;
+            }
+            v += carry;
+            if (c < tiles_x) cnt[static_cast<size_t>(g) * tiles_x + c] = static_cast<uint32_t>(v);
+            carry = __shfl_sync(0xffffffffu, v, 31);
+        }
+    }
+}
+
 // per (row, column): exclusive scan of the segment counts over the row's segments, offset by
 // the tile's list start
 __global__ void k_seg_scan(const uint4* __restrict__ segs, const uint32_t* __restrict__ nseg,
@@ -706,7 +741,8 @@ void launch_row_scatter(const unsigned long long* row_list, const uint2* row_ran
     const int blocks = (tiles_x + 31) / 32;  // 32-column blocks, one warp each
     const int warps = std::min(8, blocks);
     const dim3 grid(static_cast<unsigned>(gmax), static_cast<unsigned>((blocks + warps - 1) / warps));
-    k_seg_pass<false><<<grid, 32 * warps, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list);
+    k_seg_count<<<static_cast<unsigned>(gmax), 256, sizeof(int) * (tiles_x + 1), s>>>(
+        row_list, segs, nseg, tiles_x, cnt);
     k_seg_scan<<<blocks_for(static_cast<uint64_t>(tiles_x) * tiles_y, 256), 256, 0, s>>>(
         segs, nseg, tile_ranges, tiles_x, tiles_y, cnt);
     k_seg_pass<true><<<grid, 32 * warps, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list);

@@ -17,7 +17,7 @@ ctx = Context(0)
 gm = scenes.make_map(a.config)
 cam = scenes.CONFIGS[a.config].camera()
 poses = [c.camera_pose() for c in scenes.make_candidates(a.config, a.views)]
-score_poses(gm, cam, poses[:8], ctx=ctx)
+score_poses(gm, cam, poses, ctx=ctx)  # warm-up: buffers at steady-state size
 ctx.set_profiling(True)
 ctx.reset_stats()
 ctx.synchronize()
