@@ -115,7 +115,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     const uint2 rg = vd.ranges[bin];
     const uint32_t L0 = rg.x;
     const uint32_t Ln = rg.y - rg.x;
-    const int nbatch = static_cast<int>((Ln + kNB - 1) / kNB);
     const bool want_sem = !kRender || vd.sem != nullptr;
     const int g = warp;  // phase C / epilogue channel group
     const int c0 = g * Cg, c1 = min(C, c0 + Cg);
@@ -129,9 +128,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     // ---- cp.async pipeline over batches of kNB Gaussians (depth-rank order) ----
     const int qi = kpad / 8, qp = kpad / 2;
     const int Q = 5 + qi + qp + (kRender ? 2 : 0);  // 16-byte chunks per Gaussian
+    __shared__ int scnt[3];  // entries of batch b in scnt[b % 3]
     auto issue = [&](int b) {
         unsigned char* sb = stg + (b & 1) * L.stage_bytes;
-        const int n = min(kNB, static_cast<int>(Ln) - b * kNB);
+        const int n = scnt[b % 3];
         const uint2* slot = rm + (b & 1) * kNB;
         for (int c = t; c < n * Q; c += kThreads) {
             const int e = c / Q;
@@ -160,20 +160,54 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
         }
         cp_async_commit();
     };
-    auto fetch_rm = [&](int b, int slot) {
-        if (t < kNB) {
-            const uint32_t q = static_cast<uint32_t>(b) * kNB + t;
+    // Batches are formed by warp 0 two ahead: the next kNB entries of the bin (depth
+    // order) that can reach a pixel of this block. An entry whose float probe circle
+    // (:276-278) misses the box of the block's pixel centres by a relative margin above
+    // the probe's rounding cannot pass the prefilter at any pixel, so skipping it changes
+    // nothing; about a fifth of the bin entries are such corner entries of the square
+    // tile rectangle (:205-209). (The anisotropic mode has no float probe: no skipping.)
+    const float bx0 = static_cast<float>(bx * kTile) + 0.5f, bx1 = bx0 + static_cast<float>(kTile - 1);
+    const float by0 = static_cast<float>(by * kTile) + 0.5f, by1 = by0 + static_cast<float>(kTile - 1);
+    uint32_t cursor = 0;  // warp 0: next bin entry to examine
+    auto fill = [&](int b) {
+        if (warp != 0) return;
+        uint2* slot = rm + (b & 1) * kNB;
+        int filled = 0;
+        while (filled < kNB && cursor < Ln) {
+            const uint32_t q = cursor + lane;
+            bool keep = false;
+            uint32_t r = 0;
             if (q < Ln) {
-                const uint32_t r = vd.list[L0 + q];
-                rm[slot * kNB + t] = make_uint2(r, vd.order[r]);
+                r = vd.list[L0 + q];
+                keep = true;
+                if (!kAniso) {
+                    const float4 pf = *reinterpret_cast<const float4*>(&vd.packed[r].pmx);
+                    const double ex = fmax(fmax(static_cast<double>(bx0) - pf.x, 0.0),
+                                           static_cast<double>(pf.x) - bx1);
+                    const double ey = fmax(fmax(static_cast<double>(by0) - pf.y, 0.0),
+                                           static_cast<double>(pf.y) - by1);
+                    keep = !((ex * ex + ey * ey) * (1.0 - 1e-6) > static_cast<double>(pf.z));
+                }
             }
+            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+            const int need = kNB - filled;
+            const int avail = __popc(bal);
+            // entries consumed: through the need-th kept one, else the whole window
+            const uint32_t window = min(32u, Ln - cursor);
+            const int rank = __popc(bal & ((1u << lane) - 1u));
+            const uint32_t lastk = __ballot_sync(0xffffffffu, keep && rank == need - 1);  // need-th kept
+            const uint32_t used = avail > need ? static_cast<uint32_t>(__ffs(lastk)) : window;
+            if (keep && rank < need) slot[filled + rank] = make_uint2(r, vd.order[r]);
+            filled += min(avail, need);
+            cursor += used;
         }
+        if (lane == 0) scnt[b % 3] = filled;
     };
 
-    fetch_rm(0, 0);
-    fetch_rm(1, 1);
+    fill(0);
+    fill(1);
     __syncthreads();
-    if (nbatch > 0) issue(0);
+    if (scnt[0] > 0) issue(0);
 
     const double dpx = x + 0.5, dpy = y + 0.5;                                 // :261, :263
     const float fpx = static_cast<float>(dpx), fpy = static_cast<float>(dpy);  // :274
@@ -186,18 +220,19 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     const size_t pix_t = inside ? static_cast<size_t>(y) * p.cam.W + x : 0;
     const int e_first = t >> 6;  // phase A: this thread's entries e_first + 4i
 
-    for (int b = 0; b < nbatch; ++b) {
+    for (int b = 0;; ++b) {
         cp_async_wait_all();
         __syncthreads();  // batch b landed; rm slot for b+1 visible; W / bnd free
-        if (b + 1 < nbatch) issue(b + 1);
-        if (b + 2 < nbatch) fetch_rm(b + 2, b & 1);
+        const int n = scnt[b % 3];
+        if (n == 0) break;  // the bin is exhausted
+        if (scnt[(b + 1) % 3] > 0) issue(b + 1);
+        fill(b + 2);  // rm slot b & 1 (batch b was issued last iteration), scnt[(b + 2) % 3]
         const unsigned char* sb = stg + (b & 1) * L.stage_bytes;
         const PackedSplat* sp = reinterpret_cast<const PackedSplat*>(sb + L.st_packed);
         const uint16_t* sbnd = reinterpret_cast<const uint16_t*>(sb + L.st_bnd);  // [kNB][8]
         const uint16_t* si = reinterpret_cast<const uint16_t*>(sb + L.st_idx);
         const double* spr = reinterpret_cast<const double*>(sb + L.st_prob);
         const double* scol = reinterpret_cast<const double*>(sb + L.st_color);
-        const int n = min(kNB, static_cast<int>(Ln) - b * kNB);
 
         // ---- phase A: footprints (independent of T) ----
         {
