@@ -187,7 +187,6 @@ __global__ void __launch_bounds__(kBThreads, 2) k_backward(RasterParams p, Backw
     const uint2 rg = vd.ranges[bin];
     const uint32_t L0 = rg.x;
     const uint32_t Ln = rg.y - rg.x;
-    const int nbatch = static_cast<int>((Ln + kBNB - 1) / kBNB);
     const double dpx = x + 0.5, dpy = y + 0.5;
     const float fpx = static_cast<float>(dpx), fpy = static_cast<float>(dpy);
     const int e_first = t >> 6;
@@ -264,9 +263,10 @@ __global__ void __launch_bounds__(kBThreads, 2) k_backward(RasterParams p, Backw
     constexpr int Qc = 4 + 2;  // PackedSplat + colour (16-byte chunks); rows copied separately
     const int qi = kpad / 8, qp = kpad / 2;
     const int Q = Qc + qi + qp;
+    __shared__ int scnt[3];  // entries of batch bb in scnt[bb % 3]
     auto issue = [&](int bb) {
         unsigned char* sb = stg + (bb & 1) * L.stage_bytes;
-        const int n = min(kBNB, static_cast<int>(Ln) - bb * kBNB);
+        const int n = scnt[bb % 3];
         const uint2* slot = rm + (bb & 1) * kBNB;
         for (int c = t; c < n * Q; c += kBThreads) {
             const int e = c / Q;
@@ -294,33 +294,35 @@ __global__ void __launch_bounds__(kBThreads, 2) k_backward(RasterParams p, Backw
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    auto fetch_rm = [&](int bb, int slot) {
-        if (t < kBNB) {
-            const uint32_t q = static_cast<uint32_t>(bb) * kBNB + t;
-            if (q < Ln) {
-                const uint32_t r = vd.list[L0 + q];
-                rm[slot * kBNB + t] = make_uint2(r, vd.order[r]);
-            }
-        }
+    // batches skip bin entries that cannot reach a pixel of the block (fill_batch)
+    const float bx0 = static_cast<float>(bx * kTile) + 0.5f, bx1 = bx0 + static_cast<float>(kTile - 1);
+    const float by0 = static_cast<float>(by * kTile) + 0.5f, by1 = by0 + static_cast<float>(kTile - 1);
+    uint32_t cursor = 0;
+    auto fill = [&](int bb) {
+        if ((t >> 5) != 0) return;
+        const int filled = fill_batch<kBNB>(vd, L0, Ln, cursor, rm + (bb & 1) * kBNB, true, bx0, bx1,
+                                            by0, by1, lane);
+        if (lane == 0) scnt[bb % 3] = filled;
     };
 
-    fetch_rm(0, 0);
-    fetch_rm(1, 1);
+    fill(0);
+    fill(1);
     __syncthreads();
-    if (nbatch > 0) issue(0);
+    if (scnt[0] > 0) issue(0);
     double T = 1.0, Pc[4] = {0.0, 0.0, 0.0, 0.0};
     bool done = t < kTilePx ? sdone[t] != 0 : true;
-    for (int bb = 0; bb < nbatch; ++bb) {
+    for (int bb = 0;; ++bb) {
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
-        if (bb + 1 < nbatch) issue(bb + 1);
-        if (bb + 2 < nbatch) fetch_rm(bb + 2, bb & 1);
+        const int n = scnt[bb % 3];
+        if (n == 0) break;  // the bin is exhausted
+        if (scnt[(bb + 1) % 3] > 0) issue(bb + 1);
+        fill(bb + 2);
         const unsigned char* sb = stg + (bb & 1) * L.stage_bytes;
         const PackedSplat* sp = reinterpret_cast<const PackedSplat*>(sb);
         const double* scol = reinterpret_cast<const double*>(sb + L.st_color);
         const uint16_t* si = reinterpret_cast<const uint16_t*>(sb + L.st_idx);
         const uint32_t* em = emap + (bb & 1) * kBNB;
-        const int n = min(kBNB, static_cast<int>(Ln) - bb * kBNB);
 
         // phase A: footprints (:242-257), clamp recorded
         {

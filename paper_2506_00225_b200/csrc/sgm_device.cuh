@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "sgm_internal.h"
+
 namespace sgm {
 namespace {
 
@@ -81,6 +83,46 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
 }
+// Forms one batch of up to kB bin entries (depth order) for an 8x8 pixel block: called by
+// all 32 lanes of one warp; `cursor` (the next bin entry to examine, same in every lane)
+// advances past the consumed entries; slot[i] = (depth rank, map index). With `skip`, an
+// entry whose float probe circle (splat_render.cpp:276-278) misses the box of the block's
+// pixel centres [bx0, bx1] x [by0, by1] by a relative margin above the probe's fp32
+// rounding is passed over: it cannot pass the prefilter at any pixel, so the composite is
+// unchanged. Returns the number of entries placed.
+template <int kB>
+__device__ __forceinline__ int fill_batch(const ViewDesc& vd, uint32_t L0, uint32_t Ln,
+                                          uint32_t& cursor, uint2* slot, bool skip, float bx0,
+                                          float bx1, float by0, float by1, int lane) {
+    int filled = 0;
+    while (filled < kB && cursor < Ln) {
+        const uint32_t q = cursor + lane;
+        bool keep = false;
+        uint32_t r = 0;
+        if (q < Ln) {
+            r = vd.list[L0 + q];
+            keep = true;
+            if (skip) {
+                const float4 pf = *reinterpret_cast<const float4*>(&vd.packed[r].pmx);
+                const double ex = fmax(fmax(static_cast<double>(bx0) - pf.x, 0.0), static_cast<double>(pf.x) - bx1);
+                const double ey = fmax(fmax(static_cast<double>(by0) - pf.y, 0.0), static_cast<double>(pf.y) - by1);
+                keep = !((ex * ex + ey * ey) * (1.0 - 1e-6) > static_cast<double>(pf.z));
+            }
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        const int need = kB - filled;
+        const int avail = __popc(bal);
+        const int rank = __popc(bal & ((1u << lane) - 1u));
+        // entries consumed: through the need-th kept one, else the whole window
+        const uint32_t lastk = __ballot_sync(0xffffffffu, keep && rank == need - 1);
+        const uint32_t used = avail > need ? static_cast<uint32_t>(__ffs(lastk)) : min(32u, Ln - cursor);
+        if (keep && rank < need) slot[filled + rank] = make_uint2(r, vd.order[r]);
+        filled += min(avail, need);
+        cursor += used;
+    }
+    return filled;
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 

@@ -81,15 +81,15 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
     const uint2 rg = vd.ranges[bin];
     const uint32_t L0 = rg.x;
     const uint32_t Ln = rg.y - rg.x;
-    const int nbatch = static_cast<int>((Ln + kFNB - 1) / kFNB);
     const double dpx = x + 0.5, dpy = y + 0.5;
     const float fpx = static_cast<float>(dpx), fpy = static_cast<float>(dpy);
     const int e_first = t >> 6;
 
     constexpr int Q = 4 + 2;  // 16-byte chunks per Gaussian: PackedSplat + colour
+    __shared__ int scnt[3];  // entries of batch b in scnt[b % 3]
     auto issue = [&](int b) {
         unsigned char* sb = stg + (b & 1) * L.stage_bytes;
-        const int n = min(kFNB, static_cast<int>(Ln) - b * kFNB);
+        const int n = scnt[b % 3];
         const uint2* slot = rm + (b & 1) * kFNB;
         for (int c = t; c < n * Q; c += kFThreads) {
             const int e = c / Q;
@@ -110,14 +110,16 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    auto fetch_rm = [&](int b, int slot) {
-        if (t < kFNB) {
-            const uint32_t q = static_cast<uint32_t>(b) * kFNB + t;
-            if (q < Ln) {
-                const uint32_t r = vd.list[L0 + q];
-                rm[slot * kFNB + t] = make_uint2(r, vd.order[r]);
-            }
-        }
+    // batches skip bin entries that cannot reach a pixel of the block (fill_batch)
+    const float bx0 = static_cast<float>(bx * kTile) + 0.5f, bx1 = bx0 + static_cast<float>(kTile - 1);
+    const float by0 = static_cast<float>(by * kTile) + 0.5f, by1 = by0 + static_cast<float>(kTile - 1);
+    const int fwarp = t >> 5;
+    uint32_t cursor = 0;
+    auto fill = [&](int b) {
+        if (fwarp != 0) return;
+        const int filled = fill_batch<kFNB>(vd, L0, Ln, cursor, rm + (b & 1) * kFNB, true, bx0, bx1,
+                                            by0, by1, lane);
+        if (lane == 0) scnt[b % 3] = filled;
     };
 
     if (t < 9) sR[t] = vd.pose->Rcw[t];
@@ -130,20 +132,22 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
         bool done = !inside;
         if (t < kTilePx) sdone[t] = inside ? 0 : 1;
         __syncthreads();
-        fetch_rm(0, 0);
-        fetch_rm(1, 1);
+        cursor = 0;
+        fill(0);
+        fill(1);
         __syncthreads();
-        if (nbatch > 0) issue(0);
-        for (int b = 0; b < nbatch; ++b) {
+        if (scnt[0] > 0) issue(0);
+        for (int b = 0;; ++b) {
             asm volatile("cp.async.wait_all;\n" ::: "memory");
             __syncthreads();
-            if (b + 1 < nbatch) issue(b + 1);
-            if (b + 2 < nbatch) fetch_rm(b + 2, b & 1);
+            const int n = scnt[b % 3];
+            if (n == 0) break;  // the bin is exhausted
+            if (scnt[(b + 1) % 3] > 0) issue(b + 1);
+            fill(b + 2);
             const unsigned char* sb = stg + (b & 1) * L.stage_bytes;
             const PackedSplat* sp = reinterpret_cast<const PackedSplat*>(sb);
             const double* scol = reinterpret_cast<const double*>(sb + L.st_color);
             const uint32_t* em = emap + (b & 1) * kFNB;
-            const int n = min(kFNB, static_cast<int>(Ln) - b * kFNB);
 
             // phase A: raw footprints (splat_render.cpp:276-285), clamp recorded
             {

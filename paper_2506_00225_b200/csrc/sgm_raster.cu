@@ -171,36 +171,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     uint32_t cursor = 0;  // warp 0: next bin entry to examine
     auto fill = [&](int b) {
         if (warp != 0) return;
-        uint2* slot = rm + (b & 1) * kNB;
-        int filled = 0;
-        while (filled < kNB && cursor < Ln) {
-            const uint32_t q = cursor + lane;
-            bool keep = false;
-            uint32_t r = 0;
-            if (q < Ln) {
-                r = vd.list[L0 + q];
-                keep = true;
-                if (!kAniso) {
-                    const float4 pf = *reinterpret_cast<const float4*>(&vd.packed[r].pmx);
-                    const double ex = fmax(fmax(static_cast<double>(bx0) - pf.x, 0.0),
-                                           static_cast<double>(pf.x) - bx1);
-                    const double ey = fmax(fmax(static_cast<double>(by0) - pf.y, 0.0),
-                                           static_cast<double>(pf.y) - by1);
-                    keep = !((ex * ex + ey * ey) * (1.0 - 1e-6) > static_cast<double>(pf.z));
-                }
-            }
-            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-            const int need = kNB - filled;
-            const int avail = __popc(bal);
-            // entries consumed: through the need-th kept one, else the whole window
-            const uint32_t window = min(32u, Ln - cursor);
-            const int rank = __popc(bal & ((1u << lane) - 1u));
-            const uint32_t lastk = __ballot_sync(0xffffffffu, keep && rank == need - 1);  // need-th kept
-            const uint32_t used = avail > need ? static_cast<uint32_t>(__ffs(lastk)) : window;
-            if (keep && rank < need) slot[filled + rank] = make_uint2(r, vd.order[r]);
-            filled += min(avail, need);
-            cursor += used;
-        }
+        const int filled = fill_batch<kNB>(vd, L0, Ln, cursor, rm + (b & 1) * kNB, !kAniso, bx0, bx1,
+                                           by0, by1, lane);
         if (lane == 0) scnt[b % 3] = filled;
     };
 
