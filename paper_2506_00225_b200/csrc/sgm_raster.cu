@@ -192,9 +192,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     const size_t pix_t = inside ? static_cast<size_t>(y) * p.cam.W + x : 0;
     const int e_first = t >> 6;  // phase A: this thread's entries e_first + 4i
 
+    int mine = 0;  // this thread's vote that its pixel is done (the block stops when all are)
     for (int b = 0;; ++b) {
         cp_async_wait_all();
-        __syncthreads();  // batch b landed; rm slot for b+1 visible; W / bnd free
+        // batch b landed; rm slot for b+1 visible; W / bnd free; and the early termination
+        // of the whole block (:312 for every pixel) decided on the previous batch's votes
+        if (__syncthreads_and(mine)) break;
         const int n = scnt[b % 3];
         if (n == 0) break;  // the bin is exhausted
         if (scnt[(b + 1) % 3] > 0) issue(b + 1);
@@ -206,48 +209,51 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
         const double* spr = reinterpret_cast<const double*>(sb + L.st_prob);
         const double* scol = reinterpret_cast<const double*>(sb + L.st_color);
 
-        // ---- phase A: footprints (independent of T) ----
-        {
-            const bool pdone = sdone[px] != 0;
-#pragma unroll
-            for (int i = 0; i < kNB / 4; ++i) {
-                const int e = e_first + 4 * i;
-                if (e >= n) break;
-                double f = -1.0;  // not a contributor
-                if (kAniso && !pdone) {
-                    // f4 (no reference): f = alpha exp(-q / 2), q = d^T Sigma2D^-1 d, cut at
-                    // q > trunc^2 -- the order of oracle/sgm_oracle.c composite()
-                    const PackedSplatA& a = reinterpret_cast<const PackedSplatA&>(sp[e]);
-                    const double dx = dpx - a.mx;
-                    const double dy = dpy - a.my;
-                    const double q = (a.qa * (dx * dx) + (2.0 * a.qb) * (dx * dy)) + a.qc * (dy * dy);
-                    if (!(q > p.opt.cut_sq)) {
-                        f = a.alpha * exp_footprint(-0.5 * q);
-                        if (f > kMaxFootprint) f = kMaxFootprint;
-                    }
-                } else if (!pdone) {
-                    const float4 pf = *reinterpret_cast<const float4*>(&sp[e].pmx);
-                    const float fdx = fpx - pf.x;
-                    const float fdy = fpy - pf.y;
-                    if (!(fdx * fdx + fdy * fdy > pf.z)) {  // :276-278
-                        const double dx = dpx - sp[e].mx;
-                        const double dy = dpy - sp[e].my;
-                        const double d2 = dx * dx + dy * dy;
-                        if (!(d2 > sp[e].cutoff_d2)) {  // :283
-                            f = sp[e].alpha * exp_footprint(-d2 * sp[e].inv_two_r2);  // :284
-                            if (f > kMaxFootprint) f = kMaxFootprint;                 // :285
-                        }
+        // footprint of entry e at this thread's pixel (:276-285); -1 = not a contributor
+        auto footprint = [&](int e) -> double {
+            double f = -1.0;
+            if (kAniso) {
+                // f4 (no reference): f = alpha exp(-q / 2), q = d^T Sigma2D^-1 d, cut at
+                // q > trunc^2 -- the order of oracle/sgm_oracle.c composite()
+                const PackedSplatA& a = reinterpret_cast<const PackedSplatA&>(sp[e]);
+                const double dx = dpx - a.mx;
+                const double dy = dpy - a.my;
+                const double q = (a.qa * (dx * dx) + (2.0 * a.qb) * (dx * dy)) + a.qc * (dy * dy);
+                if (!(q > p.opt.cut_sq)) {
+                    f = a.alpha * exp_footprint(-0.5 * q);
+                    if (f > kMaxFootprint) f = kMaxFootprint;
+                }
+            } else {
+                const float4 pf = *reinterpret_cast<const float4*>(&sp[e].pmx);
+                const float fdx = fpx - pf.x;
+                const float fdy = fpy - pf.y;
+                if (!(fdx * fdx + fdy * fdy > pf.z)) {  // :276-278
+                    const double dx = dpx - sp[e].mx;
+                    const double dy = dpy - sp[e].my;
+                    const double d2 = dx * dx + dy * dy;
+                    if (!(d2 > sp[e].cutoff_d2)) {  // :283
+                        f = sp[e].alpha * exp_footprint(-d2 * sp[e].inv_two_r2);  // :284
+                        if (f > kMaxFootprint) f = kMaxFootprint;                 // :285
                     }
                 }
-                W[pair_slot(e, 32, px)] = f;
             }
-        }
-        __syncthreads();
+            return f;
+        };
 
-        // ---- phase B: transmittance chain (:286-312) ----
         if (kRender) {
-            // render: sequential per pixel (warps 0-1): colour/depth and the ordered
-            // contributor lists of retain_contributors
+            // ---- phase A: footprints (independent of T) ----
+            {
+                const bool pdone = sdone[px] != 0;
+#pragma unroll
+                for (int i = 0; i < kNB / 4; ++i) {
+                    const int e = e_first + 4 * i;
+                    if (e >= n) break;
+                    W[pair_slot(e, 32, px)] = pdone ? -1.0 : footprint(e);
+                }
+            }
+            __syncthreads();
+            // ---- phase B: transmittance chain (:286-312), sequential per pixel (warps 0-1):
+            // colour/depth and the ordered contributor lists of retain_contributors ----
             if (t < kTilePx) {
                 for (int e = 0; e < n; ++e) {
                     const int s = pair_slot(e, 32, t);
@@ -275,39 +281,45 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
                 sdone[t] = done ? 1 : 0;
             }
         } else {
-            // score: all 8 warps, 4 threads per pixel, 4 entries each. A segment starts at
-            // T_pixel * prod(earlier segments' (1 - f)) (fixed association); since T only
-            // decreases, a segment starting below eps lies after the early exit (:312).
+            // ---- score: footprints and transmittance fused. Thread (part, px) owns the
+            // contiguous entries 4 part .. 4 part + 3 of pixel px (warp-uniform entries). A
+            // segment starts at T_pixel * prod(earlier segments' (1 - f)) (fixed association);
+            // since T only decreases, a segment starting below eps lies after the early exit
+            // (:312). The pixel's T and done flag are read before the barrier and written
+            // (by part 3) after it. ----
             const int part = t >> 6;
-            const int eb = 4 * part, ee = min(n, eb + 4);
             const bool pdone = sdone[px] != 0;
+            const double T0 = sT[px];
+            double f[4];
             double prod = 1.0;
-            if (!pdone)
-                for (int e = eb; e < ee; ++e) {
-                    const double f = W[pair_slot(e, 32, px)];
-                    if (f >= 0.0) prod = prod * (1.0 - f);
-                }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int e = 4 * part + i;
+                f[i] = (e < n && !pdone) ? footprint(e) : -1.0;
+                if (f[i] >= 0.0) prod = prod * (1.0 - f[i]);
+            }
             segp[part * kTilePx + px] = prod;
             __syncthreads();
-            double Ts = sT[px];
+            double Ts = T0;
 #pragma unroll
             for (int q = 0; q < 3; ++q)
                 if (q < part) Ts = Ts * segp[q * kTilePx + px];
             bool exited = pdone || (p.opt.early_exit && Ts < p.opt.eps);
             double Tc = Ts;
-            for (int e = eb; e < ee; ++e) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int e = 4 * part + i;
+                if (e >= n) break;
                 const int s = pair_slot(e, 32, px);
-                const double f = W[s];
-                if (exited || f < 0.0) {
+                if (exited || f[i] < 0.0) {
                     W[s] = 0.0;
                     continue;
                 }
-                W[s] = f * Tc;
+                W[s] = f[i] * Tc;
                 ++contrib;
-                Tc = Tc * (1.0 - f);
+                Tc = Tc * (1.0 - f[i]);
                 if (p.opt.early_exit && Tc < p.opt.eps) exited = true;
             }
-            __syncthreads();  // all segments read sT / segp
             if (part == 3) {
                 sT[px] = Tc;  // product over the batch (only its == 1 / < eps matter later)
                 sdone[px] = (pdone || (p.opt.early_exit && Tc < p.opt.eps)) ? 1 : 0;
@@ -358,9 +370,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
                 }
             }
         }
-        // early termination of the whole block (:312 for every pixel)
-        const int mine = kRender ? ((t < kTilePx) ? (done ? 1 : 0) : 1) : sdone[px];
-        if (__syncthreads_and(mine)) break;
+        mine = kRender ? ((t < kTilePx) ? (done ? 1 : 0) : 1) : sdone[px];
     }
     cp_async_wait_all();
     __syncthreads();
