@@ -192,6 +192,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     const size_t pix_t = inside ? static_cast<size_t>(y) * p.cam.W + x : 0;
     const int e_first = t >> 6;  // phase A: this thread's entries e_first + 4i
 
+    __shared__ uint32_t slive[2];  // batch b: entries with a nonzero weight at some pixel
+    if (t < 2) slive[t] = 0u;
     int mine = 0;  // this thread's vote that its pixel is done (the block stops when all are)
     for (int b = 0;; ++b) {
         cp_async_wait_all();
@@ -200,6 +202,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
         if (__syncthreads_and(mine)) break;
         const int n = scnt[b % 3];
         if (n == 0) break;  // the bin is exhausted
+        if (t == 0) slive[(b + 1) & 1] = 0u;  // last read by phase C of batch b - 1
         if (scnt[(b + 1) % 3] > 0) issue(b + 1);
         fill(b + 2);  // rm slot b & 1 (batch b was issued last iteration), scnt[(b + 2) % 3]
         const unsigned char* sb = stg + (b & 1) * L.stage_bytes;
@@ -240,6 +243,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
             return f;
         };
 
+        uint32_t nzbits = 0;  // entries this thread gave a nonzero weight
         if (kRender) {
             // ---- phase A: footprints (independent of T) ----
             {
@@ -277,6 +281,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
                     T = T * (1.0 - f);                        // :311
                     if (p.opt.early_exit && T < p.opt.eps)   // :312
                         done = true;
+                    if (w != 0.0) nzbits |= 1u << e;
                 }
                 sdone[t] = done ? 1 : 0;
             }
@@ -316,6 +321,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
                     continue;
                 }
                 W[s] = f[i] * Tc;
+                if (W[s] != 0.0) nzbits |= 1u << e;
                 ++contrib;
                 Tc = Tc * (1.0 - f[i]);
                 if (p.opt.early_exit && Tc < p.opt.eps) exited = true;
@@ -325,15 +331,25 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
                 sdone[px] = (pdone || (p.opt.early_exit && Tc < p.opt.eps)) ? 1 : 0;
             }
         }
+        {
+            const uint32_t lv = __reduce_or_sync(0xffffffffu, nzbits);
+            if (lane == 0 && lv) atomicOr(&slive[b & 1], lv);
+        }
         __syncthreads();
 
         // ---- phase C: sparse semantic scatter; warp g = channel group g, 64 px ----
         if (want_sem) {
             double2* accl = acc2 + lane;
-            for (int e = 0; e < n; ++e) {
+            // the live entries (some pixel weighted) with classes in this warp's group, in
+            // depth order (lane l tests entry l)
+            const int glo = (lane < n && g > 0) ? sbnd[lane * 8 + g - 1] : 0;
+            const int ghi = lane < n ? sbnd[lane * 8 + g] : 0;
+            uint32_t todo = __ballot_sync(0xffffffffu, ghi > glo) & slive[b & 1];
+            while (todo) {
+                const int e = __ffs(todo) - 1;
+                todo &= todo - 1u;
                 const double2 w = W2[e * 32 + lane];
                 const bool nz = (w.x != 0.0) | (w.y != 0.0);
-                if (!__any_sync(0xffffffffu, nz)) continue;
                 const int lo = g == 0 ? 0 : sbnd[e * 8 + g - 1], hi = sbnd[e * 8 + g];
                 const uint16_t* ei = si + e * kpad;
                 const double* ep = spr + e * kpad;
