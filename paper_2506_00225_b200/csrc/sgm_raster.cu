@@ -83,6 +83,14 @@ __device__ __forceinline__ int pair_slot(int row, int pitch2, int q) {
     return row * pitch2 * 2 + q;
 }
 
+// Tile-local pixel index q -> (column, row) in the 8x8 block: q / 16 selects a 4x4
+// quadrant, so a quarter-warp (lanes 8j .. 8j+7, pixels 16j .. 16j+15) covers a compact
+// 4x4 square: a Gaussian's disc leaves more quarter-warps without weight (and their
+// shared-memory wavefronts skipped) than with row pairs. Horizontal pairs (2l, 2l+1) stay
+// adjacent.
+__device__ __forceinline__ int px_col(int q) { return ((q >> 4) & 1) * 4 + (q & 3); }
+__device__ __forceinline__ int px_row(int q) { return (q >> 5) * 4 + ((q >> 2) & 3); }
+
 template <bool kRender, bool kDup, bool kAniso>
 __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -108,8 +116,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
     const int px = t & (kTilePx - 1);  // this thread's pixel in phase A / B / epilogues
-    const int x = bx * kTile + (px & (kTile - 1));
-    const int y = by * kTile + px / kTile;
+    const int x = bx * kTile + px_col(px);
+    const int y = by * kTile + px_row(px);
     const bool inside = x < p.cam.W && y < p.cam.H;
     const int bin = ((by * kTile) / p.opt.ts) * p.opt.tiles_x + (bx * kTile) / p.opt.ts;
     const uint2 rg = vd.ranges[bin];
@@ -409,8 +417,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
             for (int l = t; l < kTilePx * C; l += kThreads) {
                 const int q = l / C;
                 const int c = l - q * C;
-                const int qx = bx * kTile + (q & (kTile - 1));
-                const int qy = by * kTile + q / kTile;
+                const int qx = bx * kTile + px_col(q);
+                const int qy = by * kTile + px_row(q);
                 if (qx < p.cam.W && qy < p.cam.H)
                     vd.sem[(static_cast<size_t>(qy) * p.cam.W + qx) * C + c] =
                         acc[pair_slot(c, apitch, q)];
