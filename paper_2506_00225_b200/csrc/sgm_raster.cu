@@ -427,14 +427,22 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     } else {
         // clipped_entropy (:360-369) split by channel group: warp g, pixels 2 lane, 2 lane + 1
         double S1x = 0.0, S2x = 0.0, S1y = 0.0, S2y = 0.0;
+        // a channel below the clamp at all 64 pixels (about a fifth of them) takes the
+        // clamped constant's log once: the same operands, so the same sums
+        const double lclamp = log_table(0.001);
 #pragma unroll 2
         for (int c = c0; c < c1; ++c) {
             const double2 v = acc2[c * apitch + lane];
             const double ax = clamp_prob(v.x), ay = clamp_prob(v.y);
             S1x += ax;
             S1y += ay;
-            S2x = __fma_rn(ax, log_table(ax), S2x);
-            S2y = __fma_rn(ay, log_table(ay), S2y);
+            if (__all_sync(0xffffffffu, ax == 0.001 && ay == 0.001)) {
+                S2x = __fma_rn(0.001, lclamp, S2x);
+                S2y = __fma_rn(0.001, lclamp, S2y);
+            } else {
+                S2x = __fma_rn(ax, log_table(ax), S2x);
+                S2y = __fma_rn(ay, log_table(ay), S2y);
+            }
         }
         red[g * kTilePx + 2 * lane] = make_double2(S1x, S2x);
         red[g * kTilePx + 2 * lane + 1] = make_double2(S1y, S2y);
