@@ -15,6 +15,7 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -1176,46 +1177,43 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, con
         double* col = reinterpret_cast<double*>(hs + geo_b);
         double* rprob = reinterpret_cast<double*>(hs + geo_b + col_b);
         uint16_t* ridx = reinterpret_cast<uint16_t*>(hs + geo_b + col_b + prob_b);
-        // host side (reference libm, gaussian_map.hpp:36-37), split over threads
+        // Host side (reference libm, gaussian_map.hpp:36-37) in kChunks chunks over a pool of
+        // threads; as soon as every thread has finished chunk c, its slices go to the GPU
+        // (async H2D), so the copies overlap the host work on the next chunks.
         const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
         const unsigned nth = n > 65536 ? hw : 1;
+        const unsigned kChunks = n > 65536 ? 8 : 1;
         std::vector<int> bad(nth, -1), dup(nth, 0);
+        std::unique_ptr<std::atomic<unsigned>[]> finished(new std::atomic<unsigned>[kChunks]);
+        for (unsigned c = 0; c < kChunks; ++c) finished[c].store(0);
         auto work = [&](unsigned w) {
-            const uint64_t a = n * w / nth, b = n * (w + 1) / nth;
             std::vector<uint32_t> seen(static_cast<size_t>(C), 0xffffffffu);
-            for (uint64_t i = a; i < b; ++i) {
-                geo[i] = centers[3 * i];
-                geo[ns + i] = centers[3 * i + 1];
-                geo[2 * ns + i] = centers[3 * i + 2];
-                geo[3 * ns + i] = std::exp(log_radii[i]);                      // radius()
-                geo[4 * ns + i] = 1.0 / (1.0 + std::exp(-opacity_logits[i]));  // sigmoid
-                for (int c = 0; c < 3; ++c) col[4 * i + c] = std::clamp(colors[3 * i + c], 0.0, 1.0);
-                col[4 * i + 3] = 0.0;
-                for (int j = 0; j < k; ++j) {
-                    const uint16_t c = sem_indices[i * k + j];
-                    if (c >= C) {
-                        if (bad[w] < 0) bad[w] = static_cast<int>(i % 0x7fffffff);
-                        continue;
+            for (unsigned c = 0; c < kChunks; ++c) {
+                const uint64_t ca = n * c / kChunks, cb = n * (c + 1) / kChunks;
+                const uint64_t a = ca + (cb - ca) * w / nth, b = ca + (cb - ca) * (w + 1) / nth;
+                for (uint64_t i = a; i < b; ++i) {
+                    geo[i] = centers[3 * i];
+                    geo[ns + i] = centers[3 * i + 1];
+                    geo[2 * ns + i] = centers[3 * i + 2];
+                    geo[3 * ns + i] = std::exp(log_radii[i]);                      // radius()
+                    geo[4 * ns + i] = 1.0 / (1.0 + std::exp(-opacity_logits[i]));  // sigmoid
+                    for (int q = 0; q < 3; ++q) col[4 * i + q] = std::clamp(colors[3 * i + q], 0.0, 1.0);
+                    col[4 * i + 3] = 0.0;
+                    for (int j = 0; j < k; ++j) {
+                        const uint16_t cl = sem_indices[i * k + j];
+                        if (cl >= C) {
+                            if (bad[w] < 0) bad[w] = static_cast<int>(i % 0x7fffffff);
+                            continue;
+                        }
+                        if (seen[cl] == static_cast<uint32_t>(i)) dup[w] = 1;
+                        seen[cl] = static_cast<uint32_t>(i);
                     }
-                    if (seen[c] == static_cast<uint32_t>(i)) dup[w] = 1;
-                    seen[c] = static_cast<uint32_t>(i);
                 }
+                std::memcpy(ridx + a * k, sem_indices + a * k, 2 * (b - a) * k);
+                std::memcpy(rprob + a * k, sem_probs + a * k, 8 * (b - a) * k);
+                finished[c].fetch_add(1, std::memory_order_release);
             }
-            std::memcpy(ridx + a * k, sem_indices + a * k, 2 * (b - a) * k);
-            std::memcpy(rprob + a * k, sem_probs + a * k, 8 * (b - a) * k);
         };
-        if (nth == 1) {
-            work(0);
-        } else {
-            std::vector<std::thread> pool;
-            for (unsigned w = 0; w < nth; ++w) pool.emplace_back(work, w);
-            for (auto& th : pool) th.join();
-        }
-        for (unsigned w = 0; w < nth; ++w)
-            if (bad[w] >= 0)
-                fail(SGM_ERR_INVALID, "map: semantic index >= channels %d (near gaussian %d)", C, bad[w]);
-        int has_dup = 0;
-        for (unsigned w = 0; w < nth; ++w) has_dup |= dup[w];
         cudaStream_t s = ctx->stream;
         ctx->take(m->geo, geo_b);
         ctx->take(m->color, col_b);
@@ -1229,10 +1227,37 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, con
         CK(m->perm.reserve(2 * ns * kpad));
         CK(ctx->upload_tmp.reserve(idx_b + prob_b + 64));
         char* draw = ctx->upload_tmp.as<char>();
-        CK(cudaMemcpyAsync(m->geo.p, geo, geo_b, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(m->color.p, col, col_b, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(draw, rprob, prob_b, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(draw + prob_b, ridx, idx_b, cudaMemcpyHostToDevice, s));
+        std::vector<std::thread> pool;
+        for (unsigned w = 1; w < nth; ++w) pool.emplace_back(work, w);
+        std::thread self(work, 0u);
+        cudaError_t copy_err = cudaSuccess;
+        for (unsigned c = 0; c < kChunks; ++c) {
+            while (finished[c].load(std::memory_order_acquire) < nth) std::this_thread::yield();
+            const uint64_t ca = n * c / kChunks, cb = n * (c + 1) / kChunks;
+            if (cb == ca) continue;
+            for (int f = 0; f < 5 && copy_err == cudaSuccess; ++f)
+                copy_err = cudaMemcpyAsync(m->geo.as<double>() + f * ns + ca, geo + f * ns + ca,
+                                           8 * (cb - ca), cudaMemcpyHostToDevice, s);
+            if (copy_err == cudaSuccess)
+                copy_err = cudaMemcpyAsync(m->color.as<double>() + 4 * ca, col + 4 * ca, 32 * (cb - ca),
+                                           cudaMemcpyHostToDevice, s);
+            if (copy_err == cudaSuccess)
+                copy_err = cudaMemcpyAsync(draw + 8 * k * ca, rprob + k * ca, 8 * k * (cb - ca),
+                                           cudaMemcpyHostToDevice, s);
+            if (copy_err == cudaSuccess)
+                copy_err = cudaMemcpyAsync(draw + prob_b + 2 * k * ca, ridx + k * ca, 2 * k * (cb - ca),
+                                           cudaMemcpyHostToDevice, s);
+        }
+        self.join();
+        for (auto& th : pool) th.join();
+        CK(copy_err);
+        for (unsigned w = 0; w < nth; ++w)
+            if (bad[w] >= 0) {
+                cudaStreamSynchronize(s);  // the in-flight copies target this map's buffers
+                fail(SGM_ERR_INVALID, "map: semantic index >= channels %d (near gaussian %d)", C, bad[w]);
+            }
+        int has_dup = 0;
+        for (unsigned w = 0; w < nth; ++w) has_dup |= dup[w];
         // rows sorted by class id (stable) and padded to kpad, on the GPU
         launch_sort_rows(reinterpret_cast<const uint16_t*>(draw + prob_b),
                          reinterpret_cast<const double*>(draw), n, k, kpad, m->idx.as<uint16_t>(),
