@@ -112,3 +112,15 @@ def test_aniso_rejects_fisher_and_bad_quaternions(ctx):
     bad.touch()
     with pytest.raises(RuntimeError, match="quaternion"):
         sgm.render(bad, cam, sgm.Pose(), ctx=ctx)
+
+
+def test_aniso_cfg1_full_size_vs_oracle(ctx, orc):
+    """Config 1 at full size (500k Gaussians, 1200x680) with the drawn per-axis scales and
+    quaternions: two candidate views against the oracle."""
+    gm = scenes.make_map(1, aniso=True)
+    cam = scenes.CONFIGS[1].camera()
+    poses = [c.camera_pose() for c in scenes.make_candidates(1, 2)]
+    nm, es = sgm.score_poses(gm, cam, poses, ctx=ctx)
+    nm_o, es_o, _ = orc.score_views(gm, cam, poses, threads=2)
+    np.testing.assert_array_equal(nm, nm_o)
+    np.testing.assert_allclose(es, es_o, rtol=ENT_RTOL, atol=0)

@@ -351,3 +351,35 @@ def test_wide_image_bins_exact(ctx, orc):
     assert_projections(out, orc.project(gm, cam, pose, opts))
     assert_bins(ctx, orc, gm, cam, pose, opts, out)
     assert_planes(out, orc.render(gm, cam, pose, 7, opts))
+
+
+@pytest.mark.parametrize("seed", range(100, 124))
+def test_randomised_scenes_vs_oracle(ctx, orc, seed):
+    """Seeded random cameras, poses, options and maps (sizes, radii, opacities, k, C, tile
+    size, truncation, early exit): projections and bins bit-exact, planes within the bar,
+    scores exact / within 1e-11."""
+    rng = np.random.default_rng(seed)
+    W, H = int(rng.integers(9, 140)), int(rng.integers(7, 100))
+    f = float(rng.uniform(0.4, 1.6)) * max(W, H)
+    cam = CameraModel(W, H, 0, 0, f, f * float(rng.uniform(0.8, 1.25)),
+                      float(rng.uniform(0.3, 0.7)) * W, float(rng.uniform(0.3, 0.7)) * H)
+    pose = look_at(rng.normal(0, 0.3, 3), [rng.normal(0, 0.3), rng.normal(0, 0.3), 2.5])
+    nc = int(rng.integers(1, 40))
+    k = int(rng.integers(1, min(nc + 1, 20) + 1))
+    gm = random_map(seed, int(rng.integers(1, 700)), cam, pose, k=k, num_classes=nc,
+                    rad_px=(float(rng.uniform(0.2, 2.0)), float(rng.uniform(2.0, 25.0))),
+                    logit=(float(rng.uniform(-6, 0)), float(rng.uniform(0, 8))),
+                    dup=bool(rng.integers(0, 2)) and k >= 2)
+    opts = RenderOptions(early_exit=bool(rng.integers(0, 4)),
+                         transmittance_eps=float(10 ** rng.uniform(-6, -1)),
+                         z_near=float(rng.uniform(0.01, 0.5)),
+                         truncation_sigmas=float(rng.uniform(1.5, 4.0)),
+                         tile_size=int(rng.choice([8, 16, 24])))
+    out = sgm.render(gm, cam, pose, RenderChannels.all(), opts, ctx=ctx)
+    assert_projections(out, orc.project(gm, cam, pose, opts))
+    assert_bins(ctx, orc, gm, cam, pose, opts, out)
+    assert_planes(out, orc.render(gm, cam, pose, 7, opts))
+    nm, es = sgm.score_poses(gm, cam, [pose], options=opts, ctx=ctx)
+    nm_o, es_o, _ = orc.score_views(gm, cam, [pose], opts)
+    assert nm[0] == nm_o[0]
+    np.testing.assert_allclose(es, es_o, rtol=ENT_RTOL, atol=1e-300)
