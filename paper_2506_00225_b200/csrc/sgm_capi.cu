@@ -151,7 +151,7 @@ struct sgm_ctx {
 
     // scratch
     DevBuf poses, vcount, pcount, keys, vals, keys_alt, vals_alt, packed, counts, offsets, rects,
-        bounds, bdiff, rranges, rvals, segs, segcnt;
+        bounds, bdiff, rranges, rvals, segs, segcnt, rcbuf;
     DevBuf tkeys, tvals, tkeys_alt, tvals_alt, ranges, ent_part, miss_part, views, out,
         contributors, cub_tmp, planes, dbg, ccount, coffset, contrib, fis_part, bw_frame,
         bw_flags, bw_part, bw_grad;
@@ -351,7 +351,12 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
     CK(ctx->miss_part.reserve(4ull * rtiles * B));
     CK(ctx->views.reserve(sizeof(ViewDesc) * B));
     CK(ctx->out.reserve(24 * B));
-    if (fk == Fisher::Gain) CK(ctx->fis_part.reserve(8ull * rtiles * B));
+    if (fk == Fisher::Gain) {
+        CK(ctx->fis_part.reserve(8ull * rtiles * B));
+        // rendered colour / depth per view for the gain's Jacobian pass (written by the
+        // score raster, so k_fisher skips its own pass 0)
+        CK(ctx->rcbuf.reserve(32ull * cam.W * cam.H * B));
+    }
     CK(ctx->contributors.reserve(8));
     CK(ctx->h_counts.reserve(32 * B + 16));  // V (u32) | P | R | contributors
     CK(ctx->h_views.reserve(sizeof(ViewDesc) * B));
@@ -431,6 +436,9 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 d.contrib = rt.contrib;
                 d.contrib_count = rt.contrib_count;
                 d.contrib_offset = rt.contrib_offset;
+                d.rc4 = fk == Fisher::Gain
+                            ? ctx->rcbuf.as<double>() + 4ull * cam.W * cam.H * static_cast<size_t>(v)
+                            : nullptr;
                 hvd[v - v0] = d;
                 list_off += P[v];
                 ctx->stats.visible += V[v];
@@ -449,6 +457,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
             rp.raster_tiles_x = rtx;
             rp.channels = rt.channels;
             rp.groups = map->groups;
+            rp.want_rc = fk == Fisher::Gain ? 1 : 0;
             for (int s0 = v0; s0 < v1; s0 += kSub) {
                 const int s1 = std::min(v1, s0 + kSub);
                 for (int v = s0; v < s1; ++v) {

@@ -124,9 +124,17 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
 
     if (t < 9) sR[t] = vd.pose->Rcw[t];
     double Rc[4] = {0.0, 0.0, 0.0, 0.0};  // pass 0 result (threads t < 64)
+    // gain mode after a score raster that wrote the rendered colour / depth planes (rc4):
+    // pass 0 is skipped (the planes are the same sums, in a fixed segment order)
+    const bool haveR = kGain && vd.rc4 != nullptr;
+    if (haveR && t < kTilePx && inside) {
+        const size_t pix = static_cast<size_t>(y) * p.cam.W + x;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) Rc[ch] = vd.rc4[pix * 4 + ch];
+    }
     double gsum = 0.0;                     // gain of this tile (thread 0, fixed order)
 
-    for (int pass = 0; pass < 2; ++pass) {
+    for (int pass = haveR ? 1 : 0; pass < 2; ++pass) {
         double T = 1.0;
         double Pc[4] = {0.0, 0.0, 0.0, 0.0};
         bool done = !inside;

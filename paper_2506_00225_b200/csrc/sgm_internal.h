@@ -154,6 +154,9 @@ struct ViewDesc {
     uint32_t* contrib;
     uint32_t* contrib_count;
     const unsigned long long* contrib_offset;
+    // score mode with the Fisher gain: [px][4] rendered (R, G, B, depth), written by the
+    // score raster and read by k_fisher in place of its pass 0
+    double* rc4;
 };
 
 struct RasterParams {
@@ -165,6 +168,7 @@ struct RasterParams {
     int raster_tiles_x;
     uint32_t channels;   // SGM_COLOR | SGM_DEPTH | SGM_SEMANTICS
     GroupParams groups;
+    int want_rc;         // score mode: also write vd.rc4 (colour / depth per pixel)
 };
 
 // ---- launchers (sgm_kernels.cu) ----

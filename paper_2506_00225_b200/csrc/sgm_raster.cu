@@ -53,7 +53,7 @@ struct Layout {  // byte offsets in dynamic shared memory
 // nearly conflict-free)
 __host__ __device__ constexpr int acc_pitch(bool render) { return render ? 33 : 32; }
 
-__host__ __device__ inline Layout make_layout(int C, int kpad, bool render) {
+__host__ __device__ inline Layout make_layout(int C, int kpad, bool render, bool color = false) {
     Layout L;
     L.acc = 0;
     L.w = align16(C * acc_pitch(render) * 16);
@@ -67,7 +67,7 @@ __host__ __device__ inline Layout make_layout(int C, int kpad, bool render) {
     L.st_idx = L.st_bnd + kNB * 16;
     L.st_prob = L.st_idx + kNB * kpad * 2;
     L.st_color = L.st_prob + kNB * kpad * 8;
-    L.stage_bytes = L.st_color + (render ? kNB * 32 : 0);
+    L.stage_bytes = L.st_color + ((render || color) ? kNB * 32 : 0);
     L.total = L.stage0 + 2 * L.stage_bytes;
     // the score epilogue's per-(group, pixel) (S1, S2) exchange reuses the stages
     const int red = kGroups * kTilePx * 16;
@@ -91,14 +91,17 @@ __device__ __forceinline__ int pair_slot(int row, int pitch2, int q) {
 __device__ __forceinline__ int px_col(int q) { return ((q >> 4) & 1) * 4 + (q & 3); }
 __device__ __forceinline__ int px_row(int q) { return (q >> 5) * 4 + ((q >> 2) & 3); }
 
-template <bool kRender, bool kDup, bool kAniso>
+// kRc (score mode): also accumulate each pixel's rendered colour and depth, written to
+// vd.rc4[px][4] (the Fisher gain's pass-0 quantity, losses.cpp:285-288)
+template <bool kRender, bool kDup, bool kAniso, bool kRc = false>
 __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int C = p.map.C;
     const int kpad = p.map.kpad;
     const int Cg = p.groups.Cg;
     constexpr int apitch = acc_pitch(kRender);
-    const Layout L = make_layout(C, kpad, kRender);
+    static_assert(!(kRc && kRender), "rc4 is a score-mode output");
+    const Layout L = make_layout(C, kpad, kRender, kRc);
     double2* acc2 = reinterpret_cast<double2*>(smem + L.acc);     // [C][apitch]
     double* acc = reinterpret_cast<double*>(smem + L.acc);
     double* W = reinterpret_cast<double*>(smem + L.w);             // [kNB][32] double2
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
 
     // ---- cp.async pipeline over batches of kNB Gaussians (depth-rank order) ----
     const int qi = kpad / 8, qp = kpad / 2;
-    const int Q = 5 + qi + qp + (kRender ? 2 : 0);  // 16-byte chunks per Gaussian
+    const int Q = 5 + qi + qp + ((kRender || kRc) ? 2 : 0);  // 16-byte chunks per Gaussian
     __shared__ int scnt[3];  // entries of batch b in scnt[b % 3]
     auto issue = [&](int b) {
         unsigned char* sb = stg + (b & 1) * L.stage_bytes;
@@ -202,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
 
     __shared__ uint32_t slive[2];  // batch b: entries with a nonzero weight at some pixel
     if (t < 2) slive[t] = 0u;
+    double rcs[4] = {0.0, 0.0, 0.0, 0.0};  // kRc: this (segment, pixel) thread's colour / depth
     int mine = 0;  // this thread's vote that its pixel is done (the block stops when all are)
     for (int b = 0;; ++b) {
         cp_async_wait_all();
@@ -328,8 +332,15 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
                     W[s] = 0.0;
                     continue;
                 }
-                W[s] = f[i] * Tc;
-                if (W[s] != 0.0) nzbits |= 1u << e;
+                const double wv = f[i] * Tc;
+                W[s] = wv;
+                if (wv != 0.0) nzbits |= 1u << e;
+                if (kRc) {  // this segment's share of the pixel's colour / depth (:289-293)
+                    rcs[0] += scol[4 * e] * wv;
+                    rcs[1] += scol[4 * e + 1] * wv;
+                    rcs[2] += scol[4 * e + 2] * wv;
+                    rcs[3] += sp[e].z * wv;
+                }
                 ++contrib;
                 Tc = Tc * (1.0 - f[i]);
                 if (p.opt.early_exit && Tc < p.opt.eps) exited = true;
@@ -471,6 +482,21 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
         }
         __syncthreads();
     }
+    if (kRc) {  // the pixel's colour / depth: its 4 segments summed in a fixed order
+        double* rcx = reinterpret_cast<double*>(stg);  // stages are free now: [4][64][4]
+        __syncthreads();
+        const int part = t >> 6;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) rcx[(part * kTilePx + px) * 4 + ch] = rcs[ch];
+        __syncthreads();
+        if (t < kTilePx && inside) {
+            const size_t pix = static_cast<size_t>(y) * p.cam.W + x;
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch)
+                vd.rc4[pix * 4 + ch] = ((rcx[(0 * kTilePx + t) * 4 + ch] + rcx[(1 * kTilePx + t) * 4 + ch]) +
+                                        rcx[(2 * kTilePx + t) * 4 + ch]) + rcx[(3 * kTilePx + t) * 4 + ch];
+        }
+    }
     // K (contributors) for the measurement counters
     if (kRender) {
         if (t < kTilePx) red_u[t] = contrib;
@@ -488,10 +514,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
     if (t == 0 && vd.contributors && red_u[0]) atomicAdd(vd.contributors, red_u[0]);
 }
 
-template <bool kRender, bool kDup, bool kAniso>
+template <bool kRender, bool kDup, bool kAniso, bool kRc = false>
 void launch_t(const RasterParams& p, int n_views, cudaStream_t s) {
-    auto kern = k_raster<kRender, kDup, kAniso>;
-    const size_t smem = raster_smem_bytes(p.map, p.groups, kRender);
+    auto kern = k_raster<kRender, kDup, kAniso, kRc>;
+    const size_t smem = static_cast<size_t>(make_layout(p.map.C, p.map.kpad, kRender, kRc).total);
     static size_t configured = 0;
     if (smem > configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -531,6 +557,13 @@ void launch_mode(const RasterParams& p, int n_views, cudaStream_t s) {
 }
 
 void launch_raster_score(const RasterParams& p, int n_views, cudaStream_t s) {
+    if (p.want_rc && !p.map.aniso) {  // Fisher gain: colour / depth planes for its pass 1
+        if (p.map.dup_idx)
+            launch_t<false, true, false, true>(p, n_views, s);
+        else
+            launch_t<false, false, false, true>(p, n_views, s);
+        return;
+    }
     launch_mode<false>(p, n_views, s);
 }
 
