@@ -512,7 +512,18 @@ def main() -> None:
                 "views_per_launch": per_launch_views,
                 "algorithmic_bytes_per_view": "20*N + 6*k*V + 16 (SURVEY 8d)",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}
-    roofline_aux = {"smem_rmw_GBps": smem_bytes / (raster_ms * 1e-3) / 1e9,
+    ncu = {}
+    prof_sum = ROOT / "profiles" / "r01_raster_summary.json"
+    if prof_sum.exists():
+        try:
+            ncu = json.loads(prof_sum.read_text())
+        except ValueError:
+            ncu = {}
+    roofline_aux = {"ncu_lsu_shared_pipe_frac": (ncu.get("smem_pipe_pct") or 0.0) / 100.0 or None,
+                    "ncu_issue_active_frac": (ncu.get("issue_active_pct") or 0.0) / 100.0 or None,
+                    "ncu_source": "profiles/r01_raster_summary.json (ncu --set full, one raster "
+                                  "launch of 8 cfg1 views): the pipes that bound this kernel",
+                    "smem_rmw_GBps": smem_bytes / (raster_ms * 1e-3) / 1e9,
                     "smem_peak_GBps": smem_peak,
                     "smem_frac": (smem_bytes / (raster_ms * 1e-3) / 1e9) / smem_peak,
                     "contributors_per_view": st["contributors"] / max(1, views_timed),
