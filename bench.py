@@ -409,7 +409,10 @@ def main() -> None:
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        fisher_prior(gm, cam, prior_poses, lam=1.0, ctx=ctx)
+        if dist_on:  # past poses sharded over the ranks, H all-reduced
+            sd.fisher_prior_sharded(gm, cam, prior_poses, lam=1.0, ctx=ctx)
+        else:
+            fisher_prior(gm, cam, prior_poses, lam=1.0, ctx=ctx)
         ev1.record(stream)
         ev1.synchronize()
         prior_ms = ev0.elapsed_time(ev1)

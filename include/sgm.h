@@ -187,6 +187,10 @@ int sgm_score_candidates(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam
  * FisherRF-style gain  sum_{i,theta} H_view / (H_prior + lambda)  (deterministic). */
 int sgm_fisher_prior(sgm_ctx* ctx, sgm_map* map, const sgm_camera* cam, uint64_t n,
                      const sgm_pose* poses, const sgm_options* opt, double lambda, double* H_out);
+/* Sets the map's Fisher prior from a host H (N x 8, the layout sgm_fisher_prior returns), e.g.
+ * the sum of per-rank sgm_fisher_prior results over sharded past poses (SURVEY §8e collective
+ * C2: all-reduce of H_prior), then 1 / (H + lambda) on the device as sgm_fisher_prior does. */
+int sgm_fisher_set_prior(sgm_ctx* ctx, sgm_map* map, const double* H, double lambda);
 int sgm_score_views_fisher(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam, uint64_t n,
                            const sgm_pose* poses, const sgm_options* opt, double* n_missing,
                            double* entropy_sum, double* fisher_gain);

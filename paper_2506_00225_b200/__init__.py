@@ -27,6 +27,7 @@ from .splatmap import (  # noqa: F401
     combine_scores,
     deg_to_rad,
     fisher_prior,
+    fisher_set_prior,
     look_at,
     prune_pool,
     refresh_candidate_scores,

@@ -151,6 +151,7 @@ SIGNATURES = {
                                        _pd]),
     "sgm_fisher_prior": (C.c_int, [_vp, _vp, C.POINTER(sgm_camera), C.c_uint64,
                                    C.POINTER(sgm_pose), C.POINTER(sgm_options), C.c_double, _pd]),
+    "sgm_fisher_set_prior": (C.c_int, [_vp, _vp, _pd, C.c_double]),
     "sgm_score_views_fisher": (C.c_int, [_vp, _vp, C.POINTER(sgm_camera), C.c_uint64,
                                          C.POINTER(sgm_pose), C.POINTER(sgm_options), _pd, _pd,
                                          _pd]),

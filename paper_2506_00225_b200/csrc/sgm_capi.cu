@@ -1569,6 +1569,27 @@ int sgm_fisher_prior(sgm_ctx* ctx, sgm_map* map, const sgm_camera* camera, uint6
     });
 }
 
+int sgm_fisher_set_prior(sgm_ctx* ctx, sgm_map* map, const double* H, double lambda) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!map) fail(SGM_ERR_INVALID, "map is null");
+        if (map->dev.aniso)
+            fail(SGM_ERR_UNSUPPORTED, "the Fisher / backward chain is isotropic only (anisotropic map)");
+        if (map->dev.n > 0 && !H) fail(SGM_ERR_INVALID, "H is null");
+        if (!(lambda > 0.0)) fail(SGM_ERR_INVALID, "lambda must be > 0");
+        const size_t nh = 8 * std::max<uint64_t>(map->dev.n, 1);
+        CK(map->fisher_H.reserve(8 * nh));
+        CK(map->fisher_invp.reserve(8 * nh));
+        if (map->dev.n)
+            CK(cudaMemcpyAsync(map->fisher_H.p, H, 64 * map->dev.n, cudaMemcpyHostToDevice, ctx->stream));
+        launch_fisher_invp(map->fisher_H.as<double>(), lambda, 8 * map->dev.n,
+                           map->fisher_invp.as<double>(), ctx->stream);
+        ctx->stats.kernel_launches += 1;
+        CK(cudaStreamSynchronize(ctx->stream));
+        map->has_prior = true;
+    });
+}
+
 int sgm_score_views_fisher(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, uint64_t n,
                            const sgm_pose* poses, const sgm_options* opt, double* n_missing,
                            double* entropy_sum, double* fisher_gain) {

@@ -3,6 +3,8 @@
 Views are independent (explorer.cpp:188-204), so the data path has
 no collective. The only exchanges are the ones the planning step really has:
   C1 broadcast_map   - the map snapshot from rank 0, once per map version
+  C2 all_reduce_prior - the Fisher prior H (N x 8) summed over ranks, each rank having
+                       accumulated its shard of the past poses (fisher_prior_sharded)
   C3 gather_scores   - every rank's (n_missing, entropy_sum) records, so every
                        rank can run the reference-identical combine_scores and
                        agree on the argmax.
@@ -79,6 +81,26 @@ def broadcast_map(gmap: Optional[GaussianMap], src: int = 0) -> GaussianMap:
     qs = take(4 * n).reshape(n, 4) if aniso else None
     return GaussianMap.from_arrays(k, m, centers, log_r, logits, colors, idx, probs,
                                    log_scales=ls, quats=qs)
+
+
+def all_reduce_prior(H_local: np.ndarray) -> np.ndarray:
+    """C2: element-wise sum of every rank's (N, 8) Fisher prior share (fp64)."""
+    t = torch.from_numpy(np.ascontiguousarray(H_local, dtype=np.float64)).to(_device())
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.cpu().numpy()
+
+
+def fisher_prior_sharded(gmap: GaussianMap, camera, poses, lam: float = 1.0, options=None,
+                         ctx=None) -> np.ndarray:
+    """The Fisher prior over `poses` with the poses sharded across ranks: each rank
+    accumulates its contiguous block (fisher_prior), the shares are all-reduced (C2) and the
+    sum is installed on every rank's map (fisher_set_prior). Returns the summed H."""
+    from .splatmap import fisher_prior, fisher_set_prior
+    s, e = shard_range(len(poses), dist.get_rank(), dist.get_world_size())
+    H = fisher_prior(gmap, camera, list(poses[s:e]), lam=lam, options=options, ctx=ctx)
+    H = all_reduce_prior(H)
+    fisher_set_prior(gmap, H, lam=lam, ctx=ctx)
+    return H
 
 
 def gather_scores(n_total: int, n_missing: np.ndarray, entropy_sum: np.ndarray

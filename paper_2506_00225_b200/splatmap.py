@@ -787,6 +787,16 @@ def fisher_prior(gmap: GaussianMap, camera: CameraModel, poses: Sequence[Pose],
     return H[:gmap.size()]
 
 
+def fisher_set_prior(gmap: GaussianMap, H: np.ndarray, lam: float = 1.0,
+                     ctx: Optional[Context] = None) -> None:
+    """Installs a Fisher prior given as an (N, 8) array (e.g. the all-reduced sum of per-rank
+    fisher_prior results over sharded past poses, dist.fisher_prior_sharded)."""
+    c = _ctx(ctx)
+    handle = c.upload(gmap)
+    Hc = np.ascontiguousarray(np.asarray(H, dtype=np.float64).reshape(gmap.size(), 8))
+    c.check(N.lib.sgm_fisher_set_prior(c.handle, handle, N.dptr(Hc), float(lam)))
+
+
 def score_poses_fisher(gmap: GaussianMap, camera: CameraModel, poses: Sequence[Pose],
                        options: Optional[RenderOptions] = None, ctx: Optional[Context] = None):
     """Per view (n_missing, entropy_sum, fisher_gain) with the FisherRF-style gain

@@ -73,3 +73,42 @@ def test_two_rank_gloo_broadcast_shard_gather(orc, aniso):
     cands = scenes.make_candidates(0, 7)
     nm, es, _ = orc.score_views(gm, cam, [c.camera_pose() for c in cands])
     assert a[2] == nm.tobytes() and a[3] == es.tobytes()  # sharding-invariant
+
+
+def _prior_worker(rank, world, port, out):
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import torch.distributed as dist
+    import oracle
+    from paper_2506_00225_b200 import dist as sd
+    from paper_2506_00225_b200 import scenes
+    from paper_2506_00225_b200.splatmap import CameraModel
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    gm = sd.broadcast_map(scenes.make_map(0, n=300) if rank == 0 else None)
+    cam = CameraModel(40, 26, 0, 0, 30.0, 30.0, 20.0, 13.0)
+    poses = [c.camera_pose() for c in scenes.make_candidates(0, 5, stream=2)]
+    s, e = sd.shard_range(len(poses), rank, world)
+    H = oracle.Oracle().fisher_accumulate(gm, cam, poses[s:e]) if e > s else np.zeros((gm.size(), 8))
+    out[rank] = sd.all_reduce_prior(H).tobytes()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_fisher_prior_all_reduce(orc):
+    """C2: the prior over sharded past poses, all-reduced, equals the prior over all poses
+    (to reassociation) on every rank."""
+    from paper_2506_00225_b200 import scenes
+    from paper_2506_00225_b200.splatmap import CameraModel
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_prior_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    assert out[0] == out[1]
+    gm = scenes.make_map(0, n=300)
+    cam = CameraModel(40, 26, 0, 0, 30.0, 30.0, 20.0, 13.0)
+    poses = [c.camera_pose() for c in scenes.make_candidates(0, 5, stream=2)]
+    want = orc.fisher_accumulate(gm, cam, poses)
+    got = np.frombuffer(out[0], dtype=np.float64).reshape(want.shape)
+    np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-300)
+    assert np.any(want > 0)

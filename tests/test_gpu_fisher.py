@@ -60,3 +60,22 @@ def test_fisher_cfg0_scene_vs_oracle(ctx, orc):
     np.testing.assert_allclose(H, H_o, rtol=1e-9, atol=1e-12 * H_o.max())
     _, _, g = sgm.score_poses_fisher(gm, cam, poses[4:], ctx=ctx)
     np.testing.assert_allclose(g, orc.fisher_gain(gm, cam, poses[4:], H_o, 1.0), rtol=1e-9)
+
+
+def test_prior_from_summed_shards_equals_full_prior():
+    """sgm_fisher_set_prior with the sum of two shards' priors (what the multi-GPU C2
+    all-reduce produces) gives the same gains as the prior over all poses."""
+    import paper_2506_00225_b200 as sgm
+    from paper_2506_00225_b200 import scenes
+    ctx = sgm.Context(0)
+    gm = scenes.make_map(0, n=3000)
+    cam = scenes.CONFIGS[0].camera()
+    prior = [c.camera_pose() for c in scenes.make_candidates(0, 6, stream=2)]
+    views = scenes.render_poses(0, 3)
+    H_all = sgm.fisher_prior(gm, cam, prior, lam=1.0, ctx=ctx)
+    _, _, g_all = sgm.score_poses_fisher(gm, cam, views, ctx=ctx)
+    H_sum = sgm.fisher_prior(gm, cam, prior[:2], ctx=ctx) + sgm.fisher_prior(gm, cam, prior[2:], ctx=ctx)
+    np.testing.assert_allclose(H_sum, H_all, rtol=1e-12, atol=1e-300)
+    sgm.fisher_set_prior(gm, H_sum, lam=1.0, ctx=ctx)
+    _, _, g_sum = sgm.score_poses_fisher(gm, cam, views, ctx=ctx)
+    np.testing.assert_allclose(g_sum, g_all, rtol=1e-12)
