@@ -158,7 +158,8 @@ struct sgm_ctx {
     uint64_t last_ncontrib = 0;
     bool last_has_contrib = false;
     int last_px = 0;
-    HostBuf h_counts, h_views, h_poses, h_out, h_stage;
+    HostBuf h_counts, h_views, h_poses, h_out, h_stage, h_ring;
+    cudaEvent_t ev_ring[4] = {nullptr, nullptr, nullptr, nullptr};  // copy_out pinned ring
     DevBuf upload_tmp;
     // device buffers of released maps, reused by the next upload (a map version bump
     // otherwise pays cudaFree + cudaMalloc of ~0.2 KB per Gaussian)
@@ -1120,6 +1121,8 @@ void sgm_ctx_destroy(sgm_ctx* ctx) {
         if (ev) cudaEventDestroy(ev);
     for (auto& ev : ctx->ev_r)
         if (ev) cudaEventDestroy(ev);
+    for (auto& ev : ctx->ev_ring)
+        if (ev) cudaEventDestroy(ev);
     cudaStream_t s = ctx->stream, s2 = ctx->bin_stream;
     delete ctx;
     if (s) cudaStreamDestroy(s);
@@ -1385,6 +1388,84 @@ int sgm_render_device(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam, c
     });
 }
 
+namespace {
+
+struct CopyOut {
+    void* dst;        // host (pageable) destination
+    const void* src;  // device source
+    size_t bytes;
+};
+
+// Device -> pageable host copies of large planes (a full render is px (5 + C) doubles:
+// 698 MB at cfg1). A plain cudaMemcpy to pageable memory is staged by the driver at about
+// 15 GB/s and pays the fresh pages' faults serially; here the planes go through a ring of
+// pinned buffers in kChunk pieces (DMA at full PCIe rate) while a pool of host threads
+// copies the finished pieces out in parallel.
+void copy_out(sgm_ctx* ctx, const std::vector<CopyOut>& segs) {
+    constexpr size_t kChunk = size_t(16) << 20;
+    constexpr int kSlots = 4;
+    cudaStream_t s = ctx->stream;
+    size_t total = 0;
+    for (const auto& g : segs) total += g.bytes;
+    if (total <= 2 * kChunk) {  // small: direct copies
+        for (const auto& g : segs)
+            CK(cudaMemcpyAsync(g.dst, g.src, g.bytes, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        return;
+    }
+    struct Piece {
+        char* dst;
+        const char* src;
+        size_t bytes;
+    };
+    std::vector<Piece> pieces;
+    for (const auto& g : segs)
+        for (size_t o = 0; o < g.bytes; o += kChunk)
+            pieces.push_back({static_cast<char*>(g.dst) + o, static_cast<const char*>(g.src) + o,
+                              std::min(kChunk, g.bytes - o)});
+    CK(ctx->h_ring.reserve(kSlots * kChunk));
+    for (int k = 0; k < kSlots; ++k)
+        if (!ctx->ev_ring[k]) CK(cudaEventCreateWithFlags(&ctx->ev_ring[k], cudaEventDisableTiming));
+    const unsigned nth = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    const size_t np = pieces.size();
+    std::unique_ptr<std::atomic<unsigned>[]> copied(new std::atomic<unsigned>[np]);
+    for (size_t j = 0; j < np; ++j) copied[j].store(0);
+    std::atomic<size_t> issued{0};  // pieces whose D2H + event are enqueued
+    std::atomic<int> err{0};
+    auto worker = [&](unsigned w) {
+        for (size_t j = 0; j < np; ++j) {
+            while (issued.load(std::memory_order_acquire) <= j && !err.load()) std::this_thread::yield();
+            if (err.load()) return;
+            const int slot = static_cast<int>(j % kSlots);
+            if (cudaEventSynchronize(ctx->ev_ring[slot]) != cudaSuccess) err.store(1);
+            const Piece& pc = pieces[j];
+            const size_t a = pc.bytes * w / nth, b = pc.bytes * (w + 1) / nth;
+            std::memcpy(pc.dst + a, ctx->h_ring.as<char>() + slot * kChunk + a, b - a);
+            copied[j].fetch_add(1, std::memory_order_release);
+        }
+    };
+    std::vector<std::thread> pool;
+    for (unsigned w = 0; w < nth; ++w) pool.emplace_back(worker, w);
+    cudaError_t e = cudaSuccess;
+    for (size_t j = 0; j < np && e == cudaSuccess; ++j) {
+        const int slot = static_cast<int>(j % kSlots);
+        if (j >= kSlots)  // the slot's previous piece must be copied out first
+            while (copied[j - kSlots].load(std::memory_order_acquire) < nth && !err.load())
+                std::this_thread::yield();
+        e = cudaMemcpyAsync(ctx->h_ring.as<char>() + slot * kChunk, pieces[j].src, pieces[j].bytes,
+                            cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_ring[slot], s);
+        issued.store(j + 1, std::memory_order_release);
+    }
+    if (e != cudaSuccess) err.store(1);
+    for (auto& th : pool) th.join();
+    CK(e);
+    if (err.load()) fail(SGM_ERR_CUDA, "device-to-host copy failed");
+    CK(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
 int sgm_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const sgm_pose* pose,
                uint32_t channels, const sgm_options* opt, double* color, double* depth,
                double* silhouette, double* sem, uint64_t* n_projections) {
@@ -1408,12 +1489,11 @@ int sgm_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const
         uint32_t ch = (want_c ? SGM_COLOR : 0u) | (want_d ? SGM_DEPTH : 0u) |
                       (want_s ? SGM_SEMANTICS : 0u) | (channels & SGM_RETAIN_CONTRIBUTORS);
         do_render(ctx, map, camera, pose, ch, opt, d_color, d_depth, d_sil, d_sem, n_projections);
-        cudaStream_t s = ctx->stream;
-        CK(cudaMemcpyAsync(silhouette, d_sil, 8 * px, cudaMemcpyDeviceToHost, s));
-        if (want_c) CK(cudaMemcpyAsync(color, d_color, 24 * px, cudaMemcpyDeviceToHost, s));
-        if (want_d) CK(cudaMemcpyAsync(depth, d_depth, 8 * px, cudaMemcpyDeviceToHost, s));
-        if (want_s) CK(cudaMemcpyAsync(sem, d_sem, 8 * px * C, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        std::vector<CopyOut> segs{{silhouette, d_sil, 8 * px}};
+        if (want_c) segs.push_back({color, d_color, 24 * px});
+        if (want_d) segs.push_back({depth, d_depth, 8 * px});
+        if (want_s) segs.push_back({sem, d_sem, 8 * px * C});
+        copy_out(ctx, segs);
         // Unrequested-but-provided planes: the reference leaves them empty; zero them.
         if ((channels & SGM_COLOR) == 0 && color) std::memset(color, 0, 24 * px);
         if ((channels & SGM_DEPTH) == 0 && depth) std::memset(depth, 0, 8 * px);
