@@ -1426,7 +1426,7 @@ void copy_out(sgm_ctx* ctx, const std::vector<CopyOut>& segs) {
     CK(ctx->h_ring.reserve(kSlots * kChunk));
     for (int k = 0; k < kSlots; ++k)
         if (!ctx->ev_ring[k]) CK(cudaEventCreateWithFlags(&ctx->ev_ring[k], cudaEventDisableTiming));
-    const unsigned nth = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    const unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     const size_t np = pieces.size();
     std::unique_ptr<std::atomic<unsigned>[]> copied(new std::atomic<unsigned>[np]);
     for (size_t j = 0; j < np; ++j) copied[j].store(0);
