@@ -1,0 +1,235 @@
+// Host-side internals shared by the C-ABI translation units (sgm_capi.cu, sgm_capi_ext.cu)
+// and the view pipeline (sgm_pipeline.cu): device / pinned buffers, the error plumbing
+// behind the status codes, the opaque sgm_map / sgm_ctx, and the pipeline entry points.
+#pragma once
+
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <new>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/sgm.h"
+#include "sgm_internal.h"
+
+namespace sgm {
+
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+        o.p = nullptr;
+        o.bytes = 0;
+    }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            if (p) cudaFree(p);
+            p = o.p;
+            bytes = o.bytes;
+            o.p = nullptr;
+            o.bytes = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    // Grows (never shrinks); contents are not preserved.
+    cudaError_t reserve(size_t want) {
+        if (want <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        // 1/8 headroom: per-view sizes vary, so exact-size growth would reallocate often
+        const size_t b = std::max<size_t>(want + want / 8, 256);
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e == cudaSuccess) bytes = b;
+        return e;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct HostBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~HostBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    cudaError_t reserve(size_t want) {
+        if (want <= bytes) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMallocHost(&p, std::max<size_t>(want, 256));
+        if (e == cudaSuccess) bytes = std::max<size_t>(want, 256);
+        return e;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct SgmError {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] inline void fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    throw SgmError{code, buf};
+}
+
+#define CK(call)                                                                       \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess)                                                         \
+            fail(e_ == cudaErrorMemoryAllocation ? SGM_ERR_OOM : SGM_ERR_CUDA,         \
+                 "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__,     \
+                 __LINE__);                                                            \
+    } while (0)
+
+
+}  // namespace sgm
+
+using namespace sgm;
+
+struct sgm_map {
+    DevMap dev;
+    GroupParams groups{1, 1};
+    int num_classes = 0;
+    DevBuf fisher_H, fisher_invp;  // Fisher prior (sgm_fisher_prior)
+    bool has_prior = false;
+    DevBuf geo;    // cx, cy, cz, rad, alpha (5 x n doubles)
+    DevBuf color;  // [n][4]
+    DevBuf idx;    // [n][kpad] u16 (class-sorted)
+    DevBuf prob;   // [n][kpad] f64
+    DevBuf perm;   // [n][kpad] u16 original entry index
+    DevBuf cov;    // anisotropic mode: [6][n] world covariance (sgm_map_set_anisotropic)
+};
+
+struct sgm_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    sgm_stats stats{};
+    bool profiling = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t bin_stream = nullptr;  // binning of the next sub-batch overlaps the raster
+    cudaEvent_t ev_ready = nullptr;
+    cudaEvent_t ev_binned[2] = {nullptr, nullptr};
+    cudaEvent_t ev_r[16] = {};  // raster start/stop pairs of one group (profiling)
+
+    // scratch
+    DevBuf poses, vcount, pcount, keys, vals, keys_alt, vals_alt, packed, counts, offsets, rects,
+        bounds, bdiff, rranges, rvals, segs, segcnt, rcbuf;
+    DevBuf tkeys, tvals, tkeys_alt, tvals_alt, ranges, ent_part, miss_part, views, out,
+        contributors, cub_tmp, planes, dbg, ccount, coffset, contrib, fis_part, bw_frame,
+        bw_flags, bw_part, bw_grad;
+    uint64_t last_ncontrib = 0;
+    bool last_has_contrib = false;
+    int last_px = 0;
+    HostBuf h_counts, h_views, h_poses, h_out, h_stage, h_ring;
+    cudaEvent_t ev_ring[4] = {nullptr, nullptr, nullptr, nullptr};  // copy_out pinned ring
+    DevBuf upload_tmp;
+    // device buffers of released maps, reused by the next upload (a map version bump
+    // otherwise pays cudaFree + cudaMalloc of ~0.2 KB per Gaussian)
+    std::vector<DevBuf> pool;
+
+    void take(DevBuf& dst, size_t want) {
+        if (dst.bytes >= want) return;
+        size_t best = pool.size();
+        for (size_t i = 0; i < pool.size(); ++i)
+            if (pool[i].bytes >= want && (best == pool.size() || pool[i].bytes < pool[best].bytes))
+                best = i;
+        if (best == pool.size()) return;
+        dst = std::move(pool[best]);
+        pool.erase(pool.begin() + static_cast<long>(best));
+    }
+    void give(DevBuf&& b) {
+        if (!b.p) return;
+        pool.push_back(std::move(b));
+        while (pool.size() > 16) pool.erase(pool.begin());  // bounded: oldest first
+    }
+
+    // state of the last render (for sgm_last_*)
+    bool last_valid = false;
+    uint32_t last_V = 0;
+    uint64_t last_P = 0;
+    int last_bin_tiles = 0;
+    const sgm_map* last_map = nullptr;
+    CamParams last_cam{};
+    OptParams last_opt{};
+    PoseParams last_pose{};
+};
+
+namespace sgm {
+
+CamParams to_cam(const sgm_camera* c);
+OptParams to_opt(const sgm_options* o, const CamParams& cam);
+PoseParams to_pose(const sgm_pose& p);
+// runs fn, mapping SgmError / CUDA / allocation failures to status codes and ctx->err
+int guard(sgm_ctx* ctx, const std::function<void()>& fn);
+void need_ctx(sgm_ctx* ctx);
+unsigned tile_bits(uint64_t tiles);
+
+enum class Mode { Score, Render };
+enum class Fisher { None, Prior, Gain };
+
+struct RenderTargets {
+    double* color = nullptr;
+    double* depth = nullptr;
+    double* sil = nullptr;
+    double* sem = nullptr;
+    uint32_t channels = 0;
+    uint32_t* contrib = nullptr;            // retain_contributors
+    uint32_t* contrib_count = nullptr;      // pass 1
+    const unsigned long long* contrib_offset = nullptr;  // pass 2
+};
+
+// Runs n views. Score mode writes n_missing/entropy_sum (host); render mode (n == 1)
+// writes planes to device targets. Binning of sub-batch i+1 (on ctx->bin_stream)
+// overlaps the raster of sub-batch i (on ctx->stream).
+void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const OptParams& o,
+               uint64_t n, const PoseParams* poses, Mode mode, const RenderTargets& rt,
+               double* h_missing, double* h_entropy, Fisher fk = Fisher::None,
+               double* h_fisher = nullptr, double* d_H = nullptr);
+// One render into device planes (retain_contributors: two raster passes).
+void do_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const sgm_pose* pose,
+               uint32_t channels, const sgm_options* opt, double* d_color, double* d_depth,
+               double* d_sil, double* d_sem, uint64_t* n_proj);
+// The mapping step on device-resident frame planes (see sgm_pipeline.cu).
+void backward_core(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const OptParams& o,
+                   const PoseParams& p, const float* f_rgb, const float* f_depth,
+                   const float* f_sem, const double weights[7], int include_mapping,
+                   int include_semantic, double report[7]);
+
+struct CopyOut {
+    void* dst;        // host (pageable) destination
+    const void* src;  // device source
+    size_t bytes;
+};
+void copy_out(sgm_ctx* ctx, const std::vector<CopyOut>& segs);
+
+}  // namespace sgm

@@ -1,0 +1,623 @@
+// The host pipeline that drives the sm_100a kernels for batches of views.
+//
+// Pipeline for a batch of views (all on the ctx stream):
+//   1. K1 k_preprocess over (Gaussian, view): compact visible (z, index), count V, P and
+//      the row pairs R (tile rows spanned)
+//   2. one D2H of the per-view V/P/R counts (the only host sync before the results)
+//   3. per view (binning stream): CUB radix sort on fp32(z) -> k_tiefix -> k_pack ->
+//      k_bin_hist + k_bin_scan (tile ranges) -> k_emit_rows + CUB stable row sort ->
+//      k_row_segs / k_seg_pass x2 / k_seg_scan (ordered scatter into the tile lists)
+//   4. one batched raster launch over (8x8 tile, view)
+//   5. k_reduce_scores (score) / planes already written (render)
+// Views whose pair lists do not fit the scratch budget together are split into
+// sub-batches; results do not depend on the split (per-view work is independent).
+#include "sgm_ctx.h"
+
+namespace sgm {
+
+
+CamParams to_cam(const sgm_camera* c) {
+    if (!c) fail(SGM_ERR_INVALID, "camera is null");
+    if (c->width <= 0 || c->height <= 0) fail(SGM_ERR_INVALID, "camera: resolution must be positive");
+    return CamParams{c->width, c->height, c->fx, c->fy, c->cx, c->cy};
+}
+
+OptParams to_opt(const sgm_options* o, const CamParams& cam) {
+    sgm_options d{1, 1e-4, 0.01, 3.0, 8};
+    const sgm_options& s = o ? *o : d;
+    if (s.tile_size <= 0 || s.tile_size % kTile != 0)
+        fail(SGM_ERR_UNSUPPORTED, "tile_size %d: this build bins at multiples of %d", s.tile_size,
+             kTile);
+    OptParams p;
+    p.early_exit = s.early_exit ? 1 : 0;
+    p.eps = s.transmittance_eps;
+    p.z_near = s.z_near;
+    p.trunc = s.truncation_sigmas;
+    p.cut_sq = s.truncation_sigmas * s.truncation_sigmas;
+    p.ts = s.tile_size;
+    p.tiles_x = (cam.W + s.tile_size - 1) / s.tile_size;
+    p.tiles_y = (cam.H + s.tile_size - 1) / s.tile_size;
+    return p;
+}
+
+PoseParams to_pose(const sgm_pose& p) {
+    PoseParams q;
+    for (int i = 0; i < 3; ++i)
+        for (int k = 0; k < 3; ++k) q.Rcw[3 * i + k] = p.R[3 * k + i];  // R_cw = R^T
+    for (int i = 0; i < 3; ++i) q.t[i] = p.t[i];
+    return q;
+}
+
+unsigned tile_bits(uint64_t tiles) {
+    unsigned b = 1;
+    while ((1ull << b) < tiles) ++b;
+    return b;
+}
+
+
+// Bins one view (step 3). Writes ranges / sorted list / packed into the per-view
+// slices and returns via the slice pointers. vals/keys hold the compacted (z, idx).
+static void bin_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const CamParams& cam,
+              const OptParams& o, const PoseParams* d_pose, uint32_t* keys, uint32_t* vals,
+              uint32_t V, uint64_t P, uint64_t R, PackedSplat* packed, uint4* bounds, uint32_t* list,
+              uint2* ranges, int bin_tiles) {
+    CK(cudaMemsetAsync(ranges, 0, sizeof(uint2) * bin_tiles, s));
+    if (V == 0) return;
+    // K2: depth rank (radix sort on the monotone fp32 key; runs fixed below)
+    cub::DoubleBuffer<uint32_t> dk(keys, ctx->keys_alt.as<uint32_t>());
+    cub::DoubleBuffer<uint32_t> dv(vals, ctx->vals_alt.as<uint32_t>());
+    size_t tmp = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, V, 0, 32, s));
+    CK(ctx->cub_tmp.reserve(tmp));
+    CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, dk, dv, V, 0, 32, s));
+    ctx->stats.kernel_launches += 1;  // counted as one library sort call
+    launch_tiefix(map->dev, d_pose, cam, o, dk.Current(), dv.Current(), V, s);
+    launch_pack(map->dev, d_pose, cam, o, map->groups, dv.Current(), V, packed,
+                ctx->counts.as<unsigned long long>(), ctx->rects.as<int4>(), bounds, s);
+    ctx->stats.kernel_launches += (V >= 2 ? 1 : 0) + 1;
+    // keep the sorted indices for sgm_last_projections
+    if (dv.Current() != vals) CK(cudaMemcpyAsync(vals, dv.Current(), 4ull * V, cudaMemcpyDeviceToDevice, s));
+    if (P == 0) return;
+    // K3 (row-bucketed, no sort of the P pairs): tile ranges from the rectangles' 2D
+    // difference array; each tile row's ranks in rank order (R = sum of rows spanned pairs,
+    // stably sorted by row); then one CTA per tile row scatters its ranks into the tile lists
+    // in rank order (sgm_kernels.cu)
+    const int X = o.tiles_x + 1, Y = o.tiles_y + 1;
+    int* diff = ctx->bdiff.as<int>();
+    CK(cudaMemsetAsync(diff, 0, sizeof(int) * X * Y, s));
+    unsigned long long* rows = ctx->counts.as<unsigned long long>();
+    unsigned long long* roff = ctx->offsets.as<unsigned long long>();
+    launch_bin_hist(ctx->rects.as<int4>(), V, o.tiles_x, diff, rows, s);
+    launch_bin_scan(diff, o.tiles_x, o.tiles_y, ranges, s);
+    CK(cudaMemsetAsync(rows + V, 0, sizeof(unsigned long long), s));
+    size_t tmp2 = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, rows, roff, V + 1, s));
+    CK(ctx->cub_tmp.reserve(tmp2));
+    CK(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp2, rows, roff, V + 1, s));
+    uint32_t* rk = ctx->tkeys.as<uint32_t>();
+    unsigned long long* rv = ctx->rvals.as<unsigned long long>();
+    launch_emit_rows(roff, ctx->rects.as<int4>(), V, R, rk, rv, s);
+    cub::DoubleBuffer<uint32_t> qk(rk, ctx->tkeys_alt.as<uint32_t>());
+    cub::DoubleBuffer<unsigned long long> qv(rv, ctx->tvals_alt.as<unsigned long long>());
+    tmp2 = 0;
+    const int rbits = static_cast<int>(tile_bits(static_cast<uint64_t>(o.tiles_y)));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, qk, qv, R, 0, rbits, s));
+    CK(ctx->cub_tmp.reserve(tmp2));
+    CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp2, qk, qv, R, 0, rbits, s));
+    uint2* rranges = ctx->rranges.as<uint2>();
+    CK(cudaMemsetAsync(rranges, 0, sizeof(uint2) * o.tiles_y, s));
+    launch_ranges(qk.Current(), R, rranges, s);
+    const uint64_t G = row_scatter_segments(R, o.tiles_y);  // buffers sized per group (run_views)
+    launch_row_scatter(qv.Current(), rranges, ranges, o.tiles_x, o.tiles_y, R,
+                       ctx->segs.as<uint4>(), reinterpret_cast<uint32_t*>(ctx->segs.as<char>() + sizeof(uint4) * G),
+                       ctx->segcnt.as<uint32_t>(), list, s);
+    ctx->stats.kernel_launches += 7;
+}
+
+// Runs n views. Score mode writes n_missing/entropy_sum (host); render mode (n == 1)
+// writes planes to device targets. Binning of sub-batch i+1 (on ctx->bin_stream)
+// overlaps the raster of sub-batch i (on ctx->stream).
+void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const OptParams& o,
+               uint64_t n, const PoseParams* poses, Mode mode, const RenderTargets& rt,
+               double* h_missing, double* h_entropy, Fisher fk, double* h_fisher, double* d_H) {
+    cudaStream_t s = ctx->stream;
+    cudaStream_t sb = ctx->bin_stream;
+    const uint64_t N = map->dev.n;
+    const int bin_tiles = o.tiles_x * o.tiles_y;
+    const int rtx = (cam.W + kTile - 1) / kTile;
+    const int rty = (cam.H + kTile - 1) / kTile;
+    const int rtiles = rtx * rty;
+    ctx->last_valid = false;
+
+    // batch size bounded by a scratch budget for the per-view N-sized arrays
+    const size_t per_view = std::max<uint64_t>(N, 1) * (4 + 4 + sizeof(PackedSplat) + 16) +
+                            static_cast<size_t>(bin_tiles) * sizeof(uint2) +
+                            static_cast<size_t>(rtiles) * 12 + 256;
+    const size_t budget = size_t(12) << 30;
+    uint64_t B = std::max<uint64_t>(1, std::min<uint64_t>(n, std::max<size_t>(1, budget / per_view)));
+    B = std::min<uint64_t>(B, 64);
+    if (mode == Mode::Render) B = 1;
+
+    const size_t NS = std::max<uint64_t>(N, 1);
+    CK(ctx->poses.reserve(sizeof(PoseParams) * B));
+    CK(ctx->vcount.reserve(4 * B));
+    CK(ctx->pcount.reserve(16 * B));  // pairs P | row pairs R per view
+    CK(ctx->bdiff.reserve(sizeof(int) * (o.tiles_x + 1) * (o.tiles_y + 1)));
+    CK(ctx->rranges.reserve(sizeof(uint2) * o.tiles_y));
+    CK(ctx->keys.reserve(4 * NS * B));
+    CK(ctx->vals.reserve(4 * NS * B));
+    CK(ctx->keys_alt.reserve(4 * NS));
+    CK(ctx->rects.reserve(sizeof(int4) * NS));
+    CK(ctx->vals_alt.reserve(4 * NS));
+    CK(ctx->packed.reserve(sizeof(PackedSplat) * NS * B));
+    CK(ctx->bounds.reserve(sizeof(uint4) * NS * B));
+    CK(ctx->counts.reserve(8 * (NS + 1)));
+    CK(ctx->offsets.reserve(8 * (NS + 1)));
+    CK(ctx->ranges.reserve(sizeof(uint2) * bin_tiles * B));
+    CK(ctx->ent_part.reserve(8ull * rtiles * B));
+    CK(ctx->miss_part.reserve(4ull * rtiles * B));
+    CK(ctx->views.reserve(sizeof(ViewDesc) * B));
+    CK(ctx->out.reserve(24 * B));
+    if (fk == Fisher::Gain) {
+        CK(ctx->fis_part.reserve(8ull * rtiles * B));
+        // rendered colour / depth per view for the gain's Jacobian pass (written by the
+        // score raster, so k_fisher skips its own pass 0)
+        CK(ctx->rcbuf.reserve(32ull * cam.W * cam.H * B));
+    }
+    CK(ctx->contributors.reserve(8));
+    CK(ctx->h_counts.reserve(32 * B + 16));  // V (u32) | P | R | contributors
+    CK(ctx->h_views.reserve(sizeof(ViewDesc) * B));
+    CK(ctx->h_poses.reserve(sizeof(PoseParams) * B));
+    CK(ctx->h_out.reserve(24 * B));
+
+    const int kSub = 8;  // views per raster launch (binning of the next 8 overlaps)
+    for (uint64_t b0 = 0; b0 < n; b0 += B) {
+        const int nb = static_cast<int>(std::min<uint64_t>(B, n - b0));
+        if (ctx->profiling) CK(cudaEventRecord(ctx->ev[0], s));
+        std::memcpy(ctx->h_poses.p, poses + b0, sizeof(PoseParams) * nb);
+        CK(cudaMemcpyAsync(ctx->poses.p, ctx->h_poses.p, sizeof(PoseParams) * nb,
+                           cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(ctx->vcount.p, 0, 4 * nb, s));
+        CK(cudaMemsetAsync(ctx->pcount.p, 0, 16 * nb, s));
+        CK(cudaMemsetAsync(ctx->contributors.p, 0, 8, s));
+        launch_preprocess(map->dev, ctx->poses.as<PoseParams>(), cam, o, nb, ctx->keys.as<uint32_t>(),
+                          ctx->vals.as<uint32_t>(), NS, ctx->vcount.as<uint32_t>(),
+                          ctx->pcount.as<unsigned long long>(),
+                          ctx->pcount.as<unsigned long long>() + nb, s);
+        ctx->stats.kernel_launches += (N > 0) ? 1 : 0;
+        uint32_t* hv = ctx->h_counts.as<uint32_t>();
+        unsigned long long* hp = reinterpret_cast<unsigned long long*>(ctx->h_counts.as<char>() + 8 * B);
+        CK(cudaMemcpyAsync(hv, ctx->vcount.p, 4 * nb, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hp, ctx->pcount.p, 16 * nb, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::vector<uint32_t> V(hv, hv + nb);
+        std::vector<uint64_t> P(hp, hp + nb);
+        std::vector<uint64_t> R(hp + nb, hp + 2 * nb);  // (row, rank) pairs of the binning
+        for (int v = 0; v < nb; ++v)
+            if (P[v] >= (1ull << 32)) fail(SGM_ERR_UNSUPPORTED, "view has %llu tile pairs (>= 2^32)",
+                                          static_cast<unsigned long long>(P[v]));
+
+        // groups of views whose pair lists fit the budget together
+        const uint64_t pair_budget = (uint64_t(8) << 30) / 4;  // u32 list entries
+        int v0 = 0;
+        while (v0 < nb) {
+            int v1 = v0;
+            uint64_t sumP = 0, maxP = 0;
+            while (v1 < nb && (v1 == v0 || sumP + P[v1] <= pair_budget)) {
+                sumP += P[v1];
+                maxP = std::max<uint64_t>(maxP, P[v1]);
+                ++v1;
+            }
+            uint64_t maxR = 1;
+            for (int v = v0; v < v1; ++v) maxR = std::max<uint64_t>(maxR, R[v]);
+            CK(ctx->tvals.reserve(4 * std::max<uint64_t>(sumP, 1)));
+            CK(ctx->tkeys.reserve(4 * maxR));
+            CK(ctx->tkeys_alt.reserve(4 * maxR));
+            CK(ctx->tvals_alt.reserve(8 * maxR));
+            CK(ctx->rvals.reserve(8 * maxR));
+            // row-scatter segments of the largest view (reserved here, not between the
+            // views' binning launches: a reallocation would synchronise the device)
+            const uint64_t maxG = row_scatter_segments(maxR, o.tiles_y);
+            CK(ctx->segs.reserve(sizeof(uint4) * maxG + 16));
+            CK(ctx->segcnt.reserve(sizeof(uint32_t) * maxG * o.tiles_x));
+            // descriptors for the whole group (list offsets known from the counts)
+            ViewDesc* hvd = ctx->h_views.as<ViewDesc>();
+            uint64_t list_off = 0;
+            for (int v = v0; v < v1; ++v) {
+                ViewDesc d{};
+                d.order = ctx->vals.as<uint32_t>() + NS * v;
+                d.pose = ctx->poses.as<PoseParams>() + v;
+                d.fis_partial = fk == Fisher::Gain ? ctx->fis_part.as<double>() + static_cast<size_t>(rtiles) * v
+                                                   : nullptr;
+                d.ranges = ctx->ranges.as<uint2>() + static_cast<size_t>(bin_tiles) * v;
+                d.list = ctx->tvals.as<uint32_t>() + list_off;
+                d.packed = ctx->packed.as<PackedSplat>() + NS * v;
+                d.bounds = ctx->bounds.as<uint4>() + NS * v;
+                d.ent_partial = ctx->ent_part.as<double>() + static_cast<size_t>(rtiles) * v;
+                d.miss_partial = ctx->miss_part.as<uint32_t>() + static_cast<size_t>(rtiles) * v;
+                d.color = rt.color;
+                d.depth = rt.depth;
+                d.sil = rt.sil;
+                d.sem = rt.sem;
+                d.contributors = ctx->contributors.as<unsigned long long>();
+                d.contrib = rt.contrib;
+                d.contrib_count = rt.contrib_count;
+                d.contrib_offset = rt.contrib_offset;
+                d.rc4 = fk == Fisher::Gain
+                            ? ctx->rcbuf.as<double>() + 4ull * cam.W * cam.H * static_cast<size_t>(v)
+                            : nullptr;
+                hvd[v - v0] = d;
+                list_off += P[v];
+                ctx->stats.visible += V[v];
+                ctx->stats.pairs += P[v];
+            }
+            const int ngroup = v1 - v0;
+            CK(cudaMemcpyAsync(ctx->views.p, hvd, sizeof(ViewDesc) * ngroup, cudaMemcpyHostToDevice, s));
+            // the binning stream starts after everything already queued on s
+            CK(cudaEventRecord(ctx->ev_ready, s));
+            CK(cudaStreamWaitEvent(sb, ctx->ev_ready, 0));
+            RasterParams rp{};
+            rp.map = map->dev;
+            rp.cam = cam;
+            rp.opt = o;
+            rp.tiles_per_view = rtiles;
+            rp.raster_tiles_x = rtx;
+            rp.channels = rt.channels;
+            rp.groups = map->groups;
+            rp.want_rc = fk == Fisher::Gain ? 1 : 0;
+            for (int s0 = v0; s0 < v1; s0 += kSub) {
+                const int s1 = std::min(v1, s0 + kSub);
+                for (int v = s0; v < s1; ++v) {
+                    const ViewDesc& d = hvd[v - v0];
+                    bin_view(ctx, sb, map, cam, o, ctx->poses.as<PoseParams>() + v,
+                             ctx->keys.as<uint32_t>() + NS * v, const_cast<uint32_t*>(d.order), V[v],
+                             P[v], R[v], const_cast<PackedSplat*>(d.packed), const_cast<uint4*>(d.bounds),
+                             const_cast<uint32_t*>(d.list), const_cast<uint2*>(d.ranges), bin_tiles);
+                }
+                const int slot = (s0 / kSub) & 1;
+                CK(cudaEventRecord(ctx->ev_binned[slot], sb));
+                CK(cudaStreamWaitEvent(s, ctx->ev_binned[slot], 0));
+                rp.views = ctx->views.as<ViewDesc>() + (s0 - v0);
+                const int pr = ((s0 - v0) / kSub) % 8;  // profiling event pair
+                if (ctx->profiling) CK(cudaEventRecord(ctx->ev_r[2 * pr], s));
+                FisherParams fp{};
+                fp.H = d_H;
+                fp.invp = map->fisher_invp.as<double>();
+                if (fk == Fisher::Prior) {
+                    launch_fisher_prior(rp, fp, s1 - s0, s);
+                } else {
+                    if (mode == Mode::Score)
+                        launch_raster_score(rp, s1 - s0, s);
+                    else
+                        launch_raster_render(rp, s1 - s0, s);
+                    if (fk == Fisher::Gain) {
+                        launch_fisher_gain(rp, fp, s1 - s0, s);
+                        ctx->stats.kernel_launches += 1;
+                    }
+                }
+                CK(cudaGetLastError());
+                if (ctx->profiling) CK(cudaEventRecord(ctx->ev_r[2 * pr + 1], s));
+                ctx->stats.kernel_launches += 1;
+                ctx->stats.raster_launches += 1;
+            }
+            if (mode == Mode::Score && fk != Fisher::Prior) {
+                double* dfis = fk == Fisher::Gain ? ctx->out.as<double>() + 2 * ngroup : nullptr;
+                launch_reduce_scores(ctx->views.as<ViewDesc>(), ngroup, rtiles, ctx->out.as<double>(),
+                                     ctx->out.as<double>() + ngroup, dfis, s);
+                ctx->stats.kernel_launches += 1;
+                double* ho = ctx->h_out.as<double>();
+                CK(cudaMemcpyAsync(ho, ctx->out.p, 24 * ngroup, cudaMemcpyDeviceToHost, s));
+                unsigned long long* kc = hp + 2 * B;
+                CK(cudaMemcpyAsync(kc, ctx->contributors.p, 8, cudaMemcpyDeviceToHost, s));
+                CK(cudaMemsetAsync(ctx->contributors.p, 0, 8, s));
+                CK(cudaStreamSynchronize(s));
+                for (int v = 0; v < ngroup; ++v) {
+                    h_missing[b0 + v0 + v] = ho[v];
+                    h_entropy[b0 + v0 + v] = ho[ngroup + v];
+                    if (h_fisher) h_fisher[b0 + v0 + v] = ho[2 * ngroup + v];
+                }
+                ctx->stats.contributors += *kc;
+            } else {
+                unsigned long long* kc = hp + 2 * B;
+                CK(cudaMemcpyAsync(kc, ctx->contributors.p, 8, cudaMemcpyDeviceToHost, s));
+                CK(cudaMemsetAsync(ctx->contributors.p, 0, 8, s));
+                CK(cudaStreamSynchronize(s));
+                ctx->stats.contributors += *kc;
+            }
+            if (ctx->profiling) {
+                const int nsub = std::min(8, (ngroup + kSub - 1) / kSub);
+                for (int q = 0; q < nsub; ++q) {
+                    float ms = 0;
+                    CK(cudaEventElapsedTime(&ms, ctx->ev_r[2 * q], ctx->ev_r[2 * q + 1]));
+                    ctx->stats.raster_ms += ms;
+                }
+            }
+            v0 = v1;
+        }
+        if (ctx->profiling) {
+            CK(cudaEventRecord(ctx->ev[3], s));
+            CK(cudaEventSynchronize(ctx->ev[3]));
+            float total = 0;
+            CK(cudaEventElapsedTime(&total, ctx->ev[0], ctx->ev[3]));
+            ctx->stats.binning_ms += total;  // whole-batch span; raster share in raster_ms
+        }
+        ctx->stats.views += nb;
+        if (mode == Mode::Render) {
+            ctx->last_valid = true;
+            ctx->last_V = V[0];
+            ctx->last_P = P[0];
+            ctx->last_bin_tiles = bin_tiles;
+            ctx->last_map = map;
+            ctx->last_cam = cam;
+            ctx->last_opt = o;
+            ctx->last_pose = poses[0];
+        }
+    }
+}
+
+int guard(sgm_ctx* ctx, const std::function<void()>& fn) {
+    try {
+        fn();
+        if (ctx) ctx->err.clear();
+        return SGM_OK;
+    } catch (const SgmError& e) {
+        if (ctx) ctx->err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        if (ctx) ctx->err = "host allocation failed";
+        return SGM_ERR_OOM;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->err = e.what();
+        return SGM_ERR_INVALID;
+    }
+}
+
+void need_ctx(sgm_ctx* ctx) {
+    if (!ctx) fail(SGM_ERR_INVALID, "ctx is null");
+    CK(cudaSetDevice(ctx->device));
+}
+
+void do_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const sgm_pose* pose,
+               uint32_t channels, const sgm_options* opt, double* d_color, double* d_depth,
+               double* d_sil, double* d_sem, uint64_t* n_proj) {
+    need_ctx(ctx);
+    if (!map) fail(SGM_ERR_INVALID, "map is null");
+    if (!pose) fail(SGM_ERR_INVALID, "pose is null");
+    const CamParams cam = to_cam(camera);
+    const OptParams o = to_opt(opt, cam);
+    const PoseParams p = to_pose(*pose);
+    RenderTargets rt;
+    rt.channels = channels;
+    rt.color = (channels & SGM_COLOR) ? d_color : nullptr;
+    rt.depth = (channels & SGM_DEPTH) ? d_depth : nullptr;
+    rt.sem = (channels & SGM_SEMANTICS) ? d_sem : nullptr;
+    rt.sil = d_sil;
+    ctx->last_has_contrib = false;
+    if (channels & SGM_RETAIN_CONTRIBUTORS) {
+        // pass 1: per-pixel contributor counts (splat_render.cpp:215-216, 310)
+        const size_t px = static_cast<size_t>(cam.W) * cam.H;
+        CK(ctx->ccount.reserve(4 * (px + 1)));
+        CK(ctx->coffset.reserve(8 * (px + 1)));
+        CK(ctx->contrib.reserve(4));
+        CK(cudaMemsetAsync(ctx->ccount.p, 0, 4 * (px + 1), ctx->stream));
+        rt.contrib = ctx->contrib.as<uint32_t>();
+        rt.contrib_count = ctx->ccount.as<uint32_t>();
+        run_views(ctx, map, cam, o, 1, &p, Mode::Render, rt, nullptr, nullptr);
+        // offsets = exclusive scan (flatten_contributors, :125-137)
+        size_t tmp = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ctx->ccount.as<uint32_t>(),
+                                         ctx->coffset.as<unsigned long long>(), px + 1, ctx->stream));
+        CK(ctx->cub_tmp.reserve(tmp));
+        CK(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp, ctx->ccount.as<uint32_t>(),
+                                         ctx->coffset.as<unsigned long long>(), px + 1, ctx->stream));
+        ctx->stats.kernel_launches += 1;
+        unsigned long long total = 0;
+        CK(cudaMemcpyAsync(&total, ctx->coffset.as<unsigned long long>() + px, 8,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (total >= (1ull << 32)) fail(SGM_ERR_UNSUPPORTED, "more than 2^32 contributors");
+        CK(ctx->contrib.reserve(4 * std::max<unsigned long long>(total, 1)));
+        // pass 2: write the depth-ordered contributor ranks
+        rt.contrib = ctx->contrib.as<uint32_t>();
+        rt.contrib_offset = ctx->coffset.as<unsigned long long>();
+        run_views(ctx, map, cam, o, 1, &p, Mode::Render, rt, nullptr, nullptr);
+        ctx->last_ncontrib = total;
+        ctx->last_has_contrib = true;
+        ctx->last_px = static_cast<int>(px);
+    } else {
+        run_views(ctx, map, cam, o, 1, &p, Mode::Render, rt, nullptr, nullptr);
+    }
+    if (n_proj) *n_proj = ctx->last_V;
+}
+
+
+
+// The mapping step on device-resident frame planes: render(all(true)) with contributor
+// counts, mapping_loss + semantic_loss, backward, projection->world chain, KL clip and the
+// finiteness check (losses.cpp:40-362). Gradients stay in ctx->bw_grad:
+//   center 3NS | log_radius NS | opacity_logit NS | color 3NS | sem k*NS | proj 5NS
+// (NS = max(N, 1)); report = LossReport fields. Throws like the reference on a non-finite
+// gradient.
+void backward_core(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const OptParams& o,
+                   const PoseParams& p, const float* f_rgb, const float* f_depth,
+                   const float* f_sem, const double weights[7], int include_mapping,
+                   int include_semantic, double report[7]) {
+    cudaStream_t s = ctx->stream;
+    const size_t px = static_cast<size_t>(cam.W) * cam.H;
+    const int C = map->dev.C, k = map->dev.k;
+    const uint64_t N = map->dev.n;
+    const size_t NS = std::max<uint64_t>(N, 1);
+    // device planes: rendered (sil, color, depth, sem) + frame (rgb, depth, sem)
+    const size_t rend_b = 8 * px * (5 + C);
+    CK(ctx->planes.reserve(rend_b));
+    CK(ctx->ccount.reserve(4 * (px + 1)));
+    CK(ctx->contrib.reserve(4));
+    CK(ctx->bw_flags.reserve(px + 16));
+    const size_t nlb = backward_loss_blocks(cam.W, cam.H);
+    CK(ctx->bw_part.reserve(64 * nlb + 64 + 64));
+    CK(ctx->bw_grad.reserve(8 * (NS * (8 + k) + 5 * NS) + 64));
+    double* d_sil = ctx->planes.as<double>();
+    double* d_color = d_sil + px;
+    double* d_depth = d_color + 3 * px;
+    double* d_sem = d_depth + px;
+    CK(cudaMemsetAsync(ctx->ccount.p, 0, 4 * (px + 1), s));
+    // 1. forward render + contributor counts (the reference's render(..., all(true)))
+    RenderTargets rt;
+    rt.channels = SGM_COLOR | SGM_DEPTH | SGM_SEMANTICS;
+    rt.color = d_color;
+    rt.depth = d_depth;
+    rt.sil = d_sil;
+    rt.sem = d_sem;
+    rt.contrib = ctx->contrib.as<uint32_t>();
+    rt.contrib_count = ctx->ccount.as<uint32_t>();
+    run_views(ctx, map, cam, o, 1, &p, Mode::Render, rt, nullptr, nullptr);
+    const uint32_t V = ctx->last_V;
+    // 2. loss masks, reports and mask counts
+    double* g = ctx->bw_grad.as<double>();
+    BackwardParams b{};
+    b.W = cam.W;
+    b.H = cam.H;
+    b.C = C;
+    b.color = d_color;
+    b.depth = d_depth;
+    b.sil = d_sil;
+    b.sem = d_sem;
+    b.ccount = ctx->ccount.as<uint32_t>();
+    b.rgb = f_rgb;
+    b.fdepth = f_depth;
+    b.fsem = f_sem;
+    b.flags = ctx->bw_flags.as<uint8_t>();
+    b.tau = std::log(weights[2]);
+    b.lambda_hd = weights[0];
+    b.lambda_cos = weights[1];
+    b.use_hd = weights[3] != 0.0;
+    b.use_cos = weights[4] != 0.0;
+    b.use_kl = weights[5] != 0.0;
+    b.include_mapping = include_mapping != 0;
+    b.include_semantic = include_semantic != 0;
+    double* totals = ctx->bw_part.as<double>() + 8 * nlb;
+    b.totals = totals;
+    b.gcenter = g;
+    b.glogr = g + 3 * NS;
+    b.glogit = g + 4 * NS;
+    b.gcolor = g + 5 * NS;
+    b.gsem = g + 8 * NS;
+    b.gproj = g + (8 + k) * NS;
+    b.sem_perm = map->dev.sem_perm;
+    CK(cudaMemsetAsync(g, 0, 8 * (NS * (8 + k) + 5 * NS), s));
+    launch_loss_pixels(b, ctx->bw_part.as<double>(), totals, s);
+    // 3. backward over the block lists of the render above (same binning)
+    RasterParams rp{};
+    rp.map = map->dev;
+    rp.cam = cam;
+    rp.opt = o;
+    rp.views = ctx->views.as<ViewDesc>();
+    rp.tiles_per_view = ((cam.W + kTile - 1) / kTile) * ((cam.H + kTile - 1) / kTile);
+    rp.raster_tiles_x = (cam.W + kTile - 1) / kTile;
+    rp.channels = rt.channels;
+    rp.groups = map->groups;
+    launch_backward(rp, b, s);
+    // 4. projection -> world, KL clipping, finiteness
+    launch_chain(map->dev, ctx->poses.as<PoseParams>(), cam, o, ctx->vals.as<uint32_t>(), V,
+                 b.gproj, b, s);
+    if (b.use_kl && b.include_semantic && weights[6] > 0.0)
+        launch_kl_clip(b.gsem, N, k, weights[6], s);
+    unsigned long long* bad = reinterpret_cast<unsigned long long*>(totals + 8);
+    CK(cudaMemsetAsync(bad, 0xff, 5 * 8, s));
+    const double* arrs[5] = {b.gcenter, b.glogr, b.glogit, b.gcolor, b.gsem};
+    const uint64_t lens[5] = {3 * N, N, N, 3 * N, static_cast<uint64_t>(k) * N};
+    for (int a = 0; a < 5; ++a) launch_finite(arrs[a], lens[a], bad + a, s);
+    ctx->stats.kernel_launches += 4 + 5;
+    CK(cudaGetLastError());
+    double h_tot[8];
+    unsigned long long h_bad[5];
+    CK(cudaMemcpyAsync(h_tot, totals, 64, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_bad, bad, 40, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    static const char* names[5] = {"center", "log_radius", "opacity_logit", "color", "sem"};
+    static const uint64_t stride[5] = {3, 1, 1, 3, 0};
+    for (int a = 0; a < 5; ++a)
+        if (h_bad[a] != ~0ull)  // losses.cpp:349-360
+            fail(SGM_ERR_INVALID, "backward: non-finite gradient for gaussian %llu parameter %s",
+                 static_cast<unsigned long long>(h_bad[a] / (a == 4 ? k : stride[a])), names[a]);
+    report[0] = h_tot[3] > 0 ? h_tot[0] / h_tot[3] : 0.0;  // photometric (:57)
+    report[1] = h_tot[4] > 0 ? h_tot[1] / h_tot[4] : 0.0;  // depth (:58)
+    report[2] = h_tot[5] > 0 ? h_tot[2] / h_tot[5] : 0.0;  // semantic (:158)
+    report[3] = h_tot[3];
+    report[4] = h_tot[4];
+    report[5] = h_tot[5];
+    report[6] = h_tot[6];
+}
+
+
+
+// Device -> pageable host copies of large planes (a full render is px (5 + C) doubles:
+// 698 MB at cfg1). A plain cudaMemcpy to pageable memory is staged by the driver at about
+// 15 GB/s and pays the fresh pages' faults serially; here the planes go through a ring of
+// pinned buffers in kChunk pieces (DMA at full PCIe rate) while a pool of host threads
+// copies the finished pieces out in parallel.
+void copy_out(sgm_ctx* ctx, const std::vector<CopyOut>& segs) {
+    constexpr size_t kChunk = size_t(16) << 20;
+    constexpr int kSlots = 4;
+    cudaStream_t s = ctx->stream;
+    size_t total = 0;
+    for (const auto& g : segs) total += g.bytes;
+    if (total <= 2 * kChunk) {  // small: direct copies
+        for (const auto& g : segs)
+            CK(cudaMemcpyAsync(g.dst, g.src, g.bytes, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        return;
+    }
+    struct Piece {
+        char* dst;
+        const char* src;
+        size_t bytes;
+    };
+    std::vector<Piece> pieces;
+    for (const auto& g : segs)
+        for (size_t o = 0; o < g.bytes; o += kChunk)
+            pieces.push_back({static_cast<char*>(g.dst) + o, static_cast<const char*>(g.src) + o,
+                              std::min(kChunk, g.bytes - o)});
+    CK(ctx->h_ring.reserve(kSlots * kChunk));
+    for (int k = 0; k < kSlots; ++k)
+        if (!ctx->ev_ring[k]) CK(cudaEventCreateWithFlags(&ctx->ev_ring[k], cudaEventDisableTiming));
+    const unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const size_t np = pieces.size();
+    std::unique_ptr<std::atomic<unsigned>[]> copied(new std::atomic<unsigned>[np]);
+    for (size_t j = 0; j < np; ++j) copied[j].store(0);
+    std::atomic<size_t> issued{0};  // pieces whose D2H + event are enqueued
+    std::atomic<int> err{0};
+    auto worker = [&](unsigned w) {
+        for (size_t j = 0; j < np; ++j) {
+            while (issued.load(std::memory_order_acquire) <= j && !err.load()) std::this_thread::yield();
+            if (err.load()) return;
+            const int slot = static_cast<int>(j % kSlots);
+            if (cudaEventSynchronize(ctx->ev_ring[slot]) != cudaSuccess) err.store(1);
+            const Piece& pc = pieces[j];
+            const size_t a = pc.bytes * w / nth, b = pc.bytes * (w + 1) / nth;
+            std::memcpy(pc.dst + a, ctx->h_ring.as<char>() + slot * kChunk + a, b - a);
+            copied[j].fetch_add(1, std::memory_order_release);
+        }
+    };
+    std::vector<std::thread> pool;
+    for (unsigned w = 0; w < nth; ++w) pool.emplace_back(worker, w);
+    cudaError_t e = cudaSuccess;
+    for (size_t j = 0; j < np && e == cudaSuccess; ++j) {
+        const int slot = static_cast<int>(j % kSlots);
+        if (j >= kSlots)  // the slot's previous piece must be copied out first
+            while (copied[j - kSlots].load(std::memory_order_acquire) < nth && !err.load())
+                std::this_thread::yield();
+        e = cudaMemcpyAsync(ctx->h_ring.as<char>() + slot * kChunk, pieces[j].src, pieces[j].bytes,
+                            cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_ring[slot], s);
+        issued.store(j + 1, std::memory_order_release);
+    }
+    if (e != cudaSuccess) err.store(1);
+    for (auto& th : pool) th.join();
+    CK(e);
+    if (err.load()) fail(SGM_ERR_CUDA, "device-to-host copy failed");
+    CK(cudaStreamSynchronize(s));
+}
+
+
+}  // namespace sgm
