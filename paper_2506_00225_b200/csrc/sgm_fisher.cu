@@ -28,7 +28,8 @@ constexpr int kFThreads = 256;
 constexpr int kFNB = 16;
 
 struct FLayout {
-    int f, dr, w, red, gacc, emap, rm, done, pose, stage0, stage_bytes, st_color, total;
+    int f, dr, w, red, gacc, emap, rm, done, pose, segp, sseg, st, sp, src, stage0, stage_bytes,
+        st_color, total;
 };
 
 __host__ __device__ inline FLayout fisher_layout() {
@@ -42,7 +43,12 @@ __host__ __device__ inline FLayout fisher_layout() {
     L.rm = L.emap + 2 * kFNB * 4;             // [2][kFNB] (rank, map index)
     L.done = L.rm + 2 * kFNB * 8;             // [64]
     L.pose = L.done + kTilePx * 4;            // Rcw (9 doubles) + pad
-    L.stage0 = L.pose + 16 * 8;
+    L.segp = L.pose + 16 * 8;                 // [4][64] segment products of (1 - f)
+    L.sseg = L.segp + 4 * kTilePx * 8;        // [4][64][4] segment colour / depth sums
+    L.st = L.sseg + 4 * kTilePx * 4 * 8;      // [64] pixel transmittance at the batch start
+    L.sp = L.st + kTilePx * 8;                // [2][64][4] prefix P at the batch start
+    L.src = L.sp + 2 * kTilePx * 4 * 8;       // [64][4] rendered R (pass 0 result)
+    L.stage0 = L.src + kTilePx * 4 * 8;
     L.st_color = kFNB * static_cast<int>(sizeof(PackedSplat));
     L.stage_bytes = L.st_color + kFNB * 32;
     L.total = L.stage0 + 2 * L.stage_bytes;
@@ -66,6 +72,11 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
     uint2* rm = reinterpret_cast<uint2*>(smem + L.rm);
     int* sdone = reinterpret_cast<int*>(smem + L.done);
     double* sR = reinterpret_cast<double*>(smem + L.pose);  // camera-from-world rotation
+    double* segp = reinterpret_cast<double*>(smem + L.segp);
+    double* sseg = reinterpret_cast<double*>(smem + L.sseg);
+    double* sT = reinterpret_cast<double*>(smem + L.st);
+    double* sPb = reinterpret_cast<double*>(smem + L.sp);
+    double* sRc = reinterpret_cast<double*>(smem + L.src);
     unsigned char* stg = smem + L.stage0;
 
     const ViewDesc vd = p.views[blockIdx.y];
@@ -127,19 +138,25 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
     // gain mode after a score raster that wrote the rendered colour / depth planes (rc4):
     // pass 0 is skipped (the planes are the same sums, in a fixed segment order)
     const bool haveR = kGain && vd.rc4 != nullptr;
+    if (t < kTilePx)
+        for (int ch = 0; ch < 4; ++ch) sRc[t * 4 + ch] = 0.0;
     if (haveR && t < kTilePx && inside) {
         const size_t pix = static_cast<size_t>(y) * p.cam.W + x;
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) Rc[ch] = vd.rc4[pix * 4 + ch];
+        for (int ch = 0; ch < 4; ++ch) sRc[t * 4 + ch] = vd.rc4[pix * 4 + ch];
     }
+    const int part = t >> 6;  // phase AB: this thread's segment (entries 4 part .. 4 part + 3)
     double gsum = 0.0;                     // gain of this tile (thread 0, fixed order)
 
     for (int pass = haveR ? 1 : 0; pass < 2; ++pass) {
-        double T = 1.0;
-        double Pc[4] = {0.0, 0.0, 0.0, 0.0};
-        bool done = !inside;
-        if (t < kTilePx) sdone[t] = inside ? 0 : 1;
+        if (t < kTilePx) {
+            sdone[t] = inside ? 0 : 1;
+            sT[t] = 1.0;
+            for (int ch = 0; ch < 4; ++ch) sPb[t * 4 + ch] = 0.0;
+        }
         __syncthreads();
+        if (pass == 1)
+            for (int ch = 0; ch < 4; ++ch) Rc[ch] = sRc[px * 4 + ch];  // R of this thread's pixel
         cursor = 0;
         fill(0);
         fill(1);
@@ -157,62 +174,115 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
             const double* scol = reinterpret_cast<const double*>(sb + L.st_color);
             const uint32_t* em = emap + (b & 1) * kFNB;
 
-            // phase A: raw footprints (splat_render.cpp:276-285), clamp recorded
-            {
-                const bool pdone = sdone[px] != 0;
+            // phase AB: thread (part, px) owns the contiguous entries 4 part .. 4 part + 3 of
+            // pixel px (warp-uniform entries). Footprints (splat_render.cpp:276-285, clamp
+            // recorded) and the segment product of (1 - f); after a barrier each segment starts
+            // at T_px * prod(earlier segments) (fixed association) and runs the exact chain
+            // (w = f T, T *= 1 - f, exit after accumulating, :312), summing its colour / depth.
+            // Pass 1 then forms dR/df_j = v T_j - (R - P_j) / (1 - f_j) (losses.cpp:285-288)
+            // with P_j = P at the batch start + earlier segments' sums + the local prefix.
+            const bool pdone = sdone[px] != 0;
+            const double T0 = sT[px];
+            double fcode[4];
+            double prod = 1.0;
 #pragma unroll
-                for (int i = 0; i < kFNB / 4; ++i) {
-                    const int e = e_first + 4 * i;
-                    if (e >= n) break;
-                    double f = kNotContrib;
-                    if (!pdone) {
-                        const float4 pf = *reinterpret_cast<const float4*>(&sp[e].pmx);
-                        const float fdx = fpx - pf.x;
-                        const float fdy = fpy - pf.y;
-                        if (!(fdx * fdx + fdy * fdy > pf.z)) {
-                            const double dx = dpx - sp[e].mx;
-                            const double dy = dpy - sp[e].my;
-                            const double d2 = dx * dx + dy * dy;
-                            if (!(d2 > sp[e].cutoff_d2)) {
-                                f = sp[e].alpha * exp_footprint(-d2 * sp[e].inv_two_r2);
-                                if (f > kMaxFootprint) f = kClamped;
-                            }
+            for (int i = 0; i < 4; ++i) {
+                const int e = 4 * part + i;
+                double f = kNotContrib;
+                if (e < n && !pdone) {
+                    const float4 pf = *reinterpret_cast<const float4*>(&sp[e].pmx);
+                    const float fdx = fpx - pf.x;
+                    const float fdy = fpy - pf.y;
+                    if (!(fdx * fdx + fdy * fdy > pf.z)) {
+                        const double dx = dpx - sp[e].mx;
+                        const double dy = dpy - sp[e].my;
+                        const double d2 = dx * dx + dy * dy;
+                        if (!(d2 > sp[e].cutoff_d2)) {
+                            f = sp[e].alpha * exp_footprint(-d2 * sp[e].inv_two_r2);
+                            if (f > kMaxFootprint) f = kClamped;
                         }
                     }
-                    F[e * kTilePx + px] = f;
                 }
+                fcode[i] = f;
+                if (f != kNotContrib) prod = prod * (1.0 - (f == kClamped ? kMaxFootprint : f));
+            }
+            segp[part * kTilePx + px] = prod;
+            __syncthreads();
+            double Ts = T0;
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+                if (q < part) Ts = Ts * segp[q * kTilePx + px];
+            bool exited = pdone || (p.opt.early_exit && Ts < p.opt.eps);
+            double Tc = Ts;
+            double Sg[4] = {0.0, 0.0, 0.0, 0.0};
+            double Tj[4], wj[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int e = 4 * part + i;
+                Tj[i] = 0.0;
+                wj[i] = 0.0;
+                if (e >= n) continue;
+                const int s = e * kTilePx + px;
+                if (exited || fcode[i] == kNotContrib) {
+                    fcode[i] = kNotContrib;
+                    F[s] = kNotContrib;
+                    continue;
+                }
+                F[s] = fcode[i];
+                const double f = fcode[i] == kClamped ? kMaxFootprint : fcode[i];
+                const double w = f * Tc;
+                Tj[i] = Tc;
+                wj[i] = w;
+                if (pass == 1) Wv[s] = w;
+                const double v[4] = {scol[4 * e], scol[4 * e + 1], scol[4 * e + 2], sp[e].z};
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) Sg[ch] += v[ch] * w;
+                Tc = Tc * (1.0 - f);
+                if (p.opt.early_exit && Tc < p.opt.eps) exited = true;
+            }
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) sseg[(part * kTilePx + px) * 4 + ch] = Sg[ch];
+            if (part == 3) {  // the pixel's T and done flag for the next batch
+                sT[px] = Tc;
+                sdone[px] = (pdone || (p.opt.early_exit && Tc < p.opt.eps)) ? 1 : 0;
             }
             __syncthreads();
-
-            // phase B: transmittance chain of pixel t
-            if (t < kTilePx) {
-                for (int e = 0; e < n; ++e) {
-                    const int s = e * kTilePx + t;
-                    const double code = F[s];
-                    if (done || code == kNotContrib) {
-                        F[s] = kNotContrib;
-                        continue;
-                    }
-                    const double f = code == kClamped ? kMaxFootprint : code;
-                    const double w = f * T;
-                    const double v[4] = {scol[4 * e], scol[4 * e + 1], scol[4 * e + 2], sp[e].z};
-                    if (pass == 0) {
+            {
+                const double* Pb = sPb + (b & 1) * kTilePx * 4;
+                double* Pn = sPb + ((b + 1) & 1) * kTilePx * 4;
+                if (pass == 0) {
+                    if (part == 0)  // R accumulates batch by batch, segments in a fixed order
+                        for (int ch = 0; ch < 4; ++ch)
+                            sRc[px * 4 + ch] += ((sseg[(0 * kTilePx + px) * 4 + ch] + sseg[(1 * kTilePx + px) * 4 + ch]) +
+                                                 sseg[(2 * kTilePx + px) * 4 + ch]) + sseg[(3 * kTilePx + px) * 4 + ch];
+                } else {
+                    double P[4];
 #pragma unroll
-                        for (int ch = 0; ch < 4; ++ch) Rc[ch] += v[ch] * w;
-                    } else {
-                        // dR/df_j = v T_j - S / (1 - f_j), S = R - P_j  (losses.cpp:285-288)
+                    for (int ch = 0; ch < 4; ++ch) {
+                        P[ch] = Pb[px * 4 + ch];
+#pragma unroll
+                        for (int q = 0; q < 3; ++q)
+                            if (q < part) P[ch] += sseg[(q * kTilePx + px) * 4 + ch];
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int e = 4 * part + i;
+                        if (e >= n || fcode[i] == kNotContrib) continue;
+                        const double f = fcode[i] == kClamped ? kMaxFootprint : fcode[i];
                         const double i1f = 1.0 / (1.0 - f);
+                        const double v[4] = {scol[4 * e], scol[4 * e + 1], scol[4 * e + 2], sp[e].z};
 #pragma unroll
                         for (int ch = 0; ch < 4; ++ch) {
-                            Pc[ch] += v[ch] * w;
-                            DR[(ch * kFNB + e) * kTilePx + t] = v[ch] * T - (Rc[ch] - Pc[ch]) * i1f;
+                            P[ch] += v[ch] * wj[i];
+                            DR[(ch * kFNB + e) * kTilePx + px] = v[ch] * Tj[i] - (Rc[ch] - P[ch]) * i1f;
                         }
-                        Wv[s] = w;
                     }
-                    T = T * (1.0 - f);
-                    if (p.opt.early_exit && T < p.opt.eps) done = true;
+                    if (part == 0)  // P at the next batch's start (the other buffer)
+                        for (int ch = 0; ch < 4; ++ch)
+                            Pn[px * 4 + ch] = Pb[px * 4 + ch] +
+                                              (((sseg[(0 * kTilePx + px) * 4 + ch] + sseg[(1 * kTilePx + px) * 4 + ch]) +
+                                                sseg[(2 * kTilePx + px) * 4 + ch]) + sseg[(3 * kTilePx + px) * 4 + ch]);
                 }
-                sdone[t] = done ? 1 : 0;
             }
             __syncthreads();
 
@@ -303,8 +373,7 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
                 if (kGain && t == 0)
                     for (int u = 0; u < 8; ++u) gsum += red[u];
             }
-            const int mine = (t < kTilePx) ? (done ? 1 : 0) : 1;
-            if (__syncthreads_and(mine)) break;
+            if (__syncthreads_and(sdone[px])) break;
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
