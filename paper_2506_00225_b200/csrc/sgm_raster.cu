@@ -93,8 +93,10 @@ __device__ __forceinline__ int px_row(int q) { return (q >> 5) * 4 + ((q >> 2) &
 
 // kRc (score mode): also accumulate each pixel's rendered colour and depth, written to
 // vd.rc4[px][4] (the Fisher gain's pass-0 quantity, losses.cpp:285-288)
-template <bool kRender, bool kDup, bool kAniso, bool kRc = false>
-__global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
+// kOcc: CTAs per SM the register budget is sized for; 4 when the shared-memory footprint
+// allows it (small C, e.g. cfg3's 42 channels), else 3 (the 102-channel accumulator).
+template <bool kRender, bool kDup, bool kAniso, bool kRc = false, int kOcc = 3>
+__global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int C = p.map.C;
     const int kpad = p.map.kpad;
@@ -516,12 +518,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster(RasterParams p) {
 
 template <bool kRender, bool kDup, bool kAniso, bool kRc = false>
 void launch_t(const RasterParams& p, int n_views, cudaStream_t s) {
-    auto kern = k_raster<kRender, kDup, kAniso, kRc>;
     const size_t smem = static_cast<size_t>(make_layout(p.map.C, p.map.kpad, kRender, kRc).total);
-    static size_t configured = 0;
-    if (smem > configured) {
+    // four CTAs per SM when four fit in shared memory (228 KB, 1 KB reserved per CTA)
+    const bool four = smem + 2048 <= 228 * 1024 / 4;
+    auto kern = four ? k_raster<kRender, kDup, kAniso, kRc, 4> : k_raster<kRender, kDup, kAniso, kRc, 3>;
+    static size_t configured[2] = {0, 0};
+    if (smem > configured[four]) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        configured = smem;
+        configured[four] = smem;
     }
     dim3 grid(static_cast<unsigned>(p.tiles_per_view), static_cast<unsigned>(n_views), 1);
     kern<<<grid, kThreads, smem, s>>>(p);
