@@ -194,6 +194,9 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     __syncthreads();
     if (scnt[0] > 0) issue(0);
 
+    // render with retained contributor lists keeps the sequential per-pixel chain (the lists
+    // are written in depth order); every other launch uses the fused segmented chain
+    const bool seq = kRender && vd.contrib != nullptr;
     const double dpx = x + 0.5, dpy = y + 0.5;                                 // :261, :263
     const float fpx = static_cast<float>(dpx), fpy = static_cast<float>(dpy);  // :274
     // phase-B state (warps 0-1 own pixel t)
@@ -258,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         };
 
         uint32_t nzbits = 0;  // entries this thread gave a nonzero weight
-        if (kRender) {
+        if (seq) {
             // ---- phase A: footprints (independent of T) ----
             {
                 const bool pdone = sdone[px] != 0;
@@ -337,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                 const double wv = f[i] * Tc;
                 W[s] = wv;
                 if (wv != 0.0) nzbits |= 1u << e;
-                if (kRc) {  // this segment's share of the pixel's colour / depth (:289-293)
+                if (kRc || kRender) {  // this segment's share of the colour / depth (:289-293)
                     rcs[0] += scol[4 * e] * wv;
                     rcs[1] += scol[4 * e + 1] * wv;
                     rcs[2] += scol[4 * e + 2] * wv;
@@ -347,9 +350,13 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                 Tc = Tc * (1.0 - f[i]);
                 if (p.opt.early_exit && Tc < p.opt.eps) exited = true;
             }
-            if (part == 3) {
-                sT[px] = Tc;  // product over the batch (only its == 1 / < eps matter later)
-                sdone[px] = (pdone || (p.opt.early_exit && Tc < p.opt.eps)) ? 1 : 0;
+            // The pixel's T after the batch: the T of the segment where it exits (at most one
+            // segment can: the later ones start below eps), else the last segment's. A pixel
+            // done before the batch keeps its T. So the silhouette 1 - T is the reference's.
+            const bool start_exited = pdone || (p.opt.early_exit && Ts < p.opt.eps);
+            if ((!start_exited && exited) || (part == 3 && !start_exited)) {
+                sT[px] = Tc;
+                sdone[px] = exited ? 1 : 0;
             }
         }
         {
@@ -407,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                 }
             }
         }
-        mine = kRender ? ((t < kTilePx) ? (done ? 1 : 0) : 1) : sdone[px];
+        mine = seq ? ((t < kTilePx) ? (done ? 1 : 0) : 1) : sdone[px];
     }
     cp_async_wait_all();
     __syncthreads();
@@ -415,6 +422,25 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     __shared__ double red_d[kTilePx];
     __shared__ unsigned long long red_u[kTilePx];
     if (kRender) {
+        if (!seq) {  // fused chain: the pixel's 4 segment sums in a fixed order, T from sT
+            double* rcx = reinterpret_cast<double*>(stg);  // stages are free now: [4][64][4]
+            const int part = t >> 6;
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) rcx[(part * kTilePx + px) * 4 + ch] = rcs[ch];
+            __syncthreads();
+            if (t < kTilePx) {
+                double r4[4];
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch)
+                    r4[ch] = ((rcx[(0 * kTilePx + t) * 4 + ch] + rcx[(1 * kTilePx + t) * 4 + ch]) +
+                              rcx[(2 * kTilePx + t) * 4 + ch]) + rcx[(3 * kTilePx + t) * 4 + ch];
+                ac0 = r4[0];
+                ac1 = r4[1];
+                ac2 = r4[2];
+                adep = r4[3];
+                T = sT[t];
+            }
+        }
         if (t < kTilePx && inside) {
             const size_t pix = static_cast<size_t>(y) * p.cam.W + x;
             if (vd.sil) vd.sil[pix] = 1.0 - T;  // :314
@@ -500,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         }
     }
     // K (contributors) for the measurement counters
-    if (kRender) {
+    if (seq) {
         if (t < kTilePx) red_u[t] = contrib;
     } else {
         for (int q = 0; q < 4; ++q) {  // fold the 4 segment threads of each pixel, in order
