@@ -36,12 +36,17 @@ namespace sgm {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
+constexpr int kCompute = 256;           // compute threads: warps 0-7
+constexpr int kWarps = kCompute / 32;
+constexpr int kThreads = kCompute + 32;  // + warp 8, the batch loader
 constexpr int kNB = 16;            // Gaussians per staged batch
 constexpr int kGroups = kWarps;    // channel groups: one warp each in phase C
 
 __host__ __device__ constexpr int align16(int b) { return (b + 15) & ~15; }
+
+// barrier over the 8 compute warps only (the loader warp runs ahead between the per-batch
+// block barriers)
+__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(kCompute) : "memory"); }
 
 struct Layout {  // byte offsets in dynamic shared memory
     int acc, w, segp, tpx, done, rm, stage0, stage_bytes, st_packed, st_bnd, st_idx, st_prob,
@@ -132,6 +137,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     const int g = warp;  // phase C / epilogue channel group
     const int c0 = g * Cg, c1 = min(C, c0 + Cg);
 
+    const bool loader = warp == kWarps;
     for (int i = t; i < C * apitch; i += kThreads) acc2[i] = make_double2(0.0, 0.0);
     if (t < kTilePx) {
         sdone[t] = inside ? 0 : 1;
@@ -142,11 +148,11 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     const int qi = kpad / 8, qp = kpad / 2;
     const int Q = 5 + qi + qp + ((kRender || kRc) ? 2 : 0);  // 16-byte chunks per Gaussian
     __shared__ int scnt[3];  // entries of batch b in scnt[b % 3]
-    auto issue = [&](int b) {
+    auto issue = [&](int b) {  // loader warp
         unsigned char* sb = stg + (b & 1) * L.stage_bytes;
         const int n = scnt[b % 3];
         const uint2* slot = rm + (b & 1) * kNB;
-        for (int c = t; c < n * Q; c += kThreads) {
+        for (int c = lane; c < n * Q; c += 32) {
             const int e = c / Q;
             int q = c - e * Q;
             const uint2 v = slot[e];
@@ -173,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         }
         cp_async_commit();
     };
-    // Batches are formed by warp 0 two ahead: the next kNB entries of the bin (depth
+    // Batches are formed by the loader warp two ahead (off the compute warps' path): the next kNB entries of the bin (depth
     // order) that can reach a pixel of this block. An entry whose float probe circle
     // (:276-278) misses the box of the block's pixel centres by a relative margin above
     // the probe's rounding cannot pass the prefilter at any pixel, so skipping it changes
@@ -181,18 +187,19 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     // tile rectangle (:205-209). (The anisotropic mode has no float probe: no skipping.)
     const float bx0 = static_cast<float>(bx * kTile) + 0.5f, bx1 = bx0 + static_cast<float>(kTile - 1);
     const float by0 = static_cast<float>(by * kTile) + 0.5f, by1 = by0 + static_cast<float>(kTile - 1);
-    uint32_t cursor = 0;  // warp 0: next bin entry to examine
+    uint32_t cursor = 0;  // loader: next bin entry to examine
     auto fill = [&](int b) {
-        if (warp != 0) return;
         const int filled = fill_batch<kNB>(vd, L0, Ln, cursor, rm + (b & 1) * kNB, !kAniso, bx0, bx1,
                                            by0, by1, lane);
         if (lane == 0) scnt[b % 3] = filled;
     };
 
-    fill(0);
-    fill(1);
+    if (loader) {  // only batch 0 on the tile's start-up path; batch 1 is formed in iteration 0
+        fill(0);
+        __syncwarp();
+        if (scnt[0] > 0) issue(0);
+    }
     __syncthreads();
-    if (scnt[0] > 0) issue(0);
 
     // render with retained contributor lists keeps the sequential per-pixel chain (the lists
     // are written in depth order); every other launch uses the fused segmented chain
@@ -211,17 +218,24 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     __shared__ uint32_t slive[2];  // batch b: entries with a nonzero weight at some pixel
     if (t < 2) slive[t] = 0u;
     double rcs[4] = {0.0, 0.0, 0.0, 0.0};  // kRc: this (segment, pixel) thread's colour / depth
-    int mine = 0;  // this thread's vote that its pixel is done (the block stops when all are)
+    int mine = loader ? 1 : 0;  // vote that this thread's pixel is done (the block stops when all are)
     for (int b = 0;; ++b) {
         cp_async_wait_all();
-        // batch b landed; rm slot for b+1 visible; W / bnd free; and the early termination
+        // batch b landed; scnt for b+1 visible; W / bnd free; and the early termination
         // of the whole block (:312 for every pixel) decided on the previous batch's votes
         if (__syncthreads_and(mine)) break;
         const int n = scnt[b % 3];
         if (n == 0) break;  // the bin is exhausted
+        if (loader) {  // batch b+1 in flight while the compute warps blend batch b
+            if (b == 0) {
+                fill(1);
+                __syncwarp();
+            }
+            if (scnt[(b + 1) % 3] > 0) issue(b + 1);
+            fill(b + 2);  // rm slot b & 1 (batch b was issued last iteration), scnt[(b + 2) % 3]
+            continue;
+        }
         if (t == 0) slive[(b + 1) & 1] = 0u;  // last read by phase C of batch b - 1
-        if (scnt[(b + 1) % 3] > 0) issue(b + 1);
-        fill(b + 2);  // rm slot b & 1 (batch b was issued last iteration), scnt[(b + 2) % 3]
         const unsigned char* sb = stg + (b & 1) * L.stage_bytes;
         const PackedSplat* sp = reinterpret_cast<const PackedSplat*>(sb + L.st_packed);
         const uint16_t* sbnd = reinterpret_cast<const uint16_t*>(sb + L.st_bnd);  // [kNB][8]
@@ -272,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                     W[pair_slot(e, 32, px)] = pdone ? -1.0 : footprint(e);
                 }
             }
-            __syncthreads();
+            compute_sync();
             // ---- phase B: transmittance chain (:286-312), sequential per pixel (warps 0-1):
             // colour/depth and the ordered contributor lists of retain_contributors ----
             if (t < kTilePx) {
@@ -321,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                 if (f[i] >= 0.0) prod = prod * (1.0 - f[i]);
             }
             segp[part * kTilePx + px] = prod;
-            __syncthreads();
+            compute_sync();
             double Ts = T0;
 #pragma unroll
             for (int q = 0; q < 3; ++q)
@@ -363,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
             const uint32_t lv = __reduce_or_sync(0xffffffffu, nzbits);
             if (lane == 0 && lv) atomicOr(&slive[b & 1], lv);
         }
-        __syncthreads();
+        compute_sync();
 
         // ---- phase C: sparse semantic scatter; warp g = channel group g, 64 px ----
         if (want_sem) {
@@ -425,8 +439,9 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         if (!seq) {  // fused chain: the pixel's 4 segment sums in a fixed order, T from sT
             double* rcx = reinterpret_cast<double*>(stg);  // stages are free now: [4][64][4]
             const int part = t >> 6;
+            if (!loader)
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch) rcx[(part * kTilePx + px) * 4 + ch] = rcs[ch];
+                for (int ch = 0; ch < 4; ++ch) rcx[(part * kTilePx + px) * 4 + ch] = rcs[ch];
             __syncthreads();
             if (t < kTilePx) {
                 double r4[4];
@@ -483,8 +498,10 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                 S2y = __fma_rn(ay, log_table(ay), S2y);
             }
         }
-        red[g * kTilePx + 2 * lane] = make_double2(S1x, S2x);
-        red[g * kTilePx + 2 * lane + 1] = make_double2(S1y, S2y);
+        if (!loader) {
+            red[g * kTilePx + 2 * lane] = make_double2(S1x, S2x);
+            red[g * kTilePx + 2 * lane + 1] = make_double2(S1y, S2y);
+        }
         __syncthreads();
         if (t < kTilePx) {
             double S1 = 0.0, S2 = 0.0;
@@ -514,8 +531,9 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         double* rcx = reinterpret_cast<double*>(stg);  // stages are free now: [4][64][4]
         __syncthreads();
         const int part = t >> 6;
+        if (!loader)
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) rcx[(part * kTilePx + px) * 4 + ch] = rcs[ch];
+            for (int ch = 0; ch < 4; ++ch) rcx[(part * kTilePx + px) * 4 + ch] = rcs[ch];
         __syncthreads();
         if (t < kTilePx && inside) {
             const size_t pix = static_cast<size_t>(y) * p.cam.W + x;
@@ -546,8 +564,11 @@ template <bool kRender, bool kDup, bool kAniso, bool kRc = false>
 void launch_t(const RasterParams& p, int n_views, cudaStream_t s) {
     const size_t smem = static_cast<size_t>(make_layout(p.map.C, p.map.kpad, kRender, kRc).total);
     // four CTAs per SM when four fit in shared memory (228 KB, 1 KB reserved per CTA)
-    const bool four = smem + 2048 <= 228 * 1024 / 4;
-    auto kern = four ? k_raster<kRender, kDup, kAniso, kRc, 4> : k_raster<kRender, kDup, kAniso, kRc, 3>;
+    // (score mode only: the render and rc variants would spill at the 4-CTA register budget)
+    const bool four = !kRender && !kRc && smem + 2048 <= 228 * 1024 / 4;
+    auto kern = k_raster<kRender, kDup, kAniso, kRc, 3>;
+    if constexpr (!kRender && !kRc)
+        if (four) kern = k_raster<kRender, kDup, kAniso, kRc, 4>;
     static size_t configured[2] = {0, 0};
     if (smem > configured[four]) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
