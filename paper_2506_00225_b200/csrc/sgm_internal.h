@@ -169,6 +169,8 @@ struct RasterParams {
     uint32_t channels;   // SGM_COLOR | SGM_DEPTH | SGM_SEMANTICS
     GroupParams groups;
     int want_rc;         // score mode: also write vd.rc4 (colour / depth per pixel)
+    int n_items;         // raster: (view, block) items of the launch (set by the launcher)
+    int items_per_cta;   // raster: consecutive items per CTA (set by the launcher)
 };
 
 // ---- launchers (sgm_kernels.cu) ----

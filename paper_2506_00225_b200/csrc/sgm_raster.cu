@@ -6,22 +6,22 @@
 // written explicitly (__fma_rn) below: the semantic scatter and the exp
 // polynomial. Both stay within ~1 ulp of the reference's fp64 arithmetic.
 //
-// One CTA (8 warps, 256 threads) = one 8x8 pixel block of one view. Per batch of
-// kNB Gaussians (depth order), streamed through shared memory by a
-// double-buffered cp.async pipeline:
-//   phase A  all 8 warps: footprint f[e][px] for kNB x 64 (entry, pixel) pairs,
-//            4 independent entries per thread (probe test, exact d2 test, exp);
-//   phase B  warps 0-1: the exact sequential transmittance chain per pixel
-//            (w = f T; T *= 1 - f; early exit), colour/depth in render mode;
-//            warps 2-7: per entry, the bounds of its sparse row in each of the
-//            4 channel groups (rows are class-sorted at upload);
-//   phase C  all 8 warps: the sparse semantic scatter. Warp g owns channel
-//            group g (C/8 channels) for all 64 pixels, two pixels per lane, so no
-//            two warps touch the same accumulator word. The accumulator is
-//            [C][32] double2 in shared memory (lane l holds pixels 2l, 2l+1):
-//            one LDS.128 / 2 DFMA / STS.128 per (Gaussian, class) entry covers
-//            the whole 8x8 block, and a warp's lanes hit 32 consecutive 16-byte
-//            words (no bank conflict).
+// One CTA = 8 compute warps + 1 loader warp; it blends kItemsPerCta consecutive 8x8 pixel
+// blocks (of one view, or crossing into the next). Per block, the loader forms batches of
+// kNB Gaussians (depth order) two ahead and streams their rows through shared memory with
+// cp.async (double-buffered); per batch the compute warps run
+//   phase AB footprints and the exact transmittance chain, fused: thread (part, px) owns 4
+//            contiguous entries of pixel px; segment products meet in shared memory
+//            (render with retained contributor lists: footprints, then the sequential
+//            per-pixel chain, so the lists come out in depth order);
+//   phase C  the sparse semantic scatter. Warp g owns channel group g (C/8 channels) for
+//            all 64 pixels, two pixels per lane, so no two warps touch the same
+//            accumulator word. The accumulator is [C][32] double2 in shared memory (lane l
+//            holds pixels 2l, 2l+1): one LDS.128 / 2 DFMA / STS.128 per (Gaussian, class)
+//            entry covers the whole 8x8 block, and a warp's lanes hit 32 consecutive
+//            16-byte words (no bank conflict).
+// While the compute warps run a block's epilogue the loader stages the next block's first
+// batch.
 // Score epilogue: per (pixel, group) S1 = sum c, S2 = sum c ln c with
 // c = clamp(p, 1e-3, 1) (a 128-entry table log, ~1 ulp); H = ln S1 - S2/S1
 // (== -sum q ln q, q = c / S1); the tile's
@@ -41,6 +41,10 @@ constexpr int kWarps = kCompute / 32;
 constexpr int kThreads = kCompute + 32;  // + warp 8, the batch loader
 constexpr int kNB = 16;            // Gaussians per staged batch
 constexpr int kGroups = kWarps;    // channel groups: one warp each in phase C
+// (view, block) items blended by one CTA in sequence. Measured on cfg1 (ms per 64 views):
+// 1: 81.1, 2: 78.5, 4: 77.7, 8: 78.0, 16: 79.5; a persistent grid (one wave, items from an
+// atomic counter) took 88.3, its CTAs holding the SMs the binning stream needs.
+constexpr int kItemsPerCta = 4;
 
 __host__ __device__ constexpr int align16(int b) { return (b + 15) & ~15; }
 
@@ -100,6 +104,11 @@ __device__ __forceinline__ int px_row(int q) { return (q >> 5) * 4 + ((q >> 2) &
 // vd.rc4[px][4] (the Fisher gain's pass-0 quantity, losses.cpp:285-288)
 // kOcc: CTAs per SM the register budget is sized for; 4 when the shared-memory footprint
 // allows it (small C, e.g. cfg3's 42 channels), else 3 (the 102-channel accumulator).
+//
+// Each CTA blends p.items_per_cta consecutive (view, block) items; the loader warp stages
+// the next block's first batch while the compute warps run the current block's epilogue.
+// (Not a persistent grid: CTAs still retire often enough for the prioritised binning
+// stream's kernels to take their slots.)
 template <bool kRender, bool kDup, bool kAniso, bool kRc = false, int kOcc = 3>
 __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -118,40 +127,46 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     int* sdone = reinterpret_cast<int*>(smem + L.done);            // [64]
     uint2* rm = reinterpret_cast<uint2*>(smem + L.rm);             // [2][kNB] (rank, map index)
     unsigned char* stg = smem + L.stage0;
-    double2* red = reinterpret_cast<double2*>(stg);                // [kGroups][64], epilogue
+    // epilogue exchanges reuse the weight buffer (the stages then hold the next block's
+    // first batch): [kGroups][64] double2 (entropy) or [4][64][4] double (colour / depth)
+    double2* red = reinterpret_cast<double2*>(smem + L.w);
+    double* rcx = reinterpret_cast<double*>(smem + L.w);
 
-    const ViewDesc vd = p.views[blockIdx.y];
-    const int tile = blockIdx.x;
-    const int bx = tile % p.raster_tiles_x, by = tile / p.raster_tiles_x;
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
-    const int px = t & (kTilePx - 1);  // this thread's pixel in phase A / B / epilogues
-    const int x = bx * kTile + px_col(px);
-    const int y = by * kTile + px_row(px);
-    const bool inside = x < p.cam.W && y < p.cam.H;
-    const int bin = ((by * kTile) / p.opt.ts) * p.opt.tiles_x + (bx * kTile) / p.opt.ts;
-    const uint2 rg = vd.ranges[bin];
-    const uint32_t L0 = rg.x;
-    const uint32_t Ln = rg.y - rg.x;
-    const bool want_sem = !kRender || vd.sem != nullptr;
-    const int g = warp;  // phase C / epilogue channel group
-    const int c0 = g * Cg, c1 = min(C, c0 + Cg);
-
     const bool loader = warp == kWarps;
-    for (int i = t; i < C * apitch; i += kThreads) acc2[i] = make_double2(0.0, 0.0);
-    if (t < kTilePx) {
-        sdone[t] = inside ? 0 : 1;
-        sT[t] = 1.0;
-    }
+    const int px = t & (kTilePx - 1);  // this thread's pixel in phase A / B / epilogues
+    const int g = warp;                // phase C / epilogue channel group
+    const int c0 = g * Cg, c1 = min(C, c0 + Cg);
+    const int tpv = p.tiles_per_view;
+    const int total = p.n_items;
 
-    // ---- cp.async pipeline over batches of kNB Gaussians (depth-rank order) ----
+    __shared__ int scnt[2][3];  // block parity q: entries of batch b in scnt[q][b % 3]
+    __shared__ uint32_t slive[2];  // batch b: entries with a nonzero weight at some pixel
+    __shared__ int s_item;
+    __shared__ double red_d[kTilePx];
+    __shared__ unsigned long long red_u[kTilePx];
+
+    // ---- loader state (in shared memory, so the compute warps carry no registers for it):
+    // the block it stages for, the current one and then the next ----
     const int qi = kpad / 8, qp = kpad / 2;
     const int Q = 5 + qi + qp + ((kRender || kRc) ? 2 : 0);  // 16-byte chunks per Gaussian
-    __shared__ int scnt[3];  // entries of batch b in scnt[b % 3]
-    auto issue = [&](int b) {  // loader warp
+    struct LoaderState {
+        const uint32_t* list;
+        const PackedSplat* packed;
+        const uint4* bounds;
+        const uint32_t* order;
+        uint32_t L0, Ln, cursor;  // cursor: next bin entry to examine
+        float bx0, bx1, by0, by1;
+        int q;  // parity of the loader's block
+    };
+    __shared__ LoaderState ls;
+    auto issue = [&](int b) {  // cp.async of batch b's rows into stage b & 1
         unsigned char* sb = stg + (b & 1) * L.stage_bytes;
-        const int n = scnt[b % 3];
+        const int n = scnt[ls.q][b % 3];
         const uint2* slot = rm + (b & 1) * kNB;
+        const PackedSplat* l_packed = ls.packed;
+        const uint4* l_bounds = ls.bounds;
         for (int c = lane; c < n * Q; c += 32) {
             const int e = c / Q;
             int q = c - e * Q;
@@ -159,10 +174,10 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
             const unsigned char* src;
             unsigned char* dst;
             if (q < 4) {
-                src = reinterpret_cast<const unsigned char*>(vd.packed + v.x) + 16 * q;
+                src = reinterpret_cast<const unsigned char*>(l_packed + v.x) + 16 * q;
                 dst = sb + L.st_packed + e * 64 + 16 * q;
             } else if (q == 4) {
-                src = reinterpret_cast<const unsigned char*>(vd.bounds + v.x);
+                src = reinterpret_cast<const unsigned char*>(l_bounds + v.x);
                 dst = sb + L.st_bnd + e * 16;
             } else if ((q -= 5) < qi) {
                 src = reinterpret_cast<const unsigned char*>(p.map.sem_idx + static_cast<size_t>(v.y) * kpad) + 16 * q;
@@ -179,389 +194,442 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         }
         cp_async_commit();
     };
-    // Batches are formed by the loader warp two ahead (off the compute warps' path): the next kNB entries of the bin (depth
-    // order) that can reach a pixel of this block. An entry whose float probe circle
-    // (:276-278) misses the box of the block's pixel centres by a relative margin above
-    // the probe's rounding cannot pass the prefilter at any pixel, so skipping it changes
-    // nothing; about a fifth of the bin entries are such corner entries of the square
-    // tile rectangle (:205-209). (The anisotropic mode has no float probe: no skipping.)
-    const float bx0 = static_cast<float>(bx * kTile) + 0.5f, bx1 = bx0 + static_cast<float>(kTile - 1);
-    const float by0 = static_cast<float>(by * kTile) + 0.5f, by1 = by0 + static_cast<float>(kTile - 1);
-    uint32_t cursor = 0;  // loader: next bin entry to examine
+    // Batches are formed by the loader warp two ahead (off the compute warps' path): the
+    // next kNB entries of the bin (depth order) that can reach a pixel of this block. An
+    // entry whose float probe circle (:276-278) misses the box of the block's pixel centres
+    // by a relative margin above the probe's rounding cannot pass the prefilter at any
+    // pixel, so skipping it changes nothing; about a fifth of the bin entries are such
+    // corner entries of the square tile rectangle (:205-209). (The anisotropic mode has no
+    // float probe: no skipping.)
     auto fill = [&](int b) {
-        const int filled = fill_batch<kNB>(vd, L0, Ln, cursor, rm + (b & 1) * kNB, !kAniso, bx0, bx1,
-                                           by0, by1, lane);
-        if (lane == 0) scnt[b % 3] = filled;
+        ViewDesc lv;
+        lv.list = ls.list;
+        lv.packed = ls.packed;
+        lv.order = ls.order;
+        uint32_t cursor = ls.cursor;
+        const int filled = fill_batch<kNB>(lv, ls.L0, ls.Ln, cursor, rm + (b & 1) * kNB, !kAniso, ls.bx0,
+                                           ls.bx1, ls.by0, ls.by1, lane);
+        __syncwarp();
+        if (lane == 0) {
+            scnt[ls.q][b % 3] = filled;
+            ls.cursor = cursor;
+        }
+        __syncwarp();
+    };
+    // claim the next block and stage its batch 0 (loader warp)
+    int nclaimed = 0;
+    auto claim = [&]() {
+        const int it = nclaimed < p.items_per_cta ? blockIdx.x * p.items_per_cta + nclaimed : total;
+        ++nclaimed;
+        if (lane == 0) s_item = it;
+        if (it >= total) return;
+        const int view = it / tpv, tile = it - view * tpv;
+        const ViewDesc* v = p.views + view;
+        const int tbx = tile % p.raster_tiles_x, tby = tile / p.raster_tiles_x;
+        const int bin = ((tby * kTile) / p.opt.ts) * p.opt.tiles_x + (tbx * kTile) / p.opt.ts;
+        const uint2 rg = v->ranges[bin];
+        if (lane == 0) {
+            ls.list = v->list;
+            ls.packed = v->packed;
+            ls.bounds = v->bounds;
+            ls.order = v->order;
+            ls.L0 = rg.x;
+            ls.Ln = rg.y - rg.x;
+            ls.cursor = 0;
+            ls.bx0 = static_cast<float>(tbx * kTile) + 0.5f;
+            ls.bx1 = ls.bx0 + static_cast<float>(kTile - 1);
+            ls.by0 = static_cast<float>(tby * kTile) + 0.5f;
+            ls.by1 = ls.by0 + static_cast<float>(kTile - 1);
+        }
+        __syncwarp();
+        fill(0);
+        if (scnt[ls.q][0] > 0) issue(0);
     };
 
-    if (loader) {  // only batch 0 on the tile's start-up path; batch 1 is formed in iteration 0
-        fill(0);
+    if (loader) {
+        if (lane == 0) ls.q = 0;
         __syncwarp();
-        if (scnt[0] > 0) issue(0);
+        claim();
     }
     __syncthreads();
-
-    // render with retained contributor lists keeps the sequential per-pixel chain (the lists
-    // are written in depth order); every other launch uses the fused segmented chain
-    const bool seq = kRender && vd.contrib != nullptr;
-    const double dpx = x + 0.5, dpy = y + 0.5;                                 // :261, :263
-    const float fpx = static_cast<float>(dpx), fpy = static_cast<float>(dpy);  // :274
-    // phase-B state (warps 0-1 own pixel t)
-    double T = 1.0;
-    double ac0 = 0.0, ac1 = 0.0, ac2 = 0.0, adep = 0.0;
-    bool done = !inside;
-    unsigned long long contrib = 0;
-    uint32_t ncontrib_px = 0;  // retain_contributors: this pixel's list length so far
-    const size_t pix_t = inside ? static_cast<size_t>(y) * p.cam.W + x : 0;
-    const int e_first = t >> 6;  // phase A: this thread's entries e_first + 4i
-
-    __shared__ uint32_t slive[2];  // batch b: entries with a nonzero weight at some pixel
-    if (t < 2) slive[t] = 0u;
-    double rcs[4] = {0.0, 0.0, 0.0, 0.0};  // kRc: this (segment, pixel) thread's colour / depth
-    int mine = loader ? 1 : 0;  // vote that this thread's pixel is done (the block stops when all are)
-    for (int b = 0;; ++b) {
-        cp_async_wait_all();
-        // batch b landed; scnt for b+1 visible; W / bnd free; and the early termination
-        // of the whole block (:312 for every pixel) decided on the previous batch's votes
-        if (__syncthreads_and(mine)) break;
-        const int n = scnt[b % 3];
-        if (n == 0) break;  // the bin is exhausted
-        if (loader) {  // batch b+1 in flight while the compute warps blend batch b
-            if (b == 0) {
-                fill(1);
-                __syncwarp();
+    for (int q = 0;; q ^= 1) {  // q: parity of this block (the loader's lq matches it)
+        const int item = s_item;
+        if (item >= total) break;
+        const int view = item / tpv, tile = item - view * tpv;
+        const ViewDesc vd = p.views[view];
+        const int bx = tile % p.raster_tiles_x, by = tile / p.raster_tiles_x;
+        const int x = bx * kTile + px_col(px);
+        const int y = by * kTile + px_row(px);
+        const bool inside = x < p.cam.W && y < p.cam.H;
+        const bool want_sem = !kRender || vd.sem != nullptr;
+        if (!loader) {
+            for (int i = t; i < C * apitch; i += kCompute) acc2[i] = make_double2(0.0, 0.0);
+            if (t < kTilePx) {
+                sdone[t] = inside ? 0 : 1;
+                sT[t] = 1.0;
             }
-            if (scnt[(b + 1) % 3] > 0) issue(b + 1);
-            fill(b + 2);  // rm slot b & 1 (batch b was issued last iteration), scnt[(b + 2) % 3]
-            continue;
+            if (t < 2) slive[t] = 0u;
         }
-        if (t == 0) slive[(b + 1) & 1] = 0u;  // last read by phase C of batch b - 1
-        const unsigned char* sb = stg + (b & 1) * L.stage_bytes;
-        const PackedSplat* sp = reinterpret_cast<const PackedSplat*>(sb + L.st_packed);
-        const uint16_t* sbnd = reinterpret_cast<const uint16_t*>(sb + L.st_bnd);  // [kNB][8]
-        const uint16_t* si = reinterpret_cast<const uint16_t*>(sb + L.st_idx);
-        const double* spr = reinterpret_cast<const double*>(sb + L.st_prob);
-        const double* scol = reinterpret_cast<const double*>(sb + L.st_color);
 
-        // footprint of entry e at this thread's pixel (:276-285); -1 = not a contributor
-        auto footprint = [&](int e) -> double {
-            double f = -1.0;
-            if (kAniso) {
-                // f4 (no reference): f = alpha exp(-q / 2), q = d^T Sigma2D^-1 d, cut at
-                // q > trunc^2 -- the order of oracle/sgm_oracle.c composite()
-                const PackedSplatA& a = reinterpret_cast<const PackedSplatA&>(sp[e]);
-                const double dx = dpx - a.mx;
-                const double dy = dpy - a.my;
-                const double q = (a.qa * (dx * dx) + (2.0 * a.qb) * (dx * dy)) + a.qc * (dy * dy);
-                if (!(q > p.opt.cut_sq)) {
-                    f = a.alpha * exp_footprint(-0.5 * q);
-                    if (f > kMaxFootprint) f = kMaxFootprint;
-                }
-            } else {
-                const float4 pf = *reinterpret_cast<const float4*>(&sp[e].pmx);
-                const float fdx = fpx - pf.x;
-                const float fdy = fpy - pf.y;
-                if (!(fdx * fdx + fdy * fdy > pf.z)) {  // :276-278
-                    const double dx = dpx - sp[e].mx;
-                    const double dy = dpy - sp[e].my;
-                    const double d2 = dx * dx + dy * dy;
-                    if (!(d2 > sp[e].cutoff_d2)) {  // :283
-                        f = sp[e].alpha * exp_footprint(-d2 * sp[e].inv_two_r2);  // :284
-                        if (f > kMaxFootprint) f = kMaxFootprint;                 // :285
+        // render with retained contributor lists keeps the sequential per-pixel chain (the
+        // lists are written in depth order); every other launch uses the fused segmented chain
+        const bool seq = kRender && vd.contrib != nullptr;
+        const double dpx = x + 0.5, dpy = y + 0.5;                                 // :261, :263
+        const float fpx = static_cast<float>(dpx), fpy = static_cast<float>(dpy);  // :274
+        // phase-B state (warps 0-1 own pixel t)
+        double T = 1.0;
+        double ac0 = 0.0, ac1 = 0.0, ac2 = 0.0, adep = 0.0;
+        bool done = !inside;
+        unsigned long long contrib = 0;
+        uint32_t ncontrib_px = 0;  // retain_contributors: this pixel's list length so far
+        const size_t pix_t = inside ? static_cast<size_t>(y) * p.cam.W + x : 0;
+        const int e_first = t >> 6;  // phase A: this thread's entries e_first + 4i
+
+        double rcs[4] = {0.0, 0.0, 0.0, 0.0};  // this (segment, pixel) thread's colour / depth
+        int mine = loader ? 1 : 0;  // vote that this thread's pixel is done (the block stops when all are)
+        for (int b = 0;; ++b) {
+            cp_async_wait_all();
+            // batch b landed; scnt for b+1 visible; W / bnd free; and the early termination
+            // of the whole block (:312 for every pixel) decided on the previous batch's votes
+            if (__syncthreads_and(mine)) break;
+            const int n = scnt[q][b % 3];
+            if (n == 0) break;  // the bin is exhausted
+            if (loader) {  // batch b+1 in flight while the compute warps blend batch b
+                if (b == 0) fill(1);
+                if (scnt[q][(b + 1) % 3] > 0) issue(b + 1);
+                fill(b + 2);  // rm slot b & 1 (batch b was issued last iteration), scnt[q][(b + 2) % 3]
+                continue;
+            }
+            if (t == 0) slive[(b + 1) & 1] = 0u;  // last read by phase C of batch b - 1
+            const unsigned char* sb = stg + (b & 1) * L.stage_bytes;
+            const PackedSplat* sp = reinterpret_cast<const PackedSplat*>(sb + L.st_packed);
+            const uint16_t* sbnd = reinterpret_cast<const uint16_t*>(sb + L.st_bnd);  // [kNB][8]
+            const uint16_t* si = reinterpret_cast<const uint16_t*>(sb + L.st_idx);
+            const double* spr = reinterpret_cast<const double*>(sb + L.st_prob);
+            const double* scol = reinterpret_cast<const double*>(sb + L.st_color);
+
+            // footprint of entry e at this thread's pixel (:276-285); -1 = not a contributor
+            auto footprint = [&](int e) -> double {
+                double f = -1.0;
+                if (kAniso) {
+                    // f4 (no reference): f = alpha exp(-q / 2), q = d^T Sigma2D^-1 d, cut at
+                    // q > trunc^2 -- the order of oracle/sgm_oracle.c composite()
+                    const PackedSplatA& a = reinterpret_cast<const PackedSplatA&>(sp[e]);
+                    const double dx = dpx - a.mx;
+                    const double dy = dpy - a.my;
+                    const double qf = (a.qa * (dx * dx) + (2.0 * a.qb) * (dx * dy)) + a.qc * (dy * dy);
+                    if (!(qf > p.opt.cut_sq)) {
+                        f = a.alpha * exp_footprint(-0.5 * qf);
+                        if (f > kMaxFootprint) f = kMaxFootprint;
+                    }
+                } else {
+                    const float4 pf = *reinterpret_cast<const float4*>(&sp[e].pmx);
+                    const float fdx = fpx - pf.x;
+                    const float fdy = fpy - pf.y;
+                    if (!(fdx * fdx + fdy * fdy > pf.z)) {  // :276-278
+                        const double dx = dpx - sp[e].mx;
+                        const double dy = dpy - sp[e].my;
+                        const double d2 = dx * dx + dy * dy;
+                        if (!(d2 > sp[e].cutoff_d2)) {  // :283
+                            f = sp[e].alpha * exp_footprint(-d2 * sp[e].inv_two_r2);  // :284
+                            if (f > kMaxFootprint) f = kMaxFootprint;                 // :285
+                        }
                     }
                 }
-            }
-            return f;
-        };
+                return f;
+            };
 
-        uint32_t nzbits = 0;  // entries this thread gave a nonzero weight
-        if (seq) {
-            // ---- phase A: footprints (independent of T) ----
-            {
-                const bool pdone = sdone[px] != 0;
+            uint32_t nzbits = 0;  // entries this thread gave a nonzero weight
+            if (seq) {
+                // ---- phase A: footprints (independent of T) ----
+                {
+                    const bool pdone = sdone[px] != 0;
 #pragma unroll
-                for (int i = 0; i < kNB / 4; ++i) {
-                    const int e = e_first + 4 * i;
-                    if (e >= n) break;
-                    W[pair_slot(e, 32, px)] = pdone ? -1.0 : footprint(e);
+                    for (int i = 0; i < kNB / 4; ++i) {
+                        const int e = e_first + 4 * i;
+                        if (e >= n) break;
+                        W[pair_slot(e, 32, px)] = pdone ? -1.0 : footprint(e);
+                    }
                 }
-            }
-            compute_sync();
-            // ---- phase B: transmittance chain (:286-312), sequential per pixel (warps 0-1):
-            // colour/depth and the ordered contributor lists of retain_contributors ----
-            if (t < kTilePx) {
-                for (int e = 0; e < n; ++e) {
-                    const int s = pair_slot(e, 32, t);
-                    const double f = W[s];
-                    if (done || f < 0.0) {
+                compute_sync();
+                // ---- phase B: transmittance chain (:286-312), sequential per pixel (warps
+                // 0-1): colour/depth and the ordered contributor lists of retain_contributors ----
+                if (t < kTilePx) {
+                    for (int e = 0; e < n; ++e) {
+                        const int s = pair_slot(e, 32, t);
+                        const double f = W[s];
+                        if (done || f < 0.0) {
+                            W[s] = 0.0;
+                            continue;
+                        }
+                        const double w = f * T;
+                        W[s] = w;
+                        if (vd.contrib) {  // retain_contributors (:310): depth ranks in order
+                            if (vd.contrib_offset)
+                                vd.contrib[vd.contrib_offset[pix_t] + ncontrib_px] = sp[e].aux;
+                            ++ncontrib_px;
+                        }
+                        ac0 += scol[4 * e] * w;  // :289-291 (colour clamped at upload)
+                        ac1 += scol[4 * e + 1] * w;
+                        ac2 += scol[4 * e + 2] * w;
+                        adep += sp[e].z * w;  // :293
+                        ++contrib;
+                        T = T * (1.0 - f);                        // :311
+                        if (p.opt.early_exit && T < p.opt.eps)   // :312
+                            done = true;
+                        if (w != 0.0) nzbits |= 1u << e;
+                    }
+                    sdone[t] = done ? 1 : 0;
+                }
+            } else {
+                // ---- footprints and transmittance fused. Thread (part, px) owns the
+                // contiguous entries 4 part .. 4 part + 3 of pixel px (warp-uniform entries).
+                // A segment starts at T_pixel * prod(earlier segments' (1 - f)) (fixed
+                // association); since T only decreases, a segment starting below eps lies
+                // after the early exit (:312). The pixel's T and done flag are read before the
+                // barrier and written (by the exiting or the last segment) after it. ----
+                const int part = t >> 6;
+                const bool pdone = sdone[px] != 0;
+                const double T0 = sT[px];
+                double f[4];
+                double prod = 1.0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int e = 4 * part + i;
+                    f[i] = (e < n && !pdone) ? footprint(e) : -1.0;
+                    if (f[i] >= 0.0) prod = prod * (1.0 - f[i]);
+                }
+                segp[part * kTilePx + px] = prod;
+                compute_sync();
+                double Ts = T0;
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    if (k < part) Ts = Ts * segp[k * kTilePx + px];
+                bool exited = pdone || (p.opt.early_exit && Ts < p.opt.eps);
+                double Tc = Ts;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int e = 4 * part + i;
+                    if (e >= n) break;
+                    const int s = pair_slot(e, 32, px);
+                    if (exited || f[i] < 0.0) {
                         W[s] = 0.0;
                         continue;
                     }
-                    const double w = f * T;
-                    W[s] = w;
-                    if (vd.contrib) {  // retain_contributors (:310): depth ranks in order
-                        if (vd.contrib_offset)
-                            vd.contrib[vd.contrib_offset[pix_t] + ncontrib_px] = sp[e].aux;
-                        ++ncontrib_px;
+                    const double wv = f[i] * Tc;
+                    W[s] = wv;
+                    if (wv != 0.0) nzbits |= 1u << e;
+                    if (kRc || kRender) {  // this segment's share of the colour / depth (:289-293)
+                        rcs[0] += scol[4 * e] * wv;
+                        rcs[1] += scol[4 * e + 1] * wv;
+                        rcs[2] += scol[4 * e + 2] * wv;
+                        rcs[3] += sp[e].z * wv;
                     }
-                    ac0 += scol[4 * e] * w;  // :289-291 (colour clamped at upload)
-                    ac1 += scol[4 * e + 1] * w;
-                    ac2 += scol[4 * e + 2] * w;
-                    adep += sp[e].z * w;  // :293
                     ++contrib;
-                    T = T * (1.0 - f);                        // :311
-                    if (p.opt.early_exit && T < p.opt.eps)   // :312
-                        done = true;
-                    if (w != 0.0) nzbits |= 1u << e;
+                    Tc = Tc * (1.0 - f[i]);
+                    if (p.opt.early_exit && Tc < p.opt.eps) exited = true;
                 }
-                sdone[t] = done ? 1 : 0;
+                // The pixel's T after the batch: the T of the segment where it exits (at most
+                // one segment can: the later ones start below eps), else the last segment's. A
+                // pixel done before the batch keeps its T. So the silhouette 1 - T is the
+                // reference's.
+                const bool start_exited = pdone || (p.opt.early_exit && Ts < p.opt.eps);
+                if ((!start_exited && exited) || (part == 3 && !start_exited)) {
+                    sT[px] = Tc;
+                    sdone[px] = exited ? 1 : 0;
+                }
             }
-        } else {
-            // ---- score: footprints and transmittance fused. Thread (part, px) owns the
-            // contiguous entries 4 part .. 4 part + 3 of pixel px (warp-uniform entries). A
-            // segment starts at T_pixel * prod(earlier segments' (1 - f)) (fixed association);
-            // since T only decreases, a segment starting below eps lies after the early exit
-            // (:312). The pixel's T and done flag are read before the barrier and written
-            // (by part 3) after it. ----
-            const int part = t >> 6;
-            const bool pdone = sdone[px] != 0;
-            const double T0 = sT[px];
-            double f[4];
-            double prod = 1.0;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int e = 4 * part + i;
-                f[i] = (e < n && !pdone) ? footprint(e) : -1.0;
-                if (f[i] >= 0.0) prod = prod * (1.0 - f[i]);
+            {
+                const uint32_t lv = __reduce_or_sync(0xffffffffu, nzbits);
+                if (lane == 0 && lv) atomicOr(&slive[b & 1], lv);
             }
-            segp[part * kTilePx + px] = prod;
             compute_sync();
-            double Ts = T0;
-#pragma unroll
-            for (int q = 0; q < 3; ++q)
-                if (q < part) Ts = Ts * segp[q * kTilePx + px];
-            bool exited = pdone || (p.opt.early_exit && Ts < p.opt.eps);
-            double Tc = Ts;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int e = 4 * part + i;
-                if (e >= n) break;
-                const int s = pair_slot(e, 32, px);
-                if (exited || f[i] < 0.0) {
-                    W[s] = 0.0;
-                    continue;
-                }
-                const double wv = f[i] * Tc;
-                W[s] = wv;
-                if (wv != 0.0) nzbits |= 1u << e;
-                if (kRc || kRender) {  // this segment's share of the colour / depth (:289-293)
-                    rcs[0] += scol[4 * e] * wv;
-                    rcs[1] += scol[4 * e + 1] * wv;
-                    rcs[2] += scol[4 * e + 2] * wv;
-                    rcs[3] += sp[e].z * wv;
-                }
-                ++contrib;
-                Tc = Tc * (1.0 - f[i]);
-                if (p.opt.early_exit && Tc < p.opt.eps) exited = true;
-            }
-            // The pixel's T after the batch: the T of the segment where it exits (at most one
-            // segment can: the later ones start below eps), else the last segment's. A pixel
-            // done before the batch keeps its T. So the silhouette 1 - T is the reference's.
-            const bool start_exited = pdone || (p.opt.early_exit && Ts < p.opt.eps);
-            if ((!start_exited && exited) || (part == 3 && !start_exited)) {
-                sT[px] = Tc;
-                sdone[px] = exited ? 1 : 0;
-            }
-        }
-        {
-            const uint32_t lv = __reduce_or_sync(0xffffffffu, nzbits);
-            if (lane == 0 && lv) atomicOr(&slive[b & 1], lv);
-        }
-        compute_sync();
 
-        // ---- phase C: sparse semantic scatter; warp g = channel group g, 64 px ----
-        if (want_sem) {
-            double2* accl = acc2 + lane;
-            // the live entries (some pixel weighted) with classes in this warp's group, in
-            // depth order (lane l tests entry l)
-            const int glo = (lane < n && g > 0) ? sbnd[lane * 8 + g - 1] : 0;
-            const int ghi = lane < n ? sbnd[lane * 8 + g] : 0;
-            uint32_t todo = __ballot_sync(0xffffffffu, ghi > glo) & slive[b & 1];
-            while (todo) {
-                const int e = __ffs(todo) - 1;
-                todo &= todo - 1u;
-                const double2 w = W2[e * 32 + lane];
-                const bool nz = (w.x != 0.0) | (w.y != 0.0);
-                const int lo = g == 0 ? 0 : sbnd[e * 8 + g - 1], hi = sbnd[e * 8 + g];
-                const uint16_t* ei = si + e * kpad;
-                const double* ep = spr + e * kpad;
-                if (!nz) continue;  // lanes without weight issue no shared-memory traffic
-                if (kDup) {
-                    for (int j = lo; j < hi; ++j) {  // repeated classes: in order
-                        double2* a = accl + ei[j] * apitch;
-                        double2 v = *a;
-                        v.x = __fma_rn(ep[j], w.x, v.x);  // :307
-                        v.y = __fma_rn(ep[j], w.y, v.y);
-                        *a = v;
-                    }
-                } else {
-                    int j = lo;
-                    for (; j + 2 <= hi; j += 2) {
-                        double2* a0 = accl + ei[j] * apitch;
-                        double2* a1 = accl + ei[j + 1] * apitch;
-                        const double p0 = ep[j], p1 = ep[j + 1];
-                        double2 v0 = *a0, v1 = *a1;
-                        v0.x = __fma_rn(p0, w.x, v0.x);
-                        v0.y = __fma_rn(p0, w.y, v0.y);
-                        v1.x = __fma_rn(p1, w.x, v1.x);
-                        v1.y = __fma_rn(p1, w.y, v1.y);
-                        *a0 = v0;
-                        *a1 = v1;
-                    }
-                    if (j < hi) {
-                        double2* a = accl + ei[j] * apitch;
-                        double2 v = *a;
-                        v.x = __fma_rn(ep[j], w.x, v.x);
-                        v.y = __fma_rn(ep[j], w.y, v.y);
-                        *a = v;
+            // ---- phase C: sparse semantic scatter; warp g = channel group g, 64 px ----
+            if (want_sem) {
+                double2* accl = acc2 + lane;
+                // the live entries (some pixel weighted) with classes in this warp's group, in
+                // depth order (lane l tests entry l)
+                const int glo = (lane < n && g > 0) ? sbnd[lane * 8 + g - 1] : 0;
+                const int ghi = lane < n ? sbnd[lane * 8 + g] : 0;
+                uint32_t todo = __ballot_sync(0xffffffffu, ghi > glo) & slive[b & 1];
+                while (todo) {
+                    const int e = __ffs(todo) - 1;
+                    todo &= todo - 1u;
+                    const double2 w = W2[e * 32 + lane];
+                    const bool nz = (w.x != 0.0) | (w.y != 0.0);
+                    const int lo = g == 0 ? 0 : sbnd[e * 8 + g - 1], hi = sbnd[e * 8 + g];
+                    const uint16_t* ei = si + e * kpad;
+                    const double* ep = spr + e * kpad;
+                    if (!nz) continue;  // lanes without weight issue no shared-memory traffic
+                    if (kDup) {
+                        for (int j = lo; j < hi; ++j) {  // repeated classes: in order
+                            double2* a = accl + ei[j] * apitch;
+                            double2 v = *a;
+                            v.x = __fma_rn(ep[j], w.x, v.x);  // :307
+                            v.y = __fma_rn(ep[j], w.y, v.y);
+                            *a = v;
+                        }
+                    } else {
+                        int j = lo;
+                        for (; j + 2 <= hi; j += 2) {
+                            double2* a0 = accl + ei[j] * apitch;
+                            double2* a1 = accl + ei[j + 1] * apitch;
+                            const double p0 = ep[j], p1 = ep[j + 1];
+                            double2 v0 = *a0, v1 = *a1;
+                            v0.x = __fma_rn(p0, w.x, v0.x);
+                            v0.y = __fma_rn(p0, w.y, v0.y);
+                            v1.x = __fma_rn(p1, w.x, v1.x);
+                            v1.y = __fma_rn(p1, w.y, v1.y);
+                            *a0 = v0;
+                            *a1 = v1;
+                        }
+                        if (j < hi) {
+                            double2* a = accl + ei[j] * apitch;
+                            double2 v = *a;
+                            v.x = __fma_rn(ep[j], w.x, v.x);
+                            v.y = __fma_rn(ep[j], w.y, v.y);
+                            *a = v;
+                        }
                     }
                 }
             }
+            mine = seq ? ((t < kTilePx) ? (done ? 1 : 0) : 1) : sdone[px];
         }
-        mine = seq ? ((t < kTilePx) ? (done ? 1 : 0) : 1) : sdone[px];
-    }
-    cp_async_wait_all();
-    __syncthreads();
 
-    __shared__ double red_d[kTilePx];
-    __shared__ unsigned long long red_u[kTilePx];
-    if (kRender) {
-        if (!seq) {  // fused chain: the pixel's 4 segment sums in a fixed order, T from sT
-            double* rcx = reinterpret_cast<double*>(stg);  // stages are free now: [4][64][4]
-            const int part = t >> 6;
-            if (!loader)
+        if (loader) {
+            // every copy of this block has landed (waited before the last barrier) and the
+            // compute warps no longer read the stages: stage the next block's batch 0
+            if (lane == 0) ls.q ^= 1;
+            __syncwarp();
+            claim();
+        } else {
+            if (kRender) {
+                if (!seq) {  // fused chain: the pixel's 4 segment sums in a fixed order, T from sT
+                    const int part = t >> 6;
+#pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) rcx[(part * kTilePx + px) * 4 + ch] = rcs[ch];
+                    compute_sync();
+                    if (t < kTilePx) {
+                        double r4[4];
+#pragma unroll
+                        for (int ch = 0; ch < 4; ++ch)
+                            r4[ch] = ((rcx[(0 * kTilePx + t) * 4 + ch] + rcx[(1 * kTilePx + t) * 4 + ch]) +
+                                      rcx[(2 * kTilePx + t) * 4 + ch]) + rcx[(3 * kTilePx + t) * 4 + ch];
+                        ac0 = r4[0];
+                        ac1 = r4[1];
+                        ac2 = r4[2];
+                        adep = r4[3];
+                        T = sT[t];
+                    }
+                }
+                if (t < kTilePx && inside) {
+                    const size_t pix = static_cast<size_t>(y) * p.cam.W + x;
+                    if (vd.sil) vd.sil[pix] = 1.0 - T;  // :314
+                    if (vd.color) {
+                        vd.color[pix * 3] = ac0;
+                        vd.color[pix * 3 + 1] = ac1;
+                        vd.color[pix * 3 + 2] = ac2;
+                    }
+                    if (vd.depth) vd.depth[pix] = adep;
+                    if (vd.contrib && !vd.contrib_offset) vd.contrib_count[pix] = ncontrib_px;
+                }
+                if (vd.sem) {
+                    for (int l = t; l < kTilePx * C; l += kCompute) {
+                        const int qq = l / C;
+                        const int c = l - qq * C;
+                        const int qx = bx * kTile + px_col(qq);
+                        const int qy = by * kTile + px_row(qq);
+                        if (qx < p.cam.W && qy < p.cam.H)
+                            vd.sem[(static_cast<size_t>(qy) * p.cam.W + qx) * C + c] =
+                                acc[pair_slot(c, apitch, qq)];
+                    }
+                }
+            } else {
+                // clipped_entropy (:360-369) split by channel group: warp g, pixels 2 lane, 2 lane + 1
+                double S1x = 0.0, S2x = 0.0, S1y = 0.0, S2y = 0.0;
+                // a channel below the clamp at all 64 pixels (about a fifth of them) takes the
+                // clamped constant's log once: the same operands, so the same sums
+                const double lclamp = log_table(0.001);
+#pragma unroll 2
+                for (int c = c0; c < c1; ++c) {
+                    const double2 v = acc2[c * apitch + lane];
+                    const double ax = clamp_prob(v.x), ay = clamp_prob(v.y);
+                    S1x += ax;
+                    S1y += ay;
+                    if (__all_sync(0xffffffffu, ax == 0.001 && ay == 0.001)) {
+                        S2x = __fma_rn(0.001, lclamp, S2x);
+                        S2y = __fma_rn(0.001, lclamp, S2y);
+                    } else {
+                        S2x = __fma_rn(ax, log_table(ax), S2x);
+                        S2y = __fma_rn(ay, log_table(ay), S2y);
+                    }
+                }
+                red[g * kTilePx + 2 * lane] = make_double2(S1x, S2x);
+                red[g * kTilePx + 2 * lane + 1] = make_double2(S1y, S2y);
+                compute_sync();
+                if (t < kTilePx) {
+                    double S1 = 0.0, S2 = 0.0;
+#pragma unroll
+                    for (int k = 0; k < kGroups; ++k) {
+                        S1 += red[k * kTilePx + t].x;
+                        S2 += red[k * kTilePx + t].y;
+                    }
+                    red_d[t] = inside ? log(S1) - S2 / S1 : 0.0;
+                    red_u[t] = (inside && 1.0 - sT[t] == 0.0) ? 1ull : 0ull;  // explorer.cpp:198
+                }
+                compute_sync();
+                for (int s = kTilePx / 2; s > 0; s >>= 1) {  // fixed tree: deterministic
+                    if (t < s) {
+                        red_d[t] += red_d[t + s];
+                        red_u[t] += red_u[t + s];
+                    }
+                    compute_sync();
+                }
+                if (t == 0) {
+                    vd.ent_partial[tile] = red_d[0];
+                    vd.miss_partial[tile] = static_cast<uint32_t>(red_u[0]);
+                }
+                compute_sync();
+            }
+            if (kRc) {  // the pixel's colour / depth: its 4 segments summed in a fixed order
+                const int part = t >> 6;
 #pragma unroll
                 for (int ch = 0; ch < 4; ++ch) rcx[(part * kTilePx + px) * 4 + ch] = rcs[ch];
-            __syncthreads();
-            if (t < kTilePx) {
-                double r4[4];
+                compute_sync();
+                if (t < kTilePx && inside) {
+                    const size_t pix = static_cast<size_t>(y) * p.cam.W + x;
 #pragma unroll
-                for (int ch = 0; ch < 4; ++ch)
-                    r4[ch] = ((rcx[(0 * kTilePx + t) * 4 + ch] + rcx[(1 * kTilePx + t) * 4 + ch]) +
-                              rcx[(2 * kTilePx + t) * 4 + ch]) + rcx[(3 * kTilePx + t) * 4 + ch];
-                ac0 = r4[0];
-                ac1 = r4[1];
-                ac2 = r4[2];
-                adep = r4[3];
-                T = sT[t];
+                    for (int ch = 0; ch < 4; ++ch)
+                        vd.rc4[pix * 4 + ch] = ((rcx[(0 * kTilePx + t) * 4 + ch] + rcx[(1 * kTilePx + t) * 4 + ch]) +
+                                                rcx[(2 * kTilePx + t) * 4 + ch]) + rcx[(3 * kTilePx + t) * 4 + ch];
+                }
             }
-        }
-        if (t < kTilePx && inside) {
-            const size_t pix = static_cast<size_t>(y) * p.cam.W + x;
-            if (vd.sil) vd.sil[pix] = 1.0 - T;  // :314
-            if (vd.color) {
-                vd.color[pix * 3] = ac0;
-                vd.color[pix * 3 + 1] = ac1;
-                vd.color[pix * 3 + 2] = ac2;
-            }
-            if (vd.depth) vd.depth[pix] = adep;
-            if (vd.contrib && !vd.contrib_offset) vd.contrib_count[pix] = ncontrib_px;
-        }
-        if (vd.sem) {
-            for (int l = t; l < kTilePx * C; l += kThreads) {
-                const int q = l / C;
-                const int c = l - q * C;
-                const int qx = bx * kTile + px_col(q);
-                const int qy = by * kTile + px_row(q);
-                if (qx < p.cam.W && qy < p.cam.H)
-                    vd.sem[(static_cast<size_t>(qy) * p.cam.W + qx) * C + c] =
-                        acc[pair_slot(c, apitch, q)];
-            }
-        }
-    } else {
-        // clipped_entropy (:360-369) split by channel group: warp g, pixels 2 lane, 2 lane + 1
-        double S1x = 0.0, S2x = 0.0, S1y = 0.0, S2y = 0.0;
-        // a channel below the clamp at all 64 pixels (about a fifth of them) takes the
-        // clamped constant's log once: the same operands, so the same sums
-        const double lclamp = log_table(0.001);
-#pragma unroll 2
-        for (int c = c0; c < c1; ++c) {
-            const double2 v = acc2[c * apitch + lane];
-            const double ax = clamp_prob(v.x), ay = clamp_prob(v.y);
-            S1x += ax;
-            S1y += ay;
-            if (__all_sync(0xffffffffu, ax == 0.001 && ay == 0.001)) {
-                S2x = __fma_rn(0.001, lclamp, S2x);
-                S2y = __fma_rn(0.001, lclamp, S2y);
+            // K (contributors) for the measurement counters
+            if (seq) {
+                if (t < kTilePx) red_u[t] = contrib;
             } else {
-                S2x = __fma_rn(ax, log_table(ax), S2x);
-                S2y = __fma_rn(ay, log_table(ay), S2y);
+                for (int k = 0; k < 4; ++k) {  // fold the 4 segment threads of each pixel, in order
+                    if ((t >> 6) == k) red_u[px] = (k == 0 ? 0ull : red_u[px]) + contrib;
+                    compute_sync();
+                }
             }
-        }
-        if (!loader) {
-            red[g * kTilePx + 2 * lane] = make_double2(S1x, S2x);
-            red[g * kTilePx + 2 * lane + 1] = make_double2(S1y, S2y);
-        }
-        __syncthreads();
-        if (t < kTilePx) {
-            double S1 = 0.0, S2 = 0.0;
-#pragma unroll
-            for (int q = 0; q < kGroups; ++q) {
-                S1 += red[q * kTilePx + t].x;
-                S2 += red[q * kTilePx + t].y;
+            compute_sync();
+            for (int s = kTilePx / 2; s > 0; s >>= 1) {
+                if (t < s) red_u[t] += red_u[t + s];
+                compute_sync();
             }
-            red_d[t] = inside ? log(S1) - S2 / S1 : 0.0;
-            red_u[t] = (inside && 1.0 - sT[t] == 0.0) ? 1ull : 0ull;  // explorer.cpp:198
+            if (t == 0 && vd.contributors && red_u[0]) atomicAdd(vd.contributors, red_u[0]);
         }
-        __syncthreads();
-        for (int s = kTilePx / 2; s > 0; s >>= 1) {  // fixed tree: deterministic
-            if (t < s) {
-                red_d[t] += red_d[t + s];
-                red_u[t] += red_u[t + s];
-            }
-            __syncthreads();
-        }
-        if (t == 0) {
-            vd.ent_partial[tile] = red_d[0];
-            vd.miss_partial[tile] = static_cast<uint32_t>(red_u[0]);
-        }
+        // the epilogue is done with acc / W / red_u; the next block's item and batch 0 are staged
         __syncthreads();
     }
-    if (kRc) {  // the pixel's colour / depth: its 4 segments summed in a fixed order
-        double* rcx = reinterpret_cast<double*>(stg);  // stages are free now: [4][64][4]
-        __syncthreads();
-        const int part = t >> 6;
-        if (!loader)
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch) rcx[(part * kTilePx + px) * 4 + ch] = rcs[ch];
-        __syncthreads();
-        if (t < kTilePx && inside) {
-            const size_t pix = static_cast<size_t>(y) * p.cam.W + x;
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch)
-                vd.rc4[pix * 4 + ch] = ((rcx[(0 * kTilePx + t) * 4 + ch] + rcx[(1 * kTilePx + t) * 4 + ch]) +
-                                        rcx[(2 * kTilePx + t) * 4 + ch]) + rcx[(3 * kTilePx + t) * 4 + ch];
-        }
-    }
-    // K (contributors) for the measurement counters
-    if (seq) {
-        if (t < kTilePx) red_u[t] = contrib;
-    } else {
-        for (int q = 0; q < 4; ++q) {  // fold the 4 segment threads of each pixel, in order
-            if ((t >> 6) == q) red_u[px] = (q == 0 ? 0ull : red_u[px]) + contrib;
-            __syncthreads();
-        }
-    }
-    __syncthreads();
-    for (int s = kTilePx / 2; s > 0; s >>= 1) {
-        if (t < s) red_u[t] += red_u[t + s];
-        __syncthreads();
-    }
-    if (t == 0 && vd.contributors && red_u[0]) atomicAdd(vd.contributors, red_u[0]);
 }
 
 template <bool kRender, bool kDup, bool kAniso, bool kRc = false>
-void launch_t(const RasterParams& p, int n_views, cudaStream_t s) {
+void launch_t(const RasterParams& p0, int n_views, cudaStream_t s) {
+    RasterParams p = p0;
+    p.n_items = p.tiles_per_view * n_views;
     const size_t smem = static_cast<size_t>(make_layout(p.map.C, p.map.kpad, kRender, kRc).total);
     // four CTAs per SM when four fit in shared memory (228 KB, 1 KB reserved per CTA)
     // (score mode only: the render and rc variants would spill at the 4-CTA register budget)
@@ -569,12 +637,9 @@ void launch_t(const RasterParams& p, int n_views, cudaStream_t s) {
     auto kern = k_raster<kRender, kDup, kAniso, kRc, 3>;
     if constexpr (!kRender && !kRc)
         if (four) kern = k_raster<kRender, kDup, kAniso, kRc, 4>;
-    static size_t configured[2] = {0, 0};
-    if (smem > configured[four]) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        configured[four] = smem;
-    }
-    dim3 grid(static_cast<unsigned>(p.tiles_per_view), static_cast<unsigned>(n_views), 1);
+    p.items_per_cta = kItemsPerCta;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const int grid = (p.n_items + p.items_per_cta - 1) / p.items_per_cta;
     kern<<<grid, kThreads, smem, s>>>(p);
 }
 
