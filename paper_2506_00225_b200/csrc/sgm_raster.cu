@@ -452,24 +452,27 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                 // depth order (lane l tests entry l)
                 const int glo = (lane < n && g > 0) ? sbnd[lane * 8 + g - 1] : 0;
                 const int ghi = lane < n ? sbnd[lane * 8 + g] : 0;
+                const uint32_t gb = static_cast<uint32_t>(glo) | (static_cast<uint32_t>(ghi) << 16);
                 uint32_t todo = __ballot_sync(0xffffffffu, ghi > glo) & slive[b & 1];
                 while (todo) {
                     const int e = __ffs(todo) - 1;
                     todo &= todo - 1u;
                     const double2 w = W2[e * 32 + lane];
+                    const uint32_t be = __shfl_sync(0xffffffffu, gb, e);  // entry e's group bounds
+                    const int lo = static_cast<int>(be & 0xffffu), hi = static_cast<int>(be >> 16);
                     const bool nz = (w.x != 0.0) | (w.y != 0.0);
-                    const int lo = g == 0 ? 0 : sbnd[e * 8 + g - 1], hi = sbnd[e * 8 + g];
                     const uint16_t* ei = si + e * kpad;
                     const double* ep = spr + e * kpad;
                     if (!nz) continue;  // lanes without weight issue no shared-memory traffic
+                    auto one = [&](int j) {
+                        double2* a = accl + ei[j] * apitch;
+                        double2 v = *a;
+                        v.x = __fma_rn(ep[j], w.x, v.x);  // :307
+                        v.y = __fma_rn(ep[j], w.y, v.y);
+                        *a = v;
+                    };
                     if (kDup) {
-                        for (int j = lo; j < hi; ++j) {  // repeated classes: in order
-                            double2* a = accl + ei[j] * apitch;
-                            double2 v = *a;
-                            v.x = __fma_rn(ep[j], w.x, v.x);  // :307
-                            v.y = __fma_rn(ep[j], w.y, v.y);
-                            *a = v;
-                        }
+                        for (int j = lo; j < hi; ++j) one(j);  // repeated classes: in order
                     } else {
                         int j = lo;
                         for (; j + 2 <= hi; j += 2) {
@@ -484,13 +487,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                             *a0 = v0;
                             *a1 = v1;
                         }
-                        if (j < hi) {
-                            double2* a = accl + ei[j] * apitch;
-                            double2 v = *a;
-                            v.x = __fma_rn(ep[j], w.x, v.x);
-                            v.y = __fma_rn(ep[j], w.y, v.y);
-                            *a = v;
-                        }
+                        if (j < hi) one(j);
                     }
                 }
             }
