@@ -565,29 +565,39 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                 red[g * kTilePx + 2 * lane] = make_double2(S1x, S2x);
                 red[g * kTilePx + 2 * lane + 1] = make_double2(S1y, S2y);
                 compute_sync();
-                if (t < kTilePx) {
+                if (t < kTilePx) {  // warps 0-1: pixel t
                     double S1 = 0.0, S2 = 0.0;
 #pragma unroll
                     for (int k = 0; k < kGroups; ++k) {
                         S1 += red[k * kTilePx + t].x;
                         S2 += red[k * kTilePx + t].y;
                     }
-                    red_d[t] = inside ? log(S1) - S2 / S1 : 0.0;
-                    red_u[t] = (inside && 1.0 - sT[t] == 0.0) ? 1ull : 0ull;  // explorer.cpp:198
-                }
-                compute_sync();
-                for (int s = kTilePx / 2; s > 0; s >>= 1) {  // fixed tree: deterministic
-                    if (t < s) {
-                        red_d[t] += red_d[t + s];
-                        red_u[t] += red_u[t + s];
+                    double h = inside ? log(S1) - S2 / S1 : 0.0;
+                    // fixed shuffle tree over the warp's 32 pixels: deterministic
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) h += __shfl_down_sync(0xffffffffu, h, o);
+                    const unsigned m = __reduce_add_sync(0xffffffffu, (inside && 1.0 - sT[t] == 0.0) ? 1u : 0u);  // explorer.cpp:198
+                    if (lane == 0) {
+                        red_d[warp] = h;
+                        red_u[warp] = m;
                     }
-                    compute_sync();
                 }
-                if (t == 0) {
-                    vd.ent_partial[tile] = red_d[0];
-                    vd.miss_partial[tile] = static_cast<uint32_t>(red_u[0]);
+            }
+            // K (contributors) for the measurement counters: per-warp sums (integers, any order)
+            {
+                const unsigned cw = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(contrib));
+                if (lane == 0) red_u[2 + warp] = cw;
+            }
+            compute_sync();
+            if (t == 0) {
+                if (!kRender) {
+                    vd.ent_partial[tile] = red_d[0] + red_d[1];
+                    vd.miss_partial[tile] = static_cast<uint32_t>(red_u[0] + red_u[1]);
                 }
-                compute_sync();
+                unsigned long long k = 0;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) k += red_u[2 + w];
+                if (vd.contributors && k) atomicAdd(vd.contributors, k);
             }
             if (kRc) {  // the pixel's colour / depth: its 4 segments summed in a fixed order
                 const int part = t >> 6;
@@ -602,21 +612,6 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                                                 rcx[(2 * kTilePx + t) * 4 + ch]) + rcx[(3 * kTilePx + t) * 4 + ch];
                 }
             }
-            // K (contributors) for the measurement counters
-            if (seq) {
-                if (t < kTilePx) red_u[t] = contrib;
-            } else {
-                for (int k = 0; k < 4; ++k) {  // fold the 4 segment threads of each pixel, in order
-                    if ((t >> 6) == k) red_u[px] = (k == 0 ? 0ull : red_u[px]) + contrib;
-                    compute_sync();
-                }
-            }
-            compute_sync();
-            for (int s = kTilePx / 2; s > 0; s >>= 1) {
-                if (t < s) red_u[t] += red_u[t + s];
-                compute_sync();
-            }
-            if (t == 0 && vd.contributors && red_u[0]) atomicAdd(vd.contributors, red_u[0]);
         }
         // the epilogue is done with acc / W / red_u; the next block's item and batch 0 are staged
         __syncthreads();
