@@ -345,12 +345,29 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
                         if (lane < 8) red[(e * 2 + (px >> 5)) * 8 + lane] = 0.0;
                         continue;
                     }
+                    // butterfly reduce-scatter of the 8 sums over the warp's 32 pixels (9 double
+                    // shuffles instead of 8 trees of 5; fixed pattern, deterministic): halve the
+                    // parameter set at xor 16, 8, 4, then add across xor 2, 1; lane l ends with
+                    // parameter (l >> 2) & 7
+                    {
+                        const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+                        double K4[4], K2[2];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        double v = J[q];
+                        for (int i = 0; i < 4; ++i) {
+                            const double send = h16 ? J[i] : J[i + 4];
+                            const double keep = h16 ? J[i + 4] : J[i];
+                            K4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                        }
 #pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-                        if (lane == 0) red[(e * 2 + (px >> 5)) * 8 + q] = v;
+                        for (int i = 0; i < 2; ++i) {
+                            const double send = h8 ? K4[i] : K4[i + 2];
+                            const double keep = h8 ? K4[i + 2] : K4[i];
+                            K2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                        }
+                        double v = (h4 ? K2[1] : K2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? K2[0] : K2[1], 4);
+                        v += __shfl_xor_sync(0xffffffffu, v, 2);
+                        v += __shfl_xor_sync(0xffffffffu, v, 1);
+                        if ((lane & 3) == 0) red[(e * 2 + (px >> 5)) * 8 + ((lane >> 2) & 7)] = v;
                     }
                 }
                 __syncthreads();
