@@ -24,8 +24,13 @@ namespace sgm {
 
 namespace {
 
-constexpr int kFThreads = 256;
+constexpr int kFCompute = 256;            // compute threads: warps 0-7
+constexpr int kFThreads = kFCompute + 32;  // + warp 8, the batch loader
 constexpr int kFNB = 16;
+
+// barrier over the 8 compute warps only (the loader warp runs ahead between the per-batch
+// block barriers)
+__device__ __forceinline__ void fisher_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(kFCompute) : "memory"); }
 
 struct FLayout {
     int f, dr, w, red, gacc, emap, rm, done, pose, segp, sseg, st, sp, src, stage0, stage_bytes,
@@ -98,11 +103,12 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
 
     constexpr int Q = 4 + 2;  // 16-byte chunks per Gaussian: PackedSplat + colour
     __shared__ int scnt[3];  // entries of batch b in scnt[b % 3]
-    auto issue = [&](int b) {
+    const bool loader = (t >> 5) == kFCompute / 32;
+    auto issue = [&](int b) {  // loader warp
         unsigned char* sb = stg + (b & 1) * L.stage_bytes;
         const int n = scnt[b % 3];
         const uint2* slot = rm + (b & 1) * kFNB;
-        for (int c = t; c < n * Q; c += kFThreads) {
+        for (int c = lane; c < n * Q; c += 32) {
             const int e = c / Q;
             const int q = c - e * Q;
             const uint2 v = slot[e];
@@ -121,13 +127,12 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    // batches skip bin entries that cannot reach a pixel of the block (fill_batch)
+    // batches (formed by the loader warp two ahead) skip bin entries that cannot reach a
+    // pixel of the block (fill_batch)
     const float bx0 = static_cast<float>(bx * kTile) + 0.5f, bx1 = bx0 + static_cast<float>(kTile - 1);
     const float by0 = static_cast<float>(by * kTile) + 0.5f, by1 = by0 + static_cast<float>(kTile - 1);
-    const int fwarp = t >> 5;
     uint32_t cursor = 0;
     auto fill = [&](int b) {
-        if (fwarp != 0) return;
         const int filled = fill_batch<kFNB>(vd, L0, Ln, cursor, rm + (b & 1) * kFNB, true, bx0, bx1,
                                             by0, by1, lane);
         if (lane == 0) scnt[b % 3] = filled;
@@ -146,7 +151,7 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
         for (int ch = 0; ch < 4; ++ch) sRc[t * 4 + ch] = vd.rc4[pix * 4 + ch];
     }
     const int part = t >> 6;  // phase AB: this thread's segment (entries 4 part .. 4 part + 3)
-    double gsum = 0.0;                     // gain of this tile (thread 0, fixed order)
+    double gthr = 0.0;  // gain mode: this thread's (entry slot, parameter) share, batch order
 
     for (int pass = haveR ? 1 : 0; pass < 2; ++pass) {
         if (t < kTilePx) {
@@ -154,21 +159,31 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
             sT[t] = 1.0;
             for (int ch = 0; ch < 4; ++ch) sPb[t * 4 + ch] = 0.0;
         }
+        if (loader) {  // batch 0 of this pass; batch 1 is formed in iteration 0
+            cursor = 0;
+            fill(0);
+            __syncwarp();
+            if (scnt[0] > 0) issue(0);
+        }
         __syncthreads();
         if (pass == 1)
             for (int ch = 0; ch < 4; ++ch) Rc[ch] = sRc[px * 4 + ch];  // R of this thread's pixel
-        cursor = 0;
-        fill(0);
-        fill(1);
-        __syncthreads();
-        if (scnt[0] > 0) issue(0);
+        int mine = loader ? 1 : 0;  // vote that this thread's pixel is done
         for (int b = 0;; ++b) {
             asm volatile("cp.async.wait_all;\n" ::: "memory");
-            __syncthreads();
+            // batch b landed; and the block's early termination (every pixel done, :312)
+            if (__syncthreads_and(mine)) break;
             const int n = scnt[b % 3];
             if (n == 0) break;  // the bin is exhausted
-            if (scnt[(b + 1) % 3] > 0) issue(b + 1);
-            fill(b + 2);
+            if (loader) {
+                if (b == 0) {
+                    fill(1);
+                    __syncwarp();
+                }
+                if (scnt[(b + 1) % 3] > 0) issue(b + 1);
+                fill(b + 2);
+                continue;
+            }
             const unsigned char* sb = stg + (b & 1) * L.stage_bytes;
             const PackedSplat* sp = reinterpret_cast<const PackedSplat*>(sb);
             const double* scol = reinterpret_cast<const double*>(sb + L.st_color);
@@ -207,7 +222,7 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
                 if (f != kNotContrib) prod = prod * (1.0 - (f == kClamped ? kMaxFootprint : f));
             }
             segp[part * kTilePx + px] = prod;
-            __syncthreads();
+            fisher_sync();
             double Ts = T0;
 #pragma unroll
             for (int q = 0; q < 3; ++q)
@@ -246,7 +261,7 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
                 sT[px] = Tc;
                 sdone[px] = (pdone || (p.opt.early_exit && Tc < p.opt.eps)) ? 1 : 0;
             }
-            __syncthreads();
+            fisher_sync();
             {
                 const double* Pb = sPb + (b & 1) * kTilePx * 4;
                 double* Pn = sPb + ((b + 1) & 1) * kTilePx * 4;
@@ -284,7 +299,7 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
                                                 sseg[(2 * kTilePx + px) * 4 + ch]) + sseg[(3 * kTilePx + px) * 4 + ch]);
                 }
             }
-            __syncthreads();
+            fisher_sync();
 
             // phase C (pass 1): squared Jacobians, reduced over the block's pixels
             if (pass == 1) {
@@ -370,32 +385,31 @@ __global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherP
                         if ((lane & 3) == 0) red[(e * 2 + (px >> 5)) * 8 + ((lane >> 2) & 7)] = v;
                     }
                 }
-                __syncthreads();
+                fisher_sync();
+                // (red is rewritten by the next batch's phase C, three barriers later)
                 if (t < n * 8) {
                     const int e = t >> 3, q = t & 7;
                     const double sum = red[(e * 2) * 8 + q] + red[(e * 2 + 1) * 8 + q];
                     const size_t slot = static_cast<size_t>(em[e]) * 8 + q;
                     if (kGain)
-                        gacc[t] = sum * fp.invp[slot];
+                        gthr += sum * fp.invp[slot];
                     else if (sum != 0.0)
                         atomicAdd(&fp.H[slot], sum);
                 }
-                __syncthreads();
-                if (kGain && t < 8) {  // fixed-order two-level sum: deterministic
-                    double part = 0.0;
-                    for (int u = t; u < n * 8; u += 8) part += gacc[u];
-                    red[t] = part;
-                }
-                __syncthreads();
-                if (kGain && t == 0)
-                    for (int u = 0; u < 8; ++u) gsum += red[u];
             }
-            if (__syncthreads_and(sdone[px])) break;
+            mine = sdone[px];
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
     }
-    if (kGain && t == 0) vd.fis_partial[tile] = gsum;
+    if (kGain) {  // the tile's gain: threads 0..127 in a fixed order (deterministic)
+        double v = gthr;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (lane == 0 && t < kFNB * 8) gacc[t >> 5] = v;
+        __syncthreads();
+        if (t == 0) vd.fis_partial[tile] = ((gacc[0] + gacc[1]) + gacc[2]) + gacc[3];
+    }
 }
 
 template <bool kGain>
