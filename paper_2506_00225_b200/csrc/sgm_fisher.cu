@@ -65,7 +65,7 @@ constexpr double kNotContrib = -1.0;
 constexpr double kClamped = -2.0;
 
 template <bool kGain>
-__global__ void __launch_bounds__(kFThreads, 2) k_fisher(RasterParams p, FisherParams fp) {
+__global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherParams fp) {
     extern __shared__ __align__(16) unsigned char smem[];
     const FLayout L = fisher_layout();
     double* F = reinterpret_cast<double*>(smem + L.f);
