@@ -49,10 +49,10 @@ __host__ __device__ inline FLayout fisher_layout() {
     L.done = L.rm + 2 * kFNB * 8;             // [64]
     L.pose = L.done + kTilePx * 4;            // Rcw (9 doubles) + pad
     L.segp = L.pose + 16 * 8;                 // [4][64] segment products of (1 - f)
-    L.sseg = L.segp + 4 * kTilePx * 8;        // [4][64][4] segment colour / depth sums
+    L.sseg = L.segp + 4 * kTilePx * 8;        // [4][4][64] segment colour / depth sums (part, channel, pixel)
     L.st = L.sseg + 4 * kTilePx * 4 * 8;      // [64] pixel transmittance at the batch start
-    L.sp = L.st + kTilePx * 8;                // [2][64][4] prefix P at the batch start
-    L.src = L.sp + 2 * kTilePx * 4 * 8;       // [64][4] rendered R (pass 0 result)
+    L.sp = L.st + kTilePx * 8;                // [2][4][64] prefix P at the batch start
+    L.src = L.sp + 2 * kTilePx * 4 * 8;       // [4][64] rendered R (pass 0 result)
     L.stage0 = L.src + kTilePx * 4 * 8;
     L.st_color = kFNB * static_cast<int>(sizeof(PackedSplat));
     L.stage_bytes = L.st_color + kFNB * 32;
@@ -144,11 +144,11 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
     // pass 0 is skipped (the planes are the same sums, in a fixed segment order)
     const bool haveR = kGain && vd.rc4 != nullptr;
     if (t < kTilePx)
-        for (int ch = 0; ch < 4; ++ch) sRc[t * 4 + ch] = 0.0;
+        for (int ch = 0; ch < 4; ++ch) sRc[ch * kTilePx + t] = 0.0;
     if (haveR && t < kTilePx && inside) {
         const size_t pix = static_cast<size_t>(y) * p.cam.W + x;
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) sRc[t * 4 + ch] = vd.rc4[pix * 4 + ch];
+        for (int ch = 0; ch < 4; ++ch) sRc[ch * kTilePx + t] = vd.rc4[pix * 4 + ch];
     }
     const int part = t >> 6;  // phase AB: this thread's segment (entries 4 part .. 4 part + 3)
     double gthr = 0.0;  // gain mode: this thread's (entry slot, parameter) share, batch order
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
         if (t < kTilePx) {
             sdone[t] = inside ? 0 : 1;
             sT[t] = 1.0;
-            for (int ch = 0; ch < 4; ++ch) sPb[t * 4 + ch] = 0.0;
+            for (int ch = 0; ch < 4; ++ch) sPb[ch * kTilePx + t] = 0.0;
         }
         if (loader) {  // batch 0 of this pass; batch 1 is formed in iteration 0
             cursor = 0;
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
         }
         __syncthreads();
         if (pass == 1)
-            for (int ch = 0; ch < 4; ++ch) Rc[ch] = sRc[px * 4 + ch];  // R of this thread's pixel
+            for (int ch = 0; ch < 4; ++ch) Rc[ch] = sRc[ch * kTilePx + px];  // R of this thread's pixel
         int mine = loader ? 1 : 0;  // vote that this thread's pixel is done
         for (int b = 0;; ++b) {
             asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
                 if (p.opt.early_exit && Tc < p.opt.eps) exited = true;
             }
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch) sseg[(part * kTilePx + px) * 4 + ch] = Sg[ch];
+            for (int ch = 0; ch < 4; ++ch) sseg[(part * 4 + ch) * kTilePx + px] = Sg[ch];
             if (part == 3) {  // the pixel's T and done flag for the next batch
                 sT[px] = Tc;
                 sdone[px] = (pdone || (p.opt.early_exit && Tc < p.opt.eps)) ? 1 : 0;
@@ -268,16 +268,16 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
                 if (pass == 0) {
                     if (part == 0)  // R accumulates batch by batch, segments in a fixed order
                         for (int ch = 0; ch < 4; ++ch)
-                            sRc[px * 4 + ch] += ((sseg[(0 * kTilePx + px) * 4 + ch] + sseg[(1 * kTilePx + px) * 4 + ch]) +
-                                                 sseg[(2 * kTilePx + px) * 4 + ch]) + sseg[(3 * kTilePx + px) * 4 + ch];
+                            sRc[ch * kTilePx + px] += ((sseg[(0 * 4 + ch) * kTilePx + px] + sseg[(1 * 4 + ch) * kTilePx + px]) +
+                                                 sseg[(2 * 4 + ch) * kTilePx + px]) + sseg[(3 * 4 + ch) * kTilePx + px];
                 } else {
                     double P[4];
 #pragma unroll
                     for (int ch = 0; ch < 4; ++ch) {
-                        P[ch] = Pb[px * 4 + ch];
+                        P[ch] = Pb[ch * kTilePx + px];
 #pragma unroll
                         for (int q = 0; q < 3; ++q)
-                            if (q < part) P[ch] += sseg[(q * kTilePx + px) * 4 + ch];
+                            if (q < part) P[ch] += sseg[(q * 4 + ch) * kTilePx + px];
                     }
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
@@ -294,9 +294,9 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
                     }
                     if (part == 0)  // P at the next batch's start (the other buffer)
                         for (int ch = 0; ch < 4; ++ch)
-                            Pn[px * 4 + ch] = Pb[px * 4 + ch] +
-                                              (((sseg[(0 * kTilePx + px) * 4 + ch] + sseg[(1 * kTilePx + px) * 4 + ch]) +
-                                                sseg[(2 * kTilePx + px) * 4 + ch]) + sseg[(3 * kTilePx + px) * 4 + ch]);
+                            Pn[ch * kTilePx + px] = Pb[ch * kTilePx + px] +
+                                              (((sseg[(0 * 4 + ch) * kTilePx + px] + sseg[(1 * 4 + ch) * kTilePx + px]) +
+                                                sseg[(2 * 4 + ch) * kTilePx + px]) + sseg[(3 * 4 + ch) * kTilePx + px]);
                 }
             }
             fisher_sync();
