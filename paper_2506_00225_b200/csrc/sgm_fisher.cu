@@ -188,6 +188,22 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
             const PackedSplat* sp = reinterpret_cast<const PackedSplat*>(sb);
             const double* scol = reinterpret_cast<const double*>(sb + L.st_color);
             const uint32_t* em = emap + (b & 1) * kFNB;
+            // pass 1: the per-Gaussian constants of the Jacobian chain, once per entry (the
+            // gain buffer is free during the batches; read in phase C after two barriers)
+            double* sEnt = gacc;  // [kFNB][8]
+            if (pass == 1 && t < n) {
+                const PackedSplat& g = sp[t];
+                const double r = sqrt(0.5 / g.inv_two_r2);
+                const double inv_r2 = 2.0 * g.inv_two_r2;
+                sEnt[t * 8 + 0] = r;
+                sEnt[t * 8 + 1] = 1.0 / g.z;
+                sEnt[t * 8 + 2] = g.alpha > 0.0 ? 1.0 / g.alpha : 0.0;
+                sEnt[t * 8 + 3] = inv_r2;
+                sEnt[t * 8 + 4] = inv_r2 / r;
+                sEnt[t * 8 + 5] = g.alpha * (1.0 - g.alpha);
+                sEnt[t * 8 + 6] = g.mx - p.cam.cx;
+                sEnt[t * 8 + 7] = g.my - p.cam.cy;
+            }
 
             // phase AB: thread (part, px) owns the contiguous entries 4 part .. 4 part + 3 of
             // pixel px (warp-uniform entries). Footprints (splat_render.cpp:276-285, clamp
@@ -318,22 +334,22 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
                         const PackedSplat& g = sp[e];
                         // d f / d(param) (losses.cpp:297-304); zero when clamped or alpha == 0
                         const bool chain = !clamped && g.alpha > 0.0;
-                        const double inv_r2 = 2.0 * g.inv_two_r2;
-                        const double r = sqrt(0.5 / g.inv_two_r2);
+                        const double* ek = sEnt + e * 8;  // r, 1/z, 1/alpha, 1/r^2, 1/r^3, ...
+                        const double r = ek[0];
+                        const double iz = ek[1];
                         const double dx = dpx - g.mx, dy = dpy - g.my;
                         const double d2 = dx * dx + dy * dy;
-                        const double iz = 1.0 / g.z;
-                        const double fa = chain ? f / g.alpha : 0.0;
-                        const double fmx = chain ? f * dx * inv_r2 : 0.0;
-                        const double fmy = chain ? f * dy * inv_r2 : 0.0;
-                        const double fr = chain ? f * d2 * inv_r2 / r : 0.0;
+                        const double fa = chain ? f * ek[2] : 0.0;
+                        const double fmx = chain ? f * dx * ek[3] : 0.0;
+                        const double fmy = chain ? f * dy * ek[3] : 0.0;
+                        const double fr = chain ? f * d2 * ek[4] : 0.0;
                         // d_cam(ch) = dR_ch/df * u + [ch == depth] * w * e_z with
                         // u = (fmx fx/z, fmy fy/z, -(fmx (mx-cx) + fmy (my-cy) + fr r) / z)
                         // (losses.cpp:323-326), so with v = R u (world, R = Rcw^T):
                         //   sum_ch J_a^2 = S_rgb v_a^2 + (dR_D/df v_a + w R_{a,z})^2
                         const double ux = fmx * p.cam.fx * iz;
                         const double uy = fmy * p.cam.fy * iz;
-                        const double uz = -(fmx * (g.mx - p.cam.cx) + fmy * (g.my - p.cam.cy) + fr * r) * iz;
+                        const double uz = -(fmx * ek[6] + fmy * ek[7] + fr * r) * iz;
                         const double d0 = DR[(0 * kFNB + e) * kTilePx + px];
                         const double d1 = DR[(1 * kFNB + e) * kTilePx + px];
                         const double d2c = DR[(2 * kFNB + e) * kTilePx + px];
@@ -347,7 +363,7 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
                             J[a] = Srgb * va * va + dep * dep;
                         }
                         const double jl = fr * r;                       // d/d log_r (:333)
-                        const double jo = fa * g.alpha * (1.0 - g.alpha);  // d/d logit (:334)
+                        const double jo = fa * ek[5];                   // d/d logit (:334)
                         J[3] = Sall * jl * jl;
                         J[4] = Sall * jo * jo;
 #pragma unroll
