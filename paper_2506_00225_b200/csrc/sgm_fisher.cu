@@ -7,16 +7,18 @@
 // proj/src/losses.cpp:242-335 with a unit seed per channel, chained to world space per
 // pixel before squaring:  H[i][theta] += sum_px sum_ch (dR_ch(px)/dtheta_i)^2.
 //
-// One CTA (8 warps) = one 8x8 block of one view; two passes over the block's depth-ordered
-// list (same cp.async staging as the raster):
-//   pass 0  phase A footprints, phase B transmittance chain -> rendered R_ch per pixel
-//   pass 1  phase A again; phase B: dR_ch/df_j = v_ch T_j - S_ch / (1 - f_j) with the suffix
-//           S = R - P_j (P_j the inclusive prefix, so no reverse sweep is needed); phase C
-//           (all 8 warps, 4 (Gaussian, pixel) pairs per thread): the 8 squared Jacobians,
-//           warp-reduced over pixels, then
+// One CTA (8 compute warps + 1 loader warp, as in the raster) = one 8x8 block of one view;
+// two passes over the block's depth-ordered list (same cp.async staging as the raster):
+//   pass 0  footprints and the segmented transmittance chain -> rendered R_ch per pixel
+//           (skipped in gain mode when the score raster wrote R: vd.rc4)
+//   pass 1  the chain again; then per (entry, pixel) dR_ch/df_j = v_ch T_j - S_ch / (1 - f_j)
+//           with the suffix S = R - P_j (P_j the inclusive prefix, so no reverse sweep is
+//           needed), the 8 squared Jacobians in registers, reduced over the warp's 32 pixels
+//           (a butterfly), then
 //             prior mode: one fp64 RED per (Gaussian, parameter, tile) into H
-//             gain mode : sum_theta H_tile[theta] / (H_prior[theta] + lambda) folded into a
-//                         per-tile partial in fixed order (deterministic per-view gain).
+//             gain mode : sum_theta H_tile[theta] / (H_prior[theta] + lambda) accumulated per
+//                         (entry slot, parameter) thread, folded per tile in a fixed order
+//                         (deterministic per-view gain).
 #include "sgm_device.cuh"
 #include "sgm_internal.h"
 
@@ -33,16 +35,13 @@ constexpr int kFNB = 16;
 __device__ __forceinline__ void fisher_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(kFCompute) : "memory"); }
 
 struct FLayout {
-    int f, dr, w, red, gacc, emap, rm, done, pose, segp, sseg, st, sp, src, stage0, stage_bytes,
+    int red, gacc, emap, rm, done, pose, segp, sseg, st, sp, src, stage0, stage_bytes,
         st_color, total;
 };
 
 __host__ __device__ inline FLayout fisher_layout() {
     FLayout L;
-    L.f = 0;                                  // [kFNB][64] footprint code
-    L.dr = L.f + kFNB * kTilePx * 8;          // [4][kFNB][64] dR/df
-    L.w = L.dr + 4 * kFNB * kTilePx * 8;      // [kFNB][64] w
-    L.red = L.w + kFNB * kTilePx * 8;         // [kFNB][2][8] per-half J^2 sums
+    L.red = 0;                                // [kFNB][2][8] per-half J^2 sums
     L.gacc = L.red + kFNB * 2 * 8 * 8;        // [kFNB][8] gain terms
     L.emap = L.gacc + kFNB * 8 * 8;           // [2][kFNB] map index
     L.rm = L.emap + 2 * kFNB * 4;             // [2][kFNB] (rank, map index)
@@ -68,9 +67,6 @@ template <bool kGain>
 __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherParams fp) {
     extern __shared__ __align__(16) unsigned char smem[];
     const FLayout L = fisher_layout();
-    double* F = reinterpret_cast<double*>(smem + L.f);
-    double* DR = reinterpret_cast<double*>(smem + L.dr);
-    double* Wv = reinterpret_cast<double*>(smem + L.w);
     double* red = reinterpret_cast<double*>(smem + L.red);
     double* gacc = reinterpret_cast<double*>(smem + L.gacc);
     uint32_t* emap = reinterpret_cast<uint32_t*>(smem + L.emap);
@@ -99,7 +95,6 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
     const uint32_t Ln = rg.y - rg.x;
     const double dpx = x + 0.5, dpy = y + 0.5;
     const float fpx = static_cast<float>(dpx), fpy = static_cast<float>(dpy);
-    const int e_first = t >> 6;
 
     constexpr int Q = 4 + 2;  // 16-byte chunks per Gaussian: PackedSplat + colour
     __shared__ int scnt[3];  // entries of batch b in scnt[b % 3]
@@ -256,15 +251,12 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
                 const int s = e * kTilePx + px;
                 if (exited || fcode[i] == kNotContrib) {
                     fcode[i] = kNotContrib;
-                    F[s] = kNotContrib;
                     continue;
                 }
-                F[s] = fcode[i];
                 const double f = fcode[i] == kClamped ? kMaxFootprint : fcode[i];
                 const double w = f * Tc;
                 Tj[i] = Tc;
                 wj[i] = w;
-                if (pass == 1) Wv[s] = w;
                 const double v[4] = {scol[4 * e], scol[4 * e + 1], scol[4 * e + 2], sp[e].z};
 #pragma unroll
                 for (int ch = 0; ch < 4; ++ch) Sg[ch] += v[ch] * w;
@@ -295,18 +287,91 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
                         for (int q = 0; q < 3; ++q)
                             if (q < part) P[ch] += sseg[(q * 4 + ch) * kTilePx + px];
                     }
+                    // per entry: dR_ch/df (losses.cpp:285-288), then the squared Jacobians of the
+                    // 8 parameters at this pixel, reduced over the warp's 32 pixels (the warp's
+                    // entries are uniform: entry e of half-tile px >> 5)
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const int e = 4 * part + i;
-                        if (e >= n || fcode[i] == kNotContrib) continue;
-                        const double f = fcode[i] == kClamped ? kMaxFootprint : fcode[i];
-                        const double i1f = 1.0 / (1.0 - f);
-                        const double v[4] = {scol[4 * e], scol[4 * e + 1], scol[4 * e + 2], sp[e].z};
+                        if (e >= n) break;  // warp-uniform
+                        const bool contrib = fcode[i] != kNotContrib;
+                        double J[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                        if (contrib) {
+                            const bool clamped = fcode[i] == kClamped;
+                            const double f = clamped ? kMaxFootprint : fcode[i];
+                            const double w = wj[i];
+                            const double i1f = 1.0 / (1.0 - f);
+                            const double v[4] = {scol[4 * e], scol[4 * e + 1], scol[4 * e + 2], sp[e].z};
+                            double dR[4];
 #pragma unroll
-                        for (int ch = 0; ch < 4; ++ch) {
-                            P[ch] += v[ch] * wj[i];
-                            DR[(ch * kFNB + e) * kTilePx + px] = v[ch] * Tj[i] - (Rc[ch] - P[ch]) * i1f;
+                            for (int ch = 0; ch < 4; ++ch) {
+                                P[ch] += v[ch] * w;
+                                dR[ch] = v[ch] * Tj[i] - (Rc[ch] - P[ch]) * i1f;
+                            }
+                            const PackedSplat& g = sp[e];
+                            // d f / d(param) (losses.cpp:297-304); zero when clamped or alpha == 0
+                            const bool chain = !clamped && g.alpha > 0.0;
+                            const double* ek = sEnt + e * 8;  // r, 1/z, 1/alpha, 1/r^2, 1/r^3, ...
+                            const double r = ek[0];
+                            const double iz = ek[1];
+                            const double dx = dpx - g.mx, dy = dpy - g.my;
+                            const double d2 = dx * dx + dy * dy;
+                            const double fa = chain ? f * ek[2] : 0.0;
+                            const double fmx = chain ? f * dx * ek[3] : 0.0;
+                            const double fmy = chain ? f * dy * ek[3] : 0.0;
+                            const double fr = chain ? f * d2 * ek[4] : 0.0;
+                            // d_cam(ch) = dR_ch/df * u + [ch == depth] * w * e_z with
+                            // u = (fmx fx/z, fmy fy/z, -(fmx (mx-cx) + fmy (my-cy) + fr r) / z)
+                            // (losses.cpp:323-326), so with v = R u (world, R = Rcw^T):
+                            //   sum_ch J_a^2 = S_rgb v_a^2 + (dR_D/df v_a + w R_{a,z})^2
+                            const double ux = fmx * p.cam.fx * iz;
+                            const double uy = fmy * p.cam.fy * iz;
+                            const double uz = -(fmx * ek[6] + fmy * ek[7] + fr * r) * iz;
+                            const double Srgb = dR[0] * dR[0] + dR[1] * dR[1] + dR[2] * dR[2];
+                            const double Sall = Srgb + dR[3] * dR[3];
+#pragma unroll
+                            for (int a = 0; a < 3; ++a) {
+                                const double va = sR[a] * ux + sR[3 + a] * uy + sR[6 + a] * uz;
+                                const double dep = dR[3] * va + w * sR[6 + a];
+                                J[a] = Srgb * va * va + dep * dep;
+                            }
+                            const double jl = fr * r;     // d/d log_r (:333)
+                            const double jo = fa * ek[5];  // d/d logit (:334)
+                            J[3] = Sall * jl * jl;
+                            J[4] = Sall * jo * jo;
+#pragma unroll
+                            for (int ch = 0; ch < 3; ++ch) {
+                                const double c = v[ch];
+                                if (c > 0.0 && c < 1.0) J[5 + ch] = w * w;  // losses.cpp:291-294
+                            }
                         }
+                        double* rslot = red + (e * 2 + (px >> 5)) * 8;
+                        if (!__any_sync(0xffffffffu, contrib)) {
+                            if (lane < 8) rslot[lane] = 0.0;
+                            continue;
+                        }
+                        // butterfly reduce-scatter of the 8 sums over the warp's 32 pixels (9
+                        // double shuffles instead of 8 trees of 5; fixed pattern, deterministic):
+                        // halve the parameter set at xor 16, 8, 4, then add across xor 2, 1; lane
+                        // l ends with parameter (l >> 2) & 7
+                        const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+                        double K4[4], K2[2];
+#pragma unroll
+                        for (int k4 = 0; k4 < 4; ++k4) {
+                            const double send = h16 ? J[k4] : J[k4 + 4];
+                            const double keep = h16 ? J[k4 + 4] : J[k4];
+                            K4[k4] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                        }
+#pragma unroll
+                        for (int k2 = 0; k2 < 2; ++k2) {
+                            const double send = h8 ? K4[k2] : K4[k2 + 2];
+                            const double keep = h8 ? K4[k2 + 2] : K4[k2];
+                            K2[k2] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                        }
+                        double sv = (h4 ? K2[1] : K2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? K2[0] : K2[1], 4);
+                        sv += __shfl_xor_sync(0xffffffffu, sv, 2);
+                        sv += __shfl_xor_sync(0xffffffffu, sv, 1);
+                        if ((lane & 3) == 0) rslot[(lane >> 2) & 7] = sv;
                     }
                     if (part == 0)  // P at the next batch's start (the other buffer)
                         for (int ch = 0; ch < 4; ++ch)
@@ -315,94 +380,11 @@ __global__ void __launch_bounds__(kFThreads, 3) k_fisher(RasterParams p, FisherP
                                                 sseg[(2 * 4 + ch) * kTilePx + px]) + sseg[(3 * 4 + ch) * kTilePx + px]);
                 }
             }
-            fisher_sync();
 
-            // phase C (pass 1): squared Jacobians, reduced over the block's pixels
+            // pass 1: the squared-Jacobian sums of the batch's entries -> H (prior) or the
+            // gain (red is rewritten by the next batch, two barriers later)
             if (pass == 1) {
-#pragma unroll 1
-                for (int i = 0; i < kFNB / 4; ++i) {
-                    const int e = e_first + 4 * i;
-                    if (e >= n) break;  // warp-uniform (e depends on the warp only)
-                    double J[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                    const int s = e * kTilePx + px;
-                    const double code = F[s];
-                    const bool contrib = code != kNotContrib;
-                    if (contrib) {
-                        const bool clamped = code == kClamped;
-                        const double f = clamped ? kMaxFootprint : code;
-                        const double w = Wv[s];
-                        const PackedSplat& g = sp[e];
-                        // d f / d(param) (losses.cpp:297-304); zero when clamped or alpha == 0
-                        const bool chain = !clamped && g.alpha > 0.0;
-                        const double* ek = sEnt + e * 8;  // r, 1/z, 1/alpha, 1/r^2, 1/r^3, ...
-                        const double r = ek[0];
-                        const double iz = ek[1];
-                        const double dx = dpx - g.mx, dy = dpy - g.my;
-                        const double d2 = dx * dx + dy * dy;
-                        const double fa = chain ? f * ek[2] : 0.0;
-                        const double fmx = chain ? f * dx * ek[3] : 0.0;
-                        const double fmy = chain ? f * dy * ek[3] : 0.0;
-                        const double fr = chain ? f * d2 * ek[4] : 0.0;
-                        // d_cam(ch) = dR_ch/df * u + [ch == depth] * w * e_z with
-                        // u = (fmx fx/z, fmy fy/z, -(fmx (mx-cx) + fmy (my-cy) + fr r) / z)
-                        // (losses.cpp:323-326), so with v = R u (world, R = Rcw^T):
-                        //   sum_ch J_a^2 = S_rgb v_a^2 + (dR_D/df v_a + w R_{a,z})^2
-                        const double ux = fmx * p.cam.fx * iz;
-                        const double uy = fmy * p.cam.fy * iz;
-                        const double uz = -(fmx * ek[6] + fmy * ek[7] + fr * r) * iz;
-                        const double d0 = DR[(0 * kFNB + e) * kTilePx + px];
-                        const double d1 = DR[(1 * kFNB + e) * kTilePx + px];
-                        const double d2c = DR[(2 * kFNB + e) * kTilePx + px];
-                        const double dD = DR[(3 * kFNB + e) * kTilePx + px];
-                        const double Srgb = d0 * d0 + d1 * d1 + d2c * d2c;
-                        const double Sall = Srgb + dD * dD;
-#pragma unroll
-                        for (int a = 0; a < 3; ++a) {
-                            const double va = sR[a] * ux + sR[3 + a] * uy + sR[6 + a] * uz;
-                            const double dep = dD * va + w * sR[6 + a];
-                            J[a] = Srgb * va * va + dep * dep;
-                        }
-                        const double jl = fr * r;                       // d/d log_r (:333)
-                        const double jo = fa * ek[5];                   // d/d logit (:334)
-                        J[3] = Sall * jl * jl;
-                        J[4] = Sall * jo * jo;
-#pragma unroll
-                        for (int ch = 0; ch < 3; ++ch) {
-                            const double c = scol[4 * e + ch];
-                            if (c > 0.0 && c < 1.0) J[5 + ch] = w * w;  // losses.cpp:291-294
-                        }
-                    }
-                    if (!__any_sync(0xffffffffu, contrib)) {
-                        if (lane < 8) red[(e * 2 + (px >> 5)) * 8 + lane] = 0.0;
-                        continue;
-                    }
-                    // butterfly reduce-scatter of the 8 sums over the warp's 32 pixels (9 double
-                    // shuffles instead of 8 trees of 5; fixed pattern, deterministic): halve the
-                    // parameter set at xor 16, 8, 4, then add across xor 2, 1; lane l ends with
-                    // parameter (l >> 2) & 7
-                    {
-                        const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
-                        double K4[4], K2[2];
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            const double send = h16 ? J[i] : J[i + 4];
-                            const double keep = h16 ? J[i + 4] : J[i];
-                            K4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-                        }
-#pragma unroll
-                        for (int i = 0; i < 2; ++i) {
-                            const double send = h8 ? K4[i] : K4[i + 2];
-                            const double keep = h8 ? K4[i + 2] : K4[i];
-                            K2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-                        }
-                        double v = (h4 ? K2[1] : K2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? K2[0] : K2[1], 4);
-                        v += __shfl_xor_sync(0xffffffffu, v, 2);
-                        v += __shfl_xor_sync(0xffffffffu, v, 1);
-                        if ((lane & 3) == 0) red[(e * 2 + (px >> 5)) * 8 + ((lane >> 2) & 7)] = v;
-                    }
-                }
                 fisher_sync();
-                // (red is rewritten by the next batch's phase C, three barriers later)
                 if (t < n * 8) {
                     const int e = t >> 3, q = t & 7;
                     const double sum = red[(e * 2) * 8 + q] + red[(e * 2 + 1) * 8 + q];
