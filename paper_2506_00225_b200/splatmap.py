@@ -485,8 +485,9 @@ class Context:
 
     def _forget(self, key) -> None:
         hit = self._maps.pop(key, None)
-        if hit is not None and self.handle:
-            N.lib.sgm_map_release(self.handle, hit[2])
+        lib = getattr(N, "lib", None) if N is not None else None  # None at interpreter exit
+        if hit is not None and self.handle and lib is not None:
+            lib.sgm_map_release(self.handle, hit[2])
 
     def upload_arrays(self, gmap: GaussianMap) -> C.c_void_p:
         n = gmap.size()
