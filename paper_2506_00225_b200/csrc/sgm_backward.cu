@@ -517,11 +517,9 @@ void launch_loss_pixels(const BackwardParams& b, double* part, double* totals, c
 
 void launch_backward(const RasterParams& p, const BackwardParams& b, cudaStream_t s) {
     const size_t smem = static_cast<size_t>(bw_layout(p.map.C, p.map.kpad).total);
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaFuncSetAttribute(k_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        configured = smem;
-    }
+    // (per launch: the attribute is per device, and contexts on several devices may share
+    // the process)
+    cudaFuncSetAttribute(k_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_backward<<<static_cast<unsigned>(p.tiles_per_view), kBThreads, smem, s>>>(p, b);
 }
 

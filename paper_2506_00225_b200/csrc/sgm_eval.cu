@@ -181,12 +181,11 @@ void launch_eval_view(const double* sem, const double* sil, const float* fsem, i
                       unsigned long long* confusion, unsigned long long* counters, uint16_t* label,
                       float* scores, cudaStream_t s) {
     const size_t smem = eval_view_smem(C);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
+    // (per launch: the attribute is per device, and contexts on several devices may share
+    // the process)
+    if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_eval_view, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
-        configured = smem;
-    }
     if (px > 0)
         k_eval_view<<<nb(px, kTileP), kEvalThreads, smem, s>>>(sem, sil, fsem, px, C, confusion,
                                                                counters, label, scores);

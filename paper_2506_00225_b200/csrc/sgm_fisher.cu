@@ -414,11 +414,9 @@ template <bool kGain>
 void launch_fisher_t(const RasterParams& p, const FisherParams& fp, int n_views, cudaStream_t s) {
     auto kern = k_fisher<kGain>;
     const size_t smem = static_cast<size_t>(fisher_layout().total);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        configured = true;
-    }
+    // (per launch: the attribute is per device, and contexts on several devices may share
+    // the process)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     dim3 grid(static_cast<unsigned>(p.tiles_per_view), static_cast<unsigned>(n_views), 1);
     kern<<<grid, kFThreads, smem, s>>>(p, fp);
 }
