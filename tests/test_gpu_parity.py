@@ -383,3 +383,26 @@ def test_randomised_scenes_vs_oracle(ctx, orc, seed):
     nm_o, es_o, _ = orc.score_views(gm, cam, [pose], opts)
     assert nm[0] == nm_o[0]
     np.testing.assert_allclose(es, es_o, rtol=ENT_RTOL, atol=1e-300)
+
+
+@pytest.mark.parametrize("wh", [(21, 13), (48, 8), (9, 9)], ids=["6-blocks", "6-row", "4-blocks"])
+def test_block_items_cross_views(ctx, orc, wh):
+    """A raster CTA blends 4 consecutive (view, block) items, so with 6 blocks per view one CTA
+    spans two views: every view's scores and renders must still match the oracle, and the
+    batched results must equal the one-at-a-time ones (the block a CTA starts on differs)."""
+    w, h = wh
+    cam = CameraModel(w, h, 0, 0, 0.9 * w, 0.9 * w, 0.47 * w, 0.52 * h)
+    pose = look_at([0.0, 0.0, -0.4], [0.0, 0.1, 2.5])
+    gm = random_map(11, 300, cam, pose, k=4, num_classes=9)
+    rng = np.random.default_rng(5)
+    poses = [look_at(rng.normal(0, 0.1, 3) + [0.0, 0.0, -0.4], [0.0, 0.1, 2.5] + rng.normal(0, .3, 3))
+             for _ in range(7)]
+    nm, es = sgm.score_poses(gm, cam, poses, ctx=ctx)
+    nm_o, es_o, _ = orc.score_views(gm, cam, poses, RenderOptions())
+    np.testing.assert_array_equal(nm, nm_o)
+    np.testing.assert_allclose(es, es_o, rtol=ENT_RTOL, atol=0)
+    for i in (0, 3, 6):
+        a, b = sgm.score_poses(gm, cam, [poses[i]], ctx=ctx)
+        assert a[0] == nm[i] and b[0] == es[i]
+    out = sgm.render(gm, cam, poses[2], RenderChannels.all(), ctx=ctx)
+    assert_planes(out, orc.render(gm, cam, poses[2], 7))
