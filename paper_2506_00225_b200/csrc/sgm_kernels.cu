@@ -435,12 +435,16 @@ __global__ void __launch_bounds__(kScanThreads) k_bin_scan(int* __restrict__ dif
 }
 
 // Each tile row's list (ranks in rank order) is cut into segments of kSeg entries; a
-// segment x 32-column block is one warp's work unit. Lanes hold 32 consecutive entries of
-// a chunk; for every column of the block a ballot over the chunk marks the covering
-// entries, which take consecutive slots of that column's list (coalesced stores). The
-// column cursors live in the registers of the lanes (lane l <-> column cb + l).
-//   pass 0 counts per (segment, column), k_seg_scan turns them into per-segment bases,
-//   pass 1 writes. Segments of a row are independent, so dense rows spread over the GPU.
+// segment x 32-column block is one warp's work unit. The column cursors live in the
+// registers of the lanes (lane l <-> column cb + l). Lanes load 32 consecutive entries of
+// a chunk; a ballot keeps the entries whose column span meets the block. A sparse chunk
+// (under two covering entries per column of the block: cfg1 / cfg3) is walked entry by entry
+// in rank order, the entry broadcast and every lane whose column it covers appending its
+// rank to that column's list; a dense chunk (cfg4) is walked column by column, a ballot
+// giving the covering entries consecutive slots of the column's list (coalesced stores).
+//   k_seg_count counts per (segment, column), k_seg_scan turns them into per-segment
+//   bases, k_seg_pass writes. Segments of a row are independent, so dense rows spread over
+//   the GPU.
 constexpr int kSeg = 1024;
 
 __global__ void __launch_bounds__(1024) k_row_segs(const uint2* __restrict__ row_ranges, int tiles_y,
@@ -472,11 +476,10 @@ __global__ void __launch_bounds__(1024) k_row_segs(const uint2* __restrict__ row
     if (t == 1023) *nseg_out = part[1023];
 }
 
-template <bool kWrite>
 __global__ void __launch_bounds__(256) k_seg_pass(const unsigned long long* __restrict__ row_list,
                                                   const uint4* __restrict__ segs,
                                                   const uint32_t* __restrict__ nseg, int tiles_x,
-                                                  uint32_t* __restrict__ cnt, uint32_t* __restrict__ list) {
+                                                  const uint32_t* __restrict__ cnt, uint32_t* __restrict__ list) {
     const uint32_t g = blockIdx.x;
     if (g >= *nseg) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -486,27 +489,40 @@ __global__ void __launch_bounds__(256) k_seg_pass(const unsigned long long* __re
     const int col = cb + lane;
     const bool has = col < tiles_x;
     const int last = min(tiles_x, cb + 32) - 1;
-    uint32_t cur = (kWrite && has) ? cnt[static_cast<size_t>(g) * tiles_x + col] : 0u;
-    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t cur = has ? cnt[static_cast<size_t>(g) * tiles_x + col] : 0u;
     for (uint32_t base = sg.y; base < sg.z; base += 32) {
         const bool valid = base + lane < sg.z;
         const unsigned long long e = valid ? row_list[base + lane] : 0ull;
-        const int x0 = valid ? static_cast<int>((e >> 16) & 0xffffu) : INT_MAX;
-        const int x1 = valid ? static_cast<int>(e & 0xffffu) : INT_MIN;
-        const int lo = max(cb, __reduce_min_sync(0xffffffffu, x0));
-        const int hi = min(last, __reduce_max_sync(0xffffffffu, x1));
-        for (int c = lo; c <= hi; ++c) {
-            const bool cov = x0 <= c && c <= x1;
-            const uint32_t bal = __ballot_sync(0xffffffffu, cov);
-            const int owner = c - cb;
-            if (kWrite) {
-                const uint32_t at = __shfl_sync(0xffffffffu, cur, owner);
-                if (cov) list[at + __popc(bal & lt)] = static_cast<uint32_t>(e >> 32);
+        const int x0 = static_cast<int>((e >> 16) & 0xffffu);
+        const int x1 = static_cast<int>(e & 0xffffu);
+        const bool rel = valid && x0 <= last && x1 >= cb;
+        uint32_t m = __ballot_sync(0xffffffffu, rel);
+        if (!m) continue;
+        // (entry, column) pairs of the chunk in this block: sparse below two per column
+        const int span = rel ? min(x1, last) - max(x0, cb) + 1 : 0;
+        if (__reduce_add_sync(0xffffffffu, static_cast<unsigned>(span)) < 64u) {
+            while (m) {  // sparse: the chunk's entries that reach this block, in rank order
+                const int j = __ffs(m) - 1;
+                m &= m - 1u;
+                const unsigned long long ej = __shfl_sync(0xffffffffu, e, j);
+                const int jx0 = static_cast<int>((ej >> 16) & 0xffffu), jx1 = static_cast<int>(ej & 0xffffu);
+                if (has && jx0 <= col && col <= jx1) list[cur++] = static_cast<uint32_t>(ej >> 32);
             }
-            if (lane == owner) cur += __popc(bal);
+        } else {
+            // dense: per column, a ballot gives the covering entries consecutive slots of that
+            // column's list (coalesced stores)
+            const int lo = max(cb, __reduce_min_sync(0xffffffffu, rel ? x0 : INT_MAX));
+            const int hi = min(last, __reduce_max_sync(0xffffffffu, rel ? x1 : INT_MIN));
+            for (int c = lo; c <= hi; ++c) {
+                const bool cov = rel && x0 <= c && c <= x1;
+                const uint32_t bal = __ballot_sync(0xffffffffu, cov);
+                const int owner = c - cb;
+                const uint32_t at = __shfl_sync(0xffffffffu, cur, owner);
+                if (cov) list[at + __popc(bal & ((1u << lane) - 1u))] = static_cast<uint32_t>(e >> 32);
+                if (lane == owner) cur += __popc(bal);
+            }
         }
     }
-    if (!kWrite && has) cnt[static_cast<size_t>(g) * tiles_x + col] = cur;
 }
 
 // Pass 0 without ballots: a segment's per-column counts from a shared-memory difference
@@ -745,7 +761,7 @@ void launch_row_scatter(const unsigned long long* row_list, const uint2* row_ran
         row_list, segs, nseg, tiles_x, cnt);
     k_seg_scan<<<blocks_for(static_cast<uint64_t>(tiles_x) * tiles_y, 256), 256, 0, s>>>(
         segs, nseg, tile_ranges, tiles_x, tiles_y, cnt);
-    k_seg_pass<true><<<grid, 32 * warps, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list);
+    k_seg_pass<<<grid, 32 * warps, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list);
 }
 
 uint64_t row_scatter_segments(uint64_t R, int tiles_y) {

@@ -6,8 +6,9 @@
 //   2. one D2H of the per-view V/P/R counts (the only host sync before the results)
 //   3. per view (binning stream): CUB radix sort on fp32(z) -> k_tiefix -> k_pack ->
 //      k_bin_hist + k_bin_scan (tile ranges) -> k_emit_rows + CUB stable row sort ->
-//      k_row_segs / k_seg_pass x2 / k_seg_scan (ordered scatter into the tile lists)
-//   4. one batched raster launch over (8x8 tile, view)
+//      k_row_segs / k_seg_count / k_seg_scan / k_seg_pass (ordered scatter into the tile lists)
+//   4. raster launches of 8 views each over (8x8 block, view), overlapping the binning of
+//      the next 8 views
 //   5. k_reduce_scores (score) / planes already written (render)
 // Views whose pair lists do not fit the scratch budget together are split into
 // sub-batches; results do not depend on the split (per-view work is independent).
