@@ -28,9 +28,15 @@ def mb(name):  # ncu reports DRAM bytes in Mbyte / Gbyte / byte
 stalls = {k[len("smsp__pcsamp_warps_issue_stalled_"):]: num(k) for k in m
           if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("_not_issued")}
 tot = sum(stalls.values())
+def ms(name):  # ncu picks the time unit per kernel (nsecond / usecond / msecond / second)
+    val, unit = num(name), m[name][1]
+    return val * {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0,
+                  "ms": 1.0, "second": 1e3, "s": 1e3}[unit]
+
+
 res = {
     "kernel": m["Kernel Name"][0] if "Kernel Name" in m else "",
-    "duration_ms": num("gpu__time_duration.sum"),
+    "duration_ms": ms("gpu__time_duration.sum"),
     "warp_instructions": num("smsp__inst_executed.sum"),
     "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
     "smem_wavefronts": num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
