@@ -152,27 +152,45 @@ __global__ void __launch_bounds__(256) k_preprocess(DevMap m, const PoseParams* 
     unsigned long long cnt = vis ? rect_count(rc0) : 0ull;
     unsigned long long rows = cnt ? static_cast<unsigned long long>(rc0.ty1 - rc0.ty0 + 1) : 0ull;
 
+    // block-aggregated compaction: one atomic per block and view (per-warp atomics on the
+    // view's counter serialise in L2 and dominated this kernel)
     const unsigned mask = __ballot_sync(0xffffffffu, vis);
-    const int lane = threadIdx.x & 31;
-    uint32_t base = 0;
-    if (mask) {
-        const int leader = __ffs(mask) - 1;
-        if (lane == leader) base = atomicAdd(&vcount[v], static_cast<uint32_t>(__popc(mask)));
-        base = __shfl_sync(0xffffffffu, base, leader);
-    }
-    if (vis) {
-        const uint32_t pos = base + __popc(mask & ((1u << lane) - 1u));
-        keys[v * stride + pos] = sortable(static_cast<float>(q.z));  // monotone in z
-        vals[v * stride + pos] = static_cast<uint32_t>(i);
-    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         cnt += __shfl_down_sync(0xffffffffu, cnt, off);
         rows += __shfl_down_sync(0xffffffffu, rows, off);
     }
-    if (lane == 0 && cnt) {
-        atomicAdd(&pcount[v], cnt);
-        atomicAdd(&rcount[v], rows);
+    __shared__ uint32_t wvis[8];
+    __shared__ unsigned long long wcnt[8], wrows[8];
+    __shared__ uint32_t bbase;
+    if (lane == 0) {
+        wvis[warp] = static_cast<uint32_t>(__popc(mask));
+        wcnt[warp] = cnt;
+        wrows[warp] = rows;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tot = 0;
+        unsigned long long tc = 0, tr = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            const uint32_t c = wvis[w];
+            wvis[w] = tot;  // exclusive offset of warp w
+            tot += c;
+            tc += wcnt[w];
+            tr += wrows[w];
+        }
+        bbase = tot ? atomicAdd(&vcount[v], tot) : 0u;
+        if (tc) {
+            atomicAdd(&pcount[v], tc);
+            atomicAdd(&rcount[v], tr);
+        }
+    }
+    __syncthreads();
+    if (vis) {
+        const uint32_t pos = bbase + wvis[warp] + __popc(mask & ((1u << lane) - 1u));
+        keys[v * stride + pos] = sortable(static_cast<float>(q.z));  // monotone in z
+        vals[v * stride + pos] = static_cast<uint32_t>(i);
     }
 }
 
@@ -369,10 +387,9 @@ __global__ void k_emit_rows(const unsigned long long* __restrict__ offsets, cons
 //                scan in bin order -> ranges[bin] = (begin, end);
 //   rows         (row, rank) pairs emitted in rank order and stably sorted by row (small:
 //                one pair per spanned row, not per tile) -> each row's ranks in rank order;
-//   k_row_scatter one CTA per tile row: chunks of 32 consecutive ranks; warp w owns the
-//                columns tx = w mod 8, and for each column a ballot over the chunk gives every
-//                covering rank its slot (cursor + popc of the lanes before it), so each tile's
-//                list is written in rank order with coalesced stores.
+//   row scatter  each row's ranks cut into segments of kSeg; per (segment, 32 columns) one
+//                warp appends the covering ranks to the columns' lists in rank order
+//                (k_row_segs, k_seg_count, k_seg_scan, k_seg_pass below).
 __global__ void k_bin_hist(const int4* __restrict__ rects, uint32_t V, int tiles_x,
                            int* __restrict__ diff, unsigned long long* __restrict__ rows) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
