@@ -714,6 +714,41 @@ __global__ void k_sort_rows(const uint16_t* __restrict__ idx, const double* __re
     }
 }
 
+// The same for k <= 32, coalesced: a group of G lanes (G = the power of two >= k) per row,
+// lane j holding entry j; its slot is its stable rank (entries of smaller class, or of the
+// same class and earlier position), found by broadcasting the row's classes.
+__global__ void k_sort_rows_group(const uint16_t* __restrict__ idx, const double* __restrict__ prob,
+                                  uint64_t n, int k, int kpad, int G, uint16_t* __restrict__ out_idx,
+                                  double* __restrict__ out_prob, uint16_t* __restrict__ out_perm) {
+    const uint64_t gt = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t row = gt / static_cast<unsigned>(G);
+    const int j = static_cast<int>(gt % static_cast<unsigned>(G));
+    const bool live = row < n;
+    const bool mine = live && j < k;
+    int c = 0x10000;  // above every class id
+    double pv = 0.0;
+    if (mine) {
+        c = idx[row * k + j];
+        pv = prob[row * k + j];
+    }
+    int rank = 0;
+    for (int m = 0; m < k; ++m) {
+        const int cm = __shfl_sync(0xffffffffu, c, m, G);
+        rank += (cm < c || (cm == c && m < j)) ? 1 : 0;
+    }
+    if (mine) {
+        out_idx[row * kpad + rank] = static_cast<uint16_t>(c);
+        out_prob[row * kpad + rank] = pv;
+        out_perm[row * kpad + rank] = static_cast<uint16_t>(j);
+    }
+    if (live)
+        for (int q = k + j; q < kpad; q += G) {
+            out_idx[row * kpad + q] = 0xffff;
+            out_prob[row * kpad + q] = 0.0;
+            out_perm[row * kpad + q] = 0;
+        }
+}
+
 inline unsigned blocks_for(uint64_t n, unsigned threads) {
     return static_cast<unsigned>((n + threads - 1) / threads);
 }
@@ -806,6 +841,13 @@ void launch_debug_projections(const DevMap& m, const PoseParams* d_pose, const C
 void launch_sort_rows(const uint16_t* idx, const double* prob, uint64_t n, int k, int kpad,
                       uint16_t* out_idx, double* out_prob, uint16_t* out_perm, cudaStream_t s) {
     if (n == 0) return;
+    if (k <= 32) {
+        int G = 1;
+        while (G < k) G <<= 1;
+        k_sort_rows_group<<<blocks_for(n * G, 256), 256, 0, s>>>(idx, prob, n, k, kpad, G, out_idx,
+                                                                 out_prob, out_perm);
+        return;
+    }
     k_sort_rows<<<blocks_for(n, 256), 256, 0, s>>>(idx, prob, n, k, kpad, out_idx, out_prob,
                                                    out_perm);
 }
