@@ -531,15 +531,13 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                     if (vd.depth) vd.depth[pix] = adep;
                     if (vd.contrib && !vd.contrib_offset) vd.contrib_count[pix] = ncontrib_px;
                 }
-                if (vd.sem) {
-                    for (int l = t; l < kTilePx * C; l += kCompute) {
-                        const int qq = l / C;
-                        const int c = l - qq * C;
+                if (vd.sem) {  // warp per pixel, lanes over its C channels (coalesced rows)
+                    for (int qq = warp; qq < kTilePx; qq += kWarps) {
                         const int qx = bx * kTile + px_col(qq);
                         const int qy = by * kTile + px_row(qq);
-                        if (qx < p.cam.W && qy < p.cam.H)
-                            vd.sem[(static_cast<size_t>(qy) * p.cam.W + qx) * C + c] =
-                                acc[pair_slot(c, apitch, qq)];
+                        if (qx >= p.cam.W || qy >= p.cam.H) continue;
+                        double* dst = vd.sem + (static_cast<size_t>(qy) * p.cam.W + qx) * C;
+                        for (int c = lane; c < C; c += 32) dst[c] = acc[pair_slot(c, apitch, qq)];
                     }
                 }
             } else {
@@ -629,7 +627,8 @@ void launch_t(const RasterParams& p0, int n_views, cudaStream_t s) {
     auto kern = k_raster<kRender, kDup, kAniso, kRc, 3>;
     if constexpr (!kRender && !kRc)
         if (four) kern = k_raster<kRender, kDup, kAniso, kRc, 4>;
-    p.items_per_cta = kItemsPerCta;
+    // (render: usually one view per launch, so shorter CTAs balance the last wave better)
+    p.items_per_cta = kRender ? 2 : kItemsPerCta;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const int grid = (p.n_items + p.items_per_cta - 1) / p.items_per_cta;
     kern<<<grid, kThreads, smem, s>>>(p);

@@ -34,3 +34,9 @@ for _ in range(10):
     e1.synchronize()
     ms.append(e0.elapsed_time(e1))
 print(f"cfg{a.config} render device: {np.median(ms):.3f} ms")
+ctx.set_profiling(True)
+ctx.reset_stats()
+render_device(gm, cam, pose, RenderChannels.all(), ctx=ctx, **ptrs)
+ctx.synchronize()
+st = ctx.stats()
+print(f"  raster {st['raster_ms']:.3f} ms of a {st['binning_ms']:.3f} ms call span (profiled run)")
