@@ -515,6 +515,8 @@ void launch_loss_pixels(const BackwardParams& b, double* part, double* totals, c
     k_loss_totals<<<1, 32, 0, s>>>(part, static_cast<int>(nb), totals);
 }
 
+size_t backward_smem_bytes(int C, int kpad) { return static_cast<size_t>(bw_layout(C, kpad).total); }
+
 void launch_backward(const RasterParams& p, const BackwardParams& b, cudaStream_t s) {
     const size_t smem = static_cast<size_t>(bw_layout(p.map.C, p.map.kpad).total);
     // (per launch: the attribute is per device, and contexts on several devices may share

@@ -171,6 +171,7 @@ void eval_add_view(sgm_ctx* ctx, sgm_evaluator* ev, const sgm_map* map, const Ca
     const int M = C - 1;
     CK(v.scores.reserve(4ull * px * std::max(M, 1)));
     CK(v.labels.reserve(2ull * px));
+    need_smem(ctx->device, eval_view_smem(C), C, "evaluator");
     launch_eval_view(d_sem, d_sil, f_sem, static_cast<int>(px), C, conf, cnt, v.labels.as<uint16_t>(),
                      v.scores.as<float>(), s);
     launch_eval_photo(d_color, d_depth, f_rgb, f_depth, static_cast<int>(px), ev->photo_part.as<double>(),

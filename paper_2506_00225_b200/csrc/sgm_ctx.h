@@ -101,6 +101,16 @@ struct SgmError {
     throw SgmError{code, buf};
 }
 
+// Fails with SGM_ERR_UNSUPPORTED when a kernel's shared-memory layout (which grows with the
+// channel count: the per-block fp64 accumulator) exceeds the device's per-block limit.
+inline void need_smem(int device, size_t bytes, int channels, const char* what) {
+    int lim = 0;
+    cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    if (lim > 0 && bytes > static_cast<size_t>(lim))
+        fail(SGM_ERR_UNSUPPORTED, "%s: %d semantic channels need %zu B of shared memory per block "
+             "(device limit %d B)", what, channels, bytes, lim);
+}
+
 #define CK(call)                                                                       \
     do {                                                                               \
         cudaError_t e_ = (call);                                                       \

@@ -217,6 +217,7 @@ void launch_sort_rows(const uint16_t* idx, const double* prob, uint64_t n, int k
 size_t backward_loss_blocks(int W, int H);
 void launch_loss_pixels(const BackwardParams& b, double* part, double* totals, cudaStream_t s);
 void launch_backward(const RasterParams& p, const BackwardParams& b, cudaStream_t s);
+size_t backward_smem_bytes(int C, int kpad);
 void launch_chain(const DevMap& m, const PoseParams* d_pose, const CamParams& cam, const OptParams& o,
                   const uint32_t* order, uint32_t V, const double* gproj, const BackwardParams& b,
                   cudaStream_t s);
@@ -265,6 +266,7 @@ void launch_gather_u16(const uint16_t* src, uint16_t* dst, const uint32_t* kept,
                        int stride, cudaStream_t s);
 
 // sgm_eval.cu (semantic_metrics / photometric_metrics on device planes)
+size_t eval_view_smem(int C);
 void launch_eval_view(const double* sem, const double* sil, const float* fsem, int px, int C,
                       unsigned long long* confusion, unsigned long long* counters, uint16_t* label,
                       float* scores, cudaStream_t s);

@@ -129,6 +129,8 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
     const int rty = (cam.H + kTile - 1) / kTile;
     const int rtiles = rtx * rty;
     ctx->last_valid = false;
+    // (the render layout bounds every raster variant: wider accumulator rows, colour stage)
+    need_smem(ctx->device, raster_smem_bytes(map->dev, map->groups, true), map->dev.C, "raster");
 
     // batch size bounded by a scratch budget for the per-view N-sized arrays
     const size_t per_view = std::max<uint64_t>(N, 1) * (4 + 4 + sizeof(PackedSplat) + 16) +
@@ -517,6 +519,7 @@ void backward_core(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const
     rp.raster_tiles_x = (cam.W + kTile - 1) / kTile;
     rp.channels = rt.channels;
     rp.groups = map->groups;
+    need_smem(ctx->device, backward_smem_bytes(map->dev.C, map->dev.kpad), map->dev.C, "backward");
     launch_backward(rp, b, s);
     // 4. projection -> world, KL clipping, finiteness
     launch_chain(map->dev, ctx->poses.as<PoseParams>(), cam, o, ctx->vals.as<uint32_t>(), V,

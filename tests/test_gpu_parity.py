@@ -406,3 +406,20 @@ def test_block_items_cross_views(ctx, orc, wh):
         assert a[0] == nm[i] and b[0] == es[i]
     out = sgm.render(gm, cam, poses[2], RenderChannels.all(), ctx=ctx)
     assert_planes(out, orc.render(gm, cam, poses[2], 7))
+
+
+def test_many_classes_and_the_shared_memory_limit(ctx, orc):
+    """The per-block fp64 accumulator holds C channels: 300 classes still fit (one block per SM)
+    and match the oracle; 1000 classes exceed the shared memory and fail loudly."""
+    cam = CameraModel(40, 24, 0, 0, 36.0, 36.0, 20.1, 11.9)
+    pose = look_at([0.0, 0.0, -0.4], [0.0, 0.1, 2.5])
+    gm = random_map(21, 120, cam, pose, k=12, num_classes=300)
+    out = sgm.render(gm, cam, pose, RenderChannels.all(), ctx=ctx)
+    assert_planes(out, orc.render(gm, cam, pose, 7))
+    nm, es = sgm.score_poses(gm, cam, [pose], ctx=ctx)
+    nm_o, es_o, _ = orc.score_views(gm, cam, [pose], RenderOptions())
+    np.testing.assert_array_equal(nm, nm_o)
+    np.testing.assert_allclose(es, es_o, rtol=ENT_RTOL, atol=0)
+    big = random_map(22, 50, cam, pose, k=4, num_classes=1000)
+    with pytest.raises(RuntimeError, match="shared memory"):
+        sgm.score_poses(big, cam, [pose], ctx=ctx)
