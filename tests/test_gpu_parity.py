@@ -144,6 +144,7 @@ CASES = [
     dict(seed=5, n=200, k=10, nc=9, opts=RenderOptions(transmittance_eps=1e-2)),  # k = C
     dict(seed=6, n=600, k=16, nc=101, opts=RenderOptions()),
     dict(seed=7, n=150, k=1, nc=3, opts=RenderOptions(z_near=1.0)),
+    dict(seed=8, n=200, k=40, nc=60, opts=RenderOptions()),  # k > 32: rows sorted per thread
 ]
 
 
