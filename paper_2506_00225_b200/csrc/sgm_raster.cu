@@ -463,31 +463,49 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                     const bool nz = (w.x != 0.0) | (w.y != 0.0);
                     const uint16_t* ei = si + e * kpad;
                     const double* ep = spr + e * kpad;
-                    if (!nz) continue;  // lanes without weight issue no shared-memory traffic
-                    auto one = [&](int j) {
-                        double2* a = accl + ei[j] * apitch;
-                        double2 v = *a;
-                        v.x = __fma_rn(ep[j], w.x, v.x);  // :307
-                        v.y = __fma_rn(ep[j], w.y, v.y);
-                        *a = v;
+                    // lanes without weight skip the read-modify-writes: predicated shared loads
+                    // and stores (no branch, the warp stays converged), so their quarter-warps
+                    // issue no wavefronts; the FMAs on the unloaded registers are discarded
+                    const unsigned pz = nz ? 1u : 0u;
+                    auto rmw = [&](int c, double pj) {
+                        double2* a = accl + c * apitch;
+                        const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(a));
+                        double vx, vy;
+                        asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.shared.v2.f64 {%0, %1}, [%3]; }"
+                                     : "=d"(vx), "=d"(vy) : "r"(pz), "r"(sa) : "memory");
+                        vx = __fma_rn(pj, w.x, vx);  // :307
+                        vy = __fma_rn(pj, w.y, vy);
+                        asm volatile("{ .reg .pred q; setp.ne.u32 q, %0, 0; @q st.shared.v2.f64 [%1], {%2, %3}; }"
+                                     :: "r"(pz), "r"(sa), "d"(vx), "d"(vy) : "memory");
                     };
                     if (kDup) {
-                        for (int j = lo; j < hi; ++j) one(j);  // repeated classes: in order
+#pragma unroll 1
+                        for (int j = lo; j < hi; ++j) rmw(ei[j], ep[j]);  // repeated classes: in order
                     } else {
                         int j = lo;
-                        for (; j + 2 <= hi; j += 2) {
-                            double2* a0 = accl + ei[j] * apitch;
-                            double2* a1 = accl + ei[j + 1] * apitch;
+#pragma unroll 1
+                        for (; j + 2 <= hi; j += 2) {  // two distinct classes: both loads first
+                            const int c0 = ei[j], c1 = ei[j + 1];
                             const double p0 = ep[j], p1 = ep[j + 1];
-                            double2 v0 = *a0, v1 = *a1;
-                            v0.x = __fma_rn(p0, w.x, v0.x);
-                            v0.y = __fma_rn(p0, w.y, v0.y);
-                            v1.x = __fma_rn(p1, w.x, v1.x);
-                            v1.y = __fma_rn(p1, w.y, v1.y);
-                            *a0 = v0;
-                            *a1 = v1;
+                            const unsigned s0 = static_cast<unsigned>(__cvta_generic_to_shared(accl + c0 * apitch));
+                            const unsigned s1 = static_cast<unsigned>(__cvta_generic_to_shared(accl + c1 * apitch));
+                            double ax, ay, bx, by;
+                            asm volatile("{ .reg .pred q; setp.ne.u32 q, %4, 0;\n"
+                                         " @q ld.shared.v2.f64 {%0, %1}, [%5];\n"
+                                         " @q ld.shared.v2.f64 {%2, %3}, [%6]; }"
+                                         : "=d"(ax), "=d"(ay), "=d"(bx), "=d"(by)
+                                         : "r"(pz), "r"(s0), "r"(s1) : "memory");
+                            ax = __fma_rn(p0, w.x, ax);
+                            ay = __fma_rn(p0, w.y, ay);
+                            bx = __fma_rn(p1, w.x, bx);
+                            by = __fma_rn(p1, w.y, by);
+                            asm volatile("{ .reg .pred q; setp.ne.u32 q, %0, 0;\n"
+                                         " @q st.shared.v2.f64 [%1], {%3, %4};\n"
+                                         " @q st.shared.v2.f64 [%2], {%5, %6}; }"
+                                         :: "r"(pz), "r"(s0), "r"(s1), "d"(ax), "d"(ay), "d"(bx), "d"(by)
+                                         : "memory");
                         }
-                        if (j < hi) one(j);
+                        if (j < hi) rmw(ei[j], ep[j]);
                     }
                 }
             }
