@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     // the block it stages for, the current one and then the next ----
     const int qi = kpad / 8, qp = kpad / 2;
     const int Q = 5 + qi + qp + ((kRender || kRc) ? 2 : 0);  // 16-byte chunks per Gaussian
+    const unsigned qmagic = static_cast<unsigned>((0x100000000ull + Q - 1) / Q);  // ceil(2^32 / Q)
     struct LoaderState {
         const uint32_t* list;
         const PackedSplat* packed;
@@ -168,7 +169,8 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         const PackedSplat* l_packed = ls.packed;
         const uint4* l_bounds = ls.bounds;
         for (int c = lane; c < n * Q; c += 32) {
-            const int e = c / Q;
+            // c / Q by a multiply-high (exact: c < kNB * Q is far below 2^32 / Q^2)
+            const int e = static_cast<int>(__umulhi(static_cast<unsigned>(c), qmagic));
             int q = c - e * Q;
             const uint2 v = slot[e];
             const unsigned char* src;
