@@ -144,8 +144,8 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     __shared__ int scnt[2][3];  // block parity q: entries of batch b in scnt[q][b % 3]
     __shared__ uint32_t slive[2];  // batch b: entries with a nonzero weight at some pixel
     __shared__ int s_item;
-    __shared__ double red_d[kTilePx];
-    __shared__ unsigned long long red_u[kTilePx];
+    __shared__ double red_d[2];                        // epilogue: the two pixel warps' entropy
+    __shared__ unsigned long long red_u[2 + kWarps];   // their missing counts, then K per warp
 
     // ---- loader state (in shared memory, so the compute warps carry no registers for it):
     // the block it stages for, the current one and then the next ----
