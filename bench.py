@@ -558,7 +558,9 @@ def main() -> None:
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE cfg%d)" % cfg,
-            "config": workload_config(cfg),
+            "config": dict(workload_config(cfg),
+                           parallelism=f"dp{world}: candidate views sharded over the ranks, map "
+                                       f"replicated (NCCL broadcast), per-view scores all-gathered"),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": int(st["kernel_launches"]),
