@@ -424,3 +424,19 @@ def test_many_classes_and_the_shared_memory_limit(ctx, orc):
     big = random_map(22, 50, cam, pose, k=4, num_classes=1000)
     with pytest.raises(RuntimeError, match="shared memory"):
         sgm.score_poses(big, cam, [pose], ctx=ctx)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 5, 8, 9, 16, 17, 31, 32, 33])
+def test_row_sort_widths_vs_oracle(ctx, orc, k):
+    """Rows are class-sorted on the GPU at upload by groups of lanes (the power of two >= k,
+    k <= 32) or per thread (k > 32); duplicate class ids keep their order. Every width gives
+    the oracle's planes and scores."""
+    cam = CameraModel(30, 22, 0, 0, 27.0, 27.0, 15.2, 10.9)
+    pose = look_at([0.0, 0.0, -0.4], [0.0, 0.1, 2.5])
+    gm = random_map(40 + k, 90, cam, pose, k=k, num_classes=max(k, 40), dup=k >= 2)
+    out = sgm.render(gm, cam, pose, RenderChannels.all(), ctx=ctx)
+    assert_planes(out, orc.render(gm, cam, pose, 7))
+    nm, es = sgm.score_poses(gm, cam, [pose], ctx=ctx)
+    nm_o, es_o, _ = orc.score_views(gm, cam, [pose], RenderOptions())
+    np.testing.assert_array_equal(nm, nm_o)
+    np.testing.assert_allclose(es, es_o, rtol=ENT_RTOL, atol=0)
