@@ -440,3 +440,25 @@ def test_row_sort_widths_vs_oracle(ctx, orc, k):
     nm_o, es_o, _ = orc.score_views(gm, cam, [pose], RenderOptions())
     np.testing.assert_array_equal(nm, nm_o)
     np.testing.assert_allclose(es, es_o, rtol=ENT_RTOL, atol=0)
+
+
+def test_bins_mixed_sparse_and_dense_rows(ctx, orc):
+    """Tile rows where some 32-entry chunks are sparse (Gaussians a few tiles wide: walked
+    entry by entry) and others dense (splats 30-120 px wide: walked column by column) give the
+    reference's bins bit-exactly."""
+    cam = CameraModel(600, 120, 0, 0, 300.0, 300.0, 299.5, 59.5)
+    pose = look_at([0.0, 0.0, -0.4], [0.0, 0.0, 2.5])
+    small = random_map(51, 1500, cam, pose, k=3, num_classes=7, rad_px=(0.5, 4.0))
+    big = random_map(52, 400, cam, pose, k=3, num_classes=7, rad_px=(10.0, 40.0))
+    gm = sgm.GaussianMap.from_arrays(
+        3, 7, np.concatenate([small.centers, big.centers]),
+        np.concatenate([small.log_radii, big.log_radii]),
+        np.concatenate([small.opacity_logits, big.opacity_logits]),
+        np.concatenate([small.colors, big.colors]),
+        np.concatenate([small.sem_indices, big.sem_indices]),
+        np.concatenate([small.sem_probs, big.sem_probs]))
+    opts = RenderOptions()
+    out = sgm.render(gm, cam, pose, RenderChannels.all(), opts, ctx=ctx)
+    assert_projections(out, orc.project(gm, cam, pose, opts))
+    assert_bins(ctx, orc, gm, cam, pose, opts, out)
+    assert_planes(out, orc.render(gm, cam, pose, 7, opts))
