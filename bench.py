@@ -34,6 +34,8 @@ sys.path.insert(0, str(ROOT))
 VIEWS_PER_GPU = 64
 METRIC = "candidate views scored/sec"
 UNIT = "views/s"
+DATA = "synthetic (seeded, BASELINE cfg%d)"
+CURRENT_POSITION = np.array([4.0, 1.5, 3.0])  # combine_scores' current position (box centre)
 
 
 def _mem_available_gb() -> float:
@@ -113,26 +115,81 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_run(cfg: int, views: int, threads: int, steps: int = 1, warmup: int = 0):
-    """The reference's refresh_candidate_scores (oracle/_ref) on host cores."""
+REF_SAMPLE_MAX = 16  # views per reference step: a bounded sample (about 2.5 s per view per core)
+
+
+def reference_threads() -> int:
+    """Host threads for the reference: all usable cores, bounded by RAM (one 0.7 GB
+    RenderOutput per concurrent cfg1 view) and by the sample size."""
     import oracle
-    from paper_2506_00225_b200 import scenes
-    ref = oracle.RefLib()
-    gm = scenes.make_map(cfg)
-    cam = scenes.CONFIGS[cfg].camera()
-    cands = scenes.make_candidates(cfg, views)
-    h = ref.map_create(gm)
+    return max(1, min(oracle.cpu_count(), int(_mem_available_gb() // 1.5), REF_SAMPLE_MAX))
+
+
+def assert_reference_alone() -> None:
+    """The reference arm must not map the product library (libsgm_b200.so)."""
+    try:
+        maps = open("/proc/self/maps").read()
+    except OSError:
+        return
+    if "libsgm_b200" in maps:
+        raise RuntimeError("reference arm: libsgm_b200.so is mapped in this process")
+
+
+def cpu_reference_run(gm, cam, cands, threads: int, steps: int = 1, warmup: int = 0, ref=None,
+                      handle=None):
+    """The reference's refresh_candidate_scores (oracle/_ref, compiled unmodified) over
+    `cands`, the views split into disjoint spans over `threads` host threads.
+    Returns (views/s, mean s per call, n_missing, entropy_sum)."""
+    import oracle
+    ref = ref or oracle.RefLib()
+    h = handle or ref.map_create(gm)
     pos = np.array([c.position for c in cands])
     dirs = np.array([c.direction for c in cands])
     times = []
+    nm = es = None
     for i in range(warmup + steps):
         t0 = time.perf_counter()
-        ref.refresh_scores(gm, cam, pos, dirs, threads=threads, handle=h)
+        nm, es = ref.refresh_scores(gm, cam, pos, dirs, threads=threads, handle=h)
         dt = time.perf_counter() - t0
         if i >= warmup:
             times.append(dt)
-    ref.map_destroy(h)
-    return views / float(np.mean(times)), float(np.mean(times))
+    if handle is None:
+        ref.map_destroy(h)
+    return len(cands) / float(np.mean(times)), float(np.mean(times)), nm, es
+
+
+def reference_one_thread(gm, cam, cand, ref, handle) -> dict:
+    """The reference as shipped: one thread (its candidate loop is serial,
+    explorer.cpp:188), one cfg view."""
+    v, sec, _, _ = cpu_reference_run(gm, cam, [cand], 1, 1, 0, ref=ref, handle=handle)
+    return {"value": v, "unit": UNIT, "cores": 1, "sample": f"candidate view {cand.id}, "
+            f"{sec:.2f} s"}
+
+
+def compare_scores(nm_a, es_a, nm_b, es_b, positions, current, ref) -> dict:
+    """Per-view parity of two score sets (a = ours, b = the reference) and of the
+    combine_scores decision on them (the reference's own combine_scores for both)."""
+    nm_a, es_a = np.asarray(nm_a, float), np.asarray(es_a, float)
+    nm_b, es_b = np.asarray(nm_b, float), np.asarray(es_b, float)
+    any_a, _, _, ta = ref.combine_scores(nm_a, es_a, positions, current)
+    any_b, _, _, tb = ref.combine_scores(nm_b, es_b, positions, current)
+    both_tiny = (np.abs(ta) < 1e-300) & (np.abs(tb) < 1e-300)  # SURVEY 8d parity rule
+    rel_t = np.where(both_tiny, 0.0, np.abs(ta - tb) / np.maximum(np.abs(tb), 1e-300))
+    order = lambda t: sorted(range(len(t)), key=lambda i: (-t[i], i))  # episode.cpp:410-414
+    oa, ob = order(ta), order(tb)
+    err = float(np.max(np.abs(es_a - es_b))) if len(es_a) else 0.0
+    srt = np.sort(es_b)[::-1]
+    return {"views": int(len(nm_a)),
+            "n_missing_equal": bool(np.array_equal(nm_a, nm_b)),
+            "entropy_max_rel": float(np.max(np.abs(es_a - es_b) / np.abs(es_b))) if len(es_b) else 0.0,
+            "entropy_max_abs_nats": err,
+            "i_total_max_rel": float(np.max(rel_t)) if len(rel_t) else 0.0,
+            "argmax_equal": bool(oa[0] == ob[0]), "argmax": int(ob[0]),
+            "order_equal": bool(oa == ob),
+            "pool_exhausted": {"ours": not any_a, "reference": not any_b},
+            "n_missing_min_max": [float(nm_b.min()), float(nm_b.max())],
+            "top2_entropy_gap_nats": float(srt[0] - srt[1]) if len(srt) > 1 else None,
+            "top2_i_total": [float(tb[ob[0]]), float(tb[ob[1]])] if len(tb) > 1 else None}
 
 
 def run_reference_arm(args) -> None:
@@ -140,21 +197,42 @@ def run_reference_arm(args) -> None:
     if rank != 0:
         return  # rank 0 alone runs the CPU reference
     import oracle
-    cores = oracle.cpu_count()
-    # one 0.7 GB RenderOutput per concurrent view in the reference: bound by RAM
-    threads = max(1, min(cores, int(_mem_available_gb() // 1.5), 64))
-    views = threads  # one view per thread per step: a bounded sample of the workload
-    value, sec = cpu_reference_run(args.config, views, threads, args.steps, args.warmup)
+    from paper_2506_00225_b200 import scenes  # scene / candidate geometry only: no product library
+    threads = reference_threads()
+    cfg = args.config
+    gm = scenes.make_map(cfg)
+    cam = scenes.CONFIGS[cfg].camera()
+    # the first `threads` candidate views of the list the GPU arm scores (one per thread)
+    cands = scenes.make_candidates(cfg, VIEWS_PER_GPU * args.gpus)[:threads]
+    ref = oracle.RefLib()
+    h = ref.map_create(gm)
+    value, sec, nm, es = cpu_reference_run(gm, cam, cands, threads, args.steps, args.warmup,
+                                           ref=ref, handle=h)
+    one = reference_one_thread(gm, cam, cands[0], ref, h)
+    dec = scenes.make_decision_candidates(cfg)
+    dpos = np.array([c.position for c in dec])
+    _, _, dnm, des = cpu_reference_run(gm, cam, dec, threads, 1, 0, ref=ref, handle=h)
+    _, _, _, dt = ref.combine_scores(dnm, des, dpos, CURRENT_POSITION)
+    ref.map_destroy(h)
+    assert_reference_alone()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args.config),
+        "vs_baseline": None, "dtype": "f64", "data": DATA % cfg,
+        "config": workload_config(cfg, args.gpus),
+        "views_per_step": len(cands),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{views} cfg{args.config} candidate views per step "
-                                   f"(one per thread), {_cpu_model()}"},
+                         "sample": f"candidate views 0..{len(cands) - 1} of the GPU arm's list, "
+                                   f"one per thread, {_cpu_model()}",
+                         "one_thread": one},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "product_library_mapped": False,
+        "scores": {"ids": [c.id for c in cands], "n_missing": nm.tolist(),
+                   "entropy_sum": es.tolist()},
+        "decision": {"set": "make_decision_candidates(%d): 16 views seeing the cloud in part" % cfg,
+                     "n_missing": dnm.tolist(), "entropy_sum": des.tolist(),
+                     "argmax": int(min(range(len(dt)), key=lambda i: (-dt[i], i)))},
     }
     print(json.dumps(line), flush=True)
 
@@ -260,17 +338,20 @@ def measure_mapping(ctx, args) -> dict:
     return out
 
 
-def workload_config(cfg: int) -> dict:
+def workload_config(cfg: int, n_gpus: int) -> dict:
+    """The workload both arms report (identical dicts, so the driver's same_config holds)."""
     from paper_2506_00225_b200 import scenes
     sc = scenes.CONFIGS[cfg]
-    return {"workload": f"cfg{cfg} {sc.name}: {sc.n} Gaussians in {sc.box[0]:g}x{sc.box[1]:g}x"
-                        f"{sc.box[2]:g} m, {sc.width}x{sc.height} px, k={sc.k} of "
-                        f"{sc.num_classes} classes ({sc.num_classes + 1} channels), "
-                        f"{VIEWS_PER_GPU} candidate views per GPU per step",
-            "seed": sc.seed, "views_per_gpu_per_step": VIEWS_PER_GPU,
+    return {"workload": f"cfg{cfg} {sc.name}: {sc.n} Gaussians, {sc.width}x{sc.height} px, "
+                        f"k={sc.k} of {sc.num_classes} classes, candidate views",
+            "seed": sc.seed, "box_m": list(sc.box),
+            "candidates": f"make_candidates({cfg}): {VIEWS_PER_GPU} views per GPU per step on the "
+                          f"GPU arm; the reference arm times the first views of the same list",
             "l2": "flushed (256 MiB write) between timed steps",
             "isotropic": "log_radius = mean of 3 per-axis log-scale draws (SURVEY App. A)",
-            "gain": "reference Eq.6-8 (n_missing, clipped-entropy sum, combine_scores)"}
+            "gain": "reference Eq.6-8 (n_missing, clipped-entropy sum, combine_scores)",
+            "parallelism": f"dp{n_gpus}: candidate views sharded over ranks (GPU arm) or host "
+                           f"threads (reference arm); map replicated"}
 
 
 def measure_aniso(ctx, stream, flush, args, cfg, cam, poses) -> dict:
@@ -397,7 +478,7 @@ def main() -> None:
     # all ranks agree on the argmax (combine_scores on the gathered records)
     for c, a, b in zip(cands, nm_all, es_all):
         c.n_missing, c.entropy_sum = float(a), float(b)
-    combine_scores(cands, np.array([4.0, 1.5, 3.0]))
+    combine_scores(cands, CURRENT_POSITION)
     best = max(range(n_total), key=lambda i: (cands[i].i_total, -i))
 
     # ---- cfg1 with the Fisher-information gain: prior from 32 past poses,
@@ -432,7 +513,19 @@ def main() -> None:
             ev1.record(stream)
             ev1.synchronize()
             f_ms.append(ev0.elapsed_time(ev1))
+        # the combined scalar gain (fisher + entropy) and the ranking that uses it (a14)
+        from paper_2506_00225_b200.splatmap import CandidatePose, combine_scores_fisher
+        _, esf, _ = score_poses_fisher(gm, cam, poses, ctx=ctx)
+        fc = [CandidatePose(position=c.position, direction=c.direction, entropy_sum=float(esf[i]),
+                            fisher_gain=float(gains[i]), id=c.id) for i, c in enumerate(mine)]
+        combine_scores_fisher(fc, CURRENT_POSITION, w_sem=1.0)
+        ranked = sorted(fc, key=lambda c: (-c.i_gain, c.id))
         fisher = {"views_per_s": len(poses) * args.steps / (float(np.sum(f_ms)) / 1e3),
+                  "argmax_view_combined_gain": int(ranked[0].id),
+                  "top2_i_gain": [ranked[0].i_gain, ranked[1].i_gain] if len(ranked) > 1 else None,
+                  "combined_gain": "gain = fisher_gain + 1.0 * entropy_sum; i_gain = (1 - "
+                                   "softmax(|pos - current|)) * softmax(ln gain); rank i_gain desc, "
+                                   "id asc (sgm_combine_scores_fisher)",
                   "ms_per_step": float(np.mean(f_ms)), "prior_poses": len(prior_poses),
                   "prior_ms": prior_ms, "lambda": 1.0,
                   "gain": "sum_{i,theta} H_view / (H_prior + lambda), theta = mu xyz, log_r, "
@@ -512,42 +605,91 @@ def main() -> None:
     smem_peak = 148 * 128 * clock_ghz  # GB/s, LDS/STS crossbar
     K_per_launch = st["contributors"] / raster_launches
     smem_bytes = K_per_launch * 2 * k * 8  # fp64 read+write per sparse scatter
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+    # ncu counters of one raster launch (profiles/, newest round): the pipes that bound it
+    ncu, ncu_src = {}, None
+    for cand in sorted(ROOT.glob("profiles/r*_raster_summary.json"), reverse=True):
+        try:
+            ncu, ncu_src = json.loads(cand.read_text()), str(cand.relative_to(ROOT))
+            break
+        except ValueError:
+            continue
+    K_view = st["contributors"] / max(1, views_timed)
+    # the fp64 accumulator floor: one 8-byte read + one 8-byte write of shared memory per
+    # (pixel, class) update, k updates per contributor, at the crossbar rate
+    floor_ms_view = 16.0 * k * K_view / (smem_peak * 1e9) * 1e3
+    roofline = {"bound": "lsu", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": traffic,
                 "kernel": "k_raster<score> (K5)", "raster_ms_per_launch": raster_ms,
                 "views_per_launch": per_launch_views,
                 "algorithmic_bytes_per_view": "20*N + 6*k*V + 16 (SURVEY 8d)",
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}
-    ncu = {}
-    prof_sum = ROOT / "profiles" / "r01_raster_summary.json"
-    if prof_sum.exists():
-        try:
-            ncu = json.loads(prof_sum.read_text())
-        except ValueError:
-            ncu = {}
-    roofline_aux = {"ncu_lsu_shared_pipe_frac": (ncu.get("smem_pipe_pct") or 0.0) / 100.0 or None,
-                    "ncu_lsu_data_pipe_frac": (ncu.get("lsu_data_pipe_pct") or 0.0) / 100.0 or None,
-                    "ncu_issue_active_frac": (ncu.get("issue_active_pct") or 0.0) / 100.0 or None,
-                    "ncu_source": "profiles/r01_raster_summary.json (ncu --set full, one raster "
-                                  "launch of 8 cfg1 views): the pipes that bound this kernel",
-                    "smem_rmw_GBps": smem_bytes / (raster_ms * 1e-3) / 1e9,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
+                "binding_pipe": "LSU data pipe: shared-memory wavefronts of the fp64 semantic "
+                                "accumulator, the staged weights and rows (not HBM: achieved/peak "
+                                "above is the HBM fraction the contract asks for)",
+                "lsu_data_pipe_frac": (ncu.get("lsu_data_pipe_pct") or 0.0) / 100.0 or None,
+                "lsu_shared_pipe_frac": (ncu.get("smem_pipe_pct") or 0.0) / 100.0 or None,
+                "issue_active_frac": (ncu.get("issue_active_pct") or 0.0) / 100.0 or None,
+                "fp64_pipe_frac": (ncu.get("fp64_pipe_pct") or 0.0) / 100.0 or None,
+                "ncu_source": ncu_src,
+                "fp64_accumulator_floor_ms_per_view": floor_ms_view,
+                "fp64_accumulator_floor_views_per_s": 1e3 / floor_ms_view if floor_ms_view else None,
+                "floor_note": "16 B x k x K per view at 148 SMs x 128 B/clk (LDS/STS crossbar) "
+                              "at the sampled SM clock; K = contributors per view"}
+    roofline_aux = {"smem_rmw_GBps": smem_bytes / (raster_ms * 1e-3) / 1e9,
                     "smem_peak_GBps": smem_peak,
-                    "smem_frac": (smem_bytes / (raster_ms * 1e-3) / 1e9) / smem_peak,
-                    "contributors_per_view": st["contributors"] / max(1, views_timed),
+                    "smem_rmw_frac": (smem_bytes / (raster_ms * 1e-3) / 1e9) / smem_peak,
+                    "contributors_per_view": K_view,
                     "visible_per_view": vis_per_view,
                     "pairs_per_view": st["pairs"] / max(1, views_timed),
                     "batch_span_ms_per_raster_launch": st["binning_ms"] / raster_launches}
 
+    # ---- the decision on a candidate set with varying n_missing (every cfg1 headline view
+    #      has n_missing = 0, so its i_total is 0 and combine_scores reports exhaustion) ----
+    dec = scenes.make_decision_candidates(cfg)
+    dec_poses = [c.camera_pose() for c in dec]
+    dnm, des = score_poses(gm, cam, dec_poses, ctx=ctx)
+    for c, a_, b_ in zip(dec, dnm, des):
+        c.n_missing, c.entropy_sum = float(a_), float(b_)
+    combine_scores(dec, CURRENT_POSITION)
+    dec_total = [c.i_total for c in dec]
+
     cpu_baseline = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             import oracle
-            cores = oracle.cpu_count()
-            threads = max(1, min(cores, int(_mem_available_gb() // 1.5), 64))
-            v, sec = cpu_reference_run(cfg, threads, threads, 1, 0)
+            ref = oracle.RefLib()
+            threads = reference_threads()
+            sample = cands[:threads]
+            h = ref.map_create(gm)
+            v, sec, rnm, res = cpu_reference_run(gm, cam, sample, threads, 1, 0, ref=ref, handle=h)
+            one = reference_one_thread(gm, cam, sample[0], ref, h)
+            _, _, rdnm, rdes = cpu_reference_run(gm, cam, dec, threads, 1, 0, ref=ref, handle=h)
+            ref.map_destroy(h)
             cpu_baseline = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
-                            "sample": f"{threads} cfg{cfg} candidate views, one per thread, "
-                                      f"{sec:.1f} s, {_cpu_model()}"}
+                            "sample": f"candidate views 0..{threads - 1} of this run's list, one "
+                                      f"per thread, {sec:.1f} s, {_cpu_model()}",
+                            "one_thread": one}
+            pos = np.array([c.position for c in sample])
+            dpos = np.array([c.position for c in dec])
+            parity = {
+                "reference": "oracle/_ref: the reference's refresh_candidate_scores and "
+                             "combine_scores compiled unmodified, on the same views",
+                "headline_views": dict(compare_scores(nm_all[:threads], es_all[:threads], rnm,
+                                                      res, pos, CURRENT_POSITION, ref),
+                                       note="every cfg1 headline view sees the cloud at every "
+                                            "pixel: n_missing = 0, so i_geo = i_total = 0 and "
+                                            "combine_scores returns false (pool exhausted); "
+                                            "the argmax is the id tie-break"),
+                "decision_views": dict(compare_scores(dnm, des, rdnm, rdes, dpos,
+                                                      CURRENT_POSITION, ref),
+                                       set="make_decision_candidates(%d): 16 views seeing the "
+                                           "cloud in part (n_missing varies)" % cfg)}
+            hv, dv = parity["headline_views"], parity["decision_views"]
+            parity["all_equal"] = bool(hv["n_missing_equal"] and dv["n_missing_equal"] and
+                                       hv["argmax_equal"] and dv["argmax_equal"] and
+                                       max(hv["entropy_max_rel"], dv["entropy_max_rel"]) < 1e-9 and
+                                       max(hv["i_total_max_rel"], dv["i_total_max_rel"]) < 1e-3)
         except Exception as exc:  # reported, not fatal
             cpu_baseline = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                             "sample": f"failed: {exc!r}"}
@@ -557,16 +699,18 @@ def main() -> None:
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE cfg%d)" % cfg,
-            "config": dict(workload_config(cfg),
-                           parallelism=f"dp{world}: candidate views sharded over the ranks, map "
-                                       f"replicated (NCCL broadcast), per-view scores all-gathered"),
+            "vs_baseline": None, "dtype": "f64", "data": DATA % cfg,
+            "config": workload_config(cfg, world),
+            "views_per_step": n_total,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": int(st["kernel_launches"]),
             "roofline": roofline, "roofline_aux": roofline_aux,
             "cpu_baseline": cpu_baseline, "clocks": clk,
-            "argmax_view": int(best), "views_total_per_step": n_total,
+            "parity": parity,
+            "headline_n_missing_all_zero": bool(np.all(np.asarray(nm_all) == 0)),
+            "argmax_view": int(best),
+            "decision_argmax_view": int(max(range(len(dec)), key=lambda i: (dec_total[i], -i))),
             "with_fisher_gain": fisher,
             "render_ms_per_frame": render_info,
             "mapping_optimize": mapping_info,

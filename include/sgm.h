@@ -148,6 +148,15 @@ int sgm_render_device(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam,
                       const sgm_pose* pose, uint32_t channels, const sgm_options* opt,
                       double* d_color, double* d_depth, double* d_silhouette, double* d_sem,
                       uint64_t* n_projections);
+/* ---- render_reference (splat_render.hpp:82-86, splat_render.cpp:330-358) ----
+ * The reference's plain per-pixel compositor: default RenderOptions with early_exit = false,
+ * and composite_pixel's footprint form f = min(alpha exp(-d2 / (2 r^2)), kMaxFootprint)
+ * with f <= 0 skipped (:86-92; no contributor entry, T unchanged). Outputs as sgm_render;
+ * contributor lists (SGM_RETAIN_CONTRIBUTORS) then exclude alpha == 0 splats, as the
+ * reference's do. */
+int sgm_render_reference(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam,
+                         const sgm_pose* pose, uint32_t channels, double* color, double* depth,
+                         double* silhouette, double* sem, uint64_t* n_projections);
 /* RenderOutput.projections of the last sgm_render* call (depth-sorted, culled). */
 int sgm_last_projections(sgm_ctx* ctx, sgm_projection* out, uint64_t capacity);
 /* The tile bins of the last sgm_render* call at RenderOptions::tile_size
@@ -288,6 +297,15 @@ int sgm_eval_report(sgm_ctx* ctx, sgm_evaluator* ev, double summary[7], double* 
 int sgm_combine_scores(uint64_t n, const double* n_missing, const double* entropy_sum,
                        const double* positions3, const double current[3], double* i_geo,
                        double* i_sem, double* i_total);
+/* The Fisher extension's combined scalar gain and its ranking criterion (the
+ * slot of combine_scores, explorer.cpp:225-248, followed by the sort at episode.cpp:410-414):
+ *   gain_v   = fisher_gain_v + w_sem * entropy_sum_v    (FisherRF gain + semantic entropy)
+ *   i_total_v = (n == 1 ? 1 : 1 - softmax(|pos_v - current|)_v) * softmax(ln gain_v)_v
+ * Rank by i_total descending, id ascending. Returns 1 if any i_total > 0, 0 if none or n == 0,
+ * negative on invalid arguments (null pointers, w_sem < 0 or not finite). */
+int sgm_combine_scores_fisher(uint64_t n, const double* fisher_gain, const double* entropy_sum,
+                              const double* positions3, const double current[3], double w_sem,
+                              double* gain, double* i_total);
 /* look_at(p, p + d) (geometry.hpp:44-56) with Eigen's evaluation order. */
 void sgm_candidate_pose(const double position[3], const double direction[3], sgm_pose* out);
 void sgm_look_at(const double position[3], const double target[3], sgm_pose* out);

@@ -25,16 +25,19 @@ from .splatmap import (  # noqa: F401
     bins_of_last_render,
     clipped_entropy,
     combine_scores,
+    combine_scores_fisher,
     deg_to_rad,
     fisher_prior,
     fisher_set_prior,
     look_at,
     prune_pool,
     refresh_candidate_scores,
+    refresh_candidate_scores_fisher,
     render,
     render_entropy,
     render_reference,
     score_candidates,
+    score_candidates_fisher,
     score_poses,
     score_poses_fisher,
     sigmoid,

@@ -3,6 +3,10 @@
 The library is the only compute path: there is no CPU fallback. If the shared
 object is missing this module raises ImportError on import, and creating a
 context without a CUDA device raises RuntimeError.
+
+The library is mapped on the first use of `lib` (any compute or host-math call), not
+at import: code that only builds scenes or candidate geometry (e.g. bench.py's
+reference arm, which must run the reference alone) never maps it.
 """
 from __future__ import annotations
 
@@ -20,8 +24,10 @@ if not LIB_PATH.exists():
         "paper_2506_00225_b200/csrc). There is no CPU fallback."
     )
 
-lib = C.CDLL(str(LIB_PATH))
+_lib = None
+_lib_lock = __import__("threading").Lock()
 
+SGM_ABI_VERSION = 1
 SGM_OK = 0
 SGM_ERR_INVALID = 1
 SGM_ERR_CUDA = 2
@@ -135,6 +141,8 @@ SIGNATURES = {
     "sgm_map_set_anisotropic": (C.c_int, [_vp, _vp, _pd, _pd]),
     "sgm_render": (C.c_int, [_vp, _vp, C.POINTER(sgm_camera), C.POINTER(sgm_pose), C.c_uint32,
                              C.POINTER(sgm_options), _pd, _pd, _pd, _pd, _pu64]),
+    "sgm_render_reference": (C.c_int, [_vp, _vp, C.POINTER(sgm_camera), C.POINTER(sgm_pose),
+                                       C.c_uint32, _pd, _pd, _pd, _pd, _pu64]),
     "sgm_render_device": (C.c_int, [_vp, _vp, C.POINTER(sgm_camera), C.POINTER(sgm_pose),
                                     C.c_uint32, C.POINTER(sgm_options), _vp, _vp, _vp, _vp,
                                     _pu64]),
@@ -158,18 +166,38 @@ SIGNATURES = {
     "sgm_backward": (C.c_int, [_vp, _vp, C.POINTER(sgm_camera), C.POINTER(sgm_pose),
                                C.POINTER(sgm_options), _pf, _pf, _pf, _pd, C.c_int, C.c_int, _pd,
                                _pd, _pd, _pd, _pd, _pd]),
+    "sgm_combine_scores_fisher": (C.c_int, [C.c_uint64, _pd, _pd, _pd, _pd, C.c_double, _pd, _pd]),
     "sgm_combine_scores": (C.c_int, [C.c_uint64, _pd, _pd, _pd, _pd, _pd, _pd, _pd]),
     "sgm_candidate_pose": (None, [_pd, _pd, C.POINTER(sgm_pose)]),
     "sgm_look_at": (None, [_pd, _pd, C.POINTER(sgm_pose)]),
 }
 
-for _name, (_res, _args) in SIGNATURES.items():
-    _fn = getattr(lib, _name)
-    _fn.restype = _res
-    _fn.argtypes = _args
 
-if lib.sgm_abi_version() != 1:
-    raise ImportError(f"{LIB_PATH}: unexpected ABI version {lib.sgm_abi_version()}")
+
+def _load():
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            h = C.CDLL(str(LIB_PATH))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(h, name)
+                fn.restype = res
+                fn.argtypes = args
+            if h.sgm_abi_version() != SGM_ABI_VERSION:
+                raise ImportError(f"{LIB_PATH}: unexpected ABI version {h.sgm_abi_version()}")
+            _lib = h
+    return _lib
+
+
+def __getattr__(name):  # module attribute `lib`: the library, mapped on first use
+    if name == "lib":
+        return _load()
+    raise AttributeError(name)
+
+
+def loaded() -> bool:
+    """Whether this process has mapped libsgm_b200.so."""
+    return _lib is not None
 
 
 class SgmError(RuntimeError):
@@ -182,7 +210,7 @@ class SgmError(RuntimeError):
 
 def check(code: int, ctx=None) -> None:
     if code != SGM_OK:
-        msg = lib.sgm_last_error(ctx)
+        msg = _load().sgm_last_error(ctx)
         raise SgmError(code, msg.decode() if msg else "")
 
 

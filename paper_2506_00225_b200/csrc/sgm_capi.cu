@@ -335,9 +335,11 @@ int sgm_render_device(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* cam, c
 }
 
 
-int sgm_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const sgm_pose* pose,
-               uint32_t channels, const sgm_options* opt, double* color, double* depth,
-               double* silhouette, double* sem, uint64_t* n_projections) {
+// render() / render_reference() into caller-owned host planes (reference layout)
+static int render_to_host(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera,
+                          const sgm_pose* pose, uint32_t channels, const sgm_options* opt,
+                          double* color, double* depth, double* silhouette, double* sem,
+                          uint64_t* n_projections, bool reference_form) {
     return guard(ctx, [&] {
         need_ctx(ctx);
         if (!map) fail(SGM_ERR_INVALID, "map is null");
@@ -357,7 +359,8 @@ int sgm_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const
         double* d_sem = want_s ? base + px * (1 + (want_c ? 3 : 0) + (want_d ? 1 : 0)) : nullptr;
         uint32_t ch = (want_c ? SGM_COLOR : 0u) | (want_d ? SGM_DEPTH : 0u) |
                       (want_s ? SGM_SEMANTICS : 0u) | (channels & SGM_RETAIN_CONTRIBUTORS);
-        do_render(ctx, map, camera, pose, ch, opt, d_color, d_depth, d_sil, d_sem, n_projections);
+        do_render(ctx, map, camera, pose, ch, opt, d_color, d_depth, d_sil, d_sem, n_projections,
+                  reference_form);
         std::vector<CopyOut> segs{{silhouette, d_sil, 8 * px}};
         if (want_c) segs.push_back({color, d_color, 24 * px});
         if (want_d) segs.push_back({depth, d_depth, 8 * px});
@@ -367,6 +370,23 @@ int sgm_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const
         if ((channels & SGM_COLOR) == 0 && color) std::memset(color, 0, 24 * px);
         if ((channels & SGM_DEPTH) == 0 && depth) std::memset(depth, 0, 8 * px);
     });
+}
+
+int sgm_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const sgm_pose* pose,
+               uint32_t channels, const sgm_options* opt, double* color, double* depth,
+               double* silhouette, double* sem, uint64_t* n_projections) {
+    return render_to_host(ctx, map, camera, pose, channels, opt, color, depth, silhouette, sem,
+                          n_projections, false);
+}
+
+// render_reference (splat_render.cpp:330-358): default RenderOptions with early_exit = false,
+// every projection composited in depth order with composite_pixel's footprint (:86-92).
+int sgm_render_reference(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera,
+                         const sgm_pose* pose, uint32_t channels, double* color, double* depth,
+                         double* silhouette, double* sem, uint64_t* n_projections) {
+    const sgm_options o{0, 1e-4, 0.01, 3.0, 8};  // RenderOptions{} with early_exit = false (:333-334)
+    return render_to_host(ctx, map, camera, pose, channels, &o, color, depth, silhouette, sem,
+                          n_projections, true);
 }
 
 int sgm_last_projections(sgm_ctx* ctx, sgm_projection* out, uint64_t capacity) {

@@ -228,7 +228,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
 // One render into device planes (retain_contributors: two raster passes).
 void do_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const sgm_pose* pose,
                uint32_t channels, const sgm_options* opt, double* d_color, double* d_depth,
-               double* d_sil, double* d_sem, uint64_t* n_proj);
+               double* d_sil, double* d_sem, uint64_t* n_proj, bool reference_form = false);
 // The mapping step on device-resident frame planes (see sgm_pipeline.cu).
 void backward_core(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const OptParams& o,
                    const PoseParams& p, const float* f_rgb, const float* f_depth,

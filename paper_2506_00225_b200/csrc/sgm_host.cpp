@@ -95,6 +95,38 @@ int sgm_combine_scores(uint64_t n, const double* n_missing, const double* entrop
     return any;
 }
 
+// The combined scalar gain of the Fisher extension (no reference counterpart):
+//   gain_v   = fisher_gain_v + w_sem * entropy_sum_v
+//   i_gain_v = softmax(ln gain_v)                      (as Eq. 6 treats the missing count)
+//   i_total  = (n == 1 ? 1 : 1 - softmax(dist)_v) * i_gain_v          (Eq. 8's motion cost)
+// with the reference's stable_softmax and distance (explorer.cpp:209-248). gain_v <= 0 (or
+// not finite) takes no share. Returns 1 if some i_total > 0, 0 if none (or n == 0), -1 on
+// invalid arguments.
+int sgm_combine_scores_fisher(uint64_t n, const double* fisher_gain, const double* entropy_sum,
+                              const double* positions3, const double current[3], double w_sem,
+                              double* gain, double* i_total) {
+    if (n == 0) return 0;
+    if (!fisher_gain || !entropy_sum || !positions3 || !current || !gain || !i_total) return -1;
+    if (!std::isfinite(w_sem) || w_sem < 0.0) return -1;
+    std::vector<double> log_gain(n), dist(n);
+    for (uint64_t i = 0; i < n; ++i) {
+        gain[i] = fisher_gain[i] + w_sem * entropy_sum[i];
+        log_gain[i] = gain[i] > 0.0 ? std::log(gain[i]) : -std::numeric_limits<double>::infinity();
+        const double d[3] = {positions3[3 * i] - current[0], positions3[3 * i + 1] - current[1],
+                             positions3[3 * i + 2] - current[2]};
+        dist[i] = std::sqrt(sqnorm3(d));
+    }
+    const std::vector<double> share = stable_softmax(log_gain);
+    const std::vector<double> dist_soft = stable_softmax(dist);
+    int any = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const double dist_factor = n == 1 ? 1.0 : 1.0 - dist_soft[i];
+        i_total[i] = dist_factor * share[i];
+        if (i_total[i] > 0.0) any = 1;
+    }
+    return any;
+}
+
 // look_at, proj/include/splatmap/geometry.hpp:44-56 (up = +Y).
 void sgm_look_at(const double position[3], const double target[3], sgm_pose* out) {
     static const double up[3] = {0.0, 1.0, 0.0};

@@ -60,6 +60,10 @@ struct OptParams {
     double cut_sq;  // trunc * trunc (splat_render.cpp:180)
     int ts;         // reference tile_size (binning)
     int tiles_x, tiles_y;
+    // render_reference's footprint form (splat_render.cpp:91-92): exp(-d2 / (2 r^2)) with the
+    // division, and f <= 0 skipped (not a contributor). k_pack then stores 2 r^2 in the
+    // inv_two_r2 slot. Render launches only.
+    int ref_div = 0;
 };
 
 // One culled-in projection in depth-rank order: the reference's PackedSplat

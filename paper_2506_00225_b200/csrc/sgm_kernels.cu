@@ -310,7 +310,8 @@ __global__ void k_pack(DevMap m, const PoseParams* __restrict__ pose, CamParams 
         PackedSplat ps;
         ps.mx = q.mx;
         ps.my = q.my;
-        ps.inv_two_r2 = 1.0 / (2.0 * rad * rad);  // :194
+        // :194; render_reference keeps the divisor 2 r^2 itself (:91)
+        ps.inv_two_r2 = o.ref_div ? 2.0 * rad * rad : 1.0 / (2.0 * rad * rad);
         ps.cutoff_d2 = o.cut_sq * rad * rad;      // :195
         ps.alpha = m.alpha[i];
         ps.z = q.z;

@@ -382,12 +382,13 @@ void need_ctx(sgm_ctx* ctx) {
 
 void do_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const sgm_pose* pose,
                uint32_t channels, const sgm_options* opt, double* d_color, double* d_depth,
-               double* d_sil, double* d_sem, uint64_t* n_proj) {
+               double* d_sil, double* d_sem, uint64_t* n_proj, bool reference_form) {
     need_ctx(ctx);
     if (!map) fail(SGM_ERR_INVALID, "map is null");
     if (!pose) fail(SGM_ERR_INVALID, "pose is null");
     const CamParams cam = to_cam(camera);
-    const OptParams o = to_opt(opt, cam);
+    OptParams o = to_opt(opt, cam);
+    o.ref_div = reference_form ? 1 : 0;
     const PoseParams p = to_pose(*pose);
     RenderTargets rt;
     rt.channels = channels;

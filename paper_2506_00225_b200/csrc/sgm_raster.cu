@@ -333,8 +333,15 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                         const double dy = dpy - sp[e].my;
                         const double d2 = dx * dx + dy * dy;
                         if (!(d2 > sp[e].cutoff_d2)) {  // :283
-                            f = sp[e].alpha * exp_footprint(-d2 * sp[e].inv_two_r2);  // :284
-                            if (f > kMaxFootprint) f = kMaxFootprint;                 // :285
+                            if (kRender && p.opt.ref_div) {
+                                // render_reference (:90-92): exp(-d2 / (2 r^2)), f <= 0 skipped
+                                f = sp[e].alpha * exp_footprint(-d2 / sp[e].inv_two_r2);
+                                if (f > kMaxFootprint) f = kMaxFootprint;
+                                if (!(f > 0.0)) f = -1.0;
+                            } else {
+                                f = sp[e].alpha * exp_footprint(-d2 * sp[e].inv_two_r2);  // :284
+                                if (f > kMaxFootprint) f = kMaxFootprint;                 // :285
+                            }
                         }
                     }
                 }

@@ -165,6 +165,33 @@ def make_candidates(cfg: int, count: int | None = None, stream: int = 1) -> List
     return out
 
 
+def make_decision_candidates(cfg: int, count: int = 16) -> List[CandidatePose]:
+    """A candidate set whose views see the cloud only in part, so n_missing varies from view
+    to view and combine_scores (explorer.cpp:225-248) has a non-trivial argmax. (Every view of
+    make_candidates(1..3) lies inside the cloud and sees it everywhere: n_missing = 0, so
+    i_geo = i_total = 0 and the reference reports the pool exhausted.)
+
+    Positions lie outside the box, 0.6-1.6 box half-diagonals from its centre in the
+    horizontal plane, at heights inside the box; each looks at the centre displaced by up to
+    half the box extent, so part of every image is empty. Seeded (stream 3)."""
+    sc = CONFIGS[cfg]
+    rng = np.random.Generator(np.random.PCG64([sc.seed, 3]))
+    W, D, H = sc.box
+    ox, oy, oz = sc.box_origin
+    c = np.array([ox + W / 2, oy + H / 2, oz + D / 2])
+    half = 0.5 * math.hypot(W, D)
+    out: List[CandidatePose] = []
+    for i in range(count):
+        phi = rng.uniform(0.0, 2.0 * math.pi)
+        r = half * rng.uniform(0.6, 1.6)
+        p = np.array([c[0] + r * math.cos(phi), oy + rng.uniform(0.2, 0.8) * H,
+                      c[2] + r * math.sin(phi)])
+        tgt = c + np.array([rng.uniform(-0.5, 0.5) * W, rng.uniform(-0.3, 0.3) * H,
+                            rng.uniform(-0.5, 0.5) * D])
+        out.append(CandidatePose(position=p, direction=tgt - p, id=i))
+    return out
+
+
 def render_poses(cfg: int, count: int | None = None):
     """Explicit render poses (cfg0: the 8 circle poses, look_at(p, centre))."""
     sc = CONFIGS[cfg]

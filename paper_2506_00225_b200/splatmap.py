@@ -524,6 +524,10 @@ def render(gmap: GaussianMap, camera: CameraModel, pose: Pose,
            channels: Optional[RenderChannels] = None, options: Optional[RenderOptions] = None,
            ctx: Optional[Context] = None) -> RenderOutput:
     """Tiled front-to-back compositor (splat_render.hpp:78-80) on the GPU."""
+    return _render(gmap, camera, pose, channels, options, ctx, reference_form=False)
+
+
+def _render(gmap, camera, pose, channels, options, ctx, reference_form: bool) -> RenderOutput:
     ch = channels if channels is not None else RenderChannels()
     opt = options if options is not None else RenderOptions()
     c = _ctx(ctx)
@@ -538,10 +542,14 @@ def render(gmap: GaussianMap, camera: CameraModel, pose: Pose,
     out.sem = np.empty(px * Cn) if ch.semantics else np.zeros(0)
     nproj = C.c_uint64()
     cam_c, pose_c, opt_c = camera._c(), pose._c(), opt._c()
-    c.check(N.lib.sgm_render(c.handle, handle, C.byref(cam_c), C.byref(pose_c), ch.flags(),
-                             C.byref(opt_c), N.dptr(out.color) if ch.color else None,
-                             N.dptr(out.depth) if ch.depth else None, N.dptr(out.silhouette),
-                             N.dptr(out.sem) if ch.semantics else None, C.byref(nproj)))
+    planes = (N.dptr(out.color) if ch.color else None, N.dptr(out.depth) if ch.depth else None,
+              N.dptr(out.silhouette), N.dptr(out.sem) if ch.semantics else None, C.byref(nproj))
+    if reference_form:
+        c.check(N.lib.sgm_render_reference(c.handle, handle, C.byref(cam_c), C.byref(pose_c),
+                                           ch.flags(), *planes))
+    else:
+        c.check(N.lib.sgm_render(c.handle, handle, C.byref(cam_c), C.byref(pose_c), ch.flags(),
+                                 C.byref(opt_c), *planes))
     proj = np.zeros(nproj.value, dtype=PROJECTION_DTYPE)
     if nproj.value:
         c.check(N.lib.sgm_last_projections(
@@ -597,12 +605,14 @@ def bins_of_last_render(tiles: int, ctx: Optional[Context] = None):
 def render_reference(gmap: GaussianMap, camera: CameraModel, pose: Pose,
                      channels: Optional[RenderChannels] = None,
                      ctx: Optional[Context] = None) -> RenderOutput:
-    """splat_render.hpp:82-86. The reference's untiled oracle composites every
-    projection with no early exit; on the GPU that is the tiled compositor with
-    early_exit=False (each pixel's depth-ordered contributor set is identical).
-    It differs from the reference's render_reference only in evaluating the
-    footprint as exp(-d2 * inv_two_r2) instead of exp(-d2 / (2 r^2)) (~1 ulp)."""
-    return render(gmap, camera, pose, channels, RenderOptions(early_exit=False), ctx)
+    """splat_render.hpp:82-86 / splat_render.cpp:330-358: every projection composited in depth
+    order with no early exit, with composite_pixel's footprint form (:86-92):
+    f = min(alpha exp(-d2 / (2 r^2)), kMaxFootprint), f <= 0 skipped (so alpha == 0 splats
+    are not listed as contributors). On the GPU: the tiled compositor with that footprint
+    (sgm_render_reference); each pixel's depth-ordered candidate set is the same, since the
+    tile rectangles and the float probe (:276-278) only drop splats the exact test rejects."""
+    return _render(gmap, camera, pose, channels, RenderOptions(early_exit=False), ctx,
+                   reference_form=True)
 
 
 def clipped_entropy(probs) -> float:
@@ -646,6 +656,11 @@ class CandidatePose:
     i_sem: float = 0.0
     i_total: float = 0.0
     id: int = -1
+    # Fisher extension (not in the reference): the view's FisherRF gain, the
+    # combined scalar gain (fisher_gain + w_sem * entropy_sum) and its ranking criterion
+    fisher_gain: float = 0.0
+    gain: float = 0.0
+    i_gain: float = 0.0
 
     State = CandidateState
 
@@ -859,6 +874,55 @@ def combine_scores(candidates: List[CandidatePose], current_position) -> bool:
     for i, cd in enumerate(candidates):
         cd.i_geo, cd.i_sem, cd.i_total = float(geo[i]), float(sem[i]), float(tot[i])
     return rc == 1
+
+
+def refresh_candidate_scores_fisher(candidates: List[CandidatePose], gmap: GaussianMap,
+                                    scoring_camera: CameraModel,
+                                    ctx: Optional[Context] = None) -> None:
+    """refresh_candidate_scores plus the Fisher extension: caches n_missing, entropy_sum and
+    fisher_gain (against the map's fisher_prior) on every Active candidate, in one batched
+    GPU call (sgm_score_views_fisher)."""
+    active = [cd for cd in candidates if cd.state == CandidateState.Active]
+    if not active:
+        return
+    nm, es, fg = score_poses_fisher(gmap, scoring_camera, [cd.camera_pose() for cd in active],
+                                    ctx=ctx)
+    for i, cd in enumerate(active):
+        cd.n_missing, cd.entropy_sum, cd.fisher_gain = float(nm[i]), float(es[i]), float(fg[i])
+
+
+def combine_scores_fisher(candidates: List[CandidatePose], current_position,
+                          w_sem: float = 1.0) -> bool:
+    """The Fisher extension's scalar gain and ranking criterion (sgm_combine_scores_fisher):
+    gain = fisher_gain + w_sem * entropy_sum; i_gain = (1 - softmax(distance)) *
+    softmax(ln gain), the slot of combine_scores (explorer.cpp:225-248). Returns whether any
+    i_gain > 0."""
+    n = len(candidates)
+    if n == 0:
+        return False
+    fg = np.array([cd.fisher_gain for cd in candidates], dtype=np.float64)
+    es = np.array([cd.entropy_sum for cd in candidates], dtype=np.float64)
+    pos = np.ascontiguousarray([np.asarray(cd.position, dtype=np.float64) for cd in candidates])
+    cur = np.ascontiguousarray(current_position, dtype=np.float64)
+    gain, tot = np.zeros(n), np.zeros(n)
+    rc = N.lib.sgm_combine_scores_fisher(n, N.dptr(fg), N.dptr(es), N.dptr(pos), N.dptr(cur),
+                                         float(w_sem), N.dptr(gain), N.dptr(tot))
+    if rc < 0:
+        raise ValueError("combine_scores_fisher: invalid arguments")
+    for i, cd in enumerate(candidates):
+        cd.gain, cd.i_gain = float(gain[i]), float(tot[i])
+    return rc == 1
+
+
+def score_candidates_fisher(candidates: List[CandidatePose], gmap: GaussianMap,
+                            scoring_camera: CameraModel, current_position, w_sem: float = 1.0,
+                            ctx: Optional[Context] = None) -> bool:
+    """score_candidates (explorer.cpp:250-259) with the Fisher extension's gain: refresh,
+    combine_scores_fisher, then sort by i_gain descending, id ascending."""
+    refresh_candidate_scores_fisher(candidates, gmap, scoring_camera, ctx)
+    any_pos = combine_scores_fisher(candidates, current_position, w_sem)
+    candidates.sort(key=lambda cd: (-cd.i_gain, cd.id))
+    return any_pos
 
 
 def score_candidates(candidates: List[CandidatePose], gmap: GaussianMap,

@@ -166,3 +166,40 @@ def test_prune_pool_and_candidate_pool():
     assert all(c.id != 2 for c in pool.active()) and pool.ever_visited(2)
     pool.absorb([sgm.CandidatePose(n_missing=500) for _ in range(3)])
     assert sorted(c.id for c in pool.active()) == [0, 1, 3, 4, 5, 6, 7, 8]
+
+
+def _softmax(v):
+    v = np.asarray(v, dtype=np.float64)
+    fin = np.isfinite(v)
+    out = np.zeros_like(v)
+    if not fin.any():
+        return out
+    e = np.where(fin, np.exp(np.where(fin, v, 0.0) - v[fin].max()), 0.0)
+    return e / e.sum()
+
+
+def test_combine_scores_fisher_matches_its_definition():
+    """The Fisher extension's scalar gain: gain = fisher_gain + w_sem *
+    entropy_sum, i_gain = (1 - softmax(dist)) * softmax(ln gain), ranked i_gain desc, id asc."""
+    rng = np.random.default_rng(5)
+    for n, w in ((1, 1.0), (2, 0.0), (7, 1.0), (40, 0.25)):
+        fg = rng.uniform(0.0, 3e4, n)
+        es = rng.uniform(1e5, 3e5, n)
+        fg[n // 2] = 0.0
+        pos = rng.normal(0, 2, (n, 3))
+        cur = rng.normal(0, 1, 3)
+        cands = [sgm.CandidatePose(position=pos[i], entropy_sum=es[i], fisher_gain=fg[i], id=i)
+                 for i in range(n)]
+        any_ = sgm.combine_scores_fisher(cands, cur, w_sem=w)
+        gain = fg + w * es
+        with np.errstate(divide="ignore"):
+            share = _softmax(np.where(gain > 0, np.log(np.where(gain > 0, gain, 1.0)), -np.inf))
+        dist = np.sqrt(((pos - cur) ** 2).sum(axis=1))
+        tot = (1.0 if n == 1 else 1.0 - _softmax(dist)) * share
+        np.testing.assert_allclose([c.gain for c in cands], gain, rtol=1e-15)
+        np.testing.assert_allclose([c.i_gain for c in cands], tot, rtol=1e-12, atol=1e-300)
+        assert any_ == bool((tot > 0).any())
+    zero = [sgm.CandidatePose(position=np.zeros(3), id=i) for i in range(3)]
+    assert sgm.combine_scores_fisher(zero, [0, 0, 0]) is False  # no gain anywhere: exhausted
+    with pytest.raises(ValueError):
+        sgm.combine_scores_fisher(zero, [0, 0, 0], w_sem=-1.0)

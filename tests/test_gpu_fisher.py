@@ -79,3 +79,30 @@ def test_prior_from_summed_shards_equals_full_prior():
     sgm.fisher_set_prior(gm, H_sum, lam=1.0, ctx=ctx)
     _, _, g_sum = sgm.score_poses_fisher(gm, cam, views, ctx=ctx)
     np.testing.assert_allclose(g_sum, g_all, rtol=1e-12)
+
+
+def test_combined_gain_ranking_vs_oracle(ctx, orc):
+    """The a14 scalar gain (fisher_gain + w_sem * entropy_sum) and its ranking
+    (score_candidates_fisher) from GPU scores vs the same criterion on the oracle's scores:
+    same gains (1e-9) and the same planning order."""
+    gm = scenes.make_map(0, n=3000)
+    cam = scenes.CONFIGS[0].camera()
+    prior = scenes.render_poses(0, 8)[:3]
+    sgm.fisher_prior(gm, cam, prior, lam=1.0, ctx=ctx)
+    H_o = orc.fisher_accumulate(gm, cam, prior)
+    cands = scenes.make_decision_candidates(0, 10)
+    cur = np.array([2.0, 1.5, 2.0])
+    for w in (1.0, 0.01):
+        mine = [sgm.CandidatePose(position=c.position, direction=c.direction, id=c.id) for c in cands]
+        sgm.score_candidates_fisher(mine, gm, cam, cur, w_sem=w, ctx=ctx)
+        poses = [c.camera_pose() for c in cands]
+        nm_o, es_o, _ = orc.score_views(gm, cam, poses)
+        g_o = orc.fisher_gain(gm, cam, poses, H_o, 1.0)
+        theirs = [sgm.CandidatePose(position=c.position, entropy_sum=es_o[i], fisher_gain=g_o[i],
+                                    id=c.id) for i, c in enumerate(cands)]
+        sgm.combine_scores_fisher(theirs, cur, w_sem=w)
+        theirs.sort(key=lambda c: (-c.i_gain, c.id))
+        assert [c.id for c in mine] == [c.id for c in theirs]
+        np.testing.assert_allclose([c.gain for c in mine], [c.gain for c in theirs], rtol=1e-9)
+        np.testing.assert_allclose([c.i_gain for c in mine], [c.i_gain for c in theirs], rtol=1e-6)
+        assert mine[0].i_gain > mine[-1].i_gain > 0.0

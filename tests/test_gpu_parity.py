@@ -94,6 +94,40 @@ def test_retained_contributors_random_vs_reference(ctx, ref):
         np.testing.assert_array_equal(out.contrib, r["contrib"])
 
 
+@pytest.mark.parametrize("name", ["tiled_91", "kM_11", "kM_22", "kM_33", "early_55", "perm_19"])
+def test_render_reference_matches_reference(ctx, ref, golden, name):
+    """render_reference (splat_render.cpp:330-358) against the reference's own: planes within
+    1e-12 (test_splat_render.cpp:143-158 holds the tiled path to that bar), identical
+    projections and contributor lists."""
+    gm, cam, pose, _, _, _ = golden_scene(golden, name)
+    out = sgm.render_reference(gm, cam, pose, RenderChannels.all(True), ctx=ctx)
+    r = ref.render(gm, cam, pose, 15, which=1)
+    for key in ("silhouette", "color", "depth", "sem"):
+        assert np.max(np.abs(getattr(out, key) - r[key]), initial=0.0) < 1e-12, key
+    assert_projections(out, r["projections"])
+    np.testing.assert_array_equal(out.contrib_offset, r["contrib_offset"])
+    np.testing.assert_array_equal(out.contrib, r["contrib"])
+
+
+def test_render_reference_skips_zero_footprints(ctx, ref):
+    """composite_pixel's `f <= 0` skip (:92): alpha == 0 splats are contributors of render()
+    (it has no such test) but not of render_reference()."""
+    cam = CameraModel(61, 47, 0, 0, 52.0, 50.5, 30.2, 23.4)
+    pose = look_at([0.1, 0.0, -0.3], [0.0, 0.1, 2.0])
+    gm = random_map(33, 400, cam, pose, k=3, num_classes=7)
+    gm.opacity_logits[::9] = -1e4  # sigmoid -> exactly 0
+    out = sgm.render_reference(gm, cam, pose, RenderChannels.all(True), ctx=ctx)
+    r = ref.render(gm, cam, pose, 15, which=1)
+    np.testing.assert_array_equal(out.contrib_offset, r["contrib_offset"])
+    np.testing.assert_array_equal(out.contrib, r["contrib"])
+    for key in ("silhouette", "color", "depth", "sem"):
+        assert np.max(np.abs(getattr(out, key) - r[key]), initial=0.0) < 1e-12, key
+    tiled = sgm.render(gm, cam, pose, RenderChannels.all(True), RenderOptions(early_exit=False),
+                       ctx=ctx)
+    assert len(tiled.contrib) > len(out.contrib)  # the alpha == 0 splats listed by render()
+    np.testing.assert_allclose(tiled.silhouette, out.silhouette, rtol=0, atol=1e-12)
+
+
 def test_reference_kats_on_gpu(ctx, golden):
     gm, cam, pose, opts, _, _ = golden_scene(golden, "saturated")
     out = sgm.render(gm, cam, pose, ctx=ctx)
