@@ -593,6 +593,11 @@ void copy_out(sgm_ctx* ctx, const std::vector<CopyOut>& segs) {
     std::atomic<size_t> issued{0};  // pieces whose D2H + event are enqueued
     std::atomic<int> err{0};
     auto worker = [&](unsigned w) {
+        // this thread's runtime calls must target the ctx's device (not device 0)
+        if (cudaSetDevice(ctx->device) != cudaSuccess) {
+            err.store(1);
+            return;
+        }
         for (size_t j = 0; j < np; ++j) {
             while (issued.load(std::memory_order_acquire) <= j && !err.load()) std::this_thread::yield();
             if (err.load()) return;

@@ -103,6 +103,13 @@ class MapTrainer:
 
     def __init__(self, gmap: GaussianMap, adam: Optional[AdamState] = None,
                  ctx: Optional[Context] = None):
+        if gmap.anisotropic():
+            # the trainer optimises the reference's isotropic parameters (mapper.cpp:10-51):
+            # log_radius, which an anisotropic footprint ignores, and no per-axis scales or
+            # rotations, so an anisotropic map cannot be trained (nor re-indexed by pruning)
+            raise ValueError("MapTrainer: anisotropic maps are not trainable (isotropic only); "
+                             "call gmap.set_anisotropic(None, None) first")
+        self.handle = None
         self._ctx = _ctx(ctx)
         self.k, self.num_classes = gmap.k(), gmap.num_classes()
         n = self._n0 = gmap.size()
@@ -205,6 +212,15 @@ def optimize_map(gmap: GaussianMap, adam: AdamState, frames: Sequence[Frame],
     c = _ctx(ctx)
     tr = MapTrainer(gmap, adam, ctx=c)
     dev = [DeviceFrame(f, ctx=c) for f in frames]
-    hist = tr.optimize(dev, camera, cfg, iters)
+    try:
+        hist = tr.optimize(dev, camera, cfg, iters)
+    except Exception:
+        # the reference updates the map and AdamState in place up to the iteration that
+        # throws (mapper.cpp:262-272): hand back the same partial progress, then re-raise
+        try:
+            tr.download(gmap, adam)
+        except Exception:
+            pass
+        raise
     tr.download(gmap, adam)
     return hist

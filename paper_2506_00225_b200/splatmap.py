@@ -190,8 +190,23 @@ _SGMP_MAGIC = 0x53474D50
 _SGMP_VERSION = 1
 
 
+_MAP_ARRAYS = frozenset({"centers", "log_radii", "opacity_logits", "colors", "sem_indices",
+                         "sem_probs", "log_scales", "quats"})
+
+
 class GaussianMap:
-    """Structure-of-arrays splat storage (gaussian_map.hpp:61-114)."""
+    """Structure-of-arrays splat storage (gaussian_map.hpp:61-114).
+
+    A Context caches one device snapshot per map *version* (the reference reads live spans on
+    every call; re-uploading 112 MB per call would dominate scoring). Reassigning an array
+    attribute (`gmap.colors = ...`) bumps the version by itself; after editing an array IN
+    PLACE (`gmap.colors[i] = ...`) call `touch()`, or the next call renders the snapshot
+    taken before the edit."""
+
+    def __setattr__(self, name, value):
+        object.__setattr__(self, name, value)
+        if name in _MAP_ARRAYS and "_version" in self.__dict__:
+            self.__dict__["_version"] += 1
 
     def __init__(self, k: int, num_classes: int):
         if k < 1 or k > num_classes + 1:

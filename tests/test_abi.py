@@ -203,3 +203,22 @@ def test_combine_scores_fisher_matches_its_definition():
     assert sgm.combine_scores_fisher(zero, [0, 0, 0]) is False  # no gain anywhere: exhausted
     with pytest.raises(ValueError):
         sgm.combine_scores_fisher(zero, [0, 0, 0], w_sem=-1.0)
+
+
+def test_trainer_rejects_anisotropic_maps():
+    """optimize_map trains the reference's isotropic parameters only (mapper.cpp:10-51)."""
+    from paper_2506_00225_b200.mapper import MapTrainer
+    gm = sgm.GaussianMap.from_arrays(1, 3, [[0, 0, 1.0]], [-2.0], [0.0], [[0, 0, 0]], [[2]], [[1.0]],
+                                     log_scales=[[-2.0, -2.1, -1.9]], quats=[[1.0, 0, 0, 0]])
+    with pytest.raises(ValueError, match="anisotropic"):
+        MapTrainer(gm)
+
+
+def test_map_version_bumps_on_array_reassignment():
+    gm = sgm.GaussianMap.from_arrays(1, 3, [[0, 0, 1.0]], [-2.0], [0.0], [[0, 0, 0]], [[2]], [[1.0]])
+    v = gm._version
+    gm.colors = np.array([[0.5, 0.5, 0.5]])
+    assert gm._version > v
+    v = gm._version
+    gm.touch()
+    assert gm._version == v + 1

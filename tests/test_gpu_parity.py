@@ -496,3 +496,19 @@ def test_bins_mixed_sparse_and_dense_rows(ctx, orc):
     assert_projections(out, orc.project(gm, cam, pose, opts))
     assert_bins(ctx, orc, gm, cam, pose, opts, out)
     assert_planes(out, orc.render(gm, cam, pose, 7, opts))
+
+
+def test_map_edits_reach_the_device_snapshot(ctx):
+    """The cached device snapshot follows the map: reassigning an array bumps the version by
+    itself; an in-place edit is picked up after touch()."""
+    cam = CameraModel(40, 30, 0, 0, 35.0, 35.0, 20.0, 15.0)
+    gm = random_map(4, 60, cam, k=2, num_classes=4)
+    a = sgm.render(gm, cam, Pose(), ctx=ctx)
+    gm.colors = np.clip(gm.colors, 0.0, 1.0) * 0.5  # reassignment
+    b = sgm.render(gm, cam, Pose(), ctx=ctx)
+    assert not np.array_equal(a.color, b.color)
+    np.testing.assert_allclose(b.color, 0.5 * a.color, rtol=1e-12, atol=1e-15)
+    gm.opacity_logits[:] = -1e4  # in place: every splat transparent once touched
+    gm.touch()
+    c = sgm.render(gm, cam, Pose(), ctx=ctx)
+    assert np.all(c.silhouette == 0.0)
