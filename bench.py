@@ -421,9 +421,6 @@ def main() -> None:
     cfg = args.config
     sc = scenes.CONFIGS[cfg]
     cam = sc.camera()
-    gm = scenes.make_map(cfg) if rank == 0 else None
-    if dist_on:
-        gm = sd.broadcast_map(gm)  # C1 over NCCL
     n_total = VIEWS_PER_GPU * world
     cands = scenes.make_candidates(cfg, n_total)
     s, e = sd.shard_range(n_total, rank, world)
@@ -431,7 +428,14 @@ def main() -> None:
     poses = [c.camera_pose() for c in mine]
 
     ctx = Context(local)
-    ctx.upload(gm)
+    gm_host = scenes.make_map(cfg) if rank == 0 else None  # the host map lives on rank 0
+    if dist_on:
+        # C1: rank 0 uploads once; its device snapshot goes device to device over NCCL;
+        # the other ranks score a DeviceMap
+        gm = sd.broadcast_map(gm_host, ctx)
+    else:
+        gm = gm_host
+        ctx.upload(gm)
     stream = torch.cuda.ExternalStream(ctx.stream)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
@@ -551,19 +555,58 @@ def main() -> None:
         except Exception as exc:  # reported, not fatal
             mapping_info = {"error": repr(exc)}
 
-    # ---- e2e through the public API (host inputs, map re-upload every step) ----
-    h2d = int(gm.centers.nbytes + gm.log_radii.nbytes + gm.opacity_logits.nbytes +
-              gm.colors.nbytes + gm.sem_indices.nbytes + gm.sem_probs.nbytes) + 96 * len(mine)
+    # ---- cfg2: the candidate sweep, the cfg1 map from 1024 lattice poses sharded over the
+    #      ranks (strong scaling: the same 1024 views at every N) ----
+    sweep = None
+    if cfg == 1:
+        sw = scenes.make_candidates(2)
+        ss, se = sd.shard_range(len(sw), rank, world)
+        sw_poses = [c.camera_pose() for c in sw[ss:se]]
+        score_poses(gm, cam, sw_poses, ctx=ctx)  # warm-up (scratch sized for the sweep)
+        sw_ms = []
+        for _ in range(2):
+            barrier()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            snm, ses = score_poses(gm, cam, sw_poses, ctx=ctx)
+            if dist_on:
+                snm, ses = sd.gather_scores(len(sw), snm, ses)
+            ev1.record(stream)
+            ev1.synchronize()
+            sw_ms.append(ev0.elapsed_time(ev1))
+        t_sw = float(np.mean(sw_ms))
+        if dist_on:
+            t = torch.tensor([t_sw], dtype=torch.float64, device="cuda")
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            t_sw = float(t.item())
+        for c, a, b in zip(sw, snm, ses):
+            c.n_missing, c.entropy_sum = float(a), float(b)
+        combine_scores(sw, CURRENT_POSITION)
+        sweep = {"config": "cfg2 candidate sweep: the cfg1 map, 16 x 8 lattice at 0.25 m "
+                           "(y = 1.4 m) x 8 yaws = 1024 views, sharded over the ranks",
+                 "scaling": "strong", "views": len(sw), "views_per_s": len(sw) / (t_sw / 1e3),
+                 "ms_per_pass": t_sw, "n_gpus": world,
+                 "argmax_view": int(max(range(len(sw)), key=lambda i: (sw[i].i_total, -i))),
+                 "n_missing_all_zero": bool(np.all(np.asarray(snm) == 0))}
+
+    # ---- e2e through the public API (host inputs, map re-upload every step; at N > 1 rank 0
+    #      uploads and broadcasts the device snapshot, the others import it) ----
+    h2d = (int(gm_host.centers.nbytes + gm_host.log_radii.nbytes + gm_host.opacity_logits.nbytes +
+               gm_host.colors.nbytes + gm_host.sem_indices.nbytes + gm_host.sem_probs.nbytes)
+           if gm_host is not None else 0) + 96 * len(mine)
     d2h = 16 * len(mine)
     e2e_ms = []
     for i in range(args.warmup + args.steps):
-        gm.touch()
+        if gm_host is not None:
+            gm_host.touch()
         fresh = [type(c)(position=c.position, direction=c.direction, id=c.id) for c in mine]
         barrier()
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        refresh_candidate_scores(fresh, gm, cam, ctx=ctx)
+        gm_e = sd.broadcast_map(gm_host, ctx) if dist_on else gm_host
+        refresh_candidate_scores(fresh, gm_e, cam, ctx=ctx)
         if dist_on:
             sd.gather_scores(n_total, np.array([c.n_missing for c in fresh]),
                              np.array([c.entropy_sum for c in fresh]))
@@ -715,6 +758,7 @@ def main() -> None:
             "render_ms_per_frame": render_info,
             "mapping_optimize": mapping_info,
             "anisotropic_ewa": aniso_info,
+            "cfg2_sweep": sweep,
         }
         print(json.dumps(line), flush=True)
     if dist_on:

@@ -136,6 +136,52 @@ void sgm_map_release(sgm_ctx* ctx, sgm_map* map);
 int sgm_map_set_anisotropic(sgm_ctx* ctx, sgm_map* map, const double* log_scales,
                             const double* quats);
 
+/* ---- device snapshot interchange (SURVEY §8e collective C1: the map broadcast) ----
+ * A map's device snapshot (activated geometry, clamped colours, class-sorted rows, the
+ * anisotropic covariance) packed into one blob in DEVICE memory, so a map is broadcast
+ * device to device (e.g. ncclBroadcast over NVLink, or a peer copy) instead of re-running
+ * the host activations on every rank. sgm_map_export writes into `d_blob` (capacity >=
+ * sgm_map_export_bytes) on the ctx's device; sgm_map_import builds a map on ctx's device
+ * from a blob in any device memory it can read (peer or own). The imported map is
+ * bit-identical to the exported one (the Fisher prior is not part of the snapshot). */
+/* n, k, num_classes and whether the anisotropic mode is on, of an uploaded or imported map.
+ * Any output may be NULL. */
+int sgm_map_info(sgm_ctx* ctx, const sgm_map* map, uint64_t* n, int32_t* k, int32_t* num_classes,
+                 int32_t* anisotropic);
+int sgm_map_export_bytes(sgm_ctx* ctx, const sgm_map* map, uint64_t* bytes);
+int sgm_map_export(sgm_ctx* ctx, const sgm_map* map, void* d_blob, uint64_t capacity);
+int sgm_map_import(sgm_ctx* ctx, const void* d_blob, uint64_t bytes, sgm_map** out);
+
+/* ---- multi-GPU scoring in one process (refresh_candidate_scores,
+ * explorer.cpp:186-205, whose candidate loop "parallelizes over candidates") ----
+ * One sgm_ctx per device (devices NULL: 0 .. n_devices-1; n_devices <= 0: every visible
+ * device). sgm_multi_map_upload runs the host activations and H2D once (first device) and
+ * replicates the snapshot device to device (peer copies over NVLink). Scoring shards the n
+ * views contiguously (sizes differ by <= 1) over the devices, one host thread each, and
+ * writes every view's result to its own slot: per-view results are bit-identical to
+ * sgm_score_views on one device. Errors: status + sgm_multi_last_error; a failing
+ * sgm_multi_create reports through sgm_last_error(NULL). */
+typedef struct sgm_multi sgm_multi;
+typedef struct sgm_multi_map sgm_multi_map;
+int sgm_multi_create(int32_t n_devices, const int32_t* devices, sgm_multi** out);
+void sgm_multi_destroy(sgm_multi* mg);
+const char* sgm_multi_last_error(const sgm_multi* mg);
+int32_t sgm_multi_device_count(const sgm_multi* mg);
+/* The i-th device's ctx (owned by mg), for single-device calls (render, ...). */
+sgm_ctx* sgm_multi_ctx(sgm_multi* mg, int32_t i);
+int sgm_multi_map_upload(sgm_multi* mg, uint64_t n, int32_t k, int32_t num_classes,
+                         const double* centers, const double* log_radii,
+                         const double* opacity_logits, const double* colors,
+                         const uint16_t* sem_indices, const double* sem_probs,
+                         sgm_multi_map** out);
+void sgm_multi_map_release(sgm_multi* mg, sgm_multi_map* map);
+int sgm_multi_score_views(sgm_multi* mg, const sgm_multi_map* map, const sgm_camera* cam,
+                          uint64_t n, const sgm_pose* poses, const sgm_options* opt,
+                          double* n_missing, double* entropy_sum);
+int sgm_multi_score_candidates(sgm_multi* mg, const sgm_multi_map* map, const sgm_camera* cam,
+                               uint64_t n, const sgm_candidate* cands, const sgm_options* opt,
+                               double* n_missing, double* entropy_sum);
+
 /* ---- render (splat_render.hpp:78-80, render()) ----
  * Host output planes in the reference layout; NULL for channels not requested.
  * silhouette (px) is always written. color px*3, depth px, sem px*(num_classes+1).

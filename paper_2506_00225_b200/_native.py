@@ -139,6 +139,23 @@ SIGNATURES = {
                                  _pu16, _pd, C.POINTER(_vp)]),
     "sgm_map_release": (None, [_vp, _vp]),
     "sgm_map_set_anisotropic": (C.c_int, [_vp, _vp, _pd, _pd]),
+    "sgm_map_info": (C.c_int, [_vp, _vp, _pu64, _pi32, _pi32, _pi32]),
+    "sgm_map_export_bytes": (C.c_int, [_vp, _vp, _pu64]),
+    "sgm_map_export": (C.c_int, [_vp, _vp, _vp, C.c_uint64]),
+    "sgm_map_import": (C.c_int, [_vp, _vp, C.c_uint64, C.POINTER(_vp)]),
+    "sgm_multi_create": (C.c_int, [C.c_int32, _pi32, C.POINTER(_vp)]),
+    "sgm_multi_destroy": (None, [_vp]),
+    "sgm_multi_last_error": (C.c_char_p, [_vp]),
+    "sgm_multi_device_count": (C.c_int32, [_vp]),
+    "sgm_multi_ctx": (_vp, [_vp, C.c_int32]),
+    "sgm_multi_map_upload": (C.c_int, [_vp, C.c_uint64, C.c_int32, C.c_int32, _pd, _pd, _pd, _pd,
+                                       _pu16, _pd, C.POINTER(_vp)]),
+    "sgm_multi_map_release": (None, [_vp, _vp]),
+    "sgm_multi_score_views": (C.c_int, [_vp, _vp, C.POINTER(sgm_camera), C.c_uint64,
+                                        C.POINTER(sgm_pose), C.POINTER(sgm_options), _pd, _pd]),
+    "sgm_multi_score_candidates": (C.c_int, [_vp, _vp, C.POINTER(sgm_camera), C.c_uint64,
+                                             C.POINTER(sgm_candidate), C.POINTER(sgm_options),
+                                             _pd, _pd]),
     "sgm_render": (C.c_int, [_vp, _vp, C.POINTER(sgm_camera), C.POINTER(sgm_pose), C.c_uint32,
                              C.POINTER(sgm_options), _pd, _pd, _pd, _pd, _pu64]),
     "sgm_render_reference": (C.c_int, [_vp, _vp, C.POINTER(sgm_camera), C.POINTER(sgm_pose),

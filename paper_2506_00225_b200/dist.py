@@ -2,7 +2,12 @@
 
 Views are independent (explorer.cpp:188-204), so the data path has
 no collective. The only exchanges are the ones the planning step really has:
-  C1 broadcast_map   - the map snapshot from rank 0, once per map version
+  C1 broadcast_map   - the map's DEVICE snapshot from rank 0, once per map version: rank 0
+                       uploads (host activations + H2D, once), exports the snapshot blob into
+                       a device tensor, ncclBroadcast sends it over NVLink, every other rank
+                       imports it (sgm_map_export / sgm_map_import); no rank re-derives it
+                       from host arrays. broadcast_map_arrays is the host-array variant for
+                       processes without a device (the gloo CPU tests).
   C2 all_reduce_prior - the Fisher prior H (N x 8) summed over ranks, each rank having
                        accumulated its shard of the past poses (fisher_prior_sharded)
   C3 gather_scores   - every rank's (n_missing, entropy_sum) records, so every
@@ -35,8 +40,38 @@ def _device() -> torch.device:
     return torch.device("cpu")
 
 
-def broadcast_map(gmap: Optional[GaussianMap], src: int = 0) -> GaussianMap:
-    """C1: every rank receives rank `src`'s map (fp64 SoA + u16 ids), bit-identical."""
+def broadcast_map(gmap: Optional[GaussianMap], ctx, src: int = 0):
+    """C1: rank `src`'s map snapshot to every rank, device to device. Returns `gmap` on src and
+    a DeviceMap (bit-identical snapshot on `ctx`'s device) on every other rank. With NCCL the
+    blob goes device to device; with gloo (no device transport) it is staged through host
+    memory, the same bytes."""
+    rank = dist.get_rank()
+    cuda = torch.device("cuda", ctx.device)
+    if rank == src:
+        nbytes = ctx.export_bytes(gmap)
+        blob = torch.empty(nbytes, dtype=torch.uint8, device=cuda)
+        ctx.export_map(gmap, blob.data_ptr(), nbytes)  # synchronous on the ctx stream
+    size = torch.tensor([nbytes if rank == src else 0], dtype=torch.int64, device=_device())
+    dist.broadcast(size, src)
+    nbytes = int(size.item())
+    if rank != src:
+        blob = torch.empty(nbytes, dtype=torch.uint8, device=cuda)
+    if dist.get_backend() == "nccl":
+        dist.broadcast(blob, src)
+    else:
+        host = blob.cpu() if rank == src else torch.empty(nbytes, dtype=torch.uint8)
+        dist.broadcast(host, src)
+        if rank != src:
+            blob.copy_(host)
+    torch.cuda.current_stream(cuda).synchronize()  # the blob is complete before the import
+    if rank == src:
+        return gmap
+    return ctx.import_map(blob.data_ptr(), nbytes)
+
+
+def broadcast_map_arrays(gmap: Optional[GaussianMap], src: int = 0) -> GaussianMap:
+    """C1 for processes without a device: every rank receives rank `src`'s host arrays
+    (fp64 SoA + u16 ids), bit-identical."""
     dev = _device()
     rank = dist.get_rank()
     if rank == src:

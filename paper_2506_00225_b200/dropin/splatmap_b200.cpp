@@ -11,9 +11,12 @@
 // untouched. INTEGRATION.md shows the build wiring; tests/test_dropin.py links the
 // reference's own test files against this TU and runs them on the GPU.
 //
-// Device: SGM_DEVICE (default 0), one sgm_ctx per process. The map is uploaded on
-// every call: GaussianMap is mutable through its spans, so no stale snapshot is ever
-// rendered (refresh_candidate_scores uploads once for all its candidates).
+// Devices: SGM_DEVICES ("0,1,2,3"), else SGM_DEVICE (one device), else every visible GPU;
+// one sgm_multi per process. refresh_candidate_scores shards its candidates over all of
+// them (sgm_multi: the map uploaded once, replicated device to device over NVLink, one host
+// thread per GPU); render / render_entropy run on the first. The map is uploaded on every
+// call: GaussianMap is mutable through its spans, so no stale snapshot is ever rendered
+// (refresh_candidate_scores uploads once for all its candidates).
 #include <cstdlib>
 #include <mutex>
 #include <stdexcept>
@@ -29,16 +32,30 @@ namespace {
 
 std::mutex g_mu;  // the C ABI serialises calls per ctx; the reference API is free to call from threads
 
-sgm_ctx* ctx() {
-    static sgm_ctx* c = [] {
-        const char* dev = std::getenv("SGM_DEVICE");
-        sgm_ctx* h = nullptr;
-        if (sgm_ctx_create(dev ? std::atoi(dev) : 0, &h) != SGM_OK)
-            throw std::runtime_error(std::string("sgm: ") + sgm_last_error(nullptr));
+sgm_multi* multi() {
+    static sgm_multi* m = [] {
+        std::vector<int32_t> devs;
+        if (const char* list = std::getenv("SGM_DEVICES")) {
+            for (const char* p = list; *p;) {
+                char* end = nullptr;
+                const long d = std::strtol(p, &end, 10);
+                if (end == p) break;
+                devs.push_back(static_cast<int32_t>(d));
+                p = (*end == ',') ? end + 1 : end;
+            }
+        } else if (const char* one = std::getenv("SGM_DEVICE")) {
+            devs.push_back(static_cast<int32_t>(std::atoi(one)));
+        }
+        sgm_multi* h = nullptr;
+        const int rc = devs.empty() ? sgm_multi_create(0, nullptr, &h)
+                                    : sgm_multi_create(static_cast<int32_t>(devs.size()), devs.data(), &h);
+        if (rc != SGM_OK) throw std::runtime_error(std::string("sgm: ") + sgm_last_error(nullptr));
         return h;
     }();
-    return c;
+    return m;
 }
+
+sgm_ctx* ctx() { return sgm_multi_ctx(multi(), 0); }
 
 void check(int rc) {
     if (rc == SGM_OK) return;
@@ -158,13 +175,28 @@ void refresh_candidate_scores(std::span<CandidatePose> candidates, const Gaussia
             cs[i].position[a] = active[i]->position[a];
             cs[i].direction[a] = active[i]->direction[a];
         }
-    MapHandle h(map);
+    auto mcheck = [](int rc) {
+        if (rc == SGM_OK) return;
+        const std::string msg = std::string("sgm: ") + sgm_multi_last_error(multi());
+        if (rc == SGM_ERR_INVALID) throw std::invalid_argument(msg);
+        throw std::runtime_error(msg);
+    };
+    sgm_multi_map* mm = nullptr;
+    mcheck(sgm_multi_map_upload(multi(), map.size(), map.k(), map.num_classes(),
+                                map.centers().data(), map.log_radii().data(),
+                                map.opacity_logits().data(), map.colors().data(),
+                                map.sem_indices().data(), map.sem_probs().data(), &mm));
+    struct Release {
+        sgm_multi_map* m;
+        ~Release() { sgm_multi_map_release(multi(), m); }
+    } release{mm};
     const sgm_camera cam = cam_of(scoring_camera);
     const RenderOptions defaults;  // the reference scores with default options (explorer.cpp:194)
     const sgm_options op = opt_of(defaults);
     std::vector<double> nm(active.size()), es(active.size());
-    check(sgm_score_candidates(ctx(), h.m, &cam, active.size(), cs.data(), &op, nm.data(),
-                               es.data()));
+    // candidates sharded over every device of the process
+    mcheck(sgm_multi_score_candidates(multi(), mm, &cam, active.size(), cs.data(), &op, nm.data(),
+                                      es.data()));
     for (size_t i = 0; i < active.size(); ++i) {
         active[i]->n_missing = nm[i];
         active[i]->entropy_sum = es[i];

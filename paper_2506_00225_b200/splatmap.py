@@ -484,7 +484,12 @@ class Context:
         self.check(N.lib.sgm_ctx_reset_stats(self.handle))
 
     def upload(self, gmap: GaussianMap) -> C.c_void_p:
-        """Device snapshot of `gmap`, re-uploaded when the map's version changes."""
+        """Device snapshot of `gmap`, re-uploaded when the map's version changes (a
+        DeviceMap already is one)."""
+        if isinstance(gmap, DeviceMap):
+            if gmap.ctx is not self:
+                raise ValueError("DeviceMap belongs to another Context")
+            return gmap.handle
         key = id(gmap)
         hit = self._maps.get(key)
         if hit is not None:
@@ -527,6 +532,124 @@ class Context:
 
     def release(self, handle) -> None:
         N.lib.sgm_map_release(self.handle, handle)
+
+    # ---- device snapshot interchange (the map broadcast)
+    def export_bytes(self, gmap) -> int:
+        b = C.c_uint64()
+        self.check(N.lib.sgm_map_export_bytes(self.handle, self.upload(gmap), C.byref(b)))
+        return b.value
+
+    def export_map(self, gmap, d_blob: int, capacity: int) -> None:
+        """Packs `gmap`'s device snapshot into device memory at d_blob (this ctx's device)."""
+        self.check(N.lib.sgm_map_export(self.handle, self.upload(gmap), C.c_void_p(d_blob),
+                                        int(capacity)))
+
+    def import_map(self, d_blob: int, nbytes: int) -> "DeviceMap":
+        """A map from a snapshot blob in device memory (e.g. received by ncclBroadcast)."""
+        h = C.c_void_p()
+        self.check(N.lib.sgm_map_import(self.handle, C.c_void_p(d_blob), int(nbytes), C.byref(h)))
+        return DeviceMap(self, h)
+
+
+class DeviceMap:
+    """A map that exists only as a device snapshot on one Context (sgm_map_import): accepted
+    wherever a GaussianMap is (render, score_poses, fisher_prior, ...). Released with it."""
+
+    def __init__(self, ctx: Context, handle: C.c_void_p):
+        self.ctx, self.handle = ctx, handle
+        n, k, m, a = C.c_uint64(), C.c_int32(), C.c_int32(), C.c_int32()
+        ctx.check(N.lib.sgm_map_info(ctx.handle, handle, C.byref(n), C.byref(k), C.byref(m),
+                                     C.byref(a)))
+        self._n, self._k, self._num_classes, self._aniso = n.value, k.value, m.value, bool(a.value)
+
+    def size(self) -> int:
+        return self._n
+
+    def k(self) -> int:
+        return self._k
+
+    def num_classes(self) -> int:
+        return self._num_classes
+
+    def channels(self) -> int:
+        return self._num_classes + 1
+
+    def anisotropic(self) -> bool:
+        return self._aniso
+
+    def empty(self) -> bool:
+        return self._n == 0
+
+    def __del__(self):
+        try:
+            if self.handle and self.ctx.handle:
+                N.lib.sgm_map_release(self.ctx.handle, self.handle)
+        except Exception:
+            pass
+        self.handle = None
+
+
+class MultiContext:
+    """Several GPUs driven from one process (sgm_multi): one Context per device,
+    the map uploaded once and replicated device to device, candidate views sharded over the
+    devices. score_poses / refresh_candidate_scores accept it as `ctx`; per-view results are
+    bit-identical to a single Context. devices=None: every visible device."""
+
+    def __init__(self, devices: Optional[Sequence[int]] = None):
+        h = C.c_void_p()
+        if devices is None:
+            code = N.lib.sgm_multi_create(0, None, C.byref(h))
+        else:
+            arr = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+            code = N.lib.sgm_multi_create(len(devices), arr, C.byref(h))
+        N.check(code, None)
+        self.handle = h
+        self._maps: dict = {}
+
+    def device_count(self) -> int:
+        return int(N.lib.sgm_multi_device_count(self.handle))
+
+    def check(self, code: int) -> None:
+        if code != N.SGM_OK:
+            msg = N.lib.sgm_multi_last_error(self.handle)
+            raise N.SgmError(code, msg.decode() if msg else "")
+
+    def upload(self, gmap: GaussianMap):
+        key = id(gmap)
+        hit = self._maps.get(key)
+        if hit is not None:
+            ref, ver, handle = hit
+            if ref() is gmap and ver == gmap._version:
+                return handle
+            N.lib.sgm_multi_map_release(self.handle, handle)
+            del self._maps[key]
+        if gmap.anisotropic():
+            raise ValueError("MultiContext: anisotropic maps are scored per Context")
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in
+                (gmap.centers, gmap.log_radii, gmap.opacity_logits, gmap.colors)]
+        idx = np.ascontiguousarray(gmap.sem_indices, dtype=np.uint16)
+        probs = np.ascontiguousarray(gmap.sem_probs, dtype=np.float64)
+        h = C.c_void_p()
+        self.check(N.lib.sgm_multi_map_upload(
+            self.handle, gmap.size(), gmap.k(), gmap.num_classes(), N.dptr(arrs[0]),
+            N.dptr(arrs[1]), N.dptr(arrs[2]), N.dptr(arrs[3]),
+            idx.ctypes.data_as(C.POINTER(C.c_uint16)), N.dptr(probs), C.byref(h)))
+        self._maps[key] = (weakref.ref(gmap), gmap._version, h)
+        return h
+
+    def close(self) -> None:
+        if self.handle:
+            for _, (_, _, m) in list(self._maps.items()):
+                N.lib.sgm_multi_map_release(self.handle, m)
+            self._maps.clear()
+            N.lib.sgm_multi_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def _ctx(ctx: Optional[Context]) -> Context:
@@ -689,7 +812,8 @@ class CandidatePose:
 
 def score_poses(gmap: GaussianMap, camera: CameraModel, poses: Sequence[Pose],
                 options: Optional[RenderOptions] = None, ctx: Optional[Context] = None):
-    """Batched GPU scoring of explicit poses: (n_missing[n], entropy_sum[n])."""
+    """Batched GPU scoring of explicit poses: (n_missing[n], entropy_sum[n]). With a
+    MultiContext the views are sharded over its devices."""
     c = _ctx(ctx)
     handle = c.upload(gmap)
     n = len(poses)
@@ -700,8 +824,8 @@ def score_poses(gmap: GaussianMap, camera: CameraModel, poses: Sequence[Pose],
     arr = (N.sgm_pose * n)(*[p._c() for p in poses])
     opt = (options if options is not None else RenderOptions())._c()
     cam_c = camera._c()
-    c.check(N.lib.sgm_score_views(c.handle, handle, C.byref(cam_c), n, arr, C.byref(opt),
-                                  N.dptr(nm), N.dptr(es)))
+    fn = N.lib.sgm_multi_score_views if isinstance(c, MultiContext) else N.lib.sgm_score_views
+    c.check(fn(c.handle, handle, C.byref(cam_c), n, arr, C.byref(opt), N.dptr(nm), N.dptr(es)))
     return nm, es
 
 
@@ -865,8 +989,9 @@ def refresh_candidate_scores(candidates: List[CandidatePose], gmap: GaussianMap,
     es = np.zeros(n)
     opt = RenderOptions()._c()
     cam_c = scoring_camera._c()
-    c.check(N.lib.sgm_score_candidates(c.handle, handle, C.byref(cam_c), n, arr, C.byref(opt),
-                                       N.dptr(nm), N.dptr(es)))
+    fn = (N.lib.sgm_multi_score_candidates if isinstance(c, MultiContext)
+          else N.lib.sgm_score_candidates)
+    c.check(fn(c.handle, handle, C.byref(cam_c), n, arr, C.byref(opt), N.dptr(nm), N.dptr(es)))
     for i, cd in enumerate(active):
         cd.n_missing = float(nm[i])
         cd.entropy_sum = float(es[i])

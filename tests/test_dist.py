@@ -43,7 +43,7 @@ def _worker(rank, world, port, out, aniso=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     gm = scenes.make_map(0, n=600, aniso=aniso) if rank == 0 else None
-    gm = sd.broadcast_map(gm)
+    gm = sd.broadcast_map_arrays(gm)
     cam = CameraModel(48, 30, 0, 0, 30.0, 30.0, 24.0, 15.0)
     cands = scenes.make_candidates(0, 7)
     s, e = sd.shard_range(len(cands), rank, world)
@@ -87,7 +87,7 @@ def _prior_worker(rank, world, port, out):
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    gm = sd.broadcast_map(scenes.make_map(0, n=300) if rank == 0 else None)
+    gm = sd.broadcast_map_arrays(scenes.make_map(0, n=300) if rank == 0 else None)
     cam = CameraModel(40, 26, 0, 0, 30.0, 30.0, 20.0, 13.0)
     poses = [c.camera_pose() for c in scenes.make_candidates(0, 5, stream=2)]
     s, e = sd.shard_range(len(poses), rank, world)
