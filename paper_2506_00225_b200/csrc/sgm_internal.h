@@ -282,6 +282,21 @@ void launch_eval_keys(const float* scores, const uint16_t* label, uint32_t T, in
 void launch_eval_ap_terms(const uint32_t* pos, const uint32_t* tp, uint32_t T, double P,
                           double* terms, cudaStream_t s);
 
+// sgm_sort.cu: hand-written stable LSD radix sort (8-bit digits) of (u32 key, value) pairs over
+// nseg segments (segment s at keys + s * stride, d_n[s] elements on the device, at most
+// max_len), bits [0, end_bit). Returns true when the result is in the *_alt buffers.
+size_t radix_sort_scratch_bytes(uint64_t max_len, int nseg);
+template <typename V, typename N>
+bool radix_sort_pairs(uint32_t* keys, V* vals, uint32_t* keys_alt, V* vals_alt, size_t stride,
+                      const N* d_n, uint64_t max_len, int nseg, int end_bit, uint32_t* scratch,
+                      cudaStream_t s);
+int radix_sort_launches(int end_bit);
+// exclusive scan of n counts (u32 or u64) into u64 offsets
+size_t exclusive_scan_scratch_bytes(uint64_t n);
+template <typename C>
+void exclusive_scan_u64(const C* in, uint64_t n, unsigned long long* out, unsigned long long* scratch,
+                        cudaStream_t s);
+
 // sgm_raster.cu
 GroupParams choose_groups(int C, int k);
 size_t raster_smem_bytes(const DevMap& m, const GroupParams& gp, bool render);

@@ -60,24 +60,21 @@ unsigned tile_bits(uint64_t tiles) {
 // slices and returns via the slice pointers. vals/keys hold the compacted (z, idx).
 static void bin_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const CamParams& cam,
               const OptParams& o, const PoseParams* d_pose, uint32_t* keys, uint32_t* vals,
-              uint32_t V, uint64_t P, uint64_t R, PackedSplat* packed, uint4* bounds, uint32_t* list,
-              uint2* ranges, int bin_tiles) {
+              uint32_t V, uint64_t P, uint64_t R, const uint32_t* d_V, const unsigned long long* d_R,
+              PackedSplat* packed, uint4* bounds, uint32_t* list, uint2* ranges, int bin_tiles) {
     CK(cudaMemsetAsync(ranges, 0, sizeof(uint2) * bin_tiles, s));
     if (V == 0) return;
-    // K2: depth rank (radix sort on the monotone fp32 key; runs fixed below)
-    cub::DoubleBuffer<uint32_t> dk(keys, ctx->keys_alt.as<uint32_t>());
-    cub::DoubleBuffer<uint32_t> dv(vals, ctx->vals_alt.as<uint32_t>());
-    size_t tmp = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, V, 0, 32, s));
-    CK(ctx->cub_tmp.reserve(tmp));
-    CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, dk, dv, V, 0, 32, s));
-    ctx->stats.kernel_launches += 1;  // counted as one library sort call
-    launch_tiefix(map->dev, d_pose, cam, o, dk.Current(), dv.Current(), V, s);
-    launch_pack(map->dev, d_pose, cam, o, map->groups, dv.Current(), V, packed,
+    // K2: depth rank. The (fp32 depth key, index) pairs arrive sorted by the sub-batch's
+    // hand-written radix sort (sgm_sort.cu, run_views); runs of equal keys are fixed here
+    const uint32_t* skey = keys;
+    uint32_t* sval = vals;
+    (void)d_V;
+    launch_tiefix(map->dev, d_pose, cam, o, skey, sval, V, s);
+    launch_pack(map->dev, d_pose, cam, o, map->groups, sval, V, packed,
                 ctx->counts.as<unsigned long long>(), ctx->rects.as<int4>(), bounds, s);
     ctx->stats.kernel_launches += (V >= 2 ? 1 : 0) + 1;
     // keep the sorted indices for sgm_last_projections
-    if (dv.Current() != vals) CK(cudaMemcpyAsync(vals, dv.Current(), 4ull * V, cudaMemcpyDeviceToDevice, s));
+    if (sval != vals) CK(cudaMemcpyAsync(vals, sval, 4ull * V, cudaMemcpyDeviceToDevice, s));
     if (P == 0) return;
     // K3 (row-bucketed, no sort of the P pairs): tile ranges from the rectangles' 2D
     // difference array; each tile row's ranks in rank order (R = sum of rows spanned pairs,
@@ -91,25 +88,23 @@ static void bin_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const Cam
     launch_bin_hist(ctx->rects.as<int4>(), V, o.tiles_x, diff, rows, s);
     launch_bin_scan(diff, o.tiles_x, o.tiles_y, ranges, s);
     CK(cudaMemsetAsync(rows + V, 0, sizeof(unsigned long long), s));
-    size_t tmp2 = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, rows, roff, V + 1, s));
-    CK(ctx->cub_tmp.reserve(tmp2));
-    CK(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp2, rows, roff, V + 1, s));
+    exclusive_scan_u64<unsigned long long>(rows, V + 1, roff, ctx->scan_tmp.as<unsigned long long>(), s);
     uint32_t* rk = ctx->tkeys.as<uint32_t>();
     unsigned long long* rv = ctx->rvals.as<unsigned long long>();
     launch_emit_rows(roff, ctx->rects.as<int4>(), V, R, rk, rv, s);
-    cub::DoubleBuffer<uint32_t> qk(rk, ctx->tkeys_alt.as<uint32_t>());
-    cub::DoubleBuffer<unsigned long long> qv(rv, ctx->tvals_alt.as<unsigned long long>());
-    tmp2 = 0;
+    // each tile row's (row, rank) pairs in rank order: a stable sort on the row key
     const int rbits = static_cast<int>(tile_bits(static_cast<uint64_t>(o.tiles_y)));
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, qk, qv, R, 0, rbits, s));
-    CK(ctx->cub_tmp.reserve(tmp2));
-    CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp2, qk, qv, R, 0, rbits, s));
+    const bool ralt = radix_sort_pairs<unsigned long long, unsigned long long>(
+        rk, rv, ctx->tkeys_alt.as<uint32_t>(), ctx->tvals_alt.as<unsigned long long>(), 0, d_R, R, 1,
+        rbits, ctx->sort_tmp.as<uint32_t>(), s);
+    const uint32_t* qk = ralt ? ctx->tkeys_alt.as<uint32_t>() : rk;
+    const unsigned long long* qv = ralt ? ctx->tvals_alt.as<unsigned long long>() : rv;
+    ctx->stats.kernel_launches += radix_sort_launches(rbits) + 3;  // + the 3-kernel scan
     uint2* rranges = ctx->rranges.as<uint2>();
     CK(cudaMemsetAsync(rranges, 0, sizeof(uint2) * o.tiles_y, s));
-    launch_ranges(qk.Current(), R, rranges, s);
+    launch_ranges(qk, R, rranges, s);
     const uint64_t G = row_scatter_segments(R, o.tiles_y);  // buffers sized per group (run_views)
-    launch_row_scatter(qv.Current(), rranges, ranges, o.tiles_x, o.tiles_y, R,
+    launch_row_scatter(qv, rranges, ranges, o.tiles_x, o.tiles_y, R,
                        ctx->segs.as<uint4>(), reinterpret_cast<uint32_t*>(ctx->segs.as<char>() + sizeof(uint4) * G),
                        ctx->segcnt.as<uint32_t>(), list, s);
     ctx->stats.kernel_launches += 7;
@@ -149,9 +144,9 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
     CK(ctx->rranges.reserve(sizeof(uint2) * o.tiles_y));
     CK(ctx->keys.reserve(4 * NS * B));
     CK(ctx->vals.reserve(4 * NS * B));
-    CK(ctx->keys_alt.reserve(4 * NS));
+    CK(ctx->keys_alt.reserve(4 * NS * std::min<uint64_t>(B, 8)));  // a sub-batch of depth sorts
     CK(ctx->rects.reserve(sizeof(int4) * NS));
-    CK(ctx->vals_alt.reserve(4 * NS));
+    CK(ctx->vals_alt.reserve(4 * NS * std::min<uint64_t>(B, 8)));
     CK(ctx->packed.reserve(sizeof(PackedSplat) * NS * B));
     CK(ctx->bounds.reserve(sizeof(uint4) * NS * B));
     CK(ctx->counts.reserve(8 * (NS + 1)));
@@ -218,6 +213,9 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
             CK(ctx->tkeys_alt.reserve(4 * maxR));
             CK(ctx->tvals_alt.reserve(8 * maxR));
             CK(ctx->rvals.reserve(8 * maxR));
+            CK(ctx->sort_tmp.reserve(std::max(radix_sort_scratch_bytes(maxR, 1),
+                                              radix_sort_scratch_bytes(NS, kSub))));
+            CK(ctx->scan_tmp.reserve(exclusive_scan_scratch_bytes(NS + 1)));
             // row-scatter segments of the largest view (reserved here, not between the
             // views' binning launches: a reallocation would synchronise the device)
             const uint64_t maxG = row_scatter_segments(maxR, o.tiles_y);
@@ -270,11 +268,23 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
             rp.want_rc = fk == Fisher::Gain ? 1 : 0;
             for (int s0 = v0; s0 < v1; s0 += kSub) {
                 const int s1 = std::min(v1, s0 + kSub);
+                {  // K2 for the sub-batch: one segmented radix sort of its views' depth keys
+                    uint32_t maxV = 0;
+                    for (int v = s0; v < s1; ++v) maxV = std::max(maxV, V[v]);
+                    const bool alt = radix_sort_pairs<uint32_t, uint32_t>(
+                        ctx->keys.as<uint32_t>() + NS * s0, ctx->vals.as<uint32_t>() + NS * s0,
+                        ctx->keys_alt.as<uint32_t>(), ctx->vals_alt.as<uint32_t>(), NS,
+                        ctx->vcount.as<uint32_t>() + s0, maxV, s1 - s0, 32, ctx->sort_tmp.as<uint32_t>(), sb);
+                    if (alt) fail(SGM_ERR_CUDA, "depth sort: odd pass count");  // 4 passes: in place
+                    ctx->stats.kernel_launches += maxV ? radix_sort_launches(32) : 0;
+                }
                 for (int v = s0; v < s1; ++v) {
                     const ViewDesc& d = hvd[v - v0];
                     bin_view(ctx, sb, map, cam, o, ctx->poses.as<PoseParams>() + v,
                              ctx->keys.as<uint32_t>() + NS * v, const_cast<uint32_t*>(d.order), V[v],
-                             P[v], R[v], const_cast<PackedSplat*>(d.packed), const_cast<uint4*>(d.bounds),
+                             P[v], R[v], ctx->vcount.as<uint32_t>() + v,
+                             ctx->pcount.as<unsigned long long>() + nb + v,
+                             const_cast<PackedSplat*>(d.packed), const_cast<uint4*>(d.bounds),
                              const_cast<uint32_t*>(d.list), const_cast<uint2*>(d.ranges), bin_tiles);
                 }
                 const int slot = (s0 / kSub) & 1;
@@ -408,13 +418,11 @@ void do_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const
         rt.contrib_count = ctx->ccount.as<uint32_t>();
         run_views(ctx, map, cam, o, 1, &p, Mode::Render, rt, nullptr, nullptr);
         // offsets = exclusive scan (flatten_contributors, :125-137)
-        size_t tmp = 0;
-        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ctx->ccount.as<uint32_t>(),
-                                         ctx->coffset.as<unsigned long long>(), px + 1, ctx->stream));
-        CK(ctx->cub_tmp.reserve(tmp));
-        CK(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp, ctx->ccount.as<uint32_t>(),
-                                         ctx->coffset.as<unsigned long long>(), px + 1, ctx->stream));
-        ctx->stats.kernel_launches += 1;
+        CK(ctx->scan_tmp.reserve(exclusive_scan_scratch_bytes(px + 1)));
+        exclusive_scan_u64<uint32_t>(ctx->ccount.as<uint32_t>(), px + 1,
+                                     ctx->coffset.as<unsigned long long>(),
+                                     ctx->scan_tmp.as<unsigned long long>(), ctx->stream);
+        ctx->stats.kernel_launches += 3;
         unsigned long long total = 0;
         CK(cudaMemcpyAsync(&total, ctx->coffset.as<unsigned long long>() + px, 8,
                            cudaMemcpyDeviceToHost, ctx->stream));
