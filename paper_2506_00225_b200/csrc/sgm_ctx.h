@@ -155,7 +155,8 @@ struct sgm_ctx {
     DevBuf poses, vcount, pcount, keys, vals, keys_alt, vals_alt, packed, counts, offsets, rects,
         bounds, bdiff, rranges, rvals, segs, segcnt, rcbuf;
     DevBuf tkeys, tvals, tkeys_alt, tvals_alt, ranges, ent_part, miss_part, views, out,
-        contributors, cub_tmp, sort_tmp, scan_tmp, planes, dbg, ccount, coffset, contrib, fis_part, bw_frame,
+        contributors, cub_tmp, sort_tmp, scan_tmp, franges, trunc8, bmask, incomplete, redo,
+        dense_tot, list2, planes, dbg, ccount, coffset, contrib, fis_part, bw_frame,
         bw_flags, bw_part, bw_grad;
     uint64_t last_ncontrib = 0;
     bool last_has_contrib = false;

@@ -175,6 +175,17 @@ struct RasterParams {
     int want_rc;         // score mode: also write vd.rc4 (colour / depth per pixel)
     int n_items;         // raster: (view, block) items of the launch (set by the launcher)
     int items_per_cta;   // raster: consecutive items per CTA (set by the launcher)
+    // optional explicit (view, raster tile) items (the redo pass of depth-prefix binning);
+    // null: every tile of every view of the launch
+    const uint2* item_list;
+    int n_item_list;
+    // depth-prefix binning (one dense view per launch): trunc[bin] = 1 when the bin's list
+    // holds only its first entries; a block that exhausts such a list with pixels still open
+    // appends its raster tile to incomplete[] (count *n_incomplete) to be redone from the
+    // full list. Null: every list is complete.
+    const uint8_t* trunc;
+    uint32_t* incomplete;
+    uint32_t* n_incomplete;
 };
 
 // ---- launchers (sgm_kernels.cu) ----
@@ -194,14 +205,26 @@ void launch_ranges(const uint32_t* sorted_tiles, uint64_t P, uint2* ranges, cuda
 // row's ranks in rank order, then a per-row ordered scatter into the tile lists
 void launch_bin_hist(const int4* rects, uint32_t V, int tiles_x, int* diff,
                      unsigned long long* rows, cudaStream_t s);
-void launch_bin_scan(int* diff, int tiles_x, int tiles_y, uint2* ranges, cudaStream_t s);
+// mask: bins outside it get empty lists; total: the pairs allocated; cap: a bin keeps its
+// first `cap` entries (depth-prefix binning), trunc[bin] = 1 when that drops some
+void launch_bin_scan(int* diff, int tiles_x, int tiles_y, uint2* ranges, cudaStream_t s,
+                     const uint8_t* mask = nullptr, unsigned long long* total = nullptr,
+                     uint32_t cap = 0xffffffffu, uint8_t* trunc = nullptr);
+// depth-prefix binning of dense views (sgm_pipeline.cu): the redo items / bin mask from a
+// view's incomplete raster tiles
+void launch_redo_items(const uint32_t* incomplete, uint32_t n, uint32_t view, int raster_tiles_x,
+                       int per_bin, int tiles_x, uint2* items, uint8_t* mask, cudaStream_t s);
 void launch_emit_rows(const unsigned long long* offsets, const int4* rects, uint32_t V,
                       unsigned long long R, uint32_t* row_keys, unsigned long long* row_vals,
                       cudaStream_t s);
 void launch_row_scatter(const unsigned long long* row_list, const uint2* row_ranges,
                         const uint2* tile_ranges, int tiles_x, int tiles_y, uint64_t R, uint4* segs,
-                        uint32_t* nseg, uint32_t* cnt, uint32_t* list, cudaStream_t s);
+                        uint32_t* nseg, uint32_t* cnt, uint32_t* list, cudaStream_t s,
+                        const uint8_t* mask = nullptr, bool part = false);
 uint64_t row_scatter_segments(uint64_t R, int tiles_y);  // upper bound on segments
+void launch_seg_pass(const unsigned long long* row_list, const uint2* tile_ranges, int tiles_x,
+                     uint64_t G, const uint4* segs, const uint32_t* nseg, const uint32_t* cnt,
+                     uint32_t* list, const uint8_t* mask, cudaStream_t s);
 void launch_raster_score(const RasterParams& p, int n_views, cudaStream_t s);
 void launch_raster_render(const RasterParams& p, int n_views, cudaStream_t s);
 void launch_reduce_scores(const ViewDesc* views, int n_views, int tiles, double* out_missing,

@@ -408,16 +408,30 @@ __global__ void k_bin_hist(const int4* __restrict__ rects, uint32_t V, int tiles
 }
 
 constexpr int kScanThreads = 1024;
+// One CTA: the 2D difference array becomes per-tile counts (prefix along x: a warp per row,
+// 32 columns at a time with shuffle scans; then along y: a thread per column, coalesced across
+// the columns), then an exclusive scan over the bins in row-major order (1024 bins per round,
+// warp scans + a carry) gives ranges[bin] = (begin, end).
 __global__ void __launch_bounds__(kScanThreads) k_bin_scan(int* __restrict__ diff, int tiles_x,
-                                                           int tiles_y, uint2* __restrict__ ranges) {
+                                                           int tiles_y, uint2* __restrict__ ranges,
+                                                           const uint8_t* __restrict__ mask,
+                                                           unsigned long long* __restrict__ total,
+                                                           uint32_t cap, uint8_t* __restrict__ trunc) {
     const int X = tiles_x + 1;
-    const int t = threadIdx.x;
-    // prefix along x, then along y: diff[y][x] becomes the tile count
-    for (int y = t; y < tiles_y; y += kScanThreads) {
-        int acc = 0;
-        for (int x = 0; x < tiles_x; ++x) {
-            acc += diff[y * X + x];
-            diff[y * X + x] = acc;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    for (int y = warp; y < tiles_y; y += kScanThreads / 32) {
+        int carry = 0;
+        for (int x0 = 0; x0 < tiles_x; x0 += 32) {
+            const int x = x0 + lane;
+            int v = x < tiles_x ? diff[y * X + x] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += u;
+            }
+            v += carry;
+            if (x < tiles_x) diff[y * X + x] = v;
+            carry = __shfl_sync(0xffffffffu, v, 31);
         }
     }
     __syncthreads();
@@ -429,27 +443,54 @@ __global__ void __launch_bounds__(kScanThreads) k_bin_scan(int* __restrict__ dif
         }
     }
     __syncthreads();
-    // exclusive scan over bins (row-major), each thread a contiguous segment
-    __shared__ uint32_t part[kScanThreads];
+    __shared__ uint32_t wsum[kScanThreads / 32];
+    __shared__ uint32_t base;
+    if (t == 0) base = 0u;
     const int T = tiles_x * tiles_y;
-    const int per = (T + kScanThreads - 1) / kScanThreads;
-    const int b0 = min(T, t * per), b1 = min(T, b0 + per);
-    uint32_t sum = 0;
-    for (int b = b0; b < b1; ++b) sum += static_cast<uint32_t>(diff[(b / tiles_x) * X + b % tiles_x]);
-    part[t] = sum;
-    __syncthreads();
-    for (int off = 1; off < kScanThreads; off <<= 1) {  // Hillis-Steele inclusive scan
-        const uint32_t v = t >= off ? part[t - off] : 0u;
+    for (int b0 = 0; b0 < T; b0 += kScanThreads) {
+        const int b = b0 + t;
+        uint32_t c = b < T ? static_cast<uint32_t>(diff[(b / tiles_x) * X + b % tiles_x]) : 0u;
+        if (mask && b < T && !mask[b]) c = 0u;  // bins outside the mask get empty lists
+        if (trunc && b < T) trunc[b] = c > cap ? 1 : 0;
+        if (c > cap) c = cap;  // depth-prefix binning: the first `cap` entries of the bin
+        uint32_t v = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        if (lane == 31) wsum[warp] = v;
         __syncthreads();
-        part[t] += v;
+        if (warp == 0) {
+            uint32_t w = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += u;
+            }
+            wsum[lane] = w;  // inclusive over the warps
+        }
+        __syncthreads();
+        const uint32_t begin = base + (warp ? wsum[warp - 1] : 0u) + v - c;
+        if (b < T) ranges[b] = make_uint2(begin, begin + c);
+        __syncthreads();
+        if (t == kScanThreads - 1) base += wsum[kScanThreads / 32 - 1];
         __syncthreads();
     }
-    uint32_t run = part[t] - sum;
-    for (int b = b0; b < b1; ++b) {
-        const uint32_t c = static_cast<uint32_t>(diff[(b / tiles_x) * X + b % tiles_x]);
-        ranges[b] = make_uint2(run, run + c);
-        run += c;
-    }
+    if (total && t == 0) *total = base;
+}
+
+// the redo pass of depth-prefix binning: (view, tile) items and the bin mask of the tiles
+// the raster reported incomplete
+__global__ void k_redo_items(const uint32_t* __restrict__ incomplete, uint32_t n, uint32_t view,
+                             int raster_tiles_x, int per_bin, int tiles_x, uint2* __restrict__ items,
+                             uint8_t* __restrict__ mask) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t t = incomplete[i];
+    items[i] = make_uint2(view, t);
+    const int tx = static_cast<int>(t % raster_tiles_x), ty = static_cast<int>(t / raster_tiles_x);
+    mask[(ty / per_bin) * tiles_x + tx / per_bin] = 1;
 }
 
 // Each tile row's list (ranks in rank order) is cut into segments of kSeg entries; a
@@ -494,10 +535,16 @@ __global__ void __launch_bounds__(1024) k_row_segs(const uint2* __restrict__ row
     if (t == 1023) *nseg_out = part[1023];
 }
 
+// kPart: depth-prefix binning (lists holding only a bin's first entries, or only the bins in
+// `mask`): positions are relative to the bin and writes stop at the bin's list length. The
+// plain instantiation writes every entry at absolute cursors.
+template <bool kPart>
 __global__ void __launch_bounds__(256) k_seg_pass(const unsigned long long* __restrict__ row_list,
                                                   const uint4* __restrict__ segs,
                                                   const uint32_t* __restrict__ nseg, int tiles_x,
-                                                  const uint32_t* __restrict__ cnt, uint32_t* __restrict__ list) {
+                                                  const uint32_t* __restrict__ cnt, uint32_t* __restrict__ list,
+                                                  const uint8_t* __restrict__ mask,
+                                                  const uint2* __restrict__ tile_ranges) {
     const uint32_t g = blockIdx.x;
     if (g >= *nseg) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -505,12 +552,24 @@ __global__ void __launch_bounds__(256) k_seg_pass(const unsigned long long* __re
     if (cb >= tiles_x) return;
     const uint4 sg = segs[g];
     const int col = cb + lane;
-    const bool has = col < tiles_x;
+    bool has = col < tiles_x;
+    uint32_t cur = 0, len = 0, base = 0;
+    if (kPart) {
+        has = has && (!mask || mask[static_cast<size_t>(sg.x) * tiles_x + col]);
+        const uint2 tr = has ? tile_ranges[static_cast<size_t>(sg.x) * tiles_x + col] : make_uint2(0u, 0u);
+        base = tr.x;
+        len = tr.y - tr.x;
+        cur = has ? cnt[static_cast<size_t>(g) * tiles_x + col] : 0u;  // position in the bin
+        has = has && cur < len;
+        // every column of this block already holds its list: nothing to do
+        if (!__any_sync(0xffffffffu, has)) return;
+    } else {
+        cur = has ? cnt[static_cast<size_t>(g) * tiles_x + col] : 0u;  // absolute cursor
+    }
     const int last = min(tiles_x, cb + 32) - 1;
-    uint32_t cur = has ? cnt[static_cast<size_t>(g) * tiles_x + col] : 0u;
-    for (uint32_t base = sg.y; base < sg.z; base += 32) {
-        const bool valid = base + lane < sg.z;
-        const unsigned long long e = valid ? row_list[base + lane] : 0ull;
+    for (uint32_t b0 = sg.y; b0 < sg.z; b0 += 32) {
+        const bool valid = b0 + lane < sg.z;
+        const unsigned long long e = valid ? row_list[b0 + lane] : 0ull;
         const int x0 = static_cast<int>((e >> 16) & 0xffffu);
         const int x1 = static_cast<int>(e & 0xffffu);
         const bool rel = valid && x0 <= last && x1 >= cb;
@@ -524,7 +583,14 @@ __global__ void __launch_bounds__(256) k_seg_pass(const unsigned long long* __re
                 m &= m - 1u;
                 const unsigned long long ej = __shfl_sync(0xffffffffu, e, j);
                 const int jx0 = static_cast<int>((ej >> 16) & 0xffffu), jx1 = static_cast<int>(ej & 0xffffu);
-                if (has && jx0 <= col && col <= jx1) list[cur++] = static_cast<uint32_t>(ej >> 32);
+                if (has && jx0 <= col && col <= jx1) {
+                    if (kPart) {
+                        if (cur < len) list[base + cur] = static_cast<uint32_t>(ej >> 32);
+                        ++cur;
+                    } else {
+                        list[cur++] = static_cast<uint32_t>(ej >> 32);
+                    }
+                }
             }
         } else {
             // dense: per column, a ballot gives the covering entries consecutive slots of that
@@ -532,11 +598,19 @@ __global__ void __launch_bounds__(256) k_seg_pass(const unsigned long long* __re
             const int lo = max(cb, __reduce_min_sync(0xffffffffu, rel ? x0 : INT_MAX));
             const int hi = min(last, __reduce_max_sync(0xffffffffu, rel ? x1 : INT_MIN));
             for (int c = lo; c <= hi; ++c) {
+                const int owner = c - cb;
+                if (kPart && !__shfl_sync(0xffffffffu, has ? 1 : 0, owner)) continue;  // (uniform)
                 const bool cov = rel && x0 <= c && c <= x1;
                 const uint32_t bal = __ballot_sync(0xffffffffu, cov);
-                const int owner = c - cb;
                 const uint32_t at = __shfl_sync(0xffffffffu, cur, owner);
-                if (cov) list[at + __popc(bal & ((1u << lane) - 1u))] = static_cast<uint32_t>(e >> 32);
+                const uint32_t pos = at + __popc(bal & ((1u << lane) - 1u));
+                if (kPart) {
+                    const uint32_t clen = __shfl_sync(0xffffffffu, len, owner);
+                    const uint32_t cbase = __shfl_sync(0xffffffffu, base, owner);
+                    if (cov && pos < clen) list[cbase + pos] = static_cast<uint32_t>(e >> 32);
+                } else if (cov) {
+                    list[pos] = static_cast<uint32_t>(e >> 32);
+                }
                 if (lane == owner) cur += __popc(bal);
             }
         }
@@ -578,8 +652,8 @@ __global__ void __launch_bounds__(256) k_seg_count(const unsigned long long* __r
     }
 }
 
-// per (row, column): exclusive scan of the segment counts over the row's segments, offset by
-// the tile's list start
+// per (row, column): exclusive scan of the segment counts over the row's segments: each
+// segment's first list cursor (or position in the bin)
 __global__ void k_seg_scan(const uint4* __restrict__ segs, const uint32_t* __restrict__ nseg,
                            const uint2* __restrict__ tile_ranges, int tiles_x, int tiles_y,
                            uint32_t* __restrict__ cnt) {
@@ -593,7 +667,8 @@ __global__ void k_seg_scan(const uint4* __restrict__ segs, const uint32_t* __res
         const uint32_t mid = (lo + hi) / 2;
         if (static_cast<int>(segs[mid].x) < y) lo = mid + 1; else hi = mid;
     }
-    uint32_t run = tile_ranges[i].x;
+    // absolute list cursors, or (tile_ranges null: depth-prefix binning) positions in the bin
+    uint32_t run = tile_ranges ? tile_ranges[i].x : 0u;
     for (uint32_t g = lo; g < G && static_cast<int>(segs[g].x) == y; ++g) {
         const size_t k = static_cast<size_t>(g) * tiles_x + x;
         const uint32_t c = cnt[k];
@@ -797,13 +872,22 @@ void launch_bin_hist(const int4* rects, uint32_t V, int tiles_x, int* diff,
     k_bin_hist<<<blocks_for(V, 256), 256, 0, s>>>(rects, V, tiles_x, diff, rows);
 }
 
-void launch_bin_scan(int* diff, int tiles_x, int tiles_y, uint2* ranges, cudaStream_t s) {
-    k_bin_scan<<<1, kScanThreads, 0, s>>>(diff, tiles_x, tiles_y, ranges);
+void launch_bin_scan(int* diff, int tiles_x, int tiles_y, uint2* ranges, cudaStream_t s,
+                     const uint8_t* mask, unsigned long long* total, uint32_t cap, uint8_t* trunc) {
+    k_bin_scan<<<1, kScanThreads, 0, s>>>(diff, tiles_x, tiles_y, ranges, mask, total, cap, trunc);
+}
+
+void launch_redo_items(const uint32_t* incomplete, uint32_t n, uint32_t view, int raster_tiles_x,
+                       int per_bin, int tiles_x, uint2* items, uint8_t* mask, cudaStream_t s) {
+    if (n == 0) return;
+    k_redo_items<<<blocks_for(n, 256), 256, 0, s>>>(incomplete, n, view, raster_tiles_x, per_bin,
+                                                    tiles_x, items, mask);
 }
 
 void launch_row_scatter(const unsigned long long* row_list, const uint2* row_ranges,
                         const uint2* tile_ranges, int tiles_x, int tiles_y, uint64_t R, uint4* segs,
-                        uint32_t* nseg, uint32_t* cnt, uint32_t* list, cudaStream_t s) {
+                        uint32_t* nseg, uint32_t* cnt, uint32_t* list, cudaStream_t s,
+                        const uint8_t* mask, bool part) {
     if (R == 0) return;
     const uint64_t gmax = R / kSeg + static_cast<uint64_t>(tiles_y) + 1;
     k_row_segs<<<1, 1024, 0, s>>>(row_ranges, tiles_y, segs, nseg);
@@ -813,8 +897,23 @@ void launch_row_scatter(const unsigned long long* row_list, const uint2* row_ran
     k_seg_count<<<static_cast<unsigned>(gmax), 256, sizeof(int) * (tiles_x + 1), s>>>(
         row_list, segs, nseg, tiles_x, cnt);
     k_seg_scan<<<blocks_for(static_cast<uint64_t>(tiles_x) * tiles_y, 256), 256, 0, s>>>(
-        segs, nseg, tile_ranges, tiles_x, tiles_y, cnt);
-    k_seg_pass<<<grid, 32 * warps, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list);
+        segs, nseg, part ? nullptr : tile_ranges, tiles_x, tiles_y, cnt);
+    if (part)
+        k_seg_pass<true><<<grid, 32 * warps, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list, mask, tile_ranges);
+    else
+        k_seg_pass<false><<<grid, 32 * warps, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list, nullptr, nullptr);
+}
+
+// k_seg_pass alone over the segments of a previous launch_row_scatter (the redo pass of
+// depth-prefix binning: the same row list and per-segment positions, other ranges / mask)
+void launch_seg_pass(const unsigned long long* row_list, const uint2* tile_ranges, int tiles_x,
+                     uint64_t G, const uint4* segs, const uint32_t* nseg, const uint32_t* cnt,
+                     uint32_t* list, const uint8_t* mask, cudaStream_t s) {
+    if (G == 0) return;
+    const int blocks = (tiles_x + 31) / 32;
+    const int warps = std::min(8, blocks);
+    const dim3 grid(static_cast<unsigned>(G), static_cast<unsigned>((blocks + warps - 1) / warps));
+    k_seg_pass<true><<<grid, 32 * warps, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list, mask, tile_ranges);
 }
 
 uint64_t row_scatter_segments(uint64_t R, int tiles_y) {

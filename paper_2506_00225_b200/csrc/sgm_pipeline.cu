@@ -12,6 +12,8 @@
 //   5. k_reduce_scores (score) / planes already written (render)
 // Views whose pair lists do not fit the scratch budget together are split into
 // sub-batches; results do not depend on the split (per-view work is independent).
+#include <cstdlib>
+
 #include "sgm_ctx.h"
 
 namespace sgm {
@@ -56,42 +58,55 @@ unsigned tile_bits(uint64_t tiles) {
 }
 
 
-// Bins one view (step 3). Writes ranges / sorted list / packed into the per-view
-// slices and returns via the slice pointers. vals/keys hold the compacted (z, idx).
-static void bin_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const CamParams& cam,
-              const OptParams& o, const PoseParams* d_pose, uint32_t* keys, uint32_t* vals,
-              uint32_t V, uint64_t P, uint64_t R, const uint32_t* d_V, const unsigned long long* d_R,
-              PackedSplat* packed, uint4* bounds, uint32_t* list, uint2* ranges, int bin_tiles) {
-    CK(cudaMemsetAsync(ranges, 0, sizeof(uint2) * bin_tiles, s));
+// K2 (after the sub-batch's depth sort) + K3 pack of one view: runs of equal fp32 depth keys
+// fixed by the full key, PackedSplat / bounds / tile rectangles per depth rank.
+static void pack_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const CamParams& cam,
+                      const OptParams& o, const PoseParams* d_pose, const uint32_t* keys,
+                      uint32_t* vals, uint32_t V, PackedSplat* packed, uint4* bounds) {
     if (V == 0) return;
-    // K2: depth rank. The (fp32 depth key, index) pairs arrive sorted by the sub-batch's
-    // hand-written radix sort (sgm_sort.cu, run_views); runs of equal keys are fixed here
-    const uint32_t* skey = keys;
-    uint32_t* sval = vals;
-    (void)d_V;
-    launch_tiefix(map->dev, d_pose, cam, o, skey, sval, V, s);
-    launch_pack(map->dev, d_pose, cam, o, map->groups, sval, V, packed,
+    launch_tiefix(map->dev, d_pose, cam, o, keys, vals, V, s);
+    launch_pack(map->dev, d_pose, cam, o, map->groups, vals, V, packed,
                 ctx->counts.as<unsigned long long>(), ctx->rects.as<int4>(), bounds, s);
     ctx->stats.kernel_launches += (V >= 2 ? 1 : 0) + 1;
-    // keep the sorted indices for sgm_last_projections
-    if (sval != vals) CK(cudaMemcpyAsync(vals, sval, 4ull * V, cudaMemcpyDeviceToDevice, s));
-    if (P == 0) return;
-    // K3 (row-bucketed, no sort of the P pairs): tile ranges from the rectangles' 2D
-    // difference array; each tile row's ranks in rank order (R = sum of rows spanned pairs,
-    // stably sorted by row); then one CTA per tile row scatters its ranks into the tile lists
-    // in rank order (sgm_kernels.cu)
+}
+
+// K3 counts over the ranks < Ve (a depth prefix when Ve < V): tile ranges from the
+// rectangles' 2D difference array (bins outside `mask` empty; total pairs to d_total), and
+// the row-pair offsets roff[0..Ve] (roff[Ve] = the prefix's row pairs).
+static void bin_counts(sgm_ctx* ctx, cudaStream_t s, const OptParams& o, uint32_t Ve, uint2* ranges,
+                       int bin_tiles, const uint8_t* mask, unsigned long long* d_total,
+                       uint32_t cap = 0xffffffffu, uint8_t* trunc = nullptr) {
+    CK(cudaMemsetAsync(ranges, 0, sizeof(uint2) * bin_tiles, s));
+    if (Ve == 0) {
+        if (d_total) CK(cudaMemsetAsync(d_total, 0, 8, s));
+        CK(cudaMemsetAsync(ctx->offsets.p, 0, 8, s));
+        return;
+    }
     const int X = o.tiles_x + 1, Y = o.tiles_y + 1;
     int* diff = ctx->bdiff.as<int>();
     CK(cudaMemsetAsync(diff, 0, sizeof(int) * X * Y, s));
     unsigned long long* rows = ctx->counts.as<unsigned long long>();
     unsigned long long* roff = ctx->offsets.as<unsigned long long>();
-    launch_bin_hist(ctx->rects.as<int4>(), V, o.tiles_x, diff, rows, s);
-    launch_bin_scan(diff, o.tiles_x, o.tiles_y, ranges, s);
-    CK(cudaMemsetAsync(rows + V, 0, sizeof(unsigned long long), s));
-    exclusive_scan_u64<unsigned long long>(rows, V + 1, roff, ctx->scan_tmp.as<unsigned long long>(), s);
+    launch_bin_hist(ctx->rects.as<int4>(), Ve, o.tiles_x, diff, rows, s);
+    launch_bin_scan(diff, o.tiles_x, o.tiles_y, ranges, s, mask, d_total, cap, trunc);
+    CK(cudaMemsetAsync(rows + Ve, 0, sizeof(unsigned long long), s));
+    exclusive_scan_u64<unsigned long long>(rows, Ve + 1, roff, ctx->scan_tmp.as<unsigned long long>(), s);
+    ctx->stats.kernel_launches += 2 + 3;
+}
+
+// K3 lists (row-bucketed, no sort of the P pairs) over the ranks < Ve: the (row, rank) pairs
+// (R of them, d_R on the device) in rank order, stably sorted by row; then per row segment a
+// warp scatters its ranks into the tile lists in rank order (sgm_kernels.cu). Bins outside
+// `mask` get no entries.
+static const unsigned long long* bin_lists(sgm_ctx* ctx, cudaStream_t s, const OptParams& o,
+                                           uint32_t Ve, uint64_t R, const unsigned long long* d_R,
+                                           uint32_t* list, const uint2* ranges, const uint8_t* mask,
+                                           bool part = false) {
+    if (R == 0) return nullptr;
+    const unsigned long long* roff = ctx->offsets.as<unsigned long long>();
     uint32_t* rk = ctx->tkeys.as<uint32_t>();
     unsigned long long* rv = ctx->rvals.as<unsigned long long>();
-    launch_emit_rows(roff, ctx->rects.as<int4>(), V, R, rk, rv, s);
+    launch_emit_rows(roff, ctx->rects.as<int4>(), Ve, R, rk, rv, s);
     // each tile row's (row, rank) pairs in rank order: a stable sort on the row key
     const int rbits = static_cast<int>(tile_bits(static_cast<uint64_t>(o.tiles_y)));
     const bool ralt = radix_sort_pairs<unsigned long long, unsigned long long>(
@@ -99,15 +114,140 @@ static void bin_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const Cam
         rbits, ctx->sort_tmp.as<uint32_t>(), s);
     const uint32_t* qk = ralt ? ctx->tkeys_alt.as<uint32_t>() : rk;
     const unsigned long long* qv = ralt ? ctx->tvals_alt.as<unsigned long long>() : rv;
-    ctx->stats.kernel_launches += radix_sort_launches(rbits) + 3;  // + the 3-kernel scan
+    ctx->stats.kernel_launches += radix_sort_launches(rbits);
     uint2* rranges = ctx->rranges.as<uint2>();
     CK(cudaMemsetAsync(rranges, 0, sizeof(uint2) * o.tiles_y, s));
     launch_ranges(qk, R, rranges, s);
-    const uint64_t G = row_scatter_segments(R, o.tiles_y);  // buffers sized per group (run_views)
+    const uint64_t G = row_scatter_segments(R, o.tiles_y);  // buffers sized by the caller
     launch_row_scatter(qv, rranges, ranges, o.tiles_x, o.tiles_y, R,
                        ctx->segs.as<uint4>(), reinterpret_cast<uint32_t*>(ctx->segs.as<char>() + sizeof(uint4) * G),
-                       ctx->segcnt.as<uint32_t>(), list, s);
+                       ctx->segcnt.as<uint32_t>(), list, s, mask, part);
     ctx->stats.kernel_launches += 7;
+    return qv;
+}
+
+// Bins one view (step 3): pack, then the full bins (every rank).
+static void bin_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const CamParams& cam,
+                     const OptParams& o, const PoseParams* d_pose, uint32_t* keys, uint32_t* vals,
+                     uint32_t V, uint64_t P, uint64_t R, const unsigned long long* d_R,
+                     PackedSplat* packed, uint4* bounds, uint32_t* list, uint2* ranges, int bin_tiles) {
+    pack_view(ctx, s, map, cam, o, d_pose, keys, vals, V, packed, bounds);
+    if (V == 0 || P == 0) {
+        CK(cudaMemsetAsync(ranges, 0, sizeof(uint2) * bin_tiles, s));
+        return;
+    }
+    bin_counts(ctx, s, o, V, ranges, bin_tiles, nullptr, nullptr);
+    bin_lists(ctx, s, o, V, R, d_R, list, ranges, nullptr);
+}
+
+// Reserves the row-pair scratch of the binning for up to R row pairs.
+static void reserve_rows(sgm_ctx* ctx, const OptParams& o, uint64_t R, size_t NS, int kSub) {
+    const uint64_t r = std::max<uint64_t>(R, 1);
+    CK(ctx->tkeys.reserve(4 * r));
+    CK(ctx->tkeys_alt.reserve(4 * r));
+    CK(ctx->tvals_alt.reserve(8 * r));
+    CK(ctx->rvals.reserve(8 * r));
+    CK(ctx->sort_tmp.reserve(std::max(radix_sort_scratch_bytes(r, 1), radix_sort_scratch_bytes(NS, kSub))));
+    CK(ctx->scan_tmp.reserve(exclusive_scan_scratch_bytes(NS + 1)));
+    // row-scatter segments (reserved before the launches: a reallocation synchronises)
+    const uint64_t G = row_scatter_segments(r, o.tiles_y);
+    CK(ctx->segs.reserve(sizeof(uint4) * G + 16));
+    CK(ctx->segcnt.reserve(sizeof(uint32_t) * G * o.tiles_x));
+}
+
+// A view is "dense" when its bins average more than this many entries: its tile lists are
+// then built from each bin's first entries only (depth-prefix binning, score_dense_view).
+constexpr uint64_t kDenseAvg = 4096;
+constexpr uint32_t kPrefixCap = 256;  // entries per bin of the first pass
+
+// Scores one dense view (its own group). The raster's early exit (:312) usually consumes a
+// short prefix of every bin, so each bin first gets only its first kPrefixCap entries (a
+// prefix of its full list, in the same rank order; the row list, its sort and the
+// per-segment positions are built once), flagged when that drops entries. A block that
+// exhausts a flagged list with pixels still open is reported incomplete; the second pass
+// writes the full lists of those bins only (same row list, masked) and redoes those tiles.
+// A block that completes inside its prefix stops where it would have stopped on the full
+// list, so every tile's result is the full-list result.
+static void score_dense_view(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam,
+                             const OptParams& o, int v, uint32_t V, uint64_t P, uint64_t R,
+                             const unsigned long long* d_R, size_t NS, int bin_tiles, int rtx,
+                             int rtiles, int kSub, ViewDesc d, const RasterParams& rp0) {
+    cudaStream_t s = ctx->stream;
+    const PoseParams* d_pose = ctx->poses.as<PoseParams>() + v;
+    if (ctx->profiling) CK(cudaEventRecord(ctx->ev_r[0], s));  // (raster_ms: binning included)
+    pack_view(ctx, s, map, cam, o, d_pose, ctx->keys.as<uint32_t>() + NS * v,
+              const_cast<uint32_t*>(d.order), V, const_cast<PackedSplat*>(d.packed),
+              const_cast<uint4*>(d.bounds));
+    CK(ctx->franges.reserve(sizeof(uint2) * bin_tiles));
+    CK(ctx->trunc8.reserve(bin_tiles + 16));
+    CK(ctx->bmask.reserve(bin_tiles + 16));
+    CK(ctx->incomplete.reserve(4 * static_cast<size_t>(rtiles) + 16));
+    CK(ctx->redo.reserve(sizeof(uint2) * rtiles + 16));
+    CK(ctx->dense_tot.reserve(64));
+    uint2* ranges = const_cast<uint2*>(d.ranges);
+    unsigned long long* d_tot = ctx->dense_tot.as<unsigned long long>();
+    uint32_t* n_inc = reinterpret_cast<uint32_t*>(d_tot + 2);
+    // pass 1: every bin's first kPrefixCap entries
+    bin_counts(ctx, s, o, V, ranges, bin_tiles, nullptr, d_tot, kPrefixCap, ctx->trunc8.as<uint8_t>());
+    unsigned long long Pe = 0;
+    CK(cudaMemcpyAsync(&Pe, d_tot, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(ctx->tvals.reserve(4 * std::max<unsigned long long>(Pe, 1)));
+    reserve_rows(ctx, o, R, NS, kSub);
+    const unsigned long long* rowlist =
+        bin_lists(ctx, s, o, V, R, d_R, ctx->tvals.as<uint32_t>(), ranges, nullptr, true);
+    d.list = ctx->tvals.as<uint32_t>();
+    CK(cudaMemsetAsync(n_inc, 0, 4, s));
+    CK(cudaMemcpyAsync(ctx->views.p, &d, sizeof(ViewDesc), cudaMemcpyHostToDevice, s));
+    RasterParams rp = rp0;
+    rp.views = ctx->views.as<ViewDesc>();
+    rp.trunc = ctx->trunc8.as<uint8_t>();
+    rp.incomplete = ctx->incomplete.as<uint32_t>();
+    rp.n_incomplete = n_inc;
+    launch_raster_score(rp, 1, s);
+    CK(cudaGetLastError());
+    ctx->stats.kernel_launches += 1;
+    ctx->stats.raster_launches += 1;
+    uint32_t ninc = 0;
+    CK(cudaMemcpyAsync(&ninc, n_inc, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (ninc > 0 && rowlist) {
+        // pass 2: the full lists of the incomplete tiles' bins, and those tiles again
+        CK(cudaMemsetAsync(ctx->bmask.p, 0, bin_tiles, s));
+        launch_redo_items(ctx->incomplete.as<uint32_t>(), ninc, 0, rtx, o.ts / kTile, o.tiles_x,
+                          ctx->redo.as<uint2>(), ctx->bmask.as<uint8_t>(), s);
+        const uint8_t* mask = ctx->bmask.as<uint8_t>();
+        uint2* full = ctx->franges.as<uint2>();
+        const int X = o.tiles_x + 1, Y = o.tiles_y + 1;
+        CK(cudaMemsetAsync(ctx->bdiff.p, 0, sizeof(int) * X * Y, s));
+        launch_bin_hist(ctx->rects.as<int4>(), V, o.tiles_x, ctx->bdiff.as<int>(),
+                        ctx->counts.as<unsigned long long>(), s);
+        launch_bin_scan(ctx->bdiff.as<int>(), o.tiles_x, o.tiles_y, full, s, mask, d_tot);
+        unsigned long long P2 = 0;
+        CK(cudaMemcpyAsync(&P2, d_tot, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (P2 >= (1ull << 32)) fail(SGM_ERR_UNSUPPORTED, "view has %llu tile pairs (>= 2^32)", P2);
+        CK(ctx->list2.reserve(4 * std::max<unsigned long long>(P2, 1)));
+        const uint64_t G = row_scatter_segments(R, o.tiles_y);
+        launch_seg_pass(rowlist, full, o.tiles_x, G, ctx->segs.as<uint4>(),
+                        reinterpret_cast<uint32_t*>(ctx->segs.as<char>() + sizeof(uint4) * G),
+                        ctx->segcnt.as<uint32_t>(), ctx->list2.as<uint32_t>(), mask, s);
+        d.list = ctx->list2.as<uint32_t>();
+        d.ranges = full;
+        CK(cudaMemcpyAsync(ctx->views.p, &d, sizeof(ViewDesc), cudaMemcpyHostToDevice, s));
+        rp.trunc = nullptr;
+        rp.incomplete = nullptr;
+        rp.n_incomplete = nullptr;
+        rp.item_list = ctx->redo.as<uint2>();
+        rp.n_item_list = static_cast<int>(ninc);
+        launch_raster_score(rp, 1, s);
+        CK(cudaGetLastError());
+        ctx->stats.kernel_launches += 6;
+        ctx->stats.raster_launches += 1;
+    }
+    if (ctx->profiling) CK(cudaEventRecord(ctx->ev_r[1], s));
+    // the view's pairs as binned by the reference (statistics)
+    ctx->stats.pairs += P;
 }
 
 // Runs n views. Score mode writes n_missing/entropy_sum (host); render mode (n == 1)
@@ -191,36 +331,45 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
         std::vector<uint32_t> V(hv, hv + nb);
         std::vector<uint64_t> P(hp, hp + nb);
         std::vector<uint64_t> R(hp + nb, hp + 2 * nb);  // (row, rank) pairs of the binning
-        for (int v = 0; v < nb; ++v)
-            if (P[v] >= (1ull << 32)) fail(SGM_ERR_UNSUPPORTED, "view has %llu tile pairs (>= 2^32)",
-                                          static_cast<unsigned long long>(P[v]));
 
-        // groups of views whose pair lists fit the budget together
+        // groups of views whose pair lists fit the budget together; a dense view of the plain
+        // score mode is a group of its own (depth-prefix binning, score_dense_view)
         const uint64_t pair_budget = (uint64_t(8) << 30) / 4;  // u32 list entries
+        // Depth-prefix binning serves the views whose full lists exceed the list budget (or
+        // 2^32 pairs). It is exact but not faster than full bins that fit (the binning of a
+        // full view overlaps the previous raster; the prefix path is synchronous), so full
+        // bins stay the default below the budget. SGM_PREFIX_BINNING=1 forces it for every
+        // view averaging > kDenseAvg entries per bin, =0 turns it off.
+        const char* pb = std::getenv("SGM_PREFIX_BINNING");
+        const int prefix_mode = pb ? (pb[0] == '0' ? 0 : 2) : 1;
+        auto dense = [&](int v) {
+            if (prefix_mode == 0 || mode != Mode::Score || fk != Fisher::None) return false;
+            if (P[v] <= kDenseAvg * static_cast<uint64_t>(bin_tiles)) return false;
+            return prefix_mode == 2 || P[v] > pair_budget;
+        };
         int v0 = 0;
         while (v0 < nb) {
             int v1 = v0;
             uint64_t sumP = 0, maxP = 0;
-            while (v1 < nb && (v1 == v0 || sumP + P[v1] <= pair_budget)) {
+            while (v1 < nb && (v1 == v0 || (sumP + P[v1] <= pair_budget && !dense(v1) && !dense(v0)))) {
                 sumP += P[v1];
                 maxP = std::max<uint64_t>(maxP, P[v1]);
                 ++v1;
             }
+            const bool dense_group = dense(v0);
+            for (int v = v0; v < v1; ++v)  // (a dense view's lists are built a prefix at a time)
+                if (!dense_group && P[v] >= (1ull << 32))
+                    fail(SGM_ERR_UNSUPPORTED, "view has %llu tile pairs (>= 2^32)",
+                         static_cast<unsigned long long>(P[v]));
             uint64_t maxR = 1;
             for (int v = v0; v < v1; ++v) maxR = std::max<uint64_t>(maxR, R[v]);
-            CK(ctx->tvals.reserve(4 * std::max<uint64_t>(sumP, 1)));
-            CK(ctx->tkeys.reserve(4 * maxR));
-            CK(ctx->tkeys_alt.reserve(4 * maxR));
-            CK(ctx->tvals_alt.reserve(8 * maxR));
-            CK(ctx->rvals.reserve(8 * maxR));
-            CK(ctx->sort_tmp.reserve(std::max(radix_sort_scratch_bytes(maxR, 1),
-                                              radix_sort_scratch_bytes(NS, kSub))));
-            CK(ctx->scan_tmp.reserve(exclusive_scan_scratch_bytes(NS + 1)));
-            // row-scatter segments of the largest view (reserved here, not between the
-            // views' binning launches: a reallocation would synchronise the device)
-            const uint64_t maxG = row_scatter_segments(maxR, o.tiles_y);
-            CK(ctx->segs.reserve(sizeof(uint4) * maxG + 16));
-            CK(ctx->segcnt.reserve(sizeof(uint32_t) * maxG * o.tiles_x));
+            if (!dense_group) {
+                CK(ctx->tvals.reserve(4 * std::max<uint64_t>(sumP, 1)));
+                reserve_rows(ctx, o, maxR, NS, kSub);
+            } else {
+                CK(ctx->sort_tmp.reserve(radix_sort_scratch_bytes(NS, kSub)));
+                CK(ctx->scan_tmp.reserve(exclusive_scan_scratch_bytes(NS + 1)));
+            }
             // descriptors for the whole group (list offsets known from the counts)
             ViewDesc* hvd = ctx->h_views.as<ViewDesc>();
             uint64_t list_off = 0;
@@ -248,9 +397,9 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                             ? ctx->rcbuf.as<double>() + 4ull * cam.W * cam.H * static_cast<size_t>(v)
                             : nullptr;
                 hvd[v - v0] = d;
-                list_off += P[v];
+                list_off += dense_group ? 0 : P[v];
                 ctx->stats.visible += V[v];
-                ctx->stats.pairs += P[v];
+                if (!dense_group) ctx->stats.pairs += P[v];
             }
             const int ngroup = v1 - v0;
             CK(cudaMemcpyAsync(ctx->views.p, hvd, sizeof(ViewDesc) * ngroup, cudaMemcpyHostToDevice, s));
@@ -278,12 +427,18 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                     if (alt) fail(SGM_ERR_CUDA, "depth sort: odd pass count");  // 4 passes: in place
                     ctx->stats.kernel_launches += maxV ? radix_sort_launches(32) : 0;
                 }
+                if (dense_group) {  // one view: depth-prefix binning, synchronous on s
+                    CK(cudaStreamSynchronize(sb));
+                    score_dense_view(ctx, map, cam, o, s0, V[s0], P[s0], R[s0],
+                                     ctx->pcount.as<unsigned long long>() + nb + s0, NS, bin_tiles,
+                                     rtx, rtiles, kSub, hvd[0], rp);
+                    continue;
+                }
                 for (int v = s0; v < s1; ++v) {
                     const ViewDesc& d = hvd[v - v0];
                     bin_view(ctx, sb, map, cam, o, ctx->poses.as<PoseParams>() + v,
                              ctx->keys.as<uint32_t>() + NS * v, const_cast<uint32_t*>(d.order), V[v],
-                             P[v], R[v], ctx->vcount.as<uint32_t>() + v,
-                             ctx->pcount.as<unsigned long long>() + nb + v,
+                             P[v], R[v], ctx->pcount.as<unsigned long long>() + nb + v,
                              const_cast<PackedSplat*>(d.packed), const_cast<uint4*>(d.bounds),
                              const_cast<uint32_t*>(d.list), const_cast<uint2*>(d.ranges), bin_tiles);
                 }

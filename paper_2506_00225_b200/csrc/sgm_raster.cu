@@ -109,7 +109,9 @@ __device__ __forceinline__ int px_row(int q) { return (q >> 5) * 4 + ((q >> 2) &
 // the next block's first batch while the compute warps run the current block's epilogue.
 // (Not a persistent grid: CTAs still retire often enough for the prioritised binning
 // stream's kernels to take their slots.)
-template <bool kRender, bool kDup, bool kAniso, bool kRc = false, int kOcc = 3>
+// kItems: the depth-prefix binning launch (explicit item list, truncated-list flags and the
+// incomplete-tile report); a separate instantiation, so the common launches carry none of it.
+template <bool kRender, bool kDup, bool kAniso, bool kRc = false, int kOcc = 3, bool kItems = false>
 __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int C = p.map.C;
@@ -144,6 +146,8 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     __shared__ int scnt[2][3];  // block parity q: entries of batch b in scnt[q][b % 3]
     __shared__ uint32_t slive[2];  // batch b: entries with a nonzero weight at some pixel
     __shared__ int s_item;
+    __shared__ uint8_t s_trunc[2];  // the block's bin list is a strict prefix (depth-prefix binning)
+    __shared__ int s_exh;           // the block's list ran out with pixels still open
     __shared__ double red_d[2];                        // epilogue: the two pixel warps' entropy
     __shared__ unsigned long long red_u[2 + kWarps];   // their missing counts, then K per warp
 
@@ -225,12 +229,21 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         ++nclaimed;
         if (lane == 0) s_item = it;
         if (it >= total) return;
-        const int view = it / tpv, tile = it - view * tpv;
+        int view, tile;
+        if (kItems && p.item_list) {
+            const uint2 vt = p.item_list[it];
+            view = static_cast<int>(vt.x);
+            tile = static_cast<int>(vt.y);
+        } else {
+            view = it / tpv;
+            tile = it - view * tpv;
+        }
         const ViewDesc* v = p.views + view;
         const int tbx = tile % p.raster_tiles_x, tby = tile / p.raster_tiles_x;
         const int bin = ((tby * kTile) / p.opt.ts) * p.opt.tiles_x + (tbx * kTile) / p.opt.ts;
         const uint2 rg = v->ranges[bin];
         if (lane == 0) {
+            if (kItems) s_trunc[ls.q] = p.trunc ? p.trunc[bin] : 0;
             ls.list = v->list;
             ls.packed = v->packed;
             ls.bounds = v->bounds;
@@ -253,11 +266,20 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         __syncwarp();
         claim();
     }
+    if (kItems && t == 0) s_exh = 0;
     __syncthreads();
     for (int q = 0;; q ^= 1) {  // q: parity of this block (the loader's lq matches it)
         const int item = s_item;
         if (item >= total) break;
-        const int view = item / tpv, tile = item - view * tpv;
+        int view, tile;
+        if (kItems && p.item_list) {
+            const uint2 vt = p.item_list[item];
+            view = static_cast<int>(vt.x);
+            tile = static_cast<int>(vt.y);
+        } else {
+            view = item / tpv;
+            tile = item - view * tpv;
+        }
         const ViewDesc vd = p.views[view];
         const int bx = tile % p.raster_tiles_x, by = tile / p.raster_tiles_x;
         const int x = bx * kTile + px_col(px);
@@ -295,7 +317,10 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
             // of the whole block (:312 for every pixel) decided on the previous batch's votes
             if (__syncthreads_and(mine)) break;
             const int n = scnt[q][b % 3];
-            if (n == 0) break;  // the bin is exhausted
+            if (n == 0) {  // the bin is exhausted with pixels still open
+                if (kItems && t == 0) s_exh = 1;
+                break;
+            }
             if (loader) {  // batch b+1 in flight while the compute warps blend batch b
                 if (b == 0) fill(1);
                 if (scnt[q][(b + 1) % 3] > 0) issue(b + 1);
@@ -619,6 +644,13 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                     vd.ent_partial[tile] = red_d[0] + red_d[1];
                     vd.miss_partial[tile] = static_cast<uint32_t>(red_u[0] + red_u[1]);
                 }
+                // a truncated list ran out before every pixel exited: the tile is redone
+                // from a longer depth prefix (its partials above are then overwritten)
+                if (kItems) {
+                    if (s_exh && s_trunc[q] && p.incomplete)
+                        p.incomplete[atomicAdd(p.n_incomplete, 1u)] = static_cast<uint32_t>(tile);
+                    s_exh = 0;
+                }
                 unsigned long long k = 0;
 #pragma unroll
                 for (int w = 0; w < kWarps; ++w) k += red_u[2 + w];
@@ -646,19 +678,32 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
 template <bool kRender, bool kDup, bool kAniso, bool kRc = false>
 void launch_t(const RasterParams& p0, int n_views, cudaStream_t s) {
     RasterParams p = p0;
-    p.n_items = p.tiles_per_view * n_views;
+    p.n_items = p.item_list ? p.n_item_list : p.tiles_per_view * n_views;
+    if (p.n_items == 0) return;
     const size_t smem = static_cast<size_t>(make_layout(p.map.C, p.map.kpad, kRender, kRc).total);
     // four CTAs per SM when four fit in shared memory (228 KB, 1 KB reserved per CTA)
     // (score mode only: the render and rc variants would spill at the 4-CTA register budget)
     const bool four = !kRender && !kRc && smem + 2048 <= 228 * 1024 / 4;
-    auto kern = k_raster<kRender, kDup, kAniso, kRc, 3>;
-    if constexpr (!kRender && !kRc)
-        if (four) kern = k_raster<kRender, kDup, kAniso, kRc, 4>;
     // (render: usually one view per launch, so shorter CTAs balance the last wave better)
     p.items_per_cta = kRender ? 2 : kItemsPerCta;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const int grid = (p.n_items + p.items_per_cta - 1) / p.items_per_cta;
-    kern<<<grid, kThreads, smem, s>>>(p);
+    if constexpr (!kRender && !kRc) {
+        if (p.item_list || p.trunc) {
+            cudaFuncSetAttribute(k_raster<kRender, kDup, kAniso, kRc, 3, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            k_raster<kRender, kDup, kAniso, kRc, 3, true><<<grid, kThreads, smem, s>>>(p);
+            return;
+        }
+        if (four) {
+            cudaFuncSetAttribute(k_raster<kRender, kDup, kAniso, kRc, 4, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            k_raster<kRender, kDup, kAniso, kRc, 4, false><<<grid, kThreads, smem, s>>>(p);
+            return;
+        }
+    }
+    cudaFuncSetAttribute(k_raster<kRender, kDup, kAniso, kRc, 3, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_raster<kRender, kDup, kAniso, kRc, 3, false><<<grid, kThreads, smem, s>>>(p);
 }
 
 }  // namespace

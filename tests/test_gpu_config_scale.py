@@ -149,3 +149,38 @@ def test_cfg4_prefix_decision_vs_reference(ctx, ref):
     gm = scenes.make_map(4, n=30_000)
     cam = scenes.CONFIGS[4].camera()
     _decision(ctx, ref, gm, cam, scenes.make_candidates(4, 16), np.array([0.5, 0.5, 0.5]))
+
+
+def _dense_scene():
+    """A dense-overlap scene (cfg4's cube and poses, 100k Gaussians, 240x136 px): bins average
+    several thousand entries, so scoring takes the depth-prefix binning path."""
+    from paper_2506_00225_b200.splatmap import CameraModel
+    gm = scenes.make_map(4, n=100_000)
+    cam = CameraModel(240, 136, 0, 0, 120.0, 120.0, 119.5, 67.5)
+    return gm, cam, scenes.make_candidates(4, 6)
+
+
+def test_depth_prefix_binning_is_exact(ctx, monkeypatch):
+    """Dense views: scores from depth-prefix bins (with the redo of incomplete tiles) are
+    bit-identical to scores from the full bins."""
+    gm, cam, cands = _dense_scene()
+    poses = [c.camera_pose() for c in cands]
+    ctx.reset_stats()
+    monkeypatch.setenv("SGM_PREFIX_BINNING", "1")  # (by default only past the list budget)
+    nm, es = sgm.score_poses(gm, cam, poses, ctx=ctx)
+    st = ctx.stats()
+    assert st["pairs"] / len(poses) > 4096 * 30 * 17  # dense: > 4096 entries per bin
+    monkeypatch.setenv("SGM_PREFIX_BINNING", "0")
+    nm2, es2 = sgm.score_poses(gm, cam, poses, ctx=ctx)
+    assert np.array_equal(nm, nm2) and np.array_equal(es, es2)
+    assert len(set(nm.tolist())) > 1  # some views see the background (tiles that never exit)
+
+
+def test_dense_scene_scores_vs_reference(ctx, ref, monkeypatch):
+    monkeypatch.setenv("SGM_PREFIX_BINNING", "1")
+    gm, cam, cands = _dense_scene()
+    nm, es = sgm.score_poses(gm, cam, [c.camera_pose() for c in cands], ctx=ctx)
+    rnm, res = ref.refresh_scores(gm, cam, [c.position for c in cands],
+                                  [c.direction for c in cands], threads=6)
+    np.testing.assert_array_equal(nm, rnm)
+    np.testing.assert_allclose(es, res, rtol=ENT_RTOL, atol=0)
