@@ -153,9 +153,6 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
 
     // ---- loader state (in shared memory, so the compute warps carry no registers for it):
     // the block it stages for, the current one and then the next ----
-    const int qi = kpad / 8, qp = kpad / 2;
-    const int Q = 5 + qi + qp + ((kRender || kRc) ? 2 : 0);  // 16-byte chunks per Gaussian
-    const unsigned qmagic = static_cast<unsigned>((0x100000000ull + Q - 1) / Q);  // ceil(2^32 / Q)
     struct LoaderState {
         const uint32_t* list;
         const PackedSplat* packed;
@@ -166,39 +163,42 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         int q;  // parity of the loader's block
     };
     __shared__ LoaderState ls;
-    auto issue = [&](int b) {  // cp.async of batch b's rows into stage b & 1
-        unsigned char* sb = stg + (b & 1) * L.stage_bytes;
+    // batch b's records and rows into stage b & 1: per entry one bulk copy (TMA engine) per
+    // record (PackedSplat 64 B, channel-group bounds 16 B, class row 2 kpad B, probability
+    // row 8 kpad B, colour 32 B), completing on the stage's mbarrier (expected bytes armed
+    // first). The loader alone waits on it, before the batch barrier that hands the stage
+    // to the compute warps.
+    __shared__ __align__(8) unsigned long long s_mbar[2];
+    const unsigned entry_bytes = 64u + 16u + 10u * static_cast<unsigned>(kpad) +
+                                 ((kRender || kRc) ? 32u : 0u);
+    auto issue = [&](int b) {
+        const int st = b & 1;
+        unsigned char* sb = stg + st * L.stage_bytes;
         const int n = scnt[ls.q][b % 3];
-        const uint2* slot = rm + (b & 1) * kNB;
-        const PackedSplat* l_packed = ls.packed;
-        const uint4* l_bounds = ls.bounds;
-        for (int c = lane; c < n * Q; c += 32) {
-            // c / Q by a multiply-high (exact: c < kNB * Q is far below 2^32 / Q^2)
-            const int e = static_cast<int>(__umulhi(static_cast<unsigned>(c), qmagic));
-            int q = c - e * Q;
-            const uint2 v = slot[e];
-            const unsigned char* src;
-            unsigned char* dst;
-            if (q < 4) {
-                src = reinterpret_cast<const unsigned char*>(l_packed + v.x) + 16 * q;
-                dst = sb + L.st_packed + e * 64 + 16 * q;
-            } else if (q == 4) {
-                src = reinterpret_cast<const unsigned char*>(l_bounds + v.x);
-                dst = sb + L.st_bnd + e * 16;
-            } else if ((q -= 5) < qi) {
-                src = reinterpret_cast<const unsigned char*>(p.map.sem_idx + static_cast<size_t>(v.y) * kpad) + 16 * q;
-                dst = sb + L.st_idx + e * kpad * 2 + 16 * q;
-            } else if ((q -= qi) < qp) {
-                src = reinterpret_cast<const unsigned char*>(p.map.sem_prob + static_cast<size_t>(v.y) * kpad) + 16 * q;
-                dst = sb + L.st_prob + e * kpad * 8 + 16 * q;
-            } else {
-                q -= qp;
-                src = reinterpret_cast<const unsigned char*>(p.map.color4 + static_cast<size_t>(v.y) * 4) + 16 * q;
-                dst = sb + L.st_color + e * 32 + 16 * q;
-            }
-            cp_async16(dst, src);
+        const uint32_t bar = smem_addr(&s_mbar[st]);
+        if (lane == 0) mbar_expect_tx(bar, static_cast<unsigned>(n) * entry_bytes);
+        __syncwarp();
+        if (lane < n) {
+            const uint2 v = rm[st * kNB + lane];
+            // the stage was last read (generic proxy) before the barrier this warp passed
+            fence_proxy_async();
+            bulk_g2s(sb + L.st_packed + lane * 64, ls.packed + v.x, 64u, bar);
+            bulk_g2s(sb + L.st_bnd + lane * 16, ls.bounds + v.x, 16u, bar);
+            bulk_g2s(sb + L.st_idx + lane * kpad * 2, p.map.sem_idx + static_cast<size_t>(v.y) * kpad,
+                     2u * kpad, bar);
+            bulk_g2s(sb + L.st_prob + lane * kpad * 8, p.map.sem_prob + static_cast<size_t>(v.y) * kpad,
+                     8u * kpad, bar);
+            if (kRender || kRc)
+                bulk_g2s(sb + L.st_color + lane * 32, p.map.color4 + static_cast<size_t>(v.y) * 4, 32u, bar);
         }
-        cp_async_commit();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar);
+    };
+    unsigned mphase = 0;  // loader: parity bit per stage of the mbarrier phase to wait for
+    auto wait_batch = [&](int b) {
+        const int st = b & 1;
+        mbar_wait(smem_addr(&s_mbar[st]), (mphase >> st) & 1u);
+        mphase ^= 1u << st;
     };
     // Batches are formed by the loader warp two ahead (off the compute warps' path): the
     // next kNB entries of the bin (depth order) that can reach a pixel of this block. An
@@ -261,6 +261,11 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         if (scnt[ls.q][0] > 0) issue(0);
     };
 
+    if (t == 0) {
+        mbar_init(smem_addr(&s_mbar[0]), 1);
+        mbar_init(smem_addr(&s_mbar[1]), 1);
+    }
+    __syncthreads();
     if (loader) {
         if (lane == 0) ls.q = 0;
         __syncwarp();
@@ -312,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         double rcs[4] = {0.0, 0.0, 0.0, 0.0};  // this (segment, pixel) thread's colour / depth
         int mine = loader ? 1 : 0;  // vote that this thread's pixel is done (the block stops when all are)
         for (int b = 0;; ++b) {
-            cp_async_wait_all();
+            if (loader && scnt[q][b % 3] > 0) wait_batch(b);  // batch b's bulk copies landed
             // batch b landed; scnt for b+1 visible; W / bnd free; and the early termination
             // of the whole block (:312 for every pixel) decided on the previous batch's votes
             if (__syncthreads_and(mine)) break;
