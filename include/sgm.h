@@ -121,6 +121,18 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes,
                    const double* centers, const double* log_radii,
                    const double* opacity_logits, const double* colors,
                    const uint16_t* sem_indices, const double* sem_probs, sgm_map** out);
+/* The same, returning once the geometry is on its way: the colours and semantic rows are
+ * staged by a background thread and copied / class-sorted on the ctx's upload stream while
+ * the caller already queues work (preprocess and binning need only the geometry; the raster
+ * waits for the rows). The caller keeps the host arrays alive and unchanged until the first
+ * compute call on the map returns, or sgm_map_wait / sgm_map_release (sgm_map_upload is
+ * sgm_map_upload_async + sgm_map_wait). Index errors are reported here as by sgm_map_upload. */
+int sgm_map_upload_async(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes,
+                         const double* centers, const double* log_radii,
+                         const double* opacity_logits, const double* colors,
+                         const uint16_t* sem_indices, const double* sem_probs, sgm_map** out);
+/* Waits until every copy of an uploaded map is on the device. */
+int sgm_map_wait(sgm_ctx* ctx, sgm_map* map);
 void sgm_map_release(sgm_ctx* ctx, sgm_map* map);
 
 /* ---- anisotropic splat mode (NO reference counterpart, parity unpinned) ----

@@ -137,6 +137,9 @@ SIGNATURES = {
     "sgm_ctx_reset_stats": (C.c_int, [_vp]),
     "sgm_map_upload": (C.c_int, [_vp, C.c_uint64, C.c_int32, C.c_int32, _pd, _pd, _pd, _pd,
                                  _pu16, _pd, C.POINTER(_vp)]),
+    "sgm_map_upload_async": (C.c_int, [_vp, C.c_uint64, C.c_int32, C.c_int32, _pd, _pd, _pd, _pd,
+                                       _pu16, _pd, C.POINTER(_vp)]),
+    "sgm_map_wait": (C.c_int, [_vp, _vp]),
     "sgm_map_release": (None, [_vp, _vp]),
     "sgm_map_set_anisotropic": (C.c_int, [_vp, _vp, _pd, _pd]),
     "sgm_map_info": (C.c_int, [_vp, _vp, _pu64, _pi32, _pi32, _pi32]),

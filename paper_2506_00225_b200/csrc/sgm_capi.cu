@@ -41,6 +41,7 @@ int sgm_ctx_create(int device, sgm_ctx** out) {
         // binning kernels are small and latency-bound: give them priority so the
         // block scheduler slots them in as raster CTAs of the previous sub-batch retire
         CK(cudaStreamCreateWithPriority(&ctx->bin_stream, cudaStreamNonBlocking, prio_high));
+        CK(cudaStreamCreateWithFlags(&ctx->up_stream, cudaStreamNonBlocking));
         for (auto& ev : ctx->ev) CK(cudaEventCreate(&ev));
         CK(cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming));
         for (auto& ev : ctx->ev_binned) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -57,9 +58,16 @@ int sgm_ctx_create(int device, sgm_ctx** out) {
 
 void sgm_ctx_destroy(sgm_ctx* ctx) {
     if (!ctx) return;
+    if (ctx->rows_owner && ctx->rows_owner->rows_pending) {  // its staging uses ctx buffers
+        ctx->rows_owner->rows_thread.join();
+        ctx->rows_owner->rows_pending = false;
+    }
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->bin_stream) cudaStreamSynchronize(ctx->bin_stream);
+    if (ctx->up_stream) cudaStreamSynchronize(ctx->up_stream);
+    if (ctx->ev_hstage) cudaEventDestroy(ctx->ev_hstage);
+    if (ctx->ev_hrows) cudaEventDestroy(ctx->ev_hrows);
     for (auto& ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
     if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
@@ -69,10 +77,11 @@ void sgm_ctx_destroy(sgm_ctx* ctx) {
         if (ev) cudaEventDestroy(ev);
     for (auto& ev : ctx->ev_ring)
         if (ev) cudaEventDestroy(ev);
-    cudaStream_t s = ctx->stream, s2 = ctx->bin_stream;
+    cudaStream_t s = ctx->stream, s2 = ctx->bin_stream, s3 = ctx->up_stream;
     delete ctx;
     if (s) cudaStreamDestroy(s);
     if (s2) cudaStreamDestroy(s2);
+    if (s3) cudaStreamDestroy(s3);
 }
 
 const char* sgm_last_error(const sgm_ctx* ctx) {
@@ -107,9 +116,20 @@ int sgm_ctx_reset_stats(sgm_ctx* ctx) {
     return SGM_OK;
 }
 
-int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, const double* centers,
-                   const double* log_radii, const double* opacity_logits, const double* colors,
-                   const uint16_t* sem_indices, const double* sem_probs, sgm_map** out) {
+// Map upload in two phases (the e2e step's per-step cost: about 112 MB at cfg1, bound by
+// host memory bandwidth and the host libm activations):
+//   A (this call, a pool of host threads): geometry SoA with the activations radius =
+//     exp(log_r), alpha = sigmoid(logit) (reference libm, gaussian_map.hpp:36-37), the
+//     semantic-index validation (a failure is reported here) and duplicate-class detection;
+//     copied chunk by chunk on the ctx stream. Preprocess and binning need nothing else.
+//   B (a staging thread, returning before it ends): clamped colours and the raw rows into
+//     pinned memory, copied on the upload stream, then the class sort of the rows and the
+//     channel-group bounds there; ev_rows marks the end. The raster waits for it
+//     (map_ready), so phase B overlaps the preprocess and the first binning.
+int sgm_map_upload_async(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes,
+                         const double* centers, const double* log_radii,
+                         const double* opacity_logits, const double* colors,
+                         const uint16_t* sem_indices, const double* sem_probs, sgm_map** out) {
     sgm_map* m = nullptr;
     int rc = guard(ctx, [&] {
         need_ctx(ctx);
@@ -121,30 +141,49 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, con
         if (n > 0 && (!centers || !log_radii || !opacity_logits || !colors || !sem_indices || !sem_probs))
             fail(SGM_ERR_INVALID, "map: null array with n > 0");
         if (n >= (1ull << 32)) fail(SGM_ERR_UNSUPPORTED, "map: more than 2^32-1 Gaussians");
+        // the previous upload's staging thread and copies out of the pinned buffers
+        if (ctx->rows_owner) map_ready(ctx, ctx->rows_owner);
+        if (!ctx->ev_hstage) CK(cudaEventCreateWithFlags(&ctx->ev_hstage, cudaEventDisableTiming));
+        if (!ctx->ev_hrows) CK(cudaEventCreateWithFlags(&ctx->ev_hrows, cudaEventDisableTiming));
+        CK(cudaEventSynchronize(ctx->ev_hstage));
+        CK(cudaEventSynchronize(ctx->ev_hrows));
         const int C = num_classes + 1;
         const int kpad = (k + 7) / 8 * 8;
         m = new sgm_map();
         m->num_classes = num_classes;
         const size_t ns = std::max<uint64_t>(n, 1);
-        // pinned staging: geo SoA (5 ns), colour (4 ns), raw rows (k ns u16 + k ns f64)
         const size_t geo_b = 8 * 5 * ns, col_b = 8 * 4 * ns, idx_b = 2 * static_cast<size_t>(k) * ns,
                      prob_b = 8 * static_cast<size_t>(k) * ns;
-        CK(ctx->h_stage.reserve(geo_b + col_b + prob_b + idx_b + 64));
-        char* hs = ctx->h_stage.as<char>();
-        double* geo = reinterpret_cast<double*>(hs);
-        double* col = reinterpret_cast<double*>(hs + geo_b);
-        double* rprob = reinterpret_cast<double*>(hs + geo_b + col_b);
-        uint16_t* ridx = reinterpret_cast<uint16_t*>(hs + geo_b + col_b + prob_b);
-        // Host side (reference libm, gaussian_map.hpp:36-37) in kChunks chunks over a pool of
-        // threads; as soon as every thread has finished chunk c, its slices go to the GPU
-        // (async H2D), so the copies overlap the host work on the next chunks.
+        CK(ctx->h_stage.reserve(geo_b + 64));
+        CK(ctx->h_rows.reserve(col_b + prob_b + idx_b + 64));
+        double* geo = ctx->h_stage.as<double>();
+        char* hr = ctx->h_rows.as<char>();
+        double* col = reinterpret_cast<double*>(hr);
+        double* rprob = reinterpret_cast<double*>(hr + col_b);
+        uint16_t* ridx = reinterpret_cast<uint16_t*>(hr + col_b + prob_b);
+        cudaStream_t s = ctx->stream;
+        ctx->take(m->geo, geo_b);
+        ctx->take(m->color, col_b);
+        ctx->take(m->idx, 2 * ns * kpad);
+        ctx->take(m->prob, 8 * ns * kpad);
+        ctx->take(m->perm, 2 * ns * kpad);
+        ctx->take(m->gbnd, 16 * ns);
+        CK(m->geo.reserve(geo_b));
+        CK(m->color.reserve(col_b));
+        CK(m->idx.reserve(2 * ns * kpad));
+        CK(m->prob.reserve(8 * ns * kpad));
+        CK(m->perm.reserve(2 * ns * kpad));
+        CK(m->gbnd.reserve(16 * ns));
+        CK(ctx->upload_tmp.reserve(idx_b + prob_b + 64));
+        CK(cudaEventCreateWithFlags(&m->ev_rows, cudaEventDisableTiming));
         const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
         const unsigned nth = n > 65536 ? hw : 1;
         const unsigned kChunks = n > 65536 ? 8 : 1;
+        // ---- phase A: geometry + activations + index checks, chunk copies on s ----
         std::vector<int> bad(nth, -1), dup(nth, 0);
         std::unique_ptr<std::atomic<unsigned>[]> finished(new std::atomic<unsigned>[kChunks]);
         for (unsigned c = 0; c < kChunks; ++c) finished[c].store(0);
-        auto work = [&](unsigned w) {
+        auto work_a = [&](unsigned w) {
             std::vector<uint32_t> seen(static_cast<size_t>(C), 0xffffffffu);
             for (unsigned c = 0; c < kChunks; ++c) {
                 const uint64_t ca = n * c / kChunks, cb = n * (c + 1) / kChunks;
@@ -155,8 +194,6 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, con
                     geo[2 * ns + i] = centers[3 * i + 2];
                     geo[3 * ns + i] = std::exp(log_radii[i]);                      // radius()
                     geo[4 * ns + i] = 1.0 / (1.0 + std::exp(-opacity_logits[i]));  // sigmoid
-                    for (int q = 0; q < 3; ++q) col[4 * i + q] = std::clamp(colors[3 * i + q], 0.0, 1.0);
-                    col[4 * i + 3] = 0.0;
                     for (int j = 0; j < k; ++j) {
                         const uint16_t cl = sem_indices[i * k + j];
                         if (cl >= C) {
@@ -167,48 +204,27 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, con
                         seen[cl] = static_cast<uint32_t>(i);
                     }
                 }
-                std::memcpy(ridx + a * k, sem_indices + a * k, 2 * (b - a) * k);
-                std::memcpy(rprob + a * k, sem_probs + a * k, 8 * (b - a) * k);
                 finished[c].fetch_add(1, std::memory_order_release);
             }
         };
-        cudaStream_t s = ctx->stream;
-        ctx->take(m->geo, geo_b);
-        ctx->take(m->color, col_b);
-        ctx->take(m->idx, 2 * ns * kpad);
-        ctx->take(m->prob, 8 * ns * kpad);
-        ctx->take(m->perm, 2 * ns * kpad);
-        CK(m->geo.reserve(geo_b));
-        CK(m->color.reserve(col_b));
-        CK(m->idx.reserve(2 * ns * kpad));
-        CK(m->prob.reserve(8 * ns * kpad));
-        CK(m->perm.reserve(2 * ns * kpad));
-        CK(ctx->upload_tmp.reserve(idx_b + prob_b + 64));
-        char* draw = ctx->upload_tmp.as<char>();
-        std::vector<std::thread> pool;
-        for (unsigned w = 1; w < nth; ++w) pool.emplace_back(work, w);
-        std::thread self(work, 0u);
-        cudaError_t copy_err = cudaSuccess;
-        for (unsigned c = 0; c < kChunks; ++c) {
-            while (finished[c].load(std::memory_order_acquire) < nth) std::this_thread::yield();
-            const uint64_t ca = n * c / kChunks, cb = n * (c + 1) / kChunks;
-            if (cb == ca) continue;
-            for (int f = 0; f < 5 && copy_err == cudaSuccess; ++f)
-                copy_err = cudaMemcpyAsync(m->geo.as<double>() + f * ns + ca, geo + f * ns + ca,
-                                           8 * (cb - ca), cudaMemcpyHostToDevice, s);
-            if (copy_err == cudaSuccess)
-                copy_err = cudaMemcpyAsync(m->color.as<double>() + 4 * ca, col + 4 * ca, 32 * (cb - ca),
-                                           cudaMemcpyHostToDevice, s);
-            if (copy_err == cudaSuccess)
-                copy_err = cudaMemcpyAsync(draw + 8 * k * ca, rprob + k * ca, 8 * k * (cb - ca),
-                                           cudaMemcpyHostToDevice, s);
-            if (copy_err == cudaSuccess)
-                copy_err = cudaMemcpyAsync(draw + prob_b + 2 * k * ca, ridx + k * ca, 2 * k * (cb - ca),
-                                           cudaMemcpyHostToDevice, s);
+        {
+            std::vector<std::thread> pool;
+            for (unsigned w = 1; w < nth; ++w) pool.emplace_back(work_a, w);
+            std::thread self(work_a, 0u);
+            cudaError_t copy_err = cudaSuccess;
+            for (unsigned c = 0; c < kChunks; ++c) {
+                while (finished[c].load(std::memory_order_acquire) < nth) std::this_thread::yield();
+                const uint64_t ca = n * c / kChunks, cb = n * (c + 1) / kChunks;
+                if (cb == ca) continue;
+                for (int f = 0; f < 5 && copy_err == cudaSuccess; ++f)
+                    copy_err = cudaMemcpyAsync(m->geo.as<double>() + f * ns + ca, geo + f * ns + ca,
+                                               8 * (cb - ca), cudaMemcpyHostToDevice, s);
+            }
+            self.join();
+            for (auto& th : pool) th.join();
+            CK(copy_err);
+            CK(cudaEventRecord(ctx->ev_hstage, s));
         }
-        self.join();
-        for (auto& th : pool) th.join();
-        CK(copy_err);
         for (unsigned w = 0; w < nth; ++w)
             if (bad[w] >= 0) {
                 cudaStreamSynchronize(s);  // the in-flight copies target this map's buffers
@@ -216,13 +232,6 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, con
             }
         int has_dup = 0;
         for (unsigned w = 0; w < nth; ++w) has_dup |= dup[w];
-        // rows sorted by class id (stable) and padded to kpad, on the GPU
-        launch_sort_rows(reinterpret_cast<const uint16_t*>(draw + prob_b),
-                         reinterpret_cast<const double*>(draw), n, k, kpad, m->idx.as<uint16_t>(),
-                         m->prob.as<double>(), m->perm.as<uint16_t>(), s);
-        ctx->stats.kernel_launches += n ? 1 : 0;
-        CK(cudaGetLastError());
-        CK(cudaStreamSynchronize(s));
         DevMap& d = m->dev;
         d.n = n;
         d.k = k;
@@ -239,7 +248,72 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, con
         d.sem_prob = m->prob.as<double>();
         d.sem_perm = m->perm.as<uint16_t>();
         d.dup_idx = has_dup;
+        d.gbounds = m->gbnd.as<uint4>();
         m->groups = choose_groups(C, k);
+        ctx->stats.kernel_launches += n ? 2 : 0;  // the row sort and the group bounds (phase B)
+        // ---- phase B: colours + rows, staged by a thread, copied / sorted on the upload stream
+        char* draw = ctx->upload_tmp.as<char>();
+        const int device = ctx->device;
+        cudaStream_t us = ctx->up_stream;
+        cudaEvent_t ev_hrows = ctx->ev_hrows;
+        sgm_map* mm = m;
+        m->rows_pending = true;
+        m->rows_thread = std::thread([=]() {
+            try {
+                CK(cudaSetDevice(device));
+                std::unique_ptr<std::atomic<unsigned>[]> done(new std::atomic<unsigned>[kChunks]);
+                for (unsigned c = 0; c < kChunks; ++c) done[c].store(0);
+                auto work_b = [&](unsigned w) {
+                    for (unsigned c = 0; c < kChunks; ++c) {
+                        const uint64_t ca = n * c / kChunks, cb = n * (c + 1) / kChunks;
+                        const uint64_t a = ca + (cb - ca) * w / nth, b = ca + (cb - ca) * (w + 1) / nth;
+                        for (uint64_t i = a; i < b; ++i) {
+                            for (int q = 0; q < 3; ++q) col[4 * i + q] = std::clamp(colors[3 * i + q], 0.0, 1.0);
+                            col[4 * i + 3] = 0.0;
+                        }
+                        std::memcpy(ridx + a * k, sem_indices + a * k, 2 * (b - a) * k);
+                        std::memcpy(rprob + a * k, sem_probs + a * k, 8 * (b - a) * k);
+                        done[c].fetch_add(1, std::memory_order_release);
+                    }
+                };
+                std::vector<std::thread> pool;
+                for (unsigned w = 1; w < nth; ++w) pool.emplace_back(work_b, w);
+                std::thread self(work_b, 0u);
+                cudaError_t e = cudaSuccess;
+                for (unsigned c = 0; c < kChunks; ++c) {
+                    while (done[c].load(std::memory_order_acquire) < nth) std::this_thread::yield();
+                    const uint64_t ca = n * c / kChunks, cb = n * (c + 1) / kChunks;
+                    if (cb == ca) continue;
+                    if (e == cudaSuccess)
+                        e = cudaMemcpyAsync(mm->color.as<double>() + 4 * ca, col + 4 * ca, 32 * (cb - ca),
+                                            cudaMemcpyHostToDevice, us);
+                    if (e == cudaSuccess)
+                        e = cudaMemcpyAsync(draw + 8 * k * ca, rprob + k * ca, 8 * k * (cb - ca),
+                                            cudaMemcpyHostToDevice, us);
+                    if (e == cudaSuccess)
+                        e = cudaMemcpyAsync(draw + prob_b + 2 * k * ca, ridx + k * ca, 2 * k * (cb - ca),
+                                            cudaMemcpyHostToDevice, us);
+                }
+                self.join();
+                for (auto& th : pool) th.join();
+                CK(e);
+                CK(cudaEventRecord(ev_hrows, us));
+                // rows sorted by class id (stable) and padded to kpad; their group bounds
+                launch_sort_rows(reinterpret_cast<const uint16_t*>(draw + prob_b),
+                                 reinterpret_cast<const double*>(draw), n, k, kpad,
+                                 mm->idx.as<uint16_t>(), mm->prob.as<double>(), mm->perm.as<uint16_t>(), us);
+                launch_group_bounds(mm->dev, mm->groups, mm->gbnd.as<uint4>(), us);
+                CK(cudaGetLastError());
+                CK(cudaEventRecord(mm->ev_rows, us));
+            } catch (const SgmError& err) {
+                mm->rows_code = err.code;
+                mm->rows_msg = err.msg;
+            } catch (const std::exception& err) {
+                mm->rows_code = SGM_ERR_INVALID;
+                mm->rows_msg = err.what();
+            }
+        });
+        ctx->rows_owner = m;
         *out = m;
         m = nullptr;
     });
@@ -247,12 +321,41 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, con
     return rc;
 }
 
+int sgm_map_wait(sgm_ctx* ctx, sgm_map* map) {
+    return guard(ctx, [&] {
+        need_ctx(ctx);
+        if (!map) fail(SGM_ERR_INVALID, "map is null");
+        map_ready(ctx, map);
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes, const double* centers,
+                   const double* log_radii, const double* opacity_logits, const double* colors,
+                   const uint16_t* sem_indices, const double* sem_probs, sgm_map** out) {
+    int rc = sgm_map_upload_async(ctx, n, k, num_classes, centers, log_radii, opacity_logits, colors,
+                                  sem_indices, sem_probs, out);
+    if (rc != SGM_OK) return rc;
+    rc = sgm_map_wait(ctx, *out);  // the host arrays are no longer read after this
+    if (rc != SGM_OK) {
+        sgm_map_release(ctx, *out);
+        *out = nullptr;
+    }
+    return rc;
+}
+
 void sgm_map_release(sgm_ctx* ctx, sgm_map* map) {
     if (!map) return;
+    if (map->rows_pending) {
+        map->rows_thread.join();
+        map->rows_pending = false;
+    }
     if (ctx) {
+        if (ctx->rows_owner == map) ctx->rows_owner = nullptr;
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
         cudaStreamSynchronize(ctx->bin_stream);
+        if (ctx->up_stream) cudaStreamSynchronize(ctx->up_stream);
         if (ctx->last_map == map) ctx->last_valid = false;
         ctx->give(std::move(map->geo));
         ctx->give(std::move(map->color));
@@ -260,7 +363,9 @@ void sgm_map_release(sgm_ctx* ctx, sgm_map* map) {
         ctx->give(std::move(map->prob));
         ctx->give(std::move(map->perm));
         ctx->give(std::move(map->cov));
+        ctx->give(std::move(map->gbnd));
     }
+    if (map->ev_rows) cudaEventDestroy(map->ev_rows);
     delete map;
 }
 

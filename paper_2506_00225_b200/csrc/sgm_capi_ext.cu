@@ -60,6 +60,7 @@ void trainer_rebuild(sgm_ctx* ctx, sgm_trainer* tr) {
     d.sem_perm = m.perm.as<uint16_t>();
     d.dup_idx = tr->dup;
     m.groups = choose_groups(C, k);
+    map_group_bounds(ctx, &m, s);
     if (ctx->last_map == &m) ctx->last_valid = false;
 }
 

@@ -137,6 +137,16 @@ struct sgm_map {
     DevBuf prob;   // [n][kpad] f64
     DevBuf perm;   // [n][kpad] u16 original entry index
     DevBuf cov;    // anisotropic mode: [6][n] world covariance (sgm_map_set_anisotropic)
+    DevBuf gbnd;   // [n] uint4: class-sorted rows' channel-group bounds (DevMap::gbounds)
+    // Upload split in two (sgm_map_upload): the geometry is staged and copied on the ctx
+    // stream before the call returns; the colours and semantic rows are staged by
+    // rows_thread and copied / sorted on the ctx's upload stream, ending at ev_rows. The
+    // first use of the rows (the raster) waits for both (map_ready).
+    std::thread rows_thread;
+    bool rows_pending = false;
+    int rows_code = 0;
+    std::string rows_msg;
+    cudaEvent_t ev_rows = nullptr;
 };
 
 struct sgm_ctx {
@@ -147,6 +157,10 @@ struct sgm_ctx {
     bool profiling = false;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaStream_t bin_stream = nullptr;  // binning of the next sub-batch overlaps the raster
+    cudaStream_t up_stream = nullptr;   // map uploads: colours / semantic rows (sgm_map_upload)
+    sgm_map* rows_owner = nullptr;      // the map whose rows_thread uses h_rows
+    cudaEvent_t ev_hstage = nullptr;    // the last copy out of h_stage (geometry) / h_rows
+    cudaEvent_t ev_hrows = nullptr;
     cudaEvent_t ev_ready = nullptr;
     cudaEvent_t ev_binned[2] = {nullptr, nullptr};
     cudaEvent_t ev_r[16] = {};  // raster start/stop pairs of one group (profiling)
@@ -161,7 +175,7 @@ struct sgm_ctx {
     uint64_t last_ncontrib = 0;
     bool last_has_contrib = false;
     int last_px = 0;
-    HostBuf h_counts, h_views, h_poses, h_out, h_stage, h_ring;
+    HostBuf h_counts, h_views, h_poses, h_out, h_stage, h_rows, h_ring;
     cudaEvent_t ev_ring[4] = {nullptr, nullptr, nullptr, nullptr};  // copy_out pinned ring
     DevBuf upload_tmp;
     // device buffers of released maps, reused by the next upload (a map version bump
@@ -197,6 +211,11 @@ struct sgm_ctx {
 
 namespace sgm {
 
+// The map's semantic rows (and colours, group bounds) are on the device: joins the upload's
+// staging thread (failing with its error) and makes the ctx stream wait for the rows' copies.
+void map_ready(sgm_ctx* ctx, const sgm_map* map);
+// Channel-group bounds of a map whose rows are sorted on the device (stream s).
+void map_group_bounds(sgm_ctx* ctx, sgm_map* map, cudaStream_t s);
 CamParams to_cam(const sgm_camera* c);
 OptParams to_opt(const sgm_options* o, const CamParams& cam);
 PoseParams to_pose(const sgm_pose& p);

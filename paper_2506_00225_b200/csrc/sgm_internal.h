@@ -39,6 +39,9 @@ struct DevMap {
     // covariance replaces rad; projections use the EWA footprint (sgm_kernels.cu).
     int aniso = 0;
     const double* cov = nullptr;  // [6][n] SoA: xx, xy, xz, yy, yz, zz
+    // per Gaussian: the ends of its class-sorted row's 8 raster channel groups (u16 each),
+    // computed once per map (launch_group_bounds); the raster stages them with the rows
+    const uint4* gbounds = nullptr;
 };
 
 struct CamParams {
@@ -240,6 +243,7 @@ void launch_bins_to_ids(const uint32_t* list, uint64_t P, const PackedSplat* pac
 
 void launch_sort_rows(const uint16_t* idx, const double* prob, uint64_t n, int k, int kpad,
                       uint16_t* out_idx, double* out_prob, uint16_t* out_perm, cudaStream_t s);
+void launch_group_bounds(const DevMap& m, const GroupParams& gp, uint4* out, cudaStream_t s);
 // sgm_backward.cu
 size_t backward_loss_blocks(int W, int H);
 void launch_loss_pixels(const BackwardParams& b, double* part, double* totals, cudaStream_t s);

@@ -324,21 +324,26 @@ __global__ void k_pack(DevMap m, const PoseParams* __restrict__ pose, CamParams 
     const Rect rc = tile_rect(q, o);
     counts[r] = rect_count(rc);
     rects[r] = make_int4(rc.tx0, rc.ty0, rc.tx1 - rc.tx0 + 1, rc.ty1 - rc.ty0 + 1);
-    if (bounds) {
-        // raster channel groups of the class-sorted row: b[g] = #entries with class <
-        // (g + 1) * Cg for g = 0..6, b[7] = k (u16 each)
-        const uint16_t* row = m.sem_idx + static_cast<size_t>(i) * m.kpad;
-        uint32_t b[8];
-        int j = 0;
-        for (int g = 0; g < 7; ++g) {
-            const int lim = (g + 1) * gp.Cg;
-            while (j < m.k && row[j] < lim) ++j;
-            b[g] = static_cast<uint32_t>(j);
-        }
-        b[7] = static_cast<uint32_t>(m.k);
-        bounds[r] = make_uint4(b[0] | (b[1] << 16), b[2] | (b[3] << 16), b[4] | (b[5] << 16),
-                               b[6] | (b[7] << 16));
+    (void)gp;
+    (void)bounds;  // the channel-group bounds are per map (k_group_bounds), not per view
+}
+
+// Raster channel groups of each Gaussian's class-sorted row: b[g] = #entries with class <
+// (g + 1) * Cg for g = 0..6, b[7] = k (u16 each). Per map, once (not per view): the binning
+// then needs no semantic rows, so their upload can overlap it.
+__global__ void k_group_bounds(DevMap m, GroupParams gp, uint4* __restrict__ out) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m.n) return;
+    const uint16_t* row = m.sem_idx + i * m.kpad;
+    uint32_t b[8];
+    int j = 0;
+    for (int g = 0; g < 7; ++g) {
+        const int lim = (g + 1) * gp.Cg;
+        while (j < m.k && row[j] < lim) ++j;
+        b[g] = static_cast<uint32_t>(j);
     }
+    b[7] = static_cast<uint32_t>(m.k);
+    out[i] = make_uint4(b[0] | (b[1] << 16), b[2] | (b[3] << 16), b[4] | (b[5] << 16), b[6] | (b[7] << 16));
 }
 
 // Emits (tile row, rank | column range) pairs in rank order at the scanned per-rank row
@@ -950,6 +955,11 @@ void launch_sort_rows(const uint16_t* idx, const double* prob, uint64_t n, int k
     }
     k_sort_rows<<<blocks_for(n, 256), 256, 0, s>>>(idx, prob, n, k, kpad, out_idx, out_prob,
                                                    out_perm);
+}
+
+void launch_group_bounds(const DevMap& m, const GroupParams& gp, uint4* out, cudaStream_t s) {
+    if (m.n == 0) return;
+    k_group_bounds<<<blocks_for(m.n, 256), 256, 0, s>>>(m, gp, out);
 }
 
 void launch_bins_to_ids(const uint32_t* list, uint64_t P, const PackedSplat* packed, int aniso,

@@ -85,6 +85,7 @@ int sgm_map_export(sgm_ctx* ctx, const sgm_map* map, void* d_blob, uint64_t capa
     return guard(ctx, [&] {
         need_ctx(ctx);
         if (!map || !d_blob) fail(SGM_ERR_INVALID, "map / blob is null");
+        map_ready(ctx, map);
         const DevMap& d = map->dev;
         const Segs sg = segs_of(d.n, d.kpad, d.aniso != 0);
         if (capacity < sg.total)
@@ -167,6 +168,7 @@ int sgm_map_import(sgm_ctx* ctx, const void* d_blob, uint64_t bytes, sgm_map** o
         d.aniso = h.aniso;
         d.cov = h.aniso ? m->cov.as<double>() : nullptr;
         m->groups = choose_groups(h.C, h.k);
+        map_group_bounds(ctx, m, s);
         *out = m;
         m = nullptr;
     });

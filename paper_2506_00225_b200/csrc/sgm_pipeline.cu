@@ -309,6 +309,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
     CK(ctx->h_out.reserve(24 * B));
 
     const int kSub = 8;  // views per raster launch (binning of the next 8 overlaps)
+    bool rows_ready = false;  // map_ready done (before the first raster launch)
     for (uint64_t b0 = 0; b0 < n; b0 += B) {
         const int nb = static_cast<int>(std::min<uint64_t>(B, n - b0));
         if (ctx->profiling) CK(cudaEventRecord(ctx->ev[0], s));
@@ -429,6 +430,10 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 }
                 if (dense_group) {  // one view: depth-prefix binning, synchronous on s
                     CK(cudaStreamSynchronize(sb));
+                    if (!rows_ready) {
+                        map_ready(ctx, map);
+                        rows_ready = true;
+                    }
                     score_dense_view(ctx, map, cam, o, s0, V[s0], P[s0], R[s0],
                                      ctx->pcount.as<unsigned long long>() + nb + s0, NS, bin_tiles,
                                      rtx, rtiles, kSub, hvd[0], rp);
@@ -444,6 +449,12 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 }
                 const int slot = (s0 / kSub) & 1;
                 CK(cudaEventRecord(ctx->ev_binned[slot], sb));
+                // the raster reads the semantic rows: the map's upload (phase B) has to be done;
+                // the binning just queued runs meanwhile
+                if (!rows_ready) {
+                    map_ready(ctx, map);
+                    rows_ready = true;
+                }
                 CK(cudaStreamWaitEvent(s, ctx->ev_binned[slot], 0));
                 rp.views = ctx->views.as<ViewDesc>() + (s0 - v0);
                 const int pr = ((s0 - v0) / kSub) % 8;  // profiling event pair
@@ -521,6 +532,26 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
             ctx->last_pose = poses[0];
         }
     }
+}
+
+void map_ready(sgm_ctx* ctx, const sgm_map* cmap) {
+    sgm_map* map = const_cast<sgm_map*>(cmap);  // the staging state is not the snapshot
+    if (map->rows_pending) {
+        map->rows_thread.join();
+        map->rows_pending = false;
+        if (ctx->rows_owner == map) ctx->rows_owner = nullptr;
+    }
+    if (map->rows_code != SGM_OK) fail(map->rows_code, "map upload: %s", map->rows_msg.c_str());
+    if (map->ev_rows) CK(cudaStreamWaitEvent(ctx->stream, map->ev_rows, 0));
+    if (!map->dev.gbounds && map->dev.n) map_group_bounds(ctx, map, ctx->stream);
+}
+
+void map_group_bounds(sgm_ctx* ctx, sgm_map* map, cudaStream_t s) {
+    const size_t ns = std::max<uint64_t>(map->dev.n, 1);
+    CK(map->gbnd.reserve(16 * ns));
+    map->dev.gbounds = map->gbnd.as<uint4>();
+    launch_group_bounds(map->dev, map->groups, map->gbnd.as<uint4>(), s);
+    ctx->stats.kernel_launches += map->dev.n ? 1 : 0;
 }
 
 int guard(sgm_ctx* ctx, const std::function<void()>& fn) {

@@ -156,7 +156,6 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     struct LoaderState {
         const uint32_t* list;
         const PackedSplat* packed;
-        const uint4* bounds;
         const uint32_t* order;
         uint32_t L0, Ln, cursor;  // cursor: next bin entry to examine
         float bx0, bx1, by0, by1;
@@ -183,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
             // the stage was last read (generic proxy) before the barrier this warp passed
             fence_proxy_async();
             bulk_g2s(sb + L.st_packed + lane * 64, ls.packed + v.x, 64u, bar);
-            bulk_g2s(sb + L.st_bnd + lane * 16, ls.bounds + v.x, 16u, bar);
+            bulk_g2s(sb + L.st_bnd + lane * 16, p.map.gbounds + v.y, 16u, bar);
             bulk_g2s(sb + L.st_idx + lane * kpad * 2, p.map.sem_idx + static_cast<size_t>(v.y) * kpad,
                      2u * kpad, bar);
             bulk_g2s(sb + L.st_prob + lane * kpad * 8, p.map.sem_prob + static_cast<size_t>(v.y) * kpad,
@@ -246,7 +245,6 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
             if (kItems) s_trunc[ls.q] = p.trunc ? p.trunc[bin] : 0;
             ls.list = v->list;
             ls.packed = v->packed;
-            ls.bounds = v->bounds;
             ls.order = v->order;
             ls.L0 = rg.x;
             ls.Ln = rg.y - rg.x;

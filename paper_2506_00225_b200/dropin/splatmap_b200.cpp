@@ -66,8 +66,9 @@ void check(int rc) {
 
 struct MapHandle {
     sgm_map* m = nullptr;
+    // async upload: the spans stay untouched until the call that made this handle returns
     explicit MapHandle(const GaussianMap& map) {
-        check(sgm_map_upload(ctx(), map.size(), map.k(), map.num_classes(), map.centers().data(),
+        check(sgm_map_upload_async(ctx(), map.size(), map.k(), map.num_classes(), map.centers().data(),
                              map.log_radii().data(), map.opacity_logits().data(),
                              map.colors().data(), map.sem_indices().data(), map.sem_probs().data(),
                              &m));

@@ -450,8 +450,8 @@ class Context:
 
     def close(self) -> None:
         if self.handle:
-            for _, (_, _, m) in list(self._maps.items()):
-                N.lib.sgm_map_release(self.handle, m)
+            for _, ent in list(self._maps.items()):
+                N.lib.sgm_map_release(self.handle, ent[2])
             self._maps.clear()
             N.lib.sgm_ctx_destroy(self.handle)
             self.handle = None
@@ -493,14 +493,14 @@ class Context:
         key = id(gmap)
         hit = self._maps.get(key)
         if hit is not None:
-            ref, ver, handle = hit
+            ref, ver, handle = hit[:3]
             if ref() is gmap and ver == gmap._version:
                 return handle
             N.lib.sgm_map_release(self.handle, handle)
             del self._maps[key]
-        handle = self.upload_arrays(gmap)
+        handle, keep = self._upload_async(gmap)
         self._maps[key] = (weakref.ref(gmap, lambda _r, k=key: self._forget(k)), gmap._version,
-                           handle)
+                           handle, keep)
         return handle
 
     def _forget(self, key) -> None:
@@ -508,6 +508,29 @@ class Context:
         lib = getattr(N, "lib", None) if N is not None else None  # None at interpreter exit
         if hit is not None and self.handle and lib is not None:
             lib.sgm_map_release(self.handle, hit[2])
+
+    def _upload_async(self, gmap: GaussianMap):
+        """sgm_map_upload_async: returns (handle, arrays the staging thread still reads). The
+        compute call that follows in the same API function waits for the staging."""
+        n = gmap.size()
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in
+                (gmap.centers, gmap.log_radii, gmap.opacity_logits, gmap.colors)]
+        idx = np.ascontiguousarray(gmap.sem_indices, dtype=np.uint16)
+        probs = np.ascontiguousarray(gmap.sem_probs, dtype=np.float64)
+        h = C.c_void_p()
+        self.check(N.lib.sgm_map_upload_async(
+            self.handle, n, gmap.k(), gmap.num_classes(), N.dptr(arrs[0]), N.dptr(arrs[1]),
+            N.dptr(arrs[2]), N.dptr(arrs[3]), idx.ctypes.data_as(C.POINTER(C.c_uint16)),
+            N.dptr(probs), C.byref(h)))
+        if gmap.anisotropic():
+            ls = np.ascontiguousarray(gmap.log_scales, dtype=np.float64)
+            qs = np.ascontiguousarray(gmap.quats, dtype=np.float64)
+            try:
+                self.check(N.lib.sgm_map_set_anisotropic(self.handle, h, N.dptr(ls), N.dptr(qs)))
+            except Exception:
+                N.lib.sgm_map_release(self.handle, h)
+                raise
+        return h, (arrs, idx, probs)
 
     def upload_arrays(self, gmap: GaussianMap) -> C.c_void_p:
         n = gmap.size()
