@@ -126,7 +126,8 @@ int sgm_map_upload(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes,
  * the caller already queues work (preprocess and binning need only the geometry; the raster
  * waits for the rows). The caller keeps the host arrays alive and unchanged until the first
  * compute call on the map returns, or sgm_map_wait / sgm_map_release (sgm_map_upload is
- * sgm_map_upload_async + sgm_map_wait). Index errors are reported here as by sgm_map_upload. */
+ * sgm_map_upload_async + sgm_map_wait). A semantic index >= num_classes + 1 is reported by
+ * sgm_map_wait or the first compute call on the map (sgm_map_upload reports it itself). */
 int sgm_map_upload_async(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classes,
                          const double* centers, const double* log_radii,
                          const double* opacity_logits, const double* colors,

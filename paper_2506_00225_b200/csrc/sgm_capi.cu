@@ -179,12 +179,10 @@ int sgm_map_upload_async(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classe
         const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
         const unsigned nth = n > 65536 ? hw : 1;
         const unsigned kChunks = n > 65536 ? 8 : 1;
-        // ---- phase A: geometry + activations + index checks, chunk copies on s ----
-        std::vector<int> bad(nth, -1), dup(nth, 0);
+        // ---- phase A: geometry + activations, chunk copies on s ----
         std::unique_ptr<std::atomic<unsigned>[]> finished(new std::atomic<unsigned>[kChunks]);
         for (unsigned c = 0; c < kChunks; ++c) finished[c].store(0);
         auto work_a = [&](unsigned w) {
-            std::vector<uint32_t> seen(static_cast<size_t>(C), 0xffffffffu);
             for (unsigned c = 0; c < kChunks; ++c) {
                 const uint64_t ca = n * c / kChunks, cb = n * (c + 1) / kChunks;
                 const uint64_t a = ca + (cb - ca) * w / nth, b = ca + (cb - ca) * (w + 1) / nth;
@@ -194,15 +192,6 @@ int sgm_map_upload_async(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classe
                     geo[2 * ns + i] = centers[3 * i + 2];
                     geo[3 * ns + i] = std::exp(log_radii[i]);                      // radius()
                     geo[4 * ns + i] = 1.0 / (1.0 + std::exp(-opacity_logits[i]));  // sigmoid
-                    for (int j = 0; j < k; ++j) {
-                        const uint16_t cl = sem_indices[i * k + j];
-                        if (cl >= C) {
-                            if (bad[w] < 0) bad[w] = static_cast<int>(i % 0x7fffffff);
-                            continue;
-                        }
-                        if (seen[cl] == static_cast<uint32_t>(i)) dup[w] = 1;
-                        seen[cl] = static_cast<uint32_t>(i);
-                    }
                 }
                 finished[c].fetch_add(1, std::memory_order_release);
             }
@@ -225,13 +214,6 @@ int sgm_map_upload_async(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classe
             CK(copy_err);
             CK(cudaEventRecord(ctx->ev_hstage, s));
         }
-        for (unsigned w = 0; w < nth; ++w)
-            if (bad[w] >= 0) {
-                cudaStreamSynchronize(s);  // the in-flight copies target this map's buffers
-                fail(SGM_ERR_INVALID, "map: semantic index >= channels %d (near gaussian %d)", C, bad[w]);
-            }
-        int has_dup = 0;
-        for (unsigned w = 0; w < nth; ++w) has_dup |= dup[w];
         DevMap& d = m->dev;
         d.n = n;
         d.k = k;
@@ -247,7 +229,7 @@ int sgm_map_upload_async(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classe
         d.sem_idx = m->idx.as<uint16_t>();
         d.sem_prob = m->prob.as<double>();
         d.sem_perm = m->perm.as<uint16_t>();
-        d.dup_idx = has_dup;
+        d.dup_idx = 0;  // set by map_ready from phase B's scan of the rows
         d.gbounds = m->gbnd.as<uint4>();
         m->groups = choose_groups(C, k);
         ctx->stats.kernel_launches += n ? 2 : 0;  // the row sort and the group bounds (phase B)
@@ -263,13 +245,25 @@ int sgm_map_upload_async(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classe
                 CK(cudaSetDevice(device));
                 std::unique_ptr<std::atomic<unsigned>[]> done(new std::atomic<unsigned>[kChunks]);
                 for (unsigned c = 0; c < kChunks; ++c) done[c].store(0);
+                std::vector<int> bad(nth, -1), dup(nth, 0);
                 auto work_b = [&](unsigned w) {
+                    std::vector<uint32_t> seen(static_cast<size_t>(C), 0xffffffffu);
                     for (unsigned c = 0; c < kChunks; ++c) {
                         const uint64_t ca = n * c / kChunks, cb = n * (c + 1) / kChunks;
                         const uint64_t a = ca + (cb - ca) * w / nth, b = ca + (cb - ca) * (w + 1) / nth;
                         for (uint64_t i = a; i < b; ++i) {
                             for (int q = 0; q < 3; ++q) col[4 * i + q] = std::clamp(colors[3 * i + q], 0.0, 1.0);
                             col[4 * i + 3] = 0.0;
+                            // index range (gaussian_map.hpp:63-66) and repeated classes
+                            for (int j = 0; j < k; ++j) {
+                                const uint16_t cl = sem_indices[i * k + j];
+                                if (cl >= C) {
+                                    if (bad[w] < 0) bad[w] = static_cast<int>(i % 0x7fffffff);
+                                    continue;
+                                }
+                                if (seen[cl] == static_cast<uint32_t>(i)) dup[w] = 1;
+                                seen[cl] = static_cast<uint32_t>(i);
+                            }
                         }
                         std::memcpy(ridx + a * k, sem_indices + a * k, 2 * (b - a) * k);
                         std::memcpy(rprob + a * k, sem_probs + a * k, 8 * (b - a) * k);
@@ -298,6 +292,11 @@ int sgm_map_upload_async(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classe
                 for (auto& th : pool) th.join();
                 CK(e);
                 CK(cudaEventRecord(ev_hrows, us));
+                for (unsigned w = 0; w < nth; ++w) {
+                    mm->rows_dup |= dup[w];
+                    if (bad[w] >= 0)
+                        fail(SGM_ERR_INVALID, "map: semantic index >= channels %d (near gaussian %d)", C, bad[w]);
+                }
                 // rows sorted by class id (stable) and padded to kpad; their group bounds
                 launch_sort_rows(reinterpret_cast<const uint16_t*>(draw + prob_b),
                                  reinterpret_cast<const double*>(draw), n, k, kpad,

@@ -145,6 +145,7 @@ struct sgm_map {
     std::thread rows_thread;
     bool rows_pending = false;
     int rows_code = 0;
+    int rows_dup = 0;  // phase B found a Gaussian listing a class twice (DevMap::dup_idx)
     std::string rows_msg;
     cudaEvent_t ev_rows = nullptr;
 };

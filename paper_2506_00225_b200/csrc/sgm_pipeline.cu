@@ -433,6 +433,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                     if (!rows_ready) {
                         map_ready(ctx, map);
                         rows_ready = true;
+                        rp.map = map->dev;
                     }
                     score_dense_view(ctx, map, cam, o, s0, V[s0], P[s0], R[s0],
                                      ctx->pcount.as<unsigned long long>() + nb + s0, NS, bin_tiles,
@@ -454,6 +455,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 if (!rows_ready) {
                     map_ready(ctx, map);
                     rows_ready = true;
+                    rp.map = map->dev;  // (dup_idx known now)
                 }
                 CK(cudaStreamWaitEvent(s, ctx->ev_binned[slot], 0));
                 rp.views = ctx->views.as<ViewDesc>() + (s0 - v0);
@@ -540,6 +542,7 @@ void map_ready(sgm_ctx* ctx, const sgm_map* cmap) {
         map->rows_thread.join();
         map->rows_pending = false;
         if (ctx->rows_owner == map) ctx->rows_owner = nullptr;
+        map->dev.dup_idx = map->rows_dup;
     }
     if (map->rows_code != SGM_OK) fail(map->rows_code, "map upload: %s", map->rows_msg.c_str());
     if (map->ev_rows) CK(cudaStreamWaitEvent(ctx->stream, map->ev_rows, 0));
