@@ -193,7 +193,11 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         __syncwarp();
         if (lane == 0) mbar_arrive(bar);
     };
-    unsigned mphase = 0;  // loader: parity bit per stage of the mbarrier phase to wait for
+    // Parity bits of the next mbarrier phase per stage. Compute threads: the phase of the next
+    // batch they read from the stage (they wait on it after the batch barrier; the copies
+    // were issued a whole batch earlier, so it is normally complete). Loader: the phase its
+    // last copies into the stage complete (waited only for a batch the block never read).
+    unsigned mphase = 0;
     auto wait_batch = [&](int b) {
         const int st = b & 1;
         mbar_wait(smem_addr(&s_mbar[st]), (mphase >> st) & 1u);
@@ -315,21 +319,32 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         double rcs[4] = {0.0, 0.0, 0.0, 0.0};  // this (segment, pixel) thread's colour / depth
         int mine = loader ? 1 : 0;  // vote that this thread's pixel is done (the block stops when all are)
         for (int b = 0;; ++b) {
-            if (loader && scnt[q][b % 3] > 0) wait_batch(b);  // batch b's bulk copies landed
-            // batch b landed; scnt for b+1 visible; W / bnd free; and the early termination
-            // of the whole block (:312 for every pixel) decided on the previous batch's votes
-            if (__syncthreads_and(mine)) break;
+            // scnt for b+1 visible; W / bnd free; and the early termination of the whole
+            // block (:312 for every pixel) decided on the previous batch's votes
+            if (__syncthreads_and(mine)) {
+                // batch b (if any) was issued but is never read: the compute threads skip its
+                // mbarrier phase, the loader waits for it before the stage is used again
+                if (scnt[q][b % 3] > 0) {
+                    if (loader)
+                        wait_batch(b);
+                    else
+                        mphase ^= 1u << (b & 1);
+                }
+                break;
+            }
             const int n = scnt[q][b % 3];
             if (n == 0) {  // the bin is exhausted with pixels still open
                 if (kItems && t == 0) s_exh = 1;
                 break;
             }
             if (loader) {  // batch b+1 in flight while the compute warps blend batch b
+                mphase ^= 1u << (b & 1);  // (batch b's phase: completed for the compute warps)
                 if (b == 0) fill(1);
                 if (scnt[q][(b + 1) % 3] > 0) issue(b + 1);
                 fill(b + 2);  // rm slot b & 1 (batch b was issued last iteration), scnt[q][(b + 2) % 3]
                 continue;
             }
+            wait_batch(b);  // batch b's bulk copies have landed
             if (t == 0) slive[(b + 1) & 1] = 0u;  // last read by phase C of batch b - 1
             const unsigned char* sb = stg + (b & 1) * L.stage_bytes;
             const PackedSplat* sp = reinterpret_cast<const PackedSplat*>(sb + L.st_packed);
@@ -550,8 +565,9 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         }
 
         if (loader) {
-            // every copy of this block has landed (waited before the last barrier) and the
-            // compute warps no longer read the stages: stage the next block's batch 0
+            // every copy of this block has landed (read by the compute warps, or waited for
+            // above) and the compute warps no longer read the stages: stage the next block's
+            // batch 0
             if (lane == 0) ls.q ^= 1;
             __syncwarp();
             claim();
