@@ -200,7 +200,10 @@ def _load():
         if _lib is None:
             h = C.CDLL(str(LIB_PATH))
             for name, (res, args) in SIGNATURES.items():
-                fn = getattr(h, name)
+                try:
+                    fn = getattr(h, name)
+                except AttributeError:  # an older build (A/B runs): that entry point unusable
+                    continue
                 fn.restype = res
                 fn.argtypes = args
             if h.sgm_abi_version() != SGM_ABI_VERSION:

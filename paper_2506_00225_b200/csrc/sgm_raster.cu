@@ -111,7 +111,8 @@ __device__ __forceinline__ int px_row(int q) { return (q >> 5) * 4 + ((q >> 2) &
 // stream's kernels to take their slots.)
 // kItems: the depth-prefix binning launch (explicit item list, truncated-list flags and the
 // incomplete-tile report); a separate instantiation, so the common launches carry none of it.
-template <bool kRender, bool kDup, bool kAniso, bool kRc = false, int kOcc = 3, bool kItems = false>
+template <bool kRender, bool kDup, bool kAniso, bool kRc = false, int kOcc = 3, bool kItems = false,
+          bool kRefDiv = false>
 __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int C = p.map.C;
@@ -168,30 +169,64 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     // first). The loader alone waits on it, before the batch barrier that hands the stage
     // to the compute warps.
     __shared__ __align__(8) unsigned long long s_mbar[2];
-    const unsigned entry_bytes = 64u + 16u + 10u * static_cast<unsigned>(kpad) +
-                                 ((kRender || kRc) ? 32u : 0u);
+    // (render and colour-writing launches keep 16-byte cp.async chunks: their larger register
+    // footprint spills with the bulk-copy loader)
+    constexpr bool kBulk = !kRender && !kRc;
+    const int qi = kpad / 8, qp = kpad / 2;
+    const int Q = 5 + qi + qp + ((kRender || kRc) ? 2 : 0);  // 16-byte chunks per Gaussian
     auto issue = [&](int b) {
         const int st = b & 1;
         unsigned char* sb = stg + st * L.stage_bytes;
         const int n = scnt[ls.q][b % 3];
-        const uint32_t bar = smem_addr(&s_mbar[st]);
-        if (lane == 0) mbar_expect_tx(bar, static_cast<unsigned>(n) * entry_bytes);
-        __syncwarp();
-        if (lane < n) {
-            const uint2 v = rm[st * kNB + lane];
-            // the stage was last read (generic proxy) before the barrier this warp passed
-            fence_proxy_async();
-            bulk_g2s(sb + L.st_packed + lane * 64, ls.packed + v.x, 64u, bar);
-            bulk_g2s(sb + L.st_bnd + lane * 16, p.map.gbounds + v.y, 16u, bar);
-            bulk_g2s(sb + L.st_idx + lane * kpad * 2, p.map.sem_idx + static_cast<size_t>(v.y) * kpad,
-                     2u * kpad, bar);
-            bulk_g2s(sb + L.st_prob + lane * kpad * 8, p.map.sem_prob + static_cast<size_t>(v.y) * kpad,
-                     8u * kpad, bar);
-            if (kRender || kRc)
-                bulk_g2s(sb + L.st_color + lane * 32, p.map.color4 + static_cast<size_t>(v.y) * 4, 32u, bar);
+        if constexpr (kBulk) {
+            const uint32_t bar = smem_addr(&s_mbar[st]);
+            if (lane == 0)
+                mbar_expect_tx(bar, static_cast<unsigned>(n) * (64u + 16u + 10u * static_cast<unsigned>(kpad)));
+            __syncwarp();
+            if (lane < n) {
+                const uint2 v = rm[st * kNB + lane];
+                // the stage was last read (generic proxy) before the barrier this warp passed
+                fence_proxy_async();
+                bulk_g2s(sb + L.st_packed + lane * 64, ls.packed + v.x, 64u, bar);
+                bulk_g2s(sb + L.st_bnd + lane * 16, p.map.gbounds + v.y, 16u, bar);
+                bulk_g2s(sb + L.st_idx + lane * kpad * 2, p.map.sem_idx + static_cast<size_t>(v.y) * kpad,
+                         2u * kpad, bar);
+                bulk_g2s(sb + L.st_prob + lane * kpad * 8, p.map.sem_prob + static_cast<size_t>(v.y) * kpad,
+                         8u * kpad, bar);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar);
+        } else {
+            const unsigned qmagic = static_cast<unsigned>((0x100000000ull + Q - 1) / Q);  // ceil(2^32 / Q)
+            const uint2* slot = rm + st * kNB;
+            for (int c = lane; c < n * Q; c += 32) {
+                // c / Q by a multiply-high (exact: c < kNB * Q is far below 2^32 / Q^2)
+                const int e = static_cast<int>(__umulhi(static_cast<unsigned>(c), qmagic));
+                int q = c - e * Q;
+                const uint2 v = slot[e];
+                const unsigned char* src;
+                unsigned char* dst;
+                if (q < 4) {
+                    src = reinterpret_cast<const unsigned char*>(ls.packed + v.x) + 16 * q;
+                    dst = sb + L.st_packed + e * 64 + 16 * q;
+                } else if (q == 4) {
+                    src = reinterpret_cast<const unsigned char*>(p.map.gbounds + v.y);
+                    dst = sb + L.st_bnd + e * 16;
+                } else if ((q -= 5) < qi) {
+                    src = reinterpret_cast<const unsigned char*>(p.map.sem_idx + static_cast<size_t>(v.y) * kpad) + 16 * q;
+                    dst = sb + L.st_idx + e * kpad * 2 + 16 * q;
+                } else if ((q -= qi) < qp) {
+                    src = reinterpret_cast<const unsigned char*>(p.map.sem_prob + static_cast<size_t>(v.y) * kpad) + 16 * q;
+                    dst = sb + L.st_prob + e * kpad * 8 + 16 * q;
+                } else {
+                    q -= qp;
+                    src = reinterpret_cast<const unsigned char*>(p.map.color4 + static_cast<size_t>(v.y) * 4) + 16 * q;
+                    dst = sb + L.st_color + e * 32 + 16 * q;
+                }
+                cp_async16(dst, src);
+            }
+            cp_async_commit();
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar);
     };
     // Parity bits of the next mbarrier phase per stage. Compute threads: the phase of the next
     // batch they read from the stage (they wait on it after the batch barrier; the copies
@@ -319,12 +354,13 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         double rcs[4] = {0.0, 0.0, 0.0, 0.0};  // this (segment, pixel) thread's colour / depth
         int mine = loader ? 1 : 0;  // vote that this thread's pixel is done (the block stops when all are)
         for (int b = 0;; ++b) {
+            if (!kBulk) cp_async_wait_all();  // (cp.async loader: batch b landed)
             // scnt for b+1 visible; W / bnd free; and the early termination of the whole
             // block (:312 for every pixel) decided on the previous batch's votes
             if (__syncthreads_and(mine)) {
-                // batch b (if any) was issued but is never read: the compute threads skip its
-                // mbarrier phase, the loader waits for it before the stage is used again
-                if (scnt[q][b % 3] > 0) {
+                // batch b (if any) was issued but is never read: the loader waits for it before
+                // the stage is used again
+                if (kBulk && scnt[q][b % 3] > 0) {
                     if (loader)
                         wait_batch(b);
                     else
@@ -338,13 +374,13 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                 break;
             }
             if (loader) {  // batch b+1 in flight while the compute warps blend batch b
-                mphase ^= 1u << (b & 1);  // (batch b's phase: completed for the compute warps)
+                if (kBulk) mphase ^= 1u << (b & 1);  // (batch b's phase: completed for the compute warps)
                 if (b == 0) fill(1);
                 if (scnt[q][(b + 1) % 3] > 0) issue(b + 1);
                 fill(b + 2);  // rm slot b & 1 (batch b was issued last iteration), scnt[q][(b + 2) % 3]
                 continue;
             }
-            wait_batch(b);  // batch b's bulk copies have landed
+            if (kBulk) wait_batch(b);  // batch b's bulk copies have landed
             if (t == 0) slive[(b + 1) & 1] = 0u;  // last read by phase C of batch b - 1
             const unsigned char* sb = stg + (b & 1) * L.stage_bytes;
             const PackedSplat* sp = reinterpret_cast<const PackedSplat*>(sb + L.st_packed);
@@ -376,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                         const double dy = dpy - sp[e].my;
                         const double d2 = dx * dx + dy * dy;
                         if (!(d2 > sp[e].cutoff_d2)) {  // :283
-                            if (kRender && p.opt.ref_div) {
+                            if (kRefDiv) {
                                 // render_reference (:90-92): exp(-d2 / (2 r^2)), f <= 0 skipped
                                 f = sp[e].alpha * exp_footprint(-d2 / sp[e].inv_two_r2);
                                 if (f > kMaxFootprint) f = kMaxFootprint;
@@ -717,6 +753,14 @@ void launch_t(const RasterParams& p0, int n_views, cudaStream_t s) {
             cudaFuncSetAttribute(k_raster<kRender, kDup, kAniso, kRc, 4, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             k_raster<kRender, kDup, kAniso, kRc, 4, false><<<grid, kThreads, smem, s>>>(p);
+            return;
+        }
+    }
+    if constexpr (kRender && !kAniso) {
+        if (p.opt.ref_div) {  // render_reference's footprint form
+            cudaFuncSetAttribute(k_raster<kRender, kDup, kAniso, kRc, 3, false, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            k_raster<kRender, kDup, kAniso, kRc, 3, false, true><<<grid, kThreads, smem, s>>>(p);
             return;
         }
     }

@@ -518,7 +518,8 @@ class Context:
         idx = np.ascontiguousarray(gmap.sem_indices, dtype=np.uint16)
         probs = np.ascontiguousarray(gmap.sem_probs, dtype=np.float64)
         h = C.c_void_p()
-        self.check(N.lib.sgm_map_upload_async(
+        upload = getattr(N.lib, "sgm_map_upload_async", None) or N.lib.sgm_map_upload
+        self.check(upload(
             self.handle, n, gmap.k(), gmap.num_classes(), N.dptr(arrs[0]), N.dptr(arrs[1]),
             N.dptr(arrs[2]), N.dptr(arrs[3]), idx.ctypes.data_as(C.POINTER(C.c_uint16)),
             N.dptr(probs), C.byref(h)))
