@@ -164,7 +164,7 @@ struct sgm_ctx {
     cudaEvent_t ev_hrows = nullptr;
     cudaEvent_t ev_ready = nullptr;
     cudaEvent_t ev_binned[2] = {nullptr, nullptr};
-    cudaEvent_t ev_r[16] = {};  // raster start/stop pairs of one group (profiling)
+    cudaEvent_t ev_r[32] = {};  // raster start/stop pairs of one group (profiling)
 
     // scratch
     DevBuf poses, vcount, pcount, keys, vals, keys_alt, vals_alt, packed, counts, offsets, rects,

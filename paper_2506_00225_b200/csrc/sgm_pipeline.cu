@@ -416,8 +416,12 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
             rp.channels = rt.channels;
             rp.groups = map->groups;
             rp.want_rc = fk == Fisher::Gain ? 1 : 0;
-            for (int s0 = v0; s0 < v1; s0 += kSub) {
-                const int s1 = std::min(v1, s0 + kSub);
+            // sub-batches of 1, 2, 4, then kSub views: the first raster starts after one view's
+            // binning instead of kSub views' (the pipeline fill), and each sub-batch's binning
+            // still hides under the previous one's raster (about 1/3 of its time per view)
+            int sub = 0;
+            for (int s0 = v0, len = 1; s0 < v1; s0 += len, len = std::min(kSub, 2 * len), ++sub) {
+                const int s1 = std::min(v1, s0 + len);
                 {  // K2 for the sub-batch: one segmented radix sort of its views' depth keys
                     uint32_t maxV = 0;
                     for (int v = s0; v < s1; ++v) maxV = std::max(maxV, V[v]);
@@ -448,7 +452,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                              const_cast<PackedSplat*>(d.packed), const_cast<uint4*>(d.bounds),
                              const_cast<uint32_t*>(d.list), const_cast<uint2*>(d.ranges), bin_tiles);
                 }
-                const int slot = (s0 / kSub) & 1;
+                const int slot = sub & 1;
                 CK(cudaEventRecord(ctx->ev_binned[slot], sb));
                 // the raster reads the semantic rows: the map's upload (phase B) has to be done;
                 // the binning just queued runs meanwhile
@@ -459,7 +463,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 }
                 CK(cudaStreamWaitEvent(s, ctx->ev_binned[slot], 0));
                 rp.views = ctx->views.as<ViewDesc>() + (s0 - v0);
-                const int pr = ((s0 - v0) / kSub) % 8;  // profiling event pair
+                const int pr = sub % 16;  // profiling event pair
                 if (ctx->profiling) CK(cudaEventRecord(ctx->ev_r[2 * pr], s));
                 FisherParams fp{};
                 fp.H = d_H;
@@ -506,7 +510,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 ctx->stats.contributors += *kc;
             }
             if (ctx->profiling) {
-                const int nsub = std::min(8, (ngroup + kSub - 1) / kSub);
+                const int nsub = std::min(16, sub);
                 for (int q = 0; q < nsub; ++q) {
                     float ms = 0;
                     CK(cudaEventElapsedTime(&ms, ctx->ev_r[2 * q], ctx->ev_r[2 * q + 1]));
