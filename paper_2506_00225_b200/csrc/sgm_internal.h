@@ -317,7 +317,8 @@ template <typename V, typename N>
 bool radix_sort_pairs(uint32_t* keys, V* vals, uint32_t* keys_alt, V* vals_alt, size_t stride,
                       const N* d_n, uint64_t max_len, int nseg, int end_bit, uint32_t* scratch,
                       cudaStream_t s);
-int radix_sort_launches(int end_bit);
+int radix_sort_launches(int end_bit, uint64_t max_len);
+int exclusive_scan_launches(uint64_t n);
 // exclusive scan of n counts (u32 or u64) into u64 offsets
 size_t exclusive_scan_scratch_bytes(uint64_t n);
 template <typename C>

@@ -91,7 +91,7 @@ static void bin_counts(sgm_ctx* ctx, cudaStream_t s, const OptParams& o, uint32_
     launch_bin_scan(diff, o.tiles_x, o.tiles_y, ranges, s, mask, d_total, cap, trunc);
     CK(cudaMemsetAsync(rows + Ve, 0, sizeof(unsigned long long), s));
     exclusive_scan_u64<unsigned long long>(rows, Ve + 1, roff, ctx->scan_tmp.as<unsigned long long>(), s);
-    ctx->stats.kernel_launches += 2 + 3;
+    ctx->stats.kernel_launches += 2 + exclusive_scan_launches(Ve + 1);
 }
 
 // K3 lists (row-bucketed, no sort of the P pairs) over the ranks < Ve: the (row, rank) pairs
@@ -114,7 +114,7 @@ static const unsigned long long* bin_lists(sgm_ctx* ctx, cudaStream_t s, const O
         rbits, ctx->sort_tmp.as<uint32_t>(), s);
     const uint32_t* qk = ralt ? ctx->tkeys_alt.as<uint32_t>() : rk;
     const unsigned long long* qv = ralt ? ctx->tvals_alt.as<unsigned long long>() : rv;
-    ctx->stats.kernel_launches += radix_sort_launches(rbits);
+    ctx->stats.kernel_launches += radix_sort_launches(rbits, R);
     uint2* rranges = ctx->rranges.as<uint2>();
     CK(cudaMemsetAsync(rranges, 0, sizeof(uint2) * o.tiles_y, s));
     launch_ranges(qk, R, rranges, s);
@@ -430,7 +430,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                         ctx->keys_alt.as<uint32_t>(), ctx->vals_alt.as<uint32_t>(), NS,
                         ctx->vcount.as<uint32_t>() + s0, maxV, s1 - s0, 32, ctx->sort_tmp.as<uint32_t>(), sb);
                     if (alt) fail(SGM_ERR_CUDA, "depth sort: odd pass count");  // 4 passes: in place
-                    ctx->stats.kernel_launches += maxV ? radix_sort_launches(32) : 0;
+                    ctx->stats.kernel_launches += maxV ? radix_sort_launches(32, maxV) : 0;
                 }
                 if (dense_group) {  // one view: depth-prefix binning, synchronous on s
                     CK(cudaStreamSynchronize(sb));
@@ -615,7 +615,7 @@ void do_render(sgm_ctx* ctx, const sgm_map* map, const sgm_camera* camera, const
         exclusive_scan_u64<uint32_t>(ctx->ccount.as<uint32_t>(), px + 1,
                                      ctx->coffset.as<unsigned long long>(),
                                      ctx->scan_tmp.as<unsigned long long>(), ctx->stream);
-        ctx->stats.kernel_launches += 3;
+        ctx->stats.kernel_launches += exclusive_scan_launches(px + 1);
         unsigned long long total = 0;
         CK(cudaMemcpyAsync(&total, ctx->coffset.as<unsigned long long>() + px, 8,
                            cudaMemcpyDeviceToHost, ctx->stream));

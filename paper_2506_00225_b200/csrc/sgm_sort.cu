@@ -54,11 +54,15 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint32_t* __re
     }
 }
 
+// next_counts (not null): the next pass's per-tile digit histogram, accumulated here from each
+// element's destination (its next-pass tile) and next digit, so no histogram kernel runs
+// between the passes
 template <typename V, typename N>
 __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const uint32_t* __restrict__ kin, const V* __restrict__ vin,
                                                               uint32_t* __restrict__ kout, V* __restrict__ vout,
                                                               size_t stride, const N* __restrict__ n, int shift,
-                                                              int T, const uint32_t* __restrict__ counts) {
+                                                              int T, const uint32_t* __restrict__ counts,
+                                                              uint32_t* __restrict__ next_counts) {
     __shared__ uint32_t wc[kSortWarps][kRadix];  // per (warp, digit): count, then absolute base
     const int s = blockIdx.y, t = blockIdx.x;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -102,9 +106,13 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const uint32_t* _
         if (rank[r] == 0xffffffffu) continue;
         const uint64_t i = base + r * 32 + lane;
         const uint32_t d = rank[r] >> 16;
-        const size_t dst = so + wc[w][d] + (rank[r] & 0xffffu);
+        const uint32_t pos = wc[w][d] + (rank[r] & 0xffffu);
+        const size_t dst = so + pos;
         kout[dst] = key[r];
         vout[dst] = vin[so + i];
+        if (next_counts)
+            atomicAdd(&next_counts[(static_cast<size_t>(s) * kRadix + ((key[r] >> (shift + 8)) & 0xffu)) * T +
+                                   pos / kSortTile], 1u);
     }
 }
 
@@ -113,6 +121,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const uint32_t* _
 constexpr int kScanT = 1024;
 constexpr int kScanItems = 4;
 constexpr int kScanBlock = kScanT * kScanItems;
+constexpr uint64_t kSmallScanU64 = 32 * 1024;  // one-launch scans up to this many counts
 
 template <typename C>
 __global__ void __launch_bounds__(kScanT) k_scan_sums(const C* __restrict__ in, uint64_t n,
@@ -135,6 +144,68 @@ __global__ void __launch_bounds__(kScanT) k_scan_sums(const C* __restrict__ in, 
         unsigned long long u = ws[threadIdx.x];
         for (int o = 16; o > 0; o >>= 1) u += __shfl_down_sync(0xffffffffu, u, o);
         if (threadIdx.x == 0) sums[blockIdx.x] = u;
+    }
+}
+
+// Block-wide exclusive scan of one value per thread (1024 threads); returns the thread's
+// prefix and adds the block total to *carry (after every thread has read it).
+template <typename T>
+__device__ __forceinline__ T block_exclusive(T v, T* ws, T* carry) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    T x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        T u = ws[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const T y = __shfl_up_sync(0xffffffffu, u, o);
+            if (lane >= o) u += y;
+        }
+        ws[lane] = u;
+    }
+    __syncthreads();
+    const T r = *carry + (w ? ws[w - 1] : T(0)) + x - v;
+    __syncthreads();
+    if (threadIdx.x == kScanT - 1) *carry += ws[kScanT / 32 - 1];
+    __syncthreads();
+    return r;
+}
+
+constexpr int kSmallItems = 8;  // consecutive counts per thread per round of the one-block scans
+
+// per segment (block), exclusive scan in place of n u32 counts seg_stride apart, 8192 per
+// round (small arrays: one launch); also zeroes `zero` (the next pass's counts)
+__global__ void __launch_bounds__(kScanT) k_scan_small(uint32_t* __restrict__ a, uint64_t n, uint64_t seg_stride,
+                                                      uint32_t* __restrict__ zero) {
+    __shared__ uint32_t ws[kScanT / 32];
+    __shared__ uint32_t carry;
+    uint32_t* c = a + blockIdx.x * seg_stride;
+    if (zero)
+        for (uint64_t i = threadIdx.x; i < n; i += kScanT) zero[blockIdx.x * seg_stride + i] = 0u;
+    if (threadIdx.x == 0) carry = 0u;
+    __syncthreads();
+    for (uint64_t b0 = 0; b0 < n; b0 += static_cast<uint64_t>(kScanT) * kSmallItems) {
+        const uint64_t i0 = b0 + static_cast<uint64_t>(threadIdx.x) * kSmallItems;
+        uint32_t v[kSmallItems];
+        uint32_t sum = 0;
+#pragma unroll
+        for (int q = 0; q < kSmallItems; ++q) {
+            v[q] = i0 + q < n ? c[i0 + q] : 0u;
+            sum += v[q];
+        }
+        uint32_t run = block_exclusive<uint32_t>(sum, ws, &carry);
+#pragma unroll
+        for (int q = 0; q < kSmallItems; ++q)
+            if (i0 + q < n) {
+                c[i0 + q] = run;
+                run += v[q];
+            }
     }
 }
 
@@ -213,10 +284,13 @@ void exclusive_scan_u32_inplace(uint32_t* a, uint64_t n, int nseg, uint64_t seg_
 size_t radix_sort_scratch_bytes(uint64_t max_len, int nseg) {
     const uint64_t T = (std::max<uint64_t>(max_len, 1) + kSortTile - 1) / kSortTile;
     const size_t counts = sizeof(uint32_t) * static_cast<size_t>(nseg) * kRadix * T;
-    // + the block sums of the counts' scan (16-byte aligned)
+    // two count buffers + the block sums of the counts' scan (16-byte aligned)
     const uint64_t nb = (static_cast<uint64_t>(kRadix) * T + kScanBlock - 1) / kScanBlock;
-    return ((counts + 15) & ~size_t(15)) + 8 * (static_cast<size_t>(nseg) * nb + 2);
+    return 2 * ((counts + 15) & ~size_t(15)) + 8 * (static_cast<size_t>(nseg) * nb + 2);
 }
+
+// counts of up to this many per segment are scanned by one block in one launch
+constexpr uint64_t kSmallScan = 32 * 1024;
 
 template <typename V, typename N>
 bool radix_sort_pairs(uint32_t* keys, V* vals, uint32_t* keys_alt, V* vals_alt, size_t stride,
@@ -225,20 +299,36 @@ bool radix_sort_pairs(uint32_t* keys, V* vals, uint32_t* keys_alt, V* vals_alt, 
     if (max_len == 0 || nseg == 0) return false;
     const int T = static_cast<int>((max_len + kSortTile - 1) / kSortTile);
     const dim3 grid(static_cast<unsigned>(T), static_cast<unsigned>(nseg));
+    const uint64_t per = static_cast<uint64_t>(kRadix) * T;  // counts per segment
+    const size_t cb = ((sizeof(uint32_t) * static_cast<size_t>(nseg) * per) + 15) & ~size_t(15);
+    // two count buffers: this pass's (scanned) and the next pass's (built by the scatter)
+    uint32_t* cnt[2] = {scratch, reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(scratch) + cb)};
+    unsigned long long* sums = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(scratch) + 2 * cb);
+    const bool small = per <= kSmallScan;
+    // Small arrays (latency-bound, e.g. a single rendered view): the scatter also builds the next
+    // pass's histogram (global atomics) and one block scans the counts, so a pass is two
+    // launches. Large arrays: a histogram kernel per pass (the atomics would contend) and the
+    // multi-block scan.
     bool alt = false;
+    int c = 0;
+    if (small) k_sort_hist<N><<<grid, kSortThreads, 0, s>>>(keys, stride, d_n, 0, T, cnt[0]);
     for (int shift = 0; shift < end_bit; shift += 8) {
         const uint32_t* ki = alt ? keys_alt : keys;
         const V* vi = alt ? vals_alt : vals;
         uint32_t* ko = alt ? keys : keys_alt;
         V* vo = alt ? vals : vals_alt;
-        k_sort_hist<N><<<grid, kSortThreads, 0, s>>>(ki, stride, d_n, shift, T, scratch);
-        {  // coalesced multi-block scan of each segment's 256 T counts
-            const size_t cb = ((sizeof(uint32_t) * static_cast<size_t>(nseg) * kRadix * T) + 15) & ~size_t(15);
-            exclusive_scan_u32_inplace(scratch, static_cast<uint64_t>(kRadix) * T, nseg,
-                                       static_cast<uint64_t>(kRadix) * T,
-                                       reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(scratch) + cb), s);
+        const bool more = shift + 8 < end_bit;
+        if (small) {  // one block per segment; it also clears the next pass's counts
+            k_scan_small<<<nseg, kScanT, 0, s>>>(cnt[c], per, per, more ? cnt[c ^ 1] : nullptr);
+            k_sort_scatter<V, N><<<grid, kSortThreads, 0, s>>>(ki, vi, ko, vo, stride, d_n, shift, T, cnt[c],
+                                                               more ? cnt[c ^ 1] : nullptr);
+            c ^= 1;
+        } else {
+            k_sort_hist<N><<<grid, kSortThreads, 0, s>>>(ki, stride, d_n, shift, T, cnt[0]);
+            exclusive_scan_u32_inplace(cnt[0], per, nseg, per, sums, s);
+            k_sort_scatter<V, N><<<grid, kSortThreads, 0, s>>>(ki, vi, ko, vo, stride, d_n, shift, T, cnt[0],
+                                                               nullptr);
         }
-        k_sort_scatter<V, N><<<grid, kSortThreads, 0, s>>>(ki, vi, ko, vo, stride, d_n, shift, T, scratch);
         alt = !alt;
     }
     return alt;
@@ -251,16 +341,53 @@ template bool radix_sort_pairs<unsigned long long, unsigned long long>(
     uint32_t*, unsigned long long*, uint32_t*, unsigned long long*, size_t, const unsigned long long*,
     uint64_t, int, int, uint32_t*, cudaStream_t);
 
-int radix_sort_launches(int end_bit) { return 5 * ((end_bit + 7) / 8); }
+int radix_sort_launches(int end_bit, uint64_t max_len) {
+    const uint64_t T = (std::max<uint64_t>(max_len, 1) + kSortTile - 1) / kSortTile;
+    const bool small = static_cast<uint64_t>(kRadix) * T <= kSmallScan;
+    return small ? 1 + ((end_bit + 7) / 8) * 2 : ((end_bit + 7) / 8) * 5;
+}
+
+int exclusive_scan_launches(uint64_t n) { return n <= kSmallScanU64 ? 1 : 3; }
 
 size_t exclusive_scan_scratch_bytes(uint64_t n) {
     return sizeof(unsigned long long) * ((std::max<uint64_t>(n, 1) + kScanBlock - 1) / kScanBlock + 1);
+}
+
+// one block, one launch: exclusive scan of n counts into u64 offsets (small n)
+template <typename C>
+__global__ void __launch_bounds__(kScanT) k_scan_small_u64(const C* __restrict__ in, uint64_t n,
+                                                          unsigned long long* __restrict__ out) {
+    __shared__ unsigned long long ws[kScanT / 32];
+    __shared__ unsigned long long carry;
+    if (threadIdx.x == 0) carry = 0ull;
+    __syncthreads();
+    for (uint64_t b0 = 0; b0 < n; b0 += static_cast<uint64_t>(kScanT) * kSmallItems) {
+        const uint64_t i0 = b0 + static_cast<uint64_t>(threadIdx.x) * kSmallItems;
+        unsigned long long v[kSmallItems];
+        unsigned long long sum = 0;
+#pragma unroll
+        for (int q = 0; q < kSmallItems; ++q) {
+            v[q] = i0 + q < n ? static_cast<unsigned long long>(in[i0 + q]) : 0ull;
+            sum += v[q];
+        }
+        unsigned long long run = block_exclusive<unsigned long long>(sum, ws, &carry);
+#pragma unroll
+        for (int q = 0; q < kSmallItems; ++q)
+            if (i0 + q < n) {
+                out[i0 + q] = run;
+                run += v[q];
+            }
+    }
 }
 
 template <typename C>
 void exclusive_scan_u64(const C* in, uint64_t n, unsigned long long* out, unsigned long long* scratch,
                         cudaStream_t s) {
     if (n == 0) return;
+    if (n <= kSmallScanU64) {
+        k_scan_small_u64<C><<<1, kScanT, 0, s>>>(in, n, out);
+        return;
+    }
     const uint32_t nb = static_cast<uint32_t>((n + kScanBlock - 1) / kScanBlock);
     k_scan_sums<C><<<nb, kScanT, 0, s>>>(in, n, scratch);
     k_scan_top<<<1, kScanT, 0, s>>>(scratch, nb);
