@@ -44,3 +44,21 @@ def e2e():
 
 print(f"upload {t(up):.2f} ms  score-resident {t(lambda: score_poses(gm, cam, poses, ctx=ctx)):.2f} ms  "
       f"e2e {t(e2e):.2f} ms", flush=True)
+
+# the two upload phases: the async call returns after phase A (geometry); sgm_map_wait covers
+# phase B (colours + rows staging, their copies and the row sort)
+import ctypes as C  # noqa: E402
+from paper_2506_00225_b200 import _native as N  # noqa: E402
+ta, tb = [], []
+for _ in range(5):
+    gm.touch()
+    ctx.synchronize()
+    t0 = time.perf_counter()
+    h, keep = ctx._upload_async(gm)
+    t1 = time.perf_counter()
+    N.lib.sgm_map_wait(ctx.handle, h)
+    t2 = time.perf_counter()
+    N.lib.sgm_map_release(ctx.handle, h)
+    ta.append(1e3 * (t1 - t0))
+    tb.append(1e3 * (t2 - t1))
+print(f"upload phase A {np.median(ta):.2f} ms, phase B + copies {np.median(tb):.2f} ms", flush=True)
