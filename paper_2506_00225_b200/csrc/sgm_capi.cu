@@ -168,6 +168,7 @@ int sgm_map_upload_async(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classe
         ctx->take(m->prob, 8 * ns * kpad);
         ctx->take(m->perm, 2 * ns * kpad);
         ctx->take(m->gbnd, 16 * ns);
+        ctx->take(m->rec, 16 * ns * kpad);
         CK(m->geo.reserve(geo_b));
         CK(m->color.reserve(col_b));
         CK(m->idx.reserve(2 * ns * kpad));
@@ -363,6 +364,7 @@ void sgm_map_release(sgm_ctx* ctx, sgm_map* map) {
         ctx->give(std::move(map->perm));
         ctx->give(std::move(map->cov));
         ctx->give(std::move(map->gbnd));
+        ctx->give(std::move(map->rec));
     }
     if (map->ev_rows) cudaEventDestroy(map->ev_rows);
     delete map;

@@ -61,6 +61,7 @@ void trainer_rebuild(sgm_ctx* ctx, sgm_trainer* tr) {
     d.dup_idx = tr->dup;
     m.groups = choose_groups(C, k);
     map_group_bounds(ctx, &m, s);
+    m.rec_valid = false;
     if (ctx->last_map == &m) ctx->last_valid = false;
 }
 
@@ -739,6 +740,7 @@ int sgm_optimize_map(sgm_ctx* ctx, sgm_trainer* tr, const sgm_camera* camera, ui
                         tr->V.as<double>(), tr->n, tr->k, h, bc1, bc2, s);
             launch_derive(tr->P.as<double>(), tr->n, tr->k, tr->map.dev.kpad, tr->map.dev.sem_perm,
                           tr->map.geo.as<double>(), tr->map.color.as<double>(), tr->map.prob.as<double>(), s);
+            tr->map.rec_valid = false;
             ctx->stats.kernel_launches += 3;
             CK(cudaGetLastError());
             if (ctx->last_map == &tr->map) ctx->last_valid = false;

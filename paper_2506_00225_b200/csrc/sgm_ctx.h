@@ -138,6 +138,8 @@ struct sgm_map {
     DevBuf perm;   // [n][kpad] u16 original entry index
     DevBuf cov;    // anisotropic mode: [6][n] world covariance (sgm_map_set_anisotropic)
     DevBuf gbnd;   // [n] uint4: class-sorted rows' channel-group bounds (DevMap::gbounds)
+    DevBuf rec;    // [n][kpad] uint4: DevMap::sem_rec (map_records), valid while rec_valid
+    bool rec_valid = false;  // cleared wherever sem_prob / sem_idx change
     // Upload split in two (sgm_map_upload): the geometry is staged and copied on the ctx
     // stream before the call returns; the colours and semantic rows are staged by
     // rows_thread and copied / sorted on the ctx's upload stream, ending at ev_rows. The
@@ -217,6 +219,8 @@ namespace sgm {
 void map_ready(sgm_ctx* ctx, const sgm_map* map);
 // Channel-group bounds of a map whose rows are sorted on the device (stream s).
 void map_group_bounds(sgm_ctx* ctx, sgm_map* map, cudaStream_t s);
+// builds DevMap::sem_rec on ctx->stream unless still valid (after map_ready)
+void map_records(sgm_ctx* ctx, const sgm_map* map);
 CamParams to_cam(const sgm_camera* c);
 OptParams to_opt(const sgm_options* o, const CamParams& cam);
 PoseParams to_pose(const sgm_pose& p);

@@ -42,6 +42,10 @@ struct DevMap {
     // per Gaussian: the ends of its class-sorted row's 8 raster channel groups (u16 each),
     // computed once per map (launch_group_bounds); the raster stages them with the rows
     const uint4* gbounds = nullptr;
+    // the class-sorted rows as 16-byte records {prob (lo, hi words), class, 0}, [n][kpad]:
+    // one shared-memory load per (entry, class) in the score raster's scatter. Built from
+    // sem_idx / sem_prob before a score pass (launch_sem_records; map_records)
+    const uint4* sem_rec = nullptr;
 };
 
 struct CamParams {
@@ -244,6 +248,7 @@ void launch_bins_to_ids(const uint32_t* list, uint64_t P, const PackedSplat* pac
 void launch_sort_rows(const uint16_t* idx, const double* prob, uint64_t n, int k, int kpad,
                       uint16_t* out_idx, double* out_prob, uint16_t* out_perm, cudaStream_t s);
 void launch_group_bounds(const DevMap& m, const GroupParams& gp, uint4* out, cudaStream_t s);
+void launch_sem_records(const DevMap& m, uint4* out, cudaStream_t s);
 // sgm_backward.cu
 size_t backward_loss_blocks(int W, int H);
 void launch_loss_pixels(const BackwardParams& b, double* part, double* totals, cudaStream_t s);
@@ -328,5 +333,7 @@ void exclusive_scan_u64(const C* in, uint64_t n, unsigned long long* out, unsign
 // sgm_raster.cu
 GroupParams choose_groups(int C, int k);
 size_t raster_smem_bytes(const DevMap& m, const GroupParams& gp, bool render);
+// the score raster runs 4 CTAs per SM, staging DevMap::sem_rec (needs map_records)
+bool raster_score_records(const DevMap& m);
 
 }  // namespace sgm

@@ -957,6 +957,22 @@ void launch_sort_rows(const uint16_t* idx, const double* prob, uint64_t n, int k
                                                    out_perm);
 }
 
+// DevMap::sem_rec from the class-sorted rows: one thread per (Gaussian, slot), coalesced
+__global__ void k_sem_records(const uint16_t* __restrict__ idx, const double* __restrict__ prob,
+                              uint64_t slots, uint4* __restrict__ out) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= slots) return;
+    const double pv = prob[i];
+    out[i] = make_uint4(static_cast<unsigned>(__double2loint(pv)), static_cast<unsigned>(__double2hiint(pv)),
+                        idx[i], 0u);
+}
+
+void launch_sem_records(const DevMap& m, uint4* out, cudaStream_t s) {
+    const uint64_t slots = m.n * static_cast<uint64_t>(m.kpad);
+    if (slots == 0) return;
+    k_sem_records<<<blocks_for(slots, 256), 256, 0, s>>>(m.sem_idx, m.sem_prob, slots, out);
+}
+
 void launch_group_bounds(const DevMap& m, const GroupParams& gp, uint4* out, cudaStream_t s) {
     if (m.n == 0) return;
     k_group_bounds<<<blocks_for(m.n, 256), 256, 0, s>>>(m, gp, out);

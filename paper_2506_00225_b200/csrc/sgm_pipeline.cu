@@ -436,6 +436,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                     CK(cudaStreamSynchronize(sb));
                     if (!rows_ready) {
                         map_ready(ctx, map);
+                        if (raster_score_records(map->dev)) map_records(ctx, map);
                         rows_ready = true;
                         rp.map = map->dev;
                     }
@@ -458,6 +459,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 // the binning just queued runs meanwhile
                 if (!rows_ready) {
                     map_ready(ctx, map);
+                    if (mode == Mode::Score && raster_score_records(map->dev)) map_records(ctx, map);
                     rows_ready = true;
                     rp.map = map->dev;  // (dup_idx known now)
                 }
@@ -551,6 +553,16 @@ void map_ready(sgm_ctx* ctx, const sgm_map* cmap) {
     if (map->rows_code != SGM_OK) fail(map->rows_code, "map upload: %s", map->rows_msg.c_str());
     if (map->ev_rows) CK(cudaStreamWaitEvent(ctx->stream, map->ev_rows, 0));
     if (!map->dev.gbounds && map->dev.n) map_group_bounds(ctx, map, ctx->stream);
+}
+
+void map_records(sgm_ctx* ctx, const sgm_map* cmap) {
+    sgm_map* map = const_cast<sgm_map*>(cmap);  // a derived array, like the group bounds
+    if (map->rec_valid || map->dev.n == 0) return;
+    CK(map->rec.reserve(16 * map->dev.n * static_cast<size_t>(map->dev.kpad)));
+    map->dev.sem_rec = map->rec.as<uint4>();
+    launch_sem_records(map->dev, map->rec.as<uint4>(), ctx->stream);
+    ctx->stats.kernel_launches += 1;
+    map->rec_valid = true;
 }
 
 void map_group_bounds(sgm_ctx* ctx, sgm_map* map, cudaStream_t s) {

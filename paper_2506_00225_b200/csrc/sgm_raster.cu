@@ -28,6 +28,7 @@
 // entropy and exact-zero-silhouette count go to a per-tile slot that a second
 // kernel sums in a fixed order (deterministic, batching/sharding-invariant).
 #include <algorithm>
+#include <stdexcept>
 
 #include "sgm_internal.h"
 #include "sgm_device.cuh"
@@ -62,7 +63,7 @@ struct Layout {  // byte offsets in dynamic shared memory
 // nearly conflict-free)
 __host__ __device__ constexpr int acc_pitch(bool render) { return render ? 33 : 32; }
 
-__host__ __device__ inline Layout make_layout(int C, int kpad, bool render, bool color = false) {
+__host__ __device__ inline Layout make_layout(int C, int kpad, bool render, bool color = false, bool recs = false) {
     Layout L;
     L.acc = 0;
     L.w = align16(C * acc_pitch(render) * 16);
@@ -74,8 +75,13 @@ __host__ __device__ inline Layout make_layout(int C, int kpad, bool render, bool
     L.st_packed = 0;
     L.st_bnd = kNB * static_cast<int>(sizeof(PackedSplat));      // [kNB] uint4 group bounds
     L.st_idx = L.st_bnd + kNB * 16;
-    L.st_prob = L.st_idx + kNB * kpad * 2;
-    L.st_color = L.st_prob + kNB * kpad * 8;
+    if (recs) {  // the 4-CTA score launch stages 16-byte records (DevMap::sem_rec)
+        L.st_prob = L.st_idx;
+        L.st_color = L.st_idx + kNB * kpad * 16;
+    } else {
+        L.st_prob = L.st_idx + kNB * kpad * 2;
+        L.st_color = L.st_prob + kNB * kpad * 8;
+    }
     L.stage_bytes = L.st_color + ((render || color) ? kNB * 32 : 0);
     L.total = L.stage0 + 2 * L.stage_bytes;
     // the score epilogue's per-(group, pixel) (S1, S2) exchange reuses the stages
@@ -120,7 +126,8 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     const int Cg = p.groups.Cg;
     constexpr int apitch = acc_pitch(kRender);
     static_assert(!(kRc && kRender), "rc4 is a score-mode output");
-    const Layout L = make_layout(C, kpad, kRender, kRc);
+    constexpr bool kRecs = !kRender && !kRc && kOcc == 4;  // (and kBulk)
+    const Layout L = make_layout(C, kpad, kRender, kRc, kRecs);
     double2* acc2 = reinterpret_cast<double2*>(smem + L.acc);     // [C][apitch]
     double* acc = reinterpret_cast<double*>(smem + L.acc);
     double* W = reinterpret_cast<double*>(smem + L.w);             // [kNB][32] double2
@@ -181,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         if constexpr (kBulk) {
             const uint32_t bar = smem_addr(&s_mbar[st]);
             if (lane == 0)
-                mbar_expect_tx(bar, static_cast<unsigned>(n) * (64u + 16u + 10u * static_cast<unsigned>(kpad)));
+                mbar_expect_tx(bar, static_cast<unsigned>(n) * (64u + 16u + (kRecs ? 16u : 10u) * static_cast<unsigned>(kpad)));
             __syncwarp();
             if (lane < n) {
                 const uint2 v = rm[st * kNB + lane];
@@ -189,10 +196,15 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                 fence_proxy_async();
                 bulk_g2s(sb + L.st_packed + lane * 64, ls.packed + v.x, 64u, bar);
                 bulk_g2s(sb + L.st_bnd + lane * 16, p.map.gbounds + v.y, 16u, bar);
-                bulk_g2s(sb + L.st_idx + lane * kpad * 2, p.map.sem_idx + static_cast<size_t>(v.y) * kpad,
-                         2u * kpad, bar);
-                bulk_g2s(sb + L.st_prob + lane * kpad * 8, p.map.sem_prob + static_cast<size_t>(v.y) * kpad,
-                         8u * kpad, bar);
+                if (kRecs) {
+                    bulk_g2s(sb + L.st_idx + lane * kpad * 16, p.map.sem_rec + static_cast<size_t>(v.y) * kpad,
+                             16u * kpad, bar);
+                } else {
+                    bulk_g2s(sb + L.st_idx + lane * kpad * 2, p.map.sem_idx + static_cast<size_t>(v.y) * kpad,
+                             2u * kpad, bar);
+                    bulk_g2s(sb + L.st_prob + lane * kpad * 8, p.map.sem_prob + static_cast<size_t>(v.y) * kpad,
+                             8u * kpad, bar);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(bar);
@@ -387,6 +399,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
             const uint16_t* sbnd = reinterpret_cast<const uint16_t*>(sb + L.st_bnd);  // [kNB][8]
             const uint16_t* si = reinterpret_cast<const uint16_t*>(sb + L.st_idx);
             const double* spr = reinterpret_cast<const double*>(sb + L.st_prob);
+            const uint4* srec = reinterpret_cast<const uint4*>(sb + L.st_idx);  // (kRecs)
             const double* scol = reinterpret_cast<const double*>(sb + L.st_color);
 
             // footprint of entry e at this thread's pixel (:276-285); -1 = not a contributor
@@ -551,6 +564,18 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                     const bool nz = (w.x != 0.0) | (w.y != 0.0);
                     const uint16_t* ei = si + e * kpad;
                     const double* ep = spr + e * kpad;
+                    const uint4* er = srec + e * kpad;
+                    // slot j's (class, probability): one broadcast LDS.128 of the record (kRecs)
+                    auto cls = [&](int j, double& pj) -> int {
+                        if constexpr (kRecs) {
+                            const uint4 r = er[j];
+                            pj = __hiloint2double(static_cast<int>(r.y), static_cast<int>(r.x));
+                            return static_cast<int>(r.z);
+                        } else {
+                            pj = ep[j];
+                            return ei[j];
+                        }
+                    };
                     // lanes without weight skip the read-modify-writes: predicated shared loads
                     // and stores (no branch, the warp stays converged), so their quarter-warps
                     // issue no wavefronts; the FMAs on the unloaded registers are discarded
@@ -568,13 +593,17 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                     };
                     if (kDup) {
 #pragma unroll 1
-                        for (int j = lo; j < hi; ++j) rmw(ei[j], ep[j]);  // repeated classes: in order
+                        for (int j = lo; j < hi; ++j) {  // repeated classes: in order
+                            double pj;
+                            const int c = cls(j, pj);
+                            rmw(c, pj);
+                        }
                     } else {
                         int j = lo;
 #pragma unroll 1
                         for (; j + 2 <= hi; j += 2) {  // two distinct classes: both loads first
-                            const int c0 = ei[j], c1 = ei[j + 1];
-                            const double p0 = ep[j], p1 = ep[j + 1];
+                            double p0, p1;
+                            const int c0 = cls(j, p0), c1 = cls(j + 1, p1);
                             const unsigned s0 = static_cast<unsigned>(__cvta_generic_to_shared(accl + c0 * apitch));
                             const unsigned s1 = static_cast<unsigned>(__cvta_generic_to_shared(accl + c1 * apitch));
                             double ax, ay, bx, by;
@@ -593,7 +622,11 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                                          :: "r"(pz), "r"(s0), "r"(s1), "d"(ax), "d"(ay), "d"(bx), "d"(by)
                                          : "memory");
                         }
-                        if (j < hi) rmw(ei[j], ep[j]);
+                        if (j < hi) {
+                            double pj;
+                            const int c = cls(j, pj);
+                            rmw(c, pj);
+                        }
                     }
                 }
             }
@@ -737,8 +770,10 @@ void launch_t(const RasterParams& p0, int n_views, cudaStream_t s) {
     if (p.n_items == 0) return;
     const size_t smem = static_cast<size_t>(make_layout(p.map.C, p.map.kpad, kRender, kRc).total);
     // four CTAs per SM when four fit in shared memory (228 KB, 1 KB reserved per CTA)
-    // (score mode only: the render and rc variants would spill at the 4-CTA register budget)
-    const bool four = !kRender && !kRc && smem + 2048 <= 228 * 1024 / 4;
+    // (score mode only: the render and rc variants would spill at the 4-CTA register budget);
+    // that variant stages the 16-byte semantic records
+    const bool four = !kRender && !kRc && raster_score_records(p.map);
+    const size_t smem4 = static_cast<size_t>(make_layout(p.map.C, p.map.kpad, false, false, true).total);
     // (render: usually one view per launch, so shorter CTAs balance the last wave better)
     p.items_per_cta = kRender ? 2 : kItemsPerCta;
     const int grid = (p.n_items + p.items_per_cta - 1) / p.items_per_cta;
@@ -750,9 +785,10 @@ void launch_t(const RasterParams& p0, int n_views, cudaStream_t s) {
             return;
         }
         if (four) {
+            if (p.map.n && !p.map.sem_rec) throw std::logic_error("score raster: DevMap::sem_rec not built (map_records)");
             cudaFuncSetAttribute(k_raster<kRender, kDup, kAniso, kRc, 4, false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            k_raster<kRender, kDup, kAniso, kRc, 4, false><<<grid, kThreads, smem, s>>>(p);
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem4));
+            k_raster<kRender, kDup, kAniso, kRc, 4, false><<<grid, kThreads, smem4, s>>>(p);
             return;
         }
     }
@@ -777,6 +813,10 @@ GroupParams choose_groups(int C, int k) {
     gp.P = kGroups;
     gp.Cg = (C + kGroups - 1) / kGroups;
     return gp;
+}
+
+bool raster_score_records(const DevMap& m) {
+    return make_layout(m.C, m.kpad, false, false, true).total + 2048 <= 228 * 1024 / 4;
 }
 
 size_t raster_smem_bytes(const DevMap& m, const GroupParams& gp, bool render) {
