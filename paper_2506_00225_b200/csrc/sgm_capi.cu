@@ -180,6 +180,10 @@ int sgm_map_upload_async(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classe
         const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
         const unsigned nth = n > 65536 ? hw : 1;
         const unsigned kChunks = n > 65536 ? 8 : 1;
+        // phase B's copies start per 1/16 of the rows, so the staging and the H2D copies overlap
+        const unsigned kChunksB = n > 65536 ? 16 : 1;
+        if (nth > 1 && (!ctx->workers || ctx->workers->size() < nth)) ctx->workers.reset(new HostPool(nth));
+        HostPool* pool = nth > 1 ? ctx->workers.get() : nullptr;
         // ---- phase A: geometry + activations, chunk copies on s ----
         std::unique_ptr<std::atomic<unsigned>[]> finished(new std::atomic<unsigned>[kChunks]);
         for (unsigned c = 0; c < kChunks; ++c) finished[c].store(0);
@@ -198,9 +202,8 @@ int sgm_map_upload_async(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classe
             }
         };
         {
-            std::vector<std::thread> pool;
-            for (unsigned w = 1; w < nth; ++w) pool.emplace_back(work_a, w);
-            std::thread self(work_a, 0u);
+            if (pool) pool->start(nth, work_a);
+            else work_a(0);
             cudaError_t copy_err = cudaSuccess;
             for (unsigned c = 0; c < kChunks; ++c) {
                 while (finished[c].load(std::memory_order_acquire) < nth) std::this_thread::yield();
@@ -210,8 +213,7 @@ int sgm_map_upload_async(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classe
                     copy_err = cudaMemcpyAsync(m->geo.as<double>() + f * ns + ca, geo + f * ns + ca,
                                                8 * (cb - ca), cudaMemcpyHostToDevice, s);
             }
-            self.join();
-            for (auto& th : pool) th.join();
+            if (pool) pool->wait();
             CK(copy_err);
             CK(cudaEventRecord(ctx->ev_hstage, s));
         }
@@ -244,6 +246,7 @@ int sgm_map_upload_async(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classe
         m->rows_thread = std::thread([=]() {
             try {
                 CK(cudaSetDevice(device));
+                const unsigned kChunks = kChunksB;
                 std::unique_ptr<std::atomic<unsigned>[]> done(new std::atomic<unsigned>[kChunks]);
                 for (unsigned c = 0; c < kChunks; ++c) done[c].store(0);
                 std::vector<int> bad(nth, -1), dup(nth, 0);
@@ -271,9 +274,8 @@ int sgm_map_upload_async(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classe
                         done[c].fetch_add(1, std::memory_order_release);
                     }
                 };
-                std::vector<std::thread> pool;
-                for (unsigned w = 1; w < nth; ++w) pool.emplace_back(work_b, w);
-                std::thread self(work_b, 0u);
+                if (pool) pool->start(nth, work_b);
+                else work_b(0);
                 cudaError_t e = cudaSuccess;
                 for (unsigned c = 0; c < kChunks; ++c) {
                     while (done[c].load(std::memory_order_acquire) < nth) std::this_thread::yield();
@@ -289,8 +291,7 @@ int sgm_map_upload_async(sgm_ctx* ctx, uint64_t n, int32_t k, int32_t num_classe
                         e = cudaMemcpyAsync(draw + prob_b + 2 * k * ca, ridx + k * ca, 2 * k * (cb - ca),
                                             cudaMemcpyHostToDevice, us);
                 }
-                self.join();
-                for (auto& th : pool) th.join();
+                if (pool) pool->wait();
                 CK(e);
                 CK(cudaEventRecord(ev_hrows, us));
                 for (unsigned w = 0; w < nth; ++w) {

@@ -9,11 +9,13 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <functional>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <thread>
@@ -24,6 +26,65 @@
 
 namespace sgm {
 
+
+// Persistent host workers for the map upload's staging (spawning 16 threads per upload cost
+// about 0.3 ms per phase on the bench host). start(n, fn) runs fn(0) .. fn(n - 1) on n
+// workers and returns at once; wait() blocks until they are done. One job at a time.
+class HostPool {
+public:
+    explicit HostPool(unsigned n) {
+        for (unsigned w = 0; w < n; ++w) th_.emplace_back([this, w] { loop(w); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    unsigned size() const { return static_cast<unsigned>(th_.size()); }
+    void start(unsigned n, std::function<void(unsigned)> fn) {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            fn_ = std::move(fn);
+            active_ = std::min<unsigned>(n, size());
+            left_ = active_;
+            ++gen_;
+        }
+        cv_.notify_all();
+    }
+    void wait() {
+        std::unique_lock<std::mutex> g(mu_);
+        done_cv_.wait(g, [this] { return left_ == 0; });
+    }
+
+private:
+    void loop(unsigned w) {
+        uint64_t seen = 0;
+        for (;;) {
+            std::function<void(unsigned)> fn;
+            {
+                std::unique_lock<std::mutex> g(mu_);
+                cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                if (w >= active_) continue;
+                fn = fn_;
+            }
+            fn(w);
+            std::lock_guard<std::mutex> g(mu_);
+            if (--left_ == 0) done_cv_.notify_all();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    std::function<void(unsigned)> fn_;
+    unsigned active_ = 0, left_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
 
 struct DevBuf {
     void* p = nullptr;
@@ -162,6 +223,7 @@ struct sgm_ctx {
     cudaStream_t bin_stream = nullptr;  // binning of the next sub-batch overlaps the raster
     cudaStream_t up_stream = nullptr;   // map uploads: colours / semantic rows (sgm_map_upload)
     sgm_map* rows_owner = nullptr;      // the map whose rows_thread uses h_rows
+    std::unique_ptr<HostPool> workers;  // upload staging workers (created on the first large upload)
     cudaEvent_t ev_hstage = nullptr;    // the last copy out of h_stage (geometry) / h_rows
     cudaEvent_t ev_hrows = nullptr;
     cudaEvent_t ev_ready = nullptr;
