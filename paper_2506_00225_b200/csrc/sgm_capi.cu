@@ -42,6 +42,10 @@ int sgm_ctx_create(int device, sgm_ctx** out) {
         // block scheduler slots them in as raster CTAs of the previous sub-batch retire
         CK(cudaStreamCreateWithPriority(&ctx->bin_stream, cudaStreamNonBlocking, prio_high));
         CK(cudaStreamCreateWithFlags(&ctx->up_stream, cudaStreamNonBlocking));
+        size_t free_b = 0, total_b = 0;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        // tile lists of one group of views: a fifth of the device (36 GB on a B200), at least 8 GB
+        ctx->list_budget = std::max<uint64_t>(uint64_t(8) << 30, total_b / 5) / 4;
         for (auto& ev : ctx->ev) CK(cudaEventCreate(&ev));
         CK(cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming));
         for (auto& ev : ctx->ev_binned) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));

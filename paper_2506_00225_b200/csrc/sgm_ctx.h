@@ -223,6 +223,7 @@ struct sgm_ctx {
     cudaStream_t bin_stream = nullptr;  // binning of the next sub-batch overlaps the raster
     cudaStream_t up_stream = nullptr;   // map uploads: colours / semantic rows (sgm_map_upload)
     sgm_map* rows_owner = nullptr;      // the map whose rows_thread uses h_rows
+    uint64_t list_budget = uint64_t(2) << 30;  // u32 tile-list entries per group of views
     std::unique_ptr<HostPool> workers;  // upload staging workers (created on the first large upload)
     cudaEvent_t ev_hstage = nullptr;    // the last copy out of h_stage (geometry) / h_rows
     cudaEvent_t ev_hrows = nullptr;

@@ -333,9 +333,12 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
         std::vector<uint64_t> P(hp, hp + nb);
         std::vector<uint64_t> R(hp + nb, hp + 2 * nb);  // (row, rank) pairs of the binning
 
-        // groups of views whose pair lists fit the budget together; a dense view of the plain
-        // score mode is a group of its own (depth-prefix binning, score_dense_view)
-        const uint64_t pair_budget = (uint64_t(8) << 30) / 4;  // u32 list entries
+        // groups of views whose pair lists fit ctx->list_budget together (a fifth of the device:
+        // several cfg4-dense views per group, so the binning of one overlaps the raster of the
+        // previous); a view past 2^31 entries in the plain score mode is a group of its own
+        // (depth-prefix binning, score_dense_view)
+        const uint64_t pair_budget = ctx->list_budget;
+        const uint64_t dense_pairs = uint64_t(2) << 30;
         // Depth-prefix binning serves the views whose full lists exceed the list budget (or
         // 2^32 pairs). It is exact but not faster than full bins that fit (the binning of a
         // full view overlaps the previous raster; the prefix path is synchronous), so full
@@ -346,7 +349,7 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
         auto dense = [&](int v) {
             if (prefix_mode == 0 || mode != Mode::Score || fk != Fisher::None) return false;
             if (P[v] <= kDenseAvg * static_cast<uint64_t>(bin_tiles)) return false;
-            return prefix_mode == 2 || P[v] > pair_budget;
+            return prefix_mode == 2 || P[v] > dense_pairs;
         };
         int v0 = 0;
         while (v0 < nb) {
