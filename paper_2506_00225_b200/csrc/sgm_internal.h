@@ -227,7 +227,7 @@ void launch_emit_rows(const unsigned long long* offsets, const int4* rects, uint
 void launch_row_scatter(const unsigned long long* row_list, const uint2* row_ranges,
                         const uint2* tile_ranges, int tiles_x, int tiles_y, uint64_t R, uint4* segs,
                         uint32_t* nseg, uint32_t* cnt, uint32_t* list, cudaStream_t s,
-                        const uint8_t* mask = nullptr, bool part = false);
+                        const uint8_t* mask = nullptr, bool part = false, bool cols = false);
 uint64_t row_scatter_segments(uint64_t R, int tiles_y);  // upper bound on segments
 void launch_seg_pass(const unsigned long long* row_list, const uint2* tile_ranges, int tiles_x,
                      uint64_t G, const uint4* segs, const uint32_t* nseg, const uint32_t* cnt,

@@ -622,6 +622,49 @@ __global__ void __launch_bounds__(256) k_seg_pass(const unsigned long long* __re
     }
 }
 
+// Dense rows (cfg4: entries spanning tens of columns): one CTA per segment, the segment's
+// column spans in registers (32 entries per lane) and ranks in shared memory; each warp walks
+// whole columns, so a column's share of the segment (hundreds of entries) is written by one
+// warp front to back: full sectors, instead of the block walk's few-entry pieces per chunk.
+__global__ void __launch_bounds__(256) k_seg_pass_cols(const unsigned long long* __restrict__ row_list,
+                                                       const uint4* __restrict__ segs,
+                                                       const uint32_t* __restrict__ nseg, int tiles_x,
+                                                       const uint32_t* __restrict__ cnt,
+                                                       uint32_t* __restrict__ list) {
+    __shared__ uint32_t srank[kSeg];
+    const uint32_t g = blockIdx.x;
+    if (g >= *nseg) return;
+    const uint4 sg = segs[g];
+    const int n = static_cast<int>(sg.z - sg.y);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int kPer = kSeg / 32;
+    // entry 32 k + lane of the segment: column span start and width (empty past the end)
+    uint32_t x0[kPer], wd[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const int i = 32 * k + lane;
+        const unsigned long long e = i < n ? row_list[sg.y + i] : 0ull;
+        if (warp == 0 && i < n) srank[i] = static_cast<uint32_t>(e >> 32);
+        const uint32_t a = static_cast<uint32_t>((e >> 16) & 0xffffu), b = static_cast<uint32_t>(e & 0xffffu);
+        x0[k] = i < n ? a : 0xffffu;
+        wd[k] = i < n ? b - a : 0u;
+    }
+    __syncthreads();
+    const uint32_t lt = (1u << lane) - 1u;
+    const int nk = (n + 31) / 32;
+    for (int col = warp; col < tiles_x; col += blockDim.x >> 5) {
+        uint32_t cur = cnt[static_cast<size_t>(g) * tiles_x + col];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            if (k >= nk) break;
+            const bool cov = static_cast<uint32_t>(col) - x0[k] <= wd[k];
+            const uint32_t bal = __ballot_sync(0xffffffffu, cov);
+            if (cov) list[cur + __popc(bal & lt)] = srank[32 * k + lane];
+            cur += __popc(bal);
+        }
+    }
+}
+
 // Pass 0 without ballots: a segment's per-column counts from a shared-memory difference
 // array (+1 at x0, -1 at x1 + 1 per entry), prefix-summed over the columns.
 __global__ void __launch_bounds__(256) k_seg_count(const unsigned long long* __restrict__ row_list,
@@ -892,7 +935,7 @@ void launch_redo_items(const uint32_t* incomplete, uint32_t n, uint32_t view, in
 void launch_row_scatter(const unsigned long long* row_list, const uint2* row_ranges,
                         const uint2* tile_ranges, int tiles_x, int tiles_y, uint64_t R, uint4* segs,
                         uint32_t* nseg, uint32_t* cnt, uint32_t* list, cudaStream_t s,
-                        const uint8_t* mask, bool part) {
+                        const uint8_t* mask, bool part, bool cols) {
     if (R == 0) return;
     const uint64_t gmax = R / kSeg + static_cast<uint64_t>(tiles_y) + 1;
     k_row_segs<<<1, 1024, 0, s>>>(row_ranges, tiles_y, segs, nseg);
@@ -905,6 +948,8 @@ void launch_row_scatter(const unsigned long long* row_list, const uint2* row_ran
         segs, nseg, part ? nullptr : tile_ranges, tiles_x, tiles_y, cnt);
     if (part)
         k_seg_pass<true><<<grid, 32 * warps, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list, mask, tile_ranges);
+    else if (cols)
+        k_seg_pass_cols<<<static_cast<unsigned>(gmax), 256, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list);
     else
         k_seg_pass<false><<<grid, 32 * warps, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list, nullptr, nullptr);
 }

@@ -101,7 +101,7 @@ static void bin_counts(sgm_ctx* ctx, cudaStream_t s, const OptParams& o, uint32_
 static const unsigned long long* bin_lists(sgm_ctx* ctx, cudaStream_t s, const OptParams& o,
                                            uint32_t Ve, uint64_t R, const unsigned long long* d_R,
                                            uint32_t* list, const uint2* ranges, const uint8_t* mask,
-                                           bool part = false) {
+                                           bool part = false, uint64_t P = 0) {
     if (R == 0) return nullptr;
     const unsigned long long* roff = ctx->offsets.as<unsigned long long>();
     uint32_t* rk = ctx->tkeys.as<uint32_t>();
@@ -121,7 +121,8 @@ static const unsigned long long* bin_lists(sgm_ctx* ctx, cudaStream_t s, const O
     const uint64_t G = row_scatter_segments(R, o.tiles_y);  // buffers sized by the caller
     launch_row_scatter(qv, rranges, ranges, o.tiles_x, o.tiles_y, R,
                        ctx->segs.as<uint4>(), reinterpret_cast<uint32_t*>(ctx->segs.as<char>() + sizeof(uint4) * G),
-                       ctx->segcnt.as<uint32_t>(), list, s, mask, part);
+                       ctx->segcnt.as<uint32_t>(), list, s, mask, part,
+                       /*cols: rows of wide entries (cfg4), walked column by column*/ P >= 16 * R);
     ctx->stats.kernel_launches += 7;
     return qv;
 }
@@ -137,7 +138,7 @@ static void bin_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const Cam
         return;
     }
     bin_counts(ctx, s, o, V, ranges, bin_tiles, nullptr, nullptr);
-    bin_lists(ctx, s, o, V, R, d_R, list, ranges, nullptr);
+    bin_lists(ctx, s, o, V, R, d_R, list, ranges, nullptr, false, P);
 }
 
 // Reserves the row-pair scratch of the binning for up to R row pairs.
