@@ -638,26 +638,24 @@ __global__ void __launch_bounds__(256) k_seg_pass_cols(const unsigned long long*
     const int n = static_cast<int>(sg.z - sg.y);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int kPer = kSeg / 32;
-    // entry 32 k + lane of the segment: column span start and width (empty past the end)
-    uint32_t x0[kPer], wd[kPer];
+    // entry 32 k + lane of the segment: (first column << 16) | (last - first); past the end of
+    // the segment an empty span (0xffff << 16 | 0: no column reaches it)
+    uint32_t xw[kPer];
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
         const int i = 32 * k + lane;
         const unsigned long long e = i < n ? row_list[sg.y + i] : 0ull;
         if (warp == 0 && i < n) srank[i] = static_cast<uint32_t>(e >> 32);
         const uint32_t a = static_cast<uint32_t>((e >> 16) & 0xffffu), b = static_cast<uint32_t>(e & 0xffffu);
-        x0[k] = i < n ? a : 0xffffu;
-        wd[k] = i < n ? b - a : 0u;
+        xw[k] = i < n ? (a << 16) | (b - a) : 0xffff0000u;
     }
     __syncthreads();
     const uint32_t lt = (1u << lane) - 1u;
-    const int nk = (n + 31) / 32;
     for (int col = warp; col < tiles_x; col += blockDim.x >> 5) {
         uint32_t cur = cnt[static_cast<size_t>(g) * tiles_x + col];
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
-            if (k >= nk) break;
-            const bool cov = static_cast<uint32_t>(col) - x0[k] <= wd[k];
+            const bool cov = static_cast<uint32_t>(col) - (xw[k] >> 16) <= (xw[k] & 0xffffu);
             const uint32_t bal = __ballot_sync(0xffffffffu, cov);
             if (cov) list[cur + __popc(bal & lt)] = srank[32 * k + lane];
             cur += __popc(bal);
@@ -701,23 +699,42 @@ __global__ void __launch_bounds__(256) k_seg_count(const unsigned long long* __r
 }
 
 // per (row, column): exclusive scan of the segment counts over the row's segments: each
-// segment's first list cursor (or position in the bin)
-__global__ void k_seg_scan(const uint4* __restrict__ segs, const uint32_t* __restrict__ nseg,
-                           const uint2* __restrict__ tile_ranges, int tiles_x, int tiles_y,
-                           uint32_t* __restrict__ cnt) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= tiles_x * tiles_y) return;
-    const int y = i / tiles_x, x = i - y * tiles_x;
-    const uint32_t G = *nseg;
-    // the row's segments are contiguous; find the first by binary search on segs[].x
-    uint32_t lo = 0, hi = G;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) / 2;
-        if (static_cast<int>(segs[mid].x) < y) lo = mid + 1; else hi = mid;
+// segment's first list cursor (or position in the bin). One CTA per (row, 32 columns): the
+// row's segments split over 8 warps (lane = column), warp sums combined in shared memory.
+__global__ void __launch_bounds__(256) k_seg_scan(const uint4* __restrict__ segs,
+                                                  const uint32_t* __restrict__ nseg,
+                                                  const uint2* __restrict__ tile_ranges, int tiles_x,
+                                                  int tiles_y, uint32_t* __restrict__ cnt) {
+    const int y = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int x = blockIdx.y * 32 + lane;
+    __shared__ uint32_t s_rng[2];
+    __shared__ uint32_t wsum[8][32];
+    if (threadIdx.x < 2) {  // the row's segments [first, end): contiguous, found by binary search
+        const uint32_t G = *nseg;
+        const int key = y + static_cast<int>(threadIdx.x);
+        uint32_t lo = 0, hi = G;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (static_cast<int>(segs[mid].x) < key) lo = mid + 1; else hi = mid;
+        }
+        s_rng[threadIdx.x] = lo;
     }
+    __syncthreads();
+    const uint32_t g0 = s_rng[0], ng = s_rng[1] - s_rng[0];
+    const uint32_t per = (ng + 7) / 8;
+    const uint32_t a = g0 + min(ng, warp * per), b = g0 + min(ng, (warp + 1) * per);
+    const bool on = x < tiles_x;
+    uint32_t sum = 0;
+    if (on)
+        for (uint32_t g = a; g < b; ++g) sum += cnt[static_cast<size_t>(g) * tiles_x + x];
+    wsum[warp][lane] = sum;
+    __syncthreads();
+    if (!on) return;
     // absolute list cursors, or (tile_ranges null: depth-prefix binning) positions in the bin
-    uint32_t run = tile_ranges ? tile_ranges[i].x : 0u;
-    for (uint32_t g = lo; g < G && static_cast<int>(segs[g].x) == y; ++g) {
+    uint32_t run = tile_ranges ? tile_ranges[static_cast<size_t>(y) * tiles_x + x].x : 0u;
+    for (int w = 0; w < warp; ++w) run += wsum[w][lane];
+    for (uint32_t g = a; g < b; ++g) {
         const size_t k = static_cast<size_t>(g) * tiles_x + x;
         const uint32_t c = cnt[k];
         cnt[k] = run;
@@ -944,7 +961,7 @@ void launch_row_scatter(const unsigned long long* row_list, const uint2* row_ran
     const dim3 grid(static_cast<unsigned>(gmax), static_cast<unsigned>((blocks + warps - 1) / warps));
     k_seg_count<<<static_cast<unsigned>(gmax), 256, sizeof(int) * (tiles_x + 1), s>>>(
         row_list, segs, nseg, tiles_x, cnt);
-    k_seg_scan<<<blocks_for(static_cast<uint64_t>(tiles_x) * tiles_y, 256), 256, 0, s>>>(
+    k_seg_scan<<<dim3(static_cast<unsigned>(tiles_y), static_cast<unsigned>((tiles_x + 31) / 32)), 256, 0, s>>>(
         segs, nseg, part ? nullptr : tile_ranges, tiles_x, tiles_y, cnt);
     if (part)
         k_seg_pass<true><<<grid, 32 * warps, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list, mask, tile_ranges);
