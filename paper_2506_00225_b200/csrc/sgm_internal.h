@@ -231,7 +231,7 @@ void launch_row_scatter(const unsigned long long* row_list, const uint2* row_ran
 uint64_t row_scatter_segments(uint64_t R, int tiles_y);  // upper bound on segments
 void launch_seg_pass(const unsigned long long* row_list, const uint2* tile_ranges, int tiles_x,
                      uint64_t G, const uint4* segs, const uint32_t* nseg, const uint32_t* cnt,
-                     uint32_t* list, const uint8_t* mask, cudaStream_t s);
+                     uint32_t* list, const uint8_t* mask, cudaStream_t s, bool cols = false);
 void launch_raster_score(const RasterParams& p, int n_views, cudaStream_t s);
 void launch_raster_render(const RasterParams& p, int n_views, cudaStream_t s);
 void launch_reduce_scores(const ViewDesc* views, int n_views, int tiles, double* out_missing,

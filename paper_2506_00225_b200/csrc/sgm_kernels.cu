@@ -626,11 +626,16 @@ __global__ void __launch_bounds__(256) k_seg_pass(const unsigned long long* __re
 // column spans in registers (32 entries per lane) and ranks in shared memory; each warp walks
 // whole columns, so a column's share of the segment (hundreds of entries) is written by one
 // warp front to back: full sectors, instead of the block walk's few-entry pieces per chunk.
+// kPart: depth-prefix binning (positions relative to the bin, writes stop at the bin's list
+// length, bins outside `mask` skipped); a column whose list is full stops walking.
+template <bool kPart>
 __global__ void __launch_bounds__(256) k_seg_pass_cols(const unsigned long long* __restrict__ row_list,
                                                        const uint4* __restrict__ segs,
                                                        const uint32_t* __restrict__ nseg, int tiles_x,
                                                        const uint32_t* __restrict__ cnt,
-                                                       uint32_t* __restrict__ list) {
+                                                       uint32_t* __restrict__ list,
+                                                       const uint8_t* __restrict__ mask,
+                                                       const uint2* __restrict__ tile_ranges) {
     __shared__ uint32_t srank[kSeg];
     const uint32_t g = blockIdx.x;
     if (g >= *nseg) return;
@@ -638,6 +643,16 @@ __global__ void __launch_bounds__(256) k_seg_pass_cols(const unsigned long long*
     const int n = static_cast<int>(sg.z - sg.y);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int kPer = kSeg / 32;
+    if constexpr (kPart) {  // segments past every column's prefix (most of a dense row): nothing to load
+        bool need = false;
+        for (int col = threadIdx.x; col < tiles_x; col += blockDim.x) {
+            const size_t bin = static_cast<size_t>(sg.x) * tiles_x + col;
+            if (mask && !mask[bin]) continue;
+            const uint2 tr = tile_ranges[bin];
+            need = need || cnt[static_cast<size_t>(g) * tiles_x + col] < tr.y - tr.x;
+        }
+        if (!__syncthreads_or(need)) return;
+    }
     // entry 32 k + lane of the segment: (first column << 16) | (last - first); past the end of
     // the segment an empty span (0xffff << 16 | 0: no column reaches it)
     uint32_t xw[kPer];
@@ -653,12 +668,27 @@ __global__ void __launch_bounds__(256) k_seg_pass_cols(const unsigned long long*
     const uint32_t lt = (1u << lane) - 1u;
     for (int col = warp; col < tiles_x; col += blockDim.x >> 5) {
         uint32_t cur = cnt[static_cast<size_t>(g) * tiles_x + col];
+        if constexpr (kPart) {
+            const size_t bin = static_cast<size_t>(sg.x) * tiles_x + col;
+            if (mask && !mask[bin]) continue;
+            const uint2 tr = tile_ranges[bin];
+            const uint32_t len = tr.y - tr.x;
+            uint32_t* out = list + tr.x;
+            for (int k = 0; k < kPer && cur < len; ++k) {
+                const bool cov = static_cast<uint32_t>(col) - (xw[k] >> 16) <= (xw[k] & 0xffffu);
+                const uint32_t bal = __ballot_sync(0xffffffffu, cov);
+                const uint32_t pos = cur + __popc(bal & lt);
+                if (cov && pos < len) out[pos] = srank[32 * k + lane];
+                cur += __popc(bal);
+            }
+        } else {
 #pragma unroll
-        for (int k = 0; k < kPer; ++k) {
-            const bool cov = static_cast<uint32_t>(col) - (xw[k] >> 16) <= (xw[k] & 0xffffu);
-            const uint32_t bal = __ballot_sync(0xffffffffu, cov);
-            if (cov) list[cur + __popc(bal & lt)] = srank[32 * k + lane];
-            cur += __popc(bal);
+            for (int k = 0; k < kPer; ++k) {
+                const bool cov = static_cast<uint32_t>(col) - (xw[k] >> 16) <= (xw[k] & 0xffffu);
+                const uint32_t bal = __ballot_sync(0xffffffffu, cov);
+                if (cov) list[cur + __popc(bal & lt)] = srank[32 * k + lane];
+                cur += __popc(bal);
+            }
         }
     }
 }
@@ -963,10 +993,11 @@ void launch_row_scatter(const unsigned long long* row_list, const uint2* row_ran
         row_list, segs, nseg, tiles_x, cnt);
     k_seg_scan<<<dim3(static_cast<unsigned>(tiles_y), static_cast<unsigned>((tiles_x + 31) / 32)), 256, 0, s>>>(
         segs, nseg, part ? nullptr : tile_ranges, tiles_x, tiles_y, cnt);
-    if (part)
+    if (part)  // (the block walk: faster than k_seg_pass_cols on the short prefixes)
         k_seg_pass<true><<<grid, 32 * warps, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list, mask, tile_ranges);
     else if (cols)
-        k_seg_pass_cols<<<static_cast<unsigned>(gmax), 256, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list);
+        k_seg_pass_cols<false><<<static_cast<unsigned>(gmax), 256, 0, s>>>(row_list, segs, nseg, tiles_x, cnt,
+                                                                           list, nullptr, nullptr);
     else
         k_seg_pass<false><<<grid, 32 * warps, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list, nullptr, nullptr);
 }
@@ -975,8 +1006,13 @@ void launch_row_scatter(const unsigned long long* row_list, const uint2* row_ran
 // depth-prefix binning: the same row list and per-segment positions, other ranges / mask)
 void launch_seg_pass(const unsigned long long* row_list, const uint2* tile_ranges, int tiles_x,
                      uint64_t G, const uint4* segs, const uint32_t* nseg, const uint32_t* cnt,
-                     uint32_t* list, const uint8_t* mask, cudaStream_t s) {
+                     uint32_t* list, const uint8_t* mask, cudaStream_t s, bool cols) {
     if (G == 0) return;
+    if (cols) {
+        k_seg_pass_cols<true><<<static_cast<unsigned>(G), 256, 0, s>>>(row_list, segs, nseg, tiles_x, cnt, list,
+                                                                       mask, tile_ranges);
+        return;
+    }
     const int blocks = (tiles_x + 31) / 32;
     const int warps = std::min(8, blocks);
     const dim3 grid(static_cast<unsigned>(G), static_cast<unsigned>((blocks + warps - 1) / warps));

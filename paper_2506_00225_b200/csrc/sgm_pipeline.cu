@@ -156,99 +156,77 @@ static void reserve_rows(sgm_ctx* ctx, const OptParams& o, uint64_t R, size_t NS
     CK(ctx->segcnt.reserve(sizeof(uint32_t) * G * o.tiles_x));
 }
 
-// A view is "dense" when its bins average more than this many entries: its tile lists are
-// then built from each bin's first entries only (depth-prefix binning, score_dense_view).
-constexpr uint64_t kDenseAvg = 4096;
-constexpr uint32_t kPrefixCap = 256;  // entries per bin of the first pass
+// Depth-prefix binning of "dense" views (cfg4: bins averaging hundreds of thousands of
+// entries). The raster's early exit (:312) consumes a short prefix of every bin, so each bin
+// first gets only its first `cap` entries (a prefix of its full list, same rank order),
+// flagged when that drops entries (pass 1, pipelined like any view). A block that exhausts a
+// flagged list with pixels still open is reported incomplete; after the group's rasters, the
+// full lists of those tiles' bins are built (pass 2) and those tiles redone. A block that
+// completes inside its prefix stops where it would have stopped on the full list, so every
+// tile's result is the full-list result.
+constexpr uint64_t kDenseAvg = 65536;  // entries per bin on average: a dense view
+constexpr uint64_t kForceAvg = 4096;   // (SGM_PREFIX_BINNING=1: dense from this average)
+constexpr uint32_t kPrefixCap = 8192;  // entries per bin of pass 1 (cfg4: 120 vs 106 views/s
+                                       // with full lists; 256: 85, 2048: 110, 32768: 111)
 
-// Scores one dense view (its own group). The raster's early exit (:312) usually consumes a
-// short prefix of every bin, so each bin first gets only its first kPrefixCap entries (a
-// prefix of its full list, in the same rank order; the row list, its sort and the
-// per-segment positions are built once), flagged when that drops entries. A block that
-// exhausts a flagged list with pixels still open is reported incomplete; the second pass
-// writes the full lists of those bins only (same row list, masked) and redoes those tiles.
-// A block that completes inside its prefix stops where it would have stopped on the full
-// list, so every tile's result is the full-list result.
-static void score_dense_view(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam,
-                             const OptParams& o, int v, uint32_t V, uint64_t P, uint64_t R,
-                             const unsigned long long* d_R, size_t NS, int bin_tiles, int rtx,
-                             int rtiles, int kSub, ViewDesc d, const RasterParams& rp0) {
-    cudaStream_t s = ctx->stream;
-    const PoseParams* d_pose = ctx->poses.as<PoseParams>() + v;
-    if (ctx->profiling) CK(cudaEventRecord(ctx->ev_r[0], s));  // (raster_ms: binning included)
-    pack_view(ctx, s, map, cam, o, d_pose, ctx->keys.as<uint32_t>() + NS * v,
-              const_cast<uint32_t*>(d.order), V, const_cast<PackedSplat*>(d.packed),
-              const_cast<uint4*>(d.bounds));
-    CK(ctx->franges.reserve(sizeof(uint2) * bin_tiles));
-    CK(ctx->trunc8.reserve(bin_tiles + 16));
-    CK(ctx->bmask.reserve(bin_tiles + 16));
-    CK(ctx->incomplete.reserve(4 * static_cast<size_t>(rtiles) + 16));
-    CK(ctx->redo.reserve(sizeof(uint2) * rtiles + 16));
-    CK(ctx->dense_tot.reserve(64));
+// pass 1 of a dense view on stream s (no host sync: the list region holds cap entries per bin)
+static void bin_dense_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const CamParams& cam,
+                           const OptParams& o, const PoseParams* d_pose, uint32_t* keys, const ViewDesc& d,
+                           uint32_t V, uint64_t P, uint64_t R, const unsigned long long* d_R, int bin_tiles,
+                           uint32_t cap, uint8_t* trunc) {
+    pack_view(ctx, s, map, cam, o, d_pose, keys, const_cast<uint32_t*>(d.order), V,
+              const_cast<PackedSplat*>(d.packed), const_cast<uint4*>(d.bounds));
     uint2* ranges = const_cast<uint2*>(d.ranges);
+    if (V == 0 || P == 0) {
+        CK(cudaMemsetAsync(ranges, 0, sizeof(uint2) * bin_tiles, s));
+        CK(cudaMemsetAsync(trunc, 0, bin_tiles, s));
+        return;
+    }
+    bin_counts(ctx, s, o, V, ranges, bin_tiles, nullptr, nullptr, cap, trunc);
+    bin_lists(ctx, s, o, V, R, d_R, const_cast<uint32_t*>(d.list), ranges, nullptr, true, P);
+}
+
+// pass 2 of a dense view whose raster reported `ninc` incomplete tiles (in `inc`): the view is
+// binned again from its depth order (the binning scratch has served later views since), with
+// full lists for the bins of those tiles only, and those tiles are rastered again (their
+// per-tile partials overwritten). Synchronous on s; runs before the group's score reduction.
+static void redo_dense_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const CamParams& cam,
+                            const OptParams& o, const PoseParams* d_pose, uint32_t* keys, ViewDesc d,
+                            ViewDesc* d_desc, uint32_t V, uint64_t P, uint64_t R,
+                            const unsigned long long* d_R, int bin_tiles, int rtx, const uint32_t* inc,
+                            uint32_t ninc, RasterParams rp) {
+    CK(ctx->franges.reserve(sizeof(uint2) * bin_tiles));
+    CK(ctx->bmask.reserve(bin_tiles + 16));
+    CK(ctx->redo.reserve(sizeof(uint2) * ninc + 16));
+    CK(ctx->dense_tot.reserve(64));
     unsigned long long* d_tot = ctx->dense_tot.as<unsigned long long>();
-    uint32_t* n_inc = reinterpret_cast<uint32_t*>(d_tot + 2);
-    // pass 1: every bin's first kPrefixCap entries
-    bin_counts(ctx, s, o, V, ranges, bin_tiles, nullptr, d_tot, kPrefixCap, ctx->trunc8.as<uint8_t>());
-    unsigned long long Pe = 0;
-    CK(cudaMemcpyAsync(&Pe, d_tot, 8, cudaMemcpyDeviceToHost, s));
+    uint8_t* mask = ctx->bmask.as<uint8_t>();
+    uint2* full = ctx->franges.as<uint2>();
+    CK(cudaMemsetAsync(mask, 0, bin_tiles, s));
+    launch_redo_items(inc, ninc, 0, rtx, o.ts / kTile, o.tiles_x, ctx->redo.as<uint2>(), mask, s);
+    pack_view(ctx, s, map, cam, o, d_pose, keys, const_cast<uint32_t*>(d.order), V,
+              const_cast<PackedSplat*>(d.packed), const_cast<uint4*>(d.bounds));
+    bin_counts(ctx, s, o, V, full, bin_tiles, mask, d_tot, 0xffffffffu, nullptr);
+    unsigned long long P2 = 0;
+    CK(cudaMemcpyAsync(&P2, d_tot, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    CK(ctx->tvals.reserve(4 * std::max<unsigned long long>(Pe, 1)));
-    reserve_rows(ctx, o, R, NS, kSub);
-    const unsigned long long* rowlist =
-        bin_lists(ctx, s, o, V, R, d_R, ctx->tvals.as<uint32_t>(), ranges, nullptr, true);
-    d.list = ctx->tvals.as<uint32_t>();
-    CK(cudaMemsetAsync(n_inc, 0, 4, s));
-    CK(cudaMemcpyAsync(ctx->views.p, &d, sizeof(ViewDesc), cudaMemcpyHostToDevice, s));
-    RasterParams rp = rp0;
-    rp.views = ctx->views.as<ViewDesc>();
-    rp.trunc = ctx->trunc8.as<uint8_t>();
-    rp.incomplete = ctx->incomplete.as<uint32_t>();
-    rp.n_incomplete = n_inc;
+    if (P2 >= (1ull << 32)) fail(SGM_ERR_UNSUPPORTED, "view has %llu tile pairs (>= 2^32)", P2);
+    CK(ctx->list2.reserve(4 * std::max<unsigned long long>(P2, 1)));
+    bin_lists(ctx, s, o, V, R, d_R, ctx->list2.as<uint32_t>(), full, mask, true, P);
+    d.list = ctx->list2.as<uint32_t>();
+    d.ranges = full;
+    CK(cudaMemcpyAsync(d_desc, &d, sizeof(ViewDesc), cudaMemcpyHostToDevice, s));
+    rp.views = d_desc;
+    rp.trunc = nullptr;
+    rp.incomplete = nullptr;
+    rp.n_incomplete = nullptr;
+    rp.item_list = ctx->redo.as<uint2>();
+    rp.n_item_list = static_cast<int>(ninc);
     launch_raster_score(rp, 1, s);
     CK(cudaGetLastError());
-    ctx->stats.kernel_launches += 1;
+    CK(cudaStreamSynchronize(s));  // (d lives on this stack frame)
+    ctx->stats.kernel_launches += 3;
     ctx->stats.raster_launches += 1;
-    uint32_t ninc = 0;
-    CK(cudaMemcpyAsync(&ninc, n_inc, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (ninc > 0 && rowlist) {
-        // pass 2: the full lists of the incomplete tiles' bins, and those tiles again
-        CK(cudaMemsetAsync(ctx->bmask.p, 0, bin_tiles, s));
-        launch_redo_items(ctx->incomplete.as<uint32_t>(), ninc, 0, rtx, o.ts / kTile, o.tiles_x,
-                          ctx->redo.as<uint2>(), ctx->bmask.as<uint8_t>(), s);
-        const uint8_t* mask = ctx->bmask.as<uint8_t>();
-        uint2* full = ctx->franges.as<uint2>();
-        const int X = o.tiles_x + 1, Y = o.tiles_y + 1;
-        CK(cudaMemsetAsync(ctx->bdiff.p, 0, sizeof(int) * X * Y, s));
-        launch_bin_hist(ctx->rects.as<int4>(), V, o.tiles_x, ctx->bdiff.as<int>(),
-                        ctx->counts.as<unsigned long long>(), s);
-        launch_bin_scan(ctx->bdiff.as<int>(), o.tiles_x, o.tiles_y, full, s, mask, d_tot);
-        unsigned long long P2 = 0;
-        CK(cudaMemcpyAsync(&P2, d_tot, 8, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        if (P2 >= (1ull << 32)) fail(SGM_ERR_UNSUPPORTED, "view has %llu tile pairs (>= 2^32)", P2);
-        CK(ctx->list2.reserve(4 * std::max<unsigned long long>(P2, 1)));
-        const uint64_t G = row_scatter_segments(R, o.tiles_y);
-        launch_seg_pass(rowlist, full, o.tiles_x, G, ctx->segs.as<uint4>(),
-                        reinterpret_cast<uint32_t*>(ctx->segs.as<char>() + sizeof(uint4) * G),
-                        ctx->segcnt.as<uint32_t>(), ctx->list2.as<uint32_t>(), mask, s);
-        d.list = ctx->list2.as<uint32_t>();
-        d.ranges = full;
-        CK(cudaMemcpyAsync(ctx->views.p, &d, sizeof(ViewDesc), cudaMemcpyHostToDevice, s));
-        rp.trunc = nullptr;
-        rp.incomplete = nullptr;
-        rp.n_incomplete = nullptr;
-        rp.item_list = ctx->redo.as<uint2>();
-        rp.n_item_list = static_cast<int>(ninc);
-        launch_raster_score(rp, 1, s);
-        CK(cudaGetLastError());
-        ctx->stats.kernel_launches += 6;
-        ctx->stats.raster_launches += 1;
-    }
-    if (ctx->profiling) CK(cudaEventRecord(ctx->ev_r[1], s));
-    // the view's pairs as binned by the reference (statistics)
-    ctx->stats.pairs += P;
 }
 
 // Runs n views. Score mode writes n_missing/entropy_sum (host); render mode (n == 1)
@@ -334,47 +312,50 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
         std::vector<uint64_t> P(hp, hp + nb);
         std::vector<uint64_t> R(hp + nb, hp + 2 * nb);  // (row, rank) pairs of the binning
 
-        // groups of views whose pair lists fit ctx->list_budget together (a fifth of the device:
-        // several cfg4-dense views per group, so the binning of one overlaps the raster of the
-        // previous); a view past 2^31 entries in the plain score mode is a group of its own
-        // (depth-prefix binning, score_dense_view)
-        const uint64_t pair_budget = ctx->list_budget;
-        const uint64_t dense_pairs = uint64_t(2) << 30;
-        // Depth-prefix binning serves the views whose full lists exceed the list budget (or
-        // 2^32 pairs). It is exact but not faster than full bins that fit (the binning of a
-        // full view overlaps the previous raster; the prefix path is synchronous), so full
-        // bins stay the default below the budget. SGM_PREFIX_BINNING=1 forces it for every
-        // view averaging > kDenseAvg entries per bin, =0 turns it off.
+        // Depth-prefix binning (bin_dense_view) serves the plain score mode's dense views: bins
+        // averaging more than kDenseAvg entries (cfg4), or lists past 2^31 entries.
+        // SGM_PREFIX_BINNING=1 lowers the threshold to kForceAvg, =0 turns it off;
+        // SGM_PREFIX_CAP sets the pass-1 entries per bin.
         const char* pb = std::getenv("SGM_PREFIX_BINNING");
         const int prefix_mode = pb ? (pb[0] == '0' ? 0 : 2) : 1;
+        const char* pc = std::getenv("SGM_PREFIX_CAP");
+        const uint32_t cap = pc ? std::max(1u, static_cast<uint32_t>(std::atoi(pc))) : kPrefixCap;
+        const uint64_t dense_pairs = uint64_t(2) << 30;
         auto dense = [&](int v) {
             if (prefix_mode == 0 || mode != Mode::Score || fk != Fisher::None) return false;
-            if (P[v] <= kDenseAvg * static_cast<uint64_t>(bin_tiles)) return false;
-            return prefix_mode == 2 || P[v] > dense_pairs;
+            const uint64_t avg = prefix_mode == 2 ? kForceAvg : kDenseAvg;
+            return P[v] > avg * static_cast<uint64_t>(bin_tiles) || P[v] > dense_pairs;
         };
+        // list entries a view needs: its pairs, or cap per bin for a dense view
+        auto list_len = [&](int v) {
+            return dense(v) ? std::min<uint64_t>(P[v], static_cast<uint64_t>(cap) * bin_tiles) : P[v];
+        };
+        // groups of views whose lists fit ctx->list_budget together (a fifth of the device), so
+        // the binning of each sub-batch overlaps the raster of the previous one
+        const uint64_t pair_budget = ctx->list_budget;
         int v0 = 0;
         while (v0 < nb) {
             int v1 = v0;
-            uint64_t sumP = 0, maxP = 0;
-            while (v1 < nb && (v1 == v0 || (sumP + P[v1] <= pair_budget && !dense(v1) && !dense(v0)))) {
-                sumP += P[v1];
-                maxP = std::max<uint64_t>(maxP, P[v1]);
-                ++v1;
-            }
-            const bool dense_group = dense(v0);
-            for (int v = v0; v < v1; ++v)  // (a dense view's lists are built a prefix at a time)
-                if (!dense_group && P[v] >= (1ull << 32))
+            uint64_t sumP = 0;
+            while (v1 < nb && (v1 == v0 || sumP + list_len(v1) <= pair_budget)) sumP += list_len(v1++);
+            int ndense = 0;
+            for (int v = v0; v < v1; ++v) {
+                ndense += dense(v) ? 1 : 0;
+                if (!dense(v) && P[v] >= (1ull << 32))  // (a dense view's lists hold prefixes)
                     fail(SGM_ERR_UNSUPPORTED, "view has %llu tile pairs (>= 2^32)",
                          static_cast<unsigned long long>(P[v]));
+            }
             uint64_t maxR = 1;
             for (int v = v0; v < v1; ++v) maxR = std::max<uint64_t>(maxR, R[v]);
-            if (!dense_group) {
-                CK(ctx->tvals.reserve(4 * std::max<uint64_t>(sumP, 1)));
-                reserve_rows(ctx, o, maxR, NS, kSub);
-            } else {
-                CK(ctx->sort_tmp.reserve(radix_sort_scratch_bytes(NS, kSub)));
-                CK(ctx->scan_tmp.reserve(exclusive_scan_scratch_bytes(NS + 1)));
+            CK(ctx->tvals.reserve(4 * std::max<uint64_t>(sumP, 1)));
+            reserve_rows(ctx, o, maxR, NS, kSub);
+            const int ng = v1 - v0;
+            if (ndense) {  // per view of the group: truncation flags, incomplete tiles, their count
+                CK(ctx->trunc8.reserve(static_cast<size_t>(bin_tiles) * ng + 16));
+                CK(ctx->incomplete.reserve(4 * static_cast<size_t>(rtiles) * ng + 16));
+                CK(ctx->dense_tot.reserve(16 + 4 * static_cast<size_t>(ng) + 16));
             }
+            uint32_t* d_ninc = ndense ? reinterpret_cast<uint32_t*>(ctx->dense_tot.as<char>() + 16) : nullptr;
             // descriptors for the whole group (list offsets known from the counts)
             ViewDesc* hvd = ctx->h_views.as<ViewDesc>();
             uint64_t list_off = 0;
@@ -402,12 +383,13 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                             ? ctx->rcbuf.as<double>() + 4ull * cam.W * cam.H * static_cast<size_t>(v)
                             : nullptr;
                 hvd[v - v0] = d;
-                list_off += dense_group ? 0 : P[v];
+                list_off += list_len(v);
                 ctx->stats.visible += V[v];
-                if (!dense_group) ctx->stats.pairs += P[v];
+                ctx->stats.pairs += P[v];  // (the reference's pairs, also for a dense view)
             }
             const int ngroup = v1 - v0;
             CK(cudaMemcpyAsync(ctx->views.p, hvd, sizeof(ViewDesc) * ngroup, cudaMemcpyHostToDevice, s));
+            if (ndense) CK(cudaMemsetAsync(d_ninc, 0, 4 * static_cast<size_t>(ngroup), s));
             // the binning stream starts after everything already queued on s
             CK(cudaEventRecord(ctx->ev_ready, s));
             CK(cudaStreamWaitEvent(sb, ctx->ev_ready, 0));
@@ -422,10 +404,16 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
             rp.want_rc = fk == Fisher::Gain ? 1 : 0;
             // sub-batches of 1, 2, 4, then kSub views: the first raster starts after one view's
             // binning instead of kSub views' (the pipeline fill), and each sub-batch's binning
-            // still hides under the previous one's raster (about 1/3 of its time per view)
+            // still hides under the previous one's raster (about 1/3 of its time per view). A
+            // dense view is a sub-batch of its own (its raster reports incomplete tiles).
             int sub = 0;
-            for (int s0 = v0, len = 1; s0 < v1; s0 += len, len = std::min(kSub, 2 * len), ++sub) {
-                const int s1 = std::min(v1, s0 + len);
+            for (int s0 = v0, s1 = v0, len = 1; s0 < v1; s0 = s1, ++sub) {
+                if (dense(s0)) {
+                    s1 = s0 + 1;
+                } else {
+                    while (s1 < v1 && s1 - s0 < len && !dense(s1)) ++s1;
+                    len = std::min(kSub, 2 * len);
+                }
                 {  // K2 for the sub-batch: one segmented radix sort of its views' depth keys
                     uint32_t maxV = 0;
                     for (int v = s0; v < s1; ++v) maxV = std::max(maxV, V[v]);
@@ -436,21 +424,16 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                     if (alt) fail(SGM_ERR_CUDA, "depth sort: odd pass count");  // 4 passes: in place
                     ctx->stats.kernel_launches += maxV ? radix_sort_launches(32, maxV) : 0;
                 }
-                if (dense_group) {  // one view: depth-prefix binning, synchronous on s
-                    CK(cudaStreamSynchronize(sb));
-                    if (!rows_ready) {
-                        map_ready(ctx, map);
-                        if (raster_score_records(map->dev)) map_records(ctx, map);
-                        rows_ready = true;
-                        rp.map = map->dev;
-                    }
-                    score_dense_view(ctx, map, cam, o, s0, V[s0], P[s0], R[s0],
-                                     ctx->pcount.as<unsigned long long>() + nb + s0, NS, bin_tiles,
-                                     rtx, rtiles, kSub, hvd[0], rp);
-                    continue;
-                }
+                const bool dsub = dense(s0);
                 for (int v = s0; v < s1; ++v) {
                     const ViewDesc& d = hvd[v - v0];
+                    if (dsub) {
+                        bin_dense_view(ctx, sb, map, cam, o, ctx->poses.as<PoseParams>() + v,
+                                       ctx->keys.as<uint32_t>() + NS * v, d, V[v], P[v], R[v],
+                                       ctx->pcount.as<unsigned long long>() + nb + v, bin_tiles, cap,
+                                       ctx->trunc8.as<uint8_t>() + static_cast<size_t>(bin_tiles) * (v - v0));
+                        continue;
+                    }
                     bin_view(ctx, sb, map, cam, o, ctx->poses.as<PoseParams>() + v,
                              ctx->keys.as<uint32_t>() + NS * v, const_cast<uint32_t*>(d.order), V[v],
                              P[v], R[v], ctx->pcount.as<unsigned long long>() + nb + v,
@@ -469,6 +452,9 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 }
                 CK(cudaStreamWaitEvent(s, ctx->ev_binned[slot], 0));
                 rp.views = ctx->views.as<ViewDesc>() + (s0 - v0);
+                rp.trunc = dsub ? ctx->trunc8.as<uint8_t>() + static_cast<size_t>(bin_tiles) * (s0 - v0) : nullptr;
+                rp.incomplete = dsub ? ctx->incomplete.as<uint32_t>() + static_cast<size_t>(rtiles) * (s0 - v0) : nullptr;
+                rp.n_incomplete = dsub ? d_ninc + (s0 - v0) : nullptr;
                 const int pr = sub % 16;  // profiling event pair
                 if (ctx->profiling) CK(cudaEventRecord(ctx->ev_r[2 * pr], s));
                 FisherParams fp{};
@@ -490,6 +476,23 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 if (ctx->profiling) CK(cudaEventRecord(ctx->ev_r[2 * pr + 1], s));
                 ctx->stats.kernel_launches += 1;
                 ctx->stats.raster_launches += 1;
+            }
+            if (ndense) {  // pass 2 of the dense views with incomplete tiles
+                std::vector<uint32_t> hn(ngroup);
+                CK(cudaMemcpyAsync(hn.data(), d_ninc, 4 * static_cast<size_t>(ngroup), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                rp.trunc = nullptr;
+                rp.incomplete = nullptr;
+                rp.n_incomplete = nullptr;
+                for (int v = v0; v < v1; ++v) {
+                    if (!dense(v) || hn[v - v0] == 0) continue;
+                    redo_dense_view(ctx, s, map, cam, o, ctx->poses.as<PoseParams>() + v,
+                                    ctx->keys.as<uint32_t>() + NS * v, hvd[v - v0],
+                                    ctx->views.as<ViewDesc>() + (v - v0), V[v], P[v], R[v],
+                                    ctx->pcount.as<unsigned long long>() + nb + v, bin_tiles, rtx,
+                                    ctx->incomplete.as<uint32_t>() + static_cast<size_t>(rtiles) * (v - v0),
+                                    hn[v - v0], rp);
+                }
             }
             if (mode == Mode::Score && fk != Fisher::Prior) {
                 double* dfis = fk == Fisher::Gain ? ctx->out.as<double>() + 2 * ngroup : nullptr;

@@ -160,18 +160,23 @@ def _dense_scene():
     return gm, cam, scenes.make_candidates(4, 6)
 
 
-def test_depth_prefix_binning_is_exact(ctx, monkeypatch):
-    """Dense views: scores from depth-prefix bins (with the redo of incomplete tiles) are
-    bit-identical to scores from the full bins."""
+@pytest.mark.parametrize("cap", [None, "256", "64"])
+def test_depth_prefix_binning_is_exact(ctx, monkeypatch, cap):
+    """Dense views: scores from depth-prefix bins (with the redo of incomplete tiles: small
+    caps leave many) are bit-identical to scores from the full bins."""
     gm, cam, cands = _dense_scene()
     poses = [c.camera_pose() for c in cands]
+    monkeypatch.setenv("SGM_PREFIX_BINNING", "0")
+    nm2, es2 = sgm.score_poses(gm, cam, poses, ctx=ctx)
     ctx.reset_stats()
-    monkeypatch.setenv("SGM_PREFIX_BINNING", "1")  # (by default only past the list budget)
+    monkeypatch.setenv("SGM_PREFIX_BINNING", "1")  # (by default from 65536 entries per bin)
+    if cap:
+        monkeypatch.setenv("SGM_PREFIX_CAP", cap)
     nm, es = sgm.score_poses(gm, cam, poses, ctx=ctx)
     st = ctx.stats()
     assert st["pairs"] / len(poses) > 4096 * 30 * 17  # dense: > 4096 entries per bin
-    monkeypatch.setenv("SGM_PREFIX_BINNING", "0")
-    nm2, es2 = sgm.score_poses(gm, cam, poses, ctx=ctx)
+    if cap:  # the second pass ran (one more raster launch per view with incomplete tiles)
+        assert st["raster_launches"] > len(poses)
     assert np.array_equal(nm, nm2) and np.array_equal(es, es2)
     assert len(set(nm.tolist())) > 1  # some views see the background (tiles that never exit)
 
