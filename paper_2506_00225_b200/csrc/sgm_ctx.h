@@ -236,7 +236,7 @@ struct sgm_ctx {
         bounds, bdiff, rranges, rvals, segs, segcnt, rcbuf;
     DevBuf tkeys, tvals, tkeys_alt, tvals_alt, ranges, ent_part, miss_part, views, out,
         contributors, cub_tmp, sort_tmp, scan_tmp, franges, trunc8, bmask, incomplete, redo,
-        dense_tot, list2, planes, dbg, ccount, coffset, contrib, fis_part, bw_frame,
+        dense_tot, list2, cdiff, csat, planes, dbg, ccount, coffset, contrib, fis_part, bw_frame,
         bw_flags, bw_part, bw_grad;
     uint64_t last_ncontrib = 0;
     bool last_has_contrib = false;

@@ -210,6 +210,8 @@ void launch_pack(const DevMap& m, const PoseParams* d_pose, const CamParams& cam
 void launch_ranges(const uint32_t* sorted_tiles, uint64_t P, uint2* ranges, cudaStream_t s);
 // row-bucketed binning (sgm_kernels.cu): tile ranges from a 2D difference array, each
 // row's ranks in rank order, then a per-row ordered scatter into the tile lists
+void launch_bin_hist_prefix(const int4* rects, uint32_t V, int tiles_x, int tiles_y, uint32_t cap, int nc,
+                            int* diffc, int* sat, int* diff, unsigned long long* rows, cudaStream_t s);
 void launch_bin_hist(const int4* rects, uint32_t V, int tiles_x, int* diff,
                      unsigned long long* rows, cudaStream_t s);
 // mask: bins outside it get empty lists; total: the pairs allocated; cap: a bin keeps its

@@ -370,10 +370,20 @@ __global__ void k_emit_rows(const unsigned long long* __restrict__ offsets, cons
     int4 rc = rects[r];
     const unsigned long long i1 = min(R, i0 + kPerThread);
     for (unsigned long long i = i0; i < i1; ++i) {
-        while (i >= end) {
+        if (i >= end) {
             ++r;
             beg = end;
             end = offsets[r + 1];
+            if (i >= end) {  // ranks without pairs (depth-prefix binning skips most): search
+                uint32_t a = r, b = V;
+                while (b - a > 1) {
+                    const uint32_t mid = (a + b) / 2;
+                    if (offsets[mid] <= i) a = mid; else b = mid;
+                }
+                r = a;
+                beg = offsets[r];
+                end = offsets[r + 1];
+            }
             rc = rects[r];
         }
         const uint32_t j = static_cast<uint32_t>(i - beg);
@@ -410,6 +420,94 @@ __global__ void k_bin_hist(const int4* __restrict__ rects, uint32_t V, int tiles
     atomicAdd(&diff[y0 * X + x1], -1);
     atomicAdd(&diff[y1 * X + x0], -1);
     atomicAdd(&diff[y1 * X + x1], 1);
+}
+
+// Depth-prefix binning, pass 1: which ranks can reach a bin's first `cap` entries. The
+// ranks are cut into kRankChunks chunks; per chunk, the bins' entry counts (2D difference
+// arrays, one per chunk); a bin is open in chunk c while fewer than cap entries precede the
+// chunk; a rank of chunk c whose rectangle covers no open bin is in no bin's prefix, so it
+// emits no row pairs (k_bin_hist_prefix). Its entries still count, so the truncation flags
+// and capped counts are the full lists'.
+__global__ void k_chunk_hist(const int4* __restrict__ rects, uint32_t V, int nc, int tiles_x, int tiles_y,
+                             int* __restrict__ diffc) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= V) return;
+    const int4 rc = rects[r];
+    if (rc.z <= 0 || rc.w <= 0) return;
+    const int X = tiles_x + 1, Y = tiles_y + 1;
+    int* d = diffc + static_cast<size_t>(static_cast<uint64_t>(r) * nc / V) * X * Y;
+    const int x0 = rc.x, x1 = rc.x + rc.z, y0 = rc.y, y1 = rc.y + rc.w;
+    atomicAdd(&d[y0 * X + x0], 1);
+    atomicAdd(&d[y0 * X + x1], -1);
+    atomicAdd(&d[y1 * X + x0], -1);
+    atomicAdd(&d[y1 * X + x1], 1);
+}
+
+// In place, one CTA per chunk: inclusive 2D prefix sums of a W x H int array (pitch W):
+// rows (a warp per row, 32 columns at a time) then columns (a thread per column).
+__global__ void __launch_bounds__(1024) k_prefix2d(int* __restrict__ a, int W, int H) {
+    int* d = a + static_cast<size_t>(blockIdx.x) * W * H;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    for (int y = warp; y < H; y += 32) {
+        int carry = 0;
+        for (int x0 = 0; x0 < W; x0 += 32) {
+            const int x = x0 + lane;
+            int v = x < W ? d[y * W + x] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += u;
+            }
+            v += carry;
+            if (x < W) d[y * W + x] = v;
+            carry = __shfl_sync(0xffffffffu, v, 31);
+        }
+    }
+    __syncthreads();
+    for (int x = t; x < W; x += blockDim.x) {
+        int acc = 0;
+        for (int y = 0; y < H; ++y) {
+            acc += d[y * W + x];
+            d[y * W + x] = acc;
+        }
+    }
+}
+
+// per bin: open flags per chunk into the summed-area arrays (one-cell zero border:
+// sat[c][(y + 1) * (X) + x + 1] with X = tiles_x + 1)
+__global__ void k_chunk_open(const int* __restrict__ cnt, int nc, int tiles_x, int tiles_y, uint32_t cap,
+                             int* __restrict__ sat) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= tiles_x * tiles_y) return;
+    const int y = i / tiles_x, x = i - y * tiles_x;
+    const int X = tiles_x + 1, Y = tiles_y + 1;
+    uint32_t cum = 0;
+    for (int c = 0; c < nc; ++c) {
+        sat[static_cast<size_t>(c) * X * Y + (y + 1) * X + x + 1] = cum < cap ? 1 : 0;
+        cum += static_cast<uint32_t>(cnt[static_cast<size_t>(c) * X * Y + y * X + x]);
+    }
+}
+
+// k_bin_hist for pass 1: every rank counts in its bins; only ranks covering an open bin of
+// their chunk get row pairs
+__global__ void k_bin_hist_prefix(const int4* __restrict__ rects, uint32_t V, int nc, int tiles_x,
+                                  int tiles_y, const int* __restrict__ sat, int* __restrict__ diff,
+                                  unsigned long long* __restrict__ rows) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= V) return;
+    const int4 rc = rects[r];
+    const bool any = rc.z > 0 && rc.w > 0;
+    rows[r] = 0ull;
+    if (!any) return;
+    const int X = tiles_x + 1, Y = tiles_y + 1;
+    const int x0 = rc.x, x1 = rc.x + rc.z, y0 = rc.y, y1 = rc.y + rc.w;  // half-open
+    atomicAdd(&diff[y0 * X + x0], 1);
+    atomicAdd(&diff[y0 * X + x1], -1);
+    atomicAdd(&diff[y1 * X + x0], -1);
+    atomicAdd(&diff[y1 * X + x1], 1);
+    const int* S = sat + static_cast<size_t>(static_cast<uint64_t>(r) * nc / V) * X * Y;
+    const int open = S[y1 * X + x1] - S[y0 * X + x1] - S[y1 * X + x0] + S[y0 * X + x0];
+    if (open > 0) rows[r] = static_cast<unsigned long long>(rc.w);
 }
 
 constexpr int kScanThreads = 1024;
@@ -959,6 +1057,18 @@ void launch_emit_rows(const unsigned long long* offsets, const int4* rects, uint
     if (V == 0 || R == 0) return;
     const unsigned long long threads = (R + kPerThread - 1) / kPerThread;
     k_emit_rows<<<blocks_for(threads, 256), 256, 0, s>>>(offsets, rects, V, R, row_keys, row_vals);
+}
+
+void launch_bin_hist_prefix(const int4* rects, uint32_t V, int tiles_x, int tiles_y, uint32_t cap, int nc,
+                            int* diffc, int* sat, int* diff, unsigned long long* rows, cudaStream_t s) {
+    if (V == 0) return;
+    const int X = tiles_x + 1, Y = tiles_y + 1;  // (diffc and sat zeroed by the caller)
+    k_chunk_hist<<<blocks_for(V, 256), 256, 0, s>>>(rects, V, nc, tiles_x, tiles_y, diffc);
+    k_prefix2d<<<nc, 1024, 0, s>>>(diffc, X, Y);
+    k_chunk_open<<<blocks_for(static_cast<uint64_t>(tiles_x) * tiles_y, 256), 256, 0, s>>>(diffc, nc, tiles_x,
+                                                                                           tiles_y, cap, sat);
+    k_prefix2d<<<nc, 1024, 0, s>>>(sat, X, Y);
+    k_bin_hist_prefix<<<blocks_for(V, 256), 256, 0, s>>>(rects, V, nc, tiles_x, tiles_y, sat, diff, rows);
 }
 
 void launch_bin_hist(const int4* rects, uint32_t V, int tiles_x, int* diff,

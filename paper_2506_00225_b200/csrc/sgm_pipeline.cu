@@ -73,9 +73,12 @@ static void pack_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, const Ca
 // K3 counts over the ranks < Ve (a depth prefix when Ve < V): tile ranges from the
 // rectangles' 2D difference array (bins outside `mask` empty; total pairs to d_total), and
 // the row-pair offsets roff[0..Ve] (roff[Ve] = the prefix's row pairs).
+// kRankChunks > 0 with a cap: pass 1 of depth-prefix binning, where only ranks that can reach
+// a bin's first `cap` entries get row pairs (k_bin_hist_prefix).
+constexpr int kRankChunks = 64;
 static void bin_counts(sgm_ctx* ctx, cudaStream_t s, const OptParams& o, uint32_t Ve, uint2* ranges,
                        int bin_tiles, const uint8_t* mask, unsigned long long* d_total,
-                       uint32_t cap = 0xffffffffu, uint8_t* trunc = nullptr) {
+                       uint32_t cap = 0xffffffffu, uint8_t* trunc = nullptr, bool prefix_rows = false) {
     CK(cudaMemsetAsync(ranges, 0, sizeof(uint2) * bin_tiles, s));
     if (Ve == 0) {
         if (d_total) CK(cudaMemsetAsync(d_total, 0, 8, s));
@@ -87,7 +90,16 @@ static void bin_counts(sgm_ctx* ctx, cudaStream_t s, const OptParams& o, uint32_
     CK(cudaMemsetAsync(diff, 0, sizeof(int) * X * Y, s));
     unsigned long long* rows = ctx->counts.as<unsigned long long>();
     unsigned long long* roff = ctx->offsets.as<unsigned long long>();
-    launch_bin_hist(ctx->rects.as<int4>(), Ve, o.tiles_x, diff, rows, s);
+    if (prefix_rows) {
+        const size_t cells = static_cast<size_t>(X) * Y * kRankChunks;
+        CK(cudaMemsetAsync(ctx->cdiff.p, 0, sizeof(int) * cells, s));
+        CK(cudaMemsetAsync(ctx->csat.p, 0, sizeof(int) * cells, s));
+        launch_bin_hist_prefix(ctx->rects.as<int4>(), Ve, o.tiles_x, o.tiles_y, cap, kRankChunks,
+                               ctx->cdiff.as<int>(), ctx->csat.as<int>(), diff, rows, s);
+        ctx->stats.kernel_launches += 4;
+    } else {
+        launch_bin_hist(ctx->rects.as<int4>(), Ve, o.tiles_x, diff, rows, s);
+    }
     launch_bin_scan(diff, o.tiles_x, o.tiles_y, ranges, s, mask, d_total, cap, trunc);
     CK(cudaMemsetAsync(rows + Ve, 0, sizeof(unsigned long long), s));
     exclusive_scan_u64<unsigned long long>(rows, Ve + 1, roff, ctx->scan_tmp.as<unsigned long long>(), s);
@@ -182,8 +194,15 @@ static void bin_dense_view(sgm_ctx* ctx, cudaStream_t s, const sgm_map* map, con
         CK(cudaMemsetAsync(trunc, 0, bin_tiles, s));
         return;
     }
-    bin_counts(ctx, s, o, V, ranges, bin_tiles, nullptr, nullptr, cap, trunc);
-    bin_lists(ctx, s, o, V, R, d_R, const_cast<uint32_t*>(d.list), ranges, nullptr, true, P);
+    bin_counts(ctx, s, o, V, ranges, bin_tiles, nullptr, nullptr, cap, trunc, true);
+    // the row pairs of the ranks that can reach a prefix: their count (a host round trip on the
+    // binning stream; the raster of the previous sub-batch runs meanwhile)
+    const unsigned long long* d_R1 = ctx->offsets.as<unsigned long long>() + V;
+    unsigned long long R1 = 0;
+    CK(cudaMemcpyAsync(&R1, d_R1, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    (void)R;
+    if (R1) bin_lists(ctx, s, o, V, R1, d_R1, const_cast<uint32_t*>(d.list), ranges, nullptr, true, P);
 }
 
 // pass 2 of a dense view whose raster reported `ninc` incomplete tiles (in `inc`): the view is
@@ -354,6 +373,9 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
                 CK(ctx->trunc8.reserve(static_cast<size_t>(bin_tiles) * ng + 16));
                 CK(ctx->incomplete.reserve(4 * static_cast<size_t>(rtiles) * ng + 16));
                 CK(ctx->dense_tot.reserve(16 + 4 * static_cast<size_t>(ng) + 16));
+                const size_t cells = static_cast<size_t>(o.tiles_x + 1) * (o.tiles_y + 1) * kRankChunks;
+                CK(ctx->cdiff.reserve(sizeof(int) * cells));
+                CK(ctx->csat.reserve(sizeof(int) * cells));
             }
             uint32_t* d_ninc = ndense ? reinterpret_cast<uint32_t*>(ctx->dense_tot.as<char>() + 16) : nullptr;
             // descriptors for the whole group (list offsets known from the counts)
