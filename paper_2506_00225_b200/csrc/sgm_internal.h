@@ -186,10 +186,10 @@ struct RasterParams {
     // null: every tile of every view of the launch
     const uint2* item_list;
     int n_item_list;
-    // depth-prefix binning (one dense view per launch): trunc[bin] = 1 when the bin's list
-    // holds only its first entries; a block that exhausts such a list with pixels still open
-    // appends its raster tile to incomplete[] (count *n_incomplete) to be redone from the
-    // full list. Null: every list is complete.
+    // depth-prefix binning, per view v of the launch: trunc[v * bins + bin] = 1 when the bin's
+    // list holds only its first entries; a block that exhausts such a list with pixels still
+    // open appends its raster tile to incomplete[v * tiles_per_view ..] (count
+    // n_incomplete[v]) to be redone from the full list. Null: every list is complete.
     const uint8_t* trunc;
     uint32_t* incomplete;
     uint32_t* n_incomplete;

@@ -427,15 +427,11 @@ void run_views(sgm_ctx* ctx, const sgm_map* map, const CamParams& cam, const Opt
             // sub-batches of 1, 2, 4, then kSub views: the first raster starts after one view's
             // binning instead of kSub views' (the pipeline fill), and each sub-batch's binning
             // still hides under the previous one's raster (about 1/3 of its time per view). A
-            // dense view is a sub-batch of its own (its raster reports incomplete tiles).
+            // sub-batch holds dense views only, or none (its raster reports incomplete tiles).
             int sub = 0;
             for (int s0 = v0, s1 = v0, len = 1; s0 < v1; s0 = s1, ++sub) {
-                if (dense(s0)) {
-                    s1 = s0 + 1;
-                } else {
-                    while (s1 < v1 && s1 - s0 < len && !dense(s1)) ++s1;
-                    len = std::min(kSub, 2 * len);
-                }
+                while (s1 < v1 && s1 - s0 < len && dense(s1) == dense(s0)) ++s1;
+                len = std::min(kSub, 2 * len);
                 {  // K2 for the sub-batch: one segmented radix sort of its views' depth keys
                     uint32_t maxV = 0;
                     for (int v = s0; v < s1; ++v) maxV = std::max(maxV, V[v]);

@@ -293,7 +293,8 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         const int bin = ((tby * kTile) / p.opt.ts) * p.opt.tiles_x + (tbx * kTile) / p.opt.ts;
         const uint2 rg = v->ranges[bin];
         if (lane == 0) {
-            if (kItems) s_trunc[ls.q] = p.trunc ? p.trunc[bin] : 0;
+            if (kItems)
+                s_trunc[ls.q] = p.trunc ? p.trunc[static_cast<size_t>(view) * p.opt.tiles_x * p.opt.tiles_y + bin] : 0;
             ls.list = v->list;
             ls.packed = v->packed;
             ls.order = v->order;
@@ -736,7 +737,8 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                 // from a longer depth prefix (its partials above are then overwritten)
                 if (kItems) {
                     if (s_exh && s_trunc[q] && p.incomplete)
-                        p.incomplete[atomicAdd(p.n_incomplete, 1u)] = static_cast<uint32_t>(tile);
+                        p.incomplete[static_cast<size_t>(view) * tpv + atomicAdd(p.n_incomplete + view, 1u)] =
+                            static_cast<uint32_t>(tile);
                     s_exh = 0;
                 }
                 unsigned long long k = 0;
