@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     __shared__ int s_item;
     __shared__ uint8_t s_trunc[2];  // the block's bin list is a strict prefix (depth-prefix binning)
     __shared__ int s_exh;           // the block's list ran out with pixels still open
+    __shared__ int s_view;          // (kItems) the block's view, for thread 0's epilogue
     __shared__ double red_d[2];                        // epilogue: the two pixel warps' entropy
     __shared__ unsigned long long red_u[2 + kWarps];   // their missing counts, then K per warp
 
@@ -336,6 +337,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
             tile = item - view * tpv;
         }
         const ViewDesc vd = p.views[view];
+        if (kItems && t == 0) s_view = view;  // (not a register live across the block)
         const int bx = tile % p.raster_tiles_x, by = tile / p.raster_tiles_x;
         const int x = bx * kTile + px_col(px);
         const int y = by * kTile + px_row(px);
@@ -737,7 +739,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                 // from a longer depth prefix (its partials above are then overwritten)
                 if (kItems) {
                     if (s_exh && s_trunc[q] && p.incomplete)
-                        p.incomplete[static_cast<size_t>(view) * tpv + atomicAdd(p.n_incomplete + view, 1u)] =
+                        p.incomplete[static_cast<size_t>(s_view) * tpv + atomicAdd(p.n_incomplete + s_view, 1u)] =
                             static_cast<uint32_t>(tile);
                     s_exh = 0;
                 }
