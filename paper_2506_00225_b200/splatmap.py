@@ -504,10 +504,12 @@ class Context:
         return handle
 
     def _forget(self, key) -> None:
-        hit = self._maps.pop(key, None)
-        lib = getattr(N, "lib", None) if N is not None else None  # None at interpreter exit
-        if hit is not None and self.handle and lib is not None:
-            lib.sgm_map_release(self.handle, hit[2])
+        try:
+            hit = self._maps.pop(key, None)
+            if hit is not None and self.handle:
+                N.lib.sgm_map_release(self.handle, hit[2])
+        except Exception:  # interpreter exit: module globals and builtins already torn down
+            pass
 
     def _upload_async(self, gmap: GaussianMap):
         """sgm_map_upload_async: returns (handle, arrays the staging thread still reads). The
