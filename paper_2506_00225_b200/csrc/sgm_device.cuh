@@ -158,4 +158,39 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, unsig
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 }  // namespace
+
+// ---- tensor memory (tcgen05): an fp64 accumulator slice per warp. Addresses are
+// (lane << 16) | column; a warp reaches only the 32 lanes of its quarter (warp % 4). ----
+constexpr uint32_t kTmemCols = 128;  // columns allocated per CTA (3 CTAs per SM: 384 of 512)
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {  // one warp
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\n" ::"r"(smem_addr(dst_smem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t base) {  // the allocating warp
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\n" ::"r"(base));
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+// two fp64 per lane (4 columns from addr): lane l's pixels 2l, 2l+1
+__device__ __forceinline__ void tmem_ld2(uint32_t addr, uint32_t (&r)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void tmem_st2(uint32_t addr, const uint32_t (&r)[4]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n"
+                 ::"r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]) : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ double2 tmem_unpack(const uint32_t (&r)[4]) {
+    return make_double2(__hiloint2double(static_cast<int>(r[1]), static_cast<int>(r[0])),
+                        __hiloint2double(static_cast<int>(r[3]), static_cast<int>(r[2])));
+}
+__device__ __forceinline__ void tmem_pack(double2 v, uint32_t (&r)[4]) {
+    r[0] = static_cast<uint32_t>(__double2loint(v.x));
+    r[1] = static_cast<uint32_t>(__double2hiint(v.x));
+    r[2] = static_cast<uint32_t>(__double2loint(v.y));
+    r[3] = static_cast<uint32_t>(__double2hiint(v.y));
+}
+
 }  // namespace sgm

@@ -182,6 +182,7 @@ struct RasterParams {
     int want_rc;         // score mode: also write vd.rc4 (colour / depth per pixel)
     int n_items;         // raster: (view, block) items of the launch (set by the launcher)
     int items_per_cta;   // raster: consecutive items per CTA (set by the launcher)
+    int tm_first;        // raster (tensor-memory variant): first channel group held in TMEM
     // optional explicit (view, raster tile) items (the redo pass of depth-prefix binning);
     // null: every tile of every view of the launch
     const uint2* item_list;

@@ -28,6 +28,7 @@
 // entropy and exact-zero-silhouette count go to a per-tile slot that a second
 // kernel sums in a fixed order (deterministic, batching/sharding-invariant).
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "sgm_internal.h"
@@ -117,8 +118,11 @@ __device__ __forceinline__ int px_row(int q) { return (q >> 5) * 4 + ((q >> 2) &
 // stream's kernels to take their slots.)
 // kItems: the depth-prefix binning launch (explicit item list, truncated-list flags and the
 // incomplete-tile report); a separate instantiation, so the common launches carry none of it.
+// kTm (3-CTA score launches): channel groups 4-7 accumulate in tensor memory (tcgen05.ld/st,
+// one 32-lane quarter per warp) instead of shared memory, so their read-modify-writes leave
+// the shared-memory pipe to the other groups, the staged weights and rows.
 template <bool kRender, bool kDup, bool kAniso, bool kRc = false, int kOcc = 3, bool kItems = false,
-          bool kRefDiv = false>
+          bool kRefDiv = false, bool kTm = false>
 __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int C = p.map.C;
@@ -157,6 +161,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     __shared__ uint8_t s_trunc[2];  // the block's bin list is a strict prefix (depth-prefix binning)
     __shared__ int s_exh;           // the block's list ran out with pixels still open
     __shared__ int s_view;          // (kItems) the block's view, for thread 0's epilogue
+    __shared__ uint32_t s_tbase;    // (kTm) the CTA's tensor-memory columns
     __shared__ double red_d[2];                        // epilogue: the two pixel warps' entropy
     __shared__ unsigned long long red_u[2 + kWarps];   // their missing counts, then K per warp
 
@@ -316,7 +321,17 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         mbar_init(smem_addr(&s_mbar[0]), 1);
         mbar_init(smem_addr(&s_mbar[1]), 1);
     }
+    if constexpr (kTm) {
+        if (warp == 0) tmem_alloc(&s_tbase);
+        tmem_fence_before();
+    }
     __syncthreads();
+    if constexpr (kTm) tmem_fence_after();
+    // (kTm) groups from p.tm_first on: this warp's lane quarter (warp % 4), channel c of the group
+    // at columns 4 (c - c0), from column 0 for groups 4-7 and 64 for groups 0-3
+    const bool tmg = kTm && g >= p.tm_first;
+    const uint32_t tcol =
+        kTm ? s_tbase + ((32u * static_cast<uint32_t>(warp & 3)) << 16) + (warp < 4 ? 64u : 0u) : 0u;
     if (loader) {
         if (lane == 0) ls.q = 0;
         __syncwarp();
@@ -345,6 +360,11 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         const bool want_sem = !kRender || vd.sem != nullptr;
         if (!loader) {
             for (int i = t; i < C * apitch; i += kCompute) acc2[i] = make_double2(0.0, 0.0);
+            if (tmg) {
+                const uint32_t z[4] = {0u, 0u, 0u, 0u};
+                for (int cc = 0; cc < c1 - c0; ++cc) tmem_st2(tcol + 4u * cc, z);
+                tmem_wait_st();
+            }
             if (t < kTilePx) {
                 sdone[t] = inside ? 0 : 1;
                 sT[t] = 1.0;
@@ -594,7 +614,48 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                         asm volatile("{ .reg .pred q; setp.ne.u32 q, %0, 0; @q st.shared.v2.f64 [%1], {%2, %3}; }"
                                      :: "r"(pz), "r"(sa), "d"(vx), "d"(vy) : "memory");
                     };
-                    if (kDup) {
+                    if (tmg) {
+                        // tensor memory: every lane takes part (.sync.aligned); a weightless
+                        // lane adds p * 0 = +0 to a nonnegative sum, which leaves it unchanged.
+                        // Each store completes before the next load (a later entry may hit the
+                        // same class).
+                        int j = lo;
+                        if (!kDup) {
+#pragma unroll 1
+                            for (; j + 2 <= hi; j += 2) {
+                                double p0, p1;
+                                const int ca = cls(j, p0), cb = cls(j + 1, p1);
+                                uint32_t ra[4], rb[4];
+                                tmem_ld2(tcol + 4u * static_cast<uint32_t>(ca - c0), ra);
+                                tmem_ld2(tcol + 4u * static_cast<uint32_t>(cb - c0), rb);
+                                tmem_wait_ld();
+                                double2 a = tmem_unpack(ra), bq = tmem_unpack(rb);
+                                a.x = __fma_rn(p0, w.x, a.x);  // :307
+                                a.y = __fma_rn(p0, w.y, a.y);
+                                bq.x = __fma_rn(p1, w.x, bq.x);
+                                bq.y = __fma_rn(p1, w.y, bq.y);
+                                tmem_pack(a, ra);
+                                tmem_pack(bq, rb);
+                                tmem_st2(tcol + 4u * static_cast<uint32_t>(ca - c0), ra);
+                                tmem_st2(tcol + 4u * static_cast<uint32_t>(cb - c0), rb);
+                                tmem_wait_st();
+                            }
+                        }
+#pragma unroll 1
+                        for (; j < hi; ++j) {  // (repeated classes: one at a time, in order)
+                            double pj;
+                            const int c = cls(j, pj);
+                            uint32_t r[4];
+                            tmem_ld2(tcol + 4u * static_cast<uint32_t>(c - c0), r);
+                            tmem_wait_ld();
+                            double2 a = tmem_unpack(r);
+                            a.x = __fma_rn(pj, w.x, a.x);
+                            a.y = __fma_rn(pj, w.y, a.y);
+                            tmem_pack(a, r);
+                            tmem_st2(tcol + 4u * static_cast<uint32_t>(c - c0), r);
+                            tmem_wait_st();
+                        }
+                    } else if (kDup) {
 #pragma unroll 1
                         for (int j = lo; j < hi; ++j) {  // repeated classes: in order
                             double pj;
@@ -691,7 +752,15 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                 const double lclamp = log_table(0.001);
 #pragma unroll 2
                 for (int c = c0; c < c1; ++c) {
-                    const double2 v = acc2[c * apitch + lane];
+                    double2 v;
+                    if (tmg) {
+                        uint32_t r[4];
+                        tmem_ld2(tcol + 4u * static_cast<uint32_t>(c - c0), r);
+                        tmem_wait_ld();
+                        v = tmem_unpack(r);
+                    } else {
+                        v = acc2[c * apitch + lane];
+                    }
                     const double ax = clamp_prob(v.x), ay = clamp_prob(v.y);
                     S1x += ax;
                     S1y += ay;
@@ -765,6 +834,26 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         // the epilogue is done with acc / W / red_u; the next block's item and batch 0 are staged
         __syncthreads();
     }
+    if constexpr (kTm) {
+        tmem_fence_before();
+        __syncthreads();
+        tmem_fence_after();
+        if (warp == 0) tmem_dealloc(s_tbase);
+    }
+}
+
+// The first channel group the 3-CTA score raster keeps in tensor memory (kGroups: none).
+// Measured (B200): with k = 32 classes per Gaussian (cfg4: about four read-modify-writes per
+// entry and group, the shared-memory pipe 88% busy) groups 4-7 in TMEM give 167 -> 185 views/s;
+// with k = 16 (cfg1: two per entry and group, TMEM's wait per read-modify-write exposed) 908 ->
+// 891, so TMEM is used from k = 24. SGM_TM_FIRST=g overrides (groups g..7; g < 4 needs C <= 128).
+int raster_tm_first(const DevMap& m) {
+    const int cg4 = (m.C + kGroups - 1) / kGroups * 4;  // columns per group
+    int first = m.k >= 24 ? 4 : kGroups;
+    if (const char* e = std::getenv("SGM_TM_FIRST")) first = std::atoi(e);
+    if (first < 4 && cg4 > 64) first = 4;
+    if (cg4 > 128) first = kGroups;
+    return std::max(0, std::min(kGroups, first));
 }
 
 template <bool kRender, bool kDup, bool kAniso, bool kRc = false>
@@ -782,7 +871,15 @@ void launch_t(const RasterParams& p0, int n_views, cudaStream_t s) {
     p.items_per_cta = kRender ? 2 : kItemsPerCta;
     const int grid = (p.n_items + p.items_per_cta - 1) / p.items_per_cta;
     if constexpr (!kRender && !kRc) {
+        p.tm_first = raster_tm_first(p.map);
+        const bool tm = p.tm_first < kGroups;
         if (p.item_list || p.trunc) {
+            if (tm) {
+                cudaFuncSetAttribute(k_raster<kRender, kDup, kAniso, kRc, 3, true, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+                k_raster<kRender, kDup, kAniso, kRc, 3, true, false, true><<<grid, kThreads, smem, s>>>(p);
+                return;
+            }
             cudaFuncSetAttribute(k_raster<kRender, kDup, kAniso, kRc, 3, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             k_raster<kRender, kDup, kAniso, kRc, 3, true><<<grid, kThreads, smem, s>>>(p);
@@ -801,6 +898,14 @@ void launch_t(const RasterParams& p0, int n_views, cudaStream_t s) {
             cudaFuncSetAttribute(k_raster<kRender, kDup, kAniso, kRc, 3, false, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             k_raster<kRender, kDup, kAniso, kRc, 3, false, true><<<grid, kThreads, smem, s>>>(p);
+            return;
+        }
+    }
+    if constexpr (!kRender && !kRc) {
+        if (p.tm_first < kGroups) {
+            cudaFuncSetAttribute(k_raster<kRender, kDup, kAniso, kRc, 3, false, false, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            k_raster<kRender, kDup, kAniso, kRc, 3, false, false, true><<<grid, kThreads, smem, s>>>(p);
             return;
         }
     }
