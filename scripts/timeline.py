@@ -17,6 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=1)
 ap.add_argument("--views", type=int, default=64)
 ap.add_argument("--top", type=int, default=14)
+ap.add_argument("--fisher", action="store_true", help="the Fisher-gain scoring (prior from 32 poses)")
 a = ap.parse_args()
 torch.cuda.init()
 ctx = Context(0)
@@ -24,11 +25,17 @@ gm = scenes.make_map(a.config)
 cam = scenes.CONFIGS[a.config].camera()
 poses = [c.camera_pose() for c in scenes.make_candidates(a.config, a.views)]
 ctx.upload(gm)
+if a.fisher:
+    from paper_2506_00225_b200.splatmap import fisher_prior, score_poses_fisher
+    fisher_prior(gm, cam, [c.camera_pose() for c in scenes.make_candidates(a.config, 32, stream=2)], ctx=ctx)
+    run = lambda: score_poses_fisher(gm, cam, poses, ctx=ctx)  # noqa: E731
+else:
+    run = lambda: score_poses(gm, cam, poses, ctx=ctx)  # noqa: E731
 for _ in range(2):
-    score_poses(gm, cam, poses, ctx=ctx)
+    run()
 ctx.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
-    score_poses(gm, cam, poses, ctx=ctx)
+    run()
     ctx.synchronize()
 ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
 ks = []
@@ -61,7 +68,7 @@ def length(iv):
     return sum(e - s for s, e in iv)
 
 
-ras = union([(s, e) for s, e, n in ks if "k_raster" in n])
+ras = union([(s, e) for s, e, n in ks if "k_raster" in n or "k_fisher" in n])
 alls = union([(s, e) for s, e, n in ks])
 span = T1 - T0
 print(f"cfg{a.config} {a.views} views: span {span / 1e3:.2f} ms, raster busy {length(ras) / 1e3:.2f} ms, "
@@ -88,6 +95,7 @@ for s, e, n in ks:
             break
         ov += min(e, re_) - max(s, rs)
     exp[key] += (e - s) - ov
+print("busy per family: " + ", ".join(f"{k} {v / 1e3:.2f} ms" for k, v in sorted(tot.items(), key=lambda kv: -kv[1])[:4]))
 print("| kernel | total ms | exposed (no raster running) ms |\n|---|---|---|")
 for k, v in sorted(tot.items(), key=lambda kv: -exp[kv[0]])[: a.top]:
     print(f"| {k} | {v / 1e3:.3f} | {exp[k] / 1e3:.3f} |")
