@@ -8,8 +8,9 @@
 //
 // One CTA = 8 compute warps + 1 loader warp; it blends kItemsPerCta consecutive 8x8 pixel
 // blocks (of one view, or crossing into the next). Per block, the loader forms batches of
-// kNB Gaussians (depth order) two ahead and streams their rows through shared memory with
-// cp.async (double-buffered); per batch the compute warps run
+// kNB Gaussians (depth order) two ahead and streams their rows through shared memory
+// (double-buffered: cp.async.bulk copies completing on an mbarrier for score launches, 16-byte
+// cp.async chunks for render / colour launches); per batch the compute warps run
 //   phase AB footprints and the exact transmittance chain, fused: thread (part, px) owns 4
 //            contiguous entries of pixel px; segment products meet in shared memory
 //            (render with retained contributor lists: footprints, then the sequential
@@ -19,7 +20,9 @@
 //            accumulator word. The accumulator is [C][32] double2 in shared memory (lane l
 //            holds pixels 2l, 2l+1): one LDS.128 / 2 DFMA / STS.128 per (Gaussian, class)
 //            entry covers the whole 8x8 block, and a warp's lanes hit 32 consecutive
-//            16-byte words (no bank conflict).
+//            16-byte words (no bank conflict). With k >= 24 classes per Gaussian the score
+//            launch keeps groups 4-7 in tensor memory instead (kTm: tcgen05.ld/st, the same
+//            two pixels per lane), off the shared-memory pipe.
 // While the compute warps run a block's epilogue the loader stages the next block's first
 // batch.
 // Score epilogue: per (pixel, group) S1 = sum c, S2 = sum c ln c with
