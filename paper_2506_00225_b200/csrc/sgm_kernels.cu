@@ -671,6 +671,9 @@ __global__ void __launch_bounds__(256) k_seg_pass(const unsigned long long* __re
     }
     const int last = min(tiles_x, cb + 32) - 1;
     for (uint32_t b0 = sg.y; b0 < sg.z; b0 += 32) {
+        // (kPart) the columns whose list still takes entries; none left: this warp is done
+        const uint32_t open = kPart ? __ballot_sync(0xffffffffu, has && cur < len) : 0xffffffffu;
+        if (kPart && !open) break;
         const bool valid = b0 + lane < sg.z;
         const unsigned long long e = valid ? row_list[b0 + lane] : 0ull;
         const int x0 = static_cast<int>((e >> 16) & 0xffffu);
@@ -700,9 +703,12 @@ __global__ void __launch_bounds__(256) k_seg_pass(const unsigned long long* __re
             // column's list (coalesced stores)
             const int lo = max(cb, __reduce_min_sync(0xffffffffu, rel ? x0 : INT_MAX));
             const int hi = min(last, __reduce_max_sync(0xffffffffu, rel ? x1 : INT_MIN));
-            for (int c = lo; c <= hi; ++c) {
-                const int owner = c - cb;
-                if (kPart && !__shfl_sync(0xffffffffu, has ? 1 : 0, owner)) continue;  // (uniform)
+            // the chunk's columns (kPart: the open ones only), ascending
+            uint32_t cols = (0xffffffffu >> (31 - (hi - cb))) & (0xffffffffu << (lo - cb)) & open;
+            while (cols) {
+                const int owner = __ffs(cols) - 1;
+                cols &= cols - 1u;
+                const int c = cb + owner;
                 const bool cov = rel && x0 <= c && c <= x1;
                 const uint32_t bal = __ballot_sync(0xffffffffu, cov);
                 const uint32_t at = __shfl_sync(0xffffffffu, cur, owner);
