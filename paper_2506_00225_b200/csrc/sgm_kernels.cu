@@ -490,21 +490,26 @@ __global__ void k_chunk_open(const int* __restrict__ cnt, int nc, int tiles_x, i
 
 // k_bin_hist for pass 1: every rank counts in its bins; only ranks covering an open bin of
 // their chunk get row pairs
+// the whole view's difference array: the sum of the chunks' (before their prefix sums)
+__global__ void k_chunk_sum(const int* __restrict__ diffc, int nc, int cells, int* __restrict__ diff) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cells) return;
+    int v = 0;
+    for (int c = 0; c < nc; ++c) v += diffc[static_cast<size_t>(c) * cells + i];
+    diff[i] = v;
+}
+
+// k_bin_hist for pass 1: only ranks covering an open bin of their chunk get row pairs (the
+// view's bin counts come from the chunks' difference arrays, k_chunk_sum)
 __global__ void k_bin_hist_prefix(const int4* __restrict__ rects, uint32_t V, int nc, int tiles_x,
-                                  int tiles_y, const int* __restrict__ sat, int* __restrict__ diff,
-                                  unsigned long long* __restrict__ rows) {
+                                  int tiles_y, const int* __restrict__ sat, unsigned long long* __restrict__ rows) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= V) return;
     const int4 rc = rects[r];
-    const bool any = rc.z > 0 && rc.w > 0;
     rows[r] = 0ull;
-    if (!any) return;
+    if (rc.z <= 0 || rc.w <= 0) return;
     const int X = tiles_x + 1, Y = tiles_y + 1;
     const int x0 = rc.x, x1 = rc.x + rc.z, y0 = rc.y, y1 = rc.y + rc.w;  // half-open
-    atomicAdd(&diff[y0 * X + x0], 1);
-    atomicAdd(&diff[y0 * X + x1], -1);
-    atomicAdd(&diff[y1 * X + x0], -1);
-    atomicAdd(&diff[y1 * X + x1], 1);
     const int* S = sat + static_cast<size_t>(static_cast<uint64_t>(r) * nc / V) * X * Y;
     const int open = S[y1 * X + x1] - S[y0 * X + x1] - S[y1 * X + x0] + S[y0 * X + x0];
     if (open > 0) rows[r] = static_cast<unsigned long long>(rc.w);
@@ -1070,11 +1075,12 @@ void launch_bin_hist_prefix(const int4* rects, uint32_t V, int tiles_x, int tile
     if (V == 0) return;
     const int X = tiles_x + 1, Y = tiles_y + 1;  // (diffc and sat zeroed by the caller)
     k_chunk_hist<<<blocks_for(V, 256), 256, 0, s>>>(rects, V, nc, tiles_x, tiles_y, diffc);
+    k_chunk_sum<<<blocks_for(static_cast<uint64_t>(X) * Y, 256), 256, 0, s>>>(diffc, nc, X * Y, diff);
     k_prefix2d<<<nc, 1024, 0, s>>>(diffc, X, Y);
     k_chunk_open<<<blocks_for(static_cast<uint64_t>(tiles_x) * tiles_y, 256), 256, 0, s>>>(diffc, nc, tiles_x,
                                                                                            tiles_y, cap, sat);
     k_prefix2d<<<nc, 1024, 0, s>>>(sat, X, Y);
-    k_bin_hist_prefix<<<blocks_for(V, 256), 256, 0, s>>>(rects, V, nc, tiles_x, tiles_y, sat, diff, rows);
+    k_bin_hist_prefix<<<blocks_for(V, 256), 256, 0, s>>>(rects, V, nc, tiles_x, tiles_y, sat, rows);
 }
 
 void launch_bin_hist(const int4* rects, uint32_t V, int tiles_x, int* diff,

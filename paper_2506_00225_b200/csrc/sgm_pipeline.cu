@@ -96,7 +96,7 @@ static void bin_counts(sgm_ctx* ctx, cudaStream_t s, const OptParams& o, uint32_
         CK(cudaMemsetAsync(ctx->csat.p, 0, sizeof(int) * cells, s));
         launch_bin_hist_prefix(ctx->rects.as<int4>(), Ve, o.tiles_x, o.tiles_y, cap, kRankChunks,
                                ctx->cdiff.as<int>(), ctx->csat.as<int>(), diff, rows, s);
-        ctx->stats.kernel_launches += 4;
+        ctx->stats.kernel_launches += 5;  // (+ the k_bin_hist counted below)
     } else {
         launch_bin_hist(ctx->rects.as<int4>(), Ve, o.tiles_x, diff, rows, s);
     }
