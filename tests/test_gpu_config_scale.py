@@ -189,3 +189,23 @@ def test_dense_scene_scores_vs_reference(ctx, ref, monkeypatch):
                                   [c.direction for c in cands], threads=6)
     np.testing.assert_array_equal(nm, rnm)
     np.testing.assert_allclose(es, res, rtol=ENT_RTOL, atol=0)
+
+
+def test_cfg4_full_size_modes_bit_identical(ctx, monkeypatch):
+    """cfg4 at its full size (1M Gaussians, 1200x680, 1.19 G tile pairs per view): the default
+    path (depth-prefix binning of 8,192 entries per bin, row pairs only for ranks that can reach
+    a prefix, channel groups 4-7 in tensor memory) scores bit-identically to full bins and to the
+    shared-memory accumulator; the reference cannot hold these views (16 B per tile pair)."""
+    gm = scenes.make_map(4)
+    cam = scenes.CONFIGS[4].camera()
+    poses = [c.camera_pose() for c in scenes.make_candidates(4, 3)]
+    ctx.reset_stats()
+    nm, es = sgm.score_poses(gm, cam, poses, ctx=ctx)
+    assert ctx.stats()["pairs"] / len(poses) > 1.0e9
+    monkeypatch.setenv("SGM_PREFIX_BINNING", "0")
+    nm_full, es_full = sgm.score_poses(gm, cam, poses, ctx=ctx)
+    monkeypatch.setenv("SGM_TM_FIRST", "8")
+    nm_smem, es_smem = sgm.score_poses(gm, cam, poses, ctx=ctx)
+    assert np.array_equal(nm, nm_full) and np.array_equal(es, es_full)
+    assert np.array_equal(nm, nm_smem) and np.array_equal(es, es_smem)
+    assert np.all(es > 0)
