@@ -10,7 +10,7 @@
 // blocks (of one view, or crossing into the next). Per block, the loader forms batches of
 // kNB Gaussians (depth order) two ahead and streams their rows through shared memory
 // (double-buffered: cp.async.bulk copies completing on an mbarrier for score launches, 16-byte
-// cp.async chunks for render / colour launches); per batch the compute warps run
+// cp.async chunks for render launches); per batch the compute warps run
 //   phase AB footprints and the exact transmittance chain, fused: thread (part, px) owns 4
 //            contiguous entries of pixel px; segment products meet in shared memory
 //            (render with retained contributor lists: footprints, then the sequential
@@ -185,9 +185,10 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
     // first). The loader alone waits on it, before the batch barrier that hands the stage
     // to the compute warps.
     __shared__ __align__(8) unsigned long long s_mbar[2];
-    // (render and colour-writing launches keep 16-byte cp.async chunks: their larger register
-    // footprint spills with the bulk-copy loader)
-    constexpr bool kBulk = !kRender && !kRc;
+    // (render launches keep 16-byte cp.async chunks: their larger register footprint spills
+    // with the bulk-copy loader; the colour-writing score launch of the Fisher gain spills too,
+    // but is faster with it: 423 -> 431 views/s)
+    constexpr bool kBulk = !kRender;
     const int qi = kpad / 8, qp = kpad / 2;
     const int Q = 5 + qi + qp + ((kRender || kRc) ? 2 : 0);  // 16-byte chunks per Gaussian
     auto issue = [&](int b) {
@@ -197,7 +198,8 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
         if constexpr (kBulk) {
             const uint32_t bar = smem_addr(&s_mbar[st]);
             if (lane == 0)
-                mbar_expect_tx(bar, static_cast<unsigned>(n) * (64u + 16u + (kRecs ? 16u : 10u) * static_cast<unsigned>(kpad)));
+                mbar_expect_tx(bar, static_cast<unsigned>(n) * (64u + 16u + (kRecs ? 16u : 10u) * static_cast<unsigned>(kpad) +
+                                                               (kRc ? 32u : 0u)));
             __syncwarp();
             if (lane < n) {
                 const uint2 v = rm[st * kNB + lane];
@@ -205,6 +207,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_raster(RasterParams p) {
                 fence_proxy_async();
                 bulk_g2s(sb + L.st_packed + lane * 64, ls.packed + v.x, 64u, bar);
                 bulk_g2s(sb + L.st_bnd + lane * 16, p.map.gbounds + v.y, 16u, bar);
+                if (kRc) bulk_g2s(sb + L.st_color + lane * 32, p.map.color4 + static_cast<size_t>(v.y) * 4, 32u, bar);
                 if (kRecs) {
                     bulk_g2s(sb + L.st_idx + lane * kpad * 16, p.map.sem_rec + static_cast<size_t>(v.y) * kpad,
                              16u * kpad, bar);
