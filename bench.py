@@ -387,6 +387,40 @@ def measure_aniso(ctx, stream, flush, args, cfg, cam, poses) -> dict:
                          "Sigma from the config's per-axis log-scales and quaternions"}
 
 
+def measure_dense(ctx, stream, flush) -> dict:
+    """cfg4 (dense overlap: 1M Gaussians in a 1 m cube, k = 32 of 102, 1.19 G tile pairs per
+    view) on 32 of its candidate views: the depth-prefix binning and tensor-memory path."""
+    import torch
+    from paper_2506_00225_b200 import scenes
+    from paper_2506_00225_b200.splatmap import score_poses
+    gm4 = scenes.make_map(4)
+    cam4 = scenes.CONFIGS[4].camera()
+    poses4 = [c.camera_pose() for c in scenes.make_candidates(4, 32)]
+    ctx.upload(gm4)
+    score_poses(gm4, cam4, poses4, ctx=ctx)  # warm-up (scratch sized)
+    ms = []
+    for _ in range(2):
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)  # evict L2 (outside the events)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        nm, es = score_poses(gm4, cam4, poses4, ctx=ctx)
+        ev1.record(stream)
+        ev1.synchronize()
+        ms.append(ev0.elapsed_time(ev1))
+    ctx.reset_stats()
+    score_poses(gm4, cam4, poses4, ctx=ctx)
+    st = ctx.stats()
+    t = float(np.mean(ms))
+    return {"config": "cfg4 dense overlap: 1M Gaussians in a 1 m cube, 1200x680, k = 32 of 102, "
+                      "32 candidate views 1.2 m from the centre",
+            "views": len(poses4), "views_per_s": len(poses4) / (t / 1e3), "ms_per_pass": t,
+            "pairs_per_view": st["pairs"] / len(poses4),
+            "contributors_per_view": st["contributors"] / len(poses4),
+            "n_missing_sum": float(np.sum(nm)), "entropy_sum_total": float(np.sum(es))}
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -590,6 +624,14 @@ def main() -> None:
                  "argmax_view": int(max(range(len(sw)), key=lambda i: (sw[i].i_total, -i))),
                  "n_missing_all_zero": bool(np.all(np.asarray(snm) == 0))}
 
+    # ---- cfg4: dense views (rank 0; a secondary leg) ----
+    dense_info = None
+    if rank == 0 and cfg == 1:
+        try:
+            dense_info = measure_dense(ctx, stream, flush)
+        except Exception as exc:  # reported, not fatal
+            dense_info = {"error": repr(exc)}
+
     # ---- e2e through the public API (host inputs, map re-upload every step; at N > 1 rank 0
     #      uploads and broadcasts the device snapshot, the others import it) ----
     h2d = (int(gm_host.centers.nbytes + gm_host.log_radii.nbytes + gm_host.opacity_logits.nbytes +
@@ -759,6 +801,7 @@ def main() -> None:
             "mapping_optimize": mapping_info,
             "anisotropic_ewa": aniso_info,
             "cfg2_sweep": sweep,
+            "cfg4_dense": dense_info,
         }
         print(json.dumps(line), flush=True)
     if dist_on:
